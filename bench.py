@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Benchmark of the learned-join hot path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl b200|reference]
+
+Default workload = BASELINE.json configs[1] (C2): Gapped-RMI INLJ, R = 2^24
+unique floor(1e12*lognormal(0,2)) keys, S = 2^28 probes (95% Zipf(0.8)
+hits), RMI with 2^16 leaves at density 0.5.  One step = one fused probe
+(K1) of the whole S relation against the prebuilt index, with the result
+reduced to (count, sum, xor) on device.  Metric: join tuples/s =
+(|R| + |S|) / step time (bench.py:307-314 of the reference).
+
+Multi-GPU (torchrun, one process per GPU): the R index is replicated and
+every rank probes its own full-size S shard (weak scaling); the per-rank
+checksums are combined with NCCL (sum/count all-reduce, xor all-gather) inside
+the timed step.  value = (|R| + N*|S|) / max-over-ranks step time.
+
+``--impl reference`` times the reference algorithm's CPU implementation --
+the C restatement in oracle/ (the reference itself is Python+numba and is
+not installed on the GPU box) -- with every host thread, on a bounded
+sample of the same workload, extrapolated to the full S.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ALGO_BYTES = {"grmi-inlj": 32, "buffered-grmi-inlj": 32, "spline-hash-inlj": 32, "lsj": 80}
+
+
+def _env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+                self.lines = [ln for ln in out.splitlines() if ln.strip()]
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except (ValueError, IndexError):
+                continue
+            for name, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_inputs(cfg: str, shard: int = 0):
+    from paper_2111_08824_b200 import configs
+
+    return configs.CONFIGS[cfg](shard=shard)
+
+
+def build_index(inp):
+    import paper_2111_08824_b200 as lj
+
+    o = dict(lj.DEFAULT_OPTS, **inp.opts)
+    if inp.algorithm in ("grmi-inlj", "buffered-grmi-inlj"):
+        return lj.GappedRmiIndex(o["gap_factor"], o["rmi_fanout"]).fit(inp.r)
+    if inp.algorithm == "spline-hash-inlj":
+        return lj.SplineHashIndex(o["spline_error"], o["radix_bits"], o["table_factor"]).fit(inp.r)
+    raise ValueError(inp.algorithm)
+
+
+# ---------------------------------------------------------------- CPU arms
+
+
+def cpu_inlj(inp, target_s: float = 8.0, threads: int = 0):
+    """Oracle (C restatement of the reference path, OpenMP) on a bounded
+    sample of S, extrapolated to the whole S.  Returns (value, info)."""
+    import numpy as np
+
+    import oracle
+
+    o = inp.opts
+    rk, rp = inp.r.numpy()
+    n_s = len(inp.s)
+    if inp.algorithm in ("grmi-inlj", "buffered-grmi-inlj"):
+        idx = oracle.grmi_build(rk, rp, o["gap_factor"], o["rmi_fanout"])
+        run = lambda k, p: oracle.grmi_join(idx, k, p, threads)
+    else:
+        idx = oracle.spline_hash_build(rk, rp, o.get("spline_error", 32), o.get("radix_bits", 18),
+                                       o.get("table_factor", 4.0))
+        run = lambda k, p: oracle.spline_hash_join(idx, k, p, threads)
+    sample = min(n_s, 1 << 20)
+    while True:
+        sk = inp.s.keys[:sample].cpu().numpy().view(np.uint64)
+        sp = inp.s.payloads[:sample].cpu().numpy().view(np.uint64)
+        t0 = time.perf_counter()
+        run(sk, sp)
+        dt = time.perf_counter() - t0
+        if dt >= target_s / 4 or sample >= n_s:
+            break
+        sample = min(n_s, sample * 4)
+    t_full = dt * n_s / sample
+    value = (len(inp.r) + n_s) / t_full
+    cores = threads or oracle.num_threads()
+    info = {"value": value, "unit": "tuples/s", "cores": cores, "kind": "port",
+            "sample": f"first {sample} of {n_s} S probes against the full R index ({dt:.2f} s), "
+                      f"time extrapolated x{n_s / sample:.1f}; index build untimed as in the reference"}
+    return value, info, (sk, sp, run)
+
+
+def run_reference_arm(args):
+    import torch
+
+    rank, world, local = _env_rank()
+    if rank != 0:
+        return
+    torch.cuda.set_device(local)
+    inp = make_inputs(args.config)
+    value, info, (sk, sp, run) = cpu_inlj(inp)
+    steps = []
+    n_s = len(inp.s)
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        run(sk, sp)
+        dt = (time.perf_counter() - t0) * n_s / sk.size
+        if i >= args.warmup:
+            steps.append(dt)
+    t = statistics.median(steps)
+    value = (len(inp.r) + n_s) / t
+    info["value"] = value
+    line = {"impl": "reference", "metric": "join tuples/s ((|R|+|S|)/time)", "value": value, "unit": "tuples/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic", "config": _config_block(args, inp), "cpu_baseline": info,
+            "e2e": {"value": value, "unit": "tuples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _config_block(args, inp):
+    return {"workload": f"{args.config}: {inp.description}", "algorithm": inp.algorithm,
+            "n_r": len(inp.r), "n_s": len(inp.s), "l2": "inputs larger than L2 and L2 flushed between steps",
+            "parallelism": f"inlj-replicated-R x{args.gpus}"}
+
+
+# ---------------------------------------------------------------- GPU arm
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = _env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    inp = make_inputs(args.config, shard=rank)
+    index = build_index(inp)
+    dev = torch.device("cuda", local)
+    keys, pays = inp.s.keys, inp.s.payloads
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    out = torch.zeros(4, dtype=torch.int64, device=dev)
+    xors = torch.zeros(world, dtype=torch.int64, device=dev)
+
+    def step():
+        index.join_checksum(keys, pays, out=out)
+        if world > 1:
+            dist.all_gather_into_tensor(xors, out[2:3].contiguous())
+            dist.all_reduce(out, op=dist.ReduceOp.SUM)  # count, sum, steps (wrap mod 2^64)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()  # evict the index and S from L2 between steps
+            ev[i][0].record()
+            step()
+            ev[i][1].record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(total, op=dist.ReduceOp.MAX)
+    ms_per_step = float(total.item()) / args.steps
+    n_r, n_s = len(inp.r), len(inp.s)
+    value = (n_r + world * n_s) / (ms_per_step / 1e3)
+    w = out.cpu().tolist()
+    xor_all = 0
+    if world > 1:
+        for v in xors.cpu().tolist():
+            xor_all ^= v & (2**64 - 1)
+    else:
+        xor_all = w[2] & (2**64 - 1)
+
+    # kernel-only timing of the dominant kernel (K1) for the roofline
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()
+        kev[i][0].record()
+        index.join_checksum(keys, pays, out=out)
+        kev[i][1].record()
+    torch.cuda.synchronize()
+    k_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
+    peak, peak_kind = _peaks()
+    alg_bytes = ALGO_BYTES[inp.algorithm] * n_s
+    achieved = alg_bytes / (k_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": _ncu_traffic(args.config), "kernel": "k_grmi_probe" if "grmi" in inp.algorithm
+                else "k_hash_probe", "kernel_ms": k_ms, "peak_kind": peak_kind,
+                "algorithmic_bytes": f"{ALGO_BYTES[inp.algorithm]} B/probe x {n_s} probes"}
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = _e2e(args, inp, index, world)
+    line = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                _, cpu, _ = cpu_inlj(inp)
+            except Exception as exc:  # the baseline is reported, never required
+                cpu = {"error": repr(exc)}
+        line = {"metric": "join tuples/s ((|R|+|S|)/time)", "value": value, "unit": "tuples/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+                "config": _config_block(args, inp), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": args.steps, "clocks": clk.summary(),
+                "checksum": {"count": w[0], "sum": w[1] & (2**64 - 1), "xor": xor_all, "search_steps": w[3]}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _e2e(args, inp, index, world):
+    """Same metric through the public API from pinned HOST buffers: every
+    step copies S host->device (Relation construction), probes, and reads
+    the 3-word result back."""
+    import torch
+
+    import paper_2111_08824_b200 as lj
+
+    hk = inp.s.keys.cpu().pin_memory()
+    hp = inp.s.payloads.cpu().pin_memory()
+    steps = max(1, min(args.steps, 3))
+    times = []
+    for i in range(steps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s = lj.Relation(hk.to("cuda", non_blocking=True), hp.to("cuda", non_blocking=True), validate=True)
+        res = lj.JoinResult(words=index.join_checksum(s.keys, s.payloads))
+        _ = res.checksum
+        dt = time.perf_counter() - t0
+        del s
+        if i:
+            times.append(dt)
+    t = statistics.median(times)
+    n_s = len(inp.s)
+    return {"value": (len(inp.r) + world * n_s) / t, "unit": "tuples/s", "h2d_bytes_per_step": 16 * n_s,
+            "d2h_bytes_per_step": 4 * 8, "ms_per_step": t * 1e3, "steps": steps}
+
+
+def _ncu_traffic(cfg):
+    p = os.path.join(ROOT, "profiles", f"traffic_{cfg}.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,207 @@
+/*
+ * lj_b200.h -- C ABI of the B200-native learned-join hot paths.
+ *
+ * This is the drop-in boundary: the Python mirror of the reference's join
+ * entry points (paper_2111_08824_b200/, names as in the reference package
+ * `learned_joins`) binds exactly these symbols with ctypes; a reference
+ * maintainer would bind the same symbols from their runner registry
+ * (INTEGRATION.md).  Reference paths are relative to
+ * /root/reference/pkg/src/learned_joins/.
+ *
+ * Conventions
+ *  - Every entry point returns int: LJ_OK (0) or a negative LJ_E_* code;
+ *    lj_last_error() returns a thread-local message.  No C++ exception
+ *    crosses the ABI.
+ *  - All array arguments are CALLER-OWNED DEVICE pointers unless the name
+ *    ends in `_host`.  The library never allocates device memory: scratch
+ *    comes from a caller workspace sized by the matching *_workspace_bytes.
+ *  - Every device call is asynchronous on the caller's `stream`
+ *    (cudaStream_t passed as void*).  Calls on distinct streams with
+ *    distinct workspaces are re-entrant.
+ *  - Keys and payloads are uint64.  A key may not equal LJ_SENTINEL_KEY
+ *    (util.py:8,15-22).
+ *  - Join results are reduced on device to LjChecksum words
+ *    {count, sum, xor, search_steps} of t = R.payload + S.payload mod 2^64
+ *    (SURVEY.md 8a); pairs are materialised only through the *_count /
+ *    *_collect entry points.
+ *  - Model evaluation is bit-identical to the reference's numpy arithmetic:
+ *    separate rounded multiply and add (no FMA), round-half-even rint,
+ *    x86 float->int64 cast semantics (models.py:112-135,221-248).
+ */
+#ifndef LJ_B200_H
+#define LJ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LJ_OK 0
+#define LJ_E_INVALID (-1)   /* bad argument (ValueError in the reference) */
+#define LJ_E_CUDA (-2)      /* CUDA runtime error */
+#define LJ_E_WORKSPACE (-3) /* workspace too small */
+#define LJ_E_NCCL (-4)      /* collective error */
+#define LJ_E_UNSUPPORTED (-5)
+
+#define LJ_SENTINEL_KEY 0xFFFFFFFFFFFFFFFFULL
+
+/* One RMI leaf, 32 B = one DRAM sector (models.py:121-124 operands). */
+typedef struct LjLeaf {
+    double slope;
+    double icpt;
+    int64_t clamp_lo;
+    int64_t clamp_hi;
+} LjLeaf;
+
+/* Two-level linear RMI view (models.py:39-143, RecursiveModelIndex). */
+typedef struct LjRmi {
+    double root_slope;
+    double root_icpt;
+    int64_t m;              /* fanout: number of leaves */
+    int64_t n;              /* trained_len */
+    const LjLeaf *leaves;   /* [m] */
+    const int64_t *err;     /* [2m] interleaved {err_lo, err_hi}; may be NULL
+                               when only positions are needed */
+} LjRmi;
+
+/* Gapped RMI index view (gapped.py:206-338, GappedRmiIndex). */
+typedef struct LjGrmi {
+    LjRmi model;
+    int64_t n;              /* real entries */
+    int64_t L;              /* slot count = round(gap_factor * n) */
+    const uint64_t *slots;  /* [2L] interleaved {gkey, gpayload}; gaps hold
+                               the nearest real key to the left, payload 0 */
+    const uint32_t *bitmap; /* [ceil(L/32)] occupancy bits */
+    int32_t payload_nonzero;/* 1 if every real payload != 0: then a slot is
+                               real iff its payload != 0 and the bitmap is
+                               never read */
+    int32_t _pad;
+} LjGrmi;
+
+/* RadixSpline view (models.py:150-256, RadixSplineIndex). */
+typedef struct LjSpline {
+    int64_t npts;           /* spline points K */
+    int64_t n;              /* trained_len */
+    int64_t max_error;
+    int64_t radix_bits;
+    uint64_t shift;
+    const uint64_t *keys;   /* [K] spline keys */
+    const double *ranks;    /* [K] spline ranks as float64 (models.py:228) */
+    const uint32_t *radix;  /* [2^radix_bits + 1] radix table */
+} LjSpline;
+
+/* Spline-keyed chained hash view (learned_hash.py:17-101). */
+typedef struct LjSplineHash {
+    LjSpline model;
+    int64_t n;              /* entries */
+    int64_t table_len;      /* P */
+    int64_t stride;         /* P / n when n divides P (bucket = pos*stride,
+                               only every stride-th bucket can be occupied):
+                               starts is then indexed by bucket/stride; else 1 */
+    const uint64_t *entries;/* [2n] interleaved {key, payload}, chains in
+                               insertion order */
+    const uint32_t *starts; /* [P/stride + 1] chain offsets (n < 2^32) */
+} LjSplineHash;
+
+/* ------------------------------------------------------------ library */
+const char *lj_last_error(void);
+int lj_version(void);
+/* 1 if a CUDA device of compute capability 10.x is visible, else 0. */
+int lj_device_ok(void);
+
+/* ---------------------------------------------------------- data prep */
+/* data.py:181-192 positional payloads: mix64(i + mix64(seed)) | 1, i in
+ * [offset, offset+n). */
+int lj_fill_payloads(uint64_t *out, int64_t n, int64_t offset, uint64_t seed, void *stream);
+/* out[i] = mix64(seed ^ (offset+i)) (util.py:30-44 finaliser as a counter PRF). */
+int lj_fill_mix64(uint64_t *out, int64_t n, int64_t offset, uint64_t seed, void *stream);
+/* out[i] = src[mulhi64(mix64(seed ^ (offset+i)), src_n)]: uniform draw with
+ * replacement from src (SURVEY 8d C3/C5 counter sampler). */
+int lj_gather_uniform(uint64_t *out, int64_t n, int64_t offset, uint64_t seed, const uint64_t *src,
+                      int64_t src_n, void *stream);
+/* Stable device sort of (key, payload) pairs by key; used by index builds
+ * (data.py:84-86) and the LSJ sample.  */
+size_t lj_sort_pairs_workspace_bytes(int64_t n);
+int lj_sort_pairs(const uint64_t *keys_in, const uint64_t *pay_in, uint64_t *keys_out,
+                  uint64_t *pay_out, int64_t n, int begin_bit, int end_bit, void *ws,
+                  size_t ws_bytes, void *stream);
+
+/* ----------------------------------------------------------- RMI (K10) */
+/* models.py:57-110 on device over sorted keys.  Outputs: root[2]
+ * {slope, icpt}, leaves[m], err[2m].  Deterministic (fixed reduction
+ * order).  */
+size_t lj_rmi_fit_workspace_bytes(int64_t n, int64_t m);
+int lj_rmi_fit(const uint64_t *sorted_keys, int64_t n, int64_t m, double *root, LjLeaf *leaves,
+               int64_t *err, void *ws, size_t ws_bytes, void *stream);
+/* models.py:126-135 predict_many; any output may be NULL. */
+int lj_rmi_predict(const LjRmi *model, const uint64_t *keys, int64_t nk, int64_t *pos,
+                   int64_t *lo, int64_t *hi, int64_t *leaf, void *stream);
+/* models.py:285-299 partition_index for an RMI. */
+int lj_rmi_partition_index(const LjRmi *model, const uint64_t *keys, int64_t nk, int64_t P,
+                           int64_t *out, void *stream);
+
+/* ---------------------------------------------------------- GRMI (K11, K1) */
+/* gapped.py:221-256: model-based insertion of sorted (key, payload) into
+ * L slots + bitmap; *payload_nonzero_dev (1 word) gets the flag. */
+size_t lj_grmi_build_workspace_bytes(int64_t n, int64_t L);
+int lj_grmi_build(const LjRmi *model, const uint64_t *sorted_keys, const uint64_t *sorted_pay,
+                  int64_t n, int64_t L, uint64_t *slots, uint32_t *bitmap,
+                  int32_t *payload_nonzero_dev, void *ws, size_t ws_bytes, void *stream);
+/* gapped.py:258-261 predicted slot per probe. */
+int lj_grmi_predict_slots(const LjGrmi *idx, const uint64_t *keys, int64_t nk, int64_t *out,
+                          void *stream);
+/* gapped.py:86-160 exponential search from given start slots: out_slot
+ * (-1 = absent), out_probes. */
+int lj_grmi_search(const LjGrmi *idx, const int64_t *slots0, const uint64_t *keys, int64_t nk,
+                   int64_t *out_slot, int64_t *out_probes, void *stream);
+/* K1: fused predict + search + run scan + checksum of S against the index.
+ * out[4] = {count, sum, xor, search_steps}; zeroed first unless accumulate. */
+int lj_grmi_probe(const LjGrmi *idx, const uint64_t *s_keys, const uint64_t *s_pay, int64_t nk,
+                  uint64_t *out, int accumulate, void *stream);
+/* Materialisation, gapped.py:163-203: per-probe leftmost slot + match
+ * count, then (after an exclusive scan of counts into offsets) the R
+ * payloads and source indices of every match.  slots0 = start slots of the
+ * searches (gapped.py:294 search_from), or NULL to predict them. */
+int lj_grmi_count(const LjGrmi *idx, const int64_t *slots0, const uint64_t *keys, int64_t nk,
+                  int64_t *lefts, int64_t *counts, int64_t *probes, void *stream);
+int lj_grmi_collect(const LjGrmi *idx, const uint64_t *keys, int64_t nk, const int64_t *lefts,
+                    const int64_t *offsets, uint64_t *out_pay, int64_t *out_src, void *stream);
+
+/* ------------------------------------------------- Request Buffers (K4) */
+/* buffers.py:73-150 analogue: reorder S by RMI leaf (stable counting sort)
+ * so that K1 walks the index leaf by leaf.  hist needs m+1 words of
+ * device scratch inside ws. */
+size_t lj_leaf_bucket_workspace_bytes(int64_t nk, int64_t m);
+int lj_leaf_bucket(const LjRmi *model, const uint64_t *keys, const uint64_t *pay, int64_t nk,
+                   uint64_t *keys_out, uint64_t *pay_out, void *ws, size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------- RadixSpline (K5) */
+/* models.py:171-219 greedy-corridor fit on HOST sorted keys (sequential by
+ * nature).  keys_out/ranks_out hold up to n entries, radix_out 2^r+1.  */
+int lj_spline_fit_host(const uint64_t *sorted_keys_host, int64_t n, int64_t max_error,
+                       int64_t radix_bits, uint64_t *keys_out_host, int64_t *ranks_out_host,
+                       int64_t *radix_out_host, int64_t *npts_out, uint64_t *shift_out);
+int lj_spline_predict(const LjSpline *model, const uint64_t *keys, int64_t nk, int64_t *pos,
+                      int64_t *lo, int64_t *hi, void *stream);
+int lj_spline_partition_index(const LjSpline *model, const uint64_t *keys, int64_t nk, int64_t P,
+                              int64_t *out, void *stream);
+/* learned_hash.py:55-66: chains by partition_index(model, key, P), stable. */
+size_t lj_spline_hash_build_workspace_bytes(int64_t n, int64_t P);
+int lj_spline_hash_build(const LjSpline *model, const uint64_t *keys, const uint64_t *pay,
+                         int64_t n, int64_t P, uint64_t *entries, uint32_t *starts, void *ws,
+                         size_t ws_bytes, void *stream);
+/* K5: learned_hash.py:81-96 fused with the checksum. */
+int lj_spline_hash_probe(const LjSplineHash *idx, const uint64_t *s_keys, const uint64_t *s_pay,
+                         int64_t nk, uint64_t *out, int accumulate, void *stream);
+int lj_spline_hash_count(const LjSplineHash *idx, const uint64_t *keys, int64_t nk,
+                         int64_t *counts, void *stream);
+int lj_spline_hash_collect(const LjSplineHash *idx, const uint64_t *keys, int64_t nk,
+                           const int64_t *offsets, uint64_t *out_pay, int64_t *out_src,
+                           void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LJ_B200_H */

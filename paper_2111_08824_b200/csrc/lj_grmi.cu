@@ -1,0 +1,365 @@
+// lj_grmi.cu -- Gapped-RMI index build (K11), the fused INLJ probe (K1),
+// per-probe search/materialisation kernels and the Request-Buffer analogue
+// (K4, leaf bucketing).  Reference: gapped.py:20-338, buffers.py:73-150.
+//
+// Layout in HBM: one 16-B slot per gapped position, {gkey, gpayload}
+// interleaved, so the slot that ends a search also carries its payload in
+// the same 32-B sector; gap slots copy the nearest real key to their left
+// and hold payload 0 (gapped.py:245-255).  The occupancy bitmap is packed
+// 32 slots per word and is only read when some real payload is 0.
+#include <cub/cub.cuh>
+
+#include "lj_common.cuh"
+
+namespace lj {
+
+struct MaxOpG {
+    __device__ __forceinline__ i64 operator()(const i64 &a, const i64 &b) const {
+        return a > b ? a : b;
+    }
+};
+
+struct GrmiDev {
+    RmiDev model;
+    i64 n, L;
+    const u64 *slots;
+    const u32 *bitmap;
+    int payload_nonzero;
+    __host__ explicit GrmiDev(const LjGrmi &g)
+        : model(g.model), n(g.n), L(g.L), slots(g.slots), bitmap(g.bitmap),
+          payload_nonzero(g.payload_nonzero) {}
+
+    __device__ __forceinline__ u64 key(i64 i) const { return ldg(slots + 2 * i); }
+    __device__ __forceinline__ i64 predict_slot(u64 k) const {
+        return grmi_slot_of_pos(model.pos(u64_to_f64(k)), n, L);
+    }
+    __device__ __forceinline__ bool real(i64 i, u64 pay) const {
+        if (payload_nonzero) return pay != 0;
+        return (__ldg(bitmap + (i >> 5)) >> (i & 31)) & 1u;
+    }
+
+    // gapped.py:86-160 -- exponential search from `start`, one lane per
+    // probe; returns any slot of the equal-key run or -1 and counts probes
+    // exactly as the reference does.
+    __device__ __forceinline__ i64 search(i64 start, u64 k, i64 &probes) const {
+        probes = 1;
+        u64 v = key(start);
+        if (v == k) return start;
+        i64 lo, hi;
+        if (v < k) {
+            i64 prev = start, step = 1;
+            for (;;) {
+                i64 idx = start + step;
+                if (idx >= L) { lo = prev + 1; hi = L; break; }
+                ++probes;
+                u64 w = key(idx);
+                if (w < k) { prev = idx; step <<= 1; }
+                else if (w == k) return idx;
+                else { lo = prev + 1; hi = idx; break; }
+            }
+        } else {
+            i64 prev = start, step = 1;
+            for (;;) {
+                i64 idx = start - step;
+                if (idx < 0) { lo = 0; hi = prev; break; }
+                ++probes;
+                u64 w = key(idx);
+                if (w > k) { prev = idx; step <<= 1; }
+                else if (w == k) return idx;
+                else { lo = idx + 1; hi = prev; break; }
+            }
+        }
+        while (lo < hi) {
+            i64 mid = (lo + hi) >> 1;
+            ++probes;
+            if (key(mid) < k) lo = mid + 1; else hi = mid;
+        }
+        if (lo < L) {
+            ++probes;
+            if (key(lo) == k) return lo;
+        }
+        return -1;
+    }
+};
+
+// ------------------------------------------------------------ build (K11)
+
+// target_i - i, target_i = rint(pos_i / n * L) (gapped.py:238-240)
+__global__ void k_grmi_targets(RmiDev r, const u64 *sk, i64 n, i64 L, i64 *d) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+        i64 pos = r.pos(u64_to_f64(sk[i]));
+        double t = rint(__dmul_rn(__ddiv_rn(i64_to_f64(pos), i64_to_f64(n)), i64_to_f64(L)));
+        d[i] = f64_to_i64(t) - i;
+    }
+}
+
+// slot_i = min(cummax_i + i, L - n + i) (gapped.py:241-243); scatter
+__global__ void k_grmi_place(const i64 *cm, const u64 *sk, const u64 *sp, i64 n, i64 L, u64 *slots,
+                             u32 *bitmap, int *nonzero) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+        i64 s = cm[i] + i, cap = L - n + i;
+        s = s < cap ? s : cap;
+        u64 pay = sp[i];
+        slots[2 * s] = sk[i];
+        slots[2 * s + 1] = pay;
+        atomicOr(bitmap + (s >> 5), 1u << (s & 31));
+        if (pay == 0) *nonzero = 0;
+    }
+}
+
+__global__ void k_grmi_fill_src(const u32 *bitmap, i64 L, i64 *f) {
+    for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < L; j += (i64)gridDim.x * blockDim.x)
+        f[j] = ((bitmap[j >> 5] >> (j & 31)) & 1u) ? j : -1;
+}
+
+// gap fill with the nearest real key to the left; slots before the first
+// entry copy it (gapped.py:250-252)
+__global__ void k_grmi_fill(const u32 *bitmap, const i64 *f, const i64 *cm, i64 n, i64 L, u64 *slots) {
+    i64 first = cm[0] < L - n ? cm[0] : L - n;  // slot of entry 0
+    for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < L; j += (i64)gridDim.x * blockDim.x) {
+        if ((bitmap[j >> 5] >> (j & 31)) & 1u) continue;
+        i64 src = f[j] < 0 ? first : f[j];
+        slots[2 * j] = slots[2 * src];
+    }
+}
+
+// ------------------------------------------------------------ probe (K1)
+
+// Fused per-probe join: predict (gapped.py:258-261), exponential search
+// (:86-160), equal-run scan and real-entry gather (:163-203), reduced to
+// the checksum of t = R.payload + S.payload.  One lane per probe; the S
+// stream is read once with evict-first loads.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_grmi_probe(GrmiDev g, const u64 *__restrict__ skeys,
+                                                   const u64 *__restrict__ spay, i64 nk, u64 *out) {
+    u64 cnt = 0, sum = 0, x = 0, steps = 0;
+    for (i64 t = blockIdx.x * (i64)NT + threadIdx.x; t < nk; t += (i64)gridDim.x * NT) {
+        u64 k = ld_stream(skeys + t);
+        u64 ps = ld_stream(spay + t);
+        i64 probes;
+        i64 s = g.search(g.predict_slot(k), k, probes);
+        steps += (u64)probes;
+        if (s < 0) continue;
+        while (s > 0 && g.key(s - 1) == k) --s;  // leftmost slot of the run is real
+        for (; s < g.L; ++s) {
+            ulonglong2 e = ldg2(g.slots + 2 * s);
+            if (e.x != k) break;
+            if (!g.real(s, e.y)) continue;
+            u64 v = e.y + ps;
+            ++cnt;
+            sum += v;
+            x ^= v;
+        }
+    }
+    reduce_checksum(cnt, sum, x, steps, out);
+}
+
+__global__ void k_grmi_predict_slots(GrmiDev g, const u64 *keys, i64 nk, i64 *out) {
+    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < nk; t += (i64)gridDim.x * blockDim.x)
+        out[t] = g.predict_slot(keys[t]);
+}
+
+__global__ void k_grmi_search(GrmiDev g, const i64 *slots0, const u64 *keys, i64 nk, i64 *out_slot,
+                              i64 *out_probes) {
+    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < nk; t += (i64)gridDim.x * blockDim.x) {
+        i64 probes;
+        i64 start = slots0[t];
+        start = start < 0 ? 0 : (start >= g.L ? g.L - 1 : start);
+        out_slot[t] = g.search(start, keys[t], probes);
+        out_probes[t] = probes;
+    }
+}
+
+// gapped.py:163-185 (+ the search): leftmost slot and real-entry count
+__global__ void k_grmi_count(GrmiDev g, const i64 *slots0, const u64 *keys, i64 nk, i64 *lefts, i64 *counts,
+                             i64 *probes_out) {
+    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < nk; t += (i64)gridDim.x * blockDim.x) {
+        u64 k = keys[t];
+        i64 probes;
+        i64 start = slots0 ? clip_i64(slots0[t], 0, g.L - 1) : g.predict_slot(k);
+        i64 s = g.search(start, k, probes);
+        if (probes_out) probes_out[t] = probes;
+        i64 c = 0;
+        if (s >= 0) {
+            while (s > 0 && g.key(s - 1) == k) --s;
+            for (i64 i = s; i < g.L; ++i) {
+                ulonglong2 e = ldg2(g.slots + 2 * i);
+                if (e.x != k) break;
+                c += g.real(i, e.y) ? 1 : 0;
+            }
+        }
+        lefts[t] = s;
+        counts[t] = c;
+    }
+}
+
+// gapped.py:188-203
+__global__ void k_grmi_collect(GrmiDev g, const u64 *keys, i64 nk, const i64 *lefts, const i64 *offsets,
+                               u64 *out_pay, i64 *out_src) {
+    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < nk; t += (i64)gridDim.x * blockDim.x) {
+        i64 s = lefts[t];
+        if (s < 0) continue;
+        u64 k = keys[t];
+        i64 o = offsets[t];
+        for (i64 i = s; i < g.L; ++i) {
+            ulonglong2 e = ldg2(g.slots + 2 * i);
+            if (e.x != k) break;
+            if (!g.real(i, e.y)) continue;
+            out_pay[o] = e.y;
+            out_src[o] = t;
+            ++o;
+        }
+    }
+}
+
+// ------------------------------------------------------- leaf bucket (K4)
+
+__global__ void k_leaf_hist(RmiDev r, const u64 *keys, i64 nk, u32 *hist) {
+    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < nk; t += (i64)gridDim.x * blockDim.x)
+        atomicAdd(hist + r.route(u64_to_f64(ld_stream(keys + t))), 1u);
+}
+
+__global__ void k_leaf_scatter(RmiDev r, const u64 *keys, const u64 *pay, i64 nk, u32 *cursor,
+                               u64 *ko, u64 *po) {
+    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < nk; t += (i64)gridDim.x * blockDim.x) {
+        u64 k = ld_stream(keys + t);
+        u32 d = atomicAdd(cursor + r.route(u64_to_f64(k)), 1u);
+        ko[d] = k;
+        po[d] = ld_stream(pay + t);
+    }
+}
+
+static size_t al(size_t v) { return (v + 255) & ~(size_t)255; }
+
+static size_t scan_i64_bytes(i64 n) {
+    size_t t = 0;
+    cub::DeviceScan::InclusiveScan((void *)nullptr, t, (i64 *)nullptr, (i64 *)nullptr, MaxOpG(), (int64_t)n);
+    return t;
+}
+
+}  // namespace lj
+
+using namespace lj;
+
+extern "C" {
+
+size_t lj_grmi_build_workspace_bytes(int64_t n, int64_t L) {
+    size_t a = scan_i64_bytes(n), b = scan_i64_bytes(L);
+    return al(sizeof(i64) * (size_t)n) + al(sizeof(i64) * (size_t)L) + al(a > b ? a : b);
+}
+
+int lj_grmi_build(const LjRmi *model, const uint64_t *sk, const uint64_t *sp, int64_t n, int64_t L,
+                  uint64_t *slots, uint32_t *bitmap, int32_t *payload_nonzero_dev, void *ws,
+                  size_t ws_bytes, void *stream) {
+    LJ_REQUIRE(model && model->m >= 1 && model->n == n, "model must be fitted on the n sorted keys");
+    LJ_REQUIRE(n >= 1 && L >= n, "need n >= 1 and L >= n");
+    if (ws_bytes < lj_grmi_build_workspace_bytes(n, L)) {
+        set_error("lj_grmi_build: workspace too small");
+        return LJ_E_WORKSPACE;
+    }
+    cudaStream_t st = as_stream(stream);
+    char *p = (char *)ws;
+    i64 *cm = (i64 *)p;
+    p += al(sizeof(i64) * (size_t)n);
+    i64 *f = (i64 *)p;
+    p += al(sizeof(i64) * (size_t)L);
+    size_t sb = scan_i64_bytes(n > L ? n : L);
+    int one = 1;
+    LJ_CK(cudaMemsetAsync(slots, 0, sizeof(u64) * 2 * (size_t)L, st));
+    LJ_CK(cudaMemsetAsync(bitmap, 0, sizeof(u32) * (size_t)((L + 31) / 32), st));
+    LJ_CK(cudaMemcpyAsync(payload_nonzero_dev, &one, sizeof(int), cudaMemcpyHostToDevice, st));
+    k_grmi_targets<<<grid_for(n, 256, 8), 256, 0, st>>>(RmiDev(*model), sk, n, L, cm);
+    LJ_CK_LAUNCH();
+    LJ_CK(cub::DeviceScan::InclusiveScan(p, sb, cm, cm, MaxOpG(), (int64_t)n, st));
+    k_grmi_place<<<grid_for(n, 256, 8), 256, 0, st>>>(cm, sk, sp, n, L, slots, bitmap, payload_nonzero_dev);
+    k_grmi_fill_src<<<grid_for(L, 256, 8), 256, 0, st>>>(bitmap, L, f);
+    LJ_CK_LAUNCH();
+    LJ_CK(cub::DeviceScan::InclusiveScan(p, sb, f, f, MaxOpG(), (int64_t)L, st));
+    k_grmi_fill<<<grid_for(L, 256, 8), 256, 0, st>>>(bitmap, f, cm, n, L, slots);
+    LJ_CK_LAUNCH();
+    // the host copy of `one` must outlive the async copy
+    LJ_CK(cudaStreamSynchronize(st));
+    return LJ_OK;
+}
+
+int lj_grmi_predict_slots(const LjGrmi *idx, const uint64_t *keys, int64_t nk, int64_t *out, void *stream) {
+    LJ_REQUIRE(idx && idx->n >= 1, "index is empty");
+    if (nk <= 0) return LJ_OK;
+    k_grmi_predict_slots<<<grid_for(nk, 256, 8), 256, 0, as_stream(stream)>>>(GrmiDev(*idx), keys, nk, out);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+int lj_grmi_search(const LjGrmi *idx, const int64_t *slots0, const uint64_t *keys, int64_t nk,
+                   int64_t *out_slot, int64_t *out_probes, void *stream) {
+    LJ_REQUIRE(idx && idx->n >= 1, "index is empty");
+    if (nk <= 0) return LJ_OK;
+    k_grmi_search<<<grid_for(nk, 256, 8), 256, 0, as_stream(stream)>>>(GrmiDev(*idx), slots0, keys, nk,
+                                                                        out_slot, out_probes);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+int lj_grmi_probe(const LjGrmi *idx, const uint64_t *s_keys, const uint64_t *s_pay, int64_t nk,
+                  uint64_t *out, int accumulate, void *stream) {
+    LJ_REQUIRE(idx != nullptr, "null index");
+    cudaStream_t st = as_stream(stream);
+    if (!accumulate) LJ_CK(cudaMemsetAsync(out, 0, 4 * sizeof(u64), st));
+    if (nk <= 0 || idx->n == 0) return LJ_OK;
+    constexpr int NT = 256;
+    k_grmi_probe<NT><<<grid_for(nk, NT, 8), NT, 0, st>>>(GrmiDev(*idx), s_keys, s_pay, nk, out);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+int lj_grmi_count(const LjGrmi *idx, const int64_t *slots0, const uint64_t *keys, int64_t nk, int64_t *lefts,
+                  int64_t *counts, int64_t *probes, void *stream) {
+    LJ_REQUIRE(idx && idx->n >= 1, "index is empty");
+    if (nk <= 0) return LJ_OK;
+    k_grmi_count<<<grid_for(nk, 256, 8), 256, 0, as_stream(stream)>>>(GrmiDev(*idx), slots0, keys, nk,
+                                                                       lefts, counts, probes);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+int lj_grmi_collect(const LjGrmi *idx, const uint64_t *keys, int64_t nk, const int64_t *lefts,
+                    const int64_t *offsets, uint64_t *out_pay, int64_t *out_src, void *stream) {
+    LJ_REQUIRE(idx && idx->n >= 1, "index is empty");
+    if (nk <= 0) return LJ_OK;
+    k_grmi_collect<<<grid_for(nk, 256, 8), 256, 0, as_stream(stream)>>>(GrmiDev(*idx), keys, nk, lefts,
+                                                                         offsets, out_pay, out_src);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+size_t lj_leaf_bucket_workspace_bytes(int64_t nk, int64_t m) {
+    size_t t = 0;
+    cub::DeviceScan::ExclusiveSum((void *)nullptr, t, (u32 *)nullptr, (u32 *)nullptr, (int64_t)m);
+    return al(sizeof(u32) * (size_t)(m + 1)) + al(t);
+}
+
+int lj_leaf_bucket(const LjRmi *model, const uint64_t *keys, const uint64_t *pay, int64_t nk,
+                   uint64_t *keys_out, uint64_t *pay_out, void *ws, size_t ws_bytes, void *stream) {
+    LJ_REQUIRE(model && model->m >= 1, "model is not fitted");
+    LJ_REQUIRE(nk < (int64_t)0xFFFFFFFFLL, "leaf bucketing counts in 32 bits");
+    if (ws_bytes < lj_leaf_bucket_workspace_bytes(nk, model->m)) {
+        set_error("lj_leaf_bucket: workspace too small");
+        return LJ_E_WORKSPACE;
+    }
+    if (nk <= 0) return LJ_OK;
+    cudaStream_t st = as_stream(stream);
+    u32 *hist = (u32 *)ws;
+    char *tmp = (char *)ws + al(sizeof(u32) * (size_t)(model->m + 1));
+    size_t t = 0;
+    cub::DeviceScan::ExclusiveSum((void *)nullptr, t, hist, hist, (int64_t)model->m);
+    LJ_CK(cudaMemsetAsync(hist, 0, sizeof(u32) * (size_t)(model->m + 1), st));
+    RmiDev r(*model);
+    k_leaf_hist<<<grid_for(nk, 256, 8), 256, 0, st>>>(r, keys, nk, hist);
+    LJ_CK_LAUNCH();
+    LJ_CK(cub::DeviceScan::ExclusiveSum(tmp, t, hist, hist, (int64_t)model->m, st));
+    k_leaf_scatter<<<grid_for(nk, 256, 8), 256, 0, st>>>(r, keys, pay, nk, hist, keys_out, pay_out);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+}  // extern "C"

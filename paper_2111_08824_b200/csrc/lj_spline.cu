@@ -1,0 +1,224 @@
+// lj_spline.cu -- RadixSpline evaluation, the spline-keyed chained hash
+// build and the fused probe (K5).  Reference: models.py:150-299,
+// learned_hash.py:17-101.
+//
+// Layout in HBM: entries {key, payload} interleaved 16 B, grouped by
+// bucket in insertion order (the reference's stable argsort,
+// learned_hash.py:60); chain offsets `starts` in 32-bit words.  When the
+// table length P is a multiple of n (the default table_factor 4.0 gives
+// P = 4n), partition_index is exactly pos * (P/n) -- injective, with every
+// non-multiple bucket empty -- so starts is indexed by pos and holds n+1
+// words instead of P+1 (16 B/key smaller, results identical).
+#include <cub/cub.cuh>
+
+#include "lj_common.cuh"
+
+namespace lj {
+
+struct HashDev {
+    SplineDev model;
+    i64 n, P, stride;
+    const u64 *entries;
+    const u32 *starts;
+    __host__ explicit HashDev(const LjSplineHash &h)
+        : model(h.model), n(h.n), P(h.table_len), stride(h.stride), entries(h.entries), starts(h.starts) {}
+    __device__ __forceinline__ i64 slot_of(u64 k) const {
+        return scale_bucket(model.pos(k), P, model.n) / stride;
+    }
+};
+
+__global__ void k_spline_predict(SplineDev m, const u64 *keys, i64 nk, i64 *pos, i64 *lo, i64 *hi) {
+    i64 last = m.n - 1;
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < nk; i += (i64)gridDim.x * blockDim.x) {
+        i64 p = m.pos(keys[i]);
+        if (pos) pos[i] = p;
+        if (lo) lo[i] = clip_i64(p - m.max_error, 0, last);
+        if (hi) hi[i] = clip_i64(p + m.max_error, 0, last);
+    }
+}
+
+__global__ void k_spline_partition(SplineDev m, const u64 *keys, i64 nk, i64 P, i64 *out) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < nk; i += (i64)gridDim.x * blockDim.x)
+        out[i] = scale_bucket(m.pos(keys[i]), P, m.n);
+}
+
+// build: (bucket/stride, original index) pairs for a stable sort
+__global__ void k_hash_bucket_of(SplineDev m, const u64 *keys, i64 n, i64 P, i64 stride, u64 *bk, u64 *idx) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+        bk[i] = (u64)(scale_bucket(m.pos(keys[i]), P, m.n) / stride);
+        idx[i] = (u64)i;
+    }
+}
+
+__global__ void k_hash_gather(const u64 *order, const u64 *keys, const u64 *pay, i64 n, u64 *entries) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+        u64 j = order[i];
+        entries[2 * i] = keys[j];
+        entries[2 * i + 1] = pay[j];
+    }
+}
+
+// starts[b] = first sorted position with bucket >= b, for b in [0, nb]
+__global__ void k_hash_starts(const u64 *sorted_b, i64 n, i64 nb, u32 *starts) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i <= n; i += (i64)gridDim.x * blockDim.x) {
+        i64 prev = i == 0 ? -1 : (i64)sorted_b[i - 1];
+        i64 cur = i == n ? nb : (i64)sorted_b[i];
+        for (i64 b = prev + 1; b <= cur; ++b) starts[b] = (u32)i;
+    }
+}
+
+// K5: learned_hash.py:81-96 fused with the checksum.  One lane per probe:
+// spline position (radix table + bounded search over spline points, both
+// L2-resident), bucket, chain offsets, chain scan.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_hash_probe(HashDev h, const u64 *__restrict__ skeys,
+                                                   const u64 *__restrict__ spay, i64 nk, u64 *out) {
+    u64 cnt = 0, sum = 0, x = 0;
+    for (i64 t = blockIdx.x * (i64)NT + threadIdx.x; t < nk; t += (i64)gridDim.x * NT) {
+        u64 k = ld_stream(skeys + t);
+        u64 ps = ld_stream(spay + t);
+        i64 b = h.slot_of(k);
+        u32 a = __ldg(h.starts + b), e = __ldg(h.starts + b + 1);
+        for (u32 i = a; i < e; ++i) {
+            ulonglong2 en = ldg2(h.entries + 2 * (i64)i);
+            if (en.x != k) continue;
+            u64 v = en.y + ps;
+            ++cnt;
+            sum += v;
+            x ^= v;
+        }
+    }
+    reduce_checksum(cnt, sum, x, 0, out);
+}
+
+__global__ void k_hash_count(HashDev h, const u64 *keys, i64 nk, i64 *counts) {
+    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < nk; t += (i64)gridDim.x * blockDim.x) {
+        u64 k = keys[t];
+        i64 b = h.slot_of(k);
+        i64 c = 0;
+        for (u32 i = h.starts[b]; i < h.starts[b + 1]; ++i) c += h.entries[2 * (i64)i] == k;
+        counts[t] = c;
+    }
+}
+
+__global__ void k_hash_collect(HashDev h, const u64 *keys, i64 nk, const i64 *offsets, u64 *out_pay,
+                               i64 *out_src) {
+    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < nk; t += (i64)gridDim.x * blockDim.x) {
+        u64 k = keys[t];
+        i64 b = h.slot_of(k);
+        i64 o = offsets[t];
+        for (u32 i = h.starts[b]; i < h.starts[b + 1]; ++i) {
+            if (h.entries[2 * (i64)i] != k) continue;
+            out_pay[o] = h.entries[2 * (i64)i + 1];
+            out_src[o] = t;
+            ++o;
+        }
+    }
+}
+
+static size_t al(size_t v) { return (v + 255) & ~(size_t)255; }
+
+static int end_bit_for(u64 maxv) {
+    int b = 0;
+    while (b < 64 && (maxv >> b)) ++b;
+    return b < 1 ? 1 : b;
+}
+
+}  // namespace lj
+
+using namespace lj;
+
+extern "C" {
+
+int lj_spline_predict(const LjSpline *model, const uint64_t *keys, int64_t nk, int64_t *pos, int64_t *lo,
+                      int64_t *hi, void *stream) {
+    LJ_REQUIRE(model && model->npts >= 1 && model->n >= 1, "model is not fitted");
+    if (nk <= 0) return LJ_OK;
+    k_spline_predict<<<grid_for(nk, 256, 8), 256, 0, as_stream(stream)>>>(SplineDev(*model), keys, nk,
+                                                                           pos, lo, hi);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+int lj_spline_partition_index(const LjSpline *model, const uint64_t *keys, int64_t nk, int64_t P,
+                              int64_t *out, void *stream) {
+    LJ_REQUIRE(model && model->npts >= 1 && model->n >= 1, "model is not fitted");
+    LJ_REQUIRE(P >= 1, "num_partitions must be >= 1");
+    if (nk <= 0) return LJ_OK;
+    k_spline_partition<<<grid_for(nk, 256, 8), 256, 0, as_stream(stream)>>>(SplineDev(*model), keys, nk,
+                                                                             P, out);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+size_t lj_spline_hash_build_workspace_bytes(int64_t n, int64_t P) {
+    (void)P;
+    size_t t = 0;
+    cub::DeviceRadixSort::SortPairs((void *)nullptr, t, (const u64 *)nullptr, (u64 *)nullptr,
+                                    (const u64 *)nullptr, (u64 *)nullptr, (int64_t)n, 0, 64);
+    return 4 * al(sizeof(u64) * (size_t)n) + al(t);
+}
+
+int lj_spline_hash_build(const LjSpline *model, const uint64_t *keys, const uint64_t *pay, int64_t n,
+                         int64_t P, uint64_t *entries, uint32_t *starts, void *ws, size_t ws_bytes,
+                         void *stream) {
+    LJ_REQUIRE(model && model->npts >= 1 && model->n >= 1, "model is not fitted");
+    LJ_REQUIRE(n >= 1 && P >= 1, "need n >= 1 and P >= 1");
+    LJ_REQUIRE(n < (int64_t)0xFFFFFFFFLL, "chain offsets are 32-bit: n must be < 2^32");
+    if (ws_bytes < lj_spline_hash_build_workspace_bytes(n, P)) {
+        set_error("lj_spline_hash_build: workspace too small");
+        return LJ_E_WORKSPACE;
+    }
+    cudaStream_t st = as_stream(stream);
+    i64 stride = (P % n == 0) ? P / n : 1;
+    i64 nb = P / stride;
+    char *p = (char *)ws;
+    u64 *bk = (u64 *)p; p += al(sizeof(u64) * (size_t)n);
+    u64 *idx = (u64 *)p; p += al(sizeof(u64) * (size_t)n);
+    u64 *bk2 = (u64 *)p; p += al(sizeof(u64) * (size_t)n);
+    u64 *idx2 = (u64 *)p; p += al(sizeof(u64) * (size_t)n);
+    k_hash_bucket_of<<<grid_for(n, 256, 8), 256, 0, st>>>(SplineDev(*model), keys, n, P, stride, bk, idx);
+    LJ_CK_LAUNCH();
+    int eb = end_bit_for((u64)nb);
+    size_t t = 0;
+    LJ_CK(cub::DeviceRadixSort::SortPairs((void *)nullptr, t, bk, bk2, idx, idx2, (int64_t)n, 0, eb, st));
+    // radix sort is stable: chains keep insertion order (learned_hash.py:60)
+    LJ_CK(cub::DeviceRadixSort::SortPairs(p, t, bk, bk2, idx, idx2, (int64_t)n, 0, eb, st));
+    k_hash_gather<<<grid_for(n, 256, 8), 256, 0, st>>>(idx2, keys, pay, n, entries);
+    k_hash_starts<<<grid_for(n + 1, 256, 8), 256, 0, st>>>(bk2, n, nb, starts);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+int lj_spline_hash_probe(const LjSplineHash *idx, const uint64_t *s_keys, const uint64_t *s_pay,
+                         int64_t nk, uint64_t *out, int accumulate, void *stream) {
+    LJ_REQUIRE(idx != nullptr, "null index");
+    cudaStream_t st = as_stream(stream);
+    if (!accumulate) LJ_CK(cudaMemsetAsync(out, 0, 4 * sizeof(u64), st));
+    if (nk <= 0 || idx->n == 0) return LJ_OK;
+    constexpr int NT = 256;
+    k_hash_probe<NT><<<grid_for(nk, NT, 8), NT, 0, st>>>(HashDev(*idx), s_keys, s_pay, nk, out);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+int lj_spline_hash_count(const LjSplineHash *idx, const uint64_t *keys, int64_t nk, int64_t *counts,
+                         void *stream) {
+    LJ_REQUIRE(idx && idx->n >= 1, "index is empty");
+    if (nk <= 0) return LJ_OK;
+    k_hash_count<<<grid_for(nk, 256, 8), 256, 0, as_stream(stream)>>>(HashDev(*idx), keys, nk, counts);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+int lj_spline_hash_collect(const LjSplineHash *idx, const uint64_t *keys, int64_t nk, const int64_t *offsets,
+                           uint64_t *out_pay, int64_t *out_src, void *stream) {
+    LJ_REQUIRE(idx && idx->n >= 1, "index is empty");
+    if (nk <= 0) return LJ_OK;
+    k_hash_collect<<<grid_for(nk, 256, 8), 256, 0, as_stream(stream)>>>(HashDev(*idx), keys, nk, offsets,
+                                                                         out_pay, out_src);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+}  // extern "C"

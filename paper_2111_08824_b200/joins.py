@@ -1,0 +1,226 @@
+"""The drop-in boundary: the reference's runner registry (bench.py:277-318)
+for the learned-join hot paths, backed by the CUDA library.
+
+Every runner has the reference signature
+``fn(r, s, workers, opts) -> (JoinResult, PhaseBreakdown, runtime_s)``.
+``workers`` is the share-nothing unit: S is cut into ``workers`` chunks
+with ``chunk_bounds`` exactly like the reference (bench.py:111-125), each
+chunk probed on the device, partial checksums accumulated on device.  (Across
+GPUs the unit is one process per GPU: see ``dist.py``.)  Index builds are
+untimed, as in the reference (bench.py:138-144,202-209); LSJ is timed end to
+end.  Results come back as device-reduced checksums; ``opts["materialize"]``
+returns the pairs themselves (reference ``JoinResult`` semantics).
+"""
+
+from __future__ import annotations
+
+import json
+import time
+from dataclasses import dataclass
+
+import torch
+
+from .buffers import DEFAULT_BUFFER_CAP, schedule_leaf_switches
+from .data import Relation
+from .gapped import GappedRmiIndex
+from .learned_hash import SplineHashIndex
+from .results import JoinResult, PhaseBreakdown
+from .util import chunk_bounds
+
+DEFAULT_OPTS = {
+    "gap_factor": 4.0,
+    "rmi_fanout": 1000,
+    "buffer_cap": DEFAULT_BUFFER_CAP,
+    "spline_error": 32,
+    "radix_bits": 18,
+    "table_factor": 4.0,
+    "bucket_size": 4,
+    "sample_rate": 0.01,
+    "hash_sample_rate": 0.02,
+    "fanout": 10000,
+    "swwc": True,
+    "passes": 2,
+    "bits_per_pass": 6,
+    "seed": 42,
+    # GPU-only knobs (absent from the reference)
+    "materialize": False,
+    "counters": True,
+}
+
+
+@dataclass
+class BenchReport:
+    """bench.py:46-71 one JSON object per run, plus the checksum."""
+
+    algorithm: str
+    dataset: dict
+    workers: int
+    config: dict
+    runtime_s: float
+    throughput: float
+    result_count: int
+    breakdown: dict
+    repetition: int = 0
+    checksum: tuple = (0, 0, 0)
+
+    def to_json(self) -> str:
+        return json.dumps({
+            "algorithm": self.algorithm, "dataset": self.dataset, "workers": self.workers,
+            "config": self.config, "runtime_s": self.runtime_s, "throughput": self.throughput,
+            "result_count": self.result_count, "repetition": self.repetition, "breakdown": self.breakdown,
+            "checksum_sum": self.checksum[1], "checksum_xor": self.checksum[2],
+        })
+
+
+def _timed(fn):
+    """Wall time of a device-synchronised call (the reference times with
+    perf_counter around the whole probe, bench.py:141-143)."""
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    out = fn()
+    torch.cuda.synchronize()
+    return out, time.perf_counter() - t0
+
+
+def _chunks(n, workers):
+    b = chunk_bounds(n, max(1, int(workers)))
+    return [(int(b[w]), int(b[w + 1])) for w in range(len(b) - 1)]
+
+
+def _materialized_probe(index, s: Relation, workers: int, br: PhaseBreakdown) -> JoinResult:
+    parts = []
+    for lo, hi in _chunks(len(s), workers):
+        if hi == lo:
+            continue
+        if isinstance(index, GappedRmiIndex):
+            pays, src, _ = index.search_from(None, s.keys[lo:hi], br.lookup_stats)
+        else:
+            pays, src = index.probe_batch(s.keys[lo:hi])
+        parts.append(JoinResult(pays, s.payloads[lo:hi][src]))
+    return JoinResult.concatenate(parts)
+
+
+def _fused_probe(index, s: Relation, workers: int) -> torch.Tensor:
+    out = torch.zeros(4, dtype=torch.int64, device=s.keys.device)
+    for lo, hi in _chunks(len(s), workers):
+        index.join_checksum(s.keys[lo:hi], s.payloads[lo:hi], out=out, accumulate=True)
+    return out
+
+
+def _empty():
+    return JoinResult(), PhaseBreakdown(), 0.0
+
+
+def _run_grmi_inlj(r, s, workers, opts):
+    """bench.py:138-144: GRMI fit untimed, probe timed."""
+    index = GappedRmiIndex(opts["gap_factor"], opts["rmi_fanout"]).fit(r)
+    br = PhaseBreakdown()
+    if opts.get("materialize"):
+        result, runtime = _timed(lambda: _materialized_probe(index, s, workers, br))
+    else:
+        words, runtime = _timed(lambda: _fused_probe(index, s, workers))
+        w = words.cpu().tolist()
+        result = JoinResult(checksum=(int(w[0]), int(w[1]) & (2**64 - 1), int(w[2]) & (2**64 - 1)))
+        br.lookup_stats.search_steps = int(w[3])
+        br.lookup_stats.predictions = len(s)
+    br.srch = runtime  # predict + search are one fused kernel (K1)
+    if opts.get("counters", True) and len(s) and index.n:
+        leaf = index.leaf_of(s.keys)  # canonical full-stream counter (bench.py:130-134)
+        br.lookup_stats.leaf_switches = int((leaf[1:] != leaf[:-1]).sum().item())
+    return result, br, runtime
+
+
+def _run_buffered_grmi_inlj(r, s, workers, opts):
+    """bench.py:147-181: request buffers -> device leaf bucketing (K4) of
+    each S chunk, then the fused probe (K1) over the bucketed chunk."""
+    from . import _lib
+    import ctypes
+
+    index = GappedRmiIndex(opts["gap_factor"], opts["rmi_fanout"]).fit(r)
+    br = PhaseBreakdown()
+    if index.n == 0 or len(s) == 0:
+        return JoinResult(), br, 0.0
+    lib = _lib.lib()
+    m = index.rmi.fanout
+    kb = torch.empty_like(s.keys)
+    pb = torch.empty_like(s.payloads)
+    ws = _lib.workspace(lib.lj_leaf_bucket_workspace_bytes(len(s), m), s.keys.device)
+    c = index.rmi.c_struct()
+
+    def run():
+        out = torch.zeros(4, dtype=torch.int64, device=s.keys.device)
+        for lo, hi in _chunks(len(s), workers):
+            if hi == lo:
+                continue
+            _lib.check(lib.lj_leaf_bucket(ctypes.byref(c), _lib.ptr(s.keys[lo:hi]), _lib.ptr(s.payloads[lo:hi]),
+                                          hi - lo, _lib.ptr(kb[lo:hi]), _lib.ptr(pb[lo:hi]), _lib.ptr(ws),
+                                          ws.numel(), _lib.stream_ptr()), "leaf_bucket")
+            index.join_checksum(kb[lo:hi], pb[lo:hi], out=out, accumulate=True)
+        return out
+
+    if opts.get("materialize"):
+        result, runtime = _timed(lambda: _materialized_probe(index, s, workers, br))
+    else:
+        words, runtime = _timed(run)
+        w = words.cpu().tolist()
+        result = JoinResult(checksum=(int(w[0]), int(w[1]) & (2**64 - 1), int(w[2]) & (2**64 - 1)))
+        br.lookup_stats.search_steps = int(w[3])
+        br.lookup_stats.predictions = len(s)
+    if opts.get("counters", True):
+        br.lookup_stats.leaf_switches = schedule_leaf_switches(index.leaf_of(s.keys), opts["buffer_cap"])
+    br.join = runtime
+    return result, br, runtime
+
+
+def _run_spline_hash_inlj(r, s, workers, opts):
+    """bench.py:202-221: spline-hash fit untimed, probe timed (booked as pred)."""
+    if len(r) == 0:
+        return _empty()
+    index = SplineHashIndex(opts["spline_error"], opts["radix_bits"], opts["table_factor"]).fit(r)
+    br = PhaseBreakdown()
+    if opts.get("materialize"):
+        result, runtime = _timed(lambda: _materialized_probe(index, s, workers, br))
+    else:
+        words, runtime = _timed(lambda: _fused_probe(index, s, workers))
+        w = words.cpu().tolist()
+        result = JoinResult(checksum=(int(w[0]), int(w[1]) & (2**64 - 1), int(w[2]) & (2**64 - 1)))
+    br.pred = runtime
+    br.lookup_stats.predictions = len(s)
+    return result, br, runtime
+
+
+def _run_lsj(r, s, workers, opts):
+    """bench.py:224-234: LSJ timed end to end."""
+    from .lsj import LsjConfig, lsj_join
+
+    config = LsjConfig(workers=workers, sample_rate=opts["sample_rate"], fanout=opts["fanout"],
+                       swwc=opts["swwc"], seed=opts["seed"])
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    result, br = lsj_join(r, s, config, materialize=bool(opts.get("materialize")))
+    _ = result.checksum  # the 3-word readback is part of the join
+    return result, br, time.perf_counter() - t0
+
+
+ALGORITHMS = {
+    "buffered-grmi-inlj": _run_buffered_grmi_inlj,
+    "grmi-inlj": _run_grmi_inlj,
+    "spline-hash-inlj": _run_spline_hash_inlj,
+    "lsj": _run_lsj,
+}
+
+
+def run_join(algorithm: str, r: Relation, s: Relation, workers: int = 1, opts: dict | None = None,
+             dataset_echo: dict | None = None, repetition: int = 0) -> BenchReport:
+    """bench.py:292-318."""
+    if algorithm not in ALGORITHMS:
+        raise ValueError(f"unknown algorithm {algorithm!r}")
+    merged = dict(DEFAULT_OPTS)
+    if opts:
+        merged.update(opts)
+    result, br, runtime = ALGORITHMS[algorithm](r, s, workers, merged)
+    total = len(r) + len(s)
+    return BenchReport(algorithm=algorithm, dataset=dataset_echo or {"n_r": len(r), "n_s": len(s)},
+                       workers=workers, config=merged, runtime_s=runtime,
+                       throughput=total / runtime if runtime > 0 else 0.0, result_count=result.count,
+                       breakdown=br.as_dict(), repetition=repetition, checksum=result.checksum)

@@ -1,0 +1,130 @@
+"""Spline-keyed chained hash index on the GPU (reference learned_hash.py).
+
+Chains are keyed by partition_index(spline, key, table_len) and keep
+insertion order.  The build sorts (bucket, original index) pairs with a
+stable device radix sort; the probe (K5) evaluates the spline, finds the
+chain and scans it in one kernel, reducing to the checksum on device.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .data import Relation
+from .models import RadixSplineIndex
+from .util import as_key_tensor, exclusive_offsets, sort_pairs, to_device_u64, to_numpy_u64
+
+
+class SplineHashIndex:
+    """Bucket-chained hash table keyed by a scaled spline CDF prediction."""
+
+    def __init__(self, max_error: int = 32, radix_bits: int = 18, table_factor: float = 4.0):
+        if table_factor < 1.0:
+            raise ValueError("table_factor must be >= 1")
+        self.max_error = max_error
+        self.radix_bits = radix_bits
+        self.table_factor = float(table_factor)
+        self.n = 0
+
+    def get_params(self) -> dict:
+        return {"max_error": self.max_error, "radix_bits": self.radix_bits, "table_factor": self.table_factor}
+
+    def fit(self, relation: Relation, model: RadixSplineIndex | None = None) -> "SplineHashIndex":
+        """learned_hash.py:35-40: spline on the sorted build keys, then chains."""
+        if model is None:
+            sk, _ = sort_pairs(relation.keys, relation.payloads)
+            model = RadixSplineIndex(self.max_error, self.radix_bits).fit(sk)
+        table_len = max(1, int(round(self.table_factor * len(relation))))
+        return self._index_with(model, relation, table_len)
+
+    @classmethod
+    def from_model(cls, model, relation: Relation, table_len: int) -> "SplineHashIndex":
+        """learned_hash.py:42-53: index under an externally trained model."""
+        self = cls.__new__(cls)
+        self.max_error = getattr(model, "max_error", 0)
+        self.radix_bits = getattr(model, "radix_bits", 0)
+        self.table_factor = table_len / max(1, len(relation))
+        return self._index_with(model, relation, table_len)
+
+    def _index_with(self, model, relation: Relation, table_len: int) -> "SplineHashIndex":
+        self.model = model
+        self.n = n = len(relation)
+        self.table_len = P = int(table_len)
+        self.stride = (P // n) if n and P % n == 0 else 1
+        dev = relation.device
+        self.entries = torch.empty(2 * max(n, 1), dtype=torch.int64, device=dev)
+        self.starts = torch.zeros(P // self.stride + 1, dtype=torch.int32, device=dev)
+        if n == 0:
+            return self
+        lib = _lib.lib()
+        ws = _lib.workspace(lib.lj_spline_hash_build_workspace_bytes(n, P), dev)
+        c = model.c_struct()
+        _lib.check(lib.lj_spline_hash_build(ctypes.byref(c), _lib.ptr(relation.keys), _lib.ptr(relation.payloads),
+                                            n, P, _lib.ptr(self.entries), _lib.ptr(self.starts), _lib.ptr(ws),
+                                            ws.numel(), _lib.stream_ptr()), "spline_hash_build")
+        return self
+
+    def c_struct(self) -> _lib.LjSplineHash:
+        return _lib.LjSplineHash(self.model.c_struct(), self.n, self.table_len, self.stride,
+                                 _lib.ptr(self.entries), _lib.ptr(self.starts))
+
+    @property
+    def _keys(self) -> np.ndarray:
+        return to_numpy_u64(self.entries[0 : 2 * self.n : 2].contiguous())
+
+    @property
+    def _payloads(self) -> np.ndarray:
+        return to_numpy_u64(self.entries[1 : 2 * self.n : 2].contiguous())
+
+    def collision_fraction(self) -> float:
+        """learned_hash.py:68-79: inserts that landed in an occupied bucket."""
+        if self.n == 0:
+            return 0.0
+        st = self.starts.to(torch.int64)
+        occupied = int((st[1:] != st[:-1]).sum().item())
+        return (self.n - occupied) / self.n
+
+    def join_checksum(self, s_keys: torch.Tensor, s_payloads: torch.Tensor, out: torch.Tensor | None = None,
+                      accumulate: bool = False, stream=None) -> torch.Tensor:
+        """K5 -> device int64[4] {count, sum, xor, 0}."""
+        if out is None:
+            out = torch.zeros(4, dtype=torch.int64, device=s_keys.device)
+        c = self.c_struct()
+        _lib.check(_lib.lib().lj_spline_hash_probe(ctypes.byref(c), _lib.ptr(s_keys), _lib.ptr(s_payloads),
+                                                   s_keys.numel(), _lib.ptr(out), int(bool(accumulate)),
+                                                   _lib.stream_ptr(stream)), "spline_hash_probe")
+        return out
+
+    def probe_batch(self, keys):
+        """learned_hash.py:81-96 -> (payloads, source_index) device tensors;
+        per probe, matches in chain (insertion) order."""
+        k = as_key_tensor(keys)
+        n = k.numel()
+        if self.n == 0 or n == 0:
+            e = torch.empty(0, dtype=torch.int64, device=k.device)
+            return e, e.clone()
+        lib = _lib.lib()
+        c = self.c_struct()
+        counts = torch.empty(n, dtype=torch.int64, device=k.device)
+        _lib.check(lib.lj_spline_hash_count(ctypes.byref(c), _lib.ptr(k), n, _lib.ptr(counts), _lib.stream_ptr()),
+                   "spline_hash_count")
+        offsets, total = exclusive_offsets(counts)
+        pays = torch.empty(total, dtype=torch.int64, device=k.device)
+        src = torch.empty(total, dtype=torch.int64, device=k.device)
+        if total:
+            _lib.check(lib.lj_spline_hash_collect(ctypes.byref(c), _lib.ptr(k), n, _lib.ptr(offsets), _lib.ptr(pays),
+                                                  _lib.ptr(src), _lib.stream_ptr()), "spline_hash_collect")
+        return pays, src
+
+    def probe(self, key) -> np.ndarray:
+        pays, _ = self.probe_batch(np.asarray([key], dtype=np.uint64))
+        return to_numpy_u64(pays)
+
+
+def build_spline_hash(relation: Relation, max_error: int = 32, radix_bits: int = 18,
+                      table_factor: float = 4.0) -> SplineHashIndex:
+    return SplineHashIndex(max_error, radix_bits, table_factor).fit(relation)

@@ -1,0 +1,238 @@
+"""GPU parity: the CUDA path against the reference's golden vectors and the
+C oracle, through the C ABI.  Bit-exact for every integer output."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import rmi_from_fixture
+
+pytestmark = pytest.mark.gpu
+
+MASK = (1 << 64) - 1
+
+
+@pytest.fixture(scope="module")
+def lj():
+    import paper_2111_08824_b200 as lj
+
+    return lj
+
+
+def _np(t):
+    from paper_2111_08824_b200.util import to_numpy_u64
+
+    return to_numpy_u64(t)
+
+
+def _i64(t):
+    return t.cpu().numpy().astype(np.int64)
+
+
+def ref_rmi(lj, d, prefix=""):
+    return lj.RecursiveModelIndex.from_params(
+        d[prefix + "root"][0], d[prefix + "root"][1], int(d[prefix + "trained_len"]), d[prefix + "leaf_slope"],
+        d[prefix + "leaf_intercept"], d[prefix + "clamp_lo"], d[prefix + "clamp_hi"], d[prefix + "err_lo"],
+        d[prefix + "err_hi"])
+
+
+MODEL_SETS = ["unif63", "lognorm1e12", "clusters", "seq_h", "lognorm_ref", "dups", "linear", "tiny", "single",
+              "dbl_collide"]
+
+
+@pytest.mark.parametrize("name", MODEL_SETS)
+def test_rmi_eval_bitwise(golden, lj, name):
+    """L0: models.py:112-135 + partition_index on device == reference."""
+    d = golden("models")[name]
+    m = ref_rmi(lj, d)
+    pos, lo, hi = m.predict_many(d["probes"])
+    assert np.array_equal(_i64(pos), d["pos"])
+    assert np.array_equal(_i64(lo), d["lo"])
+    assert np.array_equal(_i64(hi), d["hi"])
+    assert np.array_equal(_i64(m.route_many(d["probes"])), d["route"])
+    for P in (1, 7, 4096):
+        assert np.array_equal(_i64(lj.partition_index(m, d["probes"], P)), d[f"part_{P}"])
+
+
+@pytest.mark.parametrize("name", MODEL_SETS)
+def test_spline_eval_bitwise(golden, lj, name):
+    d = golden("models")[name]
+    me, rb = int(d["sp_max_error"]), int(d["sp_radix_bits"])
+    sp = lj.RadixSplineIndex(me, rb).fit(d["keys"])
+    assert np.array_equal(sp.spline_keys, d["sp_keys"])
+    pos, lo, hi = sp.predict_many(d["probes"])
+    assert np.array_equal(_i64(pos), d["sp_pos"])
+    assert np.array_equal(_i64(lo), d["sp_lo"])
+    assert np.array_equal(_i64(hi), d["sp_hi"])
+    n = d["keys"].size
+    assert np.array_equal(_i64(lj.partition_index(sp, d["probes"], 4 * n)), d["sp_part_4n"])
+    assert np.array_equal(_i64(lj.partition_index(sp, d["probes"], 3)), d["sp_part_3"])
+
+
+@pytest.mark.parametrize("name", MODEL_SETS)
+def test_rmi_fit_on_device_is_sound(golden, lj, name):
+    """K10: bounds contain every true rank, predictions monotone, clamps
+    equal the reference's (they are integer segment bounds)."""
+    d = golden("models")[name]
+    keys = d["keys"]
+    m = lj.RecursiveModelIndex(int(d["fanout"])).fit(keys)
+    pos, lo, hi = (_i64(t) for t in m.predict_many(keys))
+    truth = np.searchsorted(keys, keys, side="left")
+    assert np.all((lo <= truth) & (truth <= hi))
+    assert np.all(np.diff(pos) >= 0)
+    if name != "dbl_collide":
+        assert np.array_equal(m.clamp_lo, d["clamp_lo"])
+        assert np.array_equal(m.clamp_hi, d["clamp_hi"])
+        np.testing.assert_allclose(m.leaf_slope, d["leaf_slope"], rtol=1e-6, atol=1e-12)
+
+
+def test_grmi_layout_search_and_join_bitwise(golden, lj):
+    """L0-L2 on every golden GRMI case, with the reference's own model:
+    identical gapped arrays, slots, per-probe search results and probe
+    counts, pairs, checksum and search_steps."""
+    for case, d in golden("grmi").items():
+        rel = lj.Relation(d["keys"], d["payloads"])
+        idx = lj.GappedRmiIndex(float(d["gap"]), int(d["fanout"])).fit(rel, model=ref_rmi(lj, d))
+        assert idx.slot_count == int(d["L"]), case
+        assert np.array_equal(idx.gkeys, d["gkeys"]), case
+        assert np.array_equal(idx.gpayloads, d["gpayloads"]), case
+        assert np.array_equal(idx.bitmap, d["bitmap"]), case
+        slots0 = idx.predict_slots(d["probes"])
+        assert np.array_equal(_i64(slots0), d["slots0"]), case
+        slot, probes = idx.search(slots0, d["probes"])
+        assert np.array_equal(_i64(slot), d["out_slot"]), case
+        assert np.array_equal(_i64(probes), d["out_probes"]), case
+        st = lj.LookupStats()
+        pays, src, found = idx.lookup_batch(d["probes"], st)
+        assert np.array_equal(_np(pays), d["pairs_r"]), case
+        assert np.array_equal(_i64(src), d["pairs_src"]), case
+        assert np.array_equal(found.cpu().numpy(), d["found"]), case
+        assert [st.search_steps, st.predictions, st.leaf_switches] == d["stats"].tolist(), case
+        s = lj.Relation(d["probes"], d["probe_payloads"])
+        w = idx.join_checksum(s.keys, s.payloads).cpu().tolist()
+        assert (w[0], w[1] & MASK, w[2] & MASK) == tuple(int(v) for v in d["checksum"]), case
+        assert w[3] == int(d["stats"][0]), case
+
+
+def test_grmi_zero_payloads_use_the_bitmap(lj):
+    """A real payload of 0 switches the kernel to bitmap occupancy."""
+    keys = np.array([5, 5, 5, 9, 20, 21, 40], np.uint64)
+    pays = np.array([0, 1, 2, 0, 4, 5, 0], np.uint64)
+    idx = lj.GappedRmiIndex(2.0, 2).fit(lj.Relation(keys, pays))
+    assert idx.payload_nonzero == 0
+    probes = np.array([5, 9, 40, 7, 21, 5], np.uint64)
+    pp = np.arange(10, 16, dtype=np.uint64)
+    w = idx.join_checksum(lj.Relation(probes, pp).keys, lj.Relation(probes, pp).payloads).cpu().tolist()
+    want = oracle.nlj_checksum(keys, pays, probes, pp)
+    assert (w[0], w[1] & MASK, w[2] & MASK) == want
+    assert sorted(idx.lookup_range(5).tolist()) == [0, 1, 2]
+
+
+def test_spline_hash_build_and_probe_bitwise(golden, lj):
+    for case, d in golden("spline_hash").items():
+        n = d["keys"].size
+        model = lj.RadixSplineIndex.from_params(d["sp_keys"], d["sp_ranks"], d["sp_radix_table"], int(d["sp_shift"]),
+                                                n, int(d["max_error"]), int(d["radix_bits"]))
+        rel = lj.Relation(d["keys"], d["payloads"])
+        idx = lj.SplineHashIndex(int(d["max_error"]), int(d["radix_bits"]), float(d["table_factor"])).fit(rel, model)
+        assert idx.table_len == int(d["table_len"]), case
+        assert np.array_equal(idx._keys, d["e_keys"]), case
+        assert np.array_equal(idx._payloads, d["e_payloads"]), case
+        assert idx.collision_fraction() == float(d["collision_fraction"]), case
+        pays, src = idx.probe_batch(d["probes"])
+        assert np.array_equal(_np(pays), d["pairs_r"]), case
+        assert np.array_equal(_i64(src), d["pairs_src"]), case
+        s = lj.Relation(d["probes"], d["probe_payloads"])
+        w = idx.join_checksum(s.keys, s.payloads).cpu().tolist()
+        assert (w[0], w[1] & MASK, w[2] & MASK) == tuple(int(v) for v in d["checksum"]), case
+        # own host fit picks the same spline
+        own = lj.SplineHashIndex(int(d["max_error"]), int(d["radix_bits"]), float(d["table_factor"])).fit(rel)
+        assert np.array_equal(own.model.spline_keys, d["sp_keys"]), case
+
+
+@pytest.mark.parametrize("algo", ["grmi-inlj", "buffered-grmi-inlj", "spline-hash-inlj"])
+@pytest.mark.parametrize("workers", [1, 4])
+def test_algorithms_registry_matches_reference(golden, lj, algo, workers):
+    """L2 through the drop-in boundary (bench.py:277-289): every c01-style
+    case's checksum equals the reference runner's; materialised pairs equal
+    the reference multiset."""
+    for case, d in golden("algos").items():
+        r = lj.Relation(d["r_keys"], d["r_payloads"])
+        s = lj.Relation(d["s_keys"], d["s_payloads"])
+        opts = dict(lj.DEFAULT_OPTS)
+        res, br, rt = lj.ALGORITHMS[algo](r, s, workers, opts)
+        assert res.checksum == tuple(int(v) for v in d["checksum"]), (case, algo)
+        assert br.lookup_stats.predictions == len(s)
+        opts["materialize"] = True
+        res2, _, _ = lj.ALGORITHMS[algo](r, s, workers, opts)
+        assert res2.checksum == res.checksum
+        want = oracle.nlj_checksum(d["r_keys"], d["r_payloads"], d["s_keys"], d["s_payloads"])
+        assert res2.checksum == want
+
+
+def test_config1_full_size_against_oracle(lj):
+    """C1 at full size (R 2^20, S 2^22): GPU checksum and search_steps equal
+    the oracle's on the same inputs and the same model."""
+    from paper_2111_08824_b200 import configs
+
+    inp = configs.config1()
+    idx = lj.GappedRmiIndex(2.0, 1024).fit(inp.r)
+    w = idx.join_checksum(inp.s.keys, inp.s.payloads).cpu().tolist()
+    rk, rp = inp.r.numpy()
+    sk, sp = inp.s.numpy()
+    om = oracle.Rmi(idx.rmi.root_slope, idx.rmi.root_intercept, idx.rmi.trained_len, idx.rmi.leaf_slope,
+                    idx.rmi.leaf_intercept, idx.rmi.clamp_lo, idx.rmi.clamp_hi, idx.rmi.err_lo, idx.rmi.err_hi)
+    og = oracle.grmi_build(rk, rp, 2.0, 1024, model=om)
+    assert np.array_equal(og.gkeys, idx.gkeys)
+    want = oracle.grmi_join(og, sk, sp)
+    assert (w[0], w[1] & MASK, w[2] & MASK, w[3]) == want
+    assert want[0] == int(round(0.9 * (1 << 22)))  # every hit matches exactly once
+    assert oracle.smj_checksum(rk, rp, sk, sp) == want[:3]
+
+
+def test_config2_reduced_against_oracle(lj):
+    from paper_2111_08824_b200 import configs
+
+    inp = configs.config2(scale=6)
+    res, br, _ = lj.ALGORITHMS["grmi-inlj"](inp.r, inp.s, 1, dict(lj.DEFAULT_OPTS, **inp.opts))
+    rk, rp = inp.r.numpy()
+    sk, sp = inp.s.numpy()
+    assert res.checksum == oracle.smj_checksum(rk, rp, sk, sp)
+    res_b, _, _ = lj.ALGORITHMS["buffered-grmi-inlj"](inp.r, inp.s, 1, dict(lj.DEFAULT_OPTS, **inp.opts))
+    assert res_b.checksum == res.checksum
+
+
+def test_edge_cases(lj):
+    empty = lj.Relation(np.empty(0, np.uint64), np.empty(0, np.uint64))
+    one = lj.make_relation(np.array([7], np.uint64), 1)
+    for algo in ("grmi-inlj", "buffered-grmi-inlj", "spline-hash-inlj"):
+        for r, s in ((empty, one), (one, empty), (one, one)):
+            res, _, _ = lj.ALGORITHMS[algo](r, s, 1, dict(lj.DEFAULT_OPTS))
+            assert res.checksum == oracle.nlj_checksum(*r.numpy(), *s.numpy()), algo
+    # keys at the top of the u64 range, all-duplicate build side
+    big = np.array([2**64 - 2, 2**64 - 3, 2**63, 2**63 + 1, 0, 1], np.uint64)
+    dup = np.full(50, 12345, np.uint64)
+    for keys in (big, dup):
+        r = lj.make_relation(keys, 3)
+        s = lj.make_relation(np.concatenate([keys, keys[:3], np.array([99], np.uint64)]), 4)
+        want = oracle.nlj_checksum(*r.numpy(), *s.numpy())
+        for algo in ("grmi-inlj", "buffered-grmi-inlj", "spline-hash-inlj"):
+            res, _, _ = lj.ALGORITHMS[algo](r, s, 2, dict(lj.DEFAULT_OPTS, gap_factor=2.5, rmi_fanout=3))
+            assert res.checksum == want, (algo, keys[:3])
+    with pytest.raises(ValueError):
+        lj.Relation(np.array([2**64 - 1], np.uint64), np.array([1], np.uint64))
+
+
+def test_linearity_over_s_slices(lj):
+    """Size-independent property: the checksum of S equals the combination
+    of the checksums of its two halves (counts and sums add, xors xor)."""
+    from paper_2111_08824_b200 import configs
+
+    inp = configs.config1(scale=2)
+    idx = lj.GappedRmiIndex(2.0, 256).fit(inp.r)
+    n = len(inp.s)
+    a = idx.join_checksum(inp.s.keys[: n // 3], inp.s.payloads[: n // 3]).cpu().tolist()
+    b = idx.join_checksum(inp.s.keys[n // 3:], inp.s.payloads[n // 3:]).cpu().tolist()
+    w = idx.join_checksum(inp.s.keys, inp.s.payloads).cpu().tolist()
+    assert w[0] == a[0] + b[0] and (w[1] - a[1] - b[1]) & MASK == 0 and w[2] == a[2] ^ b[2] and w[3] == a[3] + b[3]
