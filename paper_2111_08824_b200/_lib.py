@@ -90,6 +90,19 @@ SIGNATURES = {
     "lj_spline_hash_probe": (_int, [ctypes.POINTER(LjSplineHash), _P, _P, _i64, _P, _int, _P]),
     "lj_spline_hash_count": (_int, [ctypes.POINTER(LjSplineHash), _P, _i64, _P, _P]),
     "lj_spline_hash_collect": (_int, [ctypes.POINTER(LjSplineHash), _P, _i64, _P, _P, _P, _P]),
+    "lj_lsj_sample_workspace_bytes": (_size_t, [_i64]),
+    "lj_lsj_sample": (_int, [_P, _i64, _i64, _u64, _P, _P, _size_t, _P]),
+    "lj_lsj_partition_workspace_bytes": (_size_t, [_i64, _i64]),
+    "lj_lsj_partition": (_int, [ctypes.POINTER(LjRmi), _P, _P, _i64, _i64, _P, _P, _P, _size_t, _P]),
+    "lj_lsj_sort_workspace_bytes": (_size_t, [_i64, _i64]),
+    "lj_lsj_sort_buckets": (_int, [ctypes.POINTER(LjRmi), _P, _i64, _i64, _P, _P, _size_t, _P, _P]),
+    "lj_lsj_oversized_list_host": (_int, [_P, _i64, _i64, _P]),
+    "lj_lsj_sort_oversized_workspace_bytes": (_size_t, [_i64, _i64]),
+    "lj_lsj_sort_oversized": (_int, [ctypes.POINTER(LjRmi), _P, _i64, _i64, _P, _P, _P, _i64, _P, _P, _size_t,
+                                     _P, _P]),
+    "lj_lsj_sort_runs": (_int, [_P, _i64, _P, _P]),
+    "lj_lsj_join": (_int, [ctypes.POINTER(LjRmi), _P, _i64, _i64, _P, _P, _i64, _int, _P, _P, _P, _P, _P, _int,
+                           _P]),
 }
 
 _lib = None

@@ -181,4 +181,83 @@ def config2(scale: int = 0, device="cuda", seed: int = 0xC2, shard: int = 0) -> 
                   f"density 0.5, {leaves} leaves")
 
 
-CONFIGS = {"c1": config1, "c2": config2}
+def config3(scale: int = 1, device="cuda", seed: int = 0xC3, shard: int = 0, shards: int = 1) -> Inputs:
+    """C3: R = 2*10^8 unique keys from 64 normal clusters (centres uniform
+    in [0, 2^62), sigma 2^40; draws outside [0, 2^63) rejected); S = 2*10^9
+    keys drawn uniformly from R (counter sampler).  RadixSpline with 18 radix
+    bits, max error 32, table_factor 4.  ``shards``/``shard`` give rank
+    ``shard`` its contiguous 1/shards of S; ``scale`` divides both sides."""
+    nr, ns_total = 200_000_000 // scale, 2_000_000_000 // scale
+    lo_s = ns_total * shard // shards
+    ns = ns_total * (shard + 1) // shards - lo_s
+    centres = (uniform63(64, seed ^ 0x31, 0, device) >> 1).to(torch.float64)
+
+    def draw(c, o):
+        cl = ((_mix(c, seed ^ 0x32, o, device) >> 58) & 63)
+        v = centres[cl] + float(2**40) * normal(c, seed ^ 0x33, o, device)
+        ok = (v >= 0) & (v < float(2**63 - 1024))
+        return v[ok].to(torch.int64)
+
+    rk = distinct_first(draw, nr, device)
+    rp = fill_payloads(nr, seed ^ 0x34, device=device)
+    sk = _gather_uniform(rk, ns, seed ^ 0x35, lo_s)
+    s = Relation(sk, fill_payloads(ns, seed ^ 0x36, offset=lo_s, device=device), validate=False)
+    return Inputs("c3", Relation(rk, rp, validate=False), s,
+                  {"spline_error": 32, "radix_bits": 18, "table_factor": 4.0}, "spline-hash-inlj",
+                  f"RadixSpline learned-hash INLJ: R={nr} clustered-normal unique, S={ns} of {ns_total} "
+                  f"uniform from R, 18 radix bits, max error 32, P=4|R|")
+
+
+def config4(scale: int = 0, device="cuda", seed: int = 0xC4, shard: int = 0) -> Inputs:
+    """C4: R = 2^28 unique floor(2^40 * lognormal(0, 1.5)); S = 2^28 keys
+    R_sorted[Zipf(1.0) rank] (duplicates); LSJ with 4096 partitions and a
+    1% sample per relation (per-relation models, as the reference)."""
+    nr = ns = (1 << 28) >> scale
+
+    def draw(c, o):
+        v = torch.floor(float(2**40) * torch.exp(1.5 * normal(c, seed, o, device)))
+        return torch.clamp(v, 0, float(2**63 - 1024)).to(torch.int64)
+
+    rk = distinct_first(draw, nr, device)
+    rp = fill_payloads(nr, seed ^ 0x41, device=device)
+    srt = torch.sort(rk).values
+    sk = srt[zipf_ranks(ns, nr, 1.0, seed ^ 0x42 ^ (shard << 40), device)]
+    del srt
+    s = Relation(sk, fill_payloads(ns, seed ^ 0x43 ^ (shard << 40), device=device), validate=False)
+    return Inputs("c4", Relation(rk, rp, validate=False), s,
+                  {"fanout": 4096, "sample_rate": 0.01}, "lsj",
+                  f"LSJ: R={nr} lognormal(0,1.5)x2^40 unique, S={ns} Zipf(1.0) over R ranks, 4096 partitions, "
+                  f"1% sample models")
+
+
+def bijective63(i: torch.Tensor, seed: int) -> torch.Tensor:
+    """A bijection of [0, 2^63): odd multiplies, adds and xorshifts mod 2^63."""
+    m = MAX63
+    x = (i + (seed & m)) & m
+    for mul, sh in ((0x5851F42D4C957F2D, 29), (0x14057B7EF767814F, 31), (0x2545F4914F6CDD1D, 27)):
+        x = (x * mul) & m  # odd multiplier: a bijection mod 2^63 (int64 wraps mod 2^64)
+        x = x ^ (x >> sh)
+    return x
+
+
+def config5(scale: int = 0, device="cuda", seed: int = 0xC5, shard: int = 0, shards: int = 1) -> Inputs:
+    """C5: R = S = 2*10^9 (per all GPUs): R unique uniform keys by a
+    bijective 63-bit mix of the counter (no dedup needed), S = R[idx] with a
+    uniform counter draw; rank ``shard`` holds the contiguous 1/shards of
+    both relations.  LSJ with one shared model in the multi-GPU path."""
+    n_total = 2_000_000_000 >> scale
+    lo = n_total * shard // shards
+    n = n_total * (shard + 1) // shards - lo
+    idx = torch.arange(lo, lo + n, dtype=torch.int64, device=device)
+    rk = bijective63(idx, seed)
+    rp = fill_payloads(n, seed ^ 0x51, offset=lo, device=device)
+    j = _mix(n, seed ^ 0x52, lo, device)
+    sidx = ((j >> 1) & MAX63) % n_total  # uniform over all of R (every rank's)
+    sk = bijective63(sidx, seed)
+    sp = fill_payloads(n, seed ^ 0x53, offset=lo, device=device)
+    return Inputs("c5", Relation(rk, rp, validate=False), Relation(sk, sp, validate=False),
+                  {"fanout": 4096, "sample_rate": 0.01}, "lsj",
+                  f"LSJ: R=S={n} of {n_total} uniform unique (bijective mix) / uniform from R")
+
+
+CONFIGS = {"c1": config1, "c2": config2, "c3": config3, "c4": config4, "c5": config5}

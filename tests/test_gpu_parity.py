@@ -151,7 +151,7 @@ def test_spline_hash_build_and_probe_bitwise(golden, lj):
         assert np.array_equal(own.model.spline_keys, d["sp_keys"]), case
 
 
-@pytest.mark.parametrize("algo", ["grmi-inlj", "buffered-grmi-inlj", "spline-hash-inlj"])
+@pytest.mark.parametrize("algo", ["grmi-inlj", "buffered-grmi-inlj", "spline-hash-inlj", "lsj"])
 @pytest.mark.parametrize("workers", [1, 4])
 def test_algorithms_registry_matches_reference(golden, lj, algo, workers):
     """L2 through the drop-in boundary (bench.py:277-289): every c01-style
@@ -163,7 +163,8 @@ def test_algorithms_registry_matches_reference(golden, lj, algo, workers):
         opts = dict(lj.DEFAULT_OPTS)
         res, br, rt = lj.ALGORITHMS[algo](r, s, workers, opts)
         assert res.checksum == tuple(int(v) for v in d["checksum"]), (case, algo)
-        assert br.lookup_stats.predictions == len(s)
+        if algo != "lsj":
+            assert br.lookup_stats.predictions == len(s)
         opts["materialize"] = True
         res2, _, _ = lj.ALGORITHMS[algo](r, s, workers, opts)
         assert res2.checksum == res.checksum
@@ -236,3 +237,95 @@ def test_linearity_over_s_slices(lj):
     b = idx.join_checksum(inp.s.keys[n // 3:], inp.s.payloads[n // 3:]).cpu().tolist()
     w = idx.join_checksum(inp.s.keys, inp.s.payloads).cpu().tolist()
     assert w[0] == a[0] + b[0] and (w[1] - a[1] - b[1]) & MASK == 0 and w[2] == a[2] ^ b[2] and w[3] == a[3] + b[3]
+
+
+def test_lsj_matches_reference_with_reference_models(golden, lj):
+    """lsj.py:373-405 with the reference's own sample models: identical
+    checksum AND identical sort counters (comparator_count,
+    partitions_sorted); with the GPU's own sample models the checksum is
+    unchanged (model neutrality); materialised pairs equal the NLJ oracle."""
+    for case, d in golden("lsj").items():
+        r = lj.Relation(d["r_keys"], d["r_payloads"])
+        s = lj.Relation(d["s_keys"], d["s_payloads"])
+        cfg = lj.LsjConfig(workers=int(d["workers"]), fanout=int(d["fanout"]), sample_rate=float(d["sample_rate"]))
+        want = tuple(int(v) for v in d["checksum"])
+        res, br = lj.lsj_join(r, s, cfg, models=(ref_rmi(lj, d, "mr_"), ref_rmi(lj, d, "ms_")))
+        assert res.checksum == want, case
+        assert (br.sort_stats.comparator_count, br.sort_stats.partitions_sorted) == tuple(
+            int(v) for v in d["sort_stats"]), case
+        own, _ = lj.lsj_join(r, s, cfg)
+        assert own.checksum == want, case
+        mat, _ = lj.lsj_join(r, s, cfg, materialize=True)
+        assert mat.checksum == want, case
+        assert mat.count == want[0]
+
+
+def test_lsj_sort_phase_sorted_and_pairs_kept(lj):
+    """Global sortedness after the sort phase, pairs still attached
+    (tests/test_lsj.py:143-155, 225-232 analogues) on skewed duplicated keys."""
+    from paper_2111_08824_b200.lsj import sort_relation
+
+    rng = np.random.default_rng(5)
+    base = np.unique(np.floor(2.0**40 * rng.lognormal(0, 1.5, 60000)).astype(np.uint64))
+    w = 1.0 / np.arange(1, base.size + 1)
+    keys = base[rng.choice(base.size, 200000, p=w / w.sum())]
+    pays = np.arange(1, keys.size + 1, dtype=np.uint64)
+    r = lj.Relation(keys, pays)
+    m = lj.RecursiveModelIndex(100).fit(np.sort(keys[::10]))
+    srt = sort_relation(r.keys, r.payloads, m, 64)
+    k = _np(srt.keys.contiguous())
+    p = _np(srt.payloads.contiguous())
+    assert np.all(k[:-1] <= k[1:])
+    assert sorted(zip(k.tolist(), p.tolist())) == sorted(zip(keys.tolist(), pays.tolist()))
+    bb = srt.bucket_bounds.cpu().numpy()
+    part = _i64(lj.partition_index(m, srt.keys.contiguous(), 64))
+    assert np.array_equal(np.bincount(part, minlength=64), np.diff(bb))
+
+
+def test_lsj_edge_cases(lj):
+    empty = lj.Relation(np.empty(0, np.uint64), np.empty(0, np.uint64))
+    one = lj.make_relation(np.array([7], np.uint64), 1)
+    res, _ = lj.lsj_join(empty, one)
+    assert res.count == 0
+    res, _ = lj.lsj_join(one, one)
+    assert res.checksum == oracle.nlj_checksum(*one.numpy(), *one.numpy())
+    # duplicate products 2 x 3 = 6 (tests/test_lsj.py:178-182)
+    r = lj.make_relation(np.array([7, 7, 9], np.uint64), 1)
+    s = lj.make_relation(np.array([7, 7, 7, 8], np.uint64), 2)
+    res, _ = lj.lsj_join(r, s, lj.LsjConfig(fanout=50, sample_rate=1.0))
+    assert res.count == 6
+    # disjoint ranges
+    r = lj.make_relation(np.arange(0, 100, dtype=np.uint64), 1)
+    s = lj.make_relation(np.arange(1000, 1100, dtype=np.uint64), 2)
+    assert lj.lsj_join(r, s, lj.LsjConfig(fanout=50, sample_rate=1.0))[0].count == 0
+    # one repeated key larger than shared memory on both sides of the join
+    r = lj.make_relation(np.concatenate([np.full(10000, 5, np.uint64), np.arange(10, 20000, dtype=np.uint64)]), 1)
+    s = lj.make_relation(np.concatenate([np.full(30000, 5, np.uint64), np.arange(0, 40000, 3, dtype=np.uint64)]), 2)
+    res, _ = lj.lsj_join(r, s, lj.LsjConfig(fanout=8, sample_rate=0.05))
+    assert res.checksum == oracle.smj_checksum(*r.numpy(), *s.numpy())
+    with pytest.raises(lj.ModelMismatchError):
+        from paper_2111_08824_b200.lsj import chunked_join, sort_relation
+
+        m1 = lj.RecursiveModelIndex(2).fit(np.arange(100, dtype=np.uint64))
+        m2 = lj.RecursiveModelIndex(2).fit(np.arange(100, dtype=np.uint64))
+        a = sort_relation(r.keys, r.payloads, m1, 8)
+        chunked_join(a, a, m2, 8)
+
+
+@pytest.mark.parametrize("cfg", ["c4", "c5"])
+def test_lsj_configs_reduced_against_oracle(lj, cfg):
+    from paper_2111_08824_b200 import configs
+
+    inp = configs.CONFIGS[cfg](scale=8)
+    res, br, _ = lj.ALGORITHMS["lsj"](inp.r, inp.s, 1, dict(lj.DEFAULT_OPTS, **inp.opts))
+    assert res.checksum == oracle.smj_checksum(*inp.r.numpy(), *inp.s.numpy())
+    assert br.sort_stats.partitions_sorted > 0
+
+
+def test_config3_reduced_against_oracle(lj):
+    from paper_2111_08824_b200 import configs
+
+    inp = configs.config3(scale=64)
+    res, _, _ = lj.ALGORITHMS["spline-hash-inlj"](inp.r, inp.s, 1, dict(lj.DEFAULT_OPTS, **inp.opts))
+    assert res.checksum == oracle.smj_checksum(*inp.r.numpy(), *inp.s.numpy())
+    assert res.count == len(inp.s)  # every probe is an R key, R unique
