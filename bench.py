@@ -113,7 +113,34 @@ def build_index(inp):
         return lj.GappedRmiIndex(o["gap_factor"], o["rmi_fanout"]).fit(inp.r)
     if inp.algorithm == "spline-hash-inlj":
         return lj.SplineHashIndex(o["spline_error"], o["radix_bits"], o["table_factor"]).fit(inp.r)
-    raise ValueError(inp.algorithm)
+    return None  # lsj builds nothing ahead of time: it is timed end to end
+
+
+def make_step(inp, index, variant="buffered"):
+    """-> (step(out), kernel_name, algorithmic bytes of one step).  A step
+    is one pass of the hot path over the whole S (INLJ, index prebuilt as
+    in the reference) or the whole LSJ (sample, fit, partition, sort, join)."""
+    import paper_2111_08824_b200 as lj
+
+    n_r, n_s = len(inp.r), len(inp.s)
+    if index is not None:
+        keys, pays = inp.s.keys, inp.s.payloads
+        if "grmi" in inp.algorithm and variant == "buffered":
+            scratch = index.bucket_scratch(n_s)
+            return ((lambda out: index.join_checksum_buffered(keys, pays, out=out, scratch=scratch)),
+                    "k_bin_hist+k_bin_scatter+k_grmi_probe<AosIn> (Request-Buffer analogue)",
+                    ALGO_BYTES[inp.algorithm] * n_s)
+        name = "k_grmi_probe" if "grmi" in inp.algorithm else "k_hash_probe"
+        return (lambda out: index.join_checksum(keys, pays, out=out)), name, ALGO_BYTES[inp.algorithm] * n_s
+    o = dict(lj.DEFAULT_OPTS, **inp.opts)
+    cfg = lj.LsjConfig(workers=1, fanout=o["fanout"], sample_rate=o["sample_rate"], seed=o["seed"])
+
+    def step(out):
+        res, _ = lj.lsj_join(inp.r, inp.s, cfg)
+        out.copy_(res._words)
+        return out
+
+    return step, "lsj pipeline (K10,K6,K7,K8,K9)", ALGO_BYTES["lsj"] * (n_r + n_s)
 
 
 # ---------------------------------------------------------------- CPU arms
@@ -121,14 +148,39 @@ def build_index(inp):
 
 def cpu_inlj(inp, target_s: float = 8.0, threads: int = 0):
     """Oracle (C restatement of the reference path, OpenMP) on a bounded
-    sample of S, extrapolated to the whole S.  Returns (value, info)."""
+    sample, extrapolated to the whole workload.  Returns (value, info, rerun)."""
     import numpy as np
 
     import oracle
 
     o = inp.opts
     rk, rp = inp.r.numpy()
-    n_s = len(inp.s)
+    n_r, n_s = len(inp.r), len(inp.s)
+    cores = threads or oracle.num_threads()
+    if inp.algorithm == "lsj":
+        # LSJ is timed end to end on prefixes of R and S (all phases), then
+        # scaled linearly in |R|+|S| (optimistic for the CPU: the sort is
+        # n log n)
+        sample = min(n_r, 1 << 20)
+        while True:
+            sk = inp.s.keys[:sample].cpu().numpy().view(np.uint64)
+            sp = inp.s.payloads[:sample].cpu().numpy().view(np.uint64)
+            rks, rps = rk[:sample], rp[:sample]
+            run = lambda a, b, rks=rks, rps=rps: oracle.lsj_join(rks, rps, a, b, workers=1,
+                                                                  fanout=o.get("fanout", 4096),
+                                                                  sample_rate=o.get("sample_rate", 0.01))
+            t0 = time.perf_counter()
+            run(sk, sp)
+            dt = time.perf_counter() - t0
+            if dt >= target_s / 4 or sample >= min(n_r, n_s):
+                break
+            sample = min(n_r, n_s, sample * 4)
+        scale = (n_r + n_s) / (2 * sample)
+        value = (n_r + n_s) / (dt * scale)
+        info = {"value": value, "unit": "tuples/s", "cores": 1, "kind": "port",
+                "sample": f"LSJ over the first {sample} tuples of R and of S ({dt:.2f} s, single thread), "
+                          f"time scaled x{scale:.1f} linearly to |R|+|S|"}
+        return value, info, (sk, sp, run)
     if inp.algorithm in ("grmi-inlj", "buffered-grmi-inlj"):
         idx = oracle.grmi_build(rk, rp, o["gap_factor"], o["rmi_fanout"])
         run = lambda k, p: oracle.grmi_join(idx, k, p, threads)
@@ -147,8 +199,7 @@ def cpu_inlj(inp, target_s: float = 8.0, threads: int = 0):
             break
         sample = min(n_s, sample * 4)
     t_full = dt * n_s / sample
-    value = (len(inp.r) + n_s) / t_full
-    cores = threads or oracle.num_threads()
+    value = (n_r + n_s) / t_full
     info = {"value": value, "unit": "tuples/s", "cores": cores, "kind": "port",
             "sample": f"first {sample} of {n_s} S probes against the full R index ({dt:.2f} s), "
                       f"time extrapolated x{n_s / sample:.1f}; index build untimed as in the reference"}
@@ -166,10 +217,11 @@ def run_reference_arm(args):
     value, info, (sk, sp, run) = cpu_inlj(inp)
     steps = []
     n_s = len(inp.s)
+    scale = (n_s / sk.size) if inp.algorithm != "lsj" else (len(inp.r) + n_s) / (2 * sk.size)
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
         run(sk, sp)
-        dt = (time.perf_counter() - t0) * n_s / sk.size
+        dt = (time.perf_counter() - t0) * scale
         if i >= args.warmup:
             steps.append(dt)
     t = statistics.median(steps)
@@ -185,6 +237,7 @@ def run_reference_arm(args):
 
 def _config_block(args, inp):
     return {"workload": f"{args.config}: {inp.description}", "algorithm": inp.algorithm,
+            "variant": getattr(args, "variant", None) if "grmi" in inp.algorithm else None,
             "n_r": len(inp.r), "n_s": len(inp.s), "l2": "inputs larger than L2 and L2 flushed between steps",
             "parallelism": f"inlj-replicated-R x{args.gpus}"}
 
@@ -203,13 +256,13 @@ def run_b200(args):
     inp = make_inputs(args.config, shard=rank)
     index = build_index(inp)
     dev = torch.device("cuda", local)
-    keys, pays = inp.s.keys, inp.s.payloads
+    run_step, kname, alg_bytes = make_step(inp, index, args.variant)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     out = torch.zeros(4, dtype=torch.int64, device=dev)
     xors = torch.zeros(world, dtype=torch.int64, device=dev)
 
     def step():
-        index.join_checksum(keys, pays, out=out)
+        run_step(out)
         if world > 1:
             dist.all_gather_into_tensor(xors, out[2:3].contiguous())
             dist.all_reduce(out, op=dist.ReduceOp.SUM)  # count, sum, steps (wrap mod 2^64)
@@ -250,20 +303,19 @@ def run_b200(args):
     for i in range(args.steps):
         flush.zero_()
         kev[i][0].record()
-        index.join_checksum(keys, pays, out=out)
+        run_step(out)
         kev[i][1].record()
     torch.cuda.synchronize()
     k_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
     peak, peak_kind = _peaks()
-    alg_bytes = ALGO_BYTES[inp.algorithm] * n_s
     achieved = alg_bytes / (k_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": _ncu_traffic(args.config), "kernel": "k_grmi_probe" if "grmi" in inp.algorithm
-                else "k_hash_probe", "kernel_ms": k_ms, "peak_kind": peak_kind,
-                "algorithmic_bytes": f"{ALGO_BYTES[inp.algorithm]} B/probe x {n_s} probes"}
+                "traffic": _ncu_traffic(args.config), "kernel": kname, "kernel_ms": k_ms, "peak_kind": peak_kind,
+                "algorithmic_bytes": (f"{ALGO_BYTES[inp.algorithm]} B/probe x {n_s} probes" if index is not None
+                                      else f"80 B/tuple x {n_r + n_s} tuples")}
 
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and index is not None:
         e2e = _e2e(args, inp, index, world)
     line = None
     if rank == 0:
@@ -292,6 +344,7 @@ def _e2e(args, inp, index, world):
 
     import paper_2111_08824_b200 as lj
 
+    scratch = index.bucket_scratch(len(inp.s)) if "grmi" in inp.algorithm else None
     hk = inp.s.keys.cpu().pin_memory()
     hp = inp.s.payloads.cpu().pin_memory()
     steps = max(1, min(args.steps, 3))
@@ -300,7 +353,11 @@ def _e2e(args, inp, index, world):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         s = lj.Relation(hk.to("cuda", non_blocking=True), hp.to("cuda", non_blocking=True), validate=True)
-        res = lj.JoinResult(words=index.join_checksum(s.keys, s.payloads))
+        if "grmi" in inp.algorithm and args.variant == "buffered":
+            words = index.join_checksum_buffered(s.keys, s.payloads, scratch=scratch)
+        else:
+            words = index.join_checksum(s.keys, s.payloads)
+        res = lj.JoinResult(words=words)
         _ = res.checksum
         dt = time.perf_counter() - t0
         del s
@@ -328,6 +385,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2")
+    ap.add_argument("--variant", default="buffered", choices=["buffered", "direct"],
+                    help="GRMI INLJ: group S by leaf on device first (Request-Buffer analogue) or probe directly")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -90,6 +90,15 @@ typedef struct LjSpline {
     const uint64_t *keys;   /* [K] spline keys */
     const double *ranks;    /* [K] spline ranks as float64 (models.py:228) */
     const uint32_t *radix;  /* [2^radix_bits + 1] radix table */
+    /* Optional exact search accelerator (NULL = plain bounded binary
+     * search, models.py:263-282): for radix bucket p, aux[p] = (offset << 8)
+     * | bits; when bits > 0, sub[offset + q] is the first spline point whose
+     * next `bits` key bits (below the radix prefix) are >= q, q in
+     * [0, 2^bits].  The first spline key >= k inside [radix[p], radix[p+1])
+     * is then searched in [sub[offset+q], sub[offset+q+1]) -- the same
+     * index by construction (built by lj_spline_aux_host). */
+    const uint64_t *aux;    /* [2^radix_bits] */
+    const uint32_t *sub;
 } LjSpline;
 
 /* Spline-keyed chained hash view (learned_hash.py:17-101). */
@@ -173,9 +182,17 @@ int lj_grmi_collect(const LjGrmi *idx, const uint64_t *keys, int64_t nk, const i
 /* buffers.py:73-150 analogue: reorder S by RMI leaf (stable counting sort)
  * so that K1 walks the index leaf by leaf.  hist needs m+1 words of
  * device scratch inside ws. */
+/* Bins are groups of consecutive leaves (<= 8192 groups, root model only);
+ * counting uses shared-memory-privatised histograms (no per-tuple global
+ * atomics).  pairs_out[2nk] interleaved {key, payload} grouped by bin,
+ * starts_out[bins+1].  Order inside a bin is unspecified. */
+int lj_leaf_bucket_bins(int64_t m);
 size_t lj_leaf_bucket_workspace_bytes(int64_t nk, int64_t m);
 int lj_leaf_bucket(const LjRmi *model, const uint64_t *keys, const uint64_t *pay, int64_t nk,
-                   uint64_t *keys_out, uint64_t *pay_out, void *ws, size_t ws_bytes, void *stream);
+                   uint64_t *pairs_out, int64_t *starts_out, void *ws, size_t ws_bytes, void *stream);
+/* K1 over interleaved {key, payload} probe records (e.g. bucketed S). */
+int lj_grmi_probe_pairs(const LjGrmi *idx, const uint64_t *s_pairs, int64_t nk, uint64_t *out, int accumulate,
+                        void *stream);
 
 /* ------------------------------------------------- RadixSpline (K5) */
 /* models.py:171-219 greedy-corridor fit on HOST sorted keys (sequential by
@@ -183,6 +200,11 @@ int lj_leaf_bucket(const LjRmi *model, const uint64_t *keys, const uint64_t *pay
 int lj_spline_fit_host(const uint64_t *sorted_keys_host, int64_t n, int64_t max_error,
                        int64_t radix_bits, uint64_t *keys_out_host, int64_t *ranks_out_host,
                        int64_t *radix_out_host, int64_t *npts_out, uint64_t *shift_out);
+/* Build the LjSpline.aux/sub accelerator on the host: every radix bucket
+ * holding more than 8 spline points gets ceil(log2(count)) + 1 extra key
+ * bits.  Call with sub_host = NULL to get the required sub length. */
+int lj_spline_aux_host(const uint64_t *keys_host, int64_t npts, const int64_t *radix_host, int64_t radix_bits,
+                       uint64_t shift, uint64_t *aux_host, uint32_t *sub_host, int64_t *sub_len);
 int lj_spline_predict(const LjSpline *model, const uint64_t *keys, int64_t nk, int64_t *pos,
                       int64_t *lo, int64_t *hi, void *stream);
 int lj_spline_partition_index(const LjSpline *model, const uint64_t *keys, int64_t nk, int64_t P,

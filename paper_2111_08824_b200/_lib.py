@@ -50,7 +50,8 @@ class LjGrmi(ctypes.Structure):
 
 class LjSpline(ctypes.Structure):
     _fields_ = [("npts", _i64), ("n", _i64), ("max_error", _i64), ("radix_bits", _i64), ("shift", _u64),
-                ("keys", _c_void_p), ("ranks", _c_void_p), ("radix", _c_void_p)]
+                ("keys", _c_void_p), ("ranks", _c_void_p), ("radix", _c_void_p), ("aux", _c_void_p),
+                ("sub", _c_void_p)]
 
 
 class LjSplineHash(ctypes.Structure):
@@ -80,9 +81,12 @@ SIGNATURES = {
     "lj_grmi_probe": (_int, [ctypes.POINTER(LjGrmi), _P, _P, _i64, _P, _int, _P]),
     "lj_grmi_count": (_int, [ctypes.POINTER(LjGrmi), _P, _P, _i64, _P, _P, _P, _P]),
     "lj_grmi_collect": (_int, [ctypes.POINTER(LjGrmi), _P, _i64, _P, _P, _P, _P, _P]),
+    "lj_leaf_bucket_bins": (_int, [_i64]),
     "lj_leaf_bucket_workspace_bytes": (_size_t, [_i64, _i64]),
     "lj_leaf_bucket": (_int, [ctypes.POINTER(LjRmi), _P, _P, _i64, _P, _P, _P, _size_t, _P]),
+    "lj_grmi_probe_pairs": (_int, [ctypes.POINTER(LjGrmi), _P, _i64, _P, _int, _P]),
     "lj_spline_fit_host": (_int, [_P, _i64, _i64, _i64, _P, _P, _P, _P, _P]),
+    "lj_spline_aux_host": (_int, [_P, _i64, _P, _i64, _u64, _P, _P, _P]),
     "lj_spline_predict": (_int, [ctypes.POINTER(LjSpline), _P, _i64, _P, _P, _P, _P]),
     "lj_spline_partition_index": (_int, [ctypes.POINTER(LjSpline), _P, _i64, _i64, _P, _P]),
     "lj_spline_hash_build_workspace_bytes": (_size_t, [_i64, _i64]),

@@ -83,8 +83,13 @@ def shuffle(t: torch.Tensor, seed: int) -> torch.Tensor:
 
 def zipf_ranks(n: int, N: int, s: float, seed: int, device="cuda") -> torch.Tensor:
     """n ranks in [0, N) with P(k) proportional to (k+1)^-s (exact inverse CDF)."""
-    w = torch.arange(1, N + 1, dtype=torch.float64, device=device).pow(-s)
-    cdf = torch.cumsum(w, 0)
+    # the cumulative weights are summed sequentially on the host: a device
+    # scan's float rounding order is not fixed run to run, which would move
+    # a few inverse-CDF boundaries and make the inputs irreproducible
+    import numpy as np
+
+    w = np.arange(1, N + 1, dtype=np.float64) ** (-s)
+    cdf = torch.from_numpy(np.cumsum(w)).to(device)
     u = _unit(n, seed, 0, device) * cdf[-1]
     r = torch.searchsorted(cdf, u, right=False)
     return torch.clamp(r, max=N - 1)

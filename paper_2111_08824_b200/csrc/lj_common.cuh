@@ -155,10 +155,12 @@ struct SplineDev {
     const u64 *keys;
     const double *ranks;
     const u32 *radix;
+    const u64 *aux;
+    const u32 *sub;
     __host__ SplineDev() {}
     __host__ explicit SplineDev(const LjSpline &s)
         : K(s.npts), n(s.n), max_error(s.max_error), radix_bits(s.radix_bits), shift(s.shift),
-          keys(s.keys), ranks(s.ranks), radix(s.radix) {}
+          keys(s.keys), ranks(s.ranks), radix(s.radix), aux(s.aux), sub(s.sub) {}
 
     // models.py:221-248 + _bounded_first_geq :263-282
     __device__ __forceinline__ i64 pos(u64 k) const {
@@ -175,7 +177,20 @@ struct SplineDev {
             if (prefix > rmax) prefix = rmax;
             i64 a = prefix < 0 ? prefix + len : prefix;
             i64 b = prefix + 1 < 0 ? prefix + 1 + len : prefix + 1;
-            i64 lo = (i64)__ldg(radix + (a < 0 ? 0 : a)), hi = (i64)__ldg(radix + (b < 0 ? 0 : b));
+            i64 lo, hi;
+            const u64 raw = shift >= 64 ? 0 : (k >> shift);
+            u64 ax = 0;
+            if (aux && raw <= (u64)rmax) ax = ldg(aux + raw);  // unclamped prefix: sub-table is exact
+            if (ax & 0xFF) {
+                const int bits = (int)(ax & 0xFF);
+                const u64 q = (k >> (shift - (u64)bits)) & ((1ULL << bits) - 1ULL);
+                const u32 *s = sub + (ax >> 8) + q;
+                lo = (i64)__ldg(s);
+                hi = (i64)__ldg(s + 1);
+            } else {
+                lo = (i64)__ldg(radix + (a < 0 ? 0 : a));
+                hi = (i64)__ldg(radix + (b < 0 ? 0 : b));
+            }
             if (hi < lo) hi = lo;
             if (hi > K) hi = K;
             while (lo < hi) {

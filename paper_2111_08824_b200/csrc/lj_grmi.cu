@@ -10,6 +10,7 @@
 #include <cub/cub.cuh>
 
 #include "lj_common.cuh"
+#include "lj_part.cuh"
 
 namespace lj {
 
@@ -129,13 +130,30 @@ __global__ void k_grmi_fill(const u32 *bitmap, const i64 *f, const i64 *cm, i64 
 // (:86-160), equal-run scan and real-entry gather (:163-203), reduced to
 // the checksum of t = R.payload + S.payload.  One lane per probe; the S
 // stream is read once with evict-first loads.
-template <int NT>
-__global__ void __launch_bounds__(NT) k_grmi_probe(GrmiDev g, const u64 *__restrict__ skeys,
-                                                   const u64 *__restrict__ spay, i64 nk, u64 *out) {
+// S as two columns (a Relation) or as interleaved records (bucketed S)
+struct SoaIn {
+    const u64 *__restrict__ keys;
+    const u64 *__restrict__ pay;
+    __device__ __forceinline__ void get(i64 t, u64 &k, u64 &p) const {
+        k = ld_stream(keys + t);
+        p = ld_stream(pay + t);
+    }
+};
+struct AosIn {
+    const ulonglong2 *__restrict__ rec;
+    __device__ __forceinline__ void get(i64 t, u64 &k, u64 &p) const {
+        ulonglong2 e = __ldcs(rec + t);
+        k = e.x;
+        p = e.y;
+    }
+};
+
+template <int NT, class In>
+__global__ void __launch_bounds__(NT) k_grmi_probe(GrmiDev g, In in, i64 nk, u64 *out) {
     u64 cnt = 0, sum = 0, x = 0, steps = 0;
     for (i64 t = blockIdx.x * (i64)NT + threadIdx.x; t < nk; t += (i64)gridDim.x * NT) {
-        u64 k = ld_stream(skeys + t);
-        u64 ps = ld_stream(spay + t);
+        u64 k, ps;
+        in.get(t, k, ps);
         i64 probes;
         i64 s = g.search(g.predict_slot(k), k, probes);
         steps += (u64)probes;
@@ -149,6 +167,155 @@ __global__ void __launch_bounds__(NT) k_grmi_probe(GrmiDev g, const u64 *__restr
             ++cnt;
             sum += v;
             x ^= v;
+        }
+    }
+    reduce_checksum(cnt, sum, x, steps, out);
+}
+
+// K1 v2: the same per-probe semantics as k_grmi_probe, restructured so a
+// warp never waits for its slowest search.  Every lane runs the reference's
+// search (gapped.py:86-160) as a state machine that issues exactly ONE
+// dependent load per loop iteration (leaf record, or one gapped slot); a
+// lane whose probe finishes pops the next probe from a per-warp queue in
+// shared memory, which the warp refills with coalesced, evict-first loads of
+// S.  Work per warp therefore tracks the MEAN search length, not the max,
+// and every iteration keeps 32 independent loads in flight per warp.
+enum : int { PH_IDLE = 0, PH_LEAF, PH_FIRST, PH_RIGHT, PH_LEFT, PH_BIN, PH_VERIFY, PH_WL, PH_SCAN };
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_grmi_probe_sm(GrmiDev g, const u64 *__restrict__ skeys,
+                                                      const u64 *__restrict__ spay, i64 nk, u64 *out) {
+    constexpr int QN = 64;  // probes queued per warp
+    __shared__ ulonglong2 q[NT / 32][QN];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const i64 L = g.L;
+    i64 next = ((i64)blockIdx.x * (NT / 32) + w) * 32;
+    const i64 wstride = (i64)gridDim.x * NT;
+    unsigned qh = 0, qt = 0;
+    int ph = PH_IDLE;
+    u64 k = 0, ps = 0;
+    i64 start = 0, step = 0, lo = 0, hi = 0, cur = 0;  // lo doubles as the reference's `prev`
+    unsigned probes = 0;
+    u64 cnt = 0, sum = 0, x = 0, steps = 0;
+    for (;;) {
+        if (qt - qh <= (unsigned)(QN - 32) && next < nk) {  // warp-uniform refill
+            i64 i = next + lane;
+            if (i < nk) q[w][(qt + lane) & (QN - 1)] = make_ulonglong2(ld_stream(skeys + i), ld_stream(spay + i));
+            qt += (unsigned)min((i64)32, nk - next);
+            next += wstride;
+            __syncwarp();
+        }
+        const unsigned idle = __ballot_sync(0xffffffffu, ph == PH_IDLE);
+        const unsigned avail = qt - qh;
+        if (ph == PH_IDLE) {
+            unsigned r = __popc(idle & lt);
+            if (r < avail) {
+                ulonglong2 e = q[w][(qh + r) & (QN - 1)];
+                k = e.x;
+                ps = e.y;
+                ph = PH_LEAF;
+            }
+        }
+        qh += min((unsigned)__popc(idle), avail);
+        __syncwarp();
+        if (__ballot_sync(0xffffffffu, ph != PH_IDLE) == 0 && qh == qt && next >= nk) break;
+        if (ph == PH_LEAF) {
+            // models.py:112-124 + gapped.py:258-261 (one leaf-record load)
+            double xf = u64_to_f64(k);
+            LjLeaf lf = load_leaf(g.model.leaves, g.model.route(xf));
+            start = grmi_slot_of_pos(rmi_leaf_pos(lf, xf), g.n, L);
+            cur = start;
+            ph = PH_FIRST;
+            continue;
+        }
+        if (ph == PH_IDLE) continue;
+        const ulonglong2 e = ldg2(g.slots + 2 * cur);
+        bool found = false, bsetup = false;
+        switch (ph) {
+            case PH_FIRST:
+                probes = 1;
+                if (e.x == k) {
+                    found = true;
+                } else if (e.x < k) {
+                    lo = start;  // prev
+                    step = 1;
+                    if (start + 1 >= L) { lo = start + 1; hi = L; bsetup = true; }
+                    else { cur = start + 1; ph = PH_RIGHT; }
+                } else {
+                    lo = start;  // prev
+                    step = 1;
+                    if (start - 1 < 0) { lo = 0; hi = start; bsetup = true; }
+                    else { cur = start - 1; ph = PH_LEFT; }
+                }
+                break;
+            case PH_RIGHT:
+                ++probes;
+                if (e.x < k) {
+                    lo = cur;
+                    step <<= 1;
+                    if (start + step >= L) { lo = lo + 1; hi = L; bsetup = true; }
+                    else cur = start + step;
+                } else if (e.x == k) {
+                    found = true;
+                } else {
+                    lo = lo + 1;
+                    hi = cur;
+                    bsetup = true;
+                }
+                break;
+            case PH_LEFT:
+                ++probes;
+                if (e.x > k) {
+                    lo = cur;
+                    step <<= 1;
+                    if (start - step < 0) { hi = lo; lo = 0; bsetup = true; }
+                    else cur = start - step;
+                } else if (e.x == k) {
+                    found = true;
+                } else {
+                    hi = lo;
+                    lo = cur + 1;
+                    bsetup = true;
+                }
+                break;
+            case PH_BIN:
+                ++probes;
+                if (e.x < k) lo = cur + 1; else hi = cur;
+                bsetup = true;
+                break;
+            case PH_VERIFY:
+                ++probes;
+                if (e.x == k) found = true;
+                else { steps += probes; ph = PH_IDLE; }
+                break;
+            case PH_WL:  // walk to the leftmost slot of the equal run
+                if (e.x == k && cur > 0) --cur;
+                else { cur = e.x == k ? cur : cur + 1; ph = PH_SCAN; }
+                break;
+            case PH_SCAN:  // gather the real entries of the run
+                if (e.x != k) {
+                    ph = PH_IDLE;
+                } else {
+                    if (g.real(cur, e.y)) {
+                        u64 v = e.y + ps;
+                        ++cnt;
+                        sum += v;
+                        x ^= v;
+                    }
+                    if (++cur >= L) ph = PH_IDLE;
+                }
+                break;
+        }
+        if (bsetup) {
+            if (lo < hi) { cur = (lo + hi) >> 1; ph = PH_BIN; }
+            else if (lo < L) { cur = lo; ph = PH_VERIFY; }
+            else { steps += probes; ph = PH_IDLE; }
+        }
+        if (found) {
+            steps += probes;
+            if (cur > 0) { --cur; ph = PH_WL; }
+            else ph = PH_SCAN;
         }
     }
     reduce_checksum(cnt, sum, x, steps, out);
@@ -214,19 +381,23 @@ __global__ void k_grmi_collect(GrmiDev g, const u64 *keys, i64 nk, const i64 *le
 
 // ------------------------------------------------------- leaf bucket (K4)
 
-__global__ void k_leaf_hist(RmiDev r, const u64 *keys, i64 nk, u32 *hist) {
-    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < nk; t += (i64)gridDim.x * blockDim.x)
-        atomicAdd(hist + r.route(u64_to_f64(ld_stream(keys + t))), 1u);
-}
-
-__global__ void k_leaf_scatter(RmiDev r, const u64 *keys, const u64 *pay, i64 nk, u32 *cursor,
-                               u64 *ko, u64 *po) {
-    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < nk; t += (i64)gridDim.x * blockDim.x) {
-        u64 k = ld_stream(keys + t);
-        u32 d = atomicAdd(cursor + r.route(u64_to_f64(k)), 1u);
-        ko[d] = k;
-        po[d] = ld_stream(pay + t);
+// Bin = group of 2^shift consecutive leaves (root model only: no leaf load).
+// 8192 groups of a 2^16-leaf index cover 64 KB of gapped slots each, so a
+// warp's probes after bucketing hit one L1/L2-resident index segment.
+struct LeafGroupBin {
+    double rs, ri;
+    i64 m;
+    int shift;
+    __device__ __forceinline__ void prepare() const {}
+    __device__ __forceinline__ int operator()(u64 k) const {
+        return (int)(rmi_route(rs, ri, m, u64_to_f64(k)) >> shift);
     }
+};
+
+static int leaf_group_shift(i64 m) {
+    int s = 0;
+    while (((m + ((i64)1 << s) - 1) >> s) > 8192) ++s;
+    return s;
 }
 
 static size_t al(size_t v) { return (v + 255) & ~(size_t)255; }
@@ -307,7 +478,25 @@ int lj_grmi_probe(const LjGrmi *idx, const uint64_t *s_keys, const uint64_t *s_p
     if (!accumulate) LJ_CK(cudaMemsetAsync(out, 0, 4 * sizeof(u64), st));
     if (nk <= 0 || idx->n == 0) return LJ_OK;
     constexpr int NT = 256;
-    k_grmi_probe<NT><<<grid_for(nk, NT, 8), NT, 0, st>>>(GrmiDev(*idx), s_keys, s_pay, nk, out);
+    static const int sm_variant = getenv("LJ_K1_SM") ? atoi(getenv("LJ_K1_SM")) : 0;
+    if (sm_variant) {
+        k_grmi_probe_sm<NT><<<grid_for(nk, NT, 6), NT, 0, st>>>(GrmiDev(*idx), s_keys, s_pay, nk, out);
+    } else {
+        k_grmi_probe<NT, SoaIn><<<grid_for(nk, NT, 8), NT, 0, st>>>(GrmiDev(*idx), SoaIn{s_keys, s_pay}, nk, out);
+    }
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+int lj_grmi_probe_pairs(const LjGrmi *idx, const uint64_t *s_pairs, int64_t nk, uint64_t *out, int accumulate,
+                        void *stream) {
+    LJ_REQUIRE(idx != nullptr, "null index");
+    cudaStream_t st = as_stream(stream);
+    if (!accumulate) LJ_CK(cudaMemsetAsync(out, 0, 4 * sizeof(u64), st));
+    if (nk <= 0 || idx->n == 0) return LJ_OK;
+    constexpr int NT = 256;
+    k_grmi_probe<NT, AosIn><<<grid_for(nk, NT, 8), NT, 0, st>>>(
+        GrmiDev(*idx), AosIn{reinterpret_cast<const ulonglong2 *>(s_pairs)}, nk, out);
     LJ_CK_LAUNCH();
     return LJ_OK;
 }
@@ -332,34 +521,26 @@ int lj_grmi_collect(const LjGrmi *idx, const uint64_t *keys, int64_t nk, const i
     return LJ_OK;
 }
 
-size_t lj_leaf_bucket_workspace_bytes(int64_t nk, int64_t m) {
-    size_t t = 0;
-    cub::DeviceScan::ExclusiveSum((void *)nullptr, t, (u32 *)nullptr, (u32 *)nullptr, (int64_t)m);
-    return al(sizeof(u32) * (size_t)(m + 1)) + al(t);
+int lj_leaf_bucket_bins(int64_t m) {
+    if (m < 1) return 0;
+    int sh = leaf_group_shift(m);
+    return (int)((m + ((i64)1 << sh) - 1) >> sh);
 }
 
-int lj_leaf_bucket(const LjRmi *model, const uint64_t *keys, const uint64_t *pay, int64_t nk,
-                   uint64_t *keys_out, uint64_t *pay_out, void *ws, size_t ws_bytes, void *stream) {
+size_t lj_leaf_bucket_workspace_bytes(int64_t nk, int64_t m) {
+    return part_workspace_bytes(nk, lj_leaf_bucket_bins(m));
+}
+
+int lj_leaf_bucket(const LjRmi *model, const uint64_t *keys, const uint64_t *pay, int64_t nk, uint64_t *pairs_out,
+                   int64_t *starts_out, void *ws, size_t ws_bytes, void *stream) {
     LJ_REQUIRE(model && model->m >= 1, "model is not fitted");
-    LJ_REQUIRE(nk < (int64_t)0xFFFFFFFFLL, "leaf bucketing counts in 32 bits");
-    if (ws_bytes < lj_leaf_bucket_workspace_bytes(nk, model->m)) {
-        set_error("lj_leaf_bucket: workspace too small");
-        return LJ_E_WORKSPACE;
-    }
-    if (nk <= 0) return LJ_OK;
-    cudaStream_t st = as_stream(stream);
-    u32 *hist = (u32 *)ws;
-    char *tmp = (char *)ws + al(sizeof(u32) * (size_t)(model->m + 1));
-    size_t t = 0;
-    cub::DeviceScan::ExclusiveSum((void *)nullptr, t, hist, hist, (int64_t)model->m);
-    LJ_CK(cudaMemsetAsync(hist, 0, sizeof(u32) * (size_t)(model->m + 1), st));
-    RmiDev r(*model);
-    k_leaf_hist<<<grid_for(nk, 256, 8), 256, 0, st>>>(r, keys, nk, hist);
-    LJ_CK_LAUNCH();
-    LJ_CK(cub::DeviceScan::ExclusiveSum(tmp, t, hist, hist, (int64_t)model->m, st));
-    k_leaf_scatter<<<grid_for(nk, 256, 8), 256, 0, st>>>(r, keys, pay, nk, hist, keys_out, pay_out);
-    LJ_CK_LAUNCH();
-    return LJ_OK;
+    LeafGroupBin f;
+    f.rs = model->root_slope;
+    f.ri = model->root_icpt;
+    f.m = model->m;
+    f.shift = leaf_group_shift(model->m);
+    return run_partition(f, keys, pay, nk, lj_leaf_bucket_bins(model->m), reinterpret_cast<ulonglong2 *>(pairs_out),
+                         starts_out, ws, ws_bytes, as_stream(stream));
 }
 
 }  // extern "C"

@@ -1,0 +1,169 @@
+// lj_part.cuh -- partition (key, payload) tuples into <= 32768 bins with
+// shared-memory privatised counters: no per-tuple global atomics.
+//
+// Global-atomic histograms over 10^5 random bins run at ~60 G atomics/s on
+// B200 (measured, profiles/), far below HBM speed.  Here every block owns a
+// fixed contiguous chunk of the input; pass 1 counts its chunk into a
+// shared-memory histogram and stores it as one column of a bins x blocks
+// matrix; an exclusive scan of the matrix (bin-major) gives every block its
+// private write offset per bin; pass 2 recomputes the bins of the same
+// chunk and scatters with shared-memory cursors.  Output is interleaved
+// 16-B (key, payload) records; bins are contiguous; order inside a bin is
+// unspecified.  Warps aggregate equal bins with match.any before touching
+// shared memory, which keeps hot (duplicate-key) bins cheap.
+#pragma once
+
+#include <cub/cub.cuh>
+
+#include "lj_common.cuh"
+
+namespace lj {
+
+constexpr int PART2_NT = 512;
+constexpr int PART2_MAXBINS = 32768;
+
+struct PartPlan {
+    int nbins;
+    int blocks;
+    i64 chunk;  // tuples per block (multiple of 32)
+};
+
+inline PartPlan part_plan(i64 n, int nbins) {
+    PartPlan p;
+    p.nbins = nbins;
+    // one or two resident blocks per SM, depending on the histogram size
+    int per_sm = nbins <= 8192 ? 2 : 1;
+    p.blocks = sm_count() * per_sm;
+    i64 c = (n + p.blocks - 1) / p.blocks;
+    c = (c + 31) / 32 * 32;
+    p.chunk = c < 32 ? 32 : c;
+    return p;
+}
+
+// pass 1: per-block histogram -> mat[bin * blocks + block]
+template <class BinF>
+__global__ void __launch_bounds__(PART2_NT) k_bin_hist(BinF f, const u64 *__restrict__ keys, i64 n, i64 chunk,
+                                                       int nbins, u32 *mat) {
+    extern __shared__ u32 h[];
+    for (int j = threadIdx.x; j < nbins; j += PART2_NT) h[j] = 0;
+    f.prepare();
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const i64 lo = blockIdx.x * chunk, hi = min(lo + chunk, n);
+    for (i64 base = lo + threadIdx.x - lane; base < hi; base += PART2_NT) {
+        const i64 i = base + lane;
+        int b = -1;
+        if (i < hi) b = f(ld_stream(keys + i));
+        const unsigned peers = __match_any_sync(0xffffffffu, b);
+        if (b >= 0 && lane == __ffs(peers) - 1) atomicAdd(h + b, (u32)__popc(peers));
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < nbins; j += PART2_NT) mat[(i64)j * gridDim.x + blockIdx.x] = h[j];
+}
+
+// pass 2: scatter the same chunk through shared-memory cursors
+template <class BinF>
+__global__ void __launch_bounds__(PART2_NT) k_bin_scatter(BinF f, const u64 *__restrict__ keys,
+                                                          const u64 *__restrict__ pay, i64 n, i64 chunk, int nbins,
+                                                          const i64 *__restrict__ off, ulonglong2 *out) {
+    extern __shared__ u32 cur[];
+    for (int j = threadIdx.x; j < nbins; j += PART2_NT) cur[j] = (u32)off[(i64)j * gridDim.x + blockIdx.x];
+    f.prepare();
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const i64 lo = blockIdx.x * chunk, hi = min(lo + chunk, n);
+    for (i64 base = lo + threadIdx.x - lane; base < hi; base += PART2_NT) {
+        const i64 i = base + lane;
+        int b = -1;
+        u64 k = 0, p = 0;
+        if (i < hi) {
+            k = ld_stream(keys + i);
+            p = ld_stream(pay + i);
+            b = f(k);
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, b);
+        const int leader = __ffs(peers) - 1;
+        u32 at = 0;
+        if (b >= 0 && lane == leader) at = atomicAdd(cur + b, (u32)__popc(peers));
+        at = __shfl_sync(0xffffffffu, at, leader);
+        if (b >= 0) out[at + __popc(peers & ((1u << lane) - 1u))] = make_ulonglong2(k, p);
+    }
+}
+
+// bin starts[j] = off[j * blocks] (first block's offset), starts[nbins] = n
+__global__ void k_bin_starts(const i64 *off, int nbins, int blocks, i64 n, i64 *starts) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= nbins; j += gridDim.x * blockDim.x)
+        starts[j] = j < nbins ? off[(i64)j * blocks] : n;
+}
+
+struct CastU32I64 {
+    __host__ __device__ __forceinline__ i64 operator()(const u32 &v) const { return (i64)v; }
+};
+
+inline size_t part_align(size_t v) { return (v + 255) & ~(size_t)255; }
+
+inline size_t part_scan_bytes(i64 items) {
+    size_t t = 0;
+    cub::TransformInputIterator<i64, CastU32I64, const u32 *> it(nullptr, CastU32I64());
+    cub::DeviceScan::ExclusiveSum(nullptr, t, it, (i64 *)nullptr, (int64_t)items);
+    return t;
+}
+
+inline size_t part_workspace_bytes(i64 n, int nbins) {
+    PartPlan p = part_plan(n, nbins);
+    i64 items = (i64)nbins * p.blocks;
+    return part_align(sizeof(u32) * (size_t)items) + part_align(sizeof(i64) * (size_t)items) +
+           part_align(part_scan_bytes(items));
+}
+
+// Full partition: out[n] records grouped by bin, starts[nbins+1].
+template <class BinF>
+int run_partition(const BinF &f, const u64 *keys, const u64 *pay, i64 n, int nbins, ulonglong2 *out, i64 *starts,
+                  void *ws, size_t ws_bytes, cudaStream_t st) {
+    if (nbins < 1 || nbins > PART2_MAXBINS) {
+        set_error("partition: nbins must be in [1, 32768]");
+        return LJ_E_INVALID;
+    }
+    if (n >= (i64)0xFFFFFFFFLL) {
+        set_error("partition: cursors are 32-bit");
+        return LJ_E_INVALID;
+    }
+    if (ws_bytes < part_workspace_bytes(n, nbins)) {
+        set_error("partition: workspace too small");
+        return LJ_E_WORKSPACE;
+    }
+    PartPlan p = part_plan(n, nbins);
+    i64 items = (i64)nbins * p.blocks;
+    char *q = (char *)ws;
+    u32 *mat = (u32 *)q;
+    q += part_align(sizeof(u32) * (size_t)items);
+    i64 *off = (i64 *)q;
+    q += part_align(sizeof(i64) * (size_t)items);
+    size_t sm = sizeof(u32) * (size_t)nbins;
+    static bool attr_set = false;
+    if (!attr_set) {
+        LJ_CK(cudaFuncSetAttribute(k_bin_hist<BinF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(sizeof(u32) * PART2_MAXBINS)));
+        LJ_CK(cudaFuncSetAttribute(k_bin_scatter<BinF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(sizeof(u32) * PART2_MAXBINS)));
+        attr_set = true;
+    }
+    if (n > 0) {
+        k_bin_hist<BinF><<<p.blocks, PART2_NT, sm, st>>>(f, keys, n, p.chunk, nbins, mat);
+        LJ_CK_LAUNCH();
+    } else {
+        LJ_CK(cudaMemsetAsync(mat, 0, sizeof(u32) * (size_t)items, st));
+    }
+    size_t t = part_scan_bytes(items);
+    cub::TransformInputIterator<i64, CastU32I64, const u32 *> it(mat, CastU32I64());
+    LJ_CK(cub::DeviceScan::ExclusiveSum(q, t, it, off, (int64_t)items, st));
+    k_bin_starts<<<(nbins + 256) / 256, 256, 0, st>>>(off, nbins, p.blocks, n, starts);
+    LJ_CK_LAUNCH();
+    if (n > 0) {
+        k_bin_scatter<BinF><<<p.blocks, PART2_NT, sm, st>>>(f, keys, pay, n, p.chunk, nbins, off, out);
+        LJ_CK_LAUNCH();
+    }
+    return LJ_OK;
+}
+
+}  // namespace lj

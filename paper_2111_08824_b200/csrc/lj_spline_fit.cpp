@@ -88,3 +88,40 @@ extern "C" int lj_spline_fit_host(const uint64_t *keys, int64_t n, int64_t max_e
     *shift_out = shift;
     return LJ_OK;
 }
+
+// Exact accelerator for the bounded search of models.py:263-282 (see
+// LjSpline.aux in lj_b200.h).  Bucket p covers keys with (k >> shift) == p;
+// its sub-table splits that range on the next `bits` key bits.
+extern "C" int lj_spline_aux_host(const uint64_t *keys, int64_t npts, const int64_t *radix, int64_t radix_bits,
+                                  uint64_t shift, uint64_t *aux, uint32_t *sub, int64_t *sub_len) {
+    if (npts < 1 || radix_bits < 1 || radix_bits > 30) return LJ_E_INVALID;
+    const int64_t nb = (int64_t)1 << radix_bits;
+    int64_t off = 0;
+    for (int64_t p = 0; p < nb; ++p) {
+        const int64_t lo = radix[p], hi = radix[p + 1], c = hi - lo;
+        int bits = 0;
+        if (c > 8 && shift > 0) {
+            while (((int64_t)1 << bits) < c) ++bits;
+            bits += 1;
+            if ((uint64_t)bits > shift) bits = (int)shift;
+            if (bits > 24) bits = 24;
+        }
+        if (aux) aux[p] = ((uint64_t)off << 8) | (uint64_t)bits;
+        if (bits) {
+            const int64_t ns = ((int64_t)1 << bits) + 1;
+            if (sub) {
+                const uint64_t sub_shift = shift - (uint64_t)bits;
+                const uint64_t mask = ((uint64_t)1 << bits) - 1;
+                int64_t j = lo;
+                for (int64_t q = 0; q < ns; ++q) {
+                    // first point in [lo, hi) whose sub-prefix is >= q
+                    while (j < hi && (int64_t)((keys[j] >> sub_shift) & mask) < q) ++j;
+                    sub[off + q] = (uint32_t)j;
+                }
+            }
+            off += ns;
+        }
+    }
+    *sub_len = off;
+    return LJ_OK;
+}

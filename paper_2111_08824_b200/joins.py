@@ -133,29 +133,18 @@ def _run_grmi_inlj(r, s, workers, opts):
 def _run_buffered_grmi_inlj(r, s, workers, opts):
     """bench.py:147-181: request buffers -> device leaf bucketing (K4) of
     each S chunk, then the fused probe (K1) over the bucketed chunk."""
-    from . import _lib
-    import ctypes
-
     index = GappedRmiIndex(opts["gap_factor"], opts["rmi_fanout"]).fit(r)
     br = PhaseBreakdown()
     if index.n == 0 or len(s) == 0:
         return JoinResult(), br, 0.0
-    lib = _lib.lib()
-    m = index.rmi.fanout
-    kb = torch.empty_like(s.keys)
-    pb = torch.empty_like(s.payloads)
-    ws = _lib.workspace(lib.lj_leaf_bucket_workspace_bytes(len(s), m), s.keys.device)
-    c = index.rmi.c_struct()
+    scratch = index.bucket_scratch(max(hi - lo for lo, hi in _chunks(len(s), workers)), s.keys.device)
 
     def run():
         out = torch.zeros(4, dtype=torch.int64, device=s.keys.device)
         for lo, hi in _chunks(len(s), workers):
-            if hi == lo:
-                continue
-            _lib.check(lib.lj_leaf_bucket(ctypes.byref(c), _lib.ptr(s.keys[lo:hi]), _lib.ptr(s.payloads[lo:hi]),
-                                          hi - lo, _lib.ptr(kb[lo:hi]), _lib.ptr(pb[lo:hi]), _lib.ptr(ws),
-                                          ws.numel(), _lib.stream_ptr()), "leaf_bucket")
-            index.join_checksum(kb[lo:hi], pb[lo:hi], out=out, accumulate=True)
+            if hi > lo:
+                index.join_checksum_buffered(s.keys[lo:hi], s.payloads[lo:hi], out=out, accumulate=True,
+                                             scratch=scratch)
         return out
 
     if opts.get("materialize"):

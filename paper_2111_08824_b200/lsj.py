@@ -305,8 +305,8 @@ def lsj_join(r: Relation, s: Relation, config: LsjConfig | None = None, material
     pr, str_ = _partition(r.keys, r.payloads, model_r, fr)
     ps, sts = _partition(s.keys, s.payloads, model_s, fs)
     ev[2].record()
-    _sort_in_place(pr, str_, model_r, len(r), fr)
-    _sort_in_place(ps, sts, model_s, len(s), fs)
+    over_r = _sort_in_place(pr, str_, model_r, len(r), fr)
+    over_s = _sort_in_place(ps, sts, model_s, len(s), fs)
     r_sorted = SortedRelation(pr[: 2 * len(r)], str_, fr, scale, model_r, (model_r.tag, scale))
     s_sorted = SortedRelation(ps[: 2 * len(s)], sts, fs, scale, model_s, (model_s.tag, scale))
     ev[3].record()
@@ -318,6 +318,7 @@ def lsj_join(r: Relation, s: Relation, config: LsjConfig | None = None, material
     br.sort = ev[2].elapsed_time(ev[3]) / 1e3
     br.join = ev[3].elapsed_time(ev[4]) / 1e3
     br.sort_stats = SortStats().merge(_sort_stats(str_, fr, scale)).merge(_sort_stats(sts, fs, scale))
+    br.extra = {"fine_scale_r": fr, "fine_scale_s": fs, "oversized_buckets_r": over_r, "oversized_buckets_s": over_s}
     return result, br
 
 

@@ -214,8 +214,31 @@ class RadixSplineIndex:
         self._d_keys = to_device_u64(self.spline_keys, device=dev)
         self._d_ranks = torch.from_numpy(self.spline_ranks.astype(np.float64)).to(dev)
         self._d_radix = torch.from_numpy(self.radix_table.astype(np.uint32).view(np.int32)).to(dev)
+        self._build_aux(dev)
         self.tag = uuid.uuid4().hex
         return self
+
+    use_aux = True  # class switch: the accelerator never changes a result
+
+    def _build_aux(self, dev):
+        """Exact sub-radix accelerator of the bounded spline search
+        (lj_spline_aux_host; see LjSpline.aux)."""
+        self._d_aux = self._d_sub = None
+        if not self.use_aux or self.spline_keys.size < 2:
+            return
+        lib = _lib.load()
+        nb = 1 << self.radix_bits
+        aux = np.zeros(nb, dtype=np.uint64)
+        ln = ctypes.c_int64(0)
+        args = (self.spline_keys.ctypes.data, self.spline_keys.size, self.radix_table.ctypes.data, self.radix_bits,
+                int(self.shift))
+        _lib.check(lib.lj_spline_aux_host(*args, aux.ctypes.data, None, ctypes.byref(ln)), "spline_aux")
+        if ln.value == 0:
+            return
+        sub = np.zeros(ln.value, dtype=np.uint32)
+        _lib.check(lib.lj_spline_aux_host(*args, aux.ctypes.data, sub.ctypes.data, ctypes.byref(ln)), "spline_aux")
+        self._d_aux = torch.from_numpy(aux.view(np.int64)).to(dev)
+        self._d_sub = torch.from_numpy(sub.view(np.int32)).to(dev)
 
     @classmethod
     def from_params(cls, spline_keys, spline_ranks, radix_table, shift, trained_len, max_error, radix_bits,
@@ -227,7 +250,7 @@ class RadixSplineIndex:
         self._check_fitted()
         return _lib.LjSpline(self.spline_keys.size, self.trained_len, self.max_error, self.radix_bits,
                              int(self.shift), _lib.ptr(self._d_keys), _lib.ptr(self._d_ranks),
-                             _lib.ptr(self._d_radix))
+                             _lib.ptr(self._d_radix), _lib.ptr(self._d_aux), _lib.ptr(self._d_sub))
 
     def _check_fitted(self):
         if self.trained_len == 0:
