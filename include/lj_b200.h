@@ -182,13 +182,15 @@ int lj_grmi_collect(const LjGrmi *idx, const uint64_t *keys, int64_t nk, const i
 /* buffers.py:73-150 analogue: reorder S by RMI leaf (stable counting sort)
  * so that K1 walks the index leaf by leaf.  hist needs m+1 words of
  * device scratch inside ws. */
-/* Bins are groups of consecutive leaves (<= 8192 groups, root model only);
- * counting uses shared-memory-privatised histograms (no per-tuple global
- * atomics).  pairs_out[2nk] interleaved {key, payload} grouped by bin,
- * starts_out[bins+1].  Order inside a bin is unspecified. */
-int lj_leaf_bucket_bins(int64_t m);
-size_t lj_leaf_bucket_workspace_bytes(int64_t nk, int64_t m);
-int lj_leaf_bucket(const LjRmi *model, const uint64_t *keys, const uint64_t *pay, int64_t nk,
+/* Request-Buffer analogue: group S by a window of 2^k gapped slots around
+ * each key's predicted slot (<= 8192 windows), so that K1 then walks the
+ * index window by window.  Counting uses shared-memory-privatised
+ * histograms (no per-tuple global atomics).  pairs_out[2nk] interleaved
+ * {key, payload} grouped by window, starts_out[bins+1]; order inside a
+ * window is unspecified.  bins = lj_leaf_bucket_bins(L). */
+int lj_leaf_bucket_bins(int64_t L);
+size_t lj_leaf_bucket_workspace_bytes(int64_t nk, int64_t L);
+int lj_leaf_bucket(const LjGrmi *idx, const uint64_t *keys, const uint64_t *pay, int64_t nk,
                    uint64_t *pairs_out, int64_t *starts_out, void *ws, size_t ws_bytes, void *stream);
 /* K1 over interleaved {key, payload} probe records (e.g. bucketed S). */
 int lj_grmi_probe_pairs(const LjGrmi *idx, const uint64_t *s_pairs, int64_t nk, uint64_t *out, int accumulate,

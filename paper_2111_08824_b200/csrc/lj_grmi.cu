@@ -381,22 +381,25 @@ __global__ void k_grmi_collect(GrmiDev g, const u64 *keys, i64 nk, const i64 *le
 
 // ------------------------------------------------------- leaf bucket (K4)
 
-// Bin = group of 2^shift consecutive leaves (root model only: no leaf load).
-// 8192 groups of a 2^16-leaf index cover 64 KB of gapped slots each, so a
-// warp's probes after bucketing hit one L1/L2-resident index segment.
-struct LeafGroupBin {
-    double rs, ri;
-    i64 m;
+// Bin = window of 2^shift gapped slots around the PREDICTED slot of the key
+// (gapped.py:258-261).  A leaf-based grouping is useless on skewed keys:
+// the linear root routes most lognormal keys to a handful of huge leaves.
+// Predicted-slot windows (<= 8192 bins, e.g. 4096 slots = 64 KB at C2) make
+// every warp's searches after bucketing stay inside one L1/L2-resident
+// stretch of the index, so each index sector comes from DRAM ~once.
+struct SlotBin {
+    RmiDev m;
+    i64 n, L;
     int shift;
     __device__ __forceinline__ void prepare() const {}
     __device__ __forceinline__ int operator()(u64 k) const {
-        return (int)(rmi_route(rs, ri, m, u64_to_f64(k)) >> shift);
+        return (int)(grmi_slot_of_pos(m.pos(u64_to_f64(k)), n, L) >> shift);
     }
 };
 
-static int leaf_group_shift(i64 m) {
+static int slot_window_shift(i64 L) {
     int s = 0;
-    while (((m + ((i64)1 << s) - 1) >> s) > 8192) ++s;
+    while (((L + ((i64)1 << s) - 1) >> s) > 8192) ++s;
     return s;
 }
 
@@ -521,25 +524,25 @@ int lj_grmi_collect(const LjGrmi *idx, const uint64_t *keys, int64_t nk, const i
     return LJ_OK;
 }
 
-int lj_leaf_bucket_bins(int64_t m) {
-    if (m < 1) return 0;
-    int sh = leaf_group_shift(m);
-    return (int)((m + ((i64)1 << sh) - 1) >> sh);
+int lj_leaf_bucket_bins(int64_t L) {
+    if (L < 1) return 0;
+    int sh = slot_window_shift(L);
+    return (int)((L + ((i64)1 << sh) - 1) >> sh);
 }
 
-size_t lj_leaf_bucket_workspace_bytes(int64_t nk, int64_t m) {
-    return part_workspace_bytes(nk, lj_leaf_bucket_bins(m));
+size_t lj_leaf_bucket_workspace_bytes(int64_t nk, int64_t L) {
+    return part_workspace_bytes(nk, lj_leaf_bucket_bins(L));
 }
 
-int lj_leaf_bucket(const LjRmi *model, const uint64_t *keys, const uint64_t *pay, int64_t nk, uint64_t *pairs_out,
+int lj_leaf_bucket(const LjGrmi *idx, const uint64_t *keys, const uint64_t *pay, int64_t nk, uint64_t *pairs_out,
                    int64_t *starts_out, void *ws, size_t ws_bytes, void *stream) {
-    LJ_REQUIRE(model && model->m >= 1, "model is not fitted");
-    LeafGroupBin f;
-    f.rs = model->root_slope;
-    f.ri = model->root_icpt;
-    f.m = model->m;
-    f.shift = leaf_group_shift(model->m);
-    return run_partition(f, keys, pay, nk, lj_leaf_bucket_bins(model->m), reinterpret_cast<ulonglong2 *>(pairs_out),
+    LJ_REQUIRE(idx && idx->n >= 1 && idx->L >= 1, "index is empty");
+    SlotBin f;
+    f.m = RmiDev(idx->model);
+    f.n = idx->n;
+    f.L = idx->L;
+    f.shift = slot_window_shift(idx->L);
+    return run_partition(f, keys, pay, nk, lj_leaf_bucket_bins(idx->L), reinterpret_cast<ulonglong2 *>(pairs_out),
                          starts_out, ws, ws_bytes, as_stream(stream));
 }
 

@@ -70,22 +70,43 @@ __global__ void k_hash_starts(const u64 *sorted_b, i64 n, i64 nb, u32 *starts) {
 // K5: learned_hash.py:81-96 fused with the checksum.  One lane per probe:
 // spline position (radix table + bounded search over spline points, both
 // L2-resident), bucket, chain offsets, chain scan.
-template <int NT>
+// Each thread carries U independent probes through the same stages so their
+// dependent load chains overlap (the chain is latency-bound: radix/aux ->
+// sub-table -> spline points -> chain offsets -> entries).  Chain offsets
+// and entries are random, touched once: they are read evict-first so they do
+// not push the (L2-resident) spline structures out of L2.
+template <int NT, int U>
 __global__ void __launch_bounds__(NT) k_hash_probe(HashDev h, const u64 *__restrict__ skeys,
                                                    const u64 *__restrict__ spay, i64 nk, u64 *out) {
     u64 cnt = 0, sum = 0, x = 0;
-    for (i64 t = blockIdx.x * (i64)NT + threadIdx.x; t < nk; t += (i64)gridDim.x * NT) {
-        u64 k = ld_stream(skeys + t);
-        u64 ps = ld_stream(spay + t);
-        i64 b = h.slot_of(k);
-        u32 a = __ldg(h.starts + b), e = __ldg(h.starts + b + 1);
-        for (u32 i = a; i < e; ++i) {
-            ulonglong2 en = ldg2(h.entries + 2 * (i64)i);
-            if (en.x != k) continue;
-            u64 v = en.y + ps;
-            ++cnt;
-            sum += v;
-            x ^= v;
+    const i64 stride = (i64)gridDim.x * NT;
+    for (i64 t0 = blockIdx.x * (i64)NT + threadIdx.x; t0 < nk; t0 += stride * U) {
+        u64 k[U], ps[U];
+        i64 b[U];
+        u32 a[U], e[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const i64 t = t0 + u * stride;
+            k[u] = t < nk ? ld_stream(skeys + t) : 0;
+            ps[u] = t < nk ? ld_stream(spay + t) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) b[u] = t0 + u * stride < nk ? h.slot_of(k[u]) : -1;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            a[u] = b[u] >= 0 ? __ldcs(h.starts + b[u]) : 0;
+            e[u] = b[u] >= 0 ? __ldcs(h.starts + b[u] + 1) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            for (u32 i = a[u]; i < e[u]; ++i) {
+                ulonglong2 en = __ldcs(reinterpret_cast<const ulonglong2 *>(h.entries) + i);
+                if (en.x != k[u]) continue;
+                u64 v = en.y + ps[u];
+                ++cnt;
+                sum += v;
+                x ^= v;
+            }
         }
     }
     reduce_checksum(cnt, sum, x, 0, out);
@@ -197,7 +218,13 @@ int lj_spline_hash_probe(const LjSplineHash *idx, const uint64_t *s_keys, const 
     if (!accumulate) LJ_CK(cudaMemsetAsync(out, 0, 4 * sizeof(u64), st));
     if (nk <= 0 || idx->n == 0) return LJ_OK;
     constexpr int NT = 256;
-    k_hash_probe<NT><<<grid_for(nk, NT, 8), NT, 0, st>>>(HashDev(*idx), s_keys, s_pay, nk, out);
+    static const int ilp = getenv("LJ_K5_ILP") ? atoi(getenv("LJ_K5_ILP")) : 2;
+    if (ilp >= 4)
+        k_hash_probe<NT, 4><<<grid_for((nk + 3) / 4, NT, 8), NT, 0, st>>>(HashDev(*idx), s_keys, s_pay, nk, out);
+    else if (ilp == 2)
+        k_hash_probe<NT, 2><<<grid_for((nk + 1) / 2, NT, 8), NT, 0, st>>>(HashDev(*idx), s_keys, s_pay, nk, out);
+    else
+        k_hash_probe<NT, 1><<<grid_for(nk, NT, 8), NT, 0, st>>>(HashDev(*idx), s_keys, s_pay, nk, out);
     LJ_CK_LAUNCH();
     return LJ_OK;
 }

@@ -102,18 +102,19 @@ class GappedRmiIndex:
         to n probes (bucketed records + bin bounds + partition workspace)."""
         lib = _lib.lib()
         dev = device or self.slots.device
-        m = self.rmi.fanout
+        L = self.slot_count
         return {"pairs": torch.empty(2 * max(n, 1), dtype=torch.int64, device=dev),
-                "starts": torch.empty(lib.lj_leaf_bucket_bins(m) + 1, dtype=torch.int64, device=dev),
-                "ws": _lib.workspace(lib.lj_leaf_bucket_workspace_bytes(n, m), dev)}
+                "starts": torch.empty(lib.lj_leaf_bucket_bins(L) + 1, dtype=torch.int64, device=dev),
+                "ws": _lib.workspace(lib.lj_leaf_bucket_workspace_bytes(n, L), dev)}
 
     def join_checksum_buffered(self, s_keys: torch.Tensor, s_payloads: torch.Tensor,
                                out: torch.Tensor | None = None, accumulate: bool = False, scratch: dict | None = None,
                                stream=None) -> torch.Tensor:
-        """Request-Buffer analogue (buffers.py:103-150): group S by RMI leaf
-        group on device (K4, shared-memory privatised partition), then run K1
-        over the grouped records, so each warp walks one index segment that
-        stays in L1/L2.  Same result words as ``join_checksum``."""
+        """Request-Buffer analogue (buffers.py:103-150): group S on device by
+        the window of predicted gapped slots it will search (K4, shared-memory
+        privatised partition), then run K1 over the grouped records, so each
+        warp walks one index segment that stays in L1/L2.  Same result words
+        as ``join_checksum``."""
         n = s_keys.numel()
         if out is None:
             out = torch.zeros(4, dtype=torch.int64, device=s_keys.device)
@@ -124,12 +125,11 @@ class GappedRmiIndex:
         scratch = scratch or self.bucket_scratch(n, s_keys.device)
         lib = _lib.lib()
         st = _lib.stream_ptr(stream)
-        c = self.rmi.c_struct()
+        g = self.c_struct()
         ws = scratch["ws"]
-        _lib.check(lib.lj_leaf_bucket(ctypes.byref(c), _lib.ptr(s_keys), _lib.ptr(s_payloads), n,
+        _lib.check(lib.lj_leaf_bucket(ctypes.byref(g), _lib.ptr(s_keys), _lib.ptr(s_payloads), n,
                                       _lib.ptr(scratch["pairs"]), _lib.ptr(scratch["starts"]), _lib.ptr(ws),
                                       ws.numel(), st), "leaf_bucket")
-        g = self.c_struct()
         _lib.check(lib.lj_grmi_probe_pairs(ctypes.byref(g), _lib.ptr(scratch["pairs"]), n, _lib.ptr(out),
                                            int(bool(accumulate)), st), "grmi_probe_pairs")
         return out
