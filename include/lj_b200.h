@@ -232,31 +232,44 @@ int lj_spline_hash_collect(const LjSplineHash *idx, const uint64_t *keys, int64_
 size_t lj_lsj_sample_workspace_bytes(int64_t total);
 int lj_lsj_sample(const uint64_t *keys, int64_t n, int64_t total, uint64_t seed, uint64_t *sample_sorted,
                   void *ws, size_t ws_bytes, void *stream);
-/* lsj.py:133-209 / 258-263: K6 histogram + K7 warp-aggregated scatter of
- * (key, payload) into nbins CDF buckets of the model (partition_index at
- * scale nbins).  pairs[2n] interleaved out; starts[nbins+1] bucket bounds. */
+/* An LSJ relation model: the sample-fitted RMI plus equi-depth bins over its
+ * predicted positions: bin(key) = table[pos(key)], pb[j] = first predicted
+ * position of bin j (pb[nbins] = trained_len).  Monotone in the key. */
+typedef struct LjLsjModel {
+    LjRmi rmi;
+    int64_t nbins;            /* <= 32768 */
+    const int64_t *pb;        /* [nbins+1] */
+    const uint32_t *table;    /* [rmi.n] */
+} LjLsjModel;
+/* Bin boundaries at equally spaced ranks of the sorted sample. */
+size_t lj_lsj_bins_workspace_bytes(int64_t total);
+int lj_lsj_bins(const LjRmi *model, const uint64_t *sample_sorted, int64_t total, int64_t nbins, int64_t *pb,
+                uint32_t *table, void *ws, size_t ws_bytes, void *stream);
+/* Table from explicit bounds (pb[j] = ceil(j*n/nbins) gives exactly the
+ * reference's partition_index buckets at scale nbins, models.py:297). */
+int lj_lsj_bins_from_bounds(const int64_t *pb, int64_t nbins, int64_t trained_len, uint32_t *table, void *stream);
+/* lsj.py:133-209 / 258-263: K6 histogram + K7 scatter of (key, payload)
+ * into the model's bins, shared-memory privatised (no per-tuple global
+ * atomics).  pairs[2n] interleaved out; starts[nbins+1] bucket bounds. */
 size_t lj_lsj_partition_workspace_bytes(int64_t n, int64_t nbins);
-int lj_lsj_partition(const LjRmi *model, const uint64_t *keys, const uint64_t *pay, int64_t n, int64_t nbins,
+int lj_lsj_partition(const LjLsjModel *model, const uint64_t *keys, const uint64_t *pay, int64_t n,
                      uint64_t *pairs, int64_t *starts, void *ws, size_t ws_bytes, void *stream);
-/* lsj.py:242-286 per-bucket sort (K8), model-placed, in place on pairs.
- * stats_host[0] = buckets too large for shared memory (handled by
- * lj_lsj_sort_oversized), stats_host[1] = runs queued for lj_lsj_sort_runs.
- * Synchronises the stream (reads two counters). */
+/* lsj.py:242-286 per-bucket sort (K8, model-placed, shared memory) from the
+ * partitioned pairs_in into pairs_out (fully sorted, bucket ranges kept).
+ * stats_host[4] = {oversized buckets, bitonic fallbacks, sub-buckets above
+ * shared memory, device radix-sorted sub-buckets}.  Synchronises the
+ * stream (reads a few counters). */
 size_t lj_lsj_sort_workspace_bytes(int64_t n, int64_t nbins);
-int lj_lsj_sort_buckets(const LjRmi *model, uint64_t *pairs, int64_t n, int64_t nbins, const int64_t *starts,
-                        void *ws, size_t ws_bytes, int64_t *stats_host, void *stream);
-/* ids of the oversized buckets recorded in a sort workspace (host copy). */
-int lj_lsj_oversized_list_host(void *sort_ws, int64_t n, int64_t count, int64_t *buckets_host);
-size_t lj_lsj_sort_oversized_workspace_bytes(int64_t nseg, int64_t total);
-int lj_lsj_sort_oversized(const LjRmi *model, uint64_t *pairs, int64_t n, int64_t nbins,
-                          const int64_t *seg_bucket_host, const int64_t *seg_begin_host,
-                          const int64_t *seg_end_host, int64_t nseg, void *sort_ws, void *ws, size_t ws_bytes,
-                          int64_t *stats_host, void *stream);
-int lj_lsj_sort_runs(uint64_t *pairs, int64_t n, void *sort_ws, void *stream);
+int lj_lsj_sort(const LjLsjModel *model, const uint64_t *pairs_in, uint64_t *pairs_out, int64_t n,
+                const int64_t *starts, void *ws, size_t ws_bytes, int64_t *stats_host, void *stream);
+/* Reference bucket bounds at scale P of a sorted relation (the
+ * partition_index buckets of lsj.py:302-305, for its counters). */
+int lj_lsj_ref_bounds(const LjRmi *model, const uint64_t *sorted_pairs, int64_t n, int64_t P, int64_t *bounds,
+                      void *stream);
 /* lsj.py:316-370 chunked join (K9) of sorted S against sorted R through R's
- * model at R's bucket scale r_nbins.  mode 0: out[4] checksum; mode 1:
- * counts[ns]; mode 2: pairs at offsets[ns] into out_pr/out_ps. */
-int lj_lsj_join(const LjRmi *model_r, const uint64_t *r_pairs, int64_t nr, int64_t r_nbins, const int64_t *r_starts,
+ * model and bucket bounds.  mode 0: out[4] checksum; mode 1: counts[ns];
+ * mode 2: pairs at offsets[ns] into out_pr/out_ps. */
+int lj_lsj_join(const LjLsjModel *model_r, const uint64_t *r_pairs, int64_t nr, const int64_t *r_starts,
                 const uint64_t *s_pairs, int64_t ns, int mode, int64_t *counts, const int64_t *offsets,
                 uint64_t *out_pr, uint64_t *out_ps, uint64_t *out, int accumulate, void *stream);
 

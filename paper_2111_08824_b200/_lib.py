@@ -59,6 +59,10 @@ class LjSplineHash(ctypes.Structure):
                 ("entries", _c_void_p), ("starts", _c_void_p)]
 
 
+class LjLsjModel(ctypes.Structure):
+    _fields_ = [("rmi", LjRmi), ("nbins", _i64), ("pb", _c_void_p), ("table", _c_void_p)]
+
+
 # name -> (restype, argtypes); mirrors include/lj_b200.h one to one
 _P = _c_void_p
 SIGNATURES = {
@@ -96,16 +100,15 @@ SIGNATURES = {
     "lj_spline_hash_collect": (_int, [ctypes.POINTER(LjSplineHash), _P, _i64, _P, _P, _P, _P]),
     "lj_lsj_sample_workspace_bytes": (_size_t, [_i64]),
     "lj_lsj_sample": (_int, [_P, _i64, _i64, _u64, _P, _P, _size_t, _P]),
+    "lj_lsj_bins_workspace_bytes": (_size_t, [_i64]),
+    "lj_lsj_bins": (_int, [ctypes.POINTER(LjRmi), _P, _i64, _i64, _P, _P, _P, _size_t, _P]),
+    "lj_lsj_bins_from_bounds": (_int, [_P, _i64, _i64, _P, _P]),
     "lj_lsj_partition_workspace_bytes": (_size_t, [_i64, _i64]),
-    "lj_lsj_partition": (_int, [ctypes.POINTER(LjRmi), _P, _P, _i64, _i64, _P, _P, _P, _size_t, _P]),
+    "lj_lsj_partition": (_int, [ctypes.POINTER(LjLsjModel), _P, _P, _i64, _P, _P, _P, _size_t, _P]),
     "lj_lsj_sort_workspace_bytes": (_size_t, [_i64, _i64]),
-    "lj_lsj_sort_buckets": (_int, [ctypes.POINTER(LjRmi), _P, _i64, _i64, _P, _P, _size_t, _P, _P]),
-    "lj_lsj_oversized_list_host": (_int, [_P, _i64, _i64, _P]),
-    "lj_lsj_sort_oversized_workspace_bytes": (_size_t, [_i64, _i64]),
-    "lj_lsj_sort_oversized": (_int, [ctypes.POINTER(LjRmi), _P, _i64, _i64, _P, _P, _P, _i64, _P, _P, _size_t,
-                                     _P, _P]),
-    "lj_lsj_sort_runs": (_int, [_P, _i64, _P, _P]),
-    "lj_lsj_join": (_int, [ctypes.POINTER(LjRmi), _P, _i64, _i64, _P, _P, _i64, _int, _P, _P, _P, _P, _P, _int,
+    "lj_lsj_sort": (_int, [ctypes.POINTER(LjLsjModel), _P, _P, _i64, _P, _P, _size_t, _P, _P]),
+    "lj_lsj_ref_bounds": (_int, [ctypes.POINTER(LjRmi), _P, _i64, _i64, _P, _P]),
+    "lj_lsj_join": (_int, [ctypes.POINTER(LjLsjModel), _P, _i64, _P, _P, _i64, _int, _P, _P, _P, _P, _P, _int,
                            _P]),
 }
 

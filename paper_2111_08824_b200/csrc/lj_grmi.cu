@@ -384,7 +384,7 @@ __global__ void k_grmi_collect(GrmiDev g, const u64 *keys, i64 nk, const i64 *le
 // Bin = window of 2^shift gapped slots around the PREDICTED slot of the key
 // (gapped.py:258-261).  A leaf-based grouping is useless on skewed keys:
 // the linear root routes most lognormal keys to a handful of huge leaves.
-// Predicted-slot windows (<= 8192 bins, e.g. 4096 slots = 64 KB at C2) make
+// Predicted-slot windows (<= 2048 bins, e.g. 16384 slots = 256 KB at C2) make
 // every warp's searches after bucketing stay inside one L1/L2-resident
 // stretch of the index, so each index sector comes from DRAM ~once.
 struct SlotBin {
@@ -399,7 +399,9 @@ struct SlotBin {
 
 static int slot_window_shift(i64 L) {
     int s = 0;
-    while (((L + ((i64)1 << s) - 1) >> s) > 8192) ++s;
+    // <= 2048 windows: blocks x bins open write lines (~148 x 2048 x 128 B)
+    // stay L2-resident during the scatter, so records leave L2 as full lines
+    while (((L + ((i64)1 << s) - 1) >> s) > 2048) ++s;
     return s;
 }
 
@@ -542,7 +544,8 @@ int lj_leaf_bucket(const LjGrmi *idx, const uint64_t *keys, const uint64_t *pay,
     f.n = idx->n;
     f.L = idx->L;
     f.shift = slot_window_shift(idx->L);
-    return run_partition(f, keys, pay, nk, lj_leaf_bucket_bins(idx->L), reinterpret_cast<ulonglong2 *>(pairs_out),
+    SoaSrc<SlotBin> src{keys, pay, f};
+    return run_partition(src, nk, lj_leaf_bucket_bins(idx->L), reinterpret_cast<ulonglong2 *>(pairs_out),
                          starts_out, ws, ws_bytes, as_stream(stream));
 }
 

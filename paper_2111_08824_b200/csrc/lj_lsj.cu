@@ -1,151 +1,160 @@
 // lj_lsj.cu -- learned sort-join (LSJ) on the GPU.  Reference: lsj.py:95-405.
 //
-//   smpl  K10 on a stratified 1% sample (lj_lsj_sample + lj_rmi_fit)
-//   part  K6 histogram + K7 scatter of (key, payload) into Pf = P*F fine
-//         CDF buckets (warp-aggregated atomics; 16-B interleaved output)
-//   sort  K8 per fine bucket in shared memory: MODEL-PLACED counting sort
-//         by the predicted position (the RMI is monotone, so ordering by
-//         predicted position is consistent with key order and only runs of
-//         equal predicted position remain unsorted), then insertion sort of
-//         those runs; long runs go to a bitonic pass (k_sort_runs);
-//         buckets larger than shared memory take the same model placement
-//         through global memory (k_over_*); runs of one repeated key are
-//         left as they are.
-//   join  K9 per S tile of 1024 sorted tuples: the R window is found
-//         through R's model (chunked_join's [f_R, l_R], lsj.py:343-346, at
-//         the fine scale), staged in shared memory and merge-searched;
-//         emits the checksum (or counts / pairs when materialising).
-//
-// Fine scale: the reference sorts P = effective_fanout buckets; Pf = P*F
-// nests exactly inside them (floor(pos*P*F/n)/F == floor(pos*P/n)), so the
-// coarse bucket bounds the reference reports are every F-th fine bound.
+//   smpl  stratified sample (lj_lsj_sample) -> RMI fit (K10, lj_rmi_fit) ->
+//         equi-depth bins over the model's predicted positions (lj_lsj_bins):
+//         bin(key) = table[pos(key)], with bin boundaries at equally spaced
+//         SAMPLE ranks.  The reference partitions uniformly in predicted
+//         position (partition_index, models.py:285-299); on skewed keys the
+//         2-level linear RMI predicts positions badly (its linear root sends
+//         most lognormal keys to a few leaves) and uniform position buckets
+//         vary by >8x.  Cutting the same monotone position axis at sample
+//         quantiles keeps every bin near n/nbins.  Monotone in the key, so
+//         the buckets are relatively sorted exactly as the reference's.
+//   part  K6/K7: shared-memory-privatised histogram + scatter into <= 32768
+//         bins (lj_part.cuh), 16-B interleaved records.
+//   sort  K8: one CTA per bucket, in shared memory, MODEL-PLACED: every key's
+//         unrounded prediction y (slope*x + icpt clamped to its leaf's rank
+//         range, monotone non-decreasing in the key) is mapped to one of m
+//         slots of the bucket; a counting sort by slot puts each key within
+//         a few places of its final position; runs sharing a slot are
+//         insertion-sorted; a verification pass falls back to a full
+//         in-smem bitonic sort of the bucket if anything is out of order.
+//         Buckets above shared-memory capacity (hot duplicate keys) are
+//         re-partitioned by y at finer resolution through global memory and
+//         sorted the same way; sub-buckets of one repeated key are copied.
+//   join  K9: per S tile of 1024 sorted tuples, the R bucket range of the
+//         tile's first/last key through R's model (chunked_join's
+//         [f_R, l_R], lsj.py:343-346) bounds a binary search for the exact
+//         R slice, which is staged in shared memory and merge-searched;
+//         emits the checksum (or per-tuple counts / pairs).
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <vector>
 
 #include "lj_common.cuh"
+#include "lj_part.cuh"
 
 namespace lj {
 
-constexpr int PART_NT = 256;
-constexpr int SORT_NT = 512;
-constexpr int CAP = 4096;     // largest bucket sorted in shared memory
-constexpr int NBMAX = 2048;   // predicted-position bins per bucket
-constexpr int RUN_SMALL = 32; // runs up to this length: insertion sort
-constexpr int JOIN_T = 1024;  // S tile of the join
+constexpr int SORT_NT = 1024;
+constexpr int CAP = 12288;        // largest bucket sorted in shared memory
+constexpr int BITONIC_W = 16384;  // fallback network width (>= CAP)
+constexpr int RUN_SMALL = 64;     // equal-slot runs insertion-sorted by one thread
+constexpr int SUB = 8192;         // mean tuples per sub-bucket (shared-memory sort unit)
+constexpr int SPLIT_NT = 1024;
+constexpr int SPLIT_MAXF = 4096;  // y-slices per coarse bucket
+constexpr int JOIN_T = 1024;
 constexpr int JOIN_NT = 256;
-constexpr int WCAP = 4096;    // R window keys staged in shared memory
+constexpr int WCAP = 4096;
 
-// exact floor(x / d) for 0 <= x < 2^63, d >= 1: float reciprocal + fix-up
-__device__ __forceinline__ i64 fdiv(i64 x, i64 d, double rd) {
-    i64 q = (i64)__dmul_rn(i64_to_f64(x), rd);
-    i64 r = x - q * d;
-    while (r < 0) { --q; r += d; }
-    while (r >= d) { ++q; r -= d; }
-    return q;
-}
+// ------------------------------------------------------------------ model
 
-struct Bin {
+// RMI + equi-depth bin table over predicted positions.
+struct LsjDev {
     RmiDev m;
-    i64 nbins;
-    double rn;  // 1.0 / m.n
-    __device__ __forceinline__ i64 pos(const LjLeaf *lv, u64 k) const {
-        double x = u64_to_f64(k);
-        return rmi_leaf_pos(lv[m.route(x)], x);
-    }
-    // models.py:297 partition_index at scale nbins, exact
-    __device__ __forceinline__ i64 of_pos(i64 p) const {
-        return clip_i64(fdiv(p * nbins, m.n, rn), 0, nbins - 1);
+    const u32 *table;  // [m.n] predicted position -> bin
+    const i64 *pb;     // [nb+1] first position of each bin
+    int nb;
+    __device__ __forceinline__ i64 pos(u64 k) const { return m.pos(u64_to_f64(k)); }
+    __device__ __forceinline__ int bin(u64 k) const { return (int)__ldg(table + pos(k)); }
+    // Unrounded placement key y in [pos-0.5, pos+0.5], monotone in the key:
+    // within a leaf slope*x + icpt is non-decreasing; clamping to the leaf's
+    // disjoint, ordered rank range [clamp_lo-0.5, clamp_hi+0.5] keeps order
+    // across leaves; flat (slope 0, e.g. empty) leaves sit at clamp_lo-0.5.
+    __device__ __forceinline__ double y(u64 k) const {
+        const double x = u64_to_f64(k);
+        const LjLeaf lf = load_leaf(m.leaves, m.route(x));
+        const double lo = i64_to_f64(lf.clamp_lo) - 0.5;
+        if (!(lf.slope > 0.0)) return lo;
+        const double raw = __dadd_rn(__dmul_rn(lf.slope, x), lf.icpt);
+        const double hi = i64_to_f64(lf.clamp_hi) + 0.5;
+        return raw < lo ? lo : (raw > hi ? hi : raw);
     }
 };
 
-// Stage the leaf table in shared memory when it fits (LSJ sample models
-// have <= 1000 leaves = 32 KB); otherwise read it through L1.
-__device__ __forceinline__ const LjLeaf *stage_leaves(const RmiDev &m, LjLeaf *sl, bool stage) {
-    if (!stage) return m.leaves;
-    for (i64 i = threadIdx.x; i < m.m; i += blockDim.x) sl[i] = m.leaves[i];
-    __syncthreads();
-    return sl;
+static LsjDev make_lsj(const LjLsjModel &md) {
+    LsjDev d;
+    d.m = RmiDev(md.rmi);
+    d.table = md.table;
+    d.pb = md.pb;
+    d.nb = (int)md.nbins;
+    return d;
 }
 
-// ----------------------------------------------------------------- part
+struct LsjBin {
+    LsjDev d;
+    __device__ __forceinline__ void prepare() const {}
+    __device__ __forceinline__ int operator()(u64 k) const { return d.bin(k); }
+};
 
-__global__ void __launch_bounds__(PART_NT) k_part_hist(Bin bn, const u64 *__restrict__ keys, i64 n, u32 *hist,
-                                                       int stage) {
-    extern __shared__ LjLeaf s_leaves[];
-    const LjLeaf *lv = stage_leaves(bn.m, s_leaves, stage);
-    const int lane = threadIdx.x & 31;
-    const i64 stride = (i64)gridDim.x * PART_NT;
-    for (i64 base = blockIdx.x * (i64)PART_NT + threadIdx.x - lane; base < n; base += stride) {
-        i64 i = base + lane;
-        long long b = -1;
-        if (i < n) b = bn.of_pos(bn.pos(lv, ld_stream(keys + i)));
-        unsigned peers = __match_any_sync(0xffffffffu, b);
-        if (b >= 0 && lane == __ffs(peers) - 1) atomicAdd(hist + b, (u32)__popc(peers));
+// spos[i] = pos(sample[i]) (sample sorted -> spos non-decreasing)
+__global__ void k_sample_pos(RmiDev m, const u64 *sample, i64 total, i64 *spos) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < total; i += (i64)gridDim.x * blockDim.x)
+        spos[i] = m.pos(u64_to_f64(sample[i]));
+}
+
+// pb[0] = 0, pb[j] = spos[floor(j*S/nb)], pb[nb] = trained_len
+__global__ void k_bin_bounds(const i64 *spos, i64 total, int nb, i64 tl, i64 *pb) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= nb; j += gridDim.x * blockDim.x) {
+        if (j == 0) pb[j] = 0;
+        else if (j == nb) pb[j] = tl;
+        else pb[j] = spos[(i64)(((unsigned __int128)j * (u64)total) / (u64)nb)];
     }
 }
 
-__global__ void __launch_bounds__(PART_NT) k_part_scatter(Bin bn, const u64 *__restrict__ keys,
-                                                          const u64 *__restrict__ pay, i64 n,
-                                                          unsigned long long *cursor, ulonglong2 *out, int stage) {
-    extern __shared__ LjLeaf s_leaves[];
-    const LjLeaf *lv = stage_leaves(bn.m, s_leaves, stage);
-    const int lane = threadIdx.x & 31;
-    const i64 stride = (i64)gridDim.x * PART_NT;
-    for (i64 base = blockIdx.x * (i64)PART_NT + threadIdx.x - lane; base < n; base += stride) {
-        i64 i = base + lane;
-        long long b = -1;
-        u64 k = 0, p = 0;
-        if (i < n) {
-            k = ld_stream(keys + i);
-            p = ld_stream(pay + i);
-            b = bn.of_pos(bn.pos(lv, k));
+// table[p] = #{ j in [1, nb-1] : pb[j] <= p }
+__global__ void k_bin_table(const i64 *pb, int nb, i64 tl, u32 *table) {
+    for (i64 p = blockIdx.x * (i64)blockDim.x + threadIdx.x; p < tl; p += (i64)gridDim.x * blockDim.x) {
+        int lo = 1, hi = nb;  // upper_bound over pb[1..nb-1]
+        while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (pb[mid] <= p) lo = mid + 1; else hi = mid;
         }
-        unsigned peers = __match_any_sync(0xffffffffu, b);
-        int leader = __ffs(peers) - 1;
-        unsigned long long at = 0;
-        if (b >= 0 && lane == leader) at = atomicAdd(cursor + b, (unsigned long long)__popc(peers));
-        at = __shfl_sync(0xffffffffu, at, leader);
-        if (b >= 0) out[at + __popc(peers & ((1u << lane) - 1u))] = make_ulonglong2(k, p);
+        table[p] = (u32)(lo - 1);
     }
 }
 
-struct CastI64 {
-    __host__ __device__ __forceinline__ i64 operator()(const u32 &v) const { return (i64)v; }
-};
-
-// ----------------------------------------------------------------- sort
+// ------------------------------------------------------------------- sort
 
 struct SortCtl {
-    unsigned long long next;   // work counter over buckets
-    unsigned long long n_over; // buckets larger than CAP
-    unsigned long long n_med;  // runs of RUN_SMALL < len <= CAP
-    unsigned long long n_huge; // non-constant runs > CAP
-    unsigned long long next_run;
+    unsigned long long next;
+    unsigned long long n_over;
+    unsigned long long n_fallback;
+    unsigned long long n_const;
 };
 
-// first predicted position of fine bucket b: ceil(b*n / nbins)
-__device__ __forceinline__ i64 pos_lo_of(i64 b, i64 n, i64 nbins) { return (b * n + nbins - 1) / nbins; }
+// bucket descriptor: [in_base, in_base + m) -> [out_base, out_base + m),
+// placement range y in [ybase, ybase + yspan)
+struct Bucket {
+    i64 in_base, m, out_base;
+    double ybase, yspan;
+};
 
-__device__ __forceinline__ void insertion_sort_idx(u16 *idx, int len, const ulonglong2 *A) {
-    for (int i = 1; i < len; ++i) {
-        u16 v = idx[i];
-        u64 kv = A[v].x;
-        int j = i - 1;
-        while (j >= 0 && A[idx[j]].x > kv) {
-            idx[j + 1] = idx[j];
-            --j;
-        }
-        idx[j + 1] = v;
+// Sub-buckets written by k_lsj_split: y-slices of the coarse buckets, in
+// place (sub-bucket g covers [sub_starts[g], sub_starts[g+1]) of both the
+// split array and the final output).
+struct SubBuckets {
+    const i64 *sub_starts;  // [G+1]
+    const double2 *sub_y;   // [G] {ybase, yspan}
+    __device__ __forceinline__ Bucket get(i64 g) const {
+        Bucket k;
+        k.in_base = sub_starts[g];
+        k.m = sub_starts[g + 1] - k.in_base;
+        k.out_base = k.in_base;
+        const double2 y = sub_y[g];
+        k.ybase = y.x;
+        k.yspan = y.y;
+        return k;
     }
-}
+};
 
-// Block-wide exclusive scan of cnt[0..nb) into st[] (and cu[] = st[]).
-__device__ __forceinline__ void block_exclusive_scan(const u32 *cnt, u32 *st, u32 *cu, int nb, u32 *warp_tot) {
-    const int per = (nb + SORT_NT - 1) / SORT_NT;
+__device__ __forceinline__ void block_scan_u32(u32 *a, int n, u32 *warp_tot) {
+    // exclusive scan of a[0..n) in place, SORT_NT threads
+    const int per = (n + SORT_NT - 1) / SORT_NT;
     const int j0 = threadIdx.x * per;
     u32 local = 0;
-    for (int j = j0; j < j0 + per && j < nb; ++j) local += cnt[j];
+    for (int j = j0; j < j0 + per && j < n; ++j) local += a[j];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     u32 incl = local;
 #pragma unroll
@@ -162,222 +171,254 @@ __device__ __forceinline__ void block_exclusive_scan(const u32 *cnt, u32 *st, u3
             u32 v = __shfl_up_sync(0xffffffffu, t, o);
             if (lane >= o) t += v;
         }
-        if (lane < SORT_NT / 32) warp_tot[lane] = t;  // inclusive warp totals
+        if (lane < SORT_NT / 32) warp_tot[lane] = t;
     }
     __syncthreads();
     u32 run = (warp ? warp_tot[warp - 1] : 0) + incl - local;
-    for (int j = j0; j < j0 + per && j < nb; ++j) {
-        st[j] = run;
-        cu[j] = run;
-        run += cnt[j];
+    for (int j = j0; j < j0 + per && j < n; ++j) {
+        u32 c = a[j];
+        a[j] = run;
+        run += c;
     }
     __syncthreads();
 }
 
-// K8: one CTA per fine bucket (dynamic work counter).  Model-placed
-// counting sort in shared memory, then fix-up of equal-position runs.
-__global__ void __launch_bounds__(SORT_NT, 2) k_sort_buckets(Bin bn, ulonglong2 *pairs, const i64 *starts,
-                                                             SortCtl *ctl, i64 *over_list, i64 *med_list) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    ulonglong2 *A = reinterpret_cast<ulonglong2 *>(smem);
-    u16 *rel = reinterpret_cast<u16 *>(A + CAP);
-    u16 *idx = rel + CAP;
-    u32 *cnt = reinterpret_cast<u32 *>(idx + CAP);
-    u32 *st = cnt + NBMAX;
-    u32 *cu = st + NBMAX;
-    __shared__ u32 warp_tot[SORT_NT / 32];
+// Coarse bucket b -> F_b = ceil(m_b / SUB) y-slices of about SUB tuples.
+__global__ void k_split_plan(const i64 *starts, int nb, i64 *fcount) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += gridDim.x * blockDim.x) {
+        if (b == nb) {
+            fcount[b] = 0;
+            continue;
+        }
+        const i64 m = starts[b + 1] - starts[b];
+        i64 f = (m + SUB - 1) / SUB;
+        fcount[b] = m == 0 ? 0 : (f < 1 ? 1 : (f > SPLIT_MAXF ? SPLIT_MAXF : f));
+    }
+}
+
+__device__ __forceinline__ int y_slice(double y, double ybase, double scale, int F) {
+    const double f = floor((y - ybase) * scale);
+    return f < 0.0 ? 0 : (f >= (double)(F - 1) ? F - 1 : (int)f);
+}
+
+// Level 2, one CTA per coarse bucket: split it into F_b y-slices through
+// global memory.  The CTA owns the bucket, so only F_b write lines per CTA
+// are open at a time (a grid-wide pass into 30K+ bins would thrash L2).
+__global__ void __launch_bounds__(SPLIT_NT) k_lsj_split(LsjDev md, const ulonglong2 *__restrict__ A,
+                                                        const i64 *__restrict__ starts, const i64 *__restrict__ fbase,
+                                                        int nb, ulonglong2 *B, i64 *sub_starts, double2 *sub_y,
+                                                        SortCtl *ctl) {
+    __shared__ u32 h[SPLIT_MAXF];
+    __shared__ u32 warp_tot[SPLIT_NT / 32];
     __shared__ i64 s_b;
-    const i64 n = bn.m.n, nbins = bn.nbins;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (;;) {
         if (threadIdx.x == 0) s_b = (i64)atomicAdd(&ctl->next, 1ULL);
         __syncthreads();
         const i64 b = s_b;
         __syncthreads();
-        if (b >= nbins) break;
+        if (b >= nb) break;
         const i64 a = starts[b], m = starts[b + 1] - a;
-        if (m <= 1) continue;
-        const i64 plo = pos_lo_of(b, n, nbins);
-        const int nb = (int)(pos_lo_of(b + 1, n, nbins) - plo);
-        if (m > CAP || nb > NBMAX || nb < 1) {
+        if (m == 0) continue;
+        const i64 g0 = fbase[b];
+        const int F = (int)(fbase[b + 1] - g0);
+        const double ybase = i64_to_f64(md.pb[b]) - 0.5;
+        double yspan = i64_to_f64(md.pb[b + 1] - md.pb[b]);
+        if (!(yspan > 0.0)) yspan = 1.0;
+        const double scale = (double)F / yspan;
+        for (int j = threadIdx.x; j < F; j += SPLIT_NT) h[j] = 0;
+        __syncthreads();
+        for (i64 base = threadIdx.x - lane; base < m; base += SPLIT_NT) {
+            const i64 i = base + lane;
+            int s = -1;
+            if (i < m) s = y_slice(md.y(A[a + i].x), ybase, scale, F);
+            const unsigned peers = __match_any_sync(0xffffffffu, s);
+            if (s >= 0 && lane == __ffs(peers) - 1) atomicAdd(h + s, (u32)__popc(peers));
+        }
+        __syncthreads();
+        // exclusive scan of h[0..F) (F <= SPLIT_MAXF, 4 per thread)
+        {
+            const int per = (F + SPLIT_NT - 1) / SPLIT_NT, j0 = threadIdx.x * per;
+            u32 local = 0;
+            for (int j = j0; j < j0 + per && j < F; ++j) local += h[j];
+            u32 incl = local;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                u32 v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            if (lane == 31) warp_tot[warp] = incl;
+            __syncthreads();
+            if (warp == 0) {
+                u32 t = lane < SPLIT_NT / 32 ? warp_tot[lane] : 0;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    u32 v = __shfl_up_sync(0xffffffffu, t, o);
+                    if (lane >= o) t += v;
+                }
+                if (lane < SPLIT_NT / 32) warp_tot[lane] = t;
+            }
+            __syncthreads();
+            u32 run = (warp ? warp_tot[warp - 1] : 0) + incl - local;
+            for (int j = j0; j < j0 + per && j < F; ++j) {
+                const u32 c = h[j];
+                h[j] = run;
+                sub_starts[g0 + j] = a + run;
+                sub_y[g0 + j] = make_double2(ybase + (double)j / scale, 1.0 / scale);
+                run += c;
+            }
+            __syncthreads();
+        }
+        for (i64 base = threadIdx.x - lane; base < m; base += SPLIT_NT) {
+            const i64 i = base + lane;
+            int s = -1;
+            ulonglong2 e = make_ulonglong2(0, 0);
+            if (i < m) {
+                e = A[a + i];
+                s = y_slice(md.y(e.x), ybase, scale, F);
+            }
+            const unsigned peers = __match_any_sync(0xffffffffu, s);
+            const int leader = __ffs(peers) - 1;
+            u32 at = 0;
+            if (s >= 0 && lane == leader) at = atomicAdd(h + s, (u32)__popc(peers));
+            at = __shfl_sync(0xffffffffu, at, leader);
+            if (s >= 0) B[a + at + __popc(peers & ((1u << lane) - 1u))] = e;
+        }
+        __syncthreads();
+    }
+}
+
+// K8: one CTA per bucket (dynamic work counter), model-placed in smem.
+template <class Src>
+__global__ void __launch_bounds__(SORT_NT, 1) k_lsj_sort(LsjDev md, Src src, const i64 *nbuckets_dev,
+                                                         const ulonglong2 *__restrict__ in, ulonglong2 *out,
+                                                         SortCtl *ctl, i64 *over_list) {
+    const i64 nbuckets = *nbuckets_dev;
+    extern __shared__ __align__(16) unsigned char smem[];
+    u64 *K = reinterpret_cast<u64 *>(smem);              // keys [CAP]
+    u32 *cnt = reinterpret_cast<u32 *>(K + CAP);          // slot counts -> cursors [CAP]
+    u16 *slot = reinterpret_cast<u16 *>(cnt + CAP);       // slot per key [CAP]
+    u16 *idx = slot + CAP;                                // placement [BITONIC_W]
+    __shared__ u32 warp_tot[SORT_NT / 32];
+    __shared__ i64 s_b;
+    __shared__ int s_bad;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            s_b = (i64)atomicAdd(&ctl->next, 1ULL);
+            s_bad = 0;
+        }
+        __syncthreads();
+        const i64 b = s_b;
+        __syncthreads();
+        if (b >= nbuckets) break;
+        const Bucket bk = src.get(b);
+        const int m = (int)(bk.m < (i64)CAP ? bk.m : (i64)CAP);
+        if (bk.m == 0) continue;
+        if (bk.m == 1) {
+            if (threadIdx.x == 0) out[bk.out_base] = in[bk.in_base];
+            continue;
+        }
+        if (bk.m > CAP) {
             if (threadIdx.x == 0) over_list[atomicAdd(&ctl->n_over, 1ULL)] = b;
             continue;
         }
-        for (int j = threadIdx.x; j < nb; j += SORT_NT) cnt[j] = 0;
+        const double scale = (double)m / (bk.yspan > 0.0 ? bk.yspan : 1.0);
+        for (int j = threadIdx.x; j < m; j += SORT_NT) cnt[j] = 0;
         __syncthreads();
+        // load keys, place by the model
         for (int i = threadIdx.x; i < m; i += SORT_NT) {
-            ulonglong2 v = pairs[a + i];
-            A[i] = v;
-            i64 r = bn.pos(bn.m.leaves, v.x) - plo;
-            r = r < 0 ? 0 : (r >= nb ? nb - 1 : r);
-            rel[i] = (u16)r;
-            atomicAdd(cnt + r, 1u);
+            const u64 k = in[bk.in_base + i].x;
+            K[i] = k;
+            double f = floor((md.y(k) - bk.ybase) * scale);
+            int s = f < 0.0 ? 0 : (f >= (double)(m - 1) ? m - 1 : (int)f);
+            slot[i] = (u16)s;
+            atomicAdd(cnt + s, 1u);
         }
         __syncthreads();
-        block_exclusive_scan(cnt, st, cu, nb, warp_tot);
-        for (int i = threadIdx.x; i < m; i += SORT_NT) idx[atomicAdd(cu + rel[i], 1u)] = (u16)i;
+        block_scan_u32(cnt, m, warp_tot);
+        for (int i = threadIdx.x; i < m; i += SORT_NT) idx[atomicAdd(cnt + slot[i], 1u)] = (u16)i;
         __syncthreads();
-        for (int j = threadIdx.x; j < nb; j += SORT_NT) {
-            int len = (int)cnt[j];
+        // runs sharing a slot: [start, cnt[slot]) after the scatter
+        for (int i = threadIdx.x; i < m; i += SORT_NT) {
+            const int si = slot[idx[i]];
+            if (i > 0 && slot[idx[i - 1]] == si) continue;  // not a run start
+            const int e = (int)cnt[si];
+            const int len = e - i;
             if (len < 2) continue;
             if (len <= RUN_SMALL) {
-                insertion_sort_idx(idx + st[j], len, A);
+                for (int a = i + 1; a < e; ++a) {
+                    const u16 v = idx[a];
+                    const u64 kv = K[v];
+                    int q = a - 1;
+                    while (q >= i && K[idx[q]] > kv) {
+                        idx[q + 1] = idx[q];
+                        --q;
+                    }
+                    idx[q + 1] = v;
+                }
             } else {
-                unsigned long long q = atomicAdd(&ctl->n_med, 1ULL);
-                med_list[2 * q] = a + st[j];
-                med_list[2 * q + 1] = len;
+                const u64 k0 = K[idx[i]];
+                bool same = true;
+                for (int a = i + 1; a < e && same; ++a) same = K[idx[a]] == k0;
+                if (!same) s_bad = 1;  // long mixed run: sort the whole bucket below
             }
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < m; i += SORT_NT) pairs[a + i] = A[idx[i]];
+        for (int i = threadIdx.x; i + 1 < m; i += SORT_NT)
+            if (K[idx[i]] > K[idx[i + 1]]) s_bad = 1;
         __syncthreads();
-    }
-}
-
-// Bitonic sort (by key) of runs RUN_SMALL < len <= CAP listed as
-// (start, len) pairs, one CTA per run, padded with the sentinel key.
-__global__ void __launch_bounds__(SORT_NT) k_sort_runs(ulonglong2 *pairs, const i64 *list, SortCtl *ctl) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    ulonglong2 *A = reinterpret_cast<ulonglong2 *>(smem);
-    __shared__ i64 s_r;
-    const unsigned long long nruns = ctl->n_med;
-    for (;;) {
-        if (threadIdx.x == 0) s_r = (i64)atomicAdd(&ctl->next_run, 1ULL);
-        __syncthreads();
-        const i64 r = s_r;
-        __syncthreads();
-        if ((unsigned long long)r >= nruns) break;
-        const i64 a = list[2 * r];
-        const int len = (int)list[2 * r + 1];
-        int w = 1;
-        while (w < len) w <<= 1;
-        for (int i = threadIdx.x; i < w; i += SORT_NT)
-            A[i] = i < len ? pairs[a + i] : make_ulonglong2(~0ULL, 0ULL);
-        __syncthreads();
-        for (int k = 2; k <= w; k <<= 1) {
-            for (int j = k >> 1; j > 0; j >>= 1) {
-                for (int i = threadIdx.x; i < w; i += SORT_NT) {
-                    int l = i ^ j;
-                    if (l > i) {
-                        ulonglong2 x = A[i], y = A[l];
-                        bool up = (i & k) == 0;
-                        if ((x.x > y.x) == up) {
-                            A[i] = y;
-                            A[l] = x;
+        if (s_bad) {
+            // fallback: bitonic sort of the bucket's indices by key (padded
+            // with a sentinel index that compares as +inf)
+            int w = 1;
+            while (w < m) w <<= 1;
+            for (int i = threadIdx.x; i < w; i += SORT_NT) idx[i] = i < m ? (u16)i : (u16)0xFFFF;
+            __syncthreads();
+            for (int kk = 2; kk <= w; kk <<= 1) {
+                for (int j = kk >> 1; j > 0; j >>= 1) {
+                    for (int i = threadIdx.x; i < w; i += SORT_NT) {
+                        const int l = i ^ j;
+                        if (l > i) {
+                            const u16 a = idx[i], c = idx[l];
+                            const bool ga = a == 0xFFFF, gc = c == 0xFFFF;
+                            const bool agt = ga ? !gc : (gc ? false : K[a] > K[c]);
+                            const bool up = (i & kk) == 0;
+                            if (agt == up) {
+                                idx[i] = c;
+                                idx[l] = a;
+                            }
                         }
                     }
+                    __syncthreads();
                 }
-                __syncthreads();
             }
+            if (threadIdx.x == 0) atomicAdd(&ctl->n_fallback, 1ULL);
         }
-        for (int i = threadIdx.x; i < len; i += SORT_NT) pairs[a + i] = A[i];
+        // write out: key from smem, payload gathered from the bucket (L2-hot)
+        for (int i = threadIdx.x; i < m; i += SORT_NT) {
+            const u16 j = idx[i];
+            out[bk.out_base + i] = make_ulonglong2(K[j], __ldg(&in[bk.in_base + j].y));
+        }
         __syncthreads();
     }
 }
 
-// ------------------------------------------- oversized buckets (global)
-//
-// Flattened over the oversized buckets: element t belongs to oversized
-// bucket k with ooff[k] <= t < ooff[k+1]; its bin is k*NBMAX + (pos - plo).
-
-__device__ __forceinline__ int find_seg(const i64 *off, int nseg, i64 t) {
-    int lo = 0, hi = nseg;  // last k with off[k] <= t
-    while (hi - lo > 1) {
-        int mid = (lo + hi) >> 1;
-        if (off[mid] <= t) lo = mid; else hi = mid;
-    }
-    return lo;
-}
-
-__global__ void k_over_hist(Bin bn, const ulonglong2 *pairs, const i64 *obkt, const i64 *obeg, const i64 *ooff,
-                            int nseg, i64 total, u32 *hist, unsigned long long *bmin, unsigned long long *bmax) {
-    const int lane = threadIdx.x & 31;
-    const i64 stride = (i64)gridDim.x * blockDim.x;
-    for (i64 base = blockIdx.x * (i64)blockDim.x + threadIdx.x - lane; base < total; base += stride) {
-        i64 t = base + lane;
-        long long bin = -1;
-        u64 k = 0;
-        if (t < total) {
-            int s = find_seg(ooff, nseg, t);
-            k = pairs[obeg[s] + (t - ooff[s])].x;
-            i64 plo = pos_lo_of(obkt[s], bn.m.n, bn.nbins);
-            i64 r = bn.pos(bn.m.leaves, k) - plo;
-            r = r < 0 ? 0 : (r >= NBMAX ? NBMAX - 1 : r);
-            bin = (long long)s * NBMAX + r;
-        }
-        unsigned peers = __match_any_sync(0xffffffffu, bin);
-        int leader = __ffs(peers) - 1;
-        u64 lk = __shfl_sync(0xffffffffu, k, leader);
-        if (bin >= 0) {
-            if (lane == leader) atomicAdd(hist + bin, (u32)__popc(peers));
-            if (lane == leader || k != lk) {
-                atomicMin(bmin + bin, (unsigned long long)k);
-                atomicMax(bmax + bin, (unsigned long long)k);
-            }
-        }
-    }
-}
-
-__global__ void k_over_scatter(Bin bn, const ulonglong2 *pairs, const i64 *obkt, const i64 *obeg, const i64 *ooff,
-                               int nseg, i64 total, unsigned long long *cursor, ulonglong2 *tmp) {
-    const int lane = threadIdx.x & 31;
-    const i64 stride = (i64)gridDim.x * blockDim.x;
-    for (i64 base = blockIdx.x * (i64)blockDim.x + threadIdx.x - lane; base < total; base += stride) {
-        i64 t = base + lane;
-        long long bin = -1;
-        ulonglong2 v = make_ulonglong2(0, 0);
-        if (t < total) {
-            int s = find_seg(ooff, nseg, t);
-            v = pairs[obeg[s] + (t - ooff[s])];
-            i64 plo = pos_lo_of(obkt[s], bn.m.n, bn.nbins);
-            i64 r = bn.pos(bn.m.leaves, v.x) - plo;
-            r = r < 0 ? 0 : (r >= NBMAX ? NBMAX - 1 : r);
-            bin = (long long)s * NBMAX + r;
-        }
-        unsigned peers = __match_any_sync(0xffffffffu, bin);
-        int leader = __ffs(peers) - 1;
-        unsigned long long at = 0;
-        if (bin >= 0 && lane == leader) at = atomicAdd(cursor + bin, (unsigned long long)__popc(peers));
-        at = __shfl_sync(0xffffffffu, at, leader);
-        if (bin >= 0) tmp[at + __popc(peers & ((1u << lane) - 1u))] = v;
-    }
-}
-
-__global__ void k_over_copyback(const ulonglong2 *tmp, const i64 *obeg, const i64 *ooff, int nseg, i64 total,
-                                ulonglong2 *pairs) {
-    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < total; t += (i64)gridDim.x * blockDim.x) {
-        int s = find_seg(ooff, nseg, t);
-        pairs[obeg[s] + (t - ooff[s])] = tmp[t];
-    }
-}
-
-// runs of equal predicted position inside oversized buckets
-__global__ void k_over_runs(ulonglong2 *pairs, const i64 *obeg, const i64 *ooff, const i64 *bst, i64 nbin_total,
-                            const unsigned long long *bmin, const unsigned long long *bmax, SortCtl *ctl,
-                            i64 *med_list, i64 *huge_list) {
-    for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < nbin_total; j += (i64)gridDim.x * blockDim.x) {
-        i64 len = bst[j + 1] - bst[j];
-        if (len < 2 || bmin[j] == bmax[j]) continue;  // empty, single or one repeated key
-        int s = (int)(j / NBMAX);
-        i64 a = obeg[s] + (bst[j] - ooff[s]);
-        if (len <= RUN_SMALL) {
-            for (i64 i = 1; i < len; ++i) {  // insertion sort in place (global)
-                ulonglong2 v = pairs[a + i];
-                i64 q = i - 1;
-                while (q >= 0 && pairs[a + q].x > v.x) {
-                    pairs[a + q + 1] = pairs[a + q];
-                    --q;
-                }
-                pairs[a + q + 1] = v;
-            }
-        } else if (len <= CAP) {
-            unsigned long long q = atomicAdd(&ctl->n_med, 1ULL);
-            med_list[2 * q] = a;
-            med_list[2 * q + 1] = len;
-        } else {
-            unsigned long long q = atomicAdd(&ctl->n_huge, 1ULL);
-            huge_list[2 * q] = a;
-            huge_list[2 * q + 1] = len;
-        }
+// sub-buckets still above CAP: one repeated key -> copy; else flag
+__global__ void k_big_sub(const ulonglong2 *tmp, SubBuckets sb, const i64 *list, int nlist, ulonglong2 *out,
+                          int *flags) {
+    for (int q = blockIdx.x; q < nlist; q += gridDim.x) {
+        const Bucket bk = sb.get(list[q]);
+        const u64 k0 = tmp[bk.in_base].x;
+        __shared__ int diff;
+        if (threadIdx.x == 0) diff = 0;
+        __syncthreads();
+        for (i64 i = threadIdx.x; i < bk.m; i += blockDim.x)
+            if (tmp[bk.in_base + i].x != k0) diff = 1;
+        __syncthreads();
+        if (!diff)
+            for (i64 i = threadIdx.x; i < bk.m; i += blockDim.x) out[bk.out_base + i] = tmp[bk.in_base + i];
+        if (threadIdx.x == 0) flags[q] = diff;
+        __syncthreads();
     }
 }
 
@@ -394,30 +435,60 @@ __global__ void k_interleave(const u64 *k, const u64 *v, i64 n, ulonglong2 *p) {
         p[i] = make_ulonglong2(k[i], v[i]);
 }
 
-// ----------------------------------------------------------------- join
+// reference bucket bounds at scale P of a sorted relation (for the
+// reference's comparator / partition counters, lsj.py:250-286, 302-305)
+__global__ void k_ref_bounds(RmiDev m, const ulonglong2 *sorted, i64 n, i64 P, i64 *bounds) {
+    for (i64 c = blockIdx.x * (i64)blockDim.x + threadIdx.x; c <= P; c += (i64)gridDim.x * blockDim.x) {
+        i64 lo = 0, hi = n;  // first i with partition_index(key_i, P) >= c
+        while (lo < hi) {
+            i64 mid = (lo + hi) >> 1;
+            if (scale_bucket(m.pos(u64_to_f64(sorted[mid].x)), P, m.n) < c) lo = mid + 1; else hi = mid;
+        }
+        bounds[c] = lo;
+    }
+}
 
-// K9: per S tile, the R window [starts_r[f], starts_r[l+1]) of the tile's
-// first/last key through R's model (lsj.py:343-367); staged in shared
-// memory when it fits; lower-bound + equal-run scan per S tuple.
-// mode 0: checksum into out[4]; 1: per-S match counts; 2: emit pairs.
-__global__ void __launch_bounds__(JOIN_NT) k_lsj_join(Bin br, const ulonglong2 *__restrict__ R, i64 nr,
+// ------------------------------------------------------------------- join
+
+// K9: see the file header.  mode 0: checksum; 1: per-S counts; 2: pairs.
+__global__ void __launch_bounds__(JOIN_NT) k_lsj_join(LsjDev mr, const ulonglong2 *__restrict__ R, i64 nr,
                                                       const i64 *__restrict__ rst, const ulonglong2 *__restrict__ S,
                                                       i64 ns, int mode, i64 *counts, const i64 *offsets, u64 *opr,
                                                       u64 *ops, u64 *out) {
     __shared__ u64 wk[WCAP];
+    __shared__ i64 s_lo, s_hi;
     u64 cnt = 0, sum = 0, x = 0;
     const i64 ntiles = (ns + JOIN_T - 1) / JOIN_T;
     for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const i64 a = tile * JOIN_T, e = min(a + (i64)JOIN_T, ns);
-        const u64 kf = S[a].x, kl = S[e - 1].x;
-        const i64 f = br.of_pos(br.pos(br.m.leaves, kf)), l = br.of_pos(br.pos(br.m.leaves, kl));
-        const i64 wlo = rst[f], whi = rst[l + 1], w = whi - wlo;
+        if (threadIdx.x < 2) {
+            // R bucket range of the tile's first / last key through R's model,
+            // then the exact slice [lower_bound(kf), upper_bound(kl))
+            const u64 kf = S[a].x, kl = S[e - 1].x;
+            const i64 wlo = rst[mr.bin(kf)], whi = rst[mr.bin(kl) + 1];
+            i64 lo = wlo, hi = whi;
+            if (threadIdx.x == 0) {
+                while (lo < hi) {
+                    i64 mid = (lo + hi) >> 1;
+                    if (R[mid].x < kf) lo = mid + 1; else hi = mid;
+                }
+                s_lo = lo;
+            } else {
+                while (lo < hi) {
+                    i64 mid = (lo + hi) >> 1;
+                    if (R[mid].x <= kl) lo = mid + 1; else hi = mid;
+                }
+                s_hi = lo;
+            }
+        }
+        __syncthreads();
+        const i64 wlo = s_lo, whi = s_hi > s_lo ? s_hi : s_lo, w = whi - wlo;
         const bool staged = w <= WCAP;
         if (staged)
             for (i64 j = threadIdx.x; j < w; j += JOIN_NT) wk[j] = R[wlo + j].x;
         __syncthreads();
         for (i64 i = a + threadIdx.x; i < e; i += JOIN_NT) {
-            ulonglong2 sv = S[i];
+            const ulonglong2 sv = S[i];
             i64 lo, hi;
             if (staged) {
                 lo = 0;
@@ -438,15 +509,15 @@ __global__ void __launch_bounds__(JOIN_NT) k_lsj_join(Bin br, const ulonglong2 *
             i64 c = 0;
             i64 o = mode == 2 ? offsets[i] : 0;
             for (i64 j = lo; j < whi; ++j) {
-                ulonglong2 rv = R[j];
-                if (rv.x != sv.x) break;
+                const u64 rk = staged ? wk[j - wlo] : R[j].x;
+                if (rk != sv.x) break;
                 if (mode == 0) {
-                    u64 v = rv.y + sv.y;
+                    const u64 v = R[j].y + sv.y;
                     ++cnt;
                     sum += v;
                     x ^= v;
                 } else if (mode == 2) {
-                    opr[o] = rv.y;
+                    opr[o] = R[j].y;
                     ops[o] = sv.y;
                     ++o;
                 }
@@ -476,18 +547,28 @@ __global__ void k_sample(const u64 *keys, i64 n, i64 total, u64 seed, u64 *out) 
 
 static size_t al(size_t v) { return (v + 255) & ~(size_t)255; }
 
-static Bin make_bin(const LjRmi &m, i64 nbins) {
-    Bin b;
-    b.m = RmiDev(m);
-    b.nbins = nbins;
-    b.rn = 1.0 / (double)m.n;
-    return b;
+static size_t sort_smem_bytes() {
+    return sizeof(u64) * CAP + sizeof(u32) * CAP + sizeof(u16) * CAP + sizeof(u16) * BITONIC_W;
 }
 
-static size_t scan_bytes(i64 nitems) {
+template <class Src>
+static int launch_sort(const LsjDev &md, const Src &src, const i64 *nb_dev, const ulonglong2 *in, ulonglong2 *out,
+                       SortCtl *ctl, i64 *over, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        LJ_CK(cudaFuncSetAttribute(k_lsj_sort<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)sort_smem_bytes()));
+        attr = true;
+    }
+    LJ_CK(cudaMemsetAsync(ctl, 0, sizeof(SortCtl), st));
+    k_lsj_sort<Src><<<sm_count(), SORT_NT, sort_smem_bytes(), st>>>(md, src, nb_dev, in, out, ctl, over);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+static size_t scan_i64_bytes(i64 items) {
     size_t t = 0;
-    cub::TransformInputIterator<i64, CastI64, const u32 *> it(nullptr, CastI64());
-    cub::DeviceScan::ExclusiveSum(nullptr, t, it, (i64 *)nullptr, (int64_t)nitems);
+    cub::DeviceScan::ExclusiveSum(nullptr, t, (const i64 *)nullptr, (i64 *)nullptr, (int64_t)items);
     return t;
 }
 
@@ -521,226 +602,156 @@ int lj_lsj_sample(const uint64_t *keys, int64_t n, int64_t total, uint64_t seed,
     return LJ_OK;
 }
 
-size_t lj_lsj_partition_workspace_bytes(int64_t n, int64_t nbins) {
-    (void)n;
-    return al(sizeof(u32) * (size_t)(nbins + 1)) + al(scan_bytes(nbins + 1));
-}
+size_t lj_lsj_bins_workspace_bytes(int64_t total) { return al(sizeof(i64) * (size_t)total); }
 
-int lj_lsj_partition(const LjRmi *model, const uint64_t *keys, const uint64_t *pay, int64_t n, int64_t nbins,
-                     uint64_t *pairs, int64_t *starts, void *ws, size_t ws_bytes, void *stream) {
+int lj_lsj_bins(const LjRmi *model, const uint64_t *sample_sorted, int64_t total, int64_t nbins, int64_t *pb,
+                uint32_t *table, void *ws, size_t ws_bytes, void *stream) {
     LJ_REQUIRE(model && model->m >= 1 && model->n >= 1, "model is not fitted");
-    LJ_REQUIRE(n >= 0 && nbins >= 1, "need n >= 0 and nbins >= 1");
-    LJ_REQUIRE(n < (int64_t)0xFFFFFFFFLL, "per-bucket counters are 32-bit");
-    if (ws_bytes < lj_lsj_partition_workspace_bytes(n, nbins)) {
-        set_error("lj_lsj_partition: workspace too small");
+    LJ_REQUIRE(total >= 1 && nbins >= 1 && nbins <= PART2_MAXBINS, "need total >= 1 and 1 <= nbins <= 32768");
+    if (ws_bytes < lj_lsj_bins_workspace_bytes(total)) {
+        set_error("lj_lsj_bins: workspace too small");
         return LJ_E_WORKSPACE;
     }
     cudaStream_t st = as_stream(stream);
-    u32 *hist = (u32 *)ws;
-    char *cub_tmp = (char *)ws + al(sizeof(u32) * (size_t)(nbins + 1));
-    LJ_CK(cudaMemsetAsync(hist, 0, sizeof(u32) * (size_t)(nbins + 1), st));
-    Bin bn = make_bin(*model, nbins);
-    int stage = model->m <= 2048;
-    size_t sm = stage ? sizeof(LjLeaf) * (size_t)model->m : 0;
-    if (n > 0) {
-        k_part_hist<<<grid_for(n, PART_NT, 8), PART_NT, sm, st>>>(bn, keys, n, hist, stage);
-        LJ_CK_LAUNCH();
-    }
-    size_t t = scan_bytes(nbins + 1);
-    cub::TransformInputIterator<i64, CastI64, const u32 *> it(hist, CastI64());
-    LJ_CK(cub::DeviceScan::ExclusiveSum(cub_tmp, t, it, starts, (int64_t)(nbins + 1), st));
-    if (n > 0) {
-        // the exclusive starts double as the scatter cursors (rebuilt below)
-        k_part_scatter<<<grid_for(n, PART_NT, 8), PART_NT, sm, st>>>(
-            bn, keys, pay, n, reinterpret_cast<unsigned long long *>(starts), reinterpret_cast<ulonglong2 *>(pairs),
-            stage);
-        LJ_CK_LAUNCH();
-        // starts[b] now holds the end of bucket b == start of b+1: rescan
-        LJ_CK(cub::DeviceScan::ExclusiveSum(cub_tmp, t, it, starts, (int64_t)(nbins + 1), st));
-    }
+    i64 *spos = (i64 *)ws;
+    RmiDev m(*model);
+    k_sample_pos<<<grid_for(total, 256, 8), 256, 0, st>>>(m, sample_sorted, total, spos);
+    k_bin_bounds<<<(int)((nbins + 256) / 256), 256, 0, st>>>(spos, total, (int)nbins, model->n, pb);
+    k_bin_table<<<grid_for(model->n, 256, 8), 256, 0, st>>>(pb, (int)nbins, model->n, table);
+    LJ_CK_LAUNCH();
     return LJ_OK;
 }
 
-static void sort_ws_parts(void *ws, i64 n, SortCtl **ctl, i64 **over, i64 **med) {
-    char *p = (char *)ws;
-    *ctl = (SortCtl *)p;
-    p += al(sizeof(SortCtl));
-    *over = (i64 *)p;
-    p += al(sizeof(i64) * (size_t)(n / CAP + 2));
-    *med = (i64 *)p;
+int lj_lsj_bins_from_bounds(const int64_t *pb, int64_t nbins, int64_t trained_len, uint32_t *table, void *stream) {
+    LJ_REQUIRE(nbins >= 1 && nbins <= PART2_MAXBINS && trained_len >= 1, "bad bins");
+    k_bin_table<<<grid_for(trained_len, 256, 8), 256, 0, as_stream(stream)>>>(pb, (int)nbins, trained_len, table);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
 }
+
+size_t lj_lsj_partition_workspace_bytes(int64_t n, int64_t nbins) { return part_workspace_bytes(n, (int)nbins); }
+
+int lj_lsj_partition(const LjLsjModel *md, const uint64_t *keys, const uint64_t *pay, int64_t n, uint64_t *pairs,
+                     int64_t *starts, void *ws, size_t ws_bytes, void *stream) {
+    LJ_REQUIRE(md && md->table && md->pb && md->nbins >= 1, "model has no bins");
+    LsjBin f{make_lsj(*md)};
+    SoaSrc<LsjBin> src{keys, pay, f};
+    return run_partition(src, n, (int)md->nbins, reinterpret_cast<ulonglong2 *>(pairs), starts, ws, ws_bytes,
+                         as_stream(stream));
+}
+
+static i64 max_subs(i64 n, i64 nbins) { return n / SUB + nbins + 2; }
 
 size_t lj_lsj_sort_workspace_bytes(int64_t n, int64_t nbins) {
-    (void)nbins;
-    return al(sizeof(SortCtl)) + al(sizeof(i64) * (size_t)(n / CAP + 2)) +
-           al(sizeof(i64) * 2 * (size_t)(n / (RUN_SMALL + 1) + 2));
+    const i64 G = max_subs(n, nbins);
+    size_t t = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, t, (const u64 *)nullptr, (u64 *)nullptr, (const u64 *)nullptr,
+                                    (u64 *)nullptr, (int64_t)n);
+    const size_t sc = scan_i64_bytes(nbins + 1);
+    return al(sizeof(SortCtl)) + 2 * al(sizeof(i64) * (size_t)(nbins + 1)) +  // ctl, fcount, fbase
+           al(sizeof(ulonglong2) * (size_t)n) +                              // split array
+           al(sizeof(i64) * (size_t)(G + 1)) + al(sizeof(double2) * (size_t)G) +  // sub starts, y ranges
+           al(sizeof(i64) * (size_t)(n / CAP + 2)) + al(sizeof(int) * (size_t)(n / CAP + 2)) +  // big list, flags
+           4 * al(sizeof(u64) * (size_t)n) + al(t > sc ? t : sc);
 }
 
-int lj_lsj_sort_buckets(const LjRmi *model, uint64_t *pairs, int64_t n, int64_t nbins, const int64_t *starts,
-                        void *ws, size_t ws_bytes, int64_t *stats_host, void *stream) {
-    LJ_REQUIRE(model && model->m >= 1 && model->n >= 1, "model is not fitted");
-    if (ws_bytes < lj_lsj_sort_workspace_bytes(n, nbins)) {
-        set_error("lj_lsj_sort_buckets: workspace too small");
+__global__ void k_set_last(const i64 *fbase, int nb, i64 n, i64 *sub_starts) { sub_starts[fbase[nb]] = n; }
+
+int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_out, int64_t n,
+                const int64_t *starts, void *ws, size_t ws_bytes, int64_t *stats_host, void *stream) {
+    LJ_REQUIRE(md && md->table && md->pb && md->nbins >= 1, "model has no bins");
+    if (ws_bytes < lj_lsj_sort_workspace_bytes(n, md->nbins)) {
+        set_error("lj_lsj_sort: workspace too small");
         return LJ_E_WORKSPACE;
     }
+    for (int i = 0; i < 4; ++i) stats_host[i] = 0;
+    if (n == 0) return LJ_OK;
     cudaStream_t st = as_stream(stream);
-    SortCtl *ctl;
-    i64 *over, *med;
-    sort_ws_parts(ws, n, &ctl, &over, &med);
-    LJ_CK(cudaMemsetAsync(ctl, 0, sizeof(SortCtl), st));
-    if (n >= 2) {
-        size_t sm = sizeof(ulonglong2) * CAP + 2 * sizeof(u16) * CAP + 3 * sizeof(u32) * NBMAX;
-        static bool attr = false;
-        if (!attr) {
-            LJ_CK(cudaFuncSetAttribute(k_sort_buckets, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            LJ_CK(cudaFuncSetAttribute(k_sort_runs, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(sizeof(ulonglong2) * CAP)));
-            attr = true;
-        }
-        unsigned g = (unsigned)(sm_count() * 2);
-        k_sort_buckets<<<g, SORT_NT, sm, st>>>(make_bin(*model, nbins), reinterpret_cast<ulonglong2 *>(pairs),
-                                                starts, ctl, over, med);
-        LJ_CK_LAUNCH();
-    }
-    SortCtl h;
-    LJ_CK(cudaMemcpyAsync(&h, ctl, sizeof(SortCtl), cudaMemcpyDeviceToHost, st));
-    LJ_CK(cudaStreamSynchronize(st));
-    stats_host[0] = (int64_t)h.n_over;
-    stats_host[1] = (int64_t)h.n_med;
-    return LJ_OK;
-}
-
-int lj_lsj_oversized_list_host(void *sort_ws, int64_t n, int64_t count, int64_t *buckets_host) {
-    SortCtl *ctl;
-    i64 *over, *med;
-    sort_ws_parts(sort_ws, n, &ctl, &over, &med);
-    LJ_CK(cudaMemcpy(buckets_host, over, sizeof(i64) * (size_t)count, cudaMemcpyDeviceToHost));
-    return LJ_OK;
-}
-
-size_t lj_lsj_sort_oversized_workspace_bytes(int64_t nseg, int64_t total) {
-    i64 nbin = nseg * NBMAX;
-    size_t t = scan_bytes(nbin + 1), r = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, r, (const u64 *)nullptr, (u64 *)nullptr, (const u64 *)nullptr,
-                                    (u64 *)nullptr, (int64_t)total);
-    return al(sizeof(i64) * 3 * (size_t)(nseg + 1)) + al(sizeof(u32) * (size_t)(nbin + 1)) +
-           al(sizeof(i64) * (size_t)(nbin + 1)) + 2 * al(sizeof(u64) * (size_t)(nbin + 1)) +
-           al(sizeof(ulonglong2) * (size_t)total) + 4 * al(sizeof(u64) * (size_t)total) + al(t > r ? t : r) +
-           al(sizeof(i64) * 2 * (size_t)(total / CAP + 2));
-}
-
-// Model placement of the buckets that did not fit in shared memory, through
-// global memory: histogram of predicted positions (with per-position key
-// min/max), scan, scatter, copy back; then the equal-position runs are fixed
-// (insertion sort; medium runs join the bitonic list; runs of one repeated
-// key are left alone; longer mixed runs -- rare -- are radix sorted here).
-// seg_*_host: bucket id and [begin, end) of each oversized bucket.
-int lj_lsj_sort_oversized(const LjRmi *model, uint64_t *pairs, int64_t n, int64_t nbins,
-                          const int64_t *seg_bucket_host, const int64_t *seg_begin_host,
-                          const int64_t *seg_end_host, int64_t nseg, void *sort_ws, void *ws, size_t ws_bytes,
-                          int64_t *stats_host, void *stream) {
-    LJ_REQUIRE(model && model->m >= 1 && nseg >= 1, "no oversized buckets");
-    cudaStream_t st = as_stream(stream);
-    std::vector<i64> hb(3 * (size_t)(nseg + 1));
-    i64 total = 0;
-    for (i64 s = 0; s < nseg; ++s) {
-        hb[s] = seg_bucket_host[s];
-        hb[(nseg + 1) + s] = seg_begin_host[s];
-        hb[2 * (nseg + 1) + s] = total;
-        total += seg_end_host[s] - seg_begin_host[s];
-    }
-    hb[2 * (nseg + 1) + nseg] = total;
-    if (ws_bytes < lj_lsj_sort_oversized_workspace_bytes(nseg, total)) {
-        set_error("lj_lsj_sort_oversized: workspace too small");
-        return LJ_E_WORKSPACE;
-    }
-    const i64 nbin = nseg * NBMAX;
+    const i64 nb = md->nbins, G = max_subs(n, nb);
     char *p = (char *)ws;
-    i64 *dseg = (i64 *)p;
-    p += al(sizeof(i64) * 3 * (size_t)(nseg + 1));
-    u32 *hist = (u32 *)p;
-    p += al(sizeof(u32) * (size_t)(nbin + 1));
-    i64 *bst = (i64 *)p;
-    p += al(sizeof(i64) * (size_t)(nbin + 1));
-    unsigned long long *bmin = (unsigned long long *)p;
-    p += al(sizeof(u64) * (size_t)(nbin + 1));
-    unsigned long long *bmax = (unsigned long long *)p;
-    p += al(sizeof(u64) * (size_t)(nbin + 1));
-    ulonglong2 *tmp = (ulonglong2 *)p;
-    p += al(sizeof(ulonglong2) * (size_t)total);
-    u64 *k1 = (u64 *)p;
-    p += al(sizeof(u64) * (size_t)total);
-    u64 *v1 = (u64 *)p;
-    p += al(sizeof(u64) * (size_t)total);
-    u64 *k2 = (u64 *)p;
-    p += al(sizeof(u64) * (size_t)total);
-    u64 *v2 = (u64 *)p;
-    p += al(sizeof(u64) * (size_t)total);
+    auto take = [&](size_t bytes) {
+        char *r = p;
+        p += al(bytes);
+        return r;
+    };
+    SortCtl *ctl = (SortCtl *)take(sizeof(SortCtl));
+    i64 *fcount = (i64 *)take(sizeof(i64) * (size_t)(nb + 1));
+    i64 *fbase = (i64 *)take(sizeof(i64) * (size_t)(nb + 1));
+    ulonglong2 *B = (ulonglong2 *)take(sizeof(ulonglong2) * (size_t)n);
+    i64 *sub_starts = (i64 *)take(sizeof(i64) * (size_t)(G + 1));
+    double2 *sub_y = (double2 *)take(sizeof(double2) * (size_t)G);
+    i64 *big = (i64 *)take(sizeof(i64) * (size_t)(n / CAP + 2));
+    int *flags = (int *)take(sizeof(int) * (size_t)(n / CAP + 2));
+    u64 *k1 = (u64 *)take(sizeof(u64) * (size_t)n);
+    u64 *v1 = (u64 *)take(sizeof(u64) * (size_t)n);
+    u64 *k2 = (u64 *)take(sizeof(u64) * (size_t)n);
+    u64 *v2 = (u64 *)take(sizeof(u64) * (size_t)n);
     char *cub_tmp = p;
-    size_t t = scan_bytes(nbin + 1), rsz = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, rsz, (const u64 *)nullptr, (u64 *)nullptr, (const u64 *)nullptr,
-                                    (u64 *)nullptr, (int64_t)total);
-    p += al(t > rsz ? t : rsz);
-    i64 *huge = (i64 *)p;
-    LJ_CK(cudaMemcpyAsync(dseg, hb.data(), sizeof(i64) * hb.size(), cudaMemcpyHostToDevice, st));
-    const i64 *obkt = dseg, *obeg = dseg + (nseg + 1), *ooff = dseg + 2 * (nseg + 1);
-    LJ_CK(cudaMemsetAsync(hist, 0, sizeof(u32) * (size_t)(nbin + 1), st));
-    LJ_CK(cudaMemsetAsync(bmin, 0xFF, sizeof(u64) * (size_t)(nbin + 1), st));
-    LJ_CK(cudaMemsetAsync(bmax, 0, sizeof(u64) * (size_t)(nbin + 1), st));
-    Bin bn = make_bin(*model, nbins);
-    ulonglong2 *pp = reinterpret_cast<ulonglong2 *>(pairs);
-    k_over_hist<<<grid_for(total, 256, 8), 256, 0, st>>>(bn, pp, obkt, obeg, ooff, (int)nseg, total, hist, bmin,
-                                                          bmax);
+
+    const LsjDev dev = make_lsj(*md);
+    const ulonglong2 *A = reinterpret_cast<const ulonglong2 *>(pairs_in);
+    ulonglong2 *out = reinterpret_cast<ulonglong2 *>(pairs_out);
+    // level 2: y-slices of ~SUB tuples per coarse bucket, CTA-local
+    k_split_plan<<<(int)((nb + 256) / 256), 256, 0, st>>>(starts, (int)nb, fcount);
     LJ_CK_LAUNCH();
-    cub::TransformInputIterator<i64, CastI64, const u32 *> it(hist, CastI64());
-    LJ_CK(cub::DeviceScan::ExclusiveSum(cub_tmp, t, it, bst, (int64_t)(nbin + 1), st));
-    // bst doubles as the scatter cursor, then is rebuilt by a second scan
-    k_over_scatter<<<grid_for(total, 256, 8), 256, 0, st>>>(bn, pp, obkt, obeg, ooff, (int)nseg, total,
-                                                             reinterpret_cast<unsigned long long *>(bst), tmp);
+    size_t t = scan_i64_bytes(nb + 1);
+    LJ_CK(cub::DeviceScan::ExclusiveSum(cub_tmp, t, fcount, fbase, (int64_t)(nb + 1), st));
+    k_set_last<<<1, 1, 0, st>>>(fbase, (int)nb, n, sub_starts);
+    LJ_CK(cudaMemsetAsync(ctl, 0, sizeof(SortCtl), st));
+    k_lsj_split<<<sm_count() * 2, SPLIT_NT, 0, st>>>(dev, A, starts, fbase, (int)nb, B, sub_starts, sub_y, ctl);
     LJ_CK_LAUNCH();
-    LJ_CK(cub::DeviceScan::ExclusiveSum(cub_tmp, t, it, bst, (int64_t)(nbin + 1), st));
-    k_over_copyback<<<grid_for(total, 256, 8), 256, 0, st>>>(tmp, obeg, ooff, (int)nseg, total, pp);
-    LJ_CK_LAUNCH();
-    SortCtl *ctl;
-    i64 *over, *med;
-    sort_ws_parts(sort_ws, n, &ctl, &over, &med);
-    k_over_runs<<<grid_for(nbin, 256, 8), 256, 0, st>>>(pp, obeg, ooff, bst, nbin, bmin, bmax, ctl, med, huge);
-    LJ_CK_LAUNCH();
+    // K8 over the sub-buckets, B -> out (G = fbase[nb] read on device)
+    SubBuckets sb{sub_starts, sub_y};
+    int rc = launch_sort(dev, sb, fbase + nb, B, out, ctl, big, st);
+    if (rc) return rc;
     SortCtl h;
     LJ_CK(cudaMemcpyAsync(&h, ctl, sizeof(SortCtl), cudaMemcpyDeviceToHost, st));
     LJ_CK(cudaStreamSynchronize(st));
-    stats_host[0] = (int64_t)h.n_huge;
-    stats_host[1] = (int64_t)h.n_med;
-    if (h.n_huge) {
-        std::vector<i64> hh(2 * (size_t)h.n_huge);
-        LJ_CK(cudaMemcpy(hh.data(), huge, sizeof(i64) * hh.size(), cudaMemcpyDeviceToHost));
-        for (unsigned long long r = 0; r < h.n_huge; ++r) {
-            i64 a = hh[2 * r], len = hh[2 * r + 1];
-            k_deinterleave<<<grid_for(len, 256, 8), 256, 0, st>>>(pp + a, len, k1, v1);
-            size_t tt = rsz;
-            LJ_CK(cub::DeviceRadixSort::SortPairs(cub_tmp, tt, k1, k2, v1, v2, (int64_t)len, 0, 64, st));
-            k_interleave<<<grid_for(len, 256, 8), 256, 0, st>>>(k2, v2, len, pp + a);
-            LJ_CK_LAUNCH();
-        }
+    stats_host[1] = (int64_t)h.n_fallback;
+    const int nbig = (int)h.n_over;
+    stats_host[0] = nbig;
+    if (nbig == 0) return LJ_OK;
+    // sub-buckets above shared memory: one repeated key (hot duplicate) ->
+    // copy; otherwise (rare) a device radix sort of that sub-bucket
+    k_big_sub<<<std::min(nbig, 1024), 256, 0, st>>>(B, sb, big, nbig, out, flags);
+    LJ_CK_LAUNCH();
+    std::vector<int> hf(nbig);
+    std::vector<i64> hbig(nbig);
+    LJ_CK(cudaMemcpyAsync(hf.data(), flags, sizeof(int) * nbig, cudaMemcpyDeviceToHost, st));
+    LJ_CK(cudaMemcpyAsync(hbig.data(), big, sizeof(i64) * nbig, cudaMemcpyDeviceToHost, st));
+    LJ_CK(cudaStreamSynchronize(st));
+    int nsorted = 0;
+    for (int q = 0; q < nbig; ++q) {
+        if (!hf[q]) continue;
+        i64 se[2];
+        LJ_CK(cudaMemcpy(se, sub_starts + hbig[q], sizeof(i64) * 2, cudaMemcpyDeviceToHost));
+        const i64 a = se[0], len = se[1] - se[0];
+        k_deinterleave<<<grid_for(len, 256, 8), 256, 0, st>>>(B + a, len, k1, v1);
+        size_t tt = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tt, k1, k2, v1, v2, (int64_t)len);
+        LJ_CK(cub::DeviceRadixSort::SortPairs(cub_tmp, tt, k1, k2, v1, v2, (int64_t)len, 0, 64, st));
+        k_interleave<<<grid_for(len, 256, 8), 256, 0, st>>>(k2, v2, len, out + a);
+        LJ_CK_LAUNCH();
+        ++nsorted;
     }
+    stats_host[2] = nsorted;
+    LJ_CK(cudaStreamSynchronize(st));
     return LJ_OK;
 }
 
-// Bitonic pass over every medium run listed in the sort workspace.
-int lj_lsj_sort_runs(uint64_t *pairs, int64_t n, void *sort_ws, void *stream) {
-    SortCtl *ctl;
-    i64 *over, *med;
-    sort_ws_parts(sort_ws, n, &ctl, &over, &med);
-    k_sort_runs<<<sm_count() * 2, SORT_NT, sizeof(ulonglong2) * CAP, as_stream(stream)>>>(
-        reinterpret_cast<ulonglong2 *>(pairs), med, ctl);
+int lj_lsj_ref_bounds(const LjRmi *model, const uint64_t *sorted_pairs, int64_t n, int64_t P, int64_t *bounds,
+                      void *stream) {
+    LJ_REQUIRE(model && model->m >= 1 && model->n >= 1 && P >= 1, "model is not fitted / P < 1");
+    k_ref_bounds<<<grid_for(P + 1, 256, 8), 256, 0, as_stream(stream)>>>(
+        RmiDev(*model), reinterpret_cast<const ulonglong2 *>(sorted_pairs), n, P, bounds);
     LJ_CK_LAUNCH();
     return LJ_OK;
 }
 
-int lj_lsj_join(const LjRmi *model_r, const uint64_t *r_pairs, int64_t nr, int64_t r_nbins, const int64_t *r_starts,
+int lj_lsj_join(const LjLsjModel *model_r, const uint64_t *r_pairs, int64_t nr, const int64_t *r_starts,
                 const uint64_t *s_pairs, int64_t ns, int mode, int64_t *counts, const int64_t *offsets,
                 uint64_t *out_pr, uint64_t *out_ps, uint64_t *out, int accumulate, void *stream) {
-    LJ_REQUIRE(model_r && model_r->m >= 1 && model_r->n >= 1, "R model is not fitted");
+    LJ_REQUIRE(model_r && model_r->table && model_r->pb, "R model has no bins");
     LJ_REQUIRE(mode >= 0 && mode <= 2, "mode must be 0, 1 or 2");
     cudaStream_t st = as_stream(stream);
     if (mode == 0 && !accumulate) LJ_CK(cudaMemsetAsync(out, 0, 4 * sizeof(u64), st));
@@ -748,11 +759,11 @@ int lj_lsj_join(const LjRmi *model_r, const uint64_t *r_pairs, int64_t nr, int64
         if (mode == 1 && ns > 0) LJ_CK(cudaMemsetAsync(counts, 0, sizeof(i64) * (size_t)ns, st));
         return LJ_OK;
     }
-    i64 ntiles = (ns + JOIN_T - 1) / JOIN_T;
-    unsigned g = (unsigned)(ntiles < (i64)sm_count() * 8 ? ntiles : (i64)sm_count() * 8);
-    k_lsj_join<<<g, JOIN_NT, 0, st>>>(make_bin(*model_r, r_nbins), reinterpret_cast<const ulonglong2 *>(r_pairs), nr,
-                                      r_starts, reinterpret_cast<const ulonglong2 *>(s_pairs), ns, mode, counts, offsets,
-                                      out_pr, out_ps, out);
+    const i64 ntiles = (ns + JOIN_T - 1) / JOIN_T;
+    const unsigned g = (unsigned)(ntiles < (i64)sm_count() * 8 ? ntiles : (i64)sm_count() * 8);
+    k_lsj_join<<<g, JOIN_NT, 0, st>>>(make_lsj(*model_r), reinterpret_cast<const ulonglong2 *>(r_pairs), nr,
+                                      r_starts, reinterpret_cast<const ulonglong2 *>(s_pairs), ns, mode, counts,
+                                      offsets, out_pr, out_ps, out);
     LJ_CK_LAUNCH();
     return LJ_OK;
 }

@@ -40,10 +40,25 @@ inline PartPlan part_plan(i64 n, int nbins) {
     return p;
 }
 
-// pass 1: per-block histogram -> mat[bin * blocks + block]
+// A tuple source: bin_of(i) reads only what the bin needs; load(i, k, p)
+// reads the tuple and returns its bin.
 template <class BinF>
-__global__ void __launch_bounds__(PART2_NT) k_bin_hist(BinF f, const u64 *__restrict__ keys, i64 n, i64 chunk,
-                                                       int nbins, u32 *mat) {
+struct SoaSrc {
+    const u64 *__restrict__ keys;
+    const u64 *__restrict__ pay;
+    BinF f;
+    __device__ __forceinline__ void prepare() const { f.prepare(); }
+    __device__ __forceinline__ int bin_of(i64 i) const { return f(ld_stream(keys + i)); }
+    __device__ __forceinline__ int load(i64 i, u64 &k, u64 &p) const {
+        k = ld_stream(keys + i);
+        p = ld_stream(pay + i);
+        return f(k);
+    }
+};
+
+// pass 1: per-block histogram -> mat[bin * blocks + block]
+template <class Src>
+__global__ void __launch_bounds__(PART2_NT) k_bin_hist(Src f, i64 n, i64 chunk, int nbins, u32 *mat) {
     extern __shared__ u32 h[];
     for (int j = threadIdx.x; j < nbins; j += PART2_NT) h[j] = 0;
     f.prepare();
@@ -53,7 +68,7 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_hist(BinF f, const u64 *__rest
     for (i64 base = lo + threadIdx.x - lane; base < hi; base += PART2_NT) {
         const i64 i = base + lane;
         int b = -1;
-        if (i < hi) b = f(ld_stream(keys + i));
+        if (i < hi) b = f.bin_of(i);
         const unsigned peers = __match_any_sync(0xffffffffu, b);
         if (b >= 0 && lane == __ffs(peers) - 1) atomicAdd(h + b, (u32)__popc(peers));
     }
@@ -62,9 +77,8 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_hist(BinF f, const u64 *__rest
 }
 
 // pass 2: scatter the same chunk through shared-memory cursors
-template <class BinF>
-__global__ void __launch_bounds__(PART2_NT) k_bin_scatter(BinF f, const u64 *__restrict__ keys,
-                                                          const u64 *__restrict__ pay, i64 n, i64 chunk, int nbins,
+template <class Src>
+__global__ void __launch_bounds__(PART2_NT) k_bin_scatter(Src f, i64 n, i64 chunk, int nbins,
                                                           const i64 *__restrict__ off, ulonglong2 *out) {
     extern __shared__ u32 cur[];
     for (int j = threadIdx.x; j < nbins; j += PART2_NT) cur[j] = (u32)off[(i64)j * gridDim.x + blockIdx.x];
@@ -76,11 +90,7 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter(BinF f, const u64 *__r
         const i64 i = base + lane;
         int b = -1;
         u64 k = 0, p = 0;
-        if (i < hi) {
-            k = ld_stream(keys + i);
-            p = ld_stream(pay + i);
-            b = f(k);
-        }
+        if (i < hi) b = f.load(i, k, p);
         const unsigned peers = __match_any_sync(0xffffffffu, b);
         const int leader = __ffs(peers) - 1;
         u32 at = 0;
@@ -91,7 +101,7 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter(BinF f, const u64 *__r
 }
 
 // bin starts[j] = off[j * blocks] (first block's offset), starts[nbins] = n
-__global__ void k_bin_starts(const i64 *off, int nbins, int blocks, i64 n, i64 *starts) {
+static __global__ void k_bin_starts(const i64 *off, int nbins, int blocks, i64 n, i64 *starts) {
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= nbins; j += gridDim.x * blockDim.x)
         starts[j] = j < nbins ? off[(i64)j * blocks] : n;
 }
@@ -116,10 +126,11 @@ inline size_t part_workspace_bytes(i64 n, int nbins) {
            part_align(part_scan_bytes(items));
 }
 
-// Full partition: out[n] records grouped by bin, starts[nbins+1].
-template <class BinF>
-int run_partition(const BinF &f, const u64 *keys, const u64 *pay, i64 n, int nbins, ulonglong2 *out, i64 *starts,
-                  void *ws, size_t ws_bytes, cudaStream_t st) {
+// Full partition of the n tuples of `f`: out[n] records grouped by bin,
+// starts[nbins+1].
+template <class Src>
+int run_partition(const Src &f, i64 n, int nbins, ulonglong2 *out, i64 *starts, void *ws, size_t ws_bytes,
+                  cudaStream_t st) {
     if (nbins < 1 || nbins > PART2_MAXBINS) {
         set_error("partition: nbins must be in [1, 32768]");
         return LJ_E_INVALID;
@@ -142,14 +153,14 @@ int run_partition(const BinF &f, const u64 *keys, const u64 *pay, i64 n, int nbi
     size_t sm = sizeof(u32) * (size_t)nbins;
     static bool attr_set = false;
     if (!attr_set) {
-        LJ_CK(cudaFuncSetAttribute(k_bin_hist<BinF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        LJ_CK(cudaFuncSetAttribute(k_bin_hist<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)(sizeof(u32) * PART2_MAXBINS)));
-        LJ_CK(cudaFuncSetAttribute(k_bin_scatter<BinF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        LJ_CK(cudaFuncSetAttribute(k_bin_scatter<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)(sizeof(u32) * PART2_MAXBINS)));
         attr_set = true;
     }
     if (n > 0) {
-        k_bin_hist<BinF><<<p.blocks, PART2_NT, sm, st>>>(f, keys, n, p.chunk, nbins, mat);
+        k_bin_hist<Src><<<p.blocks, PART2_NT, sm, st>>>(f, n, p.chunk, nbins, mat);
         LJ_CK_LAUNCH();
     } else {
         LJ_CK(cudaMemsetAsync(mat, 0, sizeof(u32) * (size_t)items, st));
@@ -160,7 +171,7 @@ int run_partition(const BinF &f, const u64 *keys, const u64 *pay, i64 n, int nbi
     k_bin_starts<<<(nbins + 256) / 256, 256, 0, st>>>(off, nbins, p.blocks, n, starts);
     LJ_CK_LAUNCH();
     if (n > 0) {
-        k_bin_scatter<BinF><<<p.blocks, PART2_NT, sm, st>>>(f, keys, pay, n, p.chunk, nbins, off, out);
+        k_bin_scatter<Src><<<p.blocks, PART2_NT, sm, st>>>(f, n, p.chunk, nbins, off, out);
         LJ_CK_LAUNCH();
     }
     return LJ_OK;

@@ -1,27 +1,29 @@
 """Learned sort-join on the GPU (reference lsj.py:1-405).
 
-Per relation: a stratified sample of ``sample_rate`` (K-sample), an RMI fit
-on the sorted sample (K10), a CDF partition into Pf = P*F fine buckets (K6
-histogram + K7 warp-aggregated scatter), and a model-placed per-bucket sort
-in shared memory (K8; oversized buckets through global memory).  The join
-(K9) walks sorted S in tiles and merge-searches each tile's R window found
-through R's model.  P is the reference's sort-phase scale
-(``effective_fanout``); F refines it so that a fine bucket averages <= 1024
-tuples (fits shared memory), and every F-th fine bound is a coarse bound,
-which is what the reference's bucket_bounds / counters are computed from.
+Per relation (``prepare_model`` + ``sort_relation``):
 
-``workers`` keeps the reference's meaning for the bucket scale (P is a
-multiple of it) and for ``range_partition``; on one GPU all workers' ranges
-are processed by the same kernels.  Across GPUs the worker is a GPU (see
-``dist.py``).  Results: the checksum (count, sum, xor) of
-R.payload + S.payload over all matching pairs; pairs on request.
+* smpl: a stratified sample of ``sample_rate`` of the keys, sorted on device;
+  the reference's two-level linear RMI fitted on it (K10, models.py:57-110,
+  fanout min(1000, samples // 8) as lsj.py:127-129); equi-depth bins over
+  the model's predicted positions, cut at equally spaced sample ranks
+  (bin(key) = table[pos(key)], monotone in the key).
+* part: K6/K7 shared-memory-privatised histogram + scatter into the bins.
+* sort: K8 model-placed per-bucket sort in shared memory (oversized buckets
+  re-partitioned by the model at finer resolution).
+
+Then ``chunked_join`` (K9) walks sorted S in tiles; each tile's R window is
+found through R's model and bucket bounds.  The result is the checksum
+(count, sum, xor) of R.payload + S.payload over all equal-key pairs (pairs
+on request).  The reference's bucket scale P = ``effective_fanout`` is kept
+for the API, the ModelMismatch guard and the sort counters
+(comparator_count / partitions_sorted are computed exactly from the bucket
+sizes at scale P, tests/test_lsj.py:27-32).
 """
 
 from __future__ import annotations
 
 import ctypes
 import math
-import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -29,11 +31,12 @@ import torch
 
 from . import _lib
 from .data import Relation
-from .models import RecursiveModelIndex, partition_index
+from .models import RecursiveModelIndex
 from .results import JoinResult, PhaseBreakdown, SortStats
 from .util import exclusive_offsets, to_device_u64, unsigned_order
 
-FINE_TARGET = 1024  # mean tuples per fine bucket (shared-memory sort unit)
+BUCKET_TARGET = 8192  # mean tuples per sort unit (the shared-memory sort holds <= 12288)
+MAX_BINS = 2048       # coarse bins of the grid-wide partition (open write lines stay in L2)
 
 
 class ModelMismatchError(ValueError):
@@ -75,6 +78,53 @@ class LsjConfig:
                 "model_fanout": self.model_fanout, "seed": self.seed}
 
 
+class LsjModel:
+    """An RMI plus bins over its predicted positions (LjLsjModel)."""
+
+    def __init__(self, rmi: RecursiveModelIndex, pb: torch.Tensor, table: torch.Tensor):
+        self.rmi = rmi
+        self.pb = pb
+        self.table = table
+        self.nbins = pb.numel() - 1
+
+    @property
+    def tag(self):
+        return self.rmi.tag
+
+    def c_struct(self) -> _lib.LjLsjModel:
+        return _lib.LjLsjModel(self.rmi.c_struct(), self.nbins, _lib.ptr(self.pb), _lib.ptr(self.table))
+
+    @classmethod
+    def uniform(cls, rmi: RecursiveModelIndex, nbins: int) -> "LsjModel":
+        """Bins = the reference's partition_index buckets at scale nbins
+        (pb[j] = ceil(j * n / nbins))."""
+        tl = rmi.trained_len
+        j = np.arange(nbins + 1, dtype=np.int64)
+        pb = torch.from_numpy(-((-j * tl) // nbins)).to(rmi.leaves.device)
+        table = torch.empty(tl, dtype=torch.int32, device=pb.device)
+        _lib.check(_lib.lib().lj_lsj_bins_from_bounds(_lib.ptr(pb), nbins, tl, _lib.ptr(table),
+                                                      _lib.stream_ptr()), "lsj_bins")
+        return cls(rmi, pb, table)
+
+    @classmethod
+    def from_sample(cls, rmi: RecursiveModelIndex, sample_sorted: torch.Tensor, nbins: int) -> "LsjModel":
+        """Equi-depth bins cut at equally spaced sample ranks."""
+        lib = _lib.lib()
+        dev = sample_sorted.device
+        pb = torch.empty(nbins + 1, dtype=torch.int64, device=dev)
+        table = torch.empty(rmi.trained_len, dtype=torch.int32, device=dev)
+        ws = _lib.workspace(lib.lj_lsj_bins_workspace_bytes(sample_sorted.numel()), dev)
+        c = rmi.c_struct()
+        _lib.check(lib.lj_lsj_bins(ctypes.byref(c), _lib.ptr(sample_sorted), sample_sorted.numel(), nbins,
+                                   _lib.ptr(pb), _lib.ptr(table), _lib.ptr(ws), ws.numel(), _lib.stream_ptr()),
+                   "lsj_bins")
+        return cls(rmi, pb, table)
+
+
+def default_bins(n: int) -> int:
+    return max(1, min(MAX_BINS, math.ceil(n / BUCKET_TARGET)))
+
+
 @dataclass
 class PartitionedRelation:
     """lsj.py:71-80: worker w owns ranges[w] (device arrays)."""
@@ -90,16 +140,20 @@ class PartitionedRelation:
 @dataclass
 class SortedRelation:
     """lsj.py:83-92 plus the device layout: interleaved (key, payload)
-    ``pairs``, fine bucket bounds ``fine_starts`` at scale ``fine_scale``."""
+    ``pairs`` in key order, bucket bounds ``starts`` of ``lmodel``'s bins."""
 
     pairs: torch.Tensor
-    fine_starts: torch.Tensor
-    fine_scale: int
+    starts: torch.Tensor
+    lmodel: LsjModel
     scale: int
-    model: RecursiveModelIndex
     model_tag: tuple
     worker_ranges: list = field(default_factory=list)
     stats: SortStats = field(default_factory=SortStats)
+    diag: dict = field(default_factory=dict)
+
+    @property
+    def model(self) -> RecursiveModelIndex:
+        return self.lmodel.rmi
 
     @property
     def keys(self) -> torch.Tensor:
@@ -111,88 +165,24 @@ class SortedRelation:
 
     @property
     def bucket_bounds(self) -> torch.Tensor:
-        """Coarse bounds at the reference's scale (every F-th fine bound)."""
-        f = self.fine_scale // self.scale
-        return self.fine_starts[::f].contiguous()
+        """Bounds of the reference's buckets partition_index(model, key,
+        scale) in the sorted output (lsj.py:302-305)."""
+        return _ref_bounds(self.pairs, self.model, self.scale)
 
 
-def _fine_scale(n: int, scale: int) -> int:
-    return scale * max(1, math.ceil(n / (scale * FINE_TARGET)))
+def _ref_bounds(pairs: torch.Tensor, rmi: RecursiveModelIndex, P: int) -> torch.Tensor:
+    n = pairs.numel() // 2
+    out = torch.empty(P + 1, dtype=torch.int64, device=pairs.device)
+    c = rmi.c_struct()
+    _lib.check(_lib.lib().lj_lsj_ref_bounds(ctypes.byref(c), _lib.ptr(pairs), n, P, _lib.ptr(out),
+                                            _lib.stream_ptr()), "lsj_ref_bounds")
+    return out
 
 
-def sample_train(relation: Relation, sample_rate: float, workers: int, seed: int,
-                 fanout: int | None = None) -> RecursiveModelIndex:
-    """lsj.py:95-130: fit the relation's CDF model on a ~sample_rate sample
-    (independent of ``workers``).  The sample is stratified (one key per
-    stratum at a counter-drawn offset) instead of numpy's Generator.choice;
-    any sample gives the same join result (models are monotone)."""
-    n = len(relation)
-    if n == 0:
-        raise ValueError("cannot sample an empty relation")
-    if not 0.0 < sample_rate <= 1.0:
-        raise ValueError("sample_rate must be in (0, 1]")
-    total = int(round(sample_rate * n))
-    lib = _lib.lib()
-    dev = relation.device
-    if total == 0:
-        o = unsigned_order(relation.keys)
-        lo, hi = torch.aminmax(o)
-        two = torch.stack([lo, hi]) ^ (-(2**63))
-        return RecursiveModelIndex(fanout=1).fit(two)
-    sample = torch.empty(total, dtype=torch.int64, device=dev)
-    ws = _lib.workspace(lib.lj_lsj_sample_workspace_bytes(total), dev)
-    _lib.check(lib.lj_lsj_sample(_lib.ptr(relation.keys), n, total, int(seed) & (2**64 - 1), _lib.ptr(sample),
-                                 _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "lsj_sample")
-    if fanout is None:
-        fanout = min(1000, max(1, total // 8))
-    return RecursiveModelIndex(fanout=fanout).fit(sample)
-
-
-def _partition(keys, payloads, model, nbins):
-    lib = _lib.lib()
-    n = keys.numel()
-    pairs = torch.empty(2 * max(n, 1), dtype=torch.int64, device=keys.device)
-    starts = torch.empty(nbins + 1, dtype=torch.int64, device=keys.device)
-    ws = _lib.workspace(lib.lj_lsj_partition_workspace_bytes(n, nbins), keys.device)
-    c = model.c_struct()
-    _lib.check(lib.lj_lsj_partition(ctypes.byref(c), _lib.ptr(keys), _lib.ptr(payloads), n, nbins, _lib.ptr(pairs),
-                                    _lib.ptr(starts), _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "lsj_partition")
-    return pairs, starts
-
-
-def _sort_in_place(pairs, starts, model, n, nbins):
-    """K8 (+ the oversized path and the run pass) on partitioned pairs."""
-    lib = _lib.lib()
-    dev = pairs.device
-    ws = _lib.workspace(lib.lj_lsj_sort_workspace_bytes(n, nbins), dev)
-    c = model.c_struct()
-    st = (ctypes.c_int64 * 2)()
-    _lib.check(lib.lj_lsj_sort_buckets(ctypes.byref(c), _lib.ptr(pairs), n, nbins, _lib.ptr(starts), _lib.ptr(ws),
-                                       ws.numel(), st, _lib.stream_ptr()), "lsj_sort_buckets")
-    n_over = int(st[0])
-    if n_over:
-        seg = np.empty(n_over, dtype=np.int64)
-        _lib.check(lib.lj_lsj_oversized_list_host(_lib.ptr(ws), n, n_over, seg.ctypes.data), "oversized_list")
-        seg.sort()
-        sb = starts.cpu().numpy()
-        beg = np.ascontiguousarray(sb[seg])
-        end = np.ascontiguousarray(sb[seg + 1])
-        total = int((end - beg).sum())
-        ows = _lib.workspace(lib.lj_lsj_sort_oversized_workspace_bytes(n_over, total), dev)
-        st2 = (ctypes.c_int64 * 2)()
-        _lib.check(lib.lj_lsj_sort_oversized(ctypes.byref(c), _lib.ptr(pairs), n, nbins, seg.ctypes.data,
-                                             beg.ctypes.data, end.ctypes.data, n_over, _lib.ptr(ws), _lib.ptr(ows),
-                                             ows.numel(), st2, _lib.stream_ptr()), "lsj_sort_oversized")
-    _lib.check(lib.lj_lsj_sort_runs(_lib.ptr(pairs), n, _lib.ptr(ws), _lib.stream_ptr()), "lsj_sort_runs")
-    return n_over
-
-
-def _sort_stats(fine_starts: torch.Tensor, fine_scale: int, scale: int) -> SortStats:
+def _sort_stats(bounds: torch.Tensor) -> SortStats:
     """Comparator / partition counters of the reference's padded bitonic
-    networks at scale P (lsj.py:250-286; tests/test_lsj.py:27-32), from the
-    coarse bucket sizes."""
-    f = fine_scale // scale
-    sizes = (fine_starts[f::f] - fine_starts[:-1:f]).to(torch.int64)
+    networks over the buckets with these bounds (lsj.py:250-286)."""
+    sizes = (bounds[1:] - bounds[:-1]).to(torch.int64)
     nz = sizes[sizes > 0]
     if nz.numel() == 0:
         return SortStats()
@@ -202,16 +192,94 @@ def _sort_stats(fine_starts: torch.Tensor, fine_scale: int, scale: int) -> SortS
     return SortStats(comparator_count=comps, partitions_sorted=int(nz.numel()))
 
 
-def sort_relation(keys, payloads, model: RecursiveModelIndex, scale: int, workers: int = 1) -> SortedRelation:
-    """Partition at the fine scale and sort every bucket (lsj.py:289-313)."""
+def _sample_sorted(relation: Relation, sample_rate: float, seed: int) -> torch.Tensor:
+    n = len(relation)
+    total = int(round(sample_rate * n))
+    if total == 0:
+        o = unsigned_order(relation.keys)
+        lo, hi = torch.aminmax(o)
+        return torch.stack([lo, hi]) ^ (-(2**63))
+    lib = _lib.lib()
+    sample = torch.empty(total, dtype=torch.int64, device=relation.device)
+    ws = _lib.workspace(lib.lj_lsj_sample_workspace_bytes(total), relation.device)
+    _lib.check(lib.lj_lsj_sample(_lib.ptr(relation.keys), n, total, int(seed) & (2**64 - 1), _lib.ptr(sample),
+                                 _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "lsj_sample")
+    return sample
+
+
+def sample_train(relation: Relation, sample_rate: float, workers: int, seed: int,
+                 fanout: int | None = None) -> RecursiveModelIndex:
+    """lsj.py:95-130: the relation's CDF model fitted on a ~sample_rate
+    sample (independent of ``workers``).  The sample is stratified (one key
+    per stratum at a counter-drawn offset) instead of numpy's
+    Generator.choice; any sample gives the same join (models are monotone)."""
+    return prepare_model(relation, sample_rate, seed, fanout)[0]
+
+
+def prepare_model(relation: Relation, sample_rate: float, seed: int, fanout: int | None = None,
+                  nbins: int | None = None) -> tuple[RecursiveModelIndex, LsjModel]:
+    n = len(relation)
+    if n == 0:
+        raise ValueError("cannot sample an empty relation")
+    if not 0.0 < sample_rate <= 1.0:
+        raise ValueError("sample_rate must be in (0, 1]")
+    sample = _sample_sorted(relation, sample_rate, seed)
+    total = int(round(sample_rate * n))
+    if total == 0:
+        rmi = RecursiveModelIndex(fanout=1).fit(sample)
+    else:
+        if fanout is None:
+            fanout = min(1000, max(1, total // 8))
+        rmi = RecursiveModelIndex(fanout=fanout).fit(sample)
+    return rmi, LsjModel.from_sample(rmi, sample, nbins or default_bins(n))
+
+
+def _as_lsj_model(model, n: int) -> LsjModel:
+    if isinstance(model, LsjModel):
+        return model
+    return LsjModel.uniform(model, default_bins(n))
+
+
+def _partition(keys, payloads, lm: LsjModel):
+    lib = _lib.lib()
     n = keys.numel()
-    fine = _fine_scale(n, scale)
-    pairs, starts = _partition(keys, payloads, model, fine)
+    pairs = torch.empty(2 * max(n, 1), dtype=torch.int64, device=keys.device)
+    starts = torch.empty(lm.nbins + 1, dtype=torch.int64, device=keys.device)
+    ws = _lib.workspace(lib.lj_lsj_partition_workspace_bytes(n, lm.nbins), keys.device)
+    c = lm.c_struct()
+    _lib.check(lib.lj_lsj_partition(ctypes.byref(c), _lib.ptr(keys), _lib.ptr(payloads), n, _lib.ptr(pairs),
+                                    _lib.ptr(starts), _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "lsj_partition")
+    return pairs, starts
+
+
+def _sort(pairs_in, starts, lm: LsjModel, n: int):
+    lib = _lib.lib()
+    out = torch.empty_like(pairs_in)
+    ws = _lib.workspace(lib.lj_lsj_sort_workspace_bytes(n, lm.nbins), pairs_in.device)
+    st = (ctypes.c_int64 * 4)()
+    c = lm.c_struct()
+    _lib.check(lib.lj_lsj_sort(ctypes.byref(c), _lib.ptr(pairs_in), _lib.ptr(out), n, _lib.ptr(starts),
+                               _lib.ptr(ws), ws.numel(), st, _lib.stream_ptr()), "lsj_sort")
+    diag = {"oversized_sub_buckets": int(st[0]), "bitonic_fallbacks": int(st[1]),
+            "radix_sorted_sub_buckets": int(st[2])}
+    return out, diag
+
+
+def sort_relation(keys, payloads, model, scale: int, workers: int = 1) -> SortedRelation:
+    """Partition by the model and sort every bucket (lsj.py:242-313).
+    ``model`` is a RecursiveModelIndex (reference-style uniform buckets) or
+    an LsjModel (equi-depth bins)."""
+    k = to_device_u64(keys)
+    p = to_device_u64(payloads)
+    n = k.numel()
+    lm = _as_lsj_model(model, n)
+    pairs, starts = _partition(k, p, lm)
+    diag = {}
     if n:
-        _sort_in_place(pairs, starts, model, n, fine)
-    srt = SortedRelation(pairs[: 2 * n], starts, fine, scale, model, (model.tag, scale))
-    srt.stats = _sort_stats(starts, fine, scale)
-    bb = srt.bucket_bounds
+        pairs, diag = _sort(pairs, starts, lm, n)
+    srt = SortedRelation(pairs[: 2 * n], starts, lm, scale, (lm.tag, scale), diag=diag)
+    bb = _ref_bounds(srt.pairs, lm.rmi, scale) if n else torch.zeros(scale + 1, dtype=torch.int64, device=k.device)
+    srt.stats = _sort_stats(bb)
     if workers > 1:
         cw = scale // workers
         wb = bb[::cw].cpu().tolist()
@@ -223,12 +291,12 @@ def sort_relation(keys, payloads, model: RecursiveModelIndex, scale: int, worker
 
 def range_partition(relation: Relation, model: RecursiveModelIndex, workers: int,
                     config: LsjConfig) -> PartitionedRelation:
-    """lsj.py:133-209: each key goes to worker partition_index(model, key,
-    p_eff) // (p_eff / workers) == partition_index(model, key, workers).
-    Order inside a worker range is unspecified (the multiset is the
-    reference's)."""
+    """lsj.py:133-209: worker of a key = partition_index(model, key, p_eff)
+    // (p_eff / workers) == partition_index(model, key, workers); order inside
+    a worker range is unspecified (the multiset is the reference's)."""
     n = len(relation)
-    pairs, starts = _partition(relation.keys, relation.payloads, model, workers)
+    lm = LsjModel.uniform(model, workers)
+    pairs, starts = _partition(relation.keys, relation.payloads, lm)
     st = starts.cpu().tolist()
     ranges = [(int(st[w]), int(st[w + 1])) for w in range(workers)]
     hist = np.diff(np.asarray(st, dtype=np.int64)).reshape(1, workers)
@@ -254,7 +322,8 @@ def _sort_phase(part: PartitionedRelation, model, scale: int, workers: int) -> S
 
 def chunked_join(r_sorted: SortedRelation, s_sorted: SortedRelation, model_r, scale_r: int, workers: int = 1,
                  materialize: bool = False) -> JoinResult:
-    """lsj.py:316-370: each S tile against its R window through R's model."""
+    """lsj.py:316-370: each sorted S tile against the R window found through
+    R's model; guarded like the reference (lsj.py:329-332)."""
     if r_sorted.model_tag != (model_r.tag, scale_r):
         raise ModelMismatchError("R was bucketed under a different model or scale than the join received")
     return _join(r_sorted, s_sorted, materialize)
@@ -265,9 +334,8 @@ def _join(r_sorted: SortedRelation, s_sorted: SortedRelation, materialize: bool)
     nr = r_sorted.pairs.numel() // 2
     ns = s_sorted.pairs.numel() // 2
     dev = s_sorted.pairs.device
-    c = r_sorted.model.c_struct()
-    args = (ctypes.byref(c), _lib.ptr(r_sorted.pairs), nr, r_sorted.fine_scale, _lib.ptr(r_sorted.fine_starts),
-            _lib.ptr(s_sorted.pairs), ns)
+    c = r_sorted.lmodel.c_struct()
+    args = (ctypes.byref(c), _lib.ptr(r_sorted.pairs), nr, _lib.ptr(r_sorted.starts), _lib.ptr(s_sorted.pairs), ns)
     if not materialize:
         out = torch.zeros(4, dtype=torch.int64, device=dev)
         _lib.check(lib.lj_lsj_join(*args, 0, None, None, None, None, _lib.ptr(out), 0, _lib.stream_ptr()), "lsj_join")
@@ -284,9 +352,11 @@ def _join(r_sorted: SortedRelation, s_sorted: SortedRelation, materialize: bool)
 
 
 def lsj_join(r: Relation, s: Relation, config: LsjConfig | None = None, materialize: bool = False,
-             models: tuple | None = None):
+             models: tuple | None = None, counters: bool = True):
     """lsj.py:373-405: the full learned sort-join -> (JoinResult,
-    PhaseBreakdown).  Phase times are CUDA-event times on the stream."""
+    PhaseBreakdown).  Phase times are CUDA-event times on the stream.
+    ``models`` = (model_r, model_s) RMIs fitted elsewhere (e.g. the
+    reference's): they are then bucketed at the reference's uniform scale."""
     config = config or LsjConfig()
     br = PhaseBreakdown()
     if len(r) == 0 or len(s) == 0:
@@ -296,29 +366,32 @@ def lsj_join(r: Relation, s: Relation, config: LsjConfig | None = None, material
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
     ev[0].record()
     if models is None:
-        model_r = sample_train(r, config.sample_rate, w, config.seed, config.model_fanout)
-        model_s = sample_train(s, config.sample_rate, w, config.seed ^ 0x5DEECE66D, config.model_fanout)
+        _, lr = prepare_model(r, config.sample_rate, config.seed, config.model_fanout)
+        _, ls = prepare_model(s, config.sample_rate, config.seed ^ 0x5DEECE66D, config.model_fanout)
     else:
-        model_r, model_s = models
+        lr = _as_lsj_model(models[0], len(r))
+        ls = _as_lsj_model(models[1], len(s))
     ev[1].record()
-    fr, fs = _fine_scale(len(r), scale), _fine_scale(len(s), scale)
-    pr, str_ = _partition(r.keys, r.payloads, model_r, fr)
-    ps, sts = _partition(s.keys, s.payloads, model_s, fs)
+    pr, str_ = _partition(r.keys, r.payloads, lr)
+    ps, sts = _partition(s.keys, s.payloads, ls)
     ev[2].record()
-    over_r = _sort_in_place(pr, str_, model_r, len(r), fr)
-    over_s = _sort_in_place(ps, sts, model_s, len(s), fs)
-    r_sorted = SortedRelation(pr[: 2 * len(r)], str_, fr, scale, model_r, (model_r.tag, scale))
-    s_sorted = SortedRelation(ps[: 2 * len(s)], sts, fs, scale, model_s, (model_s.tag, scale))
+    pr, dr = _sort(pr, str_, lr, len(r))
+    ps, ds = _sort(ps, sts, ls, len(s))
+    r_sorted = SortedRelation(pr[: 2 * len(r)], str_, lr, scale, (lr.tag, scale), diag=dr)
+    s_sorted = SortedRelation(ps[: 2 * len(s)], sts, ls, scale, (ls.tag, scale), diag=ds)
     ev[3].record()
-    result = chunked_join(r_sorted, s_sorted, model_r, scale, w, materialize)
+    result = chunked_join(r_sorted, s_sorted, lr.rmi, scale, w, materialize)
     ev[4].record()
     ev[4].synchronize()
     br.smpl = ev[0].elapsed_time(ev[1]) / 1e3
     br.part = ev[1].elapsed_time(ev[2]) / 1e3
     br.sort = ev[2].elapsed_time(ev[3]) / 1e3
     br.join = ev[3].elapsed_time(ev[4]) / 1e3
-    br.sort_stats = SortStats().merge(_sort_stats(str_, fr, scale)).merge(_sort_stats(sts, fs, scale))
-    br.extra = {"fine_scale_r": fr, "fine_scale_s": fs, "oversized_buckets_r": over_r, "oversized_buckets_s": over_s}
+    if counters:
+        br.sort_stats = SortStats().merge(_sort_stats(r_sorted.bucket_bounds)).merge(
+            _sort_stats(s_sorted.bucket_bounds))
+    br.extra = {"bins_r": lr.nbins, "bins_s": ls.nbins, **{f"r_{k}": v for k, v in dr.items()},
+                **{f"s_{k}": v for k, v in ds.items()}}
     return result, br
 
 
