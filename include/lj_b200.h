@@ -240,6 +240,10 @@ typedef struct LjLsjModel {
     int64_t nbins;            /* <= 32768 */
     const int64_t *pb;        /* [nbins+1] */
     const uint32_t *table;    /* [rmi.n] */
+    const uint64_t *sample;   /* sorted sample the model was fitted on, or NULL;
+                                 when present it also places the split points
+                                 of the sort's second level (equi-depth) */
+    int64_t nsample;
 } LjLsjModel;
 /* Bin boundaries at equally spaced ranks of the sorted sample. */
 size_t lj_lsj_bins_workspace_bytes(int64_t total);

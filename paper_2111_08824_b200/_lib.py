@@ -60,7 +60,8 @@ class LjSplineHash(ctypes.Structure):
 
 
 class LjLsjModel(ctypes.Structure):
-    _fields_ = [("rmi", LjRmi), ("nbins", _i64), ("pb", _c_void_p), ("table", _c_void_p)]
+    _fields_ = [("rmi", LjRmi), ("nbins", _i64), ("pb", _c_void_p), ("table", _c_void_p), ("sample", _c_void_p),
+                ("nsample", _i64)]
 
 
 # name -> (restype, argtypes); mirrors include/lj_b200.h one to one

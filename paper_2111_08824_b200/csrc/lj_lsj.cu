@@ -41,9 +41,10 @@ constexpr int SORT_NT = 1024;
 constexpr int CAP = 12288;        // largest bucket sorted in shared memory
 constexpr int BITONIC_W = 16384;  // fallback network width (>= CAP)
 constexpr int RUN_SMALL = 64;     // equal-slot runs insertion-sorted by one thread
+constexpr int MAX_RUNS = 64;      // longer mixed runs sorted block-wide per bucket
 constexpr int SUB = 8192;         // mean tuples per sub-bucket (shared-memory sort unit)
 constexpr int SPLIT_NT = 1024;
-constexpr int SPLIT_MAXF = 4096;  // y-slices per coarse bucket
+constexpr int SPLIT_MAXF = 2048;  // slices per coarse bucket (point mode: 2x-1 slots)
 constexpr int JOIN_T = 1024;
 constexpr int JOIN_NT = 256;
 constexpr int WCAP = 4096;
@@ -56,6 +57,8 @@ struct LsjDev {
     const u32 *table;  // [m.n] predicted position -> bin
     const i64 *pb;     // [nb+1] first position of each bin
     int nb;
+    const u64 *sample;  // sorted fit sample (split points) or nullptr
+    i64 nsample;
     __device__ __forceinline__ i64 pos(u64 k) const { return m.pos(u64_to_f64(k)); }
     __device__ __forceinline__ int bin(u64 k) const { return (int)__ldg(table + pos(k)); }
     // Unrounded placement key y in [pos-0.5, pos+0.5], monotone in the key:
@@ -79,6 +82,8 @@ static LsjDev make_lsj(const LjLsjModel &md) {
     d.table = md.table;
     d.pb = md.pb;
     d.nb = (int)md.nbins;
+    d.sample = md.sample;
+    d.nsample = md.sample ? md.nsample : 0;
     return d;
 }
 
@@ -183,16 +188,51 @@ __device__ __forceinline__ void block_scan_u32(u32 *a, int n, u32 *warp_tot) {
     __syncthreads();
 }
 
-// Coarse bucket b -> F_b = ceil(m_b / SUB) y-slices of about SUB tuples.
-__global__ void k_split_plan(const i64 *starts, int nb, i64 *fcount) {
+// Coarse bucket b -> F_b = ceil(m_b / SUB) slices of about SUB tuples.  With
+// a fit sample the F_b - 1 split points are equi-depth sample quantiles of
+// y, and every split value also gets its own "point" slice (y == v): a key
+// repeated millions of times (Zipf) then lands alone in a point slice,
+// which the sort recognises as constant and copies.  Slots per bucket:
+// 2 F_b - 1 (many stay empty); without a sample, F_b uniform y-slices.
+__device__ __forceinline__ i64 split_count(i64 m) {
+    const i64 f = (m + SUB - 1) / SUB;
+    return m == 0 ? 0 : (f < 1 ? 1 : (f > SPLIT_MAXF ? SPLIT_MAXF : f));
+}
+
+__global__ void k_split_plan(const i64 *starts, int nb, int points, i64 *fcount) {
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += gridDim.x * blockDim.x) {
         if (b == nb) {
             fcount[b] = 0;
             continue;
         }
-        const i64 m = starts[b + 1] - starts[b];
-        i64 f = (m + SUB - 1) / SUB;
-        fcount[b] = m == 0 ? 0 : (f < 1 ? 1 : (f > SPLIT_MAXF ? SPLIT_MAXF : f));
+        const i64 f = split_count(starts[b + 1] - starts[b]);
+        fcount[b] = points && f > 0 ? 2 * f - 1 : f;
+    }
+}
+
+// split values of bucket b -> spv[fbase[b] .. fbase[b] + F_b - 1)
+__global__ void k_split_points(LsjDev md, const i64 *starts, const i64 *fbase, int nb, double *spv) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
+        const i64 F = split_count(starts[b + 1] - starts[b]);
+        if (F < 2) continue;
+        // sample index range of bin b (bins are monotone over the sorted sample)
+        i64 lo = 0, hi = md.nsample;
+        while (lo < hi) {
+            i64 mid = (lo + hi) >> 1;
+            if (md.bin(md.sample[mid]) < b) lo = mid + 1; else hi = mid;
+        }
+        const i64 sb = lo;
+        hi = md.nsample;
+        while (lo < hi) {
+            i64 mid = (lo + hi) >> 1;
+            if (md.bin(md.sample[mid]) <= b) lo = mid + 1; else hi = mid;
+        }
+        const i64 se = lo, ns = se - sb;
+        const double ybase = i64_to_f64(md.pb[b]) - 0.5;
+        const double yspan = i64_to_f64(md.pb[b + 1] - md.pb[b]);
+        for (i64 j = 1; j < F; ++j)
+            spv[fbase[b] + j - 1] = ns >= F ? md.y(md.sample[sb + (j * ns) / F])
+                                            : ybase + yspan * (double)j / (double)F;
     }
 }
 
@@ -201,17 +241,29 @@ __device__ __forceinline__ int y_slice(double y, double ybase, double scale, int
     return f < 0.0 ? 0 : (f >= (double)(F - 1) ? F - 1 : (int)f);
 }
 
+// point-slice mode: slot = 2 * lower_bound(v, y) + (y == v[lb])
+__device__ __forceinline__ int point_slot(const double *v, int K, double y) {
+    int lo = 0, hi = K;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (v[mid] < y) lo = mid + 1; else hi = mid;
+    }
+    return 2 * lo + ((lo < K && v[lo] == y) ? 1 : 0);
+}
+
 // Level 2, one CTA per coarse bucket: split it into F_b y-slices through
 // global memory.  The CTA owns the bucket, so only F_b write lines per CTA
 // are open at a time (a grid-wide pass into 30K+ bins would thrash L2).
 __global__ void __launch_bounds__(SPLIT_NT) k_lsj_split(LsjDev md, const ulonglong2 *__restrict__ A,
                                                         const i64 *__restrict__ starts, const i64 *__restrict__ fbase,
-                                                        int nb, ulonglong2 *B, i64 *sub_starts, double2 *sub_y,
-                                                        SortCtl *ctl) {
-    __shared__ u32 h[SPLIT_MAXF];
+                                                        int nb, const double *spv, ulonglong2 *B, i64 *sub_starts,
+                                                        double2 *sub_y, SortCtl *ctl) {
+    __shared__ u32 h[2 * SPLIT_MAXF];
+    __shared__ double v[SPLIT_MAXF];
     __shared__ u32 warp_tot[SPLIT_NT / 32];
     __shared__ i64 s_b;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool points = md.sample != nullptr;
     for (;;) {
         if (threadIdx.x == 0) s_b = (i64)atomicAdd(&ctl->next, 1ULL);
         __syncthreads();
@@ -221,17 +273,22 @@ __global__ void __launch_bounds__(SPLIT_NT) k_lsj_split(LsjDev md, const ulonglo
         const i64 a = starts[b], m = starts[b + 1] - a;
         if (m == 0) continue;
         const i64 g0 = fbase[b];
-        const int F = (int)(fbase[b + 1] - g0);
+        const int F = (int)(fbase[b + 1] - g0);  // slots
+        const int K = points ? (F - 1) / 2 : 0;   // split values (point mode)
         const double ybase = i64_to_f64(md.pb[b]) - 0.5;
         double yspan = i64_to_f64(md.pb[b + 1] - md.pb[b]);
         if (!(yspan > 0.0)) yspan = 1.0;
         const double scale = (double)F / yspan;
         for (int j = threadIdx.x; j < F; j += SPLIT_NT) h[j] = 0;
+        for (int j = threadIdx.x; j < K; j += SPLIT_NT) v[j] = spv[g0 + j];
         __syncthreads();
         for (i64 base = threadIdx.x - lane; base < m; base += SPLIT_NT) {
             const i64 i = base + lane;
             int s = -1;
-            if (i < m) s = y_slice(md.y(A[a + i].x), ybase, scale, F);
+            if (i < m) {
+                const double y = md.y(A[a + i].x);
+                s = points ? point_slot(v, K, y) : y_slice(y, ybase, scale, F);
+            }
             const unsigned peers = __match_any_sync(0xffffffffu, s);
             if (s >= 0 && lane == __ffs(peers) - 1) atomicAdd(h + s, (u32)__popc(peers));
         }
@@ -264,7 +321,15 @@ __global__ void __launch_bounds__(SPLIT_NT) k_lsj_split(LsjDev md, const ulonglo
                 const u32 c = h[j];
                 h[j] = run;
                 sub_starts[g0 + j] = a + run;
-                sub_y[g0 + j] = make_double2(ybase + (double)j / scale, 1.0 / scale);
+                if (!points) {
+                    sub_y[g0 + j] = make_double2(ybase + (double)j / scale, 1.0 / scale);
+                } else if (j & 1) {  // point slice: every y equals v[(j-1)/2]
+                    sub_y[g0 + j] = make_double2(v[(j - 1) >> 1], 0.0);
+                } else {             // open interval between split values
+                    const int q = j >> 1;
+                    const double lo = q == 0 ? ybase : v[q - 1], hi = q == K ? ybase + yspan : v[q];
+                    sub_y[g0 + j] = make_double2(lo, hi > lo ? hi - lo : 0.0);
+                }
                 run += c;
             }
             __syncthreads();
@@ -275,7 +340,8 @@ __global__ void __launch_bounds__(SPLIT_NT) k_lsj_split(LsjDev md, const ulonglo
             ulonglong2 e = make_ulonglong2(0, 0);
             if (i < m) {
                 e = A[a + i];
-                s = y_slice(md.y(e.x), ybase, scale, F);
+                const double y = md.y(e.x);
+                s = points ? point_slot(v, K, y) : y_slice(y, ybase, scale, F);
             }
             const unsigned peers = __match_any_sync(0xffffffffu, s);
             const int leader = __ffs(peers) - 1;
@@ -285,6 +351,34 @@ __global__ void __launch_bounds__(SPLIT_NT) k_lsj_split(LsjDev md, const ulonglo
             if (s >= 0) B[a + at + __popc(peers & ((1u << lane) - 1u))] = e;
         }
         __syncthreads();
+    }
+}
+
+// Block-wide sort of idx[base, base+len) by K[idx[.]]: a bitonic network in
+// its "flip" form, whose comparators all put the minimum at the lower index,
+// so positions >= len act as +inf and their comparators are skipped.
+__device__ void block_sort_idx(u16 *idx, int base, int len, const u64 *K) {
+    int w = 1;
+    while (w < len) w <<= 1;
+    for (int k = 2; k <= w; k <<= 1) {
+        for (int j = k; j > 1; j >>= 1) {
+            const bool flip = j == k;
+            const int h = j >> 1;
+            for (int t = threadIdx.x; t < (w >> 1); t += SORT_NT) {
+                // t-th comparator of this stage: i in the lower half of its
+                // j-block, partner mirrored (flip) or h apart
+                const int i = (t / h) * j + (t % h);
+                const int l = flip ? (i ^ (j - 1)) : (i + h);
+                if (l < len) {
+                    const u16 a = idx[base + i], c = idx[base + l];
+                    if (K[a] > K[c]) {
+                        idx[base + i] = c;
+                        idx[base + l] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
     }
 }
 
@@ -301,11 +395,13 @@ __global__ void __launch_bounds__(SORT_NT, 1) k_lsj_sort(LsjDev md, Src src, con
     u16 *idx = slot + CAP;                                // placement [BITONIC_W]
     __shared__ u32 warp_tot[SORT_NT / 32];
     __shared__ i64 s_b;
-    __shared__ int s_bad;
+    __shared__ int s_bad, s_nruns;
+    __shared__ int2 s_runs[MAX_RUNS];
     for (;;) {
         if (threadIdx.x == 0) {
             s_b = (i64)atomicAdd(&ctl->next, 1ULL);
             s_bad = 0;
+            s_nruns = 0;
         }
         __syncthreads();
         const i64 b = s_b;
@@ -360,38 +456,27 @@ __global__ void __launch_bounds__(SORT_NT, 1) k_lsj_sort(LsjDev md, Src src, con
                 const u64 k0 = K[idx[i]];
                 bool same = true;
                 for (int a = i + 1; a < e && same; ++a) same = K[idx[a]] == k0;
-                if (!same) s_bad = 1;  // long mixed run: sort the whole bucket below
+                if (!same) {  // long mixed run: queued for a block-wide sort below
+                    const int q = atomicAdd(&s_nruns, 1);
+                    if (q < MAX_RUNS) {
+                        s_runs[q] = make_int2(i, len);
+                    } else {
+                        s_bad = 1;
+                    }
+                }
             }
         }
         __syncthreads();
+        const int nruns = s_nruns < MAX_RUNS ? s_nruns : MAX_RUNS;
+        if (!s_bad)
+            for (int q = 0; q < nruns; ++q) block_sort_idx(idx, s_runs[q].x, s_runs[q].y, K);
         for (int i = threadIdx.x; i + 1 < m; i += SORT_NT)
             if (K[idx[i]] > K[idx[i + 1]]) s_bad = 1;
         __syncthreads();
         if (s_bad) {
-            // fallback: bitonic sort of the bucket's indices by key (padded
-            // with a sentinel index that compares as +inf)
-            int w = 1;
-            while (w < m) w <<= 1;
-            for (int i = threadIdx.x; i < w; i += SORT_NT) idx[i] = i < m ? (u16)i : (u16)0xFFFF;
-            __syncthreads();
-            for (int kk = 2; kk <= w; kk <<= 1) {
-                for (int j = kk >> 1; j > 0; j >>= 1) {
-                    for (int i = threadIdx.x; i < w; i += SORT_NT) {
-                        const int l = i ^ j;
-                        if (l > i) {
-                            const u16 a = idx[i], c = idx[l];
-                            const bool ga = a == 0xFFFF, gc = c == 0xFFFF;
-                            const bool agt = ga ? !gc : (gc ? false : K[a] > K[c]);
-                            const bool up = (i & kk) == 0;
-                            if (agt == up) {
-                                idx[i] = c;
-                                idx[l] = a;
-                            }
-                        }
-                    }
-                    __syncthreads();
-                }
-            }
+            // safety net (the placement key is monotone, so this only runs
+            // when too many long runs appeared): sort the whole bucket
+            block_sort_idx(idx, 0, m, K);
             if (threadIdx.x == 0) atomicAdd(&ctl->n_fallback, 1ULL);
         }
         // write out: key from smem, payload gathered from the bucket (L2-hot)
@@ -403,22 +488,42 @@ __global__ void __launch_bounds__(SORT_NT, 1) k_lsj_sort(LsjDev md, Src src, con
     }
 }
 
-// sub-buckets still above CAP: one repeated key -> copy; else flag
-__global__ void k_big_sub(const ulonglong2 *tmp, SubBuckets sb, const i64 *list, int nlist, ulonglong2 *out,
-                          int *flags) {
-    for (int q = blockIdx.x; q < nlist; q += gridDim.x) {
-        const Bucket bk = sb.get(list[q]);
-        const u64 k0 = tmp[bk.in_base].x;
-        __shared__ int diff;
-        if (threadIdx.x == 0) diff = 0;
-        __syncthreads();
-        for (i64 i = threadIdx.x; i < bk.m; i += blockDim.x)
-            if (tmp[bk.in_base + i].x != k0) diff = 1;
-        __syncthreads();
-        if (!diff)
-            for (i64 i = threadIdx.x; i < bk.m; i += blockDim.x) out[bk.out_base + i] = tmp[bk.in_base + i];
-        if (threadIdx.x == 0) flags[q] = diff;
-        __syncthreads();
+// Sub-buckets still above CAP (a hot duplicate key's point slice), over the
+// flattened list: big[q] = {start, len}, boff = exclusive prefix of len.
+__device__ __forceinline__ int find_big(const i64 *boff, int nbig, i64 t) {
+    int lo = 0, hi = nbig;  // last q with boff[q] <= t
+    while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (boff[mid] <= t) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void k_big_list(const i64 *list, int nbig, const i64 *sub_starts, i64 *big) {
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nbig; q += gridDim.x * blockDim.x) {
+        const i64 g = list[q];
+        big[2 * q] = sub_starts[g];
+        big[2 * q + 1] = sub_starts[g + 1] - sub_starts[g];
+    }
+}
+
+// flags[q] = 1 if sub-bucket q holds more than one distinct key
+__global__ void k_big_check(const ulonglong2 *B, const i64 *big, const i64 *boff, int nbig, i64 total, int *flags) {
+    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < total; t += (i64)gridDim.x * blockDim.x) {
+        const int q = find_big(boff, nbig, t);
+        const i64 a = big[2 * q];
+        if (B[a + (t - boff[q])].x != B[a].x) flags[q] = 1;
+    }
+}
+
+// one repeated key: already sorted, copy through
+__global__ void k_big_copy(const ulonglong2 *B, const i64 *big, const i64 *boff, int nbig, i64 total,
+                           const int *flags, ulonglong2 *out) {
+    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < total; t += (i64)gridDim.x * blockDim.x) {
+        const int q = find_big(boff, nbig, t);
+        if (flags[q]) continue;
+        const i64 i = big[2 * q] + (t - boff[q]);
+        out[i] = B[i];
     }
 }
 
@@ -640,10 +745,10 @@ int lj_lsj_partition(const LjLsjModel *md, const uint64_t *keys, const uint64_t 
                          as_stream(stream));
 }
 
-static i64 max_subs(i64 n, i64 nbins) { return n / SUB + nbins + 2; }
+static i64 max_subs(i64 n, i64 nbins) { return 2 * (n / SUB + nbins) + 2; }
 
 size_t lj_lsj_sort_workspace_bytes(int64_t n, int64_t nbins) {
-    const i64 G = max_subs(n, nbins);
+    const i64 G = max_subs(n, nbins), nbig = n / CAP + 2;
     size_t t = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, t, (const u64 *)nullptr, (u64 *)nullptr, (const u64 *)nullptr,
                                     (u64 *)nullptr, (int64_t)n);
@@ -651,7 +756,9 @@ size_t lj_lsj_sort_workspace_bytes(int64_t n, int64_t nbins) {
     return al(sizeof(SortCtl)) + 2 * al(sizeof(i64) * (size_t)(nbins + 1)) +  // ctl, fcount, fbase
            al(sizeof(ulonglong2) * (size_t)n) +                              // split array
            al(sizeof(i64) * (size_t)(G + 1)) + al(sizeof(double2) * (size_t)G) +  // sub starts, y ranges
-           al(sizeof(i64) * (size_t)(n / CAP + 2)) + al(sizeof(int) * (size_t)(n / CAP + 2)) +  // big list, flags
+           al(sizeof(double) * (size_t)G) +                                  // split values
+           al(sizeof(i64) * (size_t)nbig) + al(sizeof(i64) * 2 * (size_t)nbig) +  // big list, {start, len}
+           al(sizeof(i64) * (size_t)(nbig + 1)) + al(sizeof(int) * (size_t)nbig) +  // offsets, flags
            4 * al(sizeof(u64) * (size_t)n) + al(t > sc ? t : sc);
 }
 
@@ -680,8 +787,12 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
     ulonglong2 *B = (ulonglong2 *)take(sizeof(ulonglong2) * (size_t)n);
     i64 *sub_starts = (i64 *)take(sizeof(i64) * (size_t)(G + 1));
     double2 *sub_y = (double2 *)take(sizeof(double2) * (size_t)G);
-    i64 *big = (i64 *)take(sizeof(i64) * (size_t)(n / CAP + 2));
-    int *flags = (int *)take(sizeof(int) * (size_t)(n / CAP + 2));
+    double *spv = (double *)take(sizeof(double) * (size_t)G);
+    const i64 nbig_cap = n / CAP + 2;
+    i64 *biglist = (i64 *)take(sizeof(i64) * (size_t)nbig_cap);
+    i64 *big = (i64 *)take(sizeof(i64) * 2 * (size_t)nbig_cap);
+    i64 *boff = (i64 *)take(sizeof(i64) * (size_t)(nbig_cap + 1));
+    int *flags = (int *)take(sizeof(int) * (size_t)nbig_cap);
     u64 *k1 = (u64 *)take(sizeof(u64) * (size_t)n);
     u64 *v1 = (u64 *)take(sizeof(u64) * (size_t)n);
     u64 *k2 = (u64 *)take(sizeof(u64) * (size_t)n);
@@ -691,18 +802,24 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
     const LsjDev dev = make_lsj(*md);
     const ulonglong2 *A = reinterpret_cast<const ulonglong2 *>(pairs_in);
     ulonglong2 *out = reinterpret_cast<ulonglong2 *>(pairs_out);
-    // level 2: y-slices of ~SUB tuples per coarse bucket, CTA-local
-    k_split_plan<<<(int)((nb + 256) / 256), 256, 0, st>>>(starts, (int)nb, fcount);
+    // level 2: slices of ~SUB tuples per coarse bucket, CTA-local
+    const int points = dev.sample != nullptr && dev.nsample > 0;
+    k_split_plan<<<(int)((nb + 256) / 256), 256, 0, st>>>(starts, (int)nb, points, fcount);
     LJ_CK_LAUNCH();
     size_t t = scan_i64_bytes(nb + 1);
     LJ_CK(cub::DeviceScan::ExclusiveSum(cub_tmp, t, fcount, fbase, (int64_t)(nb + 1), st));
     k_set_last<<<1, 1, 0, st>>>(fbase, (int)nb, n, sub_starts);
+    if (points) {
+        k_split_points<<<(int)((nb + 127) / 128), 128, 0, st>>>(dev, starts, fbase, (int)nb, spv);
+        LJ_CK_LAUNCH();
+    }
     LJ_CK(cudaMemsetAsync(ctl, 0, sizeof(SortCtl), st));
-    k_lsj_split<<<sm_count() * 2, SPLIT_NT, 0, st>>>(dev, A, starts, fbase, (int)nb, B, sub_starts, sub_y, ctl);
+    k_lsj_split<<<sm_count() * 2, SPLIT_NT, 0, st>>>(dev, A, starts, fbase, (int)nb, spv, B, sub_starts, sub_y,
+                                                      ctl);
     LJ_CK_LAUNCH();
     // K8 over the sub-buckets, B -> out (G = fbase[nb] read on device)
     SubBuckets sb{sub_starts, sub_y};
-    int rc = launch_sort(dev, sb, fbase + nb, B, out, ctl, big, st);
+    int rc = launch_sort(dev, sb, fbase + nb, B, out, ctl, biglist, st);
     if (rc) return rc;
     SortCtl h;
     LJ_CK(cudaMemcpyAsync(&h, ctl, sizeof(SortCtl), cudaMemcpyDeviceToHost, st));
@@ -711,21 +828,32 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
     const int nbig = (int)h.n_over;
     stats_host[0] = nbig;
     if (nbig == 0) return LJ_OK;
-    // sub-buckets above shared memory: one repeated key (hot duplicate) ->
-    // copy; otherwise (rare) a device radix sort of that sub-bucket
-    k_big_sub<<<std::min(nbig, 1024), 256, 0, st>>>(B, sb, big, nbig, out, flags);
+    // sub-buckets above shared memory: one repeated key (a hot duplicate's
+    // point slice) -> already sorted, copied through over the flattened
+    // list; otherwise (rare) a device radix sort of that sub-bucket
+    k_big_list<<<(nbig + 255) / 256, 256, 0, st>>>(biglist, nbig, sub_starts, big);
+    LJ_CK_LAUNCH();
+    std::vector<i64> hbig(2 * (size_t)nbig), hoff(nbig + 1);
+    LJ_CK(cudaMemcpyAsync(hbig.data(), big, sizeof(i64) * 2 * nbig, cudaMemcpyDeviceToHost, st));
+    LJ_CK(cudaStreamSynchronize(st));
+    i64 total = 0;
+    for (int q = 0; q < nbig; ++q) {
+        hoff[q] = total;
+        total += hbig[2 * q + 1];
+    }
+    hoff[nbig] = total;
+    LJ_CK(cudaMemcpyAsync(boff, hoff.data(), sizeof(i64) * (nbig + 1), cudaMemcpyHostToDevice, st));
+    LJ_CK(cudaMemsetAsync(flags, 0, sizeof(int) * nbig, st));
+    k_big_check<<<grid_for(total, 256, 8), 256, 0, st>>>(B, big, boff, nbig, total, flags);
+    k_big_copy<<<grid_for(total, 256, 8), 256, 0, st>>>(B, big, boff, nbig, total, flags, out);
     LJ_CK_LAUNCH();
     std::vector<int> hf(nbig);
-    std::vector<i64> hbig(nbig);
     LJ_CK(cudaMemcpyAsync(hf.data(), flags, sizeof(int) * nbig, cudaMemcpyDeviceToHost, st));
-    LJ_CK(cudaMemcpyAsync(hbig.data(), big, sizeof(i64) * nbig, cudaMemcpyDeviceToHost, st));
     LJ_CK(cudaStreamSynchronize(st));
     int nsorted = 0;
     for (int q = 0; q < nbig; ++q) {
         if (!hf[q]) continue;
-        i64 se[2];
-        LJ_CK(cudaMemcpy(se, sub_starts + hbig[q], sizeof(i64) * 2, cudaMemcpyDeviceToHost));
-        const i64 a = se[0], len = se[1] - se[0];
+        const i64 a = hbig[2 * q], len = hbig[2 * q + 1];
         k_deinterleave<<<grid_for(len, 256, 8), 256, 0, st>>>(B + a, len, k1, v1);
         size_t tt = 0;
         cub::DeviceRadixSort::SortPairs(nullptr, tt, k1, k2, v1, v2, (int64_t)len);

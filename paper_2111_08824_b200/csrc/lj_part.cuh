@@ -20,6 +20,7 @@
 namespace lj {
 
 constexpr int PART2_NT = 512;
+constexpr int PART2_U = 4;  // tuple groups in flight per warp step
 constexpr int PART2_MAXBINS = 32768;
 
 struct PartPlan {
@@ -63,14 +64,22 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_hist(Src f, i64 n, i64 chunk, 
     for (int j = threadIdx.x; j < nbins; j += PART2_NT) h[j] = 0;
     f.prepare();
     __syncthreads();
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const i64 lo = blockIdx.x * chunk, hi = min(lo + chunk, n);
-    for (i64 base = lo + threadIdx.x - lane; base < hi; base += PART2_NT) {
-        const i64 i = base + lane;
-        int b = -1;
-        if (i < hi) b = f.bin_of(i);
-        const unsigned peers = __match_any_sync(0xffffffffu, b);
-        if (b >= 0 && lane == __ffs(peers) - 1) atomicAdd(h + b, (u32)__popc(peers));
+    // each warp takes PART2_U groups of 32 consecutive tuples per step: the
+    // U dependent chains (key -> model -> bin) overlap in flight
+    for (i64 base = lo + (i64)warp * 32 * PART2_U; base < hi; base += (i64)PART2_NT * PART2_U) {
+        int b[PART2_U];
+#pragma unroll
+        for (int u = 0; u < PART2_U; ++u) {
+            const i64 i = base + u * 32 + lane;
+            b[u] = i < hi ? f.bin_of(i) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < PART2_U; ++u) {
+            const unsigned peers = __match_any_sync(0xffffffffu, b[u]);
+            if (b[u] >= 0 && lane == __ffs(peers) - 1) atomicAdd(h + b[u], (u32)__popc(peers));
+        }
     }
     __syncthreads();
     for (int j = threadIdx.x; j < nbins; j += PART2_NT) mat[(i64)j * gridDim.x + blockIdx.x] = h[j];
@@ -84,19 +93,26 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter(Src f, i64 n, i64 chun
     for (int j = threadIdx.x; j < nbins; j += PART2_NT) cur[j] = (u32)off[(i64)j * gridDim.x + blockIdx.x];
     f.prepare();
     __syncthreads();
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const i64 lo = blockIdx.x * chunk, hi = min(lo + chunk, n);
-    for (i64 base = lo + threadIdx.x - lane; base < hi; base += PART2_NT) {
-        const i64 i = base + lane;
-        int b = -1;
-        u64 k = 0, p = 0;
-        if (i < hi) b = f.load(i, k, p);
-        const unsigned peers = __match_any_sync(0xffffffffu, b);
-        const int leader = __ffs(peers) - 1;
-        u32 at = 0;
-        if (b >= 0 && lane == leader) at = atomicAdd(cur + b, (u32)__popc(peers));
-        at = __shfl_sync(0xffffffffu, at, leader);
-        if (b >= 0) out[at + __popc(peers & ((1u << lane) - 1u))] = make_ulonglong2(k, p);
+    for (i64 base = lo + (i64)warp * 32 * PART2_U; base < hi; base += (i64)PART2_NT * PART2_U) {
+        int b[PART2_U];
+        u64 k[PART2_U], p[PART2_U];
+#pragma unroll
+        for (int u = 0; u < PART2_U; ++u) {
+            const i64 i = base + u * 32 + lane;
+            k[u] = p[u] = 0;
+            b[u] = i < hi ? f.load(i, k[u], p[u]) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < PART2_U; ++u) {
+            const unsigned peers = __match_any_sync(0xffffffffu, b[u]);
+            const int leader = __ffs(peers) - 1;
+            u32 at = 0;
+            if (b[u] >= 0 && lane == leader) at = atomicAdd(cur + b[u], (u32)__popc(peers));
+            at = __shfl_sync(0xffffffffu, at, leader);
+            if (b[u] >= 0) out[at + __popc(peers & ((1u << lane) - 1u))] = make_ulonglong2(k[u], p[u]);
+        }
     }
 }
 

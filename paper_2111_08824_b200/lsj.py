@@ -81,18 +81,22 @@ class LsjConfig:
 class LsjModel:
     """An RMI plus bins over its predicted positions (LjLsjModel)."""
 
-    def __init__(self, rmi: RecursiveModelIndex, pb: torch.Tensor, table: torch.Tensor):
+    def __init__(self, rmi: RecursiveModelIndex, pb: torch.Tensor, table: torch.Tensor,
+                 sample: torch.Tensor | None = None):
         self.rmi = rmi
         self.pb = pb
         self.table = table
         self.nbins = pb.numel() - 1
+        self.sample = sample
 
     @property
     def tag(self):
         return self.rmi.tag
 
     def c_struct(self) -> _lib.LjLsjModel:
-        return _lib.LjLsjModel(self.rmi.c_struct(), self.nbins, _lib.ptr(self.pb), _lib.ptr(self.table))
+        ns = self.sample.numel() if self.sample is not None else 0
+        return _lib.LjLsjModel(self.rmi.c_struct(), self.nbins, _lib.ptr(self.pb), _lib.ptr(self.table),
+                               _lib.ptr(self.sample), ns)
 
     @classmethod
     def uniform(cls, rmi: RecursiveModelIndex, nbins: int) -> "LsjModel":
@@ -118,7 +122,7 @@ class LsjModel:
         _lib.check(lib.lj_lsj_bins(ctypes.byref(c), _lib.ptr(sample_sorted), sample_sorted.numel(), nbins,
                                    _lib.ptr(pb), _lib.ptr(table), _lib.ptr(ws), ws.numel(), _lib.stream_ptr()),
                    "lsj_bins")
-        return cls(rmi, pb, table)
+        return cls(rmi, pb, table, sample_sorted)
 
 
 def default_bins(n: int) -> int:
