@@ -1,0 +1,190 @@
+"""Multi-GPU execution of the learned joins: one process per GPU,
+``torch.distributed`` (NCCL on the GPUs, gloo in the CPU tests).
+
+INLJ: every rank holds the same R index (built untimed, as the
+reference builds its index before timing) and probes its own contiguous S
+shard (``shard_bounds`` = the reference's ``chunk_bounds`` unit, one GPU per
+worker).  The only collective is the 3-word checksum reduction.
+
+LSJ: one shared model, fitted on the union of the ranks' R samples,
+range-partitions both relations into ``world`` contiguous key ranges
+(equi-depth over the sample); per-destination counts are exchanged, then an
+all-to-all-v moves the tuples (the path's one real exchange step); each rank
+then runs the single-GPU LSJ on its key range, and the checksums are reduced.
+
+The device work is injected (``partition_fn`` / ``local_join_fn``) so the
+host-side protocol -- sample gathering, count exchange, split sizes,
+all-to-all, checksum reduction -- is exercised by world-size-2 gloo tests on
+the CPU with the oracle as the local stand-in; on GPUs the defaults call the
+CUDA library.
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+MASK = (1 << 64) - 1
+
+
+def rank_world(group=None) -> tuple[int, int]:
+    if not dist.is_available() or not dist.is_initialized():
+        return 0, 1
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
+def shard_bounds(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous shard of rank (util.py:62-64 chunk_bounds semantics)."""
+    step = n / world
+    lo = int(rank * step)
+    hi = n if rank == world - 1 else int((rank + 1) * step)
+    return lo, hi
+
+
+def reduce_checksum(words: torch.Tensor, group=None) -> tuple[int, int, int]:
+    """Combine per-rank {count, sum, xor, ...} int64 words: count and sum
+    add (int64 wraps mod 2^64, as the checksum's sum does), xor is gathered
+    and folded (collectives have no XOR reduction)."""
+    rank, world = rank_world(group)
+    w = words[:3].clone()
+    if world == 1:
+        v = w.cpu().tolist()
+        return int(v[0]), int(v[1]) & MASK, int(v[2]) & MASK
+    sums = w[:2].contiguous()
+    dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
+    xs = [torch.empty_like(w[2:3]) for _ in range(world)]
+    dist.all_gather(xs, w[2:3].contiguous(), group=group)
+    x = 0
+    for t in xs:
+        x ^= int(t.item()) & MASK
+    s = sums.cpu().tolist()
+    return int(s[0]), int(s[1]) & MASK, x
+
+
+def gather_varlen(t: torch.Tensor, group=None) -> torch.Tensor:
+    """Concatenate a 1-D tensor of per-rank length across ranks (rank order)."""
+    rank, world = rank_world(group)
+    if world == 1:
+        return t
+    n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+    sizes = [torch.empty_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    sizes = [int(s.item()) for s in sizes]
+    m = max(sizes)
+    pad = torch.zeros(m, dtype=t.dtype, device=t.device)
+    pad[: t.numel()] = t
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    return torch.cat([p[:s] for p, s in zip(parts, sizes)])
+
+
+def exchange(records: torch.Tensor, send_counts: list[int], group=None) -> torch.Tensor:
+    """All-to-all-v of records grouped by destination rank.
+
+    ``records``: [n, 2] int64 (key, payload) ordered by destination;
+    ``send_counts[d]`` records go to rank d.  Returns the records received,
+    ordered by source rank."""
+    rank, world = rank_world(group)
+    if world == 1:
+        return records
+    dev = records.device
+    sc = torch.tensor(send_counts, dtype=torch.int64, device=dev)
+    rc = torch.empty_like(sc)
+    dist.all_to_all_single(rc, sc, group=group)
+    recv_counts = [int(v) for v in rc.cpu().tolist()]
+    flat = records.reshape(-1).contiguous()
+    out = torch.empty(2 * sum(recv_counts), dtype=flat.dtype, device=dev)
+    dist.all_to_all_single(out, flat, [2 * c for c in recv_counts], [2 * c for c in send_counts], group=group)
+    return out.view(-1, 2)
+
+
+# ---------------------------------------------------------------- INLJ
+
+
+def inlj_join(probe_fn, s_keys: torch.Tensor, s_payloads: torch.Tensor, group=None):
+    """Sharded INLJ: probe_fn(keys, payloads) -> int64 words on this rank's
+    S shard (replicated index), then the checksum reduction."""
+    words = probe_fn(s_keys, s_payloads)
+    return reduce_checksum(words, group)
+
+
+# ---------------------------------------------------------------- LSJ
+
+
+def _gpu_partition(keys: torch.Tensor, payloads: torch.Tensor, model, world: int):
+    """Range-partition (key, payload) into `world` bins of the shared model:
+    (records [n, 2] grouped by destination, counts per destination)."""
+    from .lsj import _partition
+
+    pairs, starts = _partition(keys, payloads, model)
+    st = starts.cpu().tolist()
+    counts = [int(st[d + 1] - st[d]) for d in range(world)]
+    return pairs[: 2 * keys.numel()].view(-1, 2), counts
+
+
+def _gpu_shared_model(r_keys: torch.Tensor, sample_rate: float, seed: int, world: int, group=None):
+    """One model for all ranks: every rank samples its R shard, the samples
+    are gathered and sorted identically everywhere, the RMI and the
+    `world` equi-depth range bins are fitted on that sorted global sample
+    (deterministic kernels -> the same model on every rank)."""
+    from . import _lib
+    from .lsj import LsjModel
+    from .models import RecursiveModelIndex
+    from .util import sort_pairs
+
+    lib = _lib.lib()
+    n = r_keys.numel()
+    total = max(1, int(round(sample_rate * n)))
+    sample = torch.empty(total, dtype=torch.int64, device=r_keys.device)
+    ws = _lib.workspace(lib.lj_lsj_sample_workspace_bytes(total), r_keys.device)
+    _lib.check(lib.lj_lsj_sample(_lib.ptr(r_keys), n, total, int(seed) & MASK, _lib.ptr(sample), _lib.ptr(ws),
+                                 ws.numel(), _lib.stream_ptr()), "lsj_sample")
+    allsamp = gather_varlen(sample, group)
+    srt, _ = sort_pairs(allsamp, allsamp)
+    fanout = min(1000, max(1, srt.numel() // 8))
+    rmi = RecursiveModelIndex(fanout).fit(srt)
+    return LsjModel.from_sample(rmi, srt, world)
+
+
+def lsj_join(r_keys, r_payloads, s_keys, s_payloads, config=None, group=None, *, model_fn=None,
+             partition_fn=None, local_join_fn=None):
+    """Distributed LSJ over this rank's shards of R and S.  Returns
+    ((count, sum, xor), phases) -- the global checksum on every rank."""
+    from .lsj import LsjConfig
+
+    config = config or LsjConfig()
+    rank, world = rank_world(group)
+    model_fn = model_fn or (lambda rk: _gpu_shared_model(rk, config.sample_rate, config.seed, world, group))
+    partition_fn = partition_fn or (lambda k, p, m: _gpu_partition(k, p, m, world))
+    if local_join_fn is None:
+        def local_join_fn(rrec, srec):
+            from . import lsj as _lsj
+            from .data import Relation
+
+            r = Relation(rrec[:, 0].contiguous(), rrec[:, 1].contiguous(), validate=False)
+            s = Relation(srec[:, 0].contiguous(), srec[:, 1].contiguous(), validate=False)
+            res, _ = _lsj.lsj_join(r, s, LsjConfig(workers=1, fanout=config.fanout,
+                                                    sample_rate=config.sample_rate, seed=config.seed),
+                                   counters=False)
+            words = res._words if res._words is not None else torch.tensor(
+                list(res.checksum) + [0], dtype=torch.int64)
+            return words
+    phases = {}
+    t0 = time.perf_counter()
+    model = model_fn(r_keys)
+    t1 = time.perf_counter()
+    r_rec, r_cnt = partition_fn(r_keys, r_payloads, model)
+    s_rec, s_cnt = partition_fn(s_keys, s_payloads, model)
+    t2 = time.perf_counter()
+    r_loc = exchange(r_rec, r_cnt, group)
+    s_loc = exchange(s_rec, s_cnt, group)
+    t3 = time.perf_counter()
+    words = local_join_fn(r_loc, s_loc)
+    t4 = time.perf_counter()
+    res = reduce_checksum(words, group)
+    phases.update(smpl=t1 - t0, part=t2 - t1, xchg=t3 - t2, local=t4 - t3, n_r_local=int(r_loc.shape[0]),
+                  n_s_local=int(s_loc.shape[0]))
+    return res, phases
