@@ -192,6 +192,13 @@ int lj_leaf_bucket_bins(int64_t L);
 size_t lj_leaf_bucket_workspace_bytes(int64_t nk, int64_t L);
 int lj_leaf_bucket(const LjGrmi *idx, const uint64_t *keys, const uint64_t *pay, int64_t nk,
                    uint64_t *pairs_out, int64_t *starts_out, void *ws, size_t ws_bytes, void *stream);
+/* K1 over the output of lj_leaf_bucket (records + window starts): each
+ * CTA stages a window's gapped keys (+halo) in shared memory and searches
+ * there; searches leaving the staged range are redone in global memory, so
+ * results and search_steps equal lj_grmi_probe's.  ws: 8 bytes of device
+ * scratch (work counter). */
+int lj_grmi_probe_bucketed(const LjGrmi *idx, const uint64_t *s_pairs, int64_t nk, const int64_t *wstarts,
+                           void *ws, uint64_t *out, int accumulate, void *stream);
 /* K1 over interleaved {key, payload} probe records (e.g. bucketed S). */
 int lj_grmi_probe_pairs(const LjGrmi *idx, const uint64_t *s_pairs, int64_t nk, uint64_t *out, int accumulate,
                         void *stream);

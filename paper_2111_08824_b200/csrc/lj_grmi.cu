@@ -321,6 +321,175 @@ __global__ void __launch_bounds__(NT) k_grmi_probe_sm(GrmiDev g, const u64 *__re
     reduce_checksum(cnt, sum, x, steps, out);
 }
 
+// ---------------------------------------------- staged probe (K1 over K4)
+//
+// After K4 every window of 2^shift predicted slots has its probes stored
+// contiguously.  A CTA takes a piece of that array; for each window segment
+// of the piece it stages the window's gapped KEYS (+ a halo of STAGE_H slots
+// each side) in shared memory and runs the reference's exponential search
+// (gapped.py:86-160, identical probe counting) there.  A search or run scan
+// that leaves the staged range is redone in global memory from scratch, so
+// results and probe counts never depend on the staging.  Payloads (needed
+// for occupancy and the checksum) are read from global memory, 1-2 per hit.
+
+constexpr int STAGE_NT = 1024;
+constexpr int STAGE_H = 2048;           // halo slots on each side
+constexpr i64 STAGE_PIECE = 65536;      // probes per work item
+constexpr i64 STAGE_MIN = 2048;         // smaller window segments: global search
+
+// exponential search over any key accessor; kf(i, ok) clears ok when slot i
+// is not available (then the result is meaningless and the caller redoes it)
+template <class KeyF>
+__device__ __forceinline__ i64 exp_search_with(const KeyF &kf, i64 L, i64 start, u64 k, i64 &probes, bool &ok) {
+    probes = 1;
+    u64 v = kf(start, ok);
+    if (v == k) return start;
+    i64 lo, hi;
+    if (v < k) {
+        i64 prev = start, step = 1;
+        for (;;) {
+            i64 idx = start + step;
+            if (idx >= L) { lo = prev + 1; hi = L; break; }
+            ++probes;
+            u64 w = kf(idx, ok);
+            if (!ok) return -1;
+            if (w < k) { prev = idx; step <<= 1; }
+            else if (w == k) return idx;
+            else { lo = prev + 1; hi = idx; break; }
+        }
+    } else {
+        i64 prev = start, step = 1;
+        for (;;) {
+            i64 idx = start - step;
+            if (idx < 0) { lo = 0; hi = prev; break; }
+            ++probes;
+            u64 w = kf(idx, ok);
+            if (!ok) return -1;
+            if (w > k) { prev = idx; step <<= 1; }
+            else if (w == k) return idx;
+            else { lo = idx + 1; hi = prev; break; }
+        }
+    }
+    while (lo < hi) {
+        i64 mid = (lo + hi) >> 1;
+        ++probes;
+        if (kf(mid, ok) < k) lo = mid + 1; else hi = mid;
+        if (!ok) return -1;
+    }
+    if (lo < L) {
+        ++probes;
+        if (kf(lo, ok) == k) return lo;
+    }
+    return -1;
+}
+
+struct StagedKeys {
+    const u64 *sk;
+    i64 lo, hi;
+    __device__ __forceinline__ u64 operator()(i64 i, bool &ok) const {
+        if (i < lo || i >= hi) {
+            ok = false;
+            return 0;
+        }
+        return sk[i - lo];
+    }
+};
+
+// one probe against the index: staged search + run scan, global redo on escape
+__device__ __forceinline__ void probe_one(const GrmiDev &g, const StagedKeys &st, u64 k, u64 ps, u64 &cnt, u64 &sum,
+                                          u64 &x, u64 &steps) {
+    const i64 start = g.predict_slot(k);
+    i64 probes;
+    bool ok = true;
+    i64 s = exp_search_with(st, g.L, start, k, probes, ok);
+    u64 c = 0, sm = 0, xx = 0;
+    if (ok && s >= 0) {
+        while (s > 0) {
+            const u64 v = st(s - 1, ok);
+            if (!ok || v != k) break;
+            --s;
+        }
+        for (i64 i = s; ok && i < g.L; ++i) {
+            const u64 v = st(i, ok);
+            if (!ok || v != k) break;
+            const u64 pay = ldg(g.slots + 2 * i + 1);
+            if (!g.real(i, pay)) continue;
+            const u64 t = pay + ps;
+            ++c;
+            sm += t;
+            xx ^= t;
+        }
+    }
+    if (!ok) {  // left the staged range: the plain global-memory probe
+        c = sm = xx = 0;
+        s = g.search(start, k, probes);
+        if (s >= 0) {
+            while (s > 0 && g.key(s - 1) == k) --s;
+            for (; s < g.L; ++s) {
+                const ulonglong2 e = ldg2(g.slots + 2 * s);
+                if (e.x != k) break;
+                if (!g.real(s, e.y)) continue;
+                const u64 t = e.y + ps;
+                ++c;
+                sm += t;
+                xx ^= t;
+            }
+        }
+    }
+    steps += (u64)probes;
+    cnt += c;
+    sum += sm;
+    x ^= xx;
+}
+
+__global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, const ulonglong2 *__restrict__ rec,
+                                                                   i64 nk, const i64 *__restrict__ wstarts,
+                                                                   int nwin, int shift, unsigned long long *work,
+                                                                   u64 *out) {
+    extern __shared__ u64 sk[];
+    __shared__ i64 s_piece;
+    const i64 wsz = (i64)1 << shift;
+    u64 cnt = 0, sum = 0, x = 0, steps = 0;
+    const StagedKeys none{sk, 0, 0};
+    for (;;) {
+        if (threadIdx.x == 0) s_piece = (i64)atomicAdd(work, 1ULL);
+        __syncthreads();
+        const i64 p0 = s_piece * STAGE_PIECE;
+        __syncthreads();
+        if (p0 >= nk) break;
+        const i64 p1 = min(p0 + STAGE_PIECE, nk);
+        // first window overlapping p0
+        int lo = 0, hi = nwin;
+        while (hi - lo > 1) {
+            int mid = (lo + hi) >> 1;
+            if (wstarts[mid] <= p0) lo = mid; else hi = mid;
+        }
+        for (int w = lo; w < nwin && wstarts[w] < p1; ++w) {
+            const i64 a = max(p0, wstarts[w]), e = min(p1, wstarts[w + 1]);
+            if (e <= a) continue;
+            if (e - a >= STAGE_MIN) {
+                const i64 slo = max((i64)0, ((i64)w << shift) - STAGE_H);
+                const i64 shi = min(g.L, (((i64)w + 1) << shift) + STAGE_H);
+                for (i64 i = threadIdx.x; i < shi - slo; i += STAGE_NT) sk[i] = ldg(g.slots + 2 * (slo + i));
+                __syncthreads();
+                const StagedKeys st{sk, slo, shi};
+                for (i64 t = a + threadIdx.x; t < e; t += STAGE_NT) {
+                    const ulonglong2 r = __ldcs(rec + t);
+                    probe_one(g, st, r.x, r.y, cnt, sum, x, steps);
+                }
+                __syncthreads();
+            } else {
+                for (i64 t = a + threadIdx.x; t < e; t += STAGE_NT) {
+                    const ulonglong2 r = __ldcs(rec + t);
+                    probe_one(g, none, r.x, r.y, cnt, sum, x, steps);
+                }
+            }
+        }
+    }
+    (void)wsz;
+    reduce_checksum(cnt, sum, x, steps, out);
+}
+
 __global__ void k_grmi_predict_slots(GrmiDev g, const u64 *keys, i64 nk, i64 *out) {
     for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < nk; t += (i64)gridDim.x * blockDim.x)
         out[t] = g.predict_slot(keys[t]);
@@ -489,6 +658,31 @@ int lj_grmi_probe(const LjGrmi *idx, const uint64_t *s_keys, const uint64_t *s_p
     } else {
         k_grmi_probe<NT, SoaIn><<<grid_for(nk, NT, 8), NT, 0, st>>>(GrmiDev(*idx), SoaIn{s_keys, s_pay}, nk, out);
     }
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+int lj_grmi_probe_bucketed(const LjGrmi *idx, const uint64_t *s_pairs, int64_t nk, const int64_t *wstarts,
+                           void *ws, uint64_t *out, int accumulate, void *stream) {
+    LJ_REQUIRE(idx != nullptr, "null index");
+    cudaStream_t st = as_stream(stream);
+    if (!accumulate) LJ_CK(cudaMemsetAsync(out, 0, 4 * sizeof(u64), st));
+    if (nk <= 0 || idx->n == 0) return LJ_OK;
+    const int shift = slot_window_shift(idx->L);
+    const int nwin = lj_leaf_bucket_bins(idx->L);
+    const size_t sm = sizeof(u64) * (size_t)(((i64)1 << shift) + 2 * STAGE_H);
+    if (sm > 200 * 1024) {  // window too large to stage: plain K1 over the grouped records
+        return lj_grmi_probe_pairs(idx, s_pairs, nk, out, 1, stream);
+    }
+    static bool attr = false;
+    if (!attr) {
+        LJ_CK(cudaFuncSetAttribute(k_grmi_probe_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    unsigned long long *work = reinterpret_cast<unsigned long long *>(ws);
+    LJ_CK(cudaMemsetAsync(work, 0, sizeof(unsigned long long), st));
+    k_grmi_probe_staged<<<sm_count(), STAGE_NT, sm, st>>>(GrmiDev(*idx), reinterpret_cast<const ulonglong2 *>(s_pairs),
+                                                          nk, wstarts, nwin, shift, work, out);
     LJ_CK_LAUNCH();
     return LJ_OK;
 }

@@ -42,8 +42,11 @@ constexpr int CAP = 12288;        // largest bucket sorted in shared memory
 constexpr int BITONIC_W = 16384;  // fallback network width (>= CAP)
 constexpr int RUN_SMALL = 64;     // equal-slot runs insertion-sorted by one thread
 constexpr int MAX_RUNS = 64;      // longer mixed runs sorted block-wide per bucket
-constexpr int SUB = 8192;         // mean tuples per sub-bucket (shared-memory sort unit)
+constexpr int SUB = 6144;         // mean tuples per sub-bucket: sample-quantile slices
+                                  // (~61 sample keys each) stay below CAP
 constexpr int SPLIT_NT = 1024;
+constexpr int SPLIT_U = 4;        // tuple groups in flight per warp step
+constexpr i64 SPLIT_CH = 65536;   // tuples per split work item
 constexpr int SPLIT_MAXF = 2048;  // slices per coarse bucket (point mode: 2x-1 slots)
 constexpr int JOIN_T = 1024;
 constexpr int JOIN_NT = 256;
@@ -251,104 +254,183 @@ __device__ __forceinline__ int point_slot(const double *v, int K, double y) {
     return 2 * lo + ((lo < K && v[lo] == y) ? 1 : 0);
 }
 
-// Level 2, one CTA per coarse bucket: split it into F_b y-slices through
-// global memory.  The CTA owns the bucket, so only F_b write lines per CTA
-// are open at a time (a grid-wide pass into 30K+ bins would thrash L2).
-__global__ void __launch_bounds__(SPLIT_NT) k_lsj_split(LsjDev md, const ulonglong2 *__restrict__ A,
-                                                        const i64 *__restrict__ starts, const i64 *__restrict__ fbase,
-                                                        int nb, const double *spv, ulonglong2 *B, i64 *sub_starts,
-                                                        double2 *sub_y, SortCtl *ctl) {
+// Level 2 as a balanced, segmented partition.  Work item = a chunk of <=
+// SPLIT_CH tuples of one coarse bucket (hot buckets span many chunks, so no
+// CTA owns a whole hot-key bucket).  Pass 1 counts each chunk's slots in
+// shared memory into a block-diagonal (slot x chunk) matrix laid out
+// bucket-major, slot-major; one exclusive scan of it yields, for every
+// (bucket, slot, chunk), the absolute output position (buckets are
+// contiguous and in order); pass 2 re-walks the chunk and scatters through
+// shared-memory cursors.  A chunk keeps <= 4095 write frontiers open.
+
+struct SplitCtx {  // per-bucket layout shared by the split kernels
+    const i64 *starts;  // [nb+1] coarse bucket bounds
+    const i64 *fbase;   // [nb+1] first slot of each bucket
+    const i64 *cbase;   // [nb+1] first chunk of each bucket
+    const i64 *mbase;   // [nb+1] first matrix entry of each bucket
+    const double *spv;  // split values (point mode), at fbase[b]
+    int nb;
+};
+
+__global__ void k_chunk_plan(const i64 *starts, const i64 *fbase, int nb, i64 *chunks, i64 *matc) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += gridDim.x * blockDim.x) {
+        if (b == nb) {
+            chunks[b] = matc[b] = 0;
+            continue;
+        }
+        const i64 m = starts[b + 1] - starts[b];
+        const i64 c = (m + SPLIT_CH - 1) / SPLIT_CH;
+        chunks[b] = c;
+        matc[b] = c * (fbase[b + 1] - fbase[b]);
+    }
+}
+
+struct SplitItem {
+    i64 b, c, chunks, a, e, g0;
+    int F, K;
+    double ybase, yspan, scale;
+};
+
+__device__ __forceinline__ SplitItem split_item(const LsjDev &md, const SplitCtx &cx, i64 q, bool points) {
+    int lo = 0, hi = cx.nb;  // last bucket with cbase[b] <= q
+    while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (cx.cbase[mid] <= q) lo = mid; else hi = mid;
+    }
+    SplitItem it;
+    it.b = lo;
+    it.c = q - cx.cbase[lo];
+    it.chunks = cx.cbase[lo + 1] - cx.cbase[lo];
+    const i64 a0 = cx.starts[lo], e0 = cx.starts[lo + 1];
+    it.a = a0 + it.c * SPLIT_CH;
+    it.e = min(it.a + (i64)SPLIT_CH, e0);
+    it.g0 = cx.fbase[lo];
+    it.F = (int)(cx.fbase[lo + 1] - it.g0);
+    it.K = points ? (it.F - 1) / 2 : 0;
+    it.ybase = i64_to_f64(md.pb[lo]) - 0.5;
+    it.yspan = i64_to_f64(md.pb[lo + 1] - md.pb[lo]);
+    if (!(it.yspan > 0.0)) it.yspan = 1.0;
+    it.scale = (double)it.F / it.yspan;
+    return it;
+}
+
+__device__ __forceinline__ int split_slot(const LsjDev &md, const SplitItem &it, const double *v, bool points, u64 k) {
+    const double y = md.y(k);
+    return points ? point_slot(v, it.K, y) : y_slice(y, it.ybase, it.scale, it.F);
+}
+
+// pass 1: mat[mbase[b] + s * chunks_b + c] = tuples of chunk c in slot s
+__global__ void __launch_bounds__(SPLIT_NT) k_split_count(LsjDev md, SplitCtx cx, const ulonglong2 *__restrict__ A,
+                                                          const i64 *nitems, u32 *mat, SortCtl *ctl) {
     __shared__ u32 h[2 * SPLIT_MAXF];
     __shared__ double v[SPLIT_MAXF];
-    __shared__ u32 warp_tot[SPLIT_NT / 32];
-    __shared__ i64 s_b;
+    __shared__ i64 s_q;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool points = md.sample != nullptr;
+    const i64 total = *nitems;
     for (;;) {
-        if (threadIdx.x == 0) s_b = (i64)atomicAdd(&ctl->next, 1ULL);
+        if (threadIdx.x == 0) s_q = (i64)atomicAdd(&ctl->next, 1ULL);
         __syncthreads();
-        const i64 b = s_b;
+        const i64 q = s_q;
+        if (q >= total) break;
+        const SplitItem it = split_item(md, cx, q, points);
+        for (int j = threadIdx.x; j < it.F; j += SPLIT_NT) h[j] = 0;
+        for (int j = threadIdx.x; j < it.K; j += SPLIT_NT) v[j] = cx.spv[it.g0 + j];
         __syncthreads();
-        if (b >= nb) break;
-        const i64 a = starts[b], m = starts[b + 1] - a;
-        if (m == 0) continue;
-        const i64 g0 = fbase[b];
-        const int F = (int)(fbase[b + 1] - g0);  // slots
-        const int K = points ? (F - 1) / 2 : 0;   // split values (point mode)
+        for (i64 base = it.a + (i64)warp * 32 * SPLIT_U; base < it.e; base += (i64)SPLIT_NT * SPLIT_U) {
+            int s[SPLIT_U];
+#pragma unroll
+            for (int u = 0; u < SPLIT_U; ++u) {
+                const i64 i = base + u * 32 + lane;
+                s[u] = i < it.e ? split_slot(md, it, v, points, A[i].x) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < SPLIT_U; ++u) {
+                const unsigned peers = __match_any_sync(0xffffffffu, s[u]);
+                if (s[u] >= 0 && lane == __ffs(peers) - 1) atomicAdd(h + s[u], (u32)__popc(peers));
+            }
+        }
+        __syncthreads();
+        const i64 mb = cx.mbase[it.b];
+        for (int j = threadIdx.x; j < it.F; j += SPLIT_NT) mat[mb + (i64)j * it.chunks + it.c] = h[j];
+        __syncthreads();
+    }
+}
+
+// slot bounds + placement ranges from the scanned matrix
+__global__ void k_split_slots(LsjDev md, SplitCtx cx, const i64 *off, i64 n, i64 *sub_starts, double2 *sub_y) {
+    const bool points = md.sample != nullptr;
+    const i64 G = cx.fbase[cx.nb];
+    for (i64 g = blockIdx.x * (i64)blockDim.x + threadIdx.x; g <= G; g += (i64)gridDim.x * blockDim.x) {
+        if (g == G) {
+            sub_starts[g] = n;
+            continue;
+        }
+        int lo = 0, hi = cx.nb;  // bucket of slot g
+        while (hi - lo > 1) {
+            int mid = (lo + hi) >> 1;
+            if (cx.fbase[mid] <= g) lo = mid; else hi = mid;
+        }
+        const i64 b = lo, j = g - cx.fbase[b], F = cx.fbase[b + 1] - cx.fbase[b];
+        const i64 chunks = cx.cbase[b + 1] - cx.cbase[b];
+        sub_starts[g] = off[cx.mbase[b] + j * chunks];
         const double ybase = i64_to_f64(md.pb[b]) - 0.5;
         double yspan = i64_to_f64(md.pb[b + 1] - md.pb[b]);
         if (!(yspan > 0.0)) yspan = 1.0;
-        const double scale = (double)F / yspan;
-        for (int j = threadIdx.x; j < F; j += SPLIT_NT) h[j] = 0;
-        for (int j = threadIdx.x; j < K; j += SPLIT_NT) v[j] = spv[g0 + j];
-        __syncthreads();
-        for (i64 base = threadIdx.x - lane; base < m; base += SPLIT_NT) {
-            const i64 i = base + lane;
-            int s = -1;
-            if (i < m) {
-                const double y = md.y(A[a + i].x);
-                s = points ? point_slot(v, K, y) : y_slice(y, ybase, scale, F);
+        if (!points) {
+            sub_y[g] = make_double2(ybase + (double)j * yspan / (double)F, yspan / (double)F);
+        } else {
+            const i64 K = (F - 1) / 2;
+            const double *v = cx.spv + cx.fbase[b];
+            if (j & 1) {  // point slot: every y equals v[(j-1)/2]
+                sub_y[g] = make_double2(v[(j - 1) >> 1], 0.0);
+            } else {      // open interval between split values
+                const i64 q = j >> 1;
+                const double l = q == 0 ? ybase : v[q - 1], h = q == K ? ybase + yspan : v[q];
+                sub_y[g] = make_double2(l, h > l ? h - l : 0.0);
             }
-            const unsigned peers = __match_any_sync(0xffffffffu, s);
-            if (s >= 0 && lane == __ffs(peers) - 1) atomicAdd(h + s, (u32)__popc(peers));
         }
+    }
+}
+
+// pass 2: scatter every chunk through shared-memory cursors
+__global__ void __launch_bounds__(SPLIT_NT) k_split_scatter(LsjDev md, SplitCtx cx, const ulonglong2 *__restrict__ A,
+                                                            const i64 *nitems, const i64 *__restrict__ off,
+                                                            ulonglong2 *B, SortCtl *ctl) {
+    __shared__ u32 cur[2 * SPLIT_MAXF];
+    __shared__ double v[SPLIT_MAXF];
+    __shared__ i64 s_q;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool points = md.sample != nullptr;
+    const i64 total = *nitems;
+    for (;;) {
+        if (threadIdx.x == 0) s_q = (i64)atomicAdd(&ctl->next, 1ULL);
         __syncthreads();
-        // exclusive scan of h[0..F) (F <= SPLIT_MAXF, 4 per thread)
-        {
-            const int per = (F + SPLIT_NT - 1) / SPLIT_NT, j0 = threadIdx.x * per;
-            u32 local = 0;
-            for (int j = j0; j < j0 + per && j < F; ++j) local += h[j];
-            u32 incl = local;
+        const i64 q = s_q;
+        if (q >= total) break;
+        const SplitItem it = split_item(md, cx, q, points);
+        const i64 a0 = cx.starts[it.b], mb = cx.mbase[it.b];
+        for (int j = threadIdx.x; j < it.F; j += SPLIT_NT) cur[j] = (u32)(off[mb + (i64)j * it.chunks + it.c] - a0);
+        for (int j = threadIdx.x; j < it.K; j += SPLIT_NT) v[j] = cx.spv[it.g0 + j];
+        __syncthreads();
+        for (i64 base = it.a + (i64)warp * 32 * SPLIT_U; base < it.e; base += (i64)SPLIT_NT * SPLIT_U) {
+            int s[SPLIT_U];
+            ulonglong2 r[SPLIT_U];
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                u32 v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += v;
+            for (int u = 0; u < SPLIT_U; ++u) {
+                const i64 i = base + u * 32 + lane;
+                r[u] = i < it.e ? A[i] : make_ulonglong2(0, 0);
+                s[u] = i < it.e ? split_slot(md, it, v, points, r[u].x) : -1;
             }
-            if (lane == 31) warp_tot[warp] = incl;
-            __syncthreads();
-            if (warp == 0) {
-                u32 t = lane < SPLIT_NT / 32 ? warp_tot[lane] : 0;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    u32 v = __shfl_up_sync(0xffffffffu, t, o);
-                    if (lane >= o) t += v;
-                }
-                if (lane < SPLIT_NT / 32) warp_tot[lane] = t;
+            for (int u = 0; u < SPLIT_U; ++u) {
+                const unsigned peers = __match_any_sync(0xffffffffu, s[u]);
+                const int leader = __ffs(peers) - 1;
+                u32 at = 0;
+                if (s[u] >= 0 && lane == leader) at = atomicAdd(cur + s[u], (u32)__popc(peers));
+                at = __shfl_sync(0xffffffffu, at, leader);
+                if (s[u] >= 0) B[a0 + at + __popc(peers & ((1u << lane) - 1u))] = r[u];
             }
-            __syncthreads();
-            u32 run = (warp ? warp_tot[warp - 1] : 0) + incl - local;
-            for (int j = j0; j < j0 + per && j < F; ++j) {
-                const u32 c = h[j];
-                h[j] = run;
-                sub_starts[g0 + j] = a + run;
-                if (!points) {
-                    sub_y[g0 + j] = make_double2(ybase + (double)j / scale, 1.0 / scale);
-                } else if (j & 1) {  // point slice: every y equals v[(j-1)/2]
-                    sub_y[g0 + j] = make_double2(v[(j - 1) >> 1], 0.0);
-                } else {             // open interval between split values
-                    const int q = j >> 1;
-                    const double lo = q == 0 ? ybase : v[q - 1], hi = q == K ? ybase + yspan : v[q];
-                    sub_y[g0 + j] = make_double2(lo, hi > lo ? hi - lo : 0.0);
-                }
-                run += c;
-            }
-            __syncthreads();
-        }
-        for (i64 base = threadIdx.x - lane; base < m; base += SPLIT_NT) {
-            const i64 i = base + lane;
-            int s = -1;
-            ulonglong2 e = make_ulonglong2(0, 0);
-            if (i < m) {
-                e = A[a + i];
-                const double y = md.y(e.x);
-                s = points ? point_slot(v, K, y) : y_slice(y, ybase, scale, F);
-            }
-            const unsigned peers = __match_any_sync(0xffffffffu, s);
-            const int leader = __ffs(peers) - 1;
-            u32 at = 0;
-            if (s >= 0 && lane == leader) at = atomicAdd(h + s, (u32)__popc(peers));
-            at = __shfl_sync(0xffffffffu, at, leader);
-            if (s >= 0) B[a + at + __popc(peers & ((1u << lane) - 1u))] = e;
         }
         __syncthreads();
     }
@@ -746,14 +828,26 @@ int lj_lsj_partition(const LjLsjModel *md, const uint64_t *keys, const uint64_t 
 }
 
 static i64 max_subs(i64 n, i64 nbins) { return 2 * (n / SUB + nbins) + 2; }
+static i64 max_mat(i64 n, i64 nbins) { return (i64)(2 * SPLIT_MAXF) * (n / SPLIT_CH + nbins + 1); }
+
+static size_t mat_scan_bytes(i64 items) {
+    size_t t = 0;
+    cub::TransformInputIterator<i64, CastU32I64, const u32 *> it(nullptr, CastU32I64());
+    cub::DeviceScan::ExclusiveSum(nullptr, t, it, (i64 *)nullptr, (int64_t)items);
+    return t;
+}
 
 size_t lj_lsj_sort_workspace_bytes(int64_t n, int64_t nbins) {
-    const i64 G = max_subs(n, nbins), nbig = n / CAP + 2;
+    const i64 G = max_subs(n, nbins), nbig = n / CAP + 2, M = max_mat(n, nbins);
     size_t t = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, t, (const u64 *)nullptr, (u64 *)nullptr, (const u64 *)nullptr,
                                     (u64 *)nullptr, (int64_t)n);
-    const size_t sc = scan_i64_bytes(nbins + 1);
+    size_t sc = scan_i64_bytes(nbins + 1);
+    const size_t ms = mat_scan_bytes(M);
+    if (ms > sc) sc = ms;
     return al(sizeof(SortCtl)) + 2 * al(sizeof(i64) * (size_t)(nbins + 1)) +  // ctl, fcount, fbase
+           4 * al(sizeof(i64) * (size_t)(nbins + 1)) +                       // chunks, cbase, matc, mbase
+           al(sizeof(u32) * (size_t)M) + al(sizeof(i64) * (size_t)M) +        // slot x chunk matrix, offsets
            al(sizeof(ulonglong2) * (size_t)n) +                              // split array
            al(sizeof(i64) * (size_t)(G + 1)) + al(sizeof(double2) * (size_t)G) +  // sub starts, y ranges
            al(sizeof(double) * (size_t)G) +                                  // split values
@@ -784,6 +878,13 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
     SortCtl *ctl = (SortCtl *)take(sizeof(SortCtl));
     i64 *fcount = (i64 *)take(sizeof(i64) * (size_t)(nb + 1));
     i64 *fbase = (i64 *)take(sizeof(i64) * (size_t)(nb + 1));
+    i64 *chunks = (i64 *)take(sizeof(i64) * (size_t)(nb + 1));
+    i64 *cbase = (i64 *)take(sizeof(i64) * (size_t)(nb + 1));
+    i64 *matc = (i64 *)take(sizeof(i64) * (size_t)(nb + 1));
+    i64 *mbase = (i64 *)take(sizeof(i64) * (size_t)(nb + 1));
+    const i64 Mcap = max_mat(n, nb);
+    u32 *mat = (u32 *)take(sizeof(u32) * (size_t)Mcap);
+    i64 *moff = (i64 *)take(sizeof(i64) * (size_t)Mcap);
     ulonglong2 *B = (ulonglong2 *)take(sizeof(ulonglong2) * (size_t)n);
     i64 *sub_starts = (i64 *)take(sizeof(i64) * (size_t)(G + 1));
     double2 *sub_y = (double2 *)take(sizeof(double2) * (size_t)G);
@@ -802,20 +903,42 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
     const LsjDev dev = make_lsj(*md);
     const ulonglong2 *A = reinterpret_cast<const ulonglong2 *>(pairs_in);
     ulonglong2 *out = reinterpret_cast<ulonglong2 *>(pairs_out);
-    // level 2: slices of ~SUB tuples per coarse bucket, CTA-local
+    // level 2: slices of ~SUB tuples per coarse bucket (segmented, chunked)
     const int points = dev.sample != nullptr && dev.nsample > 0;
     k_split_plan<<<(int)((nb + 256) / 256), 256, 0, st>>>(starts, (int)nb, points, fcount);
     LJ_CK_LAUNCH();
     size_t t = scan_i64_bytes(nb + 1);
     LJ_CK(cub::DeviceScan::ExclusiveSum(cub_tmp, t, fcount, fbase, (int64_t)(nb + 1), st));
-    k_set_last<<<1, 1, 0, st>>>(fbase, (int)nb, n, sub_starts);
     if (points) {
         k_split_points<<<(int)((nb + 127) / 128), 128, 0, st>>>(dev, starts, fbase, (int)nb, spv);
         LJ_CK_LAUNCH();
     }
+    k_chunk_plan<<<(int)((nb + 256) / 256), 256, 0, st>>>(starts, fbase, (int)nb, chunks, matc);
+    LJ_CK_LAUNCH();
+    LJ_CK(cub::DeviceScan::ExclusiveSum(cub_tmp, t, chunks, cbase, (int64_t)(nb + 1), st));
+    LJ_CK(cub::DeviceScan::ExclusiveSum(cub_tmp, t, matc, mbase, (int64_t)(nb + 1), st));
+    i64 CM[2];
+    LJ_CK(cudaMemcpyAsync(&CM[0], cbase + nb, sizeof(i64), cudaMemcpyDeviceToHost, st));
+    LJ_CK(cudaMemcpyAsync(&CM[1], mbase + nb, sizeof(i64), cudaMemcpyDeviceToHost, st));
+    LJ_CK(cudaStreamSynchronize(st));
+    const i64 M = CM[1];
+    if (M > Mcap) {
+        set_error("lj_lsj_sort: slot x chunk matrix exceeds its bound");
+        return LJ_E_WORKSPACE;
+    }
+    const SplitCtx cx{starts, fbase, cbase, mbase, spv, (int)nb};
     LJ_CK(cudaMemsetAsync(ctl, 0, sizeof(SortCtl), st));
-    k_lsj_split<<<sm_count() * 2, SPLIT_NT, 0, st>>>(dev, A, starts, fbase, (int)nb, spv, B, sub_starts, sub_y,
-                                                      ctl);
+    k_split_count<<<sm_count() * 2, SPLIT_NT, 0, st>>>(dev, cx, A, cbase + nb, mat, ctl);
+    LJ_CK_LAUNCH();
+    {
+        size_t tm = mat_scan_bytes(M);
+        cub::TransformInputIterator<i64, CastU32I64, const u32 *> it(mat, CastU32I64());
+        LJ_CK(cub::DeviceScan::ExclusiveSum(cub_tmp, tm, it, moff, (int64_t)M, st));
+    }
+    k_split_slots<<<grid_for(G + 1, 256, 8), 256, 0, st>>>(dev, cx, moff, n, sub_starts, sub_y);
+    LJ_CK_LAUNCH();
+    LJ_CK(cudaMemsetAsync(ctl, 0, sizeof(SortCtl), st));
+    k_split_scatter<<<sm_count() * 2, SPLIT_NT, 0, st>>>(dev, cx, A, cbase + nb, moff, B, ctl);
     LJ_CK_LAUNCH();
     // K8 over the sub-buckets, B -> out (G = fbase[nb] read on device)
     SubBuckets sb{sub_starts, sub_y};

@@ -19,7 +19,7 @@
 
 namespace lj {
 
-constexpr int PART2_NT = 512;
+constexpr int PART2_NT = 1024;
 constexpr int PART2_U = 4;  // tuple groups in flight per warp step
 constexpr int PART2_MAXBINS = 32768;
 
@@ -32,9 +32,9 @@ struct PartPlan {
 inline PartPlan part_plan(i64 n, int nbins) {
     PartPlan p;
     p.nbins = nbins;
-    // one or two resident blocks per SM, depending on the histogram size
-    int per_sm = nbins <= 8192 ? 2 : 1;
-    p.blocks = sm_count() * per_sm;
+    // one block per SM: blocks x bins open write lines (148 x 2048 x 128 B
+    // = 39 MB) stay inside L2, so records leave L2 as whole lines
+    p.blocks = sm_count();
     i64 c = (n + p.blocks - 1) / p.blocks;
     c = (c + 31) / 32 * 32;
     p.chunk = c < 32 ? 32 : c;

@@ -105,7 +105,8 @@ class GappedRmiIndex:
         L = self.slot_count
         return {"pairs": torch.empty(2 * max(n, 1), dtype=torch.int64, device=dev),
                 "starts": torch.empty(lib.lj_leaf_bucket_bins(L) + 1, dtype=torch.int64, device=dev),
-                "ws": _lib.workspace(lib.lj_leaf_bucket_workspace_bytes(n, L), dev)}
+                "ws": _lib.workspace(lib.lj_leaf_bucket_workspace_bytes(n, L), dev),
+                "work": torch.zeros(1, dtype=torch.int64, device=dev)}
 
     def join_checksum_buffered(self, s_keys: torch.Tensor, s_payloads: torch.Tensor,
                                out: torch.Tensor | None = None, accumulate: bool = False, scratch: dict | None = None,
@@ -130,8 +131,9 @@ class GappedRmiIndex:
         _lib.check(lib.lj_leaf_bucket(ctypes.byref(g), _lib.ptr(s_keys), _lib.ptr(s_payloads), n,
                                       _lib.ptr(scratch["pairs"]), _lib.ptr(scratch["starts"]), _lib.ptr(ws),
                                       ws.numel(), st), "leaf_bucket")
-        _lib.check(lib.lj_grmi_probe_pairs(ctypes.byref(g), _lib.ptr(scratch["pairs"]), n, _lib.ptr(out),
-                                           int(bool(accumulate)), st), "grmi_probe_pairs")
+        _lib.check(lib.lj_grmi_probe_bucketed(ctypes.byref(g), _lib.ptr(scratch["pairs"]), n,
+                                              _lib.ptr(scratch["starts"]), _lib.ptr(scratch["work"]), _lib.ptr(out),
+                                              int(bool(accumulate)), st), "grmi_probe_bucketed")
         return out
 
     def _predict_slots(self, keys: torch.Tensor) -> torch.Tensor:
