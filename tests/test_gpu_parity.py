@@ -329,3 +329,19 @@ def test_config3_reduced_against_oracle(lj):
     res, _, _ = lj.ALGORITHMS["spline-hash-inlj"](inp.r, inp.s, 1, dict(lj.DEFAULT_OPTS, **inp.opts))
     assert res.checksum == oracle.smj_checksum(*inp.r.numpy(), *inp.s.numpy())
     assert res.count == len(inp.s)  # every probe is an R key, R unique
+
+
+@pytest.mark.parametrize("fanout", [4, 256, 4096])
+def test_buffered_staged_probe_equals_direct(lj, fanout):
+    """K4 + staged K1 == K1: identical checksum AND search_steps, including
+    searches that leave the staged window (tiny fanout -> long searches)
+    and window segments too small to stage."""
+    from paper_2111_08824_b200 import configs
+
+    inp = configs.config2(scale=5)
+    idx = lj.GappedRmiIndex(2.0, fanout).fit(inp.r)
+    direct = idx.join_checksum(inp.s.keys, inp.s.payloads).cpu().tolist()
+    buffered = idx.join_checksum_buffered(inp.s.keys, inp.s.payloads).cpu().tolist()
+    assert buffered == direct
+    small = idx.join_checksum_buffered(inp.s.keys[:5000], inp.s.payloads[:5000]).cpu().tolist()
+    assert small == idx.join_checksum(inp.s.keys[:5000], inp.s.payloads[:5000]).cpu().tolist()
