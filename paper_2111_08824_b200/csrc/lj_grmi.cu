@@ -336,6 +336,7 @@ constexpr int STAGE_NT = 1024;
 constexpr int STAGE_H = 2048;           // halo slots on each side
 constexpr i64 STAGE_PIECE = 65536;      // probes per work item
 constexpr i64 STAGE_MIN = 2048;         // smaller window segments: global search
+constexpr int STAGE_U = 2;              // probes in flight per thread
 
 // exponential search over any key accessor; kf(i, ok) clears ok when slot i
 // is not available (then the result is meaningless and the caller redoes it)
@@ -381,6 +382,45 @@ __device__ __forceinline__ i64 exp_search_with(const KeyF &kf, i64 L, i64 start,
         if (kf(lo, ok) == k) return lo;
     }
     return -1;
+}
+
+// The reference's probe count (gapped.py:86-160) of an exponential search
+// from `start`, computed without touching memory from the key's position in
+// the sorted gapped array: slots [lb, re) hold the key, slots < lb are
+// smaller, slots >= re larger.  Every comparison the reference makes is
+// decided by where its index falls relative to lb and re.
+__device__ __forceinline__ i64 ref_probe_count(i64 start, i64 lb, i64 re, i64 L) {
+    i64 probes = 1;
+    if (start >= lb && start < re) return 1;
+    i64 lo, hi;
+    if (start < lb) {
+        i64 prev = start, step = 1;
+        for (;;) {
+            const i64 idx = start + step;
+            if (idx >= L) { lo = prev + 1; hi = L; break; }
+            ++probes;
+            if (idx < lb) { prev = idx; step <<= 1; }
+            else if (idx < re) return probes;
+            else { lo = prev + 1; hi = idx; break; }
+        }
+    } else {
+        i64 prev = start, step = 1;
+        for (;;) {
+            const i64 idx = start - step;
+            if (idx < 0) { lo = 0; hi = prev; break; }
+            ++probes;
+            if (idx >= re) { prev = idx; step <<= 1; }
+            else if (idx >= lb) return probes;
+            else { lo = idx + 1; hi = prev; break; }
+        }
+    }
+    while (lo < hi) {
+        const i64 mid = (lo + hi) >> 1;
+        ++probes;
+        if (mid < lb) lo = mid + 1; else hi = mid;
+    }
+    if (lo < L) ++probes;
+    return probes;
 }
 
 struct StagedKeys {
@@ -473,9 +513,69 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
                 for (i64 i = threadIdx.x; i < shi - slo; i += STAGE_NT) sk[i] = ldg(g.slots + 2 * (slo + i));
                 __syncthreads();
                 const StagedKeys st{sk, slo, shi};
-                for (i64 t = a + threadIdx.x; t < e; t += STAGE_NT) {
-                    const ulonglong2 r = __ldcs(rec + t);
-                    probe_one(g, st, r.x, r.y, cnt, sum, x, steps);
+                // STAGE_U probes per thread per step, each phase issued for
+                // all of them before the next: the global loads (probe
+                // record, leaf record, payloads) of different probes overlap
+                for (i64 t0 = a + threadIdx.x; t0 < e; t0 += (i64)STAGE_NT * STAGE_U) {
+                    u64 k[STAGE_U], ps[STAGE_U];
+                    i64 start[STAGE_U], s[STAGE_U], probes[STAGE_U];
+                    bool ok[STAGE_U];
+#pragma unroll
+                    for (int u = 0; u < STAGE_U; ++u) {
+                        const i64 t = t0 + (i64)u * STAGE_NT;
+                        ulonglong2 r = t < e ? __ldcs(rec + t) : make_ulonglong2(0, 0);
+                        k[u] = r.x;
+                        ps[u] = r.y;
+                    }
+#pragma unroll
+                    for (int u = 0; u < STAGE_U; ++u) start[u] = g.predict_slot(k[u]);
+                    // lower bound in the staged keys: a branch-free binary
+                    // search whose trip count is the same for every lane
+                    const i64 span = shi - slo;
+#pragma unroll
+                    for (int u = 0; u < STAGE_U; ++u) {
+                        i64 base = 0, len = span;
+                        while (len > 1) {
+                            const i64 half = len >> 1;
+                            base = sk[base + half - 1] < k[u] ? base + half : base;
+                            len -= half;
+                        }
+                        s[u] = slo + base + ((span > 0 && sk[base] < k[u]) ? 1 : 0);  // first slot >= key
+                        // the lower bound is exact only strictly inside the staged range
+                        ok[u] = (s[u] > slo || slo == 0) && (s[u] < shi || shi == g.L);
+                    }
+                    // payload of the first slot of the run (a one-slot run is the common case)
+                    u64 pay[STAGE_U];
+#pragma unroll
+                    for (int u = 0; u < STAGE_U; ++u)
+                        pay[u] = (ok[u] && s[u] < g.L && sk[s[u] - slo] == k[u]) ? ldg(g.slots + 2 * s[u] + 1) : 0;
+#pragma unroll
+                    for (int u = 0; u < STAGE_U; ++u) {
+                        if (t0 + (i64)u * STAGE_NT >= e) continue;
+                        u64 c = 0, sm = 0, xx = 0;
+                        i64 re = s[u];
+                        if (ok[u]) {
+                            for (; re < g.L; ++re) {
+                                if (re >= shi) { ok[u] = false; break; }
+                                if (sk[re - slo] != k[u]) break;
+                                const u64 py = re == s[u] ? pay[u] : ldg(g.slots + 2 * re + 1);
+                                if (!g.real(re, py)) continue;
+                                const u64 tt = py + ps[u];
+                                ++c;
+                                sm += tt;
+                                xx ^= tt;
+                            }
+                        }
+                        if (!ok[u]) {  // outside the staged range: the global-memory probe
+                            probe_one(g, StagedKeys{sk, 0, 0}, k[u], ps[u], cnt, sum, x, steps);
+                            continue;
+                        }
+                        probes[u] = ref_probe_count(start[u], s[u], re, g.L);
+                        steps += (u64)probes[u];
+                        cnt += c;
+                        sum += sm;
+                        x ^= xx;
+                    }
                 }
                 __syncthreads();
             } else {

@@ -37,12 +37,12 @@
 
 namespace lj {
 
-constexpr int SORT_NT = 1024;
-constexpr int CAP = 12288;        // largest bucket sorted in shared memory
-constexpr int BITONIC_W = 16384;  // fallback network width (>= CAP)
+constexpr int SORT_NT = 512;     // two sort CTAs per SM (their barrier waits overlap)
+constexpr int CAP = 6144;         // largest bucket sorted in shared memory (96 KB per CTA)
 constexpr int RUN_SMALL = 64;     // equal-slot runs insertion-sorted by one thread
 constexpr int MAX_RUNS = 64;      // longer mixed runs sorted block-wide per bucket
-constexpr int SUB = 6144;         // mean tuples per sub-bucket: sample-quantile slices
+constexpr int SORT_U = 4;         // tuples in flight per thread in the load / write-out phases
+constexpr int SUB = 3072;         // mean tuples per sub-bucket: sample-quantile slices
                                   // (~61 sample keys each) stay below CAP
 constexpr int SPLIT_NT = 1024;
 constexpr int SPLIT_U = 4;        // tuple groups in flight per warp step
@@ -466,7 +466,7 @@ __device__ void block_sort_idx(u16 *idx, int base, int len, const u64 *K) {
 
 // K8: one CTA per bucket (dynamic work counter), model-placed in smem.
 template <class Src>
-__global__ void __launch_bounds__(SORT_NT, 1) k_lsj_sort(LsjDev md, Src src, const i64 *nbuckets_dev,
+__global__ void __launch_bounds__(SORT_NT, 2) k_lsj_sort(LsjDev md, Src src, const i64 *nbuckets_dev,
                                                          const ulonglong2 *__restrict__ in, ulonglong2 *out,
                                                          SortCtl *ctl, i64 *over_list) {
     const i64 nbuckets = *nbuckets_dev;
@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(SORT_NT, 1) k_lsj_sort(LsjDev md, Src src, con
     u64 *K = reinterpret_cast<u64 *>(smem);              // keys [CAP]
     u32 *cnt = reinterpret_cast<u32 *>(K + CAP);          // slot counts -> cursors [CAP]
     u16 *slot = reinterpret_cast<u16 *>(cnt + CAP);       // slot per key [CAP]
-    u16 *idx = slot + CAP;                                // placement [BITONIC_W]
+    u16 *idx = slot + CAP;                                // placement [CAP]
     __shared__ u32 warp_tot[SORT_NT / 32];
     __shared__ i64 s_b;
     __shared__ int s_bad, s_nruns;
@@ -503,14 +503,24 @@ __global__ void __launch_bounds__(SORT_NT, 1) k_lsj_sort(LsjDev md, Src src, con
         const double scale = (double)m / (bk.yspan > 0.0 ? bk.yspan : 1.0);
         for (int j = threadIdx.x; j < m; j += SORT_NT) cnt[j] = 0;
         __syncthreads();
-        // load keys, place by the model
-        for (int i = threadIdx.x; i < m; i += SORT_NT) {
-            const u64 k = in[bk.in_base + i].x;
-            K[i] = k;
-            double f = floor((md.y(k) - bk.ybase) * scale);
-            int s = f < 0.0 ? 0 : (f >= (double)(m - 1) ? m - 1 : (int)f);
-            slot[i] = (u16)s;
-            atomicAdd(cnt + s, 1u);
+        // load keys, place by the model (SORT_U keys in flight per thread)
+        for (int i0 = threadIdx.x; i0 < m; i0 += SORT_NT * SORT_U) {
+            u64 k[SORT_U];
+#pragma unroll
+            for (int u = 0; u < SORT_U; ++u) {
+                const int i = i0 + u * SORT_NT;
+                k[u] = i < m ? in[bk.in_base + i].x : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < SORT_U; ++u) {
+                const int i = i0 + u * SORT_NT;
+                if (i >= m) break;
+                K[i] = k[u];
+                const double f = floor((md.y(k[u]) - bk.ybase) * scale);
+                const int s = f < 0.0 ? 0 : (f >= (double)(m - 1) ? m - 1 : (int)f);
+                slot[i] = (u16)s;
+                atomicAdd(cnt + s, 1u);
+            }
         }
         __syncthreads();
         block_scan_u32(cnt, m, warp_tot);
@@ -562,9 +572,20 @@ __global__ void __launch_bounds__(SORT_NT, 1) k_lsj_sort(LsjDev md, Src src, con
             if (threadIdx.x == 0) atomicAdd(&ctl->n_fallback, 1ULL);
         }
         // write out: key from smem, payload gathered from the bucket (L2-hot)
-        for (int i = threadIdx.x; i < m; i += SORT_NT) {
-            const u16 j = idx[i];
-            out[bk.out_base + i] = make_ulonglong2(K[j], __ldg(&in[bk.in_base + j].y));
+        for (int i0 = threadIdx.x; i0 < m; i0 += SORT_NT * SORT_U) {
+            u64 p[SORT_U];
+            u16 j[SORT_U];
+#pragma unroll
+            for (int u = 0; u < SORT_U; ++u) {
+                const int i = i0 + u * SORT_NT;
+                j[u] = i < m ? idx[i] : 0;
+                p[u] = i < m ? __ldg(&in[bk.in_base + j[u]].y) : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < SORT_U; ++u) {
+                const int i = i0 + u * SORT_NT;
+                if (i < m) out[bk.out_base + i] = make_ulonglong2(K[j[u]], p[u]);
+            }
         }
         __syncthreads();
     }
@@ -735,7 +756,7 @@ __global__ void k_sample(const u64 *keys, i64 n, i64 total, u64 seed, u64 *out) 
 static size_t al(size_t v) { return (v + 255) & ~(size_t)255; }
 
 static size_t sort_smem_bytes() {
-    return sizeof(u64) * CAP + sizeof(u32) * CAP + sizeof(u16) * CAP + sizeof(u16) * BITONIC_W;
+    return sizeof(u64) * CAP + sizeof(u32) * CAP + sizeof(u16) * CAP + sizeof(u16) * CAP;
 }
 
 template <class Src>
@@ -748,7 +769,7 @@ static int launch_sort(const LsjDev &md, const Src &src, const i64 *nb_dev, cons
         attr = true;
     }
     LJ_CK(cudaMemsetAsync(ctl, 0, sizeof(SortCtl), st));
-    k_lsj_sort<Src><<<sm_count(), SORT_NT, sort_smem_bytes(), st>>>(md, src, nb_dev, in, out, ctl, over);
+    k_lsj_sort<Src><<<sm_count() * 2, SORT_NT, sort_smem_bytes(), st>>>(md, src, nb_dev, in, out, ctl, over);
     LJ_CK_LAUNCH();
     return LJ_OK;
 }
