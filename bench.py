@@ -125,11 +125,12 @@ def make_step(inp, index, variant="buffered"):
     n_r, n_s = len(inp.r), len(inp.s)
     if index is not None:
         keys, pays = inp.s.keys, inp.s.payloads
-        if "grmi" in inp.algorithm and variant == "buffered":
+        if variant == "buffered":
             scratch = index.bucket_scratch(n_s)
+            name = ("k_bin_hist+k_bin_scatter+k_grmi_probe_staged" if "grmi" in inp.algorithm
+                    else "k_bin_hist+k_bin_scatter+k_hash_probe<grouped>")
             return ((lambda out: index.join_checksum_buffered(keys, pays, out=out, scratch=scratch)),
-                    "k_bin_hist+k_bin_scatter+k_grmi_probe<AosIn> (Request-Buffer analogue)",
-                    ALGO_BYTES[inp.algorithm] * n_s)
+                    name + " (Request-Buffer analogue)", ALGO_BYTES[inp.algorithm] * n_s)
         name = "k_grmi_probe" if "grmi" in inp.algorithm else "k_hash_probe"
         return (lambda out: index.join_checksum(keys, pays, out=out)), name, ALGO_BYTES[inp.algorithm] * n_s
     o = dict(lj.DEFAULT_OPTS, **inp.opts)
@@ -237,7 +238,7 @@ def run_reference_arm(args):
 
 def _config_block(args, inp):
     return {"workload": f"{args.config}: {inp.description}", "algorithm": inp.algorithm,
-            "variant": getattr(args, "variant", None) if "grmi" in inp.algorithm else None,
+            "variant": getattr(args, "variant", None) if inp.algorithm != "lsj" else None,
             "n_r": len(inp.r), "n_s": len(inp.s), "l2": "inputs larger than L2 and L2 flushed between steps",
             "parallelism": f"inlj-replicated-R x{args.gpus}"}
 
@@ -344,7 +345,7 @@ def _e2e(args, inp, index, world):
 
     import paper_2111_08824_b200 as lj
 
-    scratch = index.bucket_scratch(len(inp.s)) if "grmi" in inp.algorithm else None
+    scratch = index.bucket_scratch(len(inp.s)) if args.variant == "buffered" else None
     hk = inp.s.keys.cpu().pin_memory()
     hp = inp.s.payloads.cpu().pin_memory()
     steps = max(1, min(args.steps, 3))
@@ -353,7 +354,7 @@ def _e2e(args, inp, index, world):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         s = lj.Relation(hk.to("cuda", non_blocking=True), hp.to("cuda", non_blocking=True), validate=True)
-        if "grmi" in inp.algorithm and args.variant == "buffered":
+        if args.variant == "buffered":
             words = index.join_checksum_buffered(s.keys, s.payloads, scratch=scratch)
         else:
             words = index.join_checksum(s.keys, s.payloads)

@@ -226,6 +226,14 @@ int lj_spline_hash_build(const LjSpline *model, const uint64_t *keys, const uint
 /* K5: learned_hash.py:81-96 fused with the checksum. */
 int lj_spline_hash_probe(const LjSplineHash *idx, const uint64_t *s_keys, const uint64_t *s_pay,
                          int64_t nk, uint64_t *out, int accumulate, void *stream);
+/* Request-Buffer analogue for K5: group S by a window of predicted
+ * positions (<= 2048 windows, shared-memory-privatised partition) so that
+ * the probe walks chain offsets and entries window by window (cached). */
+size_t lj_spline_hash_bucket_workspace_bytes(int64_t nk, int64_t n);
+int lj_spline_hash_bucket(const LjSplineHash *idx, const uint64_t *keys, const uint64_t *pay, int64_t nk,
+                          uint64_t *pairs_out, int64_t *starts_out, void *ws, size_t ws_bytes, void *stream);
+int lj_spline_hash_probe_grouped(const LjSplineHash *idx, const uint64_t *s_pairs, int64_t nk, uint64_t *out,
+                                 int accumulate, void *stream);
 int lj_spline_hash_count(const LjSplineHash *idx, const uint64_t *keys, int64_t nk,
                          int64_t *counts, void *stream);
 int lj_spline_hash_collect(const LjSplineHash *idx, const uint64_t *keys, int64_t nk,

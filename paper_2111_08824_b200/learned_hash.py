@@ -99,6 +99,38 @@ class SplineHashIndex:
                                                    _lib.stream_ptr(stream)), "spline_hash_probe")
         return out
 
+    def bucket_scratch(self, n: int, device=None) -> dict:
+        lib = _lib.lib()
+        dev = device or self.entries.device
+        return {"pairs": torch.empty(2 * max(n, 1), dtype=torch.int64, device=dev),
+                "starts": torch.empty(2049, dtype=torch.int64, device=dev),
+                "ws": _lib.workspace(lib.lj_spline_hash_bucket_workspace_bytes(n, self.model.trained_len), dev)}
+
+    def join_checksum_buffered(self, s_keys: torch.Tensor, s_payloads: torch.Tensor,
+                               out: torch.Tensor | None = None, accumulate: bool = False, scratch: dict | None = None,
+                               stream=None) -> torch.Tensor:
+        """Group S by predicted-position window on device, then K5 over the
+        grouped records (chain offsets and entries reused from L2).  Same
+        result words as ``join_checksum``."""
+        n = s_keys.numel()
+        if out is None:
+            out = torch.zeros(4, dtype=torch.int64, device=s_keys.device)
+        if self.n == 0 or n == 0:
+            if not accumulate:
+                out.zero_()
+            return out
+        scratch = scratch or self.bucket_scratch(n, s_keys.device)
+        lib = _lib.lib()
+        st = _lib.stream_ptr(stream)
+        c = self.c_struct()
+        ws = scratch["ws"]
+        _lib.check(lib.lj_spline_hash_bucket(ctypes.byref(c), _lib.ptr(s_keys), _lib.ptr(s_payloads), n,
+                                             _lib.ptr(scratch["pairs"]), _lib.ptr(scratch["starts"]), _lib.ptr(ws),
+                                             ws.numel(), st), "spline_hash_bucket")
+        _lib.check(lib.lj_spline_hash_probe_grouped(ctypes.byref(c), _lib.ptr(scratch["pairs"]), n, _lib.ptr(out),
+                                                    int(bool(accumulate)), st), "spline_hash_probe_grouped")
+        return out
+
     def probe_batch(self, keys):
         """learned_hash.py:81-96 -> (payloads, source_index) device tensors;
         per probe, matches in chain (insertion) order."""
