@@ -147,6 +147,27 @@ __device__ __forceinline__ i64 grmi_slot_of_pos(i64 pos, i64 n, i64 L) {
     return f64_to_i64(clip_f64(s, 0.0, i64_to_f64(L - 1)));
 }
 
+// The same slot without the division on the common path.  Both the
+// reference's RN(RN(pos/n)*L) and z = RN(pos*RN(L/n)) lie within
+// 2^-50*L of r = pos*L/n (pos is an integer < 2^53, r <= L).  When z is
+// more than g = 2^-47*L away from every half-integer, r is too, and both
+// round to the same integer; otherwise (never when n divides L) the
+// reference's own operations run.
+struct SlotMap {
+    i64 n, L;
+    double c, g, top;
+    __host__ SlotMap() {}
+    __host__ SlotMap(i64 n_, i64 L_)
+        : n(n_), L(L_), c(n_ > 0 ? (double)L_ / (double)n_ : 0.0), g(ldexp((double)L_, -47)),
+          top((double)(L_ - 1)) {}
+    __device__ __forceinline__ i64 operator()(i64 pos) const {
+        const double z = __dmul_rn(i64_to_f64(pos), c);
+        const double f = __dadd_rn(z, -floor(z));
+        if (fabs(__dadd_rn(f, -0.5)) > g) return f64_to_i64(clip_f64(rint(z), 0.0, top));
+        return grmi_slot_of_pos(pos, n, L);
+    }
+};
+
 // ------------------------------------------------------------ RadixSpline
 
 struct SplineDev {

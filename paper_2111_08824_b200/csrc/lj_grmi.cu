@@ -9,8 +9,12 @@
 // 32 slots per word and is only read when some real payload is 0.
 #include <cub/cub.cuh>
 
+#include <cstdio>
+#include <vector>
+
 #include "lj_common.cuh"
 #include "lj_part.cuh"
+#include "lj_probe_count.h"
 
 namespace lj {
 
@@ -26,17 +30,63 @@ struct GrmiDev {
     const u64 *slots;
     const u32 *bitmap;
     int payload_nonzero;
+    SlotMap slot_of;
     __host__ explicit GrmiDev(const LjGrmi &g)
         : model(g.model), n(g.n), L(g.L), slots(g.slots), bitmap(g.bitmap),
-          payload_nonzero(g.payload_nonzero) {}
+          payload_nonzero(g.payload_nonzero), slot_of(g.n, g.L) {}
 
     __device__ __forceinline__ u64 key(i64 i) const { return ldg(slots + 2 * i); }
     __device__ __forceinline__ i64 predict_slot(u64 k) const {
-        return grmi_slot_of_pos(model.pos(u64_to_f64(k)), n, L);
+        return slot_of(model.pos(u64_to_f64(k)));
     }
     __device__ __forceinline__ bool real(i64 i, u64 pay) const {
         if (payload_nonzero) return pay != 0;
         return (__ldg(bitmap + (i >> 5)) >> (i & 31)) & 1u;
+    }
+
+    // first real slot >= i, or L (bitmap words: 32 slots per load)
+    __device__ __forceinline__ i64 next_real(i64 i) const {
+        if (i >= L) return L;
+        i64 w = i >> 5;
+        const i64 nw = (L + 31) >> 5;
+        u32 v = __ldg(bitmap + w) & (0xffffffffu << (i & 31));
+        while (v == 0) {
+            if (++w >= nw) return L;
+            v = __ldg(bitmap + w);
+        }
+        const i64 r = (w << 5) + __ffs((int)v) - 1;
+        return r < L ? r : L;
+    }
+    // last real slot <= i, or -1
+    __device__ __forceinline__ i64 prev_real(i64 i) const {
+        i64 w = i >> 5;
+        u32 v = __ldg(bitmap + w) & (0xffffffffu >> (31 - (i & 31)));
+        while (v == 0) {
+            if (--w < 0) return -1;
+            v = __ldg(bitmap + w);
+        }
+        return (w << 5) + 31 - __clz((int)v);
+    }
+    // The real entries of the equal-key run that contains slot s (gapped.py:
+    // 163-203), folded into the checksum of t = payload + ps.  Gap slots copy
+    // the real key to their left (k_grmi_fill), so the key changes only at
+    // real slots and the walk visits real slots only, whatever the run length.
+    __device__ __forceinline__ void gather_run(i64 s, u64 k, u64 ps, u64 &cnt, u64 &sum, u64 &x) const {
+        i64 r = prev_real(s);
+        if (r < 0) r = next_real(s);  // s before the first entry: its copies
+        for (;;) {                    // equal real keys to the left (duplicates)
+            const i64 q = r > 0 ? prev_real(r - 1) : -1;
+            if (q < 0 || key(q) != k) break;
+            r = q;
+        }
+        for (; r < L; r = next_real(r + 1)) {
+            const ulonglong2 e = ldg2(slots + 2 * r);
+            if (e.x != k) break;
+            const u64 t = e.y + ps;
+            ++cnt;
+            sum += t;
+            x ^= t;
+        }
     }
 
     // gapped.py:86-160 -- exponential search from `start`, one lane per
@@ -155,168 +205,9 @@ __global__ void __launch_bounds__(NT) k_grmi_probe(GrmiDev g, In in, i64 nk, u64
         u64 k, ps;
         in.get(t, k, ps);
         i64 probes;
-        i64 s = g.search(g.predict_slot(k), k, probes);
+        const i64 s = g.search(g.predict_slot(k), k, probes);
         steps += (u64)probes;
-        if (s < 0) continue;
-        while (s > 0 && g.key(s - 1) == k) --s;  // leftmost slot of the run is real
-        for (; s < g.L; ++s) {
-            ulonglong2 e = ldg2(g.slots + 2 * s);
-            if (e.x != k) break;
-            if (!g.real(s, e.y)) continue;
-            u64 v = e.y + ps;
-            ++cnt;
-            sum += v;
-            x ^= v;
-        }
-    }
-    reduce_checksum(cnt, sum, x, steps, out);
-}
-
-// K1 v2: the same per-probe semantics as k_grmi_probe, restructured so a
-// warp never waits for its slowest search.  Every lane runs the reference's
-// search (gapped.py:86-160) as a state machine that issues exactly ONE
-// dependent load per loop iteration (leaf record, or one gapped slot); a
-// lane whose probe finishes pops the next probe from a per-warp queue in
-// shared memory, which the warp refills with coalesced, evict-first loads of
-// S.  Work per warp therefore tracks the MEAN search length, not the max,
-// and every iteration keeps 32 independent loads in flight per warp.
-enum : int { PH_IDLE = 0, PH_LEAF, PH_FIRST, PH_RIGHT, PH_LEFT, PH_BIN, PH_VERIFY, PH_WL, PH_SCAN };
-
-template <int NT>
-__global__ void __launch_bounds__(NT) k_grmi_probe_sm(GrmiDev g, const u64 *__restrict__ skeys,
-                                                      const u64 *__restrict__ spay, i64 nk, u64 *out) {
-    constexpr int QN = 64;  // probes queued per warp
-    __shared__ ulonglong2 q[NT / 32][QN];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const unsigned lt = (1u << lane) - 1u;
-    const i64 L = g.L;
-    i64 next = ((i64)blockIdx.x * (NT / 32) + w) * 32;
-    const i64 wstride = (i64)gridDim.x * NT;
-    unsigned qh = 0, qt = 0;
-    int ph = PH_IDLE;
-    u64 k = 0, ps = 0;
-    i64 start = 0, step = 0, lo = 0, hi = 0, cur = 0;  // lo doubles as the reference's `prev`
-    unsigned probes = 0;
-    u64 cnt = 0, sum = 0, x = 0, steps = 0;
-    for (;;) {
-        if (qt - qh <= (unsigned)(QN - 32) && next < nk) {  // warp-uniform refill
-            i64 i = next + lane;
-            if (i < nk) q[w][(qt + lane) & (QN - 1)] = make_ulonglong2(ld_stream(skeys + i), ld_stream(spay + i));
-            qt += (unsigned)min((i64)32, nk - next);
-            next += wstride;
-            __syncwarp();
-        }
-        const unsigned idle = __ballot_sync(0xffffffffu, ph == PH_IDLE);
-        const unsigned avail = qt - qh;
-        if (ph == PH_IDLE) {
-            unsigned r = __popc(idle & lt);
-            if (r < avail) {
-                ulonglong2 e = q[w][(qh + r) & (QN - 1)];
-                k = e.x;
-                ps = e.y;
-                ph = PH_LEAF;
-            }
-        }
-        qh += min((unsigned)__popc(idle), avail);
-        __syncwarp();
-        if (__ballot_sync(0xffffffffu, ph != PH_IDLE) == 0 && qh == qt && next >= nk) break;
-        if (ph == PH_LEAF) {
-            // models.py:112-124 + gapped.py:258-261 (one leaf-record load)
-            double xf = u64_to_f64(k);
-            LjLeaf lf = load_leaf(g.model.leaves, g.model.route(xf));
-            start = grmi_slot_of_pos(rmi_leaf_pos(lf, xf), g.n, L);
-            cur = start;
-            ph = PH_FIRST;
-            continue;
-        }
-        if (ph == PH_IDLE) continue;
-        const ulonglong2 e = ldg2(g.slots + 2 * cur);
-        bool found = false, bsetup = false;
-        switch (ph) {
-            case PH_FIRST:
-                probes = 1;
-                if (e.x == k) {
-                    found = true;
-                } else if (e.x < k) {
-                    lo = start;  // prev
-                    step = 1;
-                    if (start + 1 >= L) { lo = start + 1; hi = L; bsetup = true; }
-                    else { cur = start + 1; ph = PH_RIGHT; }
-                } else {
-                    lo = start;  // prev
-                    step = 1;
-                    if (start - 1 < 0) { lo = 0; hi = start; bsetup = true; }
-                    else { cur = start - 1; ph = PH_LEFT; }
-                }
-                break;
-            case PH_RIGHT:
-                ++probes;
-                if (e.x < k) {
-                    lo = cur;
-                    step <<= 1;
-                    if (start + step >= L) { lo = lo + 1; hi = L; bsetup = true; }
-                    else cur = start + step;
-                } else if (e.x == k) {
-                    found = true;
-                } else {
-                    lo = lo + 1;
-                    hi = cur;
-                    bsetup = true;
-                }
-                break;
-            case PH_LEFT:
-                ++probes;
-                if (e.x > k) {
-                    lo = cur;
-                    step <<= 1;
-                    if (start - step < 0) { hi = lo; lo = 0; bsetup = true; }
-                    else cur = start - step;
-                } else if (e.x == k) {
-                    found = true;
-                } else {
-                    hi = lo;
-                    lo = cur + 1;
-                    bsetup = true;
-                }
-                break;
-            case PH_BIN:
-                ++probes;
-                if (e.x < k) lo = cur + 1; else hi = cur;
-                bsetup = true;
-                break;
-            case PH_VERIFY:
-                ++probes;
-                if (e.x == k) found = true;
-                else { steps += probes; ph = PH_IDLE; }
-                break;
-            case PH_WL:  // walk to the leftmost slot of the equal run
-                if (e.x == k && cur > 0) --cur;
-                else { cur = e.x == k ? cur : cur + 1; ph = PH_SCAN; }
-                break;
-            case PH_SCAN:  // gather the real entries of the run
-                if (e.x != k) {
-                    ph = PH_IDLE;
-                } else {
-                    if (g.real(cur, e.y)) {
-                        u64 v = e.y + ps;
-                        ++cnt;
-                        sum += v;
-                        x ^= v;
-                    }
-                    if (++cur >= L) ph = PH_IDLE;
-                }
-                break;
-        }
-        if (bsetup) {
-            if (lo < hi) { cur = (lo + hi) >> 1; ph = PH_BIN; }
-            else if (lo < L) { cur = lo; ph = PH_VERIFY; }
-            else { steps += probes; ph = PH_IDLE; }
-        }
-        if (found) {
-            steps += probes;
-            if (cur > 0) { --cur; ph = PH_WL; }
-            else ph = PH_SCAN;
-        }
+        if (s >= 0) g.gather_run(s, k, ps, cnt, sum, x);
     }
     reduce_checksum(cnt, sum, x, steps, out);
 }
@@ -325,268 +216,267 @@ __global__ void __launch_bounds__(NT) k_grmi_probe_sm(GrmiDev g, const u64 *__re
 //
 // After K4 every window of 2^shift predicted slots has its probes stored
 // contiguously.  A CTA takes a piece of that array; for each window segment
-// of the piece it stages the window's gapped KEYS (+ a halo of STAGE_H slots
-// each side) in shared memory and runs the reference's exponential search
-// (gapped.py:86-160, identical probe counting) there.  A search or run scan
-// that leaves the staged range is redone in global memory from scratch, so
-// results and probe counts never depend on the staging.  Payloads (needed
-// for occupancy and the checksum) are read from global memory, 1-2 per hit.
+// of the piece it stages in shared memory the window's gapped KEYS (+ a halo
+// of STAGE_H slots each side), the matching occupancy-bitmap words, and a
+// 2^STAGE_TB-entry radix table over the staged key range (T[p] = first
+// staged slot whose key prefix >= p).  Per probe:
+//   * lower bound lb of the key: one table pair + a branch-free binary search
+//     whose trip count is fixed per window (the largest table bucket), so a
+//     warp never waits for its slowest lane;
+//   * run [lb, re) of equal keys and its real entries from shared memory;
+//     payloads (for the checksum) from global memory, normally one per hit;
+//   * the reference's probe count (gapped.py:86-160) computed from
+//     (start, lb, re) alone (ref_probe_count), so results and counters are
+//     exactly those of the exponential search from the predicted slot.
+// A lower bound or run that is not provably inside the staged range is
+// redone in global memory from scratch (probe_global).
 
 constexpr int STAGE_NT = 1024;
 constexpr int STAGE_H = 2048;           // halo slots on each side
 constexpr i64 STAGE_PIECE = 65536;      // probes per work item
 constexpr i64 STAGE_MIN = 2048;         // smaller window segments: global search
 constexpr int STAGE_U = 2;              // probes in flight per thread
+constexpr int STAGE_TB = 12;            // radix-table bits
+constexpr int STAGE_TBINS = 1 << STAGE_TB;
+constexpr int STAGE_MAX_SHIFT = 15;     // span < 2^16 (u16 table entries)
 
-// exponential search over any key accessor; kf(i, ok) clears ok when slot i
-// is not available (then the result is meaningless and the caller redoes it)
-template <class KeyF>
-__device__ __forceinline__ i64 exp_search_with(const KeyF &kf, i64 L, i64 start, u64 k, i64 &probes, bool &ok) {
-    probes = 1;
-    u64 v = kf(start, ok);
-    if (v == k) return start;
-    i64 lo, hi;
-    if (v < k) {
-        i64 prev = start, step = 1;
-        for (;;) {
-            i64 idx = start + step;
-            if (idx >= L) { lo = prev + 1; hi = L; break; }
-            ++probes;
-            u64 w = kf(idx, ok);
-            if (!ok) return -1;
-            if (w < k) { prev = idx; step <<= 1; }
-            else if (w == k) return idx;
-            else { lo = prev + 1; hi = idx; break; }
-        }
-    } else {
-        i64 prev = start, step = 1;
-        for (;;) {
-            i64 idx = start - step;
-            if (idx < 0) { lo = 0; hi = prev; break; }
-            ++probes;
-            u64 w = kf(idx, ok);
-            if (!ok) return -1;
-            if (w > k) { prev = idx; step <<= 1; }
-            else if (w == k) return idx;
-            else { lo = idx + 1; hi = prev; break; }
-        }
-    }
-    while (lo < hi) {
-        i64 mid = (lo + hi) >> 1;
-        ++probes;
-        if (kf(mid, ok) < k) lo = mid + 1; else hi = mid;
-        if (!ok) return -1;
-    }
-    if (lo < L) {
-        ++probes;
-        if (kf(lo, ok) == k) return lo;
-    }
-    return -1;
-}
-
-// The reference's probe count (gapped.py:86-160) of an exponential search
-// from `start`, computed without touching memory from the key's position in
-// the sorted gapped array: slots [lb, re) hold the key, slots < lb are
-// smaller, slots >= re larger.  Every comparison the reference makes is
-// decided by where its index falls relative to lb and re.
-__device__ __forceinline__ i64 ref_probe_count(i64 start, i64 lb, i64 re, i64 L) {
-    i64 probes = 1;
-    if (start >= lb && start < re) return 1;
-    i64 lo, hi;
-    if (start < lb) {
-        i64 prev = start, step = 1;
-        for (;;) {
-            const i64 idx = start + step;
-            if (idx >= L) { lo = prev + 1; hi = L; break; }
-            ++probes;
-            if (idx < lb) { prev = idx; step <<= 1; }
-            else if (idx < re) return probes;
-            else { lo = prev + 1; hi = idx; break; }
-        }
-    } else {
-        i64 prev = start, step = 1;
-        for (;;) {
-            const i64 idx = start - step;
-            if (idx < 0) { lo = 0; hi = prev; break; }
-            ++probes;
-            if (idx >= re) { prev = idx; step <<= 1; }
-            else if (idx >= lb) return probes;
-            else { lo = idx + 1; hi = prev; break; }
-        }
-    }
-    while (lo < hi) {
-        const i64 mid = (lo + hi) >> 1;
-        ++probes;
-        if (mid < lb) lo = mid + 1; else hi = mid;
-    }
-    if (lo < L) ++probes;
-    return probes;
-}
-
-struct StagedKeys {
-    const u64 *sk;
-    i64 lo, hi;
-    __device__ __forceinline__ u64 operator()(i64 i, bool &ok) const {
-        if (i < lo || i >= hi) {
-            ok = false;
-            return 0;
-        }
-        return sk[i - lo];
-    }
-};
-
-// one probe against the index: staged search + run scan, global redo on escape
-__device__ __forceinline__ void probe_one(const GrmiDev &g, const StagedKeys &st, u64 k, u64 ps, u64 &cnt, u64 &sum,
+// one probe entirely in global memory (the reference's search, gapped.py:86-160)
+__device__ __noinline__ void probe_global(const GrmiDev &g, i64 start, u64 k, u64 ps, u64 &cnt, u64 &sum,
                                           u64 &x, u64 &steps) {
-    const i64 start = g.predict_slot(k);
     i64 probes;
-    bool ok = true;
-    i64 s = exp_search_with(st, g.L, start, k, probes, ok);
-    u64 c = 0, sm = 0, xx = 0;
-    if (ok && s >= 0) {
-        while (s > 0) {
-            const u64 v = st(s - 1, ok);
-            if (!ok || v != k) break;
-            --s;
-        }
-        for (i64 i = s; ok && i < g.L; ++i) {
-            const u64 v = st(i, ok);
-            if (!ok || v != k) break;
-            const u64 pay = ldg(g.slots + 2 * i + 1);
-            if (!g.real(i, pay)) continue;
-            const u64 t = pay + ps;
-            ++c;
-            sm += t;
-            xx ^= t;
-        }
-    }
-    if (!ok) {  // left the staged range: the plain global-memory probe
-        c = sm = xx = 0;
-        s = g.search(start, k, probes);
-        if (s >= 0) {
-            while (s > 0 && g.key(s - 1) == k) --s;
-            for (; s < g.L; ++s) {
-                const ulonglong2 e = ldg2(g.slots + 2 * s);
-                if (e.x != k) break;
-                if (!g.real(s, e.y)) continue;
-                const u64 t = e.y + ps;
-                ++c;
-                sm += t;
-                xx ^= t;
-            }
-        }
-    }
+    const i64 s = g.search(start, k, probes);
+    if (s >= 0) g.gather_run(s, k, ps, cnt, sum, x);
     steps += (u64)probes;
-    cnt += c;
-    sum += sm;
-    x ^= xx;
+}
+
+static size_t staged_smem_bytes(int shift) {
+    const size_t span = ((size_t)1 << shift) + 2 * STAGE_H;
+    return sizeof(u64) * span + sizeof(u32) * (span / 32 + 2) + sizeof(u16) * (STAGE_TBINS + 2) +
+           sizeof(u16) * (span / 32 + 2);
+}
+
+// first set bit at staged slot >= j (bit of slot i is bm bit i + bo), or
+// span; nz[w] = first nonzero bitmap word >= w (0xffff: none), so long gap
+// runs cost no more than short ones
+__device__ __forceinline__ int next_real(const u32 *bm, const u16 *nz, int nbw, int bo, int j, int span) {
+    const int b = j + bo;
+    int wi = b >> 5;
+    u32 wv = bm[wi] & (0xffffffffu << (b & 31));
+    if (wv == 0) {
+        wi = wi + 1 < nbw ? (int)nz[wi + 1] : nbw;
+        if (wi >= nbw) return span;
+        wv = bm[wi];
+    }
+    return min(span, (wi << 5) + __ffs((int)wv) - 1 - bo);
 }
 
 __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, const ulonglong2 *__restrict__ rec,
                                                                    i64 nk, const i64 *__restrict__ wstarts,
                                                                    int nwin, int shift, unsigned long long *work,
-                                                                   u64 *out) {
-    extern __shared__ u64 sk[];
+                                                                   u64 *out, u64 *trace) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int span_max = (1 << shift) + 2 * STAGE_H;
+    u64 *sk = reinterpret_cast<u64 *>(smem);
+    u32 *bm = reinterpret_cast<u32 *>(sk + span_max);
+    u16 *T = reinterpret_cast<u16 *>(bm + span_max / 32 + 2);
+    u16 *nz = T + STAGE_TBINS + 2;
     __shared__ i64 s_piece;
-    const i64 wsz = (i64)1 << shift;
+    __shared__ int s_max;
+    __shared__ unsigned s_esc, s_iters;
+    __shared__ u32 s_small[2048 / 32];  // windows with < STAGE_MIN probes: global search
+    const int tid = threadIdx.x;
+    for (int j = tid; j < 2048 / 32; j += STAGE_NT) s_small[j] = 0;
+    __syncthreads();
+    for (int w = tid; w < nwin; w += STAGE_NT)
+        if (wstarts[w + 1] - wstarts[w] < STAGE_MIN) atomicOr(&s_small[w >> 5], 1u << (w & 31));
     u64 cnt = 0, sum = 0, x = 0, steps = 0;
-    const StagedKeys none{sk, 0, 0};
     for (;;) {
-        if (threadIdx.x == 0) s_piece = (i64)atomicAdd(work, 1ULL);
+        if (tid == 0) s_piece = (i64)atomicAdd(work, 1ULL);
         __syncthreads();
         const i64 p0 = s_piece * STAGE_PIECE;
         __syncthreads();
         if (p0 >= nk) break;
         const i64 p1 = min(p0 + STAGE_PIECE, nk);
-        // first window overlapping p0
-        int lo = 0, hi = nwin;
-        while (hi - lo > 1) {
-            int mid = (lo + hi) >> 1;
-            if (wstarts[mid] <= p0) lo = mid; else hi = mid;
+        u64 t_begin = 0;
+        if (trace && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
+        int nstaged = 0;
+        if (tid == 0) s_esc = s_iters = 0;
+        int wlo = 0, whi = nwin;  // first window overlapping p0
+        while (whi - wlo > 1) {
+            const int mid = (wlo + whi) >> 1;
+            if (wstarts[mid] <= p0) wlo = mid; else whi = mid;
         }
-        for (int w = lo; w < nwin && wstarts[w] < p1; ++w) {
+        bool any_small = false;
+        for (int w = wlo; w < nwin && wstarts[w] < p1; ++w) {
             const i64 a = max(p0, wstarts[w]), e = min(p1, wstarts[w + 1]);
             if (e <= a) continue;
-            if (e - a >= STAGE_MIN) {
-                const i64 slo = max((i64)0, ((i64)w << shift) - STAGE_H);
-                const i64 shi = min(g.L, (((i64)w + 1) << shift) + STAGE_H);
-                for (i64 i = threadIdx.x; i < shi - slo; i += STAGE_NT) sk[i] = ldg(g.slots + 2 * (slo + i));
+            if ((s_small[w >> 5] >> (w & 31)) & 1u) {
+                any_small = true;
+                continue;
+            }
+            ++nstaged;
+            // ---- stage keys, bitmap words and the radix table of the window
+            const i64 slo = max((i64)0, ((i64)w << shift) - STAGE_H);
+            const i64 shi = min(g.L, (((i64)w + 1) << shift) + STAGE_H);
+            const int span = (int)(shi - slo);
+            for (int i = tid; i < span; i += STAGE_NT) sk[i] = ldg(g.slots + 2 * (slo + i));
+            const i64 w0 = slo >> 5;
+            const int nbw = (int)(((shi - 1) >> 5) - w0 + 1);
+            for (int j = tid; j < nbw; j += STAGE_NT) bm[j] = __ldg(g.bitmap + w0 + j);
+            if (tid == 0) s_max = 0;
+            __syncthreads();
+            const u64 kmin = sk[0], kmax = sk[span - 1];
+            const u64 krange = kmax - kmin;
+            const int sh = krange == 0 ? 0 : max(0, 64 - __clzll((long long)krange) - STAGE_TB);
+            for (int i = tid; i < span; i += STAGE_NT) {
+                const int p = (int)((sk[i] - kmin) >> sh);
+                const int pp = i == 0 ? -1 : (int)((sk[i - 1] - kmin) >> sh);
+                for (int q = pp + 1; q <= p; ++q) T[q] = (u16)i;
+            }
+            for (int q = (int)(krange >> sh) + 1 + tid; q <= STAGE_TBINS; q += STAGE_NT) T[q] = (u16)span;
+            for (int j = tid; j < nbw; j += STAGE_NT) nz[j] = bm[j] ? (u16)j : (u16)0xffff;
+            __syncthreads();
+            // suffix minimum of nz (doubling); nbw <= 2 * STAGE_NT
+            for (int off = 1; off < nbw; off <<= 1) {
+                u16 v[2];
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const int j = tid + r * STAGE_NT;
+                    v[r] = j < nbw ? (j + off < nbw ? min(nz[j], nz[j + off]) : nz[j]) : (u16)0;
+                }
                 __syncthreads();
-                const StagedKeys st{sk, slo, shi};
-                // STAGE_U probes per thread per step, each phase issued for
-                // all of them before the next: the global loads (probe
-                // record, leaf record, payloads) of different probes overlap
-                for (i64 t0 = a + threadIdx.x; t0 < e; t0 += (i64)STAGE_NT * STAGE_U) {
-                    u64 k[STAGE_U], ps[STAGE_U];
-                    i64 start[STAGE_U], s[STAGE_U], probes[STAGE_U];
-                    bool ok[STAGE_U];
 #pragma unroll
-                    for (int u = 0; u < STAGE_U; ++u) {
-                        const i64 t = t0 + (i64)u * STAGE_NT;
-                        ulonglong2 r = t < e ? __ldcs(rec + t) : make_ulonglong2(0, 0);
-                        k[u] = r.x;
-                        ps[u] = r.y;
+                for (int r = 0; r < 2; ++r)
+                    if (tid + r * STAGE_NT < nbw) nz[tid + r * STAGE_NT] = v[r];
+                __syncthreads();
+            }
+            {
+                int mb = 0;
+                for (int q = tid; q < STAGE_TBINS; q += STAGE_NT) mb = max(mb, (int)T[q + 1] - (int)T[q]);
+                mb = __reduce_max_sync(0xffffffffu, mb);
+                if ((tid & 31) == 0 && mb) atomicMax(&s_max, mb);
+            }
+            __syncthreads();
+            const int iters = 32 - __clz(s_max);
+            if (trace && tid == 0) s_iters = max(s_iters, (unsigned)s_max);
+            const int bo = (int)(slo & 31);
+            const int lim = (int)min(g.L - slo, (i64)1 << 30);
+            const int zero = -(int)min(slo, (i64)1 << 30);
+            const bool lo_open = slo > 0, hi_open = shi < g.L;
+            // ---- probes: STAGE_U per thread per step, phase by phase
+            for (i64 t0 = a + tid; t0 < e; t0 += (i64)STAGE_NT * STAGE_U) {
+                u64 k[STAGE_U], ps[STAGE_U];
+                int start[STAGE_U], lo[STAGE_U], len[STAGE_U];
+#pragma unroll
+                for (int u = 0; u < STAGE_U; ++u) {
+                    const i64 t = t0 + (i64)u * STAGE_NT;
+                    const ulonglong2 r = t < e ? __ldcs(rec + t) : make_ulonglong2(kmin, 0);
+                    k[u] = r.x;
+                    ps[u] = r.y;
+                }
+#pragma unroll
+                for (int u = 0; u < STAGE_U; ++u) start[u] = (int)(g.predict_slot(k[u]) - slo);
+#pragma unroll
+                for (int u = 0; u < STAGE_U; ++u) {
+                    if (k[u] < kmin) { lo[u] = 0; len[u] = 0; }
+                    else if (k[u] > kmax) { lo[u] = span; len[u] = 0; }
+                    else {
+                        const int p = (int)((k[u] - kmin) >> sh);
+                        lo[u] = T[p];
+                        len[u] = (int)T[p + 1] - lo[u];
                     }
-#pragma unroll
-                    for (int u = 0; u < STAGE_U; ++u) start[u] = g.predict_slot(k[u]);
-                    // lower bound in the staged keys: a branch-free binary
-                    // search whose trip count is the same for every lane
-                    const i64 span = shi - slo;
+                }
+                for (int it = 0; it < iters; ++it) {
 #pragma unroll
                     for (int u = 0; u < STAGE_U; ++u) {
-                        i64 base = 0, len = span;
-                        while (len > 1) {
-                            const i64 half = len >> 1;
-                            base = sk[base + half - 1] < k[u] ? base + half : base;
-                            len -= half;
+                        const int half = len[u] >> 1;
+                        const bool less = sk[min(lo[u] + half, span - 1)] < k[u];
+                        if (len[u] > 0) {
+                            lo[u] = less ? lo[u] + half + 1 : lo[u];
+                            len[u] = less ? len[u] - half - 1 : half;
                         }
-                        s[u] = slo + base + ((span > 0 && sk[base] < k[u]) ? 1 : 0);  // first slot >= key
-                        // the lower bound is exact only strictly inside the staged range
-                        ok[u] = (s[u] > slo || slo == 0) && (s[u] < shi || shi == g.L);
                     }
-                    // payload of the first slot of the run (a one-slot run is the common case)
-                    u64 pay[STAGE_U];
+                }
 #pragma unroll
-                    for (int u = 0; u < STAGE_U; ++u)
-                        pay[u] = (ok[u] && s[u] < g.L && sk[s[u] - slo] == k[u]) ? ldg(g.slots + 2 * s[u] + 1) : 0;
-#pragma unroll
-                    for (int u = 0; u < STAGE_U; ++u) {
-                        if (t0 + (i64)u * STAGE_NT >= e) continue;
-                        u64 c = 0, sm = 0, xx = 0;
-                        i64 re = s[u];
-                        if (ok[u]) {
-                            for (; re < g.L; ++re) {
-                                if (re >= shi) { ok[u] = false; break; }
-                                if (sk[re - slo] != k[u]) break;
-                                const u64 py = re == s[u] ? pay[u] : ldg(g.slots + 2 * re + 1);
-                                if (!g.real(re, py)) continue;
-                                const u64 tt = py + ps[u];
-                                ++c;
-                                sm += tt;
-                                xx ^= tt;
+                for (int u = 0; u < STAGE_U; ++u) {
+                    if (t0 + (i64)u * STAGE_NT >= e) continue;
+                    const int lb = lo[u];
+                    bool ok = (lb > 0 || !lo_open) && (lb < span || !hi_open);
+                    int re = lb;
+                    u64 c = 0, sm = 0, xx = 0;
+                    if (ok && lb < span && sk[lb] == k[u]) {
+                        // gap slots copy the real key to their left, so the
+                        // key changes only at real slots: walk the real
+                        // slots of the run through the bitmap
+                        int j = lb;
+                        for (;;) {
+                            j = next_real(bm, nz, nbw, bo, j, span);
+                            if (j >= span) {
+                                re = span;
+                                if (hi_open) {  // the run goes on past the staged range
+                                    i64 ja = shi;
+                                    for (;; ++ja) {
+                                        ja = g.next_real(ja);
+                                        if (ja >= g.L) break;
+                                        const ulonglong2 ev = ldg2(g.slots + 2 * ja);
+                                        if (ev.x != k[u]) break;
+                                        const u64 tt = ev.y + ps[u];
+                                        ++c;
+                                        sm += tt;
+                                        xx ^= tt;
+                                    }
+                                    re = (int)min(ja - slo, (i64)1 << 30);
+                                }
+                                break;
                             }
+                            if (sk[j] != k[u]) {
+                                re = j;
+                                break;
+                            }
+                            const u64 tt = ldg(g.slots + 2 * (slo + j) + 1) + ps[u];
+                            ++c;
+                            sm += tt;
+                            xx ^= tt;
+                            ++j;
                         }
-                        if (!ok[u]) {  // outside the staged range: the global-memory probe
-                            probe_one(g, StagedKeys{sk, 0, 0}, k[u], ps[u], cnt, sum, x, steps);
-                            continue;
-                        }
-                        probes[u] = ref_probe_count(start[u], s[u], re, g.L);
-                        steps += (u64)probes[u];
-                        cnt += c;
-                        sum += sm;
-                        x ^= xx;
                     }
+                    if (!ok) {
+                        if (trace) atomicAdd(&s_esc, 1u);
+                        probe_global(g, start[u] + slo, k[u], ps[u], cnt, sum, x, steps);
+                        continue;
+                    }
+                    steps += (u64)ref_probe_count(start[u], lb, re, lim, zero);
+                    cnt += c;
+                    sum += sm;
+                    x ^= xx;
                 }
-                __syncthreads();
-            } else {
-                for (i64 t = a + threadIdx.x; t < e; t += STAGE_NT) {
-                    const ulonglong2 r = __ldcs(rec + t);
-                    probe_one(g, none, r.x, r.y, cnt, sum, x, steps);
-                }
+            }
+            __syncthreads();
+        }
+        if (any_small) {  // block-uniform: every thread walked the same windows
+            for (i64 t = p0 + tid; t < p1; t += STAGE_NT) {
+                const ulonglong2 r = __ldcs(rec + t);
+                const i64 start = g.predict_slot(r.x);
+                const int w = (int)(start >> shift);
+                if ((s_small[w >> 5] >> (w & 31)) & 1u) probe_global(g, start, r.x, r.y, cnt, sum, x, steps);
+            }
+        }
+        if (trace) {
+            __syncthreads();
+            if (tid == 0) {
+                u64 t_end, smid;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+                asm volatile("{ .reg .u32 r; mov.u32 r, %%smid; cvt.u64.u32 %0, r; }" : "=l"(smid));
+                u64 *tr = trace + 6 * (p0 / STAGE_PIECE);
+                tr[0] = t_begin;
+                tr[1] = t_end;
+                tr[2] = smid;
+                tr[3] = (u64)nstaged;
+                tr[4] = (u64)any_small | ((u64)s_iters << 8);
+                tr[5] = (u64)wlo | ((u64)s_esc << 16);
             }
         }
     }
-    (void)wsz;
     reduce_checksum(cnt, sum, x, steps, out);
 }
 
@@ -658,11 +548,11 @@ __global__ void k_grmi_collect(GrmiDev g, const u64 *keys, i64 nk, const i64 *le
 // stretch of the index, so each index sector comes from DRAM ~once.
 struct SlotBin {
     RmiDev m;
-    i64 n, L;
+    SlotMap slot_of;
     int shift;
     __device__ __forceinline__ void prepare() const {}
     __device__ __forceinline__ int operator()(u64 k) const {
-        return (int)(grmi_slot_of_pos(m.pos(u64_to_f64(k)), n, L) >> shift);
+        return (int)(slot_of(m.pos(u64_to_f64(k))) >> shift);
     }
 };
 
@@ -752,12 +642,7 @@ int lj_grmi_probe(const LjGrmi *idx, const uint64_t *s_keys, const uint64_t *s_p
     if (!accumulate) LJ_CK(cudaMemsetAsync(out, 0, 4 * sizeof(u64), st));
     if (nk <= 0 || idx->n == 0) return LJ_OK;
     constexpr int NT = 256;
-    static const int sm_variant = getenv("LJ_K1_SM") ? atoi(getenv("LJ_K1_SM")) : 0;
-    if (sm_variant) {
-        k_grmi_probe_sm<NT><<<grid_for(nk, NT, 6), NT, 0, st>>>(GrmiDev(*idx), s_keys, s_pay, nk, out);
-    } else {
-        k_grmi_probe<NT, SoaIn><<<grid_for(nk, NT, 8), NT, 0, st>>>(GrmiDev(*idx), SoaIn{s_keys, s_pay}, nk, out);
-    }
+    k_grmi_probe<NT, SoaIn><<<grid_for(nk, NT, 8), NT, 0, st>>>(GrmiDev(*idx), SoaIn{s_keys, s_pay}, nk, out);
     LJ_CK_LAUNCH();
     return LJ_OK;
 }
@@ -770,8 +655,9 @@ int lj_grmi_probe_bucketed(const LjGrmi *idx, const uint64_t *s_pairs, int64_t n
     if (nk <= 0 || idx->n == 0) return LJ_OK;
     const int shift = slot_window_shift(idx->L);
     const int nwin = lj_leaf_bucket_bins(idx->L);
-    const size_t sm = sizeof(u64) * (size_t)(((i64)1 << shift) + 2 * STAGE_H);
-    if (sm > 200 * 1024) {  // window too large to stage: plain K1 over the grouped records
+    const size_t sm = staged_smem_bytes(shift);
+    if (shift > STAGE_MAX_SHIFT || sm > 200 * 1024 || idx->bitmap == nullptr) {
+        // window too large to stage: plain K1 over the grouped records
         return lj_grmi_probe_pairs(idx, s_pairs, nk, out, 1, stream);
     }
     static bool attr = false;
@@ -781,9 +667,24 @@ int lj_grmi_probe_bucketed(const LjGrmi *idx, const uint64_t *s_pairs, int64_t n
     }
     unsigned long long *work = reinterpret_cast<unsigned long long *>(ws);
     LJ_CK(cudaMemsetAsync(work, 0, sizeof(unsigned long long), st));
+    // LJ_STAGE_TRACE=<file>: per-piece timing records (diagnostics only)
+    static const char *trace_path = getenv("LJ_STAGE_TRACE");
+    u64 *trace = nullptr;
+    const size_t npieces = (size_t)((nk + STAGE_PIECE - 1) / STAGE_PIECE);
+    if (trace_path) LJ_CK(cudaMalloc(&trace, npieces * 6 * sizeof(u64)));
     k_grmi_probe_staged<<<sm_count(), STAGE_NT, sm, st>>>(GrmiDev(*idx), reinterpret_cast<const ulonglong2 *>(s_pairs),
-                                                          nk, wstarts, nwin, shift, work, out);
+                                                          nk, wstarts, nwin, shift, work, out, trace);
     LJ_CK_LAUNCH();
+    if (trace) {
+        std::vector<u64> h(npieces * 6);
+        LJ_CK(cudaMemcpyAsync(h.data(), trace, h.size() * sizeof(u64), cudaMemcpyDeviceToHost, st));
+        LJ_CK(cudaStreamSynchronize(st));
+        LJ_CK(cudaFree(trace));
+        if (FILE *f = fopen(trace_path, "wb")) {
+            fwrite(h.data(), sizeof(u64), h.size(), f);
+            fclose(f);
+        }
+    }
     return LJ_OK;
 }
 
@@ -835,8 +736,7 @@ int lj_leaf_bucket(const LjGrmi *idx, const uint64_t *keys, const uint64_t *pay,
     LJ_REQUIRE(idx && idx->n >= 1 && idx->L >= 1, "index is empty");
     SlotBin f;
     f.m = RmiDev(idx->model);
-    f.n = idx->n;
-    f.L = idx->L;
+    f.slot_of = SlotMap(idx->n, idx->L);
     f.shift = slot_window_shift(idx->L);
     SoaSrc<SlotBin> src{keys, pay, f};
     return run_partition(src, nk, lj_leaf_bucket_bins(idx->L), reinterpret_cast<ulonglong2 *>(pairs_out),

@@ -345,3 +345,41 @@ def test_buffered_staged_probe_equals_direct(lj, fanout):
     assert buffered == direct
     small = idx.join_checksum_buffered(inp.s.keys[:5000], inp.s.payloads[:5000]).cpu().tolist()
     assert small == idx.join_checksum(inp.s.keys[:5000], inp.s.payloads[:5000]).cpu().tolist()
+
+
+def test_buffered_staged_probe_duplicates_and_zero_payloads(lj):
+    """Staged K1 on an R with long equal-key runs (some longer than the
+    staged halo) and real payloads of 0 (bitmap occupancy): identical to the
+    direct probe and to the oracle (checksum and search_steps)."""
+    rng = np.random.default_rng(11)
+    base = np.unique(rng.integers(0, 2**63, 40000, dtype=np.uint64))
+    reps = rng.integers(1, 4, base.size)
+    reps[::997] = 3000  # runs that cross window + halo boundaries
+    keys = np.repeat(base, reps)
+    pays = rng.integers(0, 5, keys.size, dtype=np.uint64)  # many zeros
+    r = lj.Relation(keys, pays)
+    idx = lj.GappedRmiIndex(2.0, 64).fit(r)
+    assert idx.payload_nonzero == 0
+    sk = np.concatenate([base[rng.integers(0, base.size, 400000)], rng.integers(0, 2**63, 40000, dtype=np.uint64)])
+    sp = rng.integers(0, 2**64 - 1, sk.size, dtype=np.uint64)
+    s = lj.Relation(sk, sp)
+    direct = idx.join_checksum(s.keys, s.payloads).cpu().tolist()
+    buffered = idx.join_checksum_buffered(s.keys, s.payloads).cpu().tolist()
+    assert buffered == direct
+    og = oracle.grmi_build(keys, pays, 2.0, 64, model=oracle.Rmi(
+        idx.rmi.root_slope, idx.rmi.root_intercept, idx.rmi.trained_len, idx.rmi.leaf_slope, idx.rmi.leaf_intercept,
+        idx.rmi.clamp_lo, idx.rmi.clamp_hi, idx.rmi.err_lo, idx.rmi.err_hi))
+    want = oracle.grmi_join(og, sk, sp)
+    assert (direct[0], direct[1] & MASK, direct[2] & MASK, direct[3]) == want
+
+
+def test_spline_hash_grouped_probe_equals_direct(lj):
+    from paper_2111_08824_b200 import configs
+
+    inp = configs.config3(scale=64)
+    idx = lj.SplineHashIndex(32, 18, 4.0).fit(inp.r)
+    direct = idx.join_checksum(inp.s.keys, inp.s.payloads).cpu().tolist()
+    grouped = idx.join_checksum_buffered(inp.s.keys, inp.s.payloads).cpu().tolist()
+    assert grouped == direct
+    want = oracle.smj_checksum(*inp.r.numpy(), *inp.s.numpy())
+    assert (direct[0], direct[1] & MASK, direct[2] & MASK) == want
