@@ -346,8 +346,14 @@ __global__ void __launch_bounds__(SPLIT_NT) k_split_count(LsjDev md, SplitCtx cx
             }
 #pragma unroll
             for (int u = 0; u < SPLIT_U; ++u) {
-                const unsigned peers = __match_any_sync(0xffffffffu, s[u]);
-                if (s[u] >= 0 && lane == __ffs(peers) - 1) atomicAdd(h + s[u], (u32)__popc(peers));
+                // one atomic for a warp on a single slot (runs of a hot key),
+                // else one shared atomic per tuple (match.any is ~10x slower)
+                const int s0 = __shfl_sync(0xffffffffu, s[u], 0);
+                if (__all_sync(0xffffffffu, s[u] == s0)) {
+                    if (lane == 0 && s0 >= 0) atomicAdd(h + s0, 32u);
+                } else if (s[u] >= 0) {
+                    atomicAdd(h + s[u], 1u);
+                }
             }
         }
         __syncthreads();
@@ -424,12 +430,16 @@ __global__ void __launch_bounds__(SPLIT_NT) k_split_scatter(LsjDev md, SplitCtx 
             }
 #pragma unroll
             for (int u = 0; u < SPLIT_U; ++u) {
-                const unsigned peers = __match_any_sync(0xffffffffu, s[u]);
-                const int leader = __ffs(peers) - 1;
-                u32 at = 0;
-                if (s[u] >= 0 && lane == leader) at = atomicAdd(cur + s[u], (u32)__popc(peers));
-                at = __shfl_sync(0xffffffffu, at, leader);
-                if (s[u] >= 0) B[a0 + at + __popc(peers & ((1u << lane) - 1u))] = r[u];
+                const int s0 = __shfl_sync(0xffffffffu, s[u], 0);
+                if (__all_sync(0xffffffffu, s[u] == s0)) {
+                    if (s0 >= 0) {
+                        u32 at = 0;
+                        if (lane == 0) at = atomicAdd(cur + s0, 32u);
+                        B[a0 + __shfl_sync(0xffffffffu, at, 0) + lane] = r[u];
+                    }
+                } else if (s[u] >= 0) {
+                    B[a0 + atomicAdd(cur + s[u], 1u)] = r[u];
+                }
             }
         }
         __syncthreads();
