@@ -179,24 +179,26 @@ int lj_grmi_collect(const LjGrmi *idx, const uint64_t *keys, int64_t nk, const i
                     const int64_t *offsets, uint64_t *out_pay, int64_t *out_src, void *stream);
 
 /* ------------------------------------------------- Request Buffers (K4) */
-/* buffers.py:73-150 analogue: reorder S by RMI leaf (stable counting sort)
- * so that K1 walks the index leaf by leaf.  hist needs m+1 words of
- * device scratch inside ws. */
-/* Request-Buffer analogue: group S by a window of 2^k gapped slots around
- * each key's predicted slot (<= 8192 windows), so that K1 then walks the
- * index window by window.  Counting uses shared-memory-privatised
- * histograms (no per-tuple global atomics).  pairs_out[2nk] interleaved
- * {key, payload} grouped by window, starts_out[bins+1]; order inside a
- * window is unspecified.  bins = lj_leaf_bucket_bins(L). */
+/* Request-Buffer analogue (buffers.py:73-150: the paper buffers requests per
+ * leaf so that lookups walk the index in order).  Groups S by KEY-RANGE
+ * window of 2^shift gapped slots: window w takes the keys k with
+ * W[w] < k <= W[w+1], W[w] the gapped key at slot w * 2^shift, so every
+ * key's lower bound lies inside its window's slot range.  The window is
+ * found from the model's predicted slot (gapped.py:258-261) and corrected by
+ * the neighbouring window keys.  <= 2048 windows (bins =
+ * lj_leaf_bucket_bins(L)); two passes with shared-memory histograms (no
+ * per-tuple global atomics).  pairs_out[2nk] interleaved {key, payload}
+ * grouped by window, starts_out[bins+1]; order inside a window is
+ * unspecified. */
 int lj_leaf_bucket_bins(int64_t L);
 size_t lj_leaf_bucket_workspace_bytes(int64_t nk, int64_t L);
 int lj_leaf_bucket(const LjGrmi *idx, const uint64_t *keys, const uint64_t *pay, int64_t nk,
                    uint64_t *pairs_out, int64_t *starts_out, void *ws, size_t ws_bytes, void *stream);
-/* K1 over the output of lj_leaf_bucket (records + window starts): each
- * CTA stages a window's gapped keys (+halo) in shared memory and searches
- * there; searches leaving the staged range are redone in global memory, so
- * results and search_steps equal lj_grmi_probe's.  ws: 8 bytes of device
- * scratch (work counter). */
+/* K1 over the output of lj_leaf_bucket (records + window starts): each CTA
+ * stages a window's real entries in shared memory and searches there;
+ * results and search_steps equal lj_grmi_probe's (the reference's probe
+ * count follows from the predicted slot and the key's position).  ws: 8
+ * bytes of device scratch (work counter). */
 int lj_grmi_probe_bucketed(const LjGrmi *idx, const uint64_t *s_pairs, int64_t nk, const int64_t *wstarts,
                            void *ws, uint64_t *out, int accumulate, void *stream);
 /* K1 over interleaved {key, payload} probe records (e.g. bucketed S). */

@@ -14,6 +14,7 @@
 
 #include "lj_common.cuh"
 #include "lj_part.cuh"
+#include "lj_pipe.cuh"
 #include "lj_probe_count.h"
 
 namespace lj {
@@ -214,31 +215,38 @@ __global__ void __launch_bounds__(NT) k_grmi_probe(GrmiDev g, In in, i64 nk, u64
 
 // ---------------------------------------------- staged probe (K1 over K4)
 //
-// After K4 every window of 2^shift predicted slots has its probes stored
-// contiguously.  A CTA takes a piece of that array; for each window segment
-// of the piece it stages in shared memory the window's gapped KEYS (+ a halo
-// of STAGE_H slots each side), the matching occupancy-bitmap words, and a
-// 2^STAGE_TB-entry radix table over the staged key range (T[p] = first
-// staged slot whose key prefix >= p).  Per probe:
-//   * lower bound lb of the key: one table pair + a branch-free binary search
-//     whose trip count is fixed per window (the largest table bucket), so a
-//     warp never waits for its slowest lane;
-//   * run [lb, re) of equal keys and its real entries from shared memory;
-//     payloads (for the checksum) from global memory, normally one per hit;
-//   * the reference's probe count (gapped.py:86-160) computed from
-//     (start, lb, re) alone (ref_probe_count), so results and counters are
-//     exactly those of the exponential search from the predicted slot.
-// A lower bound or run that is not provably inside the staged range is
-// redone in global memory from scratch (probe_global).
+// K4 groups S by KEY-RANGE window: window w holds the probes k with
+// W[w] < k <= W[w+1], W[w] = the gapped array's key at slot w * 2^shift.
+// Gapped keys are sorted, so such a key's lower bound lb (first slot with a
+// key >= k) lies in [w * 2^shift, (w+1) * 2^shift]: a window's lookups never
+// leave its slot range, whatever the model's error.
+//
+// A CTA takes a piece of the grouped probes; for each window segment of the
+// piece it stages in shared memory the REAL entries of the window's slot
+// range: keys ck[] and slot offsets cp[], compacted through the occupancy
+// bitmap, a 2^STAGE_TB-entry radix table over the staged key range (T[p] =
+// first entry whose key prefix >= p) and the RMI leaves the range routes to.
+// Gap slots copy the real key to their left (k_grmi_fill), so the gapped
+// array's equal-key runs are described by the real entries alone: with i the
+// first staged entry >= k and j the first > k,
+//   lb = cp[i]   (slots before it in range copy keys <= W[w] < k; slot 0
+//                 when the range starts at slot 0: slots before the first
+//                 entry copy it),
+//   re = cp[j]   (first slot with a key > k; past the range: bitmap walk),
+// the matches are entries i..j-1, and the reference's probe count
+// (gapped.py:86-160) follows from the predicted slot, lb and re alone
+// (ref_probe_count).  Per probe: model evaluation, one table pair plus a
+// branch-free binary search with a per-window trip count, the duplicates
+// scan, one payload load per match.
 
 constexpr int STAGE_NT = 1024;
-constexpr int STAGE_H = 2048;           // halo slots on each side
 constexpr i64 STAGE_PIECE = 65536;      // probes per work item
-constexpr i64 STAGE_MIN = 2048;         // smaller window segments: global search
+constexpr i64 STAGE_MIN = 2048;         // windows with fewer probes: global search
 constexpr int STAGE_U = 2;              // probes in flight per thread
 constexpr int STAGE_TB = 12;            // radix-table bits
 constexpr int STAGE_TBINS = 1 << STAGE_TB;
-constexpr int STAGE_MAX_SHIFT = 15;     // span < 2^16 (u16 table entries)
+constexpr int STAGE_MAX_SHIFT = 14;     // staged range <= 2^14 + 1 slots
+constexpr int STAGE_LEAVES = 1024;      // RMI leaves cached per window
 
 // one probe entirely in global memory (the reference's search, gapped.py:86-160)
 __device__ __noinline__ void probe_global(const GrmiDev &g, i64 start, u64 k, u64 ps, u64 &cnt, u64 &sum,
@@ -250,39 +258,56 @@ __device__ __noinline__ void probe_global(const GrmiDev &g, i64 start, u64 k, u6
 }
 
 static size_t staged_smem_bytes(int shift) {
-    const size_t span = ((size_t)1 << shift) + 2 * STAGE_H;
-    return sizeof(u64) * span + sizeof(u32) * (span / 32 + 2) + sizeof(u16) * (STAGE_TBINS + 2) +
-           sizeof(u16) * (span / 32 + 2);
+    const size_t span = ((size_t)1 << shift) + 1;
+    return ((sizeof(u64) * span + 15) & ~(size_t)15) + ((sizeof(u16) * span + 15) & ~(size_t)15) +
+           sizeof(u16) * (STAGE_TBINS + 8) + sizeof(u32) * (span / 32 + 8) + sizeof(LjLeaf) * STAGE_LEAVES;
 }
 
-// first set bit at staged slot >= j (bit of slot i is bm bit i + bo), or
-// span; nz[w] = first nonzero bitmap word >= w (0xffff: none), so long gap
-// runs cost no more than short ones
-__device__ __forceinline__ int next_real(const u32 *bm, const u16 *nz, int nbw, int bo, int j, int span) {
-    const int b = j + bo;
-    int wi = b >> 5;
-    u32 wv = bm[wi] & (0xffffffffu << (b & 31));
-    if (wv == 0) {
-        wi = wi + 1 < nbw ? (int)nz[wi + 1] : nbw;
-        if (wi >= nbw) return span;
-        wv = bm[wi];
+// exclusive scan of one value per thread over the block; returns the prefix,
+// *total gets the sum (all threads).  wsum: NT/32 + 1 words of shared memory.
+template <int NT>
+__device__ __forceinline__ u32 block_exclusive_scan(u32 v, u32 *wsum, u32 *total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    u32 inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const u32 y = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += y;
     }
-    return min(span, (wi << 5) + __ffs((int)wv) - 1 - bo);
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        const u32 w = lane < NT / 32 ? wsum[lane] : 0;
+        u32 wi = w;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const u32 y = __shfl_up_sync(0xffffffffu, wi, d);
+            if (lane >= d) wi += y;
+        }
+        if (lane < NT / 32) wsum[lane] = wi - w;
+        if (lane == 31) wsum[NT / 32] = wi;
+    }
+    __syncthreads();
+    const u32 r = wsum[warp] + inc - v;
+    *total = wsum[NT / 32];
+    return r;
 }
 
 __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, const ulonglong2 *__restrict__ rec,
                                                                    i64 nk, const i64 *__restrict__ wstarts,
                                                                    int nwin, int shift, unsigned long long *work,
-                                                                   u64 *out, u64 *trace) {
+                                                                   u64 *out, u64 *trace, int exp) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int span_max = (1 << shift) + 2 * STAGE_H;
-    u64 *sk = reinterpret_cast<u64 *>(smem);
-    u32 *bm = reinterpret_cast<u32 *>(sk + span_max);
-    u16 *T = reinterpret_cast<u16 *>(bm + span_max / 32 + 2);
-    u16 *nz = T + STAGE_TBINS + 2;
+    const int span_max = (1 << shift) + 1;
+    u64 *ck = reinterpret_cast<u64 *>(smem);  // real keys of the staged range
+    u16 *cp = reinterpret_cast<u16 *>(smem + ((sizeof(u64) * span_max + 15) & ~(size_t)15));  // slot - slo
+    u16 *T = cp + ((span_max + 7) & ~7);                                                       // radix table
+    u32 *wb = reinterpret_cast<u32 *>(T + STAGE_TBINS + 8);  // bitmap-word prefix counts
+    LjLeaf *lc = reinterpret_cast<LjLeaf *>(wb + ((span_max / 32 + 8) & ~3));  // cached RMI leaves
     __shared__ i64 s_piece;
     __shared__ int s_max;
     __shared__ unsigned s_esc, s_iters;
+    __shared__ u32 s_wsum[STAGE_NT / 32 + 1];
     __shared__ u32 s_small[2048 / 32];  // windows with < STAGE_MIN probes: global search
     const int tid = threadIdx.x;
     for (int j = tid; j < 2048 / 32; j += STAGE_NT) s_small[j] = 0;
@@ -297,7 +322,7 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
         __syncthreads();
         if (p0 >= nk) break;
         const i64 p1 = min(p0 + STAGE_PIECE, nk);
-        u64 t_begin = 0;
+        u64 t_begin = 0, t_stage = 0, t_mark = 0;
         if (trace && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
         int nstaged = 0;
         if (tid == 0) s_esc = s_iters = 0;
@@ -315,41 +340,61 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
                 continue;
             }
             ++nstaged;
-            // ---- stage keys, bitmap words and the radix table of the window
-            const i64 slo = max((i64)0, ((i64)w << shift) - STAGE_H);
-            const i64 shi = min(g.L, (((i64)w + 1) << shift) + STAGE_H);
+            if (trace && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_mark));
+            // ---- stage the real entries of [slo, shi), the radix table, the leaves
+            const i64 slo = (i64)w << shift;
+            const i64 shi = min(g.L, slo + span_max);
             const int span = (int)(shi - slo);
-            for (int i = tid; i < span; i += STAGE_NT) sk[i] = ldg(g.slots + 2 * (slo + i));
             const i64 w0 = slo >> 5;
-            const int nbw = (int)(((shi - 1) >> 5) - w0 + 1);
-            for (int j = tid; j < nbw; j += STAGE_NT) bm[j] = __ldg(g.bitmap + w0 + j);
+            const int bo = (int)(slo & 31);  // staged slot i is bit i + bo of the range's words
+            const int nbw = (span + bo + 31) >> 5;
+            auto word = [&](int j) -> u32 {  // bitmap word j, bits outside [slo, shi) cleared
+                u32 v = __ldg(g.bitmap + w0 + j);
+                if (j == 0) v &= 0xffffffffu << bo;
+                const int top = span + bo - (j << 5);
+                if (top < 32) v &= (1u << top) - 1u;
+                return v;
+            };
+            u32 nc;
+            {
+                const int j0 = 2 * tid;  // nbw <= 2 * STAGE_NT words: two per thread
+                const u32 c0 = j0 < nbw ? __popc(word(j0)) : 0, c1 = j0 + 1 < nbw ? __popc(word(j0 + 1)) : 0;
+                const u32 pre = block_exclusive_scan<STAGE_NT>(c0 + c1, s_wsum, &nc);
+                if (j0 < nbw) wb[j0] = pre;
+                if (j0 + 1 < nbw) wb[j0 + 1] = pre + c0;
+            }
             if (tid == 0) s_max = 0;
             __syncthreads();
-            const u64 kmin = sk[0], kmax = sk[span - 1];
+            for (int i = tid; i < span; i += STAGE_NT) {
+                const int b = i + bo;
+                const u32 v = word(b >> 5);
+                if ((v >> (b & 31)) & 1u) {
+                    const u32 idx = wb[b >> 5] + __popc(v & ((1u << (b & 31)) - 1u));
+                    ck[idx] = ldg(g.slots + 2 * (slo + i));
+                    cp[idx] = (u16)i;
+                }
+            }
+            __syncthreads();
+            const int n_c = (int)nc;
+            const u64 kmin = n_c ? ck[0] : 0, kmax = n_c ? ck[n_c - 1] : 0;
             const u64 krange = kmax - kmin;
             const int sh = krange == 0 ? 0 : max(0, 64 - __clzll((long long)krange) - STAGE_TB);
-            for (int i = tid; i < span; i += STAGE_NT) {
-                const int p = (int)((sk[i] - kmin) >> sh);
-                const int pp = i == 0 ? -1 : (int)((sk[i - 1] - kmin) >> sh);
+            for (int i = tid; i < n_c; i += STAGE_NT) {
+                const int p = (int)((ck[i] - kmin) >> sh);
+                const int pp = i == 0 ? -1 : (int)((ck[i - 1] - kmin) >> sh);
                 for (int q = pp + 1; q <= p; ++q) T[q] = (u16)i;
             }
-            for (int q = (int)(krange >> sh) + 1 + tid; q <= STAGE_TBINS; q += STAGE_NT) T[q] = (u16)span;
-            for (int j = tid; j < nbw; j += STAGE_NT) nz[j] = bm[j] ? (u16)j : (u16)0xffff;
-            __syncthreads();
-            // suffix minimum of nz (doubling); nbw <= 2 * STAGE_NT
-            for (int off = 1; off < nbw; off <<= 1) {
-                u16 v[2];
-#pragma unroll
-                for (int r = 0; r < 2; ++r) {
-                    const int j = tid + r * STAGE_NT;
-                    v[r] = j < nbw ? (j + off < nbw ? min(nz[j], nz[j + off]) : nz[j]) : (u16)0;
-                }
-                __syncthreads();
-#pragma unroll
-                for (int r = 0; r < 2; ++r)
-                    if (tid + r * STAGE_NT < nbw) nz[tid + r * STAGE_NT] = v[r];
-                __syncthreads();
+            for (int q = (n_c ? (int)(krange >> sh) + 1 : 0) + tid; q <= STAGE_TBINS; q += STAGE_NT) T[q] = (u16)n_c;
+            // leaves the staged keys route to (+ a margin); probes routed elsewhere
+            // read their leaf from global memory
+            i64 lc_lo = 0, lc_hi = -1;
+            if (n_c) {
+                lc_lo = max((i64)0, g.model.route(u64_to_f64(kmin)) - 8);
+                lc_hi = min(g.model.m - 1, g.model.route(u64_to_f64(kmax)) + 8);
+                lc_hi = min(lc_hi, lc_lo + STAGE_LEAVES - 1);
+                for (i64 l = lc_lo + tid; l <= lc_hi; l += STAGE_NT) lc[l - lc_lo] = load_leaf(g.model.leaves, l);
             }
+            __syncthreads();
             {
                 int mb = 0;
                 for (int q = tid; q < STAGE_TBINS; q += STAGE_NT) mb = max(mb, (int)T[q + 1] - (int)T[q]);
@@ -358,11 +403,15 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
             }
             __syncthreads();
             const int iters = 32 - __clz(s_max);
-            if (trace && tid == 0) s_iters = max(s_iters, (unsigned)s_max);
-            const int bo = (int)(slo & 31);
+            if (trace && tid == 0) {
+                s_iters = max(s_iters, (unsigned)s_max);
+                u64 t_now;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
+                t_stage += t_now - t_mark;
+            }
             const int lim = (int)min(g.L - slo, (i64)1 << 30);
             const int zero = -(int)min(slo, (i64)1 << 30);
-            const bool lo_open = slo > 0, hi_open = shi < g.L;
+            const bool hi_open = shi < g.L;
             // ---- probes: STAGE_U per thread per step, phase by phase
             for (i64 t0 = a + tid; t0 < e; t0 += (i64)STAGE_NT * STAGE_U) {
                 u64 k[STAGE_U], ps[STAGE_U];
@@ -374,78 +423,84 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
                     k[u] = r.x;
                     ps[u] = r.y;
                 }
+                if (exp & 1) {
 #pragma unroll
-                for (int u = 0; u < STAGE_U; ++u) start[u] = (int)(g.predict_slot(k[u]) - slo);
+                    for (int u = 0; u < STAGE_U; ++u) start[u] = (int)(k[u] & 1023);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < STAGE_U; ++u) {
+                        // models.py:112-124 + gapped.py:258-261, the leaf from smem
+                        const double xf = u64_to_f64(k[u]);
+                        const i64 l = g.model.route(xf);
+                        const LjLeaf lf = (l >= lc_lo && l <= lc_hi) ? lc[l - lc_lo] : load_leaf(g.model.leaves, l);
+                        start[u] = (int)max(g.slot_of(rmi_leaf_pos(lf, xf)) - slo, (i64)-(1 << 30));
+                    }
+                }
 #pragma unroll
                 for (int u = 0; u < STAGE_U; ++u) {
-                    if (k[u] < kmin) { lo[u] = 0; len[u] = 0; }
-                    else if (k[u] > kmax) { lo[u] = span; len[u] = 0; }
+                    if (n_c == 0 || k[u] < kmin) { lo[u] = 0; len[u] = 0; }
+                    else if (k[u] > kmax) { lo[u] = n_c; len[u] = 0; }
                     else {
                         const int p = (int)((k[u] - kmin) >> sh);
                         lo[u] = T[p];
                         len[u] = (int)T[p + 1] - lo[u];
                     }
                 }
-                for (int it = 0; it < iters; ++it) {
+                for (int it = 0; it < ((exp & 2) ? 0 : iters); ++it) {
 #pragma unroll
                     for (int u = 0; u < STAGE_U; ++u) {
                         const int half = len[u] >> 1;
-                        const bool less = sk[min(lo[u] + half, span - 1)] < k[u];
+                        const bool less = ck[max(min(lo[u] + half, n_c - 1), 0)] < k[u];
                         if (len[u] > 0) {
                             lo[u] = less ? lo[u] + half + 1 : lo[u];
                             len[u] = less ? len[u] - half - 1 : half;
                         }
                     }
                 }
+                // payload of the first match of every probe, all in flight at once
+                u64 pay0[STAGE_U];
+#pragma unroll
+                for (int u = 0; u < STAGE_U; ++u)
+                    pay0[u] = (!(exp & 4) && lo[u] < n_c && ck[lo[u]] == k[u]) ? ldg(g.slots + 2 * (slo + cp[lo[u]]) + 1)
+                                                                              : 0;
 #pragma unroll
                 for (int u = 0; u < STAGE_U; ++u) {
                     if (t0 + (i64)u * STAGE_NT >= e) continue;
-                    const int lb = lo[u];
-                    bool ok = (lb > 0 || !lo_open) && (lb < span || !hi_open);
-                    int re = lb;
-                    u64 c = 0, sm = 0, xx = 0;
-                    if (ok && lb < span && sk[lb] == k[u]) {
-                        // gap slots copy the real key to their left, so the
-                        // key changes only at real slots: walk the real
-                        // slots of the run through the bitmap
-                        int j = lb;
-                        for (;;) {
-                            j = next_real(bm, nz, nbw, bo, j, span);
-                            if (j >= span) {
-                                re = span;
-                                if (hi_open) {  // the run goes on past the staged range
-                                    i64 ja = shi;
-                                    for (;; ++ja) {
-                                        ja = g.next_real(ja);
-                                        if (ja >= g.L) break;
-                                        const ulonglong2 ev = ldg2(g.slots + 2 * ja);
-                                        if (ev.x != k[u]) break;
-                                        const u64 tt = ev.y + ps[u];
-                                        ++c;
-                                        sm += tt;
-                                        xx ^= tt;
-                                    }
-                                    re = (int)min(ja - slo, (i64)1 << 30);
-                                }
-                                break;
-                            }
-                            if (sk[j] != k[u]) {
-                                re = j;
-                                break;
-                            }
-                            const u64 tt = ldg(g.slots + 2 * (slo + j) + 1) + ps[u];
-                            ++c;
-                            sm += tt;
-                            xx ^= tt;
-                            ++j;
-                        }
-                    }
-                    if (!ok) {
+                    const int il = lo[u];
+                    if (il == n_c && hi_open) {  // cannot happen for a key-range window; kept as a guard
                         if (trace) atomicAdd(&s_esc, 1u);
                         probe_global(g, start[u] + slo, k[u], ps[u], cnt, sum, x, steps);
                         continue;
                     }
-                    steps += (u64)ref_probe_count(start[u], lb, re, lim, zero);
+                    u64 c = 0, sm = 0, xx = 0;
+                    int iu = il;
+                    for (; !(exp & 4) && iu < n_c && ck[iu] == k[u]; ++iu) {
+                        const u64 tt = (iu == il ? pay0[u] : ldg(g.slots + 2 * (slo + cp[iu]) + 1)) + ps[u];
+                        ++c;
+                        sm += tt;
+                        xx ^= tt;
+                    }
+                    const int lb = (il == 0 && slo == 0) ? 0 : (il < n_c ? (int)cp[il] : span);
+                    int re;
+                    if (iu < n_c) {
+                        re = cp[iu];
+                    } else if (!hi_open || iu == il) {
+                        re = iu == il ? lb : span;
+                    } else {  // the run goes on past the staged range
+                        i64 ja = shi;
+                        for (;; ++ja) {
+                            ja = g.next_real(ja);
+                            if (ja >= g.L) break;
+                            const ulonglong2 ev = ldg2(g.slots + 2 * ja);
+                            if (ev.x != k[u]) break;
+                            const u64 tt = ev.y + ps[u];
+                            ++c;
+                            sm += tt;
+                            xx ^= tt;
+                        }
+                        re = (int)min(ja - slo, (i64)1 << 30);
+                    }
+                    steps += (exp & 8) ? (u64)(lb + re) : (u64)ref_probe_count(start[u], lb, re, lim, zero);
                     cnt += c;
                     sum += sm;
                     x ^= xx;
@@ -453,12 +508,17 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
             }
             __syncthreads();
         }
+        if (trace && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_mark));
         if (any_small) {  // block-uniform: every thread walked the same windows
             for (i64 t = p0 + tid; t < p1; t += STAGE_NT) {
+                int lo = wlo, hi = nwin;  // window of probe t
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (__ldg(wstarts + mid) <= t) lo = mid; else hi = mid;
+                }
+                if (!((s_small[lo >> 5] >> (lo & 31)) & 1u)) continue;
                 const ulonglong2 r = __ldcs(rec + t);
-                const i64 start = g.predict_slot(r.x);
-                const int w = (int)(start >> shift);
-                if ((s_small[w >> 5] >> (w & 31)) & 1u) probe_global(g, start, r.x, r.y, cnt, sum, x, steps);
+                probe_global(g, g.predict_slot(r.x), r.x, r.y, cnt, sum, x, steps);
             }
         }
         if (trace) {
@@ -467,13 +527,15 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
                 u64 t_end, smid;
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
                 asm volatile("{ .reg .u32 r; mov.u32 r, %%smid; cvt.u64.u32 %0, r; }" : "=l"(smid));
-                u64 *tr = trace + 6 * (p0 / STAGE_PIECE);
+                u64 *tr = trace + 8 * (p0 / STAGE_PIECE);
                 tr[0] = t_begin;
                 tr[1] = t_end;
                 tr[2] = smid;
                 tr[3] = (u64)nstaged;
                 tr[4] = (u64)any_small | ((u64)s_iters << 8);
                 tr[5] = (u64)wlo | ((u64)s_esc << 16);
+                tr[6] = t_stage;
+                tr[7] = t_end - t_mark;
             }
         }
     }
@@ -540,21 +602,50 @@ __global__ void k_grmi_collect(GrmiDev g, const u64 *keys, i64 nk, const i64 *le
 
 // ------------------------------------------------------- leaf bucket (K4)
 
-// Bin = window of 2^shift gapped slots around the PREDICTED slot of the key
-// (gapped.py:258-261).  A leaf-based grouping is useless on skewed keys:
-// the linear root routes most lognormal keys to a handful of huge leaves.
-// Predicted-slot windows (<= 2048 bins, e.g. 16384 slots = 256 KB at C2) make
-// every warp's searches after bucketing stay inside one L1/L2-resident
-// stretch of the index, so each index sector comes from DRAM ~once.
+// Bin = KEY-RANGE window of 2^wshift gapped slots: the w with
+// wk[w] < k <= wk[w+1], wk[w] = gapped key at slot w << wshift (wk[0] = -inf,
+// wk[nwin] = +inf).  A key's lower bound then lies inside its window's slot
+// range, whatever the model's error (see the staged probe).  The window is
+// the one of the model's PREDICTED slot (gapped.py:258-261), corrected by
+// the neighbouring window keys held in shared memory (0-1 steps for all but
+// the model's worst misses).  A branch-free search over the window keys
+// alone measured 2x slower (shared-memory bank conflicts, 11 dependent
+// steps).  A leaf-based grouping is useless on skewed keys: the linear root
+// routes most lognormal keys to a handful of huge leaves.  <= 2048 windows
+// (256 KB of index each at C2).
 struct SlotBin {
     RmiDev m;
     SlotMap slot_of;
-    int shift;
-    __device__ __forceinline__ void prepare() const {}
-    __device__ __forceinline__ int operator()(u64 k) const {
-        return (int)(slot_of(m.pos(u64_to_f64(k))) >> shift);
+    int wshift, nwin;
+    const u64 *wk;
+    int shift = 0;  // code = window
+    __host__ __device__ int smem_words() const { return nwin; }
+    __device__ void stage(u64 *dst) const {
+        for (int i = threadIdx.x; i < nwin; i += blockDim.x) dst[i] = wk[i];
+    }
+    __device__ __forceinline__ SlotBin at(u64 *tab) const {
+        SlotBin c = *this;
+        c.wk = tab;
+        return c;
+    }
+    __device__ __forceinline__ u32 code(u64 k) const {
+        int w = (int)(slot_of(m.pos(u64_to_f64(k))) >> wshift);
+        const u64 a = w > 0 ? wk[w] : 0, b = w + 1 < nwin ? wk[w + 1] : ~0ULL;
+        if (w > 0 && a >= k) {
+            --w;
+            while (w > 0 && wk[w] >= k) --w;
+        } else if (w + 1 < nwin && b < k) {
+            ++w;
+            while (w + 1 < nwin && wk[w + 1] < k) ++w;
+        }
+        return (u32)w;
     }
 };
+
+__global__ void k_window_keys(const u64 *slots, int nwin, int wshift, u64 *wk) {
+    for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nwin; w += gridDim.x * blockDim.x)
+        wk[w] = slots[2 * ((i64)w << wshift)];
+}
 
 static int slot_window_shift(i64 L) {
     int s = 0;
@@ -656,27 +747,30 @@ int lj_grmi_probe_bucketed(const LjGrmi *idx, const uint64_t *s_pairs, int64_t n
     const int shift = slot_window_shift(idx->L);
     const int nwin = lj_leaf_bucket_bins(idx->L);
     const size_t sm = staged_smem_bytes(shift);
-    if (shift > STAGE_MAX_SHIFT || sm > 200 * 1024 || idx->bitmap == nullptr) {
+    if (shift > STAGE_MAX_SHIFT || sm > 220 * 1024 || idx->bitmap == nullptr) {
         // window too large to stage: plain K1 over the grouped records
         return lj_grmi_probe_pairs(idx, s_pairs, nk, out, 1, stream);
     }
     static bool attr = false;
     if (!attr) {
-        LJ_CK(cudaFuncSetAttribute(k_grmi_probe_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        LJ_CK(cudaFuncSetAttribute(k_grmi_probe_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
         attr = true;
     }
     unsigned long long *work = reinterpret_cast<unsigned long long *>(ws);
     LJ_CK(cudaMemsetAsync(work, 0, sizeof(unsigned long long), st));
     // LJ_STAGE_TRACE=<file>: per-piece timing records (diagnostics only)
     static const char *trace_path = getenv("LJ_STAGE_TRACE");
+    // LJ_STAGE_EXP=<mask>: timing experiments that skip parts of the probe
+    // (results are then wrong): 1 predict, 2 search, 4 run scan, 8 probe count
+    static const int exp = getenv("LJ_STAGE_EXP") ? atoi(getenv("LJ_STAGE_EXP")) : 0;
     u64 *trace = nullptr;
     const size_t npieces = (size_t)((nk + STAGE_PIECE - 1) / STAGE_PIECE);
-    if (trace_path) LJ_CK(cudaMalloc(&trace, npieces * 6 * sizeof(u64)));
+    if (trace_path) LJ_CK(cudaMalloc(&trace, npieces * 8 * sizeof(u64)));
     k_grmi_probe_staged<<<sm_count(), STAGE_NT, sm, st>>>(GrmiDev(*idx), reinterpret_cast<const ulonglong2 *>(s_pairs),
-                                                          nk, wstarts, nwin, shift, work, out, trace);
+                                                          nk, wstarts, nwin, shift, work, out, trace, exp);
     LJ_CK_LAUNCH();
     if (trace) {
-        std::vector<u64> h(npieces * 6);
+        std::vector<u64> h(npieces * 8);
         LJ_CK(cudaMemcpyAsync(h.data(), trace, h.size() * sizeof(u64), cudaMemcpyDeviceToHost, st));
         LJ_CK(cudaStreamSynchronize(st));
         LJ_CK(cudaFree(trace));
@@ -728,19 +822,29 @@ int lj_leaf_bucket_bins(int64_t L) {
 }
 
 size_t lj_leaf_bucket_workspace_bytes(int64_t nk, int64_t L) {
-    return part_workspace_bytes(nk, lj_leaf_bucket_bins(L));
+    return part_workspace_bytes(nk, lj_leaf_bucket_bins(L)) + al(sizeof(u64) * (size_t)lj_leaf_bucket_bins(L));
 }
 
 int lj_leaf_bucket(const LjGrmi *idx, const uint64_t *keys, const uint64_t *pay, int64_t nk, uint64_t *pairs_out,
                    int64_t *starts_out, void *ws, size_t ws_bytes, void *stream) {
     LJ_REQUIRE(idx && idx->n >= 1 && idx->L >= 1, "index is empty");
+    if (ws_bytes < lj_leaf_bucket_workspace_bytes(nk, idx->L)) {
+        set_error("lj_leaf_bucket: workspace too small");
+        return LJ_E_WORKSPACE;
+    }
+    cudaStream_t st = as_stream(stream);
+    const int nwin = lj_leaf_bucket_bins(idx->L);
+    const size_t pws = part_workspace_bytes(nk, nwin);
     SlotBin f;
     f.m = RmiDev(idx->model);
     f.slot_of = SlotMap(idx->n, idx->L);
-    f.shift = slot_window_shift(idx->L);
+    f.wshift = slot_window_shift(idx->L);
+    f.nwin = nwin;
+    f.wk = reinterpret_cast<const u64 *>((char *)ws + pws);
+    k_window_keys<<<(nwin + 255) / 256, 256, 0, st>>>(idx->slots, nwin, f.wshift, (u64 *)f.wk);
+    LJ_CK_LAUNCH();
     SoaSrc<SlotBin> src{keys, pay, f};
-    return run_partition(src, nk, lj_leaf_bucket_bins(idx->L), reinterpret_cast<ulonglong2 *>(pairs_out),
-                         starts_out, ws, ws_bytes, as_stream(stream));
+    return run_partition(src, nk, nwin, reinterpret_cast<ulonglong2 *>(pairs_out), starts_out, nullptr, ws, pws, st);
 }
 
 }  // extern "C"

@@ -90,10 +90,11 @@ static LsjDev make_lsj(const LjLsjModel &md) {
     return d;
 }
 
-struct LsjBin {
+struct LsjBin : NoTable {
     LsjDev d;
-    __device__ __forceinline__ void prepare() const {}
-    __device__ __forceinline__ int operator()(u64 k) const { return d.bin(k); }
+    int shift = 0;
+    __device__ __forceinline__ u32 code(u64 k) const { return (u32)d.bin(k); }
+    __device__ __forceinline__ LsjBin at(u64 *) const { return *this; }
 };
 
 // spos[i] = pos(sample[i]) (sample sorted -> spos non-decreasing)
@@ -852,9 +853,10 @@ size_t lj_lsj_partition_workspace_bytes(int64_t n, int64_t nbins) { return part_
 int lj_lsj_partition(const LjLsjModel *md, const uint64_t *keys, const uint64_t *pay, int64_t n, uint64_t *pairs,
                      int64_t *starts, void *ws, size_t ws_bytes, void *stream) {
     LJ_REQUIRE(md && md->table && md->pb && md->nbins >= 1, "model has no bins");
-    LsjBin f{make_lsj(*md)};
+    LsjBin f;
+    f.d = make_lsj(*md);
     SoaSrc<LsjBin> src{keys, pay, f};
-    return run_partition(src, n, (int)md->nbins, reinterpret_cast<ulonglong2 *>(pairs), starts, ws, ws_bytes,
+    return run_partition(src, n, (int)md->nbins, reinterpret_cast<ulonglong2 *>(pairs), starts, nullptr, ws, ws_bytes,
                          as_stream(stream));
 }
 

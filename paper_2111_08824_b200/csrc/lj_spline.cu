@@ -248,16 +248,17 @@ int lj_spline_hash_probe(const LjSplineHash *idx, const uint64_t *s_keys, const 
 
 // Request-Buffer analogue for the learned hash: group S by a window of
 // predicted positions (<= 2048 windows), shared-memory-privatised partition.
-struct PosBin {
+struct PosBin : NoTable {
     SplineDev m;
     i64 nb, n;
     double rn;
-    __device__ __forceinline__ void prepare() const {}
-    __device__ __forceinline__ int operator()(u64 k) const {
+    int shift = 0;
+    __device__ __forceinline__ u32 code(u64 k) const {
         const i64 p = m.pos(k);  // in [0, n)
         i64 b = (i64)(__dmul_rn(i64_to_f64(p), rn));
-        return (int)(b < 0 ? 0 : (b >= nb ? nb - 1 : b));
+        return (u32)(b < 0 ? 0 : (b >= nb ? nb - 1 : b));
     }
+    __device__ __forceinline__ PosBin at(u64 *) const { return *this; }
 };
 
 static int hash_bins(i64 n) { return (int)(n < 2048 ? (n < 1 ? 1 : n) : 2048); }
@@ -273,7 +274,8 @@ int lj_spline_hash_bucket(const LjSplineHash *idx, const uint64_t *keys, const u
     f.n = idx->model.n;
     f.rn = (double)f.nb / (double)idx->model.n;
     SoaSrc<PosBin> src{keys, pay, f};
-    return run_partition(src, nk, (int)f.nb, reinterpret_cast<ulonglong2 *>(pairs_out), starts_out, ws, ws_bytes,
+    return run_partition(src, nk, (int)f.nb, reinterpret_cast<ulonglong2 *>(pairs_out), starts_out, nullptr, ws,
+                         ws_bytes,
                          as_stream(stream));
 }
 
