@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cmath>
 #include <string>
 
 #include "../../include/lj_b200.h"
@@ -93,18 +94,22 @@ __device__ __forceinline__ u64 ld_stream(const u64 *p) {
 // ------------------------------------------------------------------ RMI
 
 // models.py:112-114: leaf = clip(floor(rs*x + ri), 0, m-1)
+// floor + clip in f64 + x86 cast == saturating cvt.rmi + integer clamp for
+// every raw (NaN: both end at 0 after the clamp; NaN parameters would index
+// out of bounds in the reference, the clamp keeps the device safe)
 __device__ __forceinline__ i64 rmi_route(double rs, double ri, i64 m, double x) {
-    double raw = __dadd_rn(__dmul_rn(rs, x), ri);
-    i64 l = f64_to_i64(clip_f64(floor(raw), 0.0, i64_to_f64(m - 1)));
-    // NaN parameters would index out of bounds in the reference as well;
-    // keep the device safe.
+    const double raw = __dadd_rn(__dmul_rn(rs, x), ri);
+    const i64 l = __double2ll_rd(raw);
     return l < 0 ? 0 : (l >= m ? m - 1 : l);
 }
 
 // models.py:121-124: pos = clip(rint(slope*x + icpt), clamp_lo, clamp_hi)
+// (x86 cast of rint(raw)) == cvt.rni(raw) whenever raw is in [-2^63, 2^63)
+// (doubles that close to 2^63 are integers); else the cast's INT64_MIN
 __device__ __forceinline__ i64 rmi_leaf_pos(const LjLeaf &lf, double x) {
-    double raw = __dadd_rn(__dmul_rn(lf.slope, x), lf.icpt);
-    return clip_i64(f64_to_i64(rint(raw)), lf.clamp_lo, lf.clamp_hi);
+    const double raw = __dadd_rn(__dmul_rn(lf.slope, x), lf.icpt);
+    const i64 p = (raw >= -9223372036854775808.0 && raw < 9223372036854775808.0) ? __double2ll_rn(raw) : INT64_MIN;
+    return clip_i64(p, lf.clamp_lo, lf.clamp_hi);
 }
 
 __device__ __forceinline__ LjLeaf load_leaf(const LjLeaf *leaves, i64 l) {
@@ -158,12 +163,15 @@ struct SlotMap {
     double c, g, top;
     __host__ SlotMap() {}
     __host__ SlotMap(i64 n_, i64 L_)
-        : n(n_), L(L_), c(n_ > 0 ? (double)L_ / (double)n_ : 0.0), g(ldexp((double)L_, -47)),
-          top((double)(L_ - 1)) {}
+        : n(n_), L(L_), c(n_ > 0 ? (double)L_ / (double)n_ : 0.0),
+          g(L_ < ((i64)1 << 52) ? ldexp((double)L_, -47) : INFINITY), top((double)(L_ - 1)) {}
     __device__ __forceinline__ i64 operator()(i64 pos) const {
         const double z = __dmul_rn(i64_to_f64(pos), c);
         const double f = __dadd_rn(z, -floor(z));
-        if (fabs(__dadd_rn(f, -0.5)) > g) return f64_to_i64(clip_f64(rint(z), 0.0, top));
+        if (fabs(__dadd_rn(f, -0.5)) > g) {  // rint + clip + cast, z finite, L - 1 exact
+            const i64 r = __double2ll_rn(z);
+            return r < 0 ? 0 : (r > L - 1 ? L - 1 : r);
+        }
         return grmi_slot_of_pos(pos, n, L);
     }
 };

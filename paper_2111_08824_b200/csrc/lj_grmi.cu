@@ -223,45 +223,54 @@ __global__ void __launch_bounds__(NT) k_grmi_probe(GrmiDev g, In in, i64 nk, u64
 //
 // A CTA takes a piece of the grouped probes; for each window segment of the
 // piece it stages in shared memory the REAL entries of the window's slot
-// range: keys ck[] and slot offsets cp[], compacted through the occupancy
-// bitmap, a 2^STAGE_TB-entry radix table over the staged key range (T[p] =
-// first entry whose key prefix >= p) and the RMI leaves the range routes to.
-// Gap slots copy the real key to their left (k_grmi_fill), so the gapped
-// array's equal-key runs are described by the real entries alone: with i the
-// first staged entry >= k and j the first > k,
+// range: keys ck[] and slot offsets cp[] (compacted through the occupancy
+// bitmap, with a sentinel entry at n_c), a 2^STAGE_TB-entry radix table over
+// the staged key range (T[p] = first entry whose key prefix >= p) and the
+// RMI leaves the range routes to.  Gap slots copy the real key to their left
+// (k_grmi_fill), so the gapped array's equal-key runs are described by the
+// real entries alone: with i the first staged entry >= k and j the first > k,
 //   lb = cp[i]   (slots before it in range copy keys <= W[w] < k; slot 0
 //                 when the range starts at slot 0: slots before the first
 //                 entry copy it),
 //   re = cp[j]   (first slot with a key > k; past the range: bitmap walk),
 // the matches are entries i..j-1, and the reference's probe count
 // (gapped.py:86-160) follows from the predicted slot, lb and re alone
-// (ref_probe_count).  Per probe: model evaluation, one table pair plus a
-// branch-free binary search with a per-window trip count, the duplicates
-// scan, one payload load per match.
+// (ref_probe_count).  Per probe: model evaluation (leaf from shared memory),
+// one table pair plus a fixed-trip branch-free binary search, one payload
+// load per match.
 
 constexpr int STAGE_NT = 1024;
-constexpr i64 STAGE_PIECE = 65536;      // probes per work item
+constexpr int STAGE_PIECE = 65536;      // probes per work item
 constexpr i64 STAGE_MIN = 2048;         // windows with fewer probes: global search
 constexpr int STAGE_U = 2;              // probes in flight per thread
 constexpr int STAGE_TB = 12;            // radix-table bits
 constexpr int STAGE_TBINS = 1 << STAGE_TB;
 constexpr int STAGE_MAX_SHIFT = 14;     // staged range <= 2^14 + 1 slots
+constexpr int STAGE_SPAN = (1 << STAGE_MAX_SHIFT) + 1;
 constexpr int STAGE_LEAVES = 1024;      // RMI leaves cached per window
+// fixed shared-memory layout (bytes), sized for the largest window
+constexpr int SO_CK = 0;                                                  // u64 [SPAN + 1]
+constexpr int SO_CP = (SO_CK + 8 * (STAGE_SPAN + 1) + 15) & ~15;          // u16 [SPAN + 1]
+constexpr int SO_T = (SO_CP + 2 * (STAGE_SPAN + 1) + 15) & ~15;           // u16 [TBINS + 1]
+constexpr int SO_WB = (SO_T + 2 * (STAGE_TBINS + 1) + 15) & ~15;          // u32 [SPAN / 32 + 2]
+constexpr int SO_LC = (SO_WB + 4 * (STAGE_SPAN / 32 + 2) + 15) & ~15;     // LjLeaf [LEAVES]
+constexpr int SO_END = SO_LC + 32 * STAGE_LEAVES;
+
+struct Acc4 {
+    u64 c, s, x, st;
+};
 
 // one probe entirely in global memory (the reference's search, gapped.py:86-160)
-__device__ __noinline__ void probe_global(const GrmiDev &g, i64 start, u64 k, u64 ps, u64 &cnt, u64 &sum,
-                                          u64 &x, u64 &steps) {
+__device__ __noinline__ Acc4 probe_global(const GrmiDev &g, i64 start, u64 k, u64 ps) {
+    Acc4 a{0, 0, 0, 0};
     i64 probes;
     const i64 s = g.search(start, k, probes);
-    if (s >= 0) g.gather_run(s, k, ps, cnt, sum, x);
-    steps += (u64)probes;
+    if (s >= 0) g.gather_run(s, k, ps, a.c, a.s, a.x);
+    a.st = (u64)probes;
+    return a;
 }
 
-static size_t staged_smem_bytes(int shift) {
-    const size_t span = ((size_t)1 << shift) + 1;
-    return ((sizeof(u64) * span + 15) & ~(size_t)15) + ((sizeof(u16) * span + 15) & ~(size_t)15) +
-           sizeof(u16) * (STAGE_TBINS + 8) + sizeof(u32) * (span / 32 + 8) + sizeof(LjLeaf) * STAGE_LEAVES;
-}
+static size_t staged_smem_bytes(int) { return SO_END; }
 
 // exclusive scan of one value per thread over the block; returns the prefix,
 // *total gets the sum (all threads).  wsum: NT/32 + 1 words of shared memory.
@@ -296,17 +305,15 @@ __device__ __forceinline__ u32 block_exclusive_scan(u32 v, u32 *wsum, u32 *total
 __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, const ulonglong2 *__restrict__ rec,
                                                                    i64 nk, const i64 *__restrict__ wstarts,
                                                                    int nwin, int shift, unsigned long long *work,
-                                                                   u64 *out, u64 *trace, int exp) {
+                                                                   u64 *out, u64 *trace, i64 *dbg) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int span_max = (1 << shift) + 1;
-    u64 *ck = reinterpret_cast<u64 *>(smem);  // real keys of the staged range
-    u16 *cp = reinterpret_cast<u16 *>(smem + ((sizeof(u64) * span_max + 15) & ~(size_t)15));  // slot - slo
-    u16 *T = cp + ((span_max + 7) & ~7);                                                       // radix table
-    u32 *wb = reinterpret_cast<u32 *>(T + STAGE_TBINS + 8);  // bitmap-word prefix counts
-    LjLeaf *lc = reinterpret_cast<LjLeaf *>(wb + ((span_max / 32 + 8) & ~3));  // cached RMI leaves
-    __shared__ i64 s_piece;
+    u64 *ck = reinterpret_cast<u64 *>(smem + SO_CK);    // real keys of the staged range (+ sentinel)
+    u16 *cp = reinterpret_cast<u16 *>(smem + SO_CP);    // their slot offsets (+ sentinel: span)
+    u16 *T = reinterpret_cast<u16 *>(smem + SO_T);      // radix table over ck
+    u32 *wb = reinterpret_cast<u32 *>(smem + SO_WB);    // bitmap-word prefix counts
+    LjLeaf *lc = reinterpret_cast<LjLeaf *>(smem + SO_LC);  // cached RMI leaves
+    __shared__ i64 s_piece, s_f0;
     __shared__ int s_max;
-    __shared__ unsigned s_esc, s_iters;
     __shared__ u32 s_wsum[STAGE_NT / 32 + 1];
     __shared__ u32 s_small[2048 / 32];  // windows with < STAGE_MIN probes: global search
     const int tid = threadIdx.x;
@@ -314,6 +321,7 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
     __syncthreads();
     for (int w = tid; w < nwin; w += STAGE_NT)
         if (wstarts[w + 1] - wstarts[w] < STAGE_MIN) atomicOr(&s_small[w >> 5], 1u << (w & 31));
+    const int span_max = (1 << shift) + 1;
     u64 cnt = 0, sum = 0, x = 0, steps = 0;
     for (;;) {
         if (tid == 0) s_piece = (i64)atomicAdd(work, 1ULL);
@@ -325,7 +333,6 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
         u64 t_begin = 0, t_stage = 0, t_mark = 0;
         if (trace && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
         int nstaged = 0;
-        if (tid == 0) s_esc = s_iters = 0;
         int wlo = 0, whi = nwin;  // first window overlapping p0
         while (whi - wlo > 1) {
             const int mid = (wlo + whi) >> 1;
@@ -374,8 +381,14 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
                     cp[idx] = (u16)i;
                 }
             }
-            __syncthreads();
             const int n_c = (int)nc;
+            if (tid == 0) {
+                ck[n_c] = ~0ULL;  // sentinel: larger than every key (keys < 2^64 - 1)
+                cp[n_c] = (u16)span;
+                // window 0 with no entry: every slot copies entry 0 (gapped.py:250-252)
+                s_f0 = (slo == 0 && n_c == 0) ? g.next_real(shi) : -1;
+            }
+            __syncthreads();
             const u64 kmin = n_c ? ck[0] : 0, kmax = n_c ? ck[n_c - 1] : 0;
             const u64 krange = kmax - kmin;
             const int sh = krange == 0 ? 0 : max(0, 64 - __clzll((long long)krange) - STAGE_TB);
@@ -387,12 +400,13 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
             for (int q = (n_c ? (int)(krange >> sh) + 1 : 0) + tid; q <= STAGE_TBINS; q += STAGE_NT) T[q] = (u16)n_c;
             // leaves the staged keys route to (+ a margin); probes routed elsewhere
             // read their leaf from global memory
-            i64 lc_lo = 0, lc_hi = -1;
+            int lc_lo = 0, lc_n = 0;
             if (n_c) {
-                lc_lo = max((i64)0, g.model.route(u64_to_f64(kmin)) - 8);
-                lc_hi = min(g.model.m - 1, g.model.route(u64_to_f64(kmax)) + 8);
-                lc_hi = min(lc_hi, lc_lo + STAGE_LEAVES - 1);
-                for (i64 l = lc_lo + tid; l <= lc_hi; l += STAGE_NT) lc[l - lc_lo] = load_leaf(g.model.leaves, l);
+                const i64 l0 = max((i64)0, g.model.route(u64_to_f64(kmin)) - 8);
+                const i64 l1 = min(g.model.m - 1, g.model.route(u64_to_f64(kmax)) + 8);
+                lc_lo = (int)l0;
+                lc_n = (int)min(l1 - l0 + 1, (i64)STAGE_LEAVES);
+                for (int l = tid; l < lc_n; l += STAGE_NT) lc[l] = load_leaf(g.model.leaves, l0 + l);
             }
             __syncthreads();
             {
@@ -402,108 +416,131 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
                 if ((tid & 31) == 0 && mb) atomicMax(&s_max, mb);
             }
             __syncthreads();
-            const int iters = 32 - __clz(s_max);
+            const int iters = 32 - __clz(s_max);  // lower-bound steps for the largest bucket
             if (trace && tid == 0) {
-                s_iters = max(s_iters, (unsigned)s_max);
                 u64 t_now;
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
                 t_stage += t_now - t_mark;
             }
-            const int lim = (int)min(g.L - slo, (i64)1 << 30);
-            const int zero = -(int)min(slo, (i64)1 << 30);
+            const int lim = (int)(g.L - slo), zero = -(int)slo;  // L < 2^30 on this path
             const bool hi_open = shi < g.L;
+            const ulonglong2 *wrec = rec + a;
+            const u64 *wpay = g.slots + 2 * slo + 1;  // payload of staged slot i: wpay[2 * i]
+            const int ne = (int)(e - a);
             // ---- probes: STAGE_U per thread per step, phase by phase
-            for (i64 t0 = a + tid; t0 < e; t0 += (i64)STAGE_NT * STAGE_U) {
+            for (int t0 = tid; t0 < ne; t0 += STAGE_NT * STAGE_U) {
                 u64 k[STAGE_U], ps[STAGE_U];
                 int start[STAGE_U], lo[STAGE_U], len[STAGE_U];
 #pragma unroll
                 for (int u = 0; u < STAGE_U; ++u) {
-                    const i64 t = t0 + (i64)u * STAGE_NT;
-                    const ulonglong2 r = t < e ? __ldcs(rec + t) : make_ulonglong2(kmin, 0);
+                    const int t = t0 + u * STAGE_NT;
+                    const ulonglong2 r = t < ne ? __ldcs(wrec + t) : make_ulonglong2(kmin, 0);
                     k[u] = r.x;
                     ps[u] = r.y;
                 }
-                if (exp & 1) {
-#pragma unroll
-                    for (int u = 0; u < STAGE_U; ++u) start[u] = (int)(k[u] & 1023);
-                } else {
-#pragma unroll
-                    for (int u = 0; u < STAGE_U; ++u) {
-                        // models.py:112-124 + gapped.py:258-261, the leaf from smem
-                        const double xf = u64_to_f64(k[u]);
-                        const i64 l = g.model.route(xf);
-                        const LjLeaf lf = (l >= lc_lo && l <= lc_hi) ? lc[l - lc_lo] : load_leaf(g.model.leaves, l);
-                        start[u] = (int)max(g.slot_of(rmi_leaf_pos(lf, xf)) - slo, (i64)-(1 << 30));
-                    }
-                }
 #pragma unroll
                 for (int u = 0; u < STAGE_U; ++u) {
-                    if (n_c == 0 || k[u] < kmin) { lo[u] = 0; len[u] = 0; }
-                    else if (k[u] > kmax) { lo[u] = n_c; len[u] = 0; }
-                    else {
-                        const int p = (int)((k[u] - kmin) >> sh);
-                        lo[u] = T[p];
-                        len[u] = (int)T[p + 1] - lo[u];
-                    }
+                    // models.py:112-124 + gapped.py:258-261, the leaf from smem
+                    const double xf = u64_to_f64(k[u]);
+                    const int l = (int)g.model.route(xf) - lc_lo;
+                    const LjLeaf lf = ((unsigned)l < (unsigned)lc_n) ? lc[l] : load_leaf(g.model.leaves, l + lc_lo);
+                    start[u] = (int)(g.slot_of(rmi_leaf_pos(lf, xf)) - slo);
                 }
-                for (int it = 0; it < ((exp & 2) ? 0 : iters); ++it) {
 #pragma unroll
-                    for (int u = 0; u < STAGE_U; ++u) {
+                for (int u = 0; u < STAGE_U; ++u) {  // table pair (branch-free)
+                    const bool below = k[u] < kmin, above = k[u] > kmax;
+                    const u64 d = k[u] - kmin;
+                    const int p = (int)((d < krange ? d : krange) >> sh);
+                    const int t_lo = T[p], t_hi = T[p + 1];
+                    lo[u] = below ? 0 : (above ? n_c : t_lo);
+                    len[u] = (below || above) ? 0 : t_hi - t_lo;
+                }
+                for (int it = 0; it < iters; ++it) {
+#pragma unroll
+                    for (int u = 0; u < STAGE_U; ++u) {  // lower bound, no branches
                         const int half = len[u] >> 1;
-                        const bool less = ck[max(min(lo[u] + half, n_c - 1), 0)] < k[u];
-                        if (len[u] > 0) {
-                            lo[u] = less ? lo[u] + half + 1 : lo[u];
-                            len[u] = less ? len[u] - half - 1 : half;
-                        }
+                        const bool go = len[u] > 0 && ck[lo[u] + half] < k[u];
+                        lo[u] = go ? lo[u] + half + 1 : lo[u];
+                        len[u] = go ? len[u] - half - 1 : half;
                     }
                 }
-                // payload of the first match of every probe, all in flight at once
+                // first match of every probe and its payload, all in flight at once
+                bool m0[STAGE_U];
                 u64 pay0[STAGE_U];
 #pragma unroll
-                for (int u = 0; u < STAGE_U; ++u)
-                    pay0[u] = (!(exp & 4) && lo[u] < n_c && ck[lo[u]] == k[u]) ? ldg(g.slots + 2 * (slo + cp[lo[u]]) + 1)
-                                                                              : 0;
+                for (int u = 0; u < STAGE_U; ++u) {
+                    m0[u] = ck[lo[u]] == k[u];
+                    pay0[u] = m0[u] ? ldg(wpay + 2 * cp[lo[u]]) : 0;
+                }
 #pragma unroll
                 for (int u = 0; u < STAGE_U; ++u) {
-                    if (t0 + (i64)u * STAGE_NT >= e) continue;
+                    if (t0 + u * STAGE_NT >= ne) continue;
                     const int il = lo[u];
-                    if (il == n_c && hi_open) {  // cannot happen for a key-range window; kept as a guard
-                        if (trace) atomicAdd(&s_esc, 1u);
-                        probe_global(g, start[u] + slo, k[u], ps[u], cnt, sum, x, steps);
+                    if (il == n_c && hi_open) {
+                        // no staged entry >= k: window 0 before the first entry
+                        // (its slots copy entry 0 and k <= entry 0), else a guard
+                        const i64 f0 = s_f0;
+                        if (f0 < 0 || f0 >= g.L) {
+                            const Acc4 ac = probe_global(g, start[u] + slo, k[u], ps[u]);
+                            cnt += ac.c;
+                            sum += ac.s;
+                            x ^= ac.x;
+                            steps += ac.st;
+                            continue;
+                        }
+                        i64 ja = f0;  // k == entry 0: entry 0 and its duplicates
+                        for (;; ++ja) {
+                            ja = g.next_real(ja);
+                            if (ja >= g.L) break;
+                            const ulonglong2 ev = ldg2(g.slots + 2 * ja);
+                            if (ev.x != k[u]) break;
+                            const u64 t2 = ev.y + ps[u];
+                            ++cnt;
+                            sum += t2;
+                            x ^= t2;
+                        }
+                        const int re0 = ja == f0 ? 0 : (int)ja;  // absent (k < entry 0): [0, 0)
+                        steps += (u64)ref_probe_count(start[u], 0, re0, lim, zero);
                         continue;
                     }
-                    u64 c = 0, sm = 0, xx = 0;
                     int iu = il;
-                    for (; !(exp & 4) && iu < n_c && ck[iu] == k[u]; ++iu) {
-                        const u64 tt = (iu == il ? pay0[u] : ldg(g.slots + 2 * (slo + cp[iu]) + 1)) + ps[u];
-                        ++c;
-                        sm += tt;
-                        xx ^= tt;
+                    const u64 cnt_before = cnt;
+                    if (m0[u]) {
+                        const u64 tt = pay0[u] + ps[u];
+                        ++cnt;
+                        sum += tt;
+                        x ^= tt;
+                        for (iu = il + 1; ck[iu] == k[u]; ++iu) {  // duplicate keys in R
+                            const u64 t2 = ldg(wpay + 2 * cp[iu]) + ps[u];
+                            ++cnt;
+                            sum += t2;
+                            x ^= t2;
+                        }
                     }
-                    const int lb = (il == 0 && slo == 0) ? 0 : (il < n_c ? (int)cp[il] : span);
-                    int re;
-                    if (iu < n_c) {
-                        re = cp[iu];
-                    } else if (!hi_open || iu == il) {
-                        re = iu == il ? lb : span;
-                    } else {  // the run goes on past the staged range
+                    const int lb = (il == 0 && slo == 0) ? 0 : (int)cp[il];
+                    int re = cp[iu];
+                    if (iu == n_c && iu > il && hi_open) {  // the run goes on past the staged range
                         i64 ja = shi;
                         for (;; ++ja) {
                             ja = g.next_real(ja);
                             if (ja >= g.L) break;
                             const ulonglong2 ev = ldg2(g.slots + 2 * ja);
                             if (ev.x != k[u]) break;
-                            const u64 tt = ev.y + ps[u];
-                            ++c;
-                            sm += tt;
-                            xx ^= tt;
+                            const u64 t2 = ev.y + ps[u];
+                            ++cnt;
+                            sum += t2;
+                            x ^= t2;
                         }
-                        re = (int)min(ja - slo, (i64)1 << 30);
+                        re = (int)(ja - slo);
                     }
-                    steps += (exp & 8) ? (u64)(lb + re) : (u64)ref_probe_count(start[u], lb, re, lim, zero);
-                    cnt += c;
-                    sum += sm;
-                    x ^= xx;
+                    steps += (u64)ref_probe_count(start[u], lb, re, lim, zero);
+                    if (dbg) {
+                        i64 *dp = dbg + 4 * (a + t0 + u * STAGE_NT);
+                        dp[0] = lb + slo;
+                        dp[1] = re + slo;
+                        dp[2] = (i64)(cnt - cnt_before);
+                        dp[3] = (i64)k[u];
+                    }
                 }
             }
             __syncthreads();
@@ -518,7 +555,11 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
                 }
                 if (!((s_small[lo >> 5] >> (lo & 31)) & 1u)) continue;
                 const ulonglong2 r = __ldcs(rec + t);
-                probe_global(g, g.predict_slot(r.x), r.x, r.y, cnt, sum, x, steps);
+                const Acc4 ac = probe_global(g, g.predict_slot(r.x), r.x, r.y);
+                cnt += ac.c;
+                sum += ac.s;
+                x ^= ac.x;
+                steps += ac.st;
             }
         }
         if (trace) {
@@ -532,8 +573,8 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
                 tr[1] = t_end;
                 tr[2] = smid;
                 tr[3] = (u64)nstaged;
-                tr[4] = (u64)any_small | ((u64)s_iters << 8);
-                tr[5] = (u64)wlo | ((u64)s_esc << 16);
+                tr[4] = (u64)any_small;
+                tr[5] = (u64)wlo;
                 tr[6] = t_stage;
                 tr[7] = t_end - t_mark;
             }
@@ -747,7 +788,7 @@ int lj_grmi_probe_bucketed(const LjGrmi *idx, const uint64_t *s_pairs, int64_t n
     const int shift = slot_window_shift(idx->L);
     const int nwin = lj_leaf_bucket_bins(idx->L);
     const size_t sm = staged_smem_bytes(shift);
-    if (shift > STAGE_MAX_SHIFT || sm > 220 * 1024 || idx->bitmap == nullptr) {
+    if (shift > STAGE_MAX_SHIFT || sm > 220 * 1024 || idx->bitmap == nullptr || idx->L >= ((int64_t)1 << 30)) {
         // window too large to stage: plain K1 over the grouped records
         return lj_grmi_probe_pairs(idx, s_pairs, nk, out, 1, stream);
     }
@@ -760,15 +801,29 @@ int lj_grmi_probe_bucketed(const LjGrmi *idx, const uint64_t *s_pairs, int64_t n
     LJ_CK(cudaMemsetAsync(work, 0, sizeof(unsigned long long), st));
     // LJ_STAGE_TRACE=<file>: per-piece timing records (diagnostics only)
     static const char *trace_path = getenv("LJ_STAGE_TRACE");
-    // LJ_STAGE_EXP=<mask>: timing experiments that skip parts of the probe
-    // (results are then wrong): 1 predict, 2 search, 4 run scan, 8 probe count
-    static const int exp = getenv("LJ_STAGE_EXP") ? atoi(getenv("LJ_STAGE_EXP")) : 0;
     u64 *trace = nullptr;
     const size_t npieces = (size_t)((nk + STAGE_PIECE - 1) / STAGE_PIECE);
     if (trace_path) LJ_CK(cudaMalloc(&trace, npieces * 8 * sizeof(u64)));
+    // LJ_STAGE_DEBUG=<file>: per-probe (lb, re, matches, key) of staged probes (diagnostics only)
+    static const char *dbg_path = getenv("LJ_STAGE_DEBUG");
+    i64 *dbg = nullptr;
+    if (dbg_path) {
+        LJ_CK(cudaMalloc(&dbg, (size_t)nk * 4 * sizeof(i64)));
+        LJ_CK(cudaMemsetAsync(dbg, 0xff, (size_t)nk * 4 * sizeof(i64), st));
+    }
     k_grmi_probe_staged<<<sm_count(), STAGE_NT, sm, st>>>(GrmiDev(*idx), reinterpret_cast<const ulonglong2 *>(s_pairs),
-                                                          nk, wstarts, nwin, shift, work, out, trace, exp);
+                                                          nk, wstarts, nwin, shift, work, out, trace, dbg);
     LJ_CK_LAUNCH();
+    if (dbg) {
+        std::vector<i64> h((size_t)nk * 4);
+        LJ_CK(cudaMemcpyAsync(h.data(), dbg, h.size() * sizeof(i64), cudaMemcpyDeviceToHost, st));
+        LJ_CK(cudaStreamSynchronize(st));
+        LJ_CK(cudaFree(dbg));
+        if (FILE *f = fopen(dbg_path, "wb")) {
+            fwrite(h.data(), sizeof(i64), h.size(), f);
+            fclose(f);
+        }
+    }
     if (trace) {
         std::vector<u64> h(npieces * 8);
         LJ_CK(cudaMemcpyAsync(h.data(), trace, h.size() * sizeof(u64), cudaMemcpyDeviceToHost, st));
