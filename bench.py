@@ -116,32 +116,86 @@ def build_index(inp):
     return None  # lsj builds nothing ahead of time: it is timed end to end
 
 
+DEFAULT_VARIANT = {"c1": "direct", "c2": "buffered", "c3": "direct"}
+
+
+class Step:
+    """One step of the hot path: `parts` run in order on the current stream;
+    `dominant` names the part the roofline is reported for and `dom_bytes`
+    its algorithmic bytes per launch."""
+
+    def __init__(self, parts, dominant, dom_bytes, kernel, bytes_note):
+        self.parts, self.dominant, self.dom_bytes = parts, dominant, dom_bytes
+        self.kernel, self.bytes_note = kernel, bytes_note
+        self.last_breakdown = None
+
+    def __call__(self, out):
+        for _, fn in self.parts:
+            fn(out)
+        return out
+
+
 def make_step(inp, index, variant="buffered"):
-    """-> (step(out), kernel_name, algorithmic bytes of one step).  A step
-    is one pass of the hot path over the whole S (INLJ, index prebuilt as
-    in the reference) or the whole LSJ (sample, fit, partition, sort, join)."""
+    """A step is one pass of the hot path over the whole S (INLJ, index
+    prebuilt as in the reference, bench.py:138-144 of the reference) or the
+    whole LSJ (sample, fit, partition, sort, join)."""
     import paper_2111_08824_b200 as lj
 
     n_r, n_s = len(inp.r), len(inp.s)
     if index is not None:
         keys, pays = inp.s.keys, inp.s.payloads
+        grmi = "grmi" in inp.algorithm
         if variant == "buffered":
             scratch = index.bucket_scratch(n_s)
-            name = ("k_bin_hist+k_bin_scatter+k_grmi_probe_staged" if "grmi" in inp.algorithm
-                    else "k_bin_hist+k_bin_scatter+k_hash_probe<grouped>")
-            return ((lambda out: index.join_checksum_buffered(keys, pays, out=out, scratch=scratch)),
-                    name + " (Request-Buffer analogue)", ALGO_BYTES[inp.algorithm] * n_s)
-        name = "k_grmi_probe" if "grmi" in inp.algorithm else "k_hash_probe"
-        return (lambda out: index.join_checksum(keys, pays, out=out)), name, ALGO_BYTES[inp.algorithm] * n_s
+            parts = [("bucket", lambda out: index.bucket_records(keys, pays, scratch)),
+                     ("probe", lambda out: index.probe_records(n_s, scratch, out))]
+            kern = "k_grmi_probe_staged" if grmi else "k_hash_probe<grouped>"
+            return Step(parts, "probe", 32 * n_s, kern,
+                        f"32 B/probe x {n_s} probes (16 B S record + 16 B R entry); the K4 bucketing "
+                        "(k_bin_hist_tma + k_bin_scatter_tma) runs before it in the step")
+        fn = (lambda out: index.join_checksum(keys, pays, out=out))
+        return Step([("probe", fn)], "probe", 32 * n_s, "k_grmi_probe" if grmi else "k_hash_probe",
+                    f"32 B/probe x {n_s} probes (16 B S record + 16 B R entry)")
     o = dict(lj.DEFAULT_OPTS, **inp.opts)
     cfg = lj.LsjConfig(workers=1, fanout=o["fanout"], sample_rate=o["sample_rate"], seed=o["seed"])
+    holder = {}
 
-    def step(out):
-        res, _ = lj.lsj_join(inp.r, inp.s, cfg)
+    def lsj_step(out):
+        res, br = lj.lsj_join(inp.r, inp.s, cfg)
+        holder["br"] = br
         out.copy_(res._words)
         return out
 
-    return step, "lsj pipeline (K10,K6,K7,K8,K9)", ALGO_BYTES["lsj"] * (n_r + n_s)
+    st = Step([("lsj", lsj_step)], "sort", 32 * (n_r + n_s), "lsj sort phase (k_split_*, k_lsj_sort)",
+              f"sort phase: 32 B/tuple (read 16 + write 16) x {n_r + n_s} tuples; whole pipeline 80 B/tuple")
+    st.holder = holder
+    return st
+
+
+def count_launches(step, out):
+    """Kernels launched by one step, counted with the CUDA profiler (CUPTI):
+    every kernel except torch's own elementwise fills."""
+    import torch
+
+    try:
+        import warnings
+
+        from torch.profiler import ProfilerActivity, profile
+
+        warnings.filterwarnings("ignore", module="torch.profiler")
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            step(out)
+            torch.cuda.synchronize()
+        n = 0
+        for e in prof.events():
+            if getattr(e, "device_type", None) is not None and str(e.device_type).endswith("CUDA"):
+                name = e.name
+                if "Memset" in name or "Memcpy" in name or name.startswith("void at::") or "native::" in name:
+                    continue
+                n += 1
+        return n
+    except Exception:
+        return None
 
 
 # ---------------------------------------------------------------- CPU arms
@@ -257,7 +311,9 @@ def run_b200(args):
     inp = make_inputs(args.config, shard=rank)
     index = build_index(inp)
     dev = torch.device("cuda", local)
-    run_step, kname, alg_bytes = make_step(inp, index, args.variant)
+    variant = args.variant or DEFAULT_VARIANT.get(args.config, "direct")
+    args.variant = variant
+    run_step = make_step(inp, index, variant)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     out = torch.zeros(4, dtype=torch.int64, device=dev)
     xors = torch.zeros(world, dtype=torch.int64, device=dev)
@@ -299,24 +355,37 @@ def run_b200(args):
     else:
         xor_all = w[2] & (2**64 - 1)
 
-    # kernel-only timing of the dominant kernel (K1) for the roofline
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    # the dominant kernel timed alone, live, with CUDA events on its stream
+    dom = []
     for i in range(args.steps):
         flush.zero_()
-        kev[i][0].record()
-        run_step(out)
-        kev[i][1].record()
-    torch.cuda.synchronize()
-    k_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
+        if run_step.dominant == "sort":  # LSJ: phase events recorded by lsj_join itself
+            run_step(out)
+            torch.cuda.synchronize()
+            dom.append(run_step.holder["br"].sort * 1e3)
+            continue
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for name, fn in run_step.parts:
+            if name == run_step.dominant:
+                e0.record()
+                fn(out)
+                e1.record()
+            else:
+                fn(out)
+        torch.cuda.synchronize()
+        dom.append(e0.elapsed_time(e1))
+    k_ms = statistics.mean(dom)
     peak, peak_kind = _peaks()
-    achieved = alg_bytes / (k_ms / 1e3) / 1e9
+    achieved = run_step.dom_bytes / (k_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": _ncu_traffic(args.config), "kernel": kname, "kernel_ms": k_ms, "peak_kind": peak_kind,
-                "algorithmic_bytes": (f"{ALGO_BYTES[inp.algorithm]} B/probe x {n_s} probes" if index is not None
-                                      else f"80 B/tuple x {n_r + n_s} tuples")}
+                "traffic": _ncu_traffic(args.config), "kernel": run_step.kernel, "kernel_ms": k_ms,
+                "peak_kind": peak_kind, "algorithmic_bytes": run_step.bytes_note,
+                "step_frac": (ALGO_BYTES[inp.algorithm] * (n_s if index is not None else n_r + n_s))
+                / (ms_per_step / 1e3) / 1e9 / peak}
+    launches = count_launches(run_step, out)
 
     e2e = None
-    if not args.no_e2e and index is not None:
+    if not args.no_e2e:
         e2e = _e2e(args, inp, index, world)
     line = None
     if rank == 0:
@@ -330,7 +399,8 @@ def run_b200(args):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
                 "config": _config_block(args, inp), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": args.steps, "clocks": clk.summary(),
+                "gpu_launches": (launches * args.steps) if launches is not None else None,
+                "clocks": clk.summary(),
                 "checksum": {"count": w[0], "sum": w[1] & (2**64 - 1), "xor": xor_all, "search_steps": w[3]}}
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -339,26 +409,37 @@ def run_b200(args):
 
 def _e2e(args, inp, index, world):
     """Same metric through the public API from pinned HOST buffers: every
-    step copies S host->device (Relation construction), probes, and reads
-    the 3-word result back."""
+    step copies S (INLJ) or R and S (LSJ) host->device into a validated
+    Relation, runs the join and reads the 3-word result back."""
     import torch
 
     import paper_2111_08824_b200 as lj
 
-    scratch = index.bucket_scratch(len(inp.s)) if args.variant == "buffered" else None
     hk = inp.s.keys.cpu().pin_memory()
     hp = inp.s.payloads.cpu().pin_memory()
+    h2d = 16 * len(inp.s)
+    if index is None:
+        rk = inp.r.keys.cpu().pin_memory()
+        rp = inp.r.payloads.cpu().pin_memory()
+        h2d += 16 * len(inp.r)
+        o = dict(lj.DEFAULT_OPTS, **inp.opts)
+        cfg = lj.LsjConfig(workers=1, fanout=o["fanout"], sample_rate=o["sample_rate"], seed=o["seed"])
+    scratch = index.bucket_scratch(len(inp.s)) if (index is not None and args.variant == "buffered") else None
     steps = max(1, min(args.steps, 3))
     times = []
     for i in range(steps + 1):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         s = lj.Relation(hk.to("cuda", non_blocking=True), hp.to("cuda", non_blocking=True), validate=True)
-        if args.variant == "buffered":
-            words = index.join_checksum_buffered(s.keys, s.payloads, scratch=scratch)
+        if index is None:
+            r = lj.Relation(rk.to("cuda", non_blocking=True), rp.to("cuda", non_blocking=True), validate=True)
+            res, _ = lj.lsj_join(r, s, cfg)
         else:
-            words = index.join_checksum(s.keys, s.payloads)
-        res = lj.JoinResult(words=words)
+            if scratch is not None:
+                words = index.join_checksum_buffered(s.keys, s.payloads, scratch=scratch)
+            else:
+                words = index.join_checksum(s.keys, s.payloads)
+            res = lj.JoinResult(words=words)
         _ = res.checksum
         dt = time.perf_counter() - t0
         del s
@@ -366,7 +447,7 @@ def _e2e(args, inp, index, world):
             times.append(dt)
     t = statistics.median(times)
     n_s = len(inp.s)
-    return {"value": (len(inp.r) + world * n_s) / t, "unit": "tuples/s", "h2d_bytes_per_step": 16 * n_s,
+    return {"value": (len(inp.r) + world * n_s) / t, "unit": "tuples/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": 4 * 8, "ms_per_step": t * 1e3, "steps": steps}
 
 
@@ -386,8 +467,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2")
-    ap.add_argument("--variant", default="buffered", choices=["buffered", "direct"],
-                    help="GRMI INLJ: group S by leaf on device first (Request-Buffer analogue) or probe directly")
+    ap.add_argument("--variant", default=None, choices=["buffered", "direct"],
+                    help="INLJ: group S by index window on device first (Request-Buffer analogue) or probe "
+                         "directly; default per config (c2 buffered, c1/c3 direct)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

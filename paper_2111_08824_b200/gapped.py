@@ -124,16 +124,26 @@ class GappedRmiIndex:
                 out.zero_()
             return out
         scratch = scratch or self.bucket_scratch(n, s_keys.device)
+        self.bucket_records(s_keys, s_payloads, scratch, stream)
+        self.probe_records(n, scratch, out, accumulate, stream)
+        return out
+
+    def bucket_records(self, s_keys: torch.Tensor, s_payloads: torch.Tensor, scratch: dict, stream=None) -> None:
+        """K4: S grouped by key-range window into scratch["pairs"] / ["starts"]."""
         lib = _lib.lib()
-        st = _lib.stream_ptr(stream)
         g = self.c_struct()
         ws = scratch["ws"]
-        _lib.check(lib.lj_leaf_bucket(ctypes.byref(g), _lib.ptr(s_keys), _lib.ptr(s_payloads), n,
+        _lib.check(lib.lj_leaf_bucket(ctypes.byref(g), _lib.ptr(s_keys), _lib.ptr(s_payloads), s_keys.numel(),
                                       _lib.ptr(scratch["pairs"]), _lib.ptr(scratch["starts"]), _lib.ptr(ws),
-                                      ws.numel(), st), "leaf_bucket")
-        _lib.check(lib.lj_grmi_probe_bucketed(ctypes.byref(g), _lib.ptr(scratch["pairs"]), n,
-                                              _lib.ptr(scratch["starts"]), _lib.ptr(scratch["work"]), _lib.ptr(out),
-                                              int(bool(accumulate)), st), "grmi_probe_bucketed")
+                                      ws.numel(), _lib.stream_ptr(stream)), "leaf_bucket")
+
+    def probe_records(self, n: int, scratch: dict, out: torch.Tensor, accumulate: bool = False, stream=None) -> None:
+        """Staged K1 over the n records bucket_records left in scratch."""
+        g = self.c_struct()
+        _lib.check(_lib.lib().lj_grmi_probe_bucketed(ctypes.byref(g), _lib.ptr(scratch["pairs"]), n,
+                                                     _lib.ptr(scratch["starts"]), _lib.ptr(scratch["work"]),
+                                                     _lib.ptr(out), int(bool(accumulate)), _lib.stream_ptr(stream)),
+                   "grmi_probe_bucketed")
         return out
 
     def _predict_slots(self, keys: torch.Tensor) -> torch.Tensor:

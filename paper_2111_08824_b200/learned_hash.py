@@ -120,15 +120,25 @@ class SplineHashIndex:
                 out.zero_()
             return out
         scratch = scratch or self.bucket_scratch(n, s_keys.device)
+        self.bucket_records(s_keys, s_payloads, scratch, stream)
+        self.probe_records(n, scratch, out, accumulate, stream)
+        return out
+
+    def bucket_records(self, s_keys: torch.Tensor, s_payloads: torch.Tensor, scratch: dict, stream=None) -> None:
+        """S grouped by predicted-position window into scratch["pairs"]."""
         lib = _lib.lib()
-        st = _lib.stream_ptr(stream)
         c = self.c_struct()
         ws = scratch["ws"]
-        _lib.check(lib.lj_spline_hash_bucket(ctypes.byref(c), _lib.ptr(s_keys), _lib.ptr(s_payloads), n,
+        _lib.check(lib.lj_spline_hash_bucket(ctypes.byref(c), _lib.ptr(s_keys), _lib.ptr(s_payloads), s_keys.numel(),
                                              _lib.ptr(scratch["pairs"]), _lib.ptr(scratch["starts"]), _lib.ptr(ws),
-                                             ws.numel(), st), "spline_hash_bucket")
-        _lib.check(lib.lj_spline_hash_probe_grouped(ctypes.byref(c), _lib.ptr(scratch["pairs"]), n, _lib.ptr(out),
-                                                    int(bool(accumulate)), st), "spline_hash_probe_grouped")
+                                             ws.numel(), _lib.stream_ptr(stream)), "spline_hash_bucket")
+
+    def probe_records(self, n: int, scratch: dict, out: torch.Tensor, accumulate: bool = False, stream=None) -> None:
+        """K5 over the n grouped records bucket_records left in scratch."""
+        c = self.c_struct()
+        _lib.check(_lib.lib().lj_spline_hash_probe_grouped(ctypes.byref(c), _lib.ptr(scratch["pairs"]), n,
+                                                           _lib.ptr(out), int(bool(accumulate)),
+                                                           _lib.stream_ptr(stream)), "spline_hash_probe_grouped")
         return out
 
     def probe_batch(self, keys):
