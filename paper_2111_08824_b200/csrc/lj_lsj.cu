@@ -215,7 +215,7 @@ __global__ void k_split_plan(const i64 *starts, int nb, int points, i64 *fcount)
 }
 
 // split values of bucket b -> spv[fbase[b] .. fbase[b] + F_b - 1)
-__global__ void k_split_points(LsjDev md, const i64 *starts, const i64 *fbase, int nb, double *spv) {
+__global__ void k_split_points(LsjDev md, const i64 *starts, const i64 *fbase, int nb, u64 *spv) {
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
         const i64 F = split_count(starts[b + 1] - starts[b]);
         if (F < 2) continue;
@@ -232,11 +232,11 @@ __global__ void k_split_points(LsjDev md, const i64 *starts, const i64 *fbase, i
             if (md.bin(md.sample[mid]) <= b) lo = mid + 1; else hi = mid;
         }
         const i64 se = lo, ns = se - sb;
-        const double ybase = i64_to_f64(md.pb[b]) - 0.5;
-        const double yspan = i64_to_f64(md.pb[b + 1] - md.pb[b]);
+        // split KEYS at sample quantiles (distinct keys always separate, even
+        // where the model's placement y is flat); too few sample keys: the
+        // quantiles repeat (empty slices), none: one slice for the bucket
         for (i64 j = 1; j < F; ++j)
-            spv[fbase[b] + j - 1] = ns >= F ? md.y(md.sample[sb + (j * ns) / F])
-                                            : ybase + yspan * (double)j / (double)F;
+            spv[fbase[b] + j - 1] = ns > 0 ? md.sample[sb + (j * ns) / F < se ? sb + (j * ns) / F : se - 1] : ~0ULL;
     }
 }
 
@@ -246,13 +246,15 @@ __device__ __forceinline__ int y_slice(double y, double ybase, double scale, int
 }
 
 // point-slice mode: slot = 2 * lower_bound(v, y) + (y == v[lb])
-__device__ __forceinline__ int point_slot(const double *v, int K, double y) {
+// slot of key k among split keys v[0..K): 2i for keys in (v[i-1], v[i]),
+// 2i+1 for k == v[i] (a repeated hot key gets a slice of its own)
+__device__ __forceinline__ int point_slot(const u64 *v, int K, u64 k) {
     int lo = 0, hi = K;
     while (lo < hi) {
         int mid = (lo + hi) >> 1;
-        if (v[mid] < y) lo = mid + 1; else hi = mid;
+        if (v[mid] < k) lo = mid + 1; else hi = mid;
     }
-    return 2 * lo + ((lo < K && v[lo] == y) ? 1 : 0);
+    return 2 * lo + ((lo < K && v[lo] == k) ? 1 : 0);
 }
 
 // Level 2 as a balanced, segmented partition.  Work item = a chunk of <=
@@ -269,7 +271,7 @@ struct SplitCtx {  // per-bucket layout shared by the split kernels
     const i64 *fbase;   // [nb+1] first slot of each bucket
     const i64 *cbase;   // [nb+1] first chunk of each bucket
     const i64 *mbase;   // [nb+1] first matrix entry of each bucket
-    const double *spv;  // split values (point mode), at fbase[b]
+    const u64 *spv;     // split keys (point mode), at fbase[b]
     int nb;
 };
 
@@ -315,16 +317,15 @@ __device__ __forceinline__ SplitItem split_item(const LsjDev &md, const SplitCtx
     return it;
 }
 
-__device__ __forceinline__ int split_slot(const LsjDev &md, const SplitItem &it, const double *v, bool points, u64 k) {
-    const double y = md.y(k);
-    return points ? point_slot(v, it.K, y) : y_slice(y, it.ybase, it.scale, it.F);
+__device__ __forceinline__ int split_slot(const LsjDev &md, const SplitItem &it, const u64 *v, bool points, u64 k) {
+    return points ? point_slot(v, it.K, k) : y_slice(md.y(k), it.ybase, it.scale, it.F);
 }
 
 // pass 1: mat[mbase[b] + s * chunks_b + c] = tuples of chunk c in slot s
 __global__ void __launch_bounds__(SPLIT_NT) k_split_count(LsjDev md, SplitCtx cx, const ulonglong2 *__restrict__ A,
                                                           const i64 *nitems, u32 *mat, SortCtl *ctl) {
     __shared__ u32 h[2 * SPLIT_MAXF];
-    __shared__ double v[SPLIT_MAXF];
+    __shared__ u64 v[SPLIT_MAXF];
     __shared__ i64 s_q;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool points = md.sample != nullptr;
@@ -388,12 +389,15 @@ __global__ void k_split_slots(LsjDev md, SplitCtx cx, const i64 *off, i64 n, i64
             sub_y[g] = make_double2(ybase + (double)j * yspan / (double)F, yspan / (double)F);
         } else {
             const i64 K = (F - 1) / 2;
-            const double *v = cx.spv + cx.fbase[b];
-            if (j & 1) {  // point slot: every y equals v[(j-1)/2]
-                sub_y[g] = make_double2(v[(j - 1) >> 1], 0.0);
-            } else {      // open interval between split values
+            const u64 *v = cx.spv + cx.fbase[b];
+            // y is monotone in the key: the slice's placement range is the
+            // y range of its bounding split keys
+            if (j & 1) {  // point slot: every key equals v[(j-1)/2]
+                sub_y[g] = make_double2(md.y(v[(j - 1) >> 1]), 0.0);
+            } else {      // open interval between split keys
                 const i64 q = j >> 1;
-                const double l = q == 0 ? ybase : v[q - 1], h = q == K ? ybase + yspan : v[q];
+                const double l = q == 0 ? ybase : md.y(v[q - 1]);
+                const double h = (q == K || v[q] == ~0ULL) ? ybase + yspan : md.y(v[q]);
                 sub_y[g] = make_double2(l, h > l ? h - l : 0.0);
             }
         }
@@ -405,7 +409,7 @@ __global__ void __launch_bounds__(SPLIT_NT) k_split_scatter(LsjDev md, SplitCtx 
                                                             const i64 *nitems, const i64 *__restrict__ off,
                                                             ulonglong2 *B, SortCtl *ctl) {
     __shared__ u32 cur[2 * SPLIT_MAXF];
-    __shared__ double v[SPLIT_MAXF];
+    __shared__ u64 v[SPLIT_MAXF];
     __shared__ i64 s_q;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool points = md.sample != nullptr;
@@ -638,6 +642,34 @@ __global__ void k_big_copy(const ulonglong2 *B, const i64 *big, const i64 *boff,
         if (flags[q]) continue;
         const i64 i = big[2 * q] + (t - boff[q]);
         out[i] = B[i];
+    }
+}
+
+// flattened segments (pos[j], cum[j+1]-cum[j]) of B <-> compact SoA columns
+__device__ __forceinline__ int find_seg(const i64 *cum, int nseg, i64 t) {
+    int lo = 0, hi = nseg;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (cum[mid] <= t) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void k_seg_gather(const ulonglong2 *B, const i64 *pos, const i64 *cum, int nseg, i64 total, u64 *k,
+                             u64 *v) {
+    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < total; t += (i64)gridDim.x * blockDim.x) {
+        const int j = find_seg(cum, nseg, t);
+        const ulonglong2 e = B[pos[j] + (t - cum[j])];
+        k[t] = e.x;
+        v[t] = e.y;
+    }
+}
+
+__global__ void k_seg_scatter(const u64 *k, const u64 *v, const i64 *pos, const i64 *cum, int nseg, i64 total,
+                              ulonglong2 *out) {
+    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < total; t += (i64)gridDim.x * blockDim.x) {
+        const int j = find_seg(cum, nseg, t);
+        out[pos[j] + (t - cum[j])] = make_ulonglong2(k[t], v[t]);
     }
 }
 
@@ -875,6 +907,11 @@ size_t lj_lsj_sort_workspace_bytes(int64_t n, int64_t nbins) {
     size_t t = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, t, (const u64 *)nullptr, (u64 *)nullptr, (const u64 *)nullptr,
                                     (u64 *)nullptr, (int64_t)n);
+    size_t tseg = 0;
+    cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tseg, (const u64 *)nullptr, (u64 *)nullptr,
+                                             (const u64 *)nullptr, (u64 *)nullptr, (int)(n < INT32_MAX ? n : INT32_MAX),
+                                             (int)nbig, (const i64 *)nullptr, (const i64 *)nullptr, 0, 64);
+    if (tseg > t) t = tseg;
     size_t sc = scan_i64_bytes(nbins + 1);
     const size_t ms = mat_scan_bytes(M);
     if (ms > sc) sc = ms;
@@ -921,7 +958,7 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
     ulonglong2 *B = (ulonglong2 *)take(sizeof(ulonglong2) * (size_t)n);
     i64 *sub_starts = (i64 *)take(sizeof(i64) * (size_t)(G + 1));
     double2 *sub_y = (double2 *)take(sizeof(double2) * (size_t)G);
-    double *spv = (double *)take(sizeof(double) * (size_t)G);
+    u64 *spv = (u64 *)take(sizeof(u64) * (size_t)G);
     const i64 nbig_cap = n / CAP + 2;
     i64 *biglist = (i64 *)take(sizeof(i64) * (size_t)nbig_cap);
     i64 *big = (i64 *)take(sizeof(i64) * 2 * (size_t)nbig_cap);
@@ -1006,19 +1043,48 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
     std::vector<int> hf(nbig);
     LJ_CK(cudaMemcpyAsync(hf.data(), flags, sizeof(int) * nbig, cudaMemcpyDeviceToHost, st));
     LJ_CK(cudaStreamSynchronize(st));
+    // the mixed ones: those above 2^16 tuples each get a device radix sort;
+    // all smaller ones ONE segmented radix sort (block per segment): gather
+    // -> sort -> scatter back, instead of a device sort per sub-bucket
+    std::vector<i64> spos, scum(1, 0);
     int nsorted = 0;
+    i64 mx = 0;
     for (int q = 0; q < nbig; ++q) {
         if (!hf[q]) continue;
+        ++nsorted;
         const i64 a = hbig[2 * q], len = hbig[2 * q + 1];
+        mx = std::max(mx, len);
+        if (len <= 65536) {
+            spos.push_back(a);
+            scum.push_back(scum.back() + len);
+            continue;
+        }
         k_deinterleave<<<grid_for(len, 256, 8), 256, 0, st>>>(B + a, len, k1, v1);
         size_t tt = 0;
         cub::DeviceRadixSort::SortPairs(nullptr, tt, k1, k2, v1, v2, (int64_t)len);
         LJ_CK(cub::DeviceRadixSort::SortPairs(cub_tmp, tt, k1, k2, v1, v2, (int64_t)len, 0, 64, st));
         k_interleave<<<grid_for(len, 256, 8), 256, 0, st>>>(k2, v2, len, out + a);
         LJ_CK_LAUNCH();
-        ++nsorted;
     }
     stats_host[2] = nsorted;
+    stats_host[3] = mx;
+    const int nseg = (int)spos.size();
+    if (nseg) {
+        const i64 T = scum.back();
+        i64 *d_pos = big;  // reuse: 2 * nbig_cap words >= 2 * nseg + 1
+        i64 *d_cum = big + nseg;
+        LJ_CK(cudaMemcpyAsync(d_pos, spos.data(), sizeof(i64) * nseg, cudaMemcpyHostToDevice, st));
+        LJ_CK(cudaMemcpyAsync(d_cum, scum.data(), sizeof(i64) * (nseg + 1), cudaMemcpyHostToDevice, st));
+        k_seg_gather<<<grid_for(T, 256, 8), 256, 0, st>>>(B, d_pos, d_cum, nseg, T, k1, v1);
+        LJ_CK_LAUNCH();
+        size_t tt = 0;
+        cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tt, k1, k2, v1, v2, (int)T, nseg, d_cum, d_cum + 1, 0, 64,
+                                                 st);
+        LJ_CK(cub::DeviceSegmentedRadixSort::SortPairs(cub_tmp, tt, k1, k2, v1, v2, (int)T, nseg, d_cum, d_cum + 1,
+                                                       0, 64, st));
+        k_seg_scatter<<<grid_for(T, 256, 8), 256, 0, st>>>(k2, v2, d_pos, d_cum, nseg, T, out);
+        LJ_CK_LAUNCH();
+    }
     LJ_CK(cudaStreamSynchronize(st));
     return LJ_OK;
 }

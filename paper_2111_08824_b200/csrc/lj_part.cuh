@@ -158,10 +158,16 @@ constexpr size_t PT_STAGE_S = (size_t)PT_TILE_S * (8 + 8 + 4);
 constexpr int PT_MAXST = 6;
 constexpr int PT_SMEM_MAX = 220 * 1024;
 
+// Pass 1, warp-specialised: the last warp issues the bulk copies, the other
+// 31 consume rows of 32 keys round-robin and release a stage on its `empty`
+// barrier, so no warp ever waits for another at a block barrier (the bin
+// function is a chain of dependent loads; a per-tile __syncthreads made
+// every tile as slow as its slowest row).
+constexpr int PT_H_CONS = PART2_NT / 32 - 1;
+
 template <class Src>
 __global__ void __launch_bounds__(PART2_NT) k_bin_hist_tma(Src f0, i64 n, i64 chunk, int nbins, int hc, int nst,
                                                            u32 *mat, u32 *codes) {
-    constexpr int U = PT_TILE_H / PART2_NT;
     extern __shared__ __align__(128) unsigned char smem_t[];
     u64 *tab = reinterpret_cast<u64 *>(smem_t);
     unsigned char *smem = smem_t + pt_table_bytes(f0.f.smem_words());
@@ -170,51 +176,61 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_hist_tma(Src f0, i64 n, i64 ch
     f.f = f0.f.at(tab);
     u32 *h = reinterpret_cast<u32 *>(smem);
     u64 *ring = reinterpret_cast<u64 *>(smem + ((nbins * hc * 4 + 127) & ~127));
-    __shared__ __align__(8) uint64_t full[PT_MAXST];
+    __shared__ __align__(8) uint64_t full[PT_MAXST], empty[PT_MAXST];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, shift = f.f.shift;
     for (int j = tid; j < nbins * hc; j += PART2_NT) h[j] = 0;
     const i64 lo = blockIdx.x * chunk, hi = min(lo + chunk, n);
     const int ntiles = hi > lo ? (int)((hi - lo + PT_TILE_H - 1) / PT_TILE_H) : 0;
-    auto issue = [&](int t) {
-        const int s = t % nst;
-        const i64 base = lo + (i64)t * PT_TILE_H;
-        const unsigned b8 = (unsigned)(min((i64)PT_TILE_H, hi - base) * 8) & ~15u;
-        if (b8) {
-            mbar_arrive_expect_tx(&full[s], b8);
-            bulk_g2s(ring + (size_t)s * PT_TILE_H, f.keys + base, b8, &full[s]);
-        } else {
-            mbar_arrive(&full[s]);
-        }
-    };
     if (tid == 0) {
-        for (int s = 0; s < nst; ++s) mbar_init(&full[s], 1);
+        for (int s = 0; s < nst; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], PT_H_CONS);
+        }
         mbar_init_fence();
-        for (int t = 0; t < min(nst - 1, ntiles); ++t) issue(t);
     }
     __syncthreads();
-    for (int t = 0; t < ntiles; ++t) {
-        const int s = t % nst;
-        if (tid == 0 && t + nst - 1 < ntiles) issue(t + nst - 1);  // stage consumed in round t-1
-        mbar_wait(&full[s], (unsigned)(t / nst) & 1u);
-        const i64 base = lo + (i64)t * PT_TILE_H;
-        const int cnt = (int)min((i64)PT_TILE_H, hi - base), nb = cnt & ~1;
-        const u64 *ks = ring + (size_t)s * PT_TILE_H;
-        u32 c[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int j = (warp * U + u) * 32 + lane;
-            c[u] = j < cnt ? f.code(j < nb ? ks[j] : ld_stream(f.keys + base + j)) : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int j = (warp * U + u) * 32 + lane;
-            if (j < cnt) {
-                const int cp = (t * (PT_TILE_H / 32) + warp * U + u) % hc;
-                atomicAdd(h + cp * nbins + (c[u] >> shift), 1u);
-                codes[base + j] = c[u];
+    if (warp == PT_H_CONS) {  // producer
+        if (lane == 0)
+            for (int t = 0; t < ntiles; ++t) {
+                const int s = t % nst;
+                if (t >= nst) mbar_wait(&empty[s], (unsigned)(t / nst - 1) & 1u);
+                const i64 base = lo + (i64)t * PT_TILE_H;
+                const unsigned b8 = (unsigned)(min((i64)PT_TILE_H, hi - base) * 8) & ~15u;
+                if (b8) {
+                    mbar_arrive_expect_tx(&full[s], b8);
+                    bulk_g2s(ring + (size_t)s * PT_TILE_H, f.keys + base, b8, &full[s]);
+                } else {
+                    mbar_arrive(&full[s]);
+                }
             }
+    } else {
+        u32 *hw = h + (warp % hc) * nbins;  // this warp's histogram copy
+        constexpr int U = 4;
+        for (int t = 0; t < ntiles; ++t) {
+            const int s = t % nst;
+            mbar_wait(&full[s], (unsigned)(t / nst) & 1u);
+            const i64 base = lo + (i64)t * PT_TILE_H;
+            const int cnt = (int)min((i64)PT_TILE_H, hi - base), nb = cnt & ~1;
+            const u64 *ks = ring + (size_t)s * PT_TILE_H;
+            for (int r0 = warp; r0 < PT_TILE_H / 32; r0 += U * PT_H_CONS) {
+                u32 c[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int j = (r0 + u * PT_H_CONS) * 32 + lane;
+                    c[u] = (j < cnt) ? f.code(j < nb ? ks[j] : ld_stream(f.keys + base + j)) : 0;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int j = (r0 + u * PT_H_CONS) * 32 + lane;
+                    if (j < cnt) {
+                        atomicAdd(hw + (c[u] >> shift), 1u);
+                        codes[base + j] = c[u];
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
         }
-        __syncthreads();
     }
     __syncthreads();
     hist_store(h, nbins, hc, mat);

@@ -265,7 +265,7 @@ def _sort(pairs_in, starts, lm: LsjModel, n: int):
     _lib.check(lib.lj_lsj_sort(ctypes.byref(c), _lib.ptr(pairs_in), _lib.ptr(out), n, _lib.ptr(starts),
                                _lib.ptr(ws), ws.numel(), st, _lib.stream_ptr()), "lsj_sort")
     diag = {"oversized_sub_buckets": int(st[0]), "bitonic_fallbacks": int(st[1]),
-            "radix_sorted_sub_buckets": int(st[2])}
+            "radix_sorted_sub_buckets": int(st[2]), "largest_radix_sorted": int(st[3])}
     return out, diag
 
 
