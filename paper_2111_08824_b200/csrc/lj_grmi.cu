@@ -243,7 +243,7 @@ constexpr int STAGE_NT = 1024;
 constexpr int STAGE_PIECE = 65536;      // probes per work item
 constexpr i64 STAGE_MIN = 2048;         // windows with fewer probes: global search
 constexpr int STAGE_U = 2;              // probes in flight per thread
-constexpr int STAGE_TB = 12;            // radix-table bits
+constexpr int STAGE_TB = 13;            // radix-table bits
 constexpr int STAGE_TBINS = 1 << STAGE_TB;
 constexpr int STAGE_MAX_SHIFT = 14;     // staged range <= 2^14 + 1 slots
 constexpr int STAGE_SPAN = (1 << STAGE_MAX_SHIFT) + 1;
