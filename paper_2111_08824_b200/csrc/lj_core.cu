@@ -196,63 +196,131 @@ __global__ void k_leaf_starts(const u64 *k, i64 n, i64 m, const double *root, i6
     }
 }
 
-// One block per leaf: means, centred moments, slope/intercept, clamps
-// (models.py:75-98) and the exact residual bounds (:101-108).
-__global__ void __launch_bounds__(FIT_THREADS) k_leaf_fit(const u64 *k, const i64 *rank, i64 n, i64 m,
-                                                          const i64 *starts, LjLeaf *leaves, i64 *err) {
-    for (i64 l = blockIdx.x; l < m; l += gridDim.x) {
-        i64 a = starts[l], b = starts[l + 1];
-        bool ne = b > a;
-        double sx = 0.0, sy = 0.0;
-        for (i64 i = a + threadIdx.x; i < b; i += FIT_THREADS) {
-            sx = __dadd_rn(sx, u64_to_f64(k[i]));
-            sy = __dadd_rn(sy, i64_to_f64(rank[i]));
+// Leaf fit (models.py:75-108) over "pieces": leaf l's key range [a, b) is
+// cut into ceil((b-a)/FIT_PIECE) pieces (at least one), one block per piece,
+// and every per-leaf quantity is combined from its pieces in a fixed order,
+// so the fit is deterministic and a leaf holding half of a skewed sample no
+// longer serialises on one block.
+constexpr i64 FIT_PIECE = 8192;
+
+__global__ void k_piece_count(const i64 *starts, i64 m, i64 *pc) {
+    for (i64 l = blockIdx.x * (i64)blockDim.x + threadIdx.x; l <= m; l += (i64)gridDim.x * blockDim.x) {
+        if (l == m) {
+            pc[l] = 0;
+            continue;
         }
-        block_sum2<FIT_THREADS>(sx, sy);
-        double c = i64_to_f64(b - a);
-        double d = c > 1.0 ? c : 1.0;
-        double mx = ne ? __ddiv_rn(sx, d) : 0.0, my = ne ? __ddiv_rn(sy, d) : 0.0;
-        double var = 0.0, cov = 0.0;
-        for (i64 i = a + threadIdx.x; i < b; i += FIT_THREADS) {
-            double cx = __dsub_rn(u64_to_f64(k[i]), mx);
-            double cy = __dsub_rn(i64_to_f64(rank[i]), my);
-            var = __dadd_rn(var, __dmul_rn(cx, cx));
-            cov = __dadd_rn(cov, __dmul_rn(cx, cy));
+        const i64 len = starts[l + 1] - starts[l];
+        pc[l] = len <= FIT_PIECE ? 1 : (len + FIT_PIECE - 1) / FIT_PIECE;
+    }
+}
+
+__device__ __forceinline__ i64 piece_leaf(const i64 *pbase, i64 m, i64 q) {
+    i64 lo = 0, hi = m;  // last l with pbase[l] <= q
+    while (hi - lo > 1) {
+        const i64 mid = (lo + hi) >> 1;
+        if (pbase[mid] <= q) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// phase 0: sums of x and rank; phase 1: centred moments around the leaf
+// means; phase 2: residual bounds of the finished leaf model
+template <int PHASE>
+__global__ void __launch_bounds__(FIT_THREADS) k_leaf_piece(const u64 *k, const i64 *rank, i64 m, const i64 *starts,
+                                                            const i64 *pbase, i64 npieces, const double *means,
+                                                            const LjLeaf *leaves, double *part, i64 *ipart) {
+    for (i64 q = blockIdx.x; q < npieces; q += gridDim.x) {
+        const i64 l = piece_leaf(pbase, m, q);
+        const i64 j = q - pbase[l];
+        const i64 a = starts[l] + j * FIT_PIECE, b = min(starts[l + 1], a + FIT_PIECE);
+        if (PHASE < 2) {
+            const double mx = PHASE ? means[2 * l] : 0.0, my = PHASE ? means[2 * l + 1] : 0.0;
+            double s0 = 0.0, s1 = 0.0;
+            for (i64 i = a + threadIdx.x; i < b; i += FIT_THREADS) {
+                if (PHASE == 0) {
+                    s0 = __dadd_rn(s0, u64_to_f64(k[i]));
+                    s1 = __dadd_rn(s1, i64_to_f64(rank[i]));
+                } else {
+                    const double cx = __dsub_rn(u64_to_f64(k[i]), mx);
+                    const double cy = __dsub_rn(i64_to_f64(rank[i]), my);
+                    s0 = __dadd_rn(s0, __dmul_rn(cx, cx));
+                    s1 = __dadd_rn(s1, __dmul_rn(cx, cy));
+                }
+            }
+            block_sum2<FIT_THREADS>(s0, s1);
+            if (threadIdx.x == 0) {
+                part[2 * q] = s0;
+                part[2 * q + 1] = s1;
+            }
+        } else {
+            __shared__ i64 s_lo[FIT_THREADS], s_hi[FIT_THREADS];
+            const LjLeaf lf = leaves[l];
+            i64 elo = 0, ehi = 0;
+            for (i64 i = a + threadIdx.x; i < b; i += FIT_THREADS) {
+                const i64 resid = rank[i] - rmi_leaf_pos(lf, u64_to_f64(k[i]));
+                elo = resid < elo ? resid : elo;
+                ehi = resid > ehi ? resid : ehi;
+            }
+            s_lo[threadIdx.x] = elo;
+            s_hi[threadIdx.x] = ehi;
+            __syncthreads();
+            for (int s = FIT_THREADS / 2; s > 0; s >>= 1) {
+                if (threadIdx.x < s) {
+                    s_lo[threadIdx.x] = min(s_lo[threadIdx.x], s_lo[threadIdx.x + s]);
+                    s_hi[threadIdx.x] = max(s_hi[threadIdx.x], s_hi[threadIdx.x + s]);
+                }
+                __syncthreads();
+            }
+            if (threadIdx.x == 0) {
+                ipart[2 * q] = s_lo[0];
+                ipart[2 * q + 1] = s_hi[0];
+            }
+            __syncthreads();
         }
-        block_sum2<FIT_THREADS>(var, cov);
-        double slope = var > 0.0 ? __ddiv_rn(cov, var) : 0.0;
+    }
+}
+
+// per leaf, pieces combined in order: phase 0 -> means; phase 1 -> the leaf
+// (slope clamped >= 0, empty leaves constant at the segment start, clamps);
+// phase 2 -> residual bounds
+template <int PHASE>
+__global__ void k_leaf_combine(const i64 *starts, i64 n, i64 m, const i64 *pbase, const double *part,
+                               const i64 *ipart, double *means, LjLeaf *leaves, i64 *err) {
+    for (i64 l = blockIdx.x * (i64)blockDim.x + threadIdx.x; l < m; l += (i64)gridDim.x * blockDim.x) {
+        const i64 a = starts[l], b = starts[l + 1];
+        const bool ne = b > a;
+        if (PHASE == 2) {
+            i64 elo = 0, ehi = 0;
+            for (i64 q = pbase[l]; q < pbase[l + 1]; ++q) {
+                elo = min(elo, ipart[2 * q]);
+                ehi = max(ehi, ipart[2 * q + 1]);
+            }
+            err[2 * l] = elo;
+            err[2 * l + 1] = ehi;
+            continue;
+        }
+        double s0 = 0.0, s1 = 0.0;
+        for (i64 q = pbase[l]; q < pbase[l + 1]; ++q) {
+            s0 = __dadd_rn(s0, part[2 * q]);
+            s1 = __dadd_rn(s1, part[2 * q + 1]);
+        }
+        if (PHASE == 0) {
+            const double c = i64_to_f64(b - a), d = c > 1.0 ? c : 1.0;
+            means[2 * l] = ne ? __ddiv_rn(s0, d) : 0.0;
+            means[2 * l + 1] = ne ? __ddiv_rn(s1, d) : 0.0;
+            continue;
+        }
+        const double mx = means[2 * l], my = means[2 * l + 1];
+        double slope = s0 > 0.0 ? __ddiv_rn(s1, s0) : 0.0;
         if (slope < 0.0) slope = 0.0;
-        double icpt = __dsub_rn(my, __dmul_rn(slope, mx));
-        i64 seg = a < n - 1 ? a : n - 1;
+        const double icpt = __dsub_rn(my, __dmul_rn(slope, mx));
+        const i64 seg = a < n - 1 ? a : n - 1;
         LjLeaf lf;
         lf.slope = ne ? slope : 0.0;
         lf.icpt = ne ? icpt : i64_to_f64(seg);
         lf.clamp_lo = ne ? a : seg;
         lf.clamp_hi = ne ? b - 1 : seg;
-        // residual bounds
-        __shared__ i64 s_lo[FIT_THREADS], s_hi[FIT_THREADS];
-        i64 elo = 0, ehi = 0;
-        for (i64 i = a + threadIdx.x; i < b; i += FIT_THREADS) {
-            i64 resid = rank[i] - rmi_leaf_pos(lf, u64_to_f64(k[i]));
-            elo = resid < elo ? resid : elo;
-            ehi = resid > ehi ? resid : ehi;
-        }
-        s_lo[threadIdx.x] = elo;
-        s_hi[threadIdx.x] = ehi;
-        __syncthreads();
-        for (int s = FIT_THREADS / 2; s > 0; s >>= 1) {
-            if (threadIdx.x < s) {
-                s_lo[threadIdx.x] = min(s_lo[threadIdx.x], s_lo[threadIdx.x + s]);
-                s_hi[threadIdx.x] = max(s_hi[threadIdx.x], s_hi[threadIdx.x + s]);
-            }
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) {
-            leaves[l] = lf;
-            err[2 * l] = s_lo[0];
-            err[2 * l + 1] = s_hi[0];
-        }
-        __syncthreads();
+        leaves[l] = lf;
     }
 }
 
@@ -336,10 +404,22 @@ int lj_sort_pairs(const uint64_t *keys_in, const uint64_t *pay_in, uint64_t *key
     return LJ_OK;
 }
 
+static i64 max_pieces(i64 n, i64 m) { return m + n / FIT_PIECE + 1; }
+
+static size_t piece_scan_bytes(i64 m) {
+    size_t t = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, t, (i64 *)nullptr, (i64 *)nullptr, (int64_t)(m + 1));
+    return t;
+}
+
 size_t lj_rmi_fit_workspace_bytes(int64_t n, int64_t m) {
+    const size_t r = rank_scan_temp_bytes(n), q = piece_scan_bytes(m);
     return align_up(sizeof(i64) * (size_t)n) + align_up(sizeof(i64) * (size_t)(m + 1)) +
            align_up(sizeof(double) * 2 * FIT_GRID) + align_up(sizeof(double) * 2) +
-           align_up(rank_scan_temp_bytes(n));
+           2 * align_up(sizeof(i64) * (size_t)(m + 1)) +                       // piece counts / bases
+           align_up(sizeof(double) * 2 * (size_t)m) +                          // leaf means
+           align_up(sizeof(double) * 2 * (size_t)max_pieces(n, m)) +            // piece sums
+           align_up(sizeof(i64) * 2 * (size_t)max_pieces(n, m)) + align_up(r > q ? r : q);
 }
 
 int lj_rmi_fit(const uint64_t *k, int64_t n, int64_t m, double *root, LjLeaf *leaves, int64_t *err,
@@ -360,6 +440,16 @@ int lj_rmi_fit(const uint64_t *k, int64_t n, int64_t m, double *root, LjLeaf *le
     p += align_up(sizeof(double) * 2 * FIT_GRID);
     double *means = (double *)p;
     p += align_up(sizeof(double) * 2);
+    i64 *pcnt = (i64 *)p;
+    p += align_up(sizeof(i64) * (size_t)(m + 1));
+    i64 *pbase = (i64 *)p;
+    p += align_up(sizeof(i64) * (size_t)(m + 1));
+    double *lmeans = (double *)p;
+    p += align_up(sizeof(double) * 2 * (size_t)m);
+    double *ppart = (double *)p;
+    p += align_up(sizeof(double) * 2 * (size_t)max_pieces(n, m));
+    i64 *ipart = (i64 *)p;
+    p += align_up(sizeof(i64) * 2 * (size_t)max_pieces(n, m));
     size_t scan_bytes = rank_scan_temp_bytes(n);
 
     k_first_occurrence<<<grid_for(n, 256, 8), 256, 0, st>>>(k, n, rank);
@@ -370,8 +460,21 @@ int lj_rmi_fit(const uint64_t *k, int64_t n, int64_t m, double *root, LjLeaf *le
     k_root_moments<<<FIT_GRID, FIT_THREADS, 0, st>>>(k, rank, n, m, means, part);
     k_root_finish<<<1, FIT_THREADS, 0, st>>>(part, means, root);
     k_leaf_starts<<<grid_for(m + 1, 256, 8), 256, 0, st>>>(k, n, m, root, starts);
-    unsigned g = (unsigned)(m < 65535 * 4 ? m : 65535 * 4);
-    k_leaf_fit<<<g, FIT_THREADS, 0, st>>>(k, rank, n, m, starts, leaves, err);
+    k_piece_count<<<grid_for(m + 1, 256, 8), 256, 0, st>>>(starts, m, pcnt);
+    LJ_CK_LAUNCH();
+    size_t pq = piece_scan_bytes(m);
+    LJ_CK(cub::DeviceScan::ExclusiveSum(p, pq, pcnt, pbase, (int64_t)(m + 1), st));
+    i64 npieces = 0;
+    LJ_CK(cudaMemcpyAsync(&npieces, pbase + m, sizeof(i64), cudaMemcpyDeviceToHost, st));
+    LJ_CK(cudaStreamSynchronize(st));
+    const unsigned gp = (unsigned)(npieces < 65535 * 4 ? npieces : 65535 * 4);
+    const unsigned gl = grid_for(m, 256, 8);
+    k_leaf_piece<0><<<gp, FIT_THREADS, 0, st>>>(k, rank, m, starts, pbase, npieces, lmeans, leaves, ppart, ipart);
+    k_leaf_combine<0><<<gl, 256, 0, st>>>(starts, n, m, pbase, ppart, ipart, lmeans, leaves, err);
+    k_leaf_piece<1><<<gp, FIT_THREADS, 0, st>>>(k, rank, m, starts, pbase, npieces, lmeans, leaves, ppart, ipart);
+    k_leaf_combine<1><<<gl, 256, 0, st>>>(starts, n, m, pbase, ppart, ipart, lmeans, leaves, err);
+    k_leaf_piece<2><<<gp, FIT_THREADS, 0, st>>>(k, rank, m, starts, pbase, npieces, lmeans, leaves, ppart, ipart);
+    k_leaf_combine<2><<<gl, 256, 0, st>>>(starts, n, m, pbase, ppart, ipart, lmeans, leaves, err);
     LJ_CK_LAUNCH();
     return LJ_OK;
 }

@@ -215,7 +215,13 @@ __global__ void k_split_plan(const i64 *starts, int nb, int points, i64 *fcount)
 }
 
 // split values of bucket b -> spv[fbase[b] .. fbase[b] + F_b - 1)
-__global__ void k_split_points(LsjDev md, const i64 *starts, const i64 *fbase, int nb, u64 *spv) {
+// bin of every sample key (the sample is sorted, so these are non-decreasing)
+__global__ void k_sample_bins(LsjDev md, u32 *sbin) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < md.nsample; i += (i64)gridDim.x * blockDim.x)
+        sbin[i] = (u32)md.bin(md.sample[i]);
+}
+
+__global__ void k_split_points(LsjDev md, const u32 *sbin, const i64 *starts, const i64 *fbase, int nb, u64 *spv) {
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
         const i64 F = split_count(starts[b + 1] - starts[b]);
         if (F < 2) continue;
@@ -223,13 +229,13 @@ __global__ void k_split_points(LsjDev md, const i64 *starts, const i64 *fbase, i
         i64 lo = 0, hi = md.nsample;
         while (lo < hi) {
             i64 mid = (lo + hi) >> 1;
-            if (md.bin(md.sample[mid]) < b) lo = mid + 1; else hi = mid;
+            if ((sbin ? (int)sbin[mid] : md.bin(md.sample[mid])) < b) lo = mid + 1; else hi = mid;
         }
         const i64 sb = lo;
         hi = md.nsample;
         while (lo < hi) {
             i64 mid = (lo + hi) >> 1;
-            if (md.bin(md.sample[mid]) <= b) lo = mid + 1; else hi = mid;
+            if ((sbin ? (int)sbin[mid] : md.bin(md.sample[mid])) <= b) lo = mid + 1; else hi = mid;
         }
         const i64 se = lo, ns = se - sb;
         // split KEYS at sample quantiles (distinct keys always separate, even
@@ -980,7 +986,11 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
     size_t t = scan_i64_bytes(nb + 1);
     LJ_CK(cub::DeviceScan::ExclusiveSum(cub_tmp, t, fcount, fbase, (int64_t)(nb + 1), st));
     if (points) {
-        k_split_points<<<(int)((nb + 127) / 128), 128, 0, st>>>(dev, starts, fbase, (int)nb, spv);
+        // sample bins precomputed into k1 (free until the oversized pass) when
+        // they fit, else evaluated inside the searches
+        u32 *sbin = dev.nsample <= 2 * n ? reinterpret_cast<u32 *>(k1) : nullptr;
+        if (sbin) k_sample_bins<<<grid_for(dev.nsample, 256, 8), 256, 0, st>>>(dev, sbin);
+        k_split_points<<<(int)((nb + 63) / 64), 64, 0, st>>>(dev, sbin, starts, fbase, (int)nb, spv);
         LJ_CK_LAUNCH();
     }
     k_chunk_plan<<<(int)((nb + 256) / 256), 256, 0, st>>>(starts, fbase, (int)nb, chunks, matc);
