@@ -138,6 +138,7 @@ struct SortCtl {
 struct Bucket {
     i64 in_base, m, out_base;
     double ybase, yspan;
+    bool point;  // a point slice (one repeated key), already written in place
 };
 
 // Sub-buckets written by k_lsj_split: y-slices of the coarse buckets, in
@@ -154,6 +155,7 @@ struct SubBuckets {
         const double2 y = sub_y[g];
         k.ybase = y.x;
         k.yspan = y.y;
+        k.point = y.y < 0.0;
         return k;
     }
 };
@@ -398,8 +400,9 @@ __global__ void k_split_slots(LsjDev md, SplitCtx cx, const i64 *off, i64 n, i64
             const u64 *v = cx.spv + cx.fbase[b];
             // y is monotone in the key: the slice's placement range is the
             // y range of its bounding split keys
-            if (j & 1) {  // point slot: every key equals v[(j-1)/2]
-                sub_y[g] = make_double2(md.y(v[(j - 1) >> 1]), 0.0);
+            if (j & 1) {  // point slot: every key equals v[(j-1)/2]; written to the
+                          // output by the split scatter (span -1 marks it)
+                sub_y[g] = make_double2(md.y(v[(j - 1) >> 1]), -1.0);
             } else {      // open interval between split keys
                 const i64 q = j >> 1;
                 const double l = q == 0 ? ybase : md.y(v[q - 1]);
@@ -413,7 +416,7 @@ __global__ void k_split_slots(LsjDev md, SplitCtx cx, const i64 *off, i64 n, i64
 // pass 2: scatter every chunk through shared-memory cursors
 __global__ void __launch_bounds__(SPLIT_NT) k_split_scatter(LsjDev md, SplitCtx cx, const ulonglong2 *__restrict__ A,
                                                             const i64 *nitems, const i64 *__restrict__ off,
-                                                            ulonglong2 *B, SortCtl *ctl) {
+                                                            ulonglong2 *B, ulonglong2 *Out, SortCtl *ctl) {
     __shared__ u32 cur[2 * SPLIT_MAXF];
     __shared__ u64 v[SPLIT_MAXF];
     __shared__ i64 s_q;
@@ -446,10 +449,13 @@ __global__ void __launch_bounds__(SPLIT_NT) k_split_scatter(LsjDev md, SplitCtx 
                     if (s0 >= 0) {
                         u32 at = 0;
                         if (lane == 0) at = atomicAdd(cur + s0, 32u);
-                        B[a0 + __shfl_sync(0xffffffffu, at, 0) + lane] = r[u];
+                        // point slices (one key) are final: straight to the output
+                        ulonglong2 *dst = (points && (s0 & 1)) ? Out : B;
+                        dst[a0 + __shfl_sync(0xffffffffu, at, 0) + lane] = r[u];
                     }
                 } else if (s[u] >= 0) {
-                    B[a0 + atomicAdd(cur + s[u], 1u)] = r[u];
+                    ulonglong2 *dst = (points && (s[u] & 1)) ? Out : B;
+                    dst[a0 + atomicAdd(cur + s[u], 1u)] = r[u];
                 }
             }
         }
@@ -512,7 +518,7 @@ __global__ void __launch_bounds__(SORT_NT, 2) k_lsj_sort(LsjDev md, Src src, con
         if (b >= nbuckets) break;
         const Bucket bk = src.get(b);
         const int m = (int)(bk.m < (i64)CAP ? bk.m : (i64)CAP);
-        if (bk.m == 0) continue;
+        if (bk.m == 0 || bk.point) continue;
         if (bk.m == 1) {
             if (threadIdx.x == 0) out[bk.out_base] = in[bk.in_base];
             continue;
@@ -1018,7 +1024,7 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
     k_split_slots<<<grid_for(G + 1, 256, 8), 256, 0, st>>>(dev, cx, moff, n, sub_starts, sub_y);
     LJ_CK_LAUNCH();
     LJ_CK(cudaMemsetAsync(ctl, 0, sizeof(SortCtl), st));
-    k_split_scatter<<<sm_count() * 2, SPLIT_NT, 0, st>>>(dev, cx, A, cbase + nb, moff, B, ctl);
+    k_split_scatter<<<sm_count() * 2, SPLIT_NT, 0, st>>>(dev, cx, A, cbase + nb, moff, B, out, ctl);
     LJ_CK_LAUNCH();
     // K8 over the sub-buckets, B -> out (G = fbase[nb] read on device)
     SubBuckets sb{sub_starts, sub_y};
