@@ -38,8 +38,8 @@
 namespace lj {
 
 constexpr int SORT_NT = 512;     // two sort CTAs per SM (their barrier waits overlap)
-constexpr int CAP = 6144;         // largest bucket sorted in shared memory (96 KB per CTA)
-constexpr int RUN_SMALL = 64;     // equal-slot runs insertion-sorted by one thread
+constexpr int CAP = 6144;         // largest bucket sorted in shared memory (108 KB per CTA)
+constexpr int RUN_SMALL = 64;     // equal-slot runs ranked element by element
 constexpr int MAX_RUNS = 64;      // longer mixed runs sorted block-wide per bucket
 constexpr int SORT_U = 4;         // tuples in flight per thread in the load / write-out phases
 constexpr int SUB = 3072;         // mean tuples per sub-bucket: sample-quantile slices
@@ -502,6 +502,7 @@ __global__ void __launch_bounds__(SORT_NT, 2) k_lsj_sort(LsjDev md, Src src, con
     u32 *cnt = reinterpret_cast<u32 *>(K + CAP);          // slot counts -> cursors [CAP]
     u16 *slot = reinterpret_cast<u16 *>(cnt + CAP);       // slot per key [CAP]
     u16 *idx = slot + CAP;                                // placement [CAP]
+    u16 *ord = idx + CAP;                                 // final order [CAP]
     __shared__ u32 warp_tot[SORT_NT / 32];
     __shared__ i64 s_b;
     __shared__ int s_bad, s_nruns;
@@ -553,49 +554,61 @@ __global__ void __launch_bounds__(SORT_NT, 2) k_lsj_sort(LsjDev md, Src src, con
         block_scan_u32(cnt, m, warp_tot);
         for (int i = threadIdx.x; i < m; i += SORT_NT) idx[atomicAdd(cnt + slot[i], 1u)] = (u16)i;
         __syncthreads();
-        // runs sharing a slot: [start, cnt[slot]) after the scatter
-        for (int i = threadIdx.x; i < m; i += SORT_NT) {
-            const int si = slot[idx[i]];
-            if (i > 0 && slot[idx[i - 1]] == si) continue;  // not a run start
-            const int e = (int)cnt[si];
-            const int len = e - i;
-            if (len < 2) continue;
-            if (len <= RUN_SMALL) {
-                for (int a = i + 1; a < e; ++a) {
-                    const u16 v = idx[a];
-                    const u64 kv = K[v];
-                    int q = a - 1;
-                    while (q >= i && K[idx[q]] > kv) {
-                        idx[q + 1] = idx[q];
-                        --q;
-                    }
-                    idx[q + 1] = v;
+        // after the scatter cnt[s] = end of slot s's run = start of slot
+        // s+1's, so every element knows its run [cnt[s-1], cnt[s]).  Pass 1
+        // flags mixed runs (an element differing from the run's first key
+        // sets bit 31 of cnt[s]); pass 2: singletons and constant runs copy
+        // through, short mixed runs (<= RUN_SMALL) place each element at its
+        // rank in the run (key, then position), long mixed runs are copied
+        // and sorted block-wide below.
+        constexpr u32 MIXED = 0x80000000u;
+        for (int p = threadIdx.x; p < m; p += SORT_NT) {
+            const u16 ip = idx[p];
+            const int si = slot[ip];
+            const int a = si > 0 ? (int)(cnt[si - 1] & ~MIXED) : 0, e = (int)(cnt[si] & ~MIXED);
+            if (e - a > 1 && p != a && K[ip] != K[idx[a]]) atomicOr(cnt + si, MIXED);
+        }
+        __syncthreads();
+        for (int p = threadIdx.x; p < m; p += SORT_NT) {
+            const u16 ip = idx[p];
+            const int si = slot[ip];
+            const u32 ce = cnt[si];
+            const int a = si > 0 ? (int)(cnt[si - 1] & ~MIXED) : 0, e = (int)(ce & ~MIXED);
+            if (!(ce & MIXED)) {  // singleton or one repeated key
+                ord[p] = ip;
+                continue;
+            }
+            if (e - a <= RUN_SMALL) {
+                const u64 kv = K[ip];
+                int r = 0;
+                for (int q = a; q < e; ++q) {
+                    const u64 kq = K[idx[q]];
+                    r += (kq < kv || (kq == kv && q < p)) ? 1 : 0;
                 }
-            } else {
-                const u64 k0 = K[idx[i]];
-                bool same = true;
-                for (int a = i + 1; a < e && same; ++a) same = K[idx[a]] == k0;
-                if (!same) {  // long mixed run: queued for a block-wide sort below
-                    const int q = atomicAdd(&s_nruns, 1);
-                    if (q < MAX_RUNS) {
-                        s_runs[q] = make_int2(i, len);
-                    } else {
-                        s_bad = 1;
-                    }
+                ord[a + r] = ip;
+                continue;
+            }
+            ord[p] = ip;  // long mixed run: copied, queued by its first element
+            if (p == a) {
+                const int q = atomicAdd(&s_nruns, 1);
+                if (q < MAX_RUNS) {
+                    s_runs[q] = make_int2(p, e - p);
+                } else {
+                    s_bad = 1;
                 }
             }
         }
         __syncthreads();
         const int nruns = s_nruns < MAX_RUNS ? s_nruns : MAX_RUNS;
         if (!s_bad)
-            for (int q = 0; q < nruns; ++q) block_sort_idx(idx, s_runs[q].x, s_runs[q].y, K);
+            for (int q = 0; q < nruns; ++q) block_sort_idx(ord, s_runs[q].x, s_runs[q].y, K);
         for (int i = threadIdx.x; i + 1 < m; i += SORT_NT)
-            if (K[idx[i]] > K[idx[i + 1]]) s_bad = 1;
+            if (K[ord[i]] > K[ord[i + 1]]) s_bad = 1;
         __syncthreads();
         if (s_bad) {
             // safety net (the placement key is monotone, so this only runs
             // when too many long runs appeared): sort the whole bucket
-            block_sort_idx(idx, 0, m, K);
+            block_sort_idx(ord, 0, m, K);
             if (threadIdx.x == 0) atomicAdd(&ctl->n_fallback, 1ULL);
         }
         // write out: key from smem, payload gathered from the bucket (L2-hot)
@@ -605,7 +618,7 @@ __global__ void __launch_bounds__(SORT_NT, 2) k_lsj_sort(LsjDev md, Src src, con
 #pragma unroll
             for (int u = 0; u < SORT_U; ++u) {
                 const int i = i0 + u * SORT_NT;
-                j[u] = i < m ? idx[i] : 0;
+                j[u] = i < m ? ord[i] : 0;
                 p[u] = i < m ? __ldg(&in[bk.in_base + j[u]].y) : 0;
             }
 #pragma unroll
@@ -811,7 +824,7 @@ __global__ void k_sample(const u64 *keys, i64 n, i64 total, u64 seed, u64 *out) 
 static size_t al(size_t v) { return (v + 255) & ~(size_t)255; }
 
 static size_t sort_smem_bytes() {
-    return sizeof(u64) * CAP + sizeof(u32) * CAP + sizeof(u16) * CAP + sizeof(u16) * CAP;
+    return sizeof(u64) * CAP + sizeof(u32) * CAP + 3 * sizeof(u16) * CAP;
 }
 
 template <class Src>
