@@ -288,11 +288,15 @@ int lj_lsj_sort(const LjLsjModel *model, const uint64_t *pairs_in, uint64_t *pai
 int lj_lsj_ref_bounds(const LjRmi *model, const uint64_t *sorted_pairs, int64_t n, int64_t P, int64_t *bounds,
                       void *stream);
 /* lsj.py:316-370 chunked join (K9) of sorted S against sorted R through R's
- * model and bucket bounds.  mode 0: out[4] checksum; mode 1: counts[ns];
- * mode 2: pairs at offsets[ns] into out_pr/out_ps. */
+ * model and bucket bounds: every S tile's exact R slice is found first (one
+ * thread per tile, into ws), then tile and slice are merged in shared
+ * memory.  mode 0: out[4] checksum; mode 1: counts[ns]; mode 2: pairs at
+ * offsets[ns] into out_pr/out_ps. */
+size_t lj_lsj_join_workspace_bytes(int64_t ns);
 int lj_lsj_join(const LjLsjModel *model_r, const uint64_t *r_pairs, int64_t nr, const int64_t *r_starts,
                 const uint64_t *s_pairs, int64_t ns, int mode, int64_t *counts, const int64_t *offsets,
-                uint64_t *out_pr, uint64_t *out_ps, uint64_t *out, int accumulate, void *stream);
+                uint64_t *out_pr, uint64_t *out_ps, uint64_t *out, int accumulate, void *ws, size_t ws_bytes,
+                void *stream);
 
 #ifdef __cplusplus
 }

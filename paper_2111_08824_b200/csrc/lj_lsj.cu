@@ -50,7 +50,7 @@ constexpr i64 SPLIT_CH = 65536;   // tuples per split work item
 constexpr int SPLIT_MAXF = 2048;  // slices per coarse bucket (point mode: 2x-1 slots)
 constexpr int JOIN_T = 1024;
 constexpr int JOIN_NT = 256;
-constexpr int WCAP = 4096;
+constexpr int WCAP = 3840;  // R slice keys staged per tile (+ the S tile: < 48 KB static)
 
 // ------------------------------------------------------------------ model
 
@@ -727,74 +727,90 @@ __global__ void k_ref_bounds(RmiDev m, const ulonglong2 *sorted, i64 n, i64 P, i
 // ------------------------------------------------------------------- join
 
 // K9: see the file header.  mode 0: checksum; 1: per-S counts; 2: pairs.
-__global__ void __launch_bounds__(JOIN_NT) k_lsj_join(LsjDev mr, const ulonglong2 *__restrict__ R, i64 nr,
-                                                      const i64 *__restrict__ rst, const ulonglong2 *__restrict__ S,
-                                                      i64 ns, int mode, i64 *counts, const i64 *offsets, u64 *opr,
-                                                      u64 *ops, u64 *out) {
-    __shared__ u64 wk[WCAP];
-    __shared__ i64 s_lo, s_hi;
+// Exact R slice of every S tile: [lower_bound(first S key),
+// upper_bound(last S key)) inside the R bucket range that R's model gives
+// for them (lsj.py:346-356).  One thread per tile, all tiles at once, so
+// the dependent probes of the searches overlap across the grid.
+__global__ void k_join_bounds(LsjDev mr, const ulonglong2 *__restrict__ R, const i64 *__restrict__ rst,
+                              const ulonglong2 *__restrict__ S, i64 ns, i64 ntiles, i64 *tb) {
+    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < ntiles; t += (i64)gridDim.x * blockDim.x) {
+        const i64 a = t * JOIN_T, e = min(a + (i64)JOIN_T, ns);
+        const u64 kf = S[a].x, kl = S[e - 1].x;
+        const i64 wlo = rst[mr.bin(kf)], whi = rst[mr.bin(kl) + 1];
+        i64 lo = wlo, hi = whi;
+        while (lo < hi) {
+            const i64 mid = (lo + hi) >> 1;
+            if (R[mid].x < kf) lo = mid + 1; else hi = mid;
+        }
+        const i64 rlo = lo;
+        hi = whi;
+        while (lo < hi) {
+            const i64 mid = (lo + hi) >> 1;
+            if (R[mid].x <= kl) lo = mid + 1; else hi = mid;
+        }
+        tb[2 * t] = rlo;
+        tb[2 * t + 1] = lo > rlo ? lo : rlo;
+    }
+}
+
+// K9: per S tile of JOIN_T, the tile (keys + payloads) and its R slice keys
+// staged in shared memory; each thread takes JOIN_PER consecutive S tuples:
+// one lower bound in the slice for the first, then a forward merge walk.
+// mode 0: checksum; mode 1: counts[ns]; mode 2: pairs at offsets[ns].
+constexpr int JOIN_PER = JOIN_T / JOIN_NT;
+
+__global__ void __launch_bounds__(JOIN_NT) k_lsj_join(const ulonglong2 *__restrict__ R,
+                                                      const ulonglong2 *__restrict__ S, i64 ns, const i64 *tb,
+                                                      int mode, i64 *counts, const i64 *offsets, u64 *opr, u64 *ops,
+                                                      u64 *out) {
+    __shared__ u64 wk[WCAP + 1];
+    __shared__ u64 sk[JOIN_T], sp[JOIN_T];
     u64 cnt = 0, sum = 0, x = 0;
     const i64 ntiles = (ns + JOIN_T - 1) / JOIN_T;
     for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const i64 a = tile * JOIN_T, e = min(a + (i64)JOIN_T, ns);
-        if (threadIdx.x < 2) {
-            // R bucket range of the tile's first / last key through R's model,
-            // then the exact slice [lower_bound(kf), upper_bound(kl))
-            const u64 kf = S[a].x, kl = S[e - 1].x;
-            const i64 wlo = rst[mr.bin(kf)], whi = rst[mr.bin(kl) + 1];
-            i64 lo = wlo, hi = whi;
-            if (threadIdx.x == 0) {
-                while (lo < hi) {
-                    i64 mid = (lo + hi) >> 1;
-                    if (R[mid].x < kf) lo = mid + 1; else hi = mid;
-                }
-                s_lo = lo;
-            } else {
-                while (lo < hi) {
-                    i64 mid = (lo + hi) >> 1;
-                    if (R[mid].x <= kl) lo = mid + 1; else hi = mid;
-                }
-                s_hi = lo;
-            }
+        const int ne = (int)(e - a);
+        const i64 wlo = tb[2 * tile], whi = tb[2 * tile + 1], w = whi - wlo;
+        const bool staged = w <= WCAP;
+        if (staged) {
+            for (int j = threadIdx.x; j < (int)w; j += JOIN_NT) wk[j] = R[wlo + j].x;
+            if (threadIdx.x == 0) wk[w] = ~0ULL;  // sentinel above every key
+        }
+        for (int j = threadIdx.x; j < ne; j += JOIN_NT) {
+            const ulonglong2 v = S[a + j];
+            sk[j] = v.x;
+            sp[j] = v.y;
         }
         __syncthreads();
-        const i64 wlo = s_lo, whi = s_hi > s_lo ? s_hi : s_lo, w = whi - wlo;
-        const bool staged = w <= WCAP;
-        if (staged)
-            for (i64 j = threadIdx.x; j < w; j += JOIN_NT) wk[j] = R[wlo + j].x;
-        __syncthreads();
-        for (i64 i = a + threadIdx.x; i < e; i += JOIN_NT) {
-            const ulonglong2 sv = S[i];
-            i64 lo, hi;
-            if (staged) {
-                lo = 0;
-                hi = w;
+        const int j0 = threadIdx.x * JOIN_PER;
+        i64 pos = 0;  // lower bound of the previous S key, relative to wlo
+        for (int u = 0; u < JOIN_PER; ++u) {
+            const int j = j0 + u;
+            if (j >= ne) break;
+            const u64 k = sk[j];
+            if (u == 0 || !staged) {
+                i64 lo = u == 0 ? 0 : pos, hi = w;
                 while (lo < hi) {
-                    i64 mid = (lo + hi) >> 1;
-                    if (wk[mid] < sv.x) lo = mid + 1; else hi = mid;
+                    const i64 mid = (lo + hi) >> 1;
+                    if ((staged ? wk[mid] : R[wlo + mid].x) < k) lo = mid + 1; else hi = mid;
                 }
-                lo += wlo;
+                pos = lo;
             } else {
-                lo = wlo;
-                hi = whi;
-                while (lo < hi) {
-                    i64 mid = (lo + hi) >> 1;
-                    if (R[mid].x < sv.x) lo = mid + 1; else hi = mid;
-                }
+                while (wk[pos] < k) ++pos;  // S is sorted: lower bounds only grow
             }
-            i64 c = 0;
-            i64 o = mode == 2 ? offsets[i] : 0;
-            for (i64 j = lo; j < whi; ++j) {
-                const u64 rk = staged ? wk[j - wlo] : R[j].x;
-                if (rk != sv.x) break;
+            const i64 i = a + j;
+            i64 c = 0, o = mode == 2 ? offsets[i] : 0;
+            for (i64 q = pos; q < w; ++q) {
+                const u64 rk = staged ? wk[q] : R[wlo + q].x;
+                if (rk != k) break;
                 if (mode == 0) {
-                    const u64 v = R[j].y + sv.y;
+                    const u64 v = R[wlo + q].y + sp[j];
                     ++cnt;
                     sum += v;
                     x ^= v;
                 } else if (mode == 2) {
-                    opr[o] = R[j].y;
-                    ops[o] = sv.y;
+                    opr[o] = R[wlo + q].y;
+                    ops[o] = sp[j];
                     ++o;
                 }
                 ++c;
@@ -1127,9 +1143,14 @@ int lj_lsj_ref_bounds(const LjRmi *model, const uint64_t *sorted_pairs, int64_t 
     return LJ_OK;
 }
 
+size_t lj_lsj_join_workspace_bytes(int64_t ns) {
+    return sizeof(i64) * 2 * (size_t)((ns + JOIN_T - 1) / JOIN_T + 1);
+}
+
 int lj_lsj_join(const LjLsjModel *model_r, const uint64_t *r_pairs, int64_t nr, const int64_t *r_starts,
                 const uint64_t *s_pairs, int64_t ns, int mode, int64_t *counts, const int64_t *offsets,
-                uint64_t *out_pr, uint64_t *out_ps, uint64_t *out, int accumulate, void *stream) {
+                uint64_t *out_pr, uint64_t *out_ps, uint64_t *out, int accumulate, void *ws, size_t ws_bytes,
+                void *stream) {
     LJ_REQUIRE(model_r && model_r->table && model_r->pb, "R model has no bins");
     LJ_REQUIRE(mode >= 0 && mode <= 2, "mode must be 0, 1 or 2");
     cudaStream_t st = as_stream(stream);
@@ -1138,11 +1159,18 @@ int lj_lsj_join(const LjLsjModel *model_r, const uint64_t *r_pairs, int64_t nr, 
         if (mode == 1 && ns > 0) LJ_CK(cudaMemsetAsync(counts, 0, sizeof(i64) * (size_t)ns, st));
         return LJ_OK;
     }
+    if (ws_bytes < lj_lsj_join_workspace_bytes(ns)) {
+        set_error("lj_lsj_join: workspace too small");
+        return LJ_E_WORKSPACE;
+    }
     const i64 ntiles = (ns + JOIN_T - 1) / JOIN_T;
+    i64 *tb = (i64 *)ws;
+    const ulonglong2 *R = reinterpret_cast<const ulonglong2 *>(r_pairs);
+    const ulonglong2 *S = reinterpret_cast<const ulonglong2 *>(s_pairs);
+    k_join_bounds<<<grid_for(ntiles, 128, 16), 128, 0, st>>>(make_lsj(*model_r), R, r_starts, S, ns, ntiles, tb);
+    LJ_CK_LAUNCH();
     const unsigned g = (unsigned)(ntiles < (i64)sm_count() * 8 ? ntiles : (i64)sm_count() * 8);
-    k_lsj_join<<<g, JOIN_NT, 0, st>>>(make_lsj(*model_r), reinterpret_cast<const ulonglong2 *>(r_pairs), nr,
-                                      r_starts, reinterpret_cast<const ulonglong2 *>(s_pairs), ns, mode, counts,
-                                      offsets, out_pr, out_ps, out);
+    k_lsj_join<<<g, JOIN_NT, 0, st>>>(R, S, ns, tb, mode, counts, offsets, out_pr, out_ps, out);
     LJ_CK_LAUNCH();
     return LJ_OK;
 }

@@ -340,18 +340,20 @@ def _join(r_sorted: SortedRelation, s_sorted: SortedRelation, materialize: bool)
     dev = s_sorted.pairs.device
     c = r_sorted.lmodel.c_struct()
     args = (ctypes.byref(c), _lib.ptr(r_sorted.pairs), nr, _lib.ptr(r_sorted.starts), _lib.ptr(s_sorted.pairs), ns)
+    ws = _lib.workspace(lib.lj_lsj_join_workspace_bytes(ns), dev)
+    tail = (_lib.ptr(ws), ws.numel(), _lib.stream_ptr())
     if not materialize:
         out = torch.zeros(4, dtype=torch.int64, device=dev)
-        _lib.check(lib.lj_lsj_join(*args, 0, None, None, None, None, _lib.ptr(out), 0, _lib.stream_ptr()), "lsj_join")
+        _lib.check(lib.lj_lsj_join(*args, 0, None, None, None, None, _lib.ptr(out), 0, *tail), "lsj_join")
         return JoinResult(words=out)
     counts = torch.empty(max(ns, 1), dtype=torch.int64, device=dev)
-    _lib.check(lib.lj_lsj_join(*args, 1, _lib.ptr(counts), None, None, None, None, 0, _lib.stream_ptr()), "lsj_join")
+    _lib.check(lib.lj_lsj_join(*args, 1, _lib.ptr(counts), None, None, None, None, 0, *tail), "lsj_join")
     offsets, total = exclusive_offsets(counts[:ns])
     pr = torch.empty(total, dtype=torch.int64, device=dev)
     ps = torch.empty(total, dtype=torch.int64, device=dev)
     if total:
-        _lib.check(lib.lj_lsj_join(*args, 2, None, _lib.ptr(offsets), _lib.ptr(pr), _lib.ptr(ps), None, 0,
-                                   _lib.stream_ptr()), "lsj_join")
+        _lib.check(lib.lj_lsj_join(*args, 2, None, _lib.ptr(offsets), _lib.ptr(pr), _lib.ptr(ps), None, 0, *tail),
+                   "lsj_join")
     return JoinResult(pr, ps)
 
 
