@@ -899,7 +899,7 @@ int lj_leaf_bucket(const LjGrmi *idx, const uint64_t *keys, const uint64_t *pay,
     k_window_keys<<<(nwin + 255) / 256, 256, 0, st>>>(idx->slots, nwin, f.wshift, (u64 *)f.wk);
     LJ_CK_LAUNCH();
     SoaSrc<SlotBin> src{keys, pay, f};
-    return run_partition(src, nk, nwin, reinterpret_cast<ulonglong2 *>(pairs_out), starts_out, nullptr, ws, pws, st);
+    return run_partition(src, nk, nwin, reinterpret_cast<ulonglong2 *>(pairs_out), starts_out, ws, pws, st);
 }
 
 }  // extern "C"

@@ -929,7 +929,7 @@ int lj_lsj_partition(const LjLsjModel *md, const uint64_t *keys, const uint64_t 
     LsjBin f;
     f.d = make_lsj(*md);
     SoaSrc<LsjBin> src{keys, pay, f};
-    return run_partition(src, n, (int)md->nbins, reinterpret_cast<ulonglong2 *>(pairs), starts, nullptr, ws, ws_bytes,
+    return run_partition(src, n, (int)md->nbins, reinterpret_cast<ulonglong2 *>(pairs), starts, ws, ws_bytes,
                          as_stream(stream));
 }
 

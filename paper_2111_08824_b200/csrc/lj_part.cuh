@@ -4,12 +4,10 @@
 // Every block owns a fixed contiguous chunk of the input.  Pass 1 evaluates
 // the bin function once per tuple, counts the chunk into a shared-memory
 // histogram stored as one column of a bins x blocks matrix, and keeps the
-// tuple's 32-bit code (bin << shift | aux); an exclusive scan of the matrix
-// (bin-major) gives every block its private write offset per bin; pass 2
-// scatters the chunk by the stored codes.  Output is interleaved 16-B
-// (key, payload) records, bins contiguous, order inside a bin unspecified;
-// optionally the low `shift` bits of each code (aux, e.g. the predicted
-// slot inside a GRMI window) are written next to the records as u16.
+// tuple's bin (u16); an exclusive scan of the matrix (bin-major) gives every
+// block its private write offset per bin; pass 2 scatters the chunk by the
+// stored bins.  Output is interleaved 16-B (key, payload) records, bins
+// contiguous, order inside a bin unspecified.
 //
 // Measured design points (B200, profiles/, tools/micro/):
 //  * one shared atomic per tuple (ATOMS: 5-7 tuples/clk/SM even with a
@@ -117,7 +115,7 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_hist(Src f0, i64 n, i64 chunk,
 
 template <class Src>
 __global__ void __launch_bounds__(PART2_NT) k_bin_scatter(Src f0, i64 n, i64 chunk, int nbins,
-                                                          const i64 *__restrict__ off, ulonglong2 *out, u16 *aux) {
+                                                          const i64 *__restrict__ off, ulonglong2 *out) {
     extern __shared__ __align__(128) unsigned char smem_c[];
     u64 *tab = reinterpret_cast<u64 *>(smem_c);
     u32 *cur = reinterpret_cast<u32 *>(smem_c + pt_table_bytes(f0.f.smem_words()));
@@ -127,7 +125,6 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter(Src f0, i64 n, i64 chu
     for (int j = threadIdx.x; j < nbins; j += PART2_NT) cur[j] = (u32)off[(i64)j * gridDim.x + blockIdx.x];
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, shift = f.f.shift;
-    const u32 amask = (1u << shift) - 1u;
     const i64 lo = blockIdx.x * chunk, hi = min(lo + chunk, n);
     for (i64 base = lo + (i64)warp * 32 * PART2_U; base < hi; base += (i64)PART2_NT * PART2_U) {
         u32 c[PART2_U];
@@ -142,9 +139,7 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter(Src f0, i64 n, i64 chu
 #pragma unroll
         for (int u = 0; u < PART2_U; ++u) {
             if (base + u * 32 + lane >= hi) continue;
-            const u32 at = atomicAdd(cur + (c[u] >> shift), 1u);
-            out[at] = make_ulonglong2(k[u], p[u]);
-            if (aux) aux[at] = (u16)(c[u] & amask);
+            out[atomicAdd(cur + (c[u] >> shift), 1u)] = make_ulonglong2(k[u], p[u]);
         }
     }
 }
@@ -152,9 +147,9 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter(Src f0, i64 n, i64 chu
 // ---- bulk-copy pipelined kernels (16-B aligned columns)
 
 constexpr int PT_TILE_H = PART2_NT * 4;  // keys per histogram tile (32 KB)
-constexpr int PT_TILE_S = 4096;          // tuples per sorted scatter tile
+constexpr int PT_TILE_S = 4096;          // tuples per sorted scatter tile (longer bin runs beat deeper rings)
 constexpr size_t PT_STAGE_H = sizeof(u64) * PT_TILE_H;
-constexpr size_t PT_STAGE_S = (size_t)PT_TILE_S * (8 + 8 + 4);
+constexpr size_t PT_STAGE_S = (size_t)PT_TILE_S * (8 + 8 + 2);
 constexpr int PT_MAXST = 6;
 constexpr int PT_SMEM_MAX = 220 * 1024;
 
@@ -167,7 +162,7 @@ constexpr int PT_H_CONS = PART2_NT / 32 - 1;
 
 template <class Src>
 __global__ void __launch_bounds__(PART2_NT) k_bin_hist_tma(Src f0, i64 n, i64 chunk, int nbins, int hc, int nst,
-                                                           u32 *mat, u32 *codes) {
+                                                           u32 *mat, u16 *bins) {
     extern __shared__ __align__(128) unsigned char smem_t[];
     u64 *tab = reinterpret_cast<u64 *>(smem_t);
     unsigned char *smem = smem_t + pt_table_bytes(f0.f.smem_words());
@@ -223,8 +218,9 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_hist_tma(Src f0, i64 n, i64 ch
                 for (int u = 0; u < U; ++u) {
                     const int j = (r0 + u * PT_H_CONS) * 32 + lane;
                     if (j < cnt) {
-                        atomicAdd(hw + (c[u] >> shift), 1u);
-                        codes[base + j] = c[u];
+                        const u32 b = c[u] >> shift;
+                        atomicAdd(hw + b, 1u);
+                        bins[base + j] = (u16)b;
                     }
                 }
             }
@@ -237,9 +233,9 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_hist_tma(Src f0, i64 n, i64 ch
 }
 
 template <class Src>
-__global__ void __launch_bounds__(PART2_NT) k_bin_scatter_tma(Src f, const u32 *__restrict__ codes, i64 n, i64 chunk,
+__global__ void __launch_bounds__(PART2_NT) k_bin_scatter_tma(Src f, const u16 *__restrict__ bins, i64 n, i64 chunk,
                                                               int nbins, int nst, const i64 *__restrict__ off,
-                                                              ulonglong2 *out, u16 *aux) {
+                                                              ulonglong2 *out) {
     constexpr int U = PT_TILE_S / PART2_NT;
     extern __shared__ __align__(128) unsigned char smem[];
     const int nb4 = (nbins + 31) & ~31;
@@ -251,8 +247,7 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_tma(Src f, const u32 *
     unsigned char *ring = reinterpret_cast<unsigned char *>(perm) + ((PT_TILE_S * 2 + 127) & ~127);
     __shared__ __align__(8) uint64_t full[PT_MAXST];
     __shared__ u32 wsum[PART2_NT / 32];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, shift = f.f.shift;
-    const u32 amask = (1u << shift) - 1u;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int j = tid; j < nbins; j += PART2_NT) {
         cur[j] = (u32)off[(i64)j * gridDim.x + blockIdx.x];
         thist[j] = 0;
@@ -263,15 +258,15 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_tma(Src f, const u32 *
         const int s = t % nst;
         const i64 base = lo + (i64)t * PT_TILE_S;
         const int cnt = (int)min((i64)PT_TILE_S, hi - base);
-        const unsigned b8 = (unsigned)(cnt * 8) & ~15u, b4 = (unsigned)(cnt * 4) & ~15u;
+        const unsigned b8 = (unsigned)(cnt * 8) & ~15u, b2 = (unsigned)(cnt * 2) & ~15u;
         unsigned char *st = ring + (size_t)s * PT_STAGE_S;
-        if (b8 + b4) {
-            mbar_arrive_expect_tx(&full[s], 2 * b8 + b4);
+        if (b8 + b2) {
+            mbar_arrive_expect_tx(&full[s], 2 * b8 + b2);
             if (b8) {
                 bulk_g2s(st, f.keys + base, b8, &full[s]);
                 bulk_g2s(st + PT_TILE_S * 8, f.pay + base, b8, &full[s]);
             }
-            if (b4) bulk_g2s(st + PT_TILE_S * 16, codes + base, b4, &full[s]);
+            if (b2) bulk_g2s(st + PT_TILE_S * 16, bins + base, b2, &full[s]);
         } else {
             mbar_arrive(&full[s]);
         }
@@ -287,16 +282,16 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_tma(Src f, const u32 *
         if (tid == 0 && t + nst - 1 < ntiles) issue(t + nst - 1);  // stage consumed in round t-1
         mbar_wait(&full[s], (unsigned)(t / nst) & 1u);
         const i64 base = lo + (i64)t * PT_TILE_S;
-        const int cnt = (int)min((i64)PT_TILE_S, hi - base), nb = cnt & ~1, nb4c = cnt & ~3;
+        const int cnt = (int)min((i64)PT_TILE_S, hi - base), nb = cnt & ~1, nb8 = cnt & ~7;
         const unsigned char *st = ring + (size_t)s * PT_STAGE_S;
         const u64 *ks = reinterpret_cast<const u64 *>(st), *ps = ks + PT_TILE_S;
-        const u32 *cs = reinterpret_cast<const u32 *>(st + PT_TILE_S * 16);
+        const u16 *bs = reinterpret_cast<const u16 *>(st + PT_TILE_S * 16);
         // (1) rank of each tuple inside its bin's run of this tile
         int bj[U], rj[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int j = u * PART2_NT + tid;
-            bj[u] = j < cnt ? (int)((j < nb4c ? cs[j] : codes[base + j]) >> shift) : -1;
+            bj[u] = j < cnt ? (int)(j < nb8 ? bs[j] : bins[base + j]) : -1;
             rj[u] = bj[u] >= 0 ? (int)atomicAdd(thist + bj[u], 1u) : 0;
         }
         __syncthreads();
@@ -350,13 +345,11 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_tma(Src f, const u32 *
             const int i = u * PART2_NT + tid;
             if (i < cnt) {
                 const int j = perm[i];
-                const u32 c = j < nb4c ? cs[j] : codes[base + j];
-                const int b = (int)(c >> shift);
+                const int b = j < nb8 ? bs[j] : bins[base + j];
                 const u64 k = j < nb ? ks[j] : ld_stream(f.keys + base + j);
                 const u64 p = j < nb ? ps[j] : ld_stream(f.pay + base + j);
                 const u32 at = gbase[b] + (u32)i - tstart[b];
                 out[at] = make_ulonglong2(k, p);
-                if (aux) aux[at] = (u16)(c & amask);
             }
         }
         __syncthreads();
@@ -391,14 +384,14 @@ inline size_t part_workspace_bytes(i64 n, int nbins) {
     PartPlan p = part_plan(n, nbins);
     i64 items = (i64)nbins * p.blocks;
     return part_align(sizeof(u32) * (size_t)items) + part_align(sizeof(i64) * (size_t)items) +
-           part_align(sizeof(u32) * (size_t)n) + part_align(part_scan_bytes(items));
+           part_align(sizeof(u16) * (size_t)n) + part_align(part_scan_bytes(items));
 }
 
 // Full partition of the n tuples of `f`: out[n] records grouped by bin,
-// starts[nbins+1]; aux[n] (optional) the low f.f.shift code bits per record.
+// starts[nbins+1].
 template <class Src>
-int run_partition(const Src &f, i64 n, int nbins, ulonglong2 *out, i64 *starts, u16 *aux, void *ws,
-                  size_t ws_bytes, cudaStream_t st) {
+int run_partition(const Src &f, i64 n, int nbins, ulonglong2 *out, i64 *starts, void *ws, size_t ws_bytes,
+                  cudaStream_t st) {
     if (nbins < 1 || nbins > PART2_MAXBINS) {
         set_error("partition: nbins must be in [1, 32768]");
         return LJ_E_INVALID;
@@ -407,8 +400,8 @@ int run_partition(const Src &f, i64 n, int nbins, ulonglong2 *out, i64 *starts, 
         set_error("partition: cursors are 32-bit");
         return LJ_E_INVALID;
     }
-    if (f.f.shift < 0 || f.f.shift > 31 || (aux && f.f.shift > 16)) {
-        set_error("partition: aux bits must fit u16");
+    if (f.f.shift < 0 || f.f.shift > 31) {
+        set_error("partition: bad bin shift");
         return LJ_E_INVALID;
     }
     if (ws_bytes < part_workspace_bytes(n, nbins)) {
@@ -422,8 +415,8 @@ int run_partition(const Src &f, i64 n, int nbins, ulonglong2 *out, i64 *starts, 
     q += part_align(sizeof(u32) * (size_t)items);
     i64 *off = (i64 *)q;
     q += part_align(sizeof(i64) * (size_t)items);
-    u32 *codes = (u32 *)q;  // pass-1 codes for the pipelined pass 2
-    q += part_align(sizeof(u32) * (size_t)n);
+    u16 *bins = (u16 *)q;  // pass-1 bins for the pipelined pass 2
+    q += part_align(sizeof(u16) * (size_t)n);
     const size_t sm_h = sizeof(u32) * (size_t)nbins * p.hc, sm_s = sizeof(u32) * (size_t)nbins;
     static bool attr_set = false;
     if (!attr_set) {
@@ -442,7 +435,7 @@ int run_partition(const Src &f, i64 n, int nbins, ulonglong2 *out, i64 *starts, 
     const bool tma = !no_tma && f.aligned16() && nst_h >= 2 && nst_s >= 2 && nbins <= 2 * PART2_NT;
     if (n > 0 && tma) {
         k_bin_hist_tma<Src><<<p.blocks, PART2_NT, fix_h + nst_h * PT_STAGE_H, st>>>(f, n, p.chunk, nbins, p.hc, nst_h,
-                                                                                     mat, codes);
+                                                                                     mat, bins);
         LJ_CK_LAUNCH();
     } else if (n > 0) {
         k_bin_hist<Src><<<p.blocks, PART2_NT, tb + sm_h, st>>>(f, n, p.chunk, nbins, p.hc, mat);
@@ -456,11 +449,11 @@ int run_partition(const Src &f, i64 n, int nbins, ulonglong2 *out, i64 *starts, 
     k_bin_starts<<<(nbins + 256) / 256, 256, 0, st>>>(off, nbins, p.blocks, n, starts);
     LJ_CK_LAUNCH();
     if (n > 0 && tma) {
-        k_bin_scatter_tma<Src><<<p.blocks, PART2_NT, fix_s + nst_s * PT_STAGE_S, st>>>(f, codes, n, p.chunk, nbins,
-                                                                                        nst_s, off, out, aux);
+        k_bin_scatter_tma<Src><<<p.blocks, PART2_NT, fix_s + nst_s * PT_STAGE_S, st>>>(f, bins, n, p.chunk, nbins,
+                                                                                        nst_s, off, out);
         LJ_CK_LAUNCH();
     } else if (n > 0) {
-        k_bin_scatter<Src><<<p.blocks, PART2_NT, tb + sm_s, st>>>(f, n, p.chunk, nbins, off, out, aux);
+        k_bin_scatter<Src><<<p.blocks, PART2_NT, tb + sm_s, st>>>(f, n, p.chunk, nbins, off, out);
         LJ_CK_LAUNCH();
     }
     return LJ_OK;

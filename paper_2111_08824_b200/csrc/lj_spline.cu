@@ -274,8 +274,7 @@ int lj_spline_hash_bucket(const LjSplineHash *idx, const uint64_t *keys, const u
     f.n = idx->model.n;
     f.rn = (double)f.nb / (double)idx->model.n;
     SoaSrc<PosBin> src{keys, pay, f};
-    return run_partition(src, nk, (int)f.nb, reinterpret_cast<ulonglong2 *>(pairs_out), starts_out, nullptr, ws,
-                         ws_bytes,
+    return run_partition(src, nk, (int)f.nb, reinterpret_cast<ulonglong2 *>(pairs_out), starts_out, ws, ws_bytes,
                          as_stream(stream));
 }
 
