@@ -191,6 +191,24 @@ struct SplineDev {
         : K(s.npts), n(s.n), max_error(s.max_error), radix_bits(s.radix_bits), shift(s.shift),
           keys(s.keys), ranks(s.ranks), radix(s.radix), aux(s.aux), sub(s.sub) {}
 
+    // first spline point of k's (sub-)radix bucket: a cheap, monotone
+    // approximation of where k lands (no search, no division)
+    __device__ __forceinline__ i64 bucket_first_point(u64 k) const {
+        if (K <= 1) return 0;
+        const i64 rmax = ((i64)1 << radix_bits) - 1;
+        const u64 raw = shift >= 64 ? 0 : (k >> shift);
+        i64 lo;
+        const u64 ax = (aux && raw <= (u64)rmax) ? ldg(aux + raw) : 0;
+        if (ax & 0xFF) {
+            const int bits = (int)(ax & 0xFF);
+            const u64 q = (k >> (shift - (u64)bits)) & ((1ULL << bits) - 1ULL);
+            lo = (i64)__ldg(sub + (ax >> 8) + q);
+        } else {
+            lo = (i64)__ldg(radix + (raw > (u64)rmax ? rmax : (i64)raw));
+        }
+        return lo < 0 ? 0 : (lo > K - 1 ? K - 1 : lo);
+    }
+
     // models.py:221-248 + _bounded_first_geq :263-282
     __device__ __forceinline__ i64 pos(u64 k) const {
         i64 p;

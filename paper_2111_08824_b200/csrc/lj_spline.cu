@@ -21,10 +21,14 @@ struct HashDev {
     i64 n, P, stride;
     const u64 *entries;
     const u32 *starts;
+    bool direct;  // P == stride * trained_len: bucket / stride == pos, no division
     __host__ explicit HashDev(const LjSplineHash &h)
-        : model(h.model), n(h.n), P(h.table_len), stride(h.stride), entries(h.entries), starts(h.starts) {}
+        : model(h.model), n(h.n), P(h.table_len), stride(h.stride), entries(h.entries), starts(h.starts),
+          direct(h.model.n > 0 && h.table_len == h.stride * h.model.n) {}
     __device__ __forceinline__ i64 slot_of(u64 k) const {
-        return scale_bucket(model.pos(k), P, model.n) / stride;
+        // models.py:297 clip(pos*P // n, 0, P-1) / stride; pos is in [0, n)
+        const i64 p = model.pos(k);
+        return direct ? p : scale_bucket(p, P, model.n) / stride;
     }
 };
 
@@ -247,15 +251,20 @@ int lj_spline_hash_probe(const LjSplineHash *idx, const uint64_t *s_keys, const 
 }
 
 // Request-Buffer analogue for the learned hash: group S by a window of
-// predicted positions (<= 2048 windows), shared-memory-privatised partition.
+// APPROXIMATE position (<= 2048 windows): the rank of the first spline point
+// of the key's (sub-)radix bucket -- two or three L2-resident loads, no
+// search and no division.  Grouping only buys locality (the probe computes
+// the exact bucket), and that rank is within one bucket's span of the
+// key's position, so a window's chains stay in one small stretch of the
+// table.  (The exact spline evaluation here cost 50 ms at C3.)
 struct PosBin : NoTable {
     SplineDev m;
     i64 nb, n;
     double rn;
     int shift = 0;
     __device__ __forceinline__ u32 code(u64 k) const {
-        const i64 p = m.pos(k);  // in [0, n)
-        i64 b = (i64)(__dmul_rn(i64_to_f64(p), rn));
+        const double r = __ldg(m.ranks + m.bucket_first_point(k));
+        const i64 b = (i64)(r * rn);
         return (u32)(b < 0 ? 0 : (b >= nb ? nb - 1 : b));
     }
     __device__ __forceinline__ PosBin at(u64 *) const { return *this; }
