@@ -383,3 +383,24 @@ def test_spline_hash_grouped_probe_equals_direct(lj):
     assert grouped == direct
     want = oracle.smj_checksum(*inp.r.numpy(), *inp.s.numpy())
     assert (direct[0], direct[1] & MASK, direct[2] & MASK) == want
+
+
+def test_partition_fallback_on_unaligned_columns(lj):
+    """Key/payload columns that are not 16-B aligned take the plain-load
+    partition kernels (no bulk copies); results are unchanged (K4 and LSJ)."""
+    from paper_2111_08824_b200 import configs
+
+    inp = configs.config2(scale=6)
+    idx = lj.GappedRmiIndex(2.0, 1024).fit(inp.r)
+    n = len(inp.s) - 1
+    base = idx.join_checksum(inp.s.keys[1:], inp.s.payloads[1:]).cpu().tolist()
+    k1, p1 = inp.s.keys[1:], inp.s.payloads[1:]  # 8-B aligned views
+    assert k1.data_ptr() % 16 == 8
+    got = idx.join_checksum_buffered(k1, p1).cpu().tolist()
+    assert got == base
+    # LSJ on unaligned views of both relations
+    r = lj.Relation(inp.r.keys[1:].contiguous(), inp.r.payloads[1:].contiguous())
+    s = lj.Relation(inp.s.keys[1:n // 2], inp.s.payloads[1:n // 2], validate=False)
+    assert s.keys.data_ptr() % 16 == 8
+    res, _ = lj.lsj_join(r, s)
+    assert res.checksum == oracle.smj_checksum(*r.numpy(), *s.numpy())
