@@ -185,22 +185,28 @@ int lj_grmi_collect(const LjGrmi *idx, const uint64_t *keys, int64_t nk, const i
  * W[w] < k <= W[w+1], W[w] the gapped key at slot w * 2^shift, so every
  * key's lower bound lies inside its window's slot range.  The window is
  * found from the model's predicted slot (gapped.py:258-261) and corrected by
- * the neighbouring window keys.  <= 2048 windows (bins =
- * lj_leaf_bucket_bins(L)); two passes with shared-memory histograms (no
- * per-tuple global atomics).  pairs_out[2nk] interleaved {key, payload}
- * grouped by window, starts_out[bins+1]; order inside a window is
- * unspecified. */
+ * the neighbouring window keys.  bins = lj_leaf_bucket_bins(L) <= 2048.
+ * Output: pairs_out (capacity lj_leaf_bucket_capacity(nk, L) records) of
+ * interleaved {key, payload}; reg_out[lj_leaf_bucket_regions(L)] =
+ * {rstart[0..bins], rend[0..bins), overflow}: window w's records are
+ * [rstart[w], rend[w]), then `overflow` records of any window follow at
+ * rstart[bins].  When the staged probe applies, one pass fills regions sized
+ * from a 1/16 sample (gaps after each window, rare overflow); otherwise two
+ * passes produce the exact, gap-free layout (overflow 0).  Order inside a
+ * window is unspecified. */
 int lj_leaf_bucket_bins(int64_t L);
+int lj_leaf_bucket_regions(int64_t L);
+int64_t lj_leaf_bucket_capacity(int64_t nk, int64_t L);
 size_t lj_leaf_bucket_workspace_bytes(int64_t nk, int64_t L);
 int lj_leaf_bucket(const LjGrmi *idx, const uint64_t *keys, const uint64_t *pay, int64_t nk,
-                   uint64_t *pairs_out, int64_t *starts_out, void *ws, size_t ws_bytes, void *stream);
-/* K1 over the output of lj_leaf_bucket (records + window starts): each CTA
- * stages a window's real entries in shared memory and searches there;
- * results and search_steps equal lj_grmi_probe's (the reference's probe
- * count follows from the predicted slot and the key's position).  ws: 8
- * bytes of device scratch (work counter). */
-int lj_grmi_probe_bucketed(const LjGrmi *idx, const uint64_t *s_pairs, int64_t nk, const int64_t *wstarts,
-                           void *ws, uint64_t *out, int accumulate, void *stream);
+                   uint64_t *pairs_out, int64_t *reg_out, void *ws, size_t ws_bytes, void *stream);
+/* K1 over the output of lj_leaf_bucket: each CTA stages a window's real
+ * entries in shared memory and searches there, the overflow records take the
+ * plain K1; results and search_steps equal lj_grmi_probe's (the reference's
+ * probe count follows from the predicted slot and the key's position).  ws:
+ * 8 bytes of device scratch (work counter). */
+int lj_grmi_probe_bucketed(const LjGrmi *idx, const uint64_t *s_pairs, const int64_t *reg, void *ws, uint64_t *out,
+                           int accumulate, void *stream);
 /* K1 over interleaved {key, payload} probe records (e.g. bucketed S). */
 int lj_grmi_probe_pairs(const LjGrmi *idx, const uint64_t *s_pairs, int64_t nk, uint64_t *out, int accumulate,
                         void *stream);

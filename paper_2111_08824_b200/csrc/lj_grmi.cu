@@ -14,6 +14,7 @@
 
 #include "lj_common.cuh"
 #include "lj_part.cuh"
+#include "lj_part_est.cuh"
 #include "lj_pipe.cuh"
 #include "lj_probe_count.h"
 
@@ -213,6 +214,21 @@ __global__ void __launch_bounds__(NT) k_grmi_probe(GrmiDev g, In in, i64 nk, u64
     reduce_checksum(cnt, sum, x, steps, out);
 }
 
+// K1 over the overflow area of K4's regions: records [reg[nwin], +reg[2nwin+1])
+__global__ void __launch_bounds__(256) k_grmi_probe_overflow(GrmiDev g, const ulonglong2 *__restrict__ rec,
+                                                            const i64 *reg, int nwin, u64 *out) {
+    const i64 base = reg[nwin], n = reg[2 * nwin + 1];
+    u64 cnt = 0, sum = 0, x = 0, steps = 0;
+    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < n; t += (i64)gridDim.x * blockDim.x) {
+        const ulonglong2 r = __ldcs(rec + base + t);
+        i64 probes;
+        const i64 s = g.search(g.predict_slot(r.x), r.x, probes);
+        steps += (u64)probes;
+        if (s >= 0) g.gather_run(s, r.x, r.y, cnt, sum, x);
+    }
+    reduce_checksum(cnt, sum, x, steps, out);
+}
+
 // ---------------------------------------------- staged probe (K1 over K4)
 //
 // K4 groups S by KEY-RANGE window: window w holds the probes k with
@@ -303,8 +319,8 @@ __device__ __forceinline__ u32 block_exclusive_scan(u32 v, u32 *wsum, u32 *total
 }
 
 __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, const ulonglong2 *__restrict__ rec,
-                                                                   i64 nk, const i64 *__restrict__ wstarts,
-                                                                   int nwin, int shift, unsigned long long *work,
+                                                                   const i64 *__restrict__ reg, int nwin, int shift,
+                                                                   unsigned long long *work,
                                                                    u64 *out, u64 *trace, i64 *dbg) {
     extern __shared__ __align__(16) unsigned char smem[];
     u64 *ck = reinterpret_cast<u64 *>(smem + SO_CK);    // real keys of the staged range (+ sentinel)
@@ -319,8 +335,12 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
     const int tid = threadIdx.x;
     for (int j = tid; j < 2048 / 32; j += STAGE_NT) s_small[j] = 0;
     __syncthreads();
+    // regions: window w's records are [reg[w], rend[w]); reg[nwin] = end of
+    // the regions (the overflow area, probed separately, starts there)
+    const i64 *rend = reg + nwin + 1;
+    const i64 nk = reg[nwin];
     for (int w = tid; w < nwin; w += STAGE_NT)
-        if (wstarts[w + 1] - wstarts[w] < STAGE_MIN) atomicOr(&s_small[w >> 5], 1u << (w & 31));
+        if (rend[w] - reg[w] < STAGE_MIN) atomicOr(&s_small[w >> 5], 1u << (w & 31));
     const int span_max = (1 << shift) + 1;
     u64 cnt = 0, sum = 0, x = 0, steps = 0;
     for (;;) {
@@ -336,11 +356,11 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
         int wlo = 0, whi = nwin;  // first window overlapping p0
         while (whi - wlo > 1) {
             const int mid = (wlo + whi) >> 1;
-            if (wstarts[mid] <= p0) wlo = mid; else whi = mid;
+            if (reg[mid] <= p0) wlo = mid; else whi = mid;
         }
         bool any_small = false;
-        for (int w = wlo; w < nwin && wstarts[w] < p1; ++w) {
-            const i64 a = max(p0, wstarts[w]), e = min(p1, wstarts[w + 1]);
+        for (int w = wlo; w < nwin && reg[w] < p1; ++w) {
+            const i64 a = max(p0, reg[w]), e = min(p1, rend[w]);
             if (e <= a) continue;
             if ((s_small[w >> 5] >> (w & 31)) & 1u) {
                 any_small = true;
@@ -551,9 +571,9 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
                 int lo = wlo, hi = nwin;  // window of probe t
                 while (hi - lo > 1) {
                     const int mid = (lo + hi) >> 1;
-                    if (__ldg(wstarts + mid) <= t) lo = mid; else hi = mid;
+                    if (__ldg(reg + mid) <= t) lo = mid; else hi = mid;
                 }
-                if (!((s_small[lo >> 5] >> (lo & 31)) & 1u)) continue;
+                if (t >= rend[lo] || !((s_small[lo >> 5] >> (lo & 31)) & 1u)) continue;  // a gap / staged window
                 const ulonglong2 r = __ldcs(rec + t);
                 const Acc4 ac = probe_global(g, g.predict_slot(r.x), r.x, r.y);
                 cnt += ac.c;
@@ -698,6 +718,22 @@ static int slot_window_shift(i64 L) {
 
 static size_t al(size_t v) { return (v + 255) & ~(size_t)255; }
 
+// the staged probe handles this index (window fits shared memory, 32-bit
+// relative slot arithmetic); otherwise K4 keeps the exact, gap-free layout
+static bool staged_ok(const LjGrmi *idx) {
+    const int shift = slot_window_shift(idx->L);
+    return shift <= STAGE_MAX_SHIFT && staged_smem_bytes(shift) <= 220 * 1024 && idx->bitmap != nullptr &&
+           idx->L < ((int64_t)1 << 30) && lj_leaf_bucket_bins(idx->L) <= 2 * PART2_NT;
+}
+
+__global__ void k_starts_to_reg(int nwin, i64 *reg) {
+    // reg[0..nwin] already holds the exact bin starts
+    for (int w = blockIdx.x * blockDim.x + threadIdx.x; w <= nwin; w += gridDim.x * blockDim.x) {
+        if (w < nwin) reg[nwin + 1 + w] = reg[w + 1];
+        else reg[2 * nwin + 1] = 0;
+    }
+}
+
 static size_t scan_i64_bytes(i64 n) {
     size_t t = 0;
     cub::DeviceScan::InclusiveScan((void *)nullptr, t, (i64 *)nullptr, (i64 *)nullptr, MaxOpG(), (int64_t)n);
@@ -779,17 +815,26 @@ int lj_grmi_probe(const LjGrmi *idx, const uint64_t *s_keys, const uint64_t *s_p
     return LJ_OK;
 }
 
-int lj_grmi_probe_bucketed(const LjGrmi *idx, const uint64_t *s_pairs, int64_t nk, const int64_t *wstarts,
-                           void *ws, uint64_t *out, int accumulate, void *stream) {
+int lj_grmi_probe_bucketed(const LjGrmi *idx, const uint64_t *s_pairs, const int64_t *reg, void *ws, uint64_t *out,
+                           int accumulate, void *stream) {
     LJ_REQUIRE(idx != nullptr, "null index");
     cudaStream_t st = as_stream(stream);
     if (!accumulate) LJ_CK(cudaMemsetAsync(out, 0, 4 * sizeof(u64), st));
-    if (nk <= 0 || idx->n == 0) return LJ_OK;
+    if (idx->n == 0) return LJ_OK;
     const int shift = slot_window_shift(idx->L);
     const int nwin = lj_leaf_bucket_bins(idx->L);
+    const GrmiDev gd(*idx);
+    // overflow records of the one-pass bucketing: plain K1
+    k_grmi_probe_overflow<<<sm_count() * 8, 256, 0, st>>>(gd, reinterpret_cast<const ulonglong2 *>(s_pairs), reg, nwin,
+                                                          out);
+    LJ_CK_LAUNCH();
     const size_t sm = staged_smem_bytes(shift);
-    if (shift > STAGE_MAX_SHIFT || sm > 220 * 1024 || idx->bitmap == nullptr || idx->L >= ((int64_t)1 << 30)) {
-        // window too large to stage: plain K1 over the grouped records
+    if (!staged_ok(idx)) {
+        // window too large to stage: plain K1 over the records (K4 used the
+        // exact, gap-free layout for such an index)
+        int64_t nk = 0;
+        LJ_CK(cudaMemcpyAsync(&nk, reg + nwin, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        LJ_CK(cudaStreamSynchronize(st));
         return lj_grmi_probe_pairs(idx, s_pairs, nk, out, 1, stream);
     }
     static bool attr = false;
@@ -802,6 +847,11 @@ int lj_grmi_probe_bucketed(const LjGrmi *idx, const uint64_t *s_pairs, int64_t n
     // LJ_STAGE_TRACE=<file>: per-piece timing records (diagnostics only)
     static const char *trace_path = getenv("LJ_STAGE_TRACE");
     u64 *trace = nullptr;
+    int64_t nk = 0;  // diagnostics only: region span for the trace buffers
+    if (trace_path || getenv("LJ_STAGE_DEBUG")) {
+        LJ_CK(cudaMemcpyAsync(&nk, reg + nwin, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        LJ_CK(cudaStreamSynchronize(st));
+    }
     const size_t npieces = (size_t)((nk + STAGE_PIECE - 1) / STAGE_PIECE);
     if (trace_path) LJ_CK(cudaMalloc(&trace, npieces * 8 * sizeof(u64)));
     // LJ_STAGE_DEBUG=<file>: per-probe (lb, re, matches, key) of staged probes (diagnostics only)
@@ -811,8 +861,8 @@ int lj_grmi_probe_bucketed(const LjGrmi *idx, const uint64_t *s_pairs, int64_t n
         LJ_CK(cudaMalloc(&dbg, (size_t)nk * 4 * sizeof(i64)));
         LJ_CK(cudaMemsetAsync(dbg, 0xff, (size_t)nk * 4 * sizeof(i64), st));
     }
-    k_grmi_probe_staged<<<sm_count(), STAGE_NT, sm, st>>>(GrmiDev(*idx), reinterpret_cast<const ulonglong2 *>(s_pairs),
-                                                          nk, wstarts, nwin, shift, work, out, trace, dbg);
+    k_grmi_probe_staged<<<sm_count(), STAGE_NT, sm, st>>>(gd, reinterpret_cast<const ulonglong2 *>(s_pairs), reg,
+                                                          nwin, shift, work, out, trace, dbg);
     LJ_CK_LAUNCH();
     if (dbg) {
         std::vector<i64> h((size_t)nk * 4);
@@ -876,12 +926,20 @@ int lj_leaf_bucket_bins(int64_t L) {
     return (int)((L + ((i64)1 << sh) - 1) >> sh);
 }
 
+int lj_leaf_bucket_regions(int64_t L) { return 2 * lj_leaf_bucket_bins(L) + 2; }
+
+int64_t lj_leaf_bucket_capacity(int64_t nk, int64_t L) {
+    return est_capacity(nk < 0 ? 0 : nk, lj_leaf_bucket_bins(L));
+}
+
 size_t lj_leaf_bucket_workspace_bytes(int64_t nk, int64_t L) {
-    return part_workspace_bytes(nk, lj_leaf_bucket_bins(L)) + al(sizeof(u64) * (size_t)lj_leaf_bucket_bins(L));
+    const int nwin = lj_leaf_bucket_bins(L);
+    const size_t a = part_workspace_bytes(nk, nwin), b = est_workspace_bytes(nwin);
+    return (a > b ? a : b) + al(sizeof(u64) * (size_t)nwin);
 }
 
 int lj_leaf_bucket(const LjGrmi *idx, const uint64_t *keys, const uint64_t *pay, int64_t nk, uint64_t *pairs_out,
-                   int64_t *starts_out, void *ws, size_t ws_bytes, void *stream) {
+                   int64_t *reg_out, void *ws, size_t ws_bytes, void *stream) {
     LJ_REQUIRE(idx && idx->n >= 1 && idx->L >= 1, "index is empty");
     if (ws_bytes < lj_leaf_bucket_workspace_bytes(nk, idx->L)) {
         set_error("lj_leaf_bucket: workspace too small");
@@ -889,7 +947,8 @@ int lj_leaf_bucket(const LjGrmi *idx, const uint64_t *keys, const uint64_t *pay,
     }
     cudaStream_t st = as_stream(stream);
     const int nwin = lj_leaf_bucket_bins(idx->L);
-    const size_t pws = part_workspace_bytes(nk, nwin);
+    const size_t a = part_workspace_bytes(nk, nwin), b = est_workspace_bytes(nwin);
+    const size_t pws = a > b ? a : b;
     SlotBin f;
     f.m = RmiDev(idx->model);
     f.slot_of = SlotMap(idx->n, idx->L);
@@ -899,7 +958,17 @@ int lj_leaf_bucket(const LjGrmi *idx, const uint64_t *keys, const uint64_t *pay,
     k_window_keys<<<(nwin + 255) / 256, 256, 0, st>>>(idx->slots, nwin, f.wshift, (u64 *)f.wk);
     LJ_CK_LAUNCH();
     SoaSrc<SlotBin> src{keys, pay, f};
-    return run_partition(src, nk, nwin, reinterpret_cast<ulonglong2 *>(pairs_out), starts_out, ws, pws, st);
+    static const bool exact_only = getenv("LJ_K4_EXACT") != nullptr;
+    if (staged_ok(idx) && src.aligned16() && !exact_only) {
+        // one pass into estimated-capacity regions (+ overflow), the layout
+        // the staged probe reads
+        return run_partition_est(src, nk, nwin, reinterpret_cast<ulonglong2 *>(pairs_out), reg_out, ws, pws, st);
+    }
+    const int rc = run_partition(src, nk, nwin, reinterpret_cast<ulonglong2 *>(pairs_out), reg_out, ws, pws, st);
+    if (rc) return rc;
+    k_starts_to_reg<<<(nwin + 256) / 256, 256, 0, st>>>(nwin, reg_out);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
 }
 
 }  // extern "C"

@@ -1,0 +1,264 @@
+// lj_part_est.cuh -- ONE-pass partition into estimated-capacity regions.
+//
+// The exact two-pass partition (lj_part.cuh) reads the keys twice and
+// evaluates the bin function in its own latency-bound pass.  When the
+// consumer can live with (a) gaps after each bin and (b) a small unsorted
+// overflow area, one pass suffices: a strided 1/EST_STRIDE sample of the
+// keys estimates every bin's count, each bin gets a region of
+// cap = est * (1 + 1/16) + EST_PAD records (exclusive scan -> rstart), and
+// the pass streams the tuples (TMA ring), evaluates the bin, counting-sorts
+// each tile by bin in shared memory and claims every bin run of the tile
+// with ONE global atomic on the bin's cursor; a run that does not fit goes
+// to the overflow area behind the regions.  Output layout (records):
+//   [rstart[b], rend[b])  bin b, rend[b] = rstart[b] + min(fill, cap)
+//   [rstart[nb], rstart[nb] + overflow)  records of any bin
+// reg[] = {rstart[0..nb], rend[0..nb), overflow count}.
+#pragma once
+
+#include <cub/cub.cuh>
+
+#include "lj_part.cuh"
+
+namespace lj {
+
+constexpr int EST_STRIDE = 16;
+constexpr i64 EST_PAD = 4096;
+constexpr int EST_TILE = 4096;
+constexpr size_t EST_STAGE = (size_t)EST_TILE * 16;
+
+// capacity of the output (records) for n tuples in nb bins: regions + overflow
+inline i64 est_capacity(i64 n, int nb) { return n + n / 16 + (i64)nb * (EST_PAD + EST_STRIDE + 1) + 64 + n; }
+
+template <class Src>
+__global__ void __launch_bounds__(256) k_est_sample(Src f0, i64 n, int nbins, u32 *est) {
+    extern __shared__ __align__(128) unsigned char smem_e[];
+    u64 *tab = reinterpret_cast<u64 *>(smem_e);
+    u32 *h = reinterpret_cast<u32 *>(smem_e + pt_table_bytes(f0.f.smem_words()));
+    f0.f.stage(tab);
+    Src f = f0;
+    f.f = f0.f.at(tab);
+    for (int j = threadIdx.x; j < nbins; j += blockDim.x) h[j] = 0;
+    __syncthreads();
+    const int shift = f.f.shift;
+    for (i64 i = (blockIdx.x * (i64)blockDim.x + threadIdx.x) * EST_STRIDE; i < n;
+         i += (i64)gridDim.x * blockDim.x * EST_STRIDE)
+        atomicAdd(h + (f.code(ld_stream(f.keys + i)) >> shift), 1u);
+    __syncthreads();
+    for (int j = threadIdx.x; j < nbins; j += blockDim.x)
+        if (h[j]) atomicAdd(est + j, h[j]);
+}
+
+__global__ void k_est_caps(const u32 *est, int nbins, i64 *cap) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b <= nbins; b += gridDim.x * blockDim.x) {
+        if (b == nbins) {
+            cap[b] = 0;
+            continue;
+        }
+        const i64 e = (i64)est[b] * EST_STRIDE;
+        cap[b] = e + e / 16 + EST_PAD + EST_STRIDE;
+    }
+}
+
+template <class Src>
+__global__ void __launch_bounds__(PART2_NT) k_bin_scatter_est(Src f0, i64 n, i64 chunk, int nbins, int nst,
+                                                              const i64 *__restrict__ rstart, u32 *gcur,
+                                                              unsigned long long *ovf, ulonglong2 *out) {
+    constexpr int U = EST_TILE / PART2_NT;
+    extern __shared__ __align__(128) unsigned char smem_s[];
+    u64 *tab = reinterpret_cast<u64 *>(smem_s);
+    unsigned char *smem = smem_s + pt_table_bytes(f0.f.smem_words());
+    f0.f.stage(tab);
+    Src f = f0;
+    f.f = f0.f.at(tab);
+    const int nb4 = (nbins + 31) & ~31;
+    u32 *thist = reinterpret_cast<u32 *>(smem);  // this tile's count per bin
+    u32 *tstart = thist + nb4;                   // this tile's run start per bin
+    u32 *gbase = tstart + nb4;                   // claimed position of the run in its bin
+    u16 *perm = reinterpret_cast<u16 *>(gbase + nb4);
+    u16 *tbin = perm + EST_TILE;                 // bin of every tuple of the tile
+    unsigned char *ring = reinterpret_cast<unsigned char *>(perm) + ((EST_TILE * 4 + 127) & ~127);
+    __shared__ __align__(8) uint64_t full[PT_MAXST];
+    __shared__ u32 wsum[PART2_NT / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, shift = f.f.shift;
+    for (int j = tid; j < nbins; j += PART2_NT) thist[j] = 0;
+    const i64 lo = blockIdx.x * chunk, hi = min(lo + chunk, n);
+    const int ntiles = hi > lo ? (int)((hi - lo + EST_TILE - 1) / EST_TILE) : 0;
+    auto issue = [&](int t) {
+        const int s = t % nst;
+        const i64 base = lo + (i64)t * EST_TILE;
+        const unsigned b8 = (unsigned)(min((i64)EST_TILE, hi - base) * 8) & ~15u;
+        unsigned char *st = ring + (size_t)s * EST_STAGE;
+        if (b8) {
+            mbar_arrive_expect_tx(&full[s], 2 * b8);
+            bulk_g2s(st, f.keys + base, b8, &full[s]);
+            bulk_g2s(st + EST_TILE * 8, f.pay + base, b8, &full[s]);
+        } else {
+            mbar_arrive(&full[s]);
+        }
+    };
+    if (tid == 0) {
+        for (int s = 0; s < nst; ++s) mbar_init(&full[s], 1);
+        mbar_init_fence();
+        for (int t = 0; t < min(nst - 1, ntiles); ++t) issue(t);
+    }
+    __syncthreads();
+    for (int t = 0; t < ntiles; ++t) {
+        const int s = t % nst;
+        if (tid == 0 && t + nst - 1 < ntiles) issue(t + nst - 1);  // stage consumed in round t-1
+        mbar_wait(&full[s], (unsigned)(t / nst) & 1u);
+        const i64 base = lo + (i64)t * EST_TILE;
+        const int cnt = (int)min((i64)EST_TILE, hi - base), nb = cnt & ~1;
+        const unsigned char *st = ring + (size_t)s * EST_STAGE;
+        const u64 *ks = reinterpret_cast<const u64 *>(st), *ps = ks + EST_TILE;
+        // (1) bin of every tuple (the model, once) and its rank in the tile's run
+        int bj[U], rj[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = u * PART2_NT + tid;
+            bj[u] = j < cnt ? (int)(f.code(j < nb ? ks[j] : ld_stream(f.keys + base + j)) >> shift) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            rj[u] = bj[u] >= 0 ? (int)atomicAdd(thist + bj[u], 1u) : 0;
+            if (bj[u] >= 0) tbin[u * PART2_NT + tid] = (u16)bj[u];
+        }
+        __syncthreads();
+        // (2) scan of the tile histogram -> run starts; claim every run in
+        // its bin with one global atomic
+        {
+            u32 v0 = 2 * tid < nbins ? thist[2 * tid] : 0, v1 = 2 * tid + 1 < nbins ? thist[2 * tid + 1] : 0;
+            const u32 tot = v0 + v1;
+            u32 inc = tot;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const u32 y = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += y;
+            }
+            if (lane == 31) wsum[warp] = inc;
+            __syncthreads();
+            if (warp == 0) {
+                const u32 w = wsum[lane];
+                u32 wi = w;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const u32 y = __shfl_up_sync(0xffffffffu, wi, d);
+                    if (lane >= d) wi += y;
+                }
+                wsum[lane] = wi - w;
+            }
+            __syncthreads();
+            const u32 r0 = wsum[warp] + inc - tot;
+            if (2 * tid < nbins) {
+                tstart[2 * tid] = r0;
+                if (v0) gbase[2 * tid] = atomicAdd(gcur + 2 * tid, v0);
+                thist[2 * tid] = 0;
+            }
+            if (2 * tid + 1 < nbins) {
+                tstart[2 * tid + 1] = r0 + v0;
+                if (v1) gbase[2 * tid + 1] = atomicAdd(gcur + 2 * tid + 1, v1);
+                thist[2 * tid + 1] = 0;
+            }
+        }
+        __syncthreads();
+        // (3) tile permutation sorted by bin
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (bj[u] >= 0) perm[tstart[bj[u]] + rj[u]] = (u16)(u * PART2_NT + tid);
+        __syncthreads();
+        // (4) write bin runs into their regions (overflow behind the regions)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = u * PART2_NT + tid;
+            if (i < cnt) {
+                const int j = perm[i];
+                const u64 k = j < nb ? ks[j] : ld_stream(f.keys + base + j);
+                const u64 p = j < nb ? ps[j] : ld_stream(f.pay + base + j);
+                const int b = tbin[j];
+                const i64 at = (i64)gbase[b] + (i - (int)tstart[b]);
+                i64 dst = rstart[b] + at;
+                if (dst >= rstart[b + 1]) dst = rstart[nbins] + (i64)atomicAdd(ovf, 1ULL);
+                out[dst] = make_ulonglong2(k, p);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_est_regions(const i64 *rstart, const u32 *gcur, const unsigned long long *ovf, int nbins,
+                              i64 *reg) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b <= nbins; b += gridDim.x * blockDim.x) {
+        reg[b] = rstart[b];
+        if (b < nbins) reg[nbins + 1 + b] = rstart[b] + min((i64)gcur[b], rstart[b + 1] - rstart[b]);
+        else reg[2 * nbins + 1] = (i64)*ovf;
+    }
+}
+
+inline size_t est_workspace_bytes(int nbins) {
+    size_t t = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, t, (i64 *)nullptr, (i64 *)nullptr, (int64_t)(nbins + 1));
+    return part_align(sizeof(u32) * (size_t)nbins) * 2 + part_align(sizeof(i64) * (size_t)(nbins + 1)) * 2 +
+           part_align(sizeof(unsigned long long)) + part_align(t);
+}
+
+// One-pass partition of the n tuples of `f` into out (est_capacity records);
+// reg[2*nbins+2] as described above.
+template <class Src>
+int run_partition_est(const Src &f, i64 n, int nbins, ulonglong2 *out, i64 *reg, void *ws, size_t ws_bytes,
+                      cudaStream_t st) {
+    if (nbins < 1 || nbins > 2 * PART2_NT) {
+        set_error("partition_est: nbins must be in [1, 2048]");
+        return LJ_E_INVALID;
+    }
+    if (ws_bytes < est_workspace_bytes(nbins)) {
+        set_error("partition_est: workspace too small");
+        return LJ_E_WORKSPACE;
+    }
+    char *q = (char *)ws;
+    u32 *est = (u32 *)q;
+    q += part_align(sizeof(u32) * (size_t)nbins);
+    u32 *gcur = (u32 *)q;
+    q += part_align(sizeof(u32) * (size_t)nbins);
+    i64 *cap = (i64 *)q;
+    q += part_align(sizeof(i64) * (size_t)(nbins + 1));
+    i64 *rstart = (i64 *)q;
+    q += part_align(sizeof(i64) * (size_t)(nbins + 1));
+    unsigned long long *ovf = (unsigned long long *)q;
+    q += part_align(sizeof(unsigned long long));
+    LJ_CK(cudaMemsetAsync(est, 0, sizeof(u32) * (size_t)nbins, st));
+    LJ_CK(cudaMemsetAsync(gcur, 0, sizeof(u32) * (size_t)nbins, st));
+    LJ_CK(cudaMemsetAsync(ovf, 0, sizeof(unsigned long long), st));
+    const size_t tb = pt_table_bytes(f.f.smem_words());
+    static bool attr = false;
+    if (!attr) {
+        LJ_CK(cudaFuncSetAttribute(k_bin_scatter_est<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_SMEM_MAX));
+        attr = true;
+    }
+    if (n > 0) {
+        k_est_sample<Src><<<grid_for((n + EST_STRIDE - 1) / EST_STRIDE, 256, 4), 256, tb + sizeof(u32) * nbins, st>>>(
+            f, n, nbins, est);
+        LJ_CK_LAUNCH();
+    }
+    k_est_caps<<<(nbins + 256) / 256, 256, 0, st>>>(est, nbins, cap);
+    LJ_CK_LAUNCH();
+    size_t t = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, t, cap, rstart, (int64_t)(nbins + 1));
+    LJ_CK(cub::DeviceScan::ExclusiveSum(q, t, cap, rstart, (int64_t)(nbins + 1), st));
+    if (n > 0) {
+        const PartPlan p = part_plan(n, nbins);
+        const size_t nb4 = (size_t)((nbins + 31) & ~31);
+        const size_t fix = tb + 3 * nb4 * sizeof(u32) + (((size_t)EST_TILE * 4 + 127) & ~(size_t)127);
+        const int nst = (int)min((size_t)PT_MAXST, (PT_SMEM_MAX - fix) / EST_STAGE);
+        if (nst < 2) {
+            set_error("partition_est: shared memory too small for the ring");
+            return LJ_E_INVALID;
+        }
+        k_bin_scatter_est<Src><<<p.blocks, PART2_NT, fix + nst * EST_STAGE, st>>>(f, n, p.chunk, nbins, nst, rstart,
+                                                                                   gcur, ovf, out);
+        LJ_CK_LAUNCH();
+    }
+    k_est_regions<<<(nbins + 256) / 256, 256, 0, st>>>(rstart, gcur, ovf, nbins, reg);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+}  // namespace lj

@@ -103,8 +103,8 @@ class GappedRmiIndex:
         lib = _lib.lib()
         dev = device or self.slots.device
         L = self.slot_count
-        return {"pairs": torch.empty(2 * max(n, 1), dtype=torch.int64, device=dev),
-                "starts": torch.empty(lib.lj_leaf_bucket_bins(L) + 1, dtype=torch.int64, device=dev),
+        return {"pairs": torch.empty(2 * max(lib.lj_leaf_bucket_capacity(n, L), 1), dtype=torch.int64, device=dev),
+                "regions": torch.empty(lib.lj_leaf_bucket_regions(L), dtype=torch.int64, device=dev),
                 "ws": _lib.workspace(lib.lj_leaf_bucket_workspace_bytes(n, L), dev),
                 "work": torch.zeros(1, dtype=torch.int64, device=dev)}
 
@@ -134,14 +134,14 @@ class GappedRmiIndex:
         g = self.c_struct()
         ws = scratch["ws"]
         _lib.check(lib.lj_leaf_bucket(ctypes.byref(g), _lib.ptr(s_keys), _lib.ptr(s_payloads), s_keys.numel(),
-                                      _lib.ptr(scratch["pairs"]), _lib.ptr(scratch["starts"]), _lib.ptr(ws),
+                                      _lib.ptr(scratch["pairs"]), _lib.ptr(scratch["regions"]), _lib.ptr(ws),
                                       ws.numel(), _lib.stream_ptr(stream)), "leaf_bucket")
 
     def probe_records(self, n: int, scratch: dict, out: torch.Tensor, accumulate: bool = False, stream=None) -> None:
         """Staged K1 over the n records bucket_records left in scratch."""
         g = self.c_struct()
-        _lib.check(_lib.lib().lj_grmi_probe_bucketed(ctypes.byref(g), _lib.ptr(scratch["pairs"]), n,
-                                                     _lib.ptr(scratch["starts"]), _lib.ptr(scratch["work"]),
+        _lib.check(_lib.lib().lj_grmi_probe_bucketed(ctypes.byref(g), _lib.ptr(scratch["pairs"]),
+                                                     _lib.ptr(scratch["regions"]), _lib.ptr(scratch["work"]),
                                                      _lib.ptr(out), int(bool(accumulate)), _lib.stream_ptr(stream)),
                    "grmi_probe_bucketed")
         return out
