@@ -74,13 +74,15 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_est(Src f0, i64 n, i64
     u32 *thist = reinterpret_cast<u32 *>(smem);  // this tile's count per bin
     u32 *tstart = thist + nb4;                   // this tile's run start per bin
     u32 *gbase = tstart + nb4;                   // claimed position of the run in its bin
-    u16 *perm = reinterpret_cast<u16 *>(gbase + nb4);
+    i64 *srst = reinterpret_cast<i64 *>(gbase + nb4);  // region starts [nbins + 1]
+    u16 *perm = reinterpret_cast<u16 *>(srst + nb4 + 32);
     u16 *tbin = perm + EST_TILE;                 // bin of every tuple of the tile
     unsigned char *ring = reinterpret_cast<unsigned char *>(perm) + ((EST_TILE * 4 + 127) & ~127);
     __shared__ __align__(8) uint64_t full[PT_MAXST];
     __shared__ u32 wsum[PART2_NT / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, shift = f.f.shift;
     for (int j = tid; j < nbins; j += PART2_NT) thist[j] = 0;
+    for (int j = tid; j <= nbins; j += PART2_NT) srst[j] = rstart[j];
     const i64 lo = blockIdx.x * chunk, hi = min(lo + chunk, n);
     const int ntiles = hi > lo ? (int)((hi - lo + EST_TILE - 1) / EST_TILE) : 0;
     auto issue = [&](int t) {
@@ -174,9 +176,8 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_est(Src f0, i64 n, i64
                 const u64 k = j < nb ? ks[j] : ld_stream(f.keys + base + j);
                 const u64 p = j < nb ? ps[j] : ld_stream(f.pay + base + j);
                 const int b = tbin[j];
-                const i64 at = (i64)gbase[b] + (i - (int)tstart[b]);
-                i64 dst = rstart[b] + at;
-                if (dst >= rstart[b + 1]) dst = rstart[nbins] + (i64)atomicAdd(ovf, 1ULL);
+                i64 dst = srst[b] + (i64)gbase[b] + (i - (int)tstart[b]);
+                if (dst >= srst[b + 1]) dst = srst[nbins] + (i64)atomicAdd(ovf, 1ULL);
                 out[dst] = make_ulonglong2(k, p);
             }
         }
@@ -246,7 +247,8 @@ int run_partition_est(const Src &f, i64 n, int nbins, ulonglong2 *out, i64 *reg,
     if (n > 0) {
         const PartPlan p = part_plan(n, nbins);
         const size_t nb4 = (size_t)((nbins + 31) & ~31);
-        const size_t fix = tb + 3 * nb4 * sizeof(u32) + (((size_t)EST_TILE * 4 + 127) & ~(size_t)127);
+        const size_t fix = tb + 3 * nb4 * sizeof(u32) + (nb4 + 32) * sizeof(i64) +
+                           (((size_t)EST_TILE * 4 + 127) & ~(size_t)127);
         const int nst = (int)min((size_t)PT_MAXST, (PT_SMEM_MAX - fix) / EST_STAGE);
         if (nst < 2) {
             set_error("partition_est: shared memory too small for the ring");
