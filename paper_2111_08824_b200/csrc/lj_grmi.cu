@@ -444,13 +444,14 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
             }
             const int lim = (int)(g.L - slo), zero = -(int)slo;  // L < 2^30 on this path
             const bool hi_open = shi < g.L;
+            const int m1 = (int)g.model.m - 1, Lm1 = (int)g.L - 1;
             const ulonglong2 *wrec = rec + a;
             const u64 *wpay = g.slots + 2 * slo + 1;  // payload of staged slot i: wpay[2 * i]
             const int ne = (int)(e - a);
             // ---- probes: STAGE_U per thread per step, phase by phase
             for (int t0 = tid; t0 < ne; t0 += STAGE_NT * STAGE_U) {
                 u64 k[STAGE_U], ps[STAGE_U];
-                int start[STAGE_U], lo[STAGE_U], len[STAGE_U];
+                int start[STAGE_U], lo[STAGE_U];
 #pragma unroll
                 for (int u = 0; u < STAGE_U; ++u) {
                     const int t = t0 + u * STAGE_NT;
@@ -461,28 +462,37 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
 #pragma unroll
                 for (int u = 0; u < STAGE_U; ++u) {
                     // models.py:112-124 + gapped.py:258-261, the leaf from smem
+                    // the same operations as RmiDev::pos + SlotMap in 32-bit
+                    // integers (n <= L < 2^30 on this path; saturating
+                    // conversions clamp exactly like the 64-bit forms)
                     const double xf = u64_to_f64(k[u]);
-                    const int l = (int)g.model.route(xf) - lc_lo;
-                    const LjLeaf lf = ((unsigned)l < (unsigned)lc_n) ? lc[l] : load_leaf(g.model.leaves, l + lc_lo);
-                    start[u] = (int)(g.slot_of(rmi_leaf_pos(lf, xf)) - slo);
+                    const double rr = __dadd_rn(__dmul_rn(g.model.rs, xf), g.model.ri);
+                    const int lr = min(max(__double2int_rd(rr), 0), m1);
+                    const int l = lr - lc_lo;
+                    const LjLeaf lf = ((unsigned)l < (unsigned)lc_n) ? lc[l] : load_leaf(g.model.leaves, lr);
+                    const double raw = __dadd_rn(__dmul_rn(lf.slope, xf), lf.icpt);
+                    const int clo = (int)lf.clamp_lo, chi = (int)lf.clamp_hi;
+                    const int pos = (raw >= -9223372036854775808.0 && raw < 9223372036854775808.0)
+                                        ? min(max(__double2int_rn(raw), clo), chi)
+                                        : clo;
+                    const double z = __dmul_rn((double)pos, g.slot_of.c);
+                    const double fr = __dadd_rn(z, -floor(z));
+                    const int slot = fabs(__dadd_rn(fr, -0.5)) > g.slot_of.g ? min(max(__double2int_rn(z), 0), Lm1)
+                                                                            : (int)grmi_slot_of_pos(pos, g.n, g.L);
+                    start[u] = slot - (int)slo;
                 }
 #pragma unroll
-                for (int u = 0; u < STAGE_U; ++u) {  // table pair (branch-free)
-                    const bool below = k[u] < kmin, above = k[u] > kmax;
+                for (int u = 0; u < STAGE_U; ++u) {  // first entry of k's table bucket
                     const u64 d = k[u] - kmin;
-                    const int p = (int)((d < krange ? d : krange) >> sh);
-                    const int t_lo = T[p], t_hi = T[p + 1];
-                    lo[u] = below ? 0 : (above ? n_c : t_lo);
-                    len[u] = (below || above) ? 0 : t_hi - t_lo;
+                    lo[u] = k[u] < kmin ? 0 : T[(int)((d < krange ? d : krange) >> sh)];
                 }
-                for (int it = 0; it < iters; ++it) {
+                // lower bound by binary lifting: the answer is at most
+                // s_max < 2^iters entries past the bucket start, and every
+                // entry past the bucket (or the sentinel at n_c) is >= k
+                for (int st = iters > 0 ? 1 << (iters - 1) : 0; st > 0; st >>= 1) {
 #pragma unroll
-                    for (int u = 0; u < STAGE_U; ++u) {  // lower bound, no branches
-                        const int half = len[u] >> 1;
-                        const bool go = len[u] > 0 && ck[lo[u] + half] < k[u];
-                        lo[u] = go ? lo[u] + half + 1 : lo[u];
-                        len[u] = go ? len[u] - half - 1 : half;
-                    }
+                    for (int u = 0; u < STAGE_U; ++u)
+                        if (ck[min(lo[u] + st - 1, n_c)] < k[u]) lo[u] += st;
                 }
                 // first match of every probe and its payload, all in flight at once
                 bool m0[STAGE_U];
