@@ -458,6 +458,9 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
                     const ulonglong2 r = t < ne ? __ldcs(wrec + t) : make_ulonglong2(kmin, 0);
                     k[u] = r.x;
                     ps[u] = r.y;
+                    // the records of two steps ahead start their way into L2
+                    const int tp = t + 2 * STAGE_NT * STAGE_U;
+                    if (tp < ne) asm volatile("prefetch.global.L2 [%0];" ::"l"(wrec + tp));
                 }
 #pragma unroll
                 for (int u = 0; u < STAGE_U; ++u) {
