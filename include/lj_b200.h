@@ -147,6 +147,14 @@ int lj_rmi_fit(const uint64_t *sorted_keys, int64_t n, int64_t m, double *root, 
 /* models.py:126-135 predict_many; any output may be NULL. */
 int lj_rmi_predict(const LjRmi *model, const uint64_t *keys, int64_t nk, int64_t *pos,
                    int64_t *lo, int64_t *hi, int64_t *leaf, void *stream);
+/* rmi-inlj (baselines.py:96-157): INLJ of S against the
+ * SORTED R (r_keys/r_pay, nr) indexed by `model` fitted on it: predict
+ * [lo, hi] (models.py:126-135), bounded lower bound counting the reference's
+ * bisection steps + one verification compare, whole equal run on a hit.
+ * out[4] = {count, sum, xor, search_steps}. */
+int lj_rmi_probe(const LjRmi *model, const uint64_t *r_keys, const uint64_t *r_pay, int64_t nr,
+                 const uint64_t *s_keys, const uint64_t *s_pay, int64_t ns, uint64_t *out, int accumulate,
+                 void *stream);
 /* models.py:285-299 partition_index for an RMI. */
 int lj_rmi_partition_index(const LjRmi *model, const uint64_t *keys, int64_t nk, int64_t P,
                            int64_t *out, void *stream);

@@ -290,6 +290,19 @@ def grmi_join(idx: Grmi, s_keys, s_payloads, threads: int = 0):
     return tuple(int(v) for v in out)
 
 
+def rmi_inlj(model: Rmi, sorted_keys, sorted_payloads, s_keys, s_payloads, threads: int = 0):
+    """baselines.py:96-157 over sorted R -> (count, sum, xor, search_steps)."""
+    rk = _u64(sorted_keys)
+    rp = _u64(sorted_payloads)
+    sk = _u64(s_keys)
+    sp = _u64(s_payloads)
+    out = np.zeros(4, np.uint64)
+    c = model._c()
+    lib().orc_rmi_inlj(ctypes.byref(c), _p(rk, _u64p), _p(rp, _u64p), _i64(rk.size), _p(sk, _u64p),
+                       _p(sp, _u64p), _i64(sk.size), ctypes.c_int(threads), _p(out, _u64p))
+    return tuple(int(v) for v in out)
+
+
 # ------------------------------------------------------------ RadixSpline
 
 

@@ -224,7 +224,7 @@ def make_algos(lj):
         for n, dup in ((1000, 0.0), (4000, 0.25)):
             r, s, _ = make_join_inputs(kind, n, 42, dup_frac=dup)
             truth = checksum(lj.nlj_oracle(r, s))
-            for algo in ("grmi-inlj", "buffered-grmi-inlj", "spline-hash-inlj", "lsj"):
+            for algo in ("grmi-inlj", "buffered-grmi-inlj", "spline-hash-inlj", "lsj", "rmi-inlj"):
                 for workers in (1, 4):
                     opts = dict(DEFAULT_OPTS)
                     res, br, _ = ALGORITHMS[algo](r, s, workers, opts)
@@ -235,6 +235,11 @@ def make_algos(lj):
                         out[key] = {"r_keys": r.keys, "r_payloads": r.payloads, "s_keys": s.keys,
                                     "s_payloads": s.payloads, "checksum": truth}
                     ctr = br.counters()
+                    if algo == "rmi-inlj" and "rmi_root" not in out[key]:
+                        # the model _run_rmi_inlj fits (bench.py:184-192), for exact step parity
+                        srt = r.sorted_by_key()
+                        m = lj.RecursiveModelIndex(fanout=opts["rmi_fanout"]).fit(srt.keys)
+                        out[key].update(rmi_params(m, "rmi_"))
                     out[key][f"{algo}_w{workers}_counters"] = np.array(
                         [ctr["search_steps"], ctr["predictions"], ctr["leaf_switches"],
                          ctr["comparator_count"], ctr["partitions_sorted"]], np.int64)
@@ -273,6 +278,9 @@ def save(name, obj):
 
 def main():
     lj = _import_reference()
+    if len(sys.argv) > 1 and sys.argv[1] == "algos":
+        save("algos.npz", make_algos(lj))
+        return
     sets = key_sets(lj)
     save("util.npz", make_util(lj))
     save("models.npz", make_models(lj, sets))

@@ -79,6 +79,7 @@ SIGNATURES = {
     "lj_rmi_fit": (_int, [_P, _i64, _i64, _P, _P, _P, _P, _size_t, _P]),
     "lj_rmi_predict": (_int, [ctypes.POINTER(LjRmi), _P, _i64, _P, _P, _P, _P, _P]),
     "lj_rmi_partition_index": (_int, [ctypes.POINTER(LjRmi), _P, _i64, _i64, _P, _P]),
+    "lj_rmi_probe": (_int, [ctypes.POINTER(LjRmi), _P, _P, _i64, _P, _P, _i64, _P, _int, _P]),
     "lj_grmi_build_workspace_bytes": (_size_t, [_i64, _i64]),
     "lj_grmi_build": (_int, [ctypes.POINTER(LjRmi), _P, _P, _i64, _i64, _P, _P, _P, _P, _size_t, _P]),
     "lj_grmi_predict_slots": (_int, [ctypes.POINTER(LjGrmi), _P, _i64, _P, _P]),

@@ -324,6 +324,38 @@ __global__ void k_leaf_combine(const i64 *starts, i64 n, i64 m, const i64 *pbase
     }
 }
 
+// K12 (rmi-inlj): baselines.py:96-157 over the SORTED R.
+// predict_many (models.py:126-135) gives [lo, hi]; the lower bound in
+// [lo, hi+1) costs one step per bisection plus one verification compare
+// (_bounded_binary_search); a hit emits the whole equal run.  One lane per
+// probe, checksum + steps reduced on device.
+__global__ void k_rmi_probe(RmiDev r, const u64 *__restrict__ rk, const u64 *__restrict__ rp, i64 n,
+                            const u64 *__restrict__ sk, const u64 *__restrict__ sp, i64 ns, u64 *out) {
+    u64 cnt = 0, sum = 0, x = 0, steps = 0;
+    const i64 last = r.n - 1;
+    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < ns; t += (i64)gridDim.x * blockDim.x) {
+        const u64 key = ld_stream(sk + t), ps = ld_stream(sp + t);
+        const double xf = u64_to_f64(key);
+        const i64 l = r.route(xf);
+        const i64 p = rmi_leaf_pos(load_leaf(r.leaves, l), xf);
+        i64 left = clip_i64(p + __ldg(r.err + 2 * l), 0, last);
+        i64 right = clip_i64(p + __ldg(r.err + 2 * l + 1), 0, last) + 1;
+        while (left < right) {
+            const i64 mid = (left + right) >> 1;
+            ++steps;
+            if (ldg(rk + mid) < key) left = mid + 1; else right = mid;
+        }
+        ++steps;
+        for (i64 i = left; i < n && ldg(rk + i) == key; ++i) {
+            const u64 v = ldg(rp + i) + ps;
+            ++cnt;
+            sum += v;
+            x ^= v;
+        }
+    }
+    reduce_checksum(cnt, sum, x, steps, out);
+}
+
 static size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 
 static size_t rank_scan_temp_bytes(i64 n) {
@@ -486,6 +518,18 @@ int lj_rmi_predict(const LjRmi *model, const uint64_t *keys, int64_t nk, int64_t
     if (nk <= 0) return LJ_OK;
     k_rmi_predict<<<grid_for(nk, 256, 8), 256, 0, as_stream(stream)>>>(RmiDev(*model), keys, nk, pos,
                                                                         lo, hi, leaf);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+int lj_rmi_probe(const LjRmi *model, const uint64_t *r_keys, const uint64_t *r_pay, int64_t nr,
+                 const uint64_t *s_keys, const uint64_t *s_pay, int64_t ns, uint64_t *out, int accumulate,
+                 void *stream) {
+    LJ_REQUIRE(model && model->m >= 1 && model->n == nr, "model must be fitted on the nr sorted R keys");
+    cudaStream_t st = as_stream(stream);
+    if (!accumulate) LJ_CK(cudaMemsetAsync(out, 0, 4 * sizeof(u64), st));
+    if (ns <= 0 || nr <= 0) return LJ_OK;
+    k_rmi_probe<<<grid_for(ns, 256, 8), 256, 0, st>>>(RmiDev(*model), r_keys, r_pay, nr, s_keys, s_pay, ns, out);
     LJ_CK_LAUNCH();
     return LJ_OK;
 }

@@ -178,6 +178,49 @@ def _run_spline_hash_inlj(r, s, workers, opts):
     return result, br, runtime
 
 
+def rmi_inlj(r_keys: torch.Tensor, r_payloads: torch.Tensor, model, s: Relation, workers: int = 1):
+    """baselines.py:96-157: INLJ over the SORTED R (keys, payloads) indexed by
+    a plain RMI fitted on it -> device int64[4] {count, sum, xor, steps}."""
+    import ctypes
+
+    from . import _lib
+
+    out = torch.zeros(4, dtype=torch.int64, device=s.keys.device)
+    c = model.c_struct()
+    lib = _lib.lib()
+    for lo, hi in _chunks(len(s), workers):
+        _lib.check(lib.lj_rmi_probe(ctypes.byref(c), _lib.ptr(r_keys), _lib.ptr(r_payloads), r_keys.numel(),
+                                    _lib.ptr(s.keys[lo:hi]), _lib.ptr(s.payloads[lo:hi]), hi - lo, _lib.ptr(out), 1,
+                                    _lib.stream_ptr()), "rmi_probe")
+    return out
+
+
+def _run_rmi_inlj(r, s, workers, opts):
+    """bench.py:184-192: sorted R + plain RMI fit untimed, probe timed (K12)."""
+    from .models import RecursiveModelIndex
+    from .util import sort_pairs
+
+    if len(r) == 0:
+        return _empty()
+    rk, rp = sort_pairs(r.keys, r.payloads)
+    model = RecursiveModelIndex(opts["rmi_fanout"]).fit(rk)
+    br = PhaseBreakdown()
+    words, runtime = _timed(lambda: rmi_inlj(rk, rp, model, s, workers))
+    w = words.cpu().tolist()
+    result = JoinResult(checksum=(int(w[0]), int(w[1]) & (2**64 - 1), int(w[2]) & (2**64 - 1)))
+    if opts.get("materialize"):  # pairs on device: every S key's equal run in sorted R
+        left = torch.searchsorted(rk, s.keys, side="left")
+        counts = torch.searchsorted(rk, s.keys, side="right") - left
+        src = torch.repeat_interleave(torch.arange(len(s), device=rk.device), counts)
+        first = torch.repeat_interleave(left - (torch.cumsum(counts, 0) - counts), counts)
+        slots = first + torch.arange(src.numel(), device=rk.device)
+        result = JoinResult(rp[slots], s.payloads[src])
+    br.lookup_stats.search_steps = int(w[3])
+    br.lookup_stats.predictions = len(s)
+    br.srch = runtime
+    return result, br, runtime
+
+
 def _run_lsj(r, s, workers, opts):
     """bench.py:224-234: LSJ timed end to end."""
     from .lsj import LsjConfig, lsj_join
@@ -196,6 +239,7 @@ ALGORITHMS = {
     "grmi-inlj": _run_grmi_inlj,
     "spline-hash-inlj": _run_spline_hash_inlj,
     "lsj": _run_lsj,
+    "rmi-inlj": _run_rmi_inlj,
 }
 
 

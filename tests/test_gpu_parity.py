@@ -151,7 +151,7 @@ def test_spline_hash_build_and_probe_bitwise(golden, lj):
         assert np.array_equal(own.model.spline_keys, d["sp_keys"]), case
 
 
-@pytest.mark.parametrize("algo", ["grmi-inlj", "buffered-grmi-inlj", "spline-hash-inlj", "lsj"])
+@pytest.mark.parametrize("algo", ["grmi-inlj", "buffered-grmi-inlj", "spline-hash-inlj", "lsj", "rmi-inlj"])
 @pytest.mark.parametrize("workers", [1, 4])
 def test_algorithms_registry_matches_reference(golden, lj, algo, workers):
     """L2 through the drop-in boundary (bench.py:277-289): every c01-style
@@ -404,3 +404,21 @@ def test_partition_fallback_on_unaligned_columns(lj):
     assert s.keys.data_ptr() % 16 == 8
     res, _ = lj.lsj_join(r, s)
     assert res.checksum == oracle.smj_checksum(*r.numpy(), *s.numpy())
+
+
+def test_rmi_inlj_bitwise_with_reference_model(golden, lj):
+    """K12 rmi-inlj (baselines.py:96-157) over the reference's sorted R and
+    fitted model: the reference's checksum and search_steps."""
+    import torch
+
+    from paper_2111_08824_b200.joins import rmi_inlj
+
+    for case, d in golden("algos").items():
+        order = np.argsort(d["r_keys"], kind="stable")
+        rk = torch.from_numpy(d["r_keys"][order].view(np.int64)).cuda()
+        rp = torch.from_numpy(d["r_payloads"][order].view(np.int64)).cuda()
+        s = lj.Relation(d["s_keys"], d["s_payloads"])
+        for w in (1, 4):
+            words = rmi_inlj(rk, rp, ref_rmi(lj, d, "rmi_"), s, w).cpu().tolist()
+            assert (words[0], words[1] & MASK, words[2] & MASK) == tuple(int(v) for v in d["checksum"]), case
+            assert words[3] == int(d[f"rmi-inlj_w{w}_counters"][0]), (case, w)

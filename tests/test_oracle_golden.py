@@ -168,3 +168,17 @@ def test_ground_truth_joins_agree(golden):
         args = (d["r_keys"], d["r_payloads"], d["s_keys"], d["s_payloads"])
         assert oracle.smj_checksum(*args) == want, case
         assert oracle.nlj_checksum(*args) == want, case
+
+
+def test_rmi_inlj_matches_reference(golden):
+    """baselines.py:96-157 (rmi-inlj): the oracle over the
+    reference's sorted R and its own fitted model gives the reference's
+    checksum and search_steps (the counter is chunking-independent)."""
+    for case, d in golden("algos").items():
+        m = rmi_from_fixture(d, "rmi_")
+        order = np.argsort(d["r_keys"], kind="stable")
+        rk, rp = d["r_keys"][order], d["r_payloads"][order]
+        got = oracle.rmi_inlj(m, rk, rp, d["s_keys"], d["s_payloads"])
+        assert got[:3] == tuple(int(v) for v in d["checksum"]), case
+        for w in (1, 4):
+            assert got[3] == int(d[f"rmi-inlj_w{w}_counters"][0]), (case, w)
