@@ -64,3 +64,44 @@ def make_relation(keys, seed: int) -> Relation:
     """Attach the reference's deterministic nonzero payloads to ``keys``."""
     k = as_key_tensor(keys)
     return Relation(k, fill_payloads(k.numel(), seed, device=k.device), validate=False)
+
+
+# ------------------------------------------------- key files (data.py:195-216)
+
+
+class CorruptKeyFileError(ValueError):
+    """data.py: a key file whose size disagrees with its count header."""
+
+
+def write_keys_file(path, keys) -> None:
+    """data.py:195-202: 8-byte LE count header plus LE uint64 keys."""
+    k = to_numpy_u64(keys) if isinstance(keys, torch.Tensor) else np.ascontiguousarray(np.asarray(keys, np.uint64))
+    with open(path, "wb") as fh:
+        np.array([k.size], dtype="<u8").tofile(fh)
+        k.astype("<u8").tofile(fh)
+
+
+def load_keys_file(path, device=None) -> torch.Tensor:
+    """data.py:205-216 loaded straight to the device: the file is read into
+    pinned host memory and copied with one H2D transfer.  Returns the keys as
+    a CUDA int64 tensor (uint64 bits), bit-exact."""
+    import os
+
+    size = os.path.getsize(path)
+    if size < 8:
+        raise CorruptKeyFileError(f"{path}: missing count header")
+    with open(path, "rb") as fh:
+        count = int(np.fromfile(fh, dtype="<u8", count=1)[0])
+        if size != 8 + 8 * count:
+            raise CorruptKeyFileError(f"{path}: header says {count} keys but file holds {(size - 8) // 8}")
+        host = torch.empty(count, dtype=torch.int64, pin_memory=True)
+        if count:
+            fh.readinto(memoryview(host.numpy()).cast("B"))
+    return host.to(device or "cuda", non_blocking=False)
+
+
+def relation_from_keys_file(path, seed: int, device=None) -> Relation:
+    """A relation over a key file with the positional payload rule
+    (data.py:181-192), built on the device."""
+    keys = load_keys_file(path, device)
+    return Relation(keys, fill_payloads(keys.numel(), seed, device=keys.device))

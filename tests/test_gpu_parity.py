@@ -422,3 +422,29 @@ def test_rmi_inlj_bitwise_with_reference_model(golden, lj):
             words = rmi_inlj(rk, rp, ref_rmi(lj, d, "rmi_"), s, w).cpu().tolist()
             assert (words[0], words[1] & MASK, words[2] & MASK) == tuple(int(v) for v in d["checksum"]), case
             assert words[3] == int(d[f"rmi-inlj_w{w}_counters"][0]), (case, w)
+
+
+def test_key_file_roundtrip_to_device_and_canonical(lj, tmp_path):
+    """data.py:195-216 key files loaded straight to the
+    device bit-exactly (corrupt headers rejected), and JoinResult.canonical
+    computed on the device equals the reference's np.lexsort order."""
+    rng = np.random.default_rng(9)
+    keys = np.concatenate([rng.integers(0, 2**63, 5000, dtype=np.uint64), np.array([0, 2**63 - 1], np.uint64)])
+    path = tmp_path / "k.bin"
+    lj.write_keys_file(path, keys)
+    dev = lj.load_keys_file(path)
+    assert dev.is_cuda and np.array_equal(_np(dev), keys)
+    bad = tmp_path / "bad.bin"
+    bad.write_bytes(path.read_bytes()[:-8])
+    with pytest.raises(lj.CorruptKeyFileError):
+        lj.load_keys_file(bad)
+    r = lj.relation_from_keys_file(path, 5)
+    assert np.array_equal(r.numpy()[1], lj.make_relation(keys, 5).numpy()[1])
+    s = lj.make_relation(np.concatenate([keys[:300], keys[:100]]), 6)
+    res, _, _ = lj.ALGORITHMS["grmi-inlj"](r, s, 1, dict(lj.DEFAULT_OPTS, materialize=True))
+    pr, ps = res.payloads_r, res.payloads_s
+    order = np.lexsort((ps, pr))
+    want = np.column_stack((pr[order], ps[order]))
+    assert np.array_equal(res.canonical(), want)
+    dr, ds = res.canonical_device()
+    assert np.array_equal(np.column_stack((_np(dr), _np(ds))), want)
