@@ -223,28 +223,45 @@ __global__ void k_sample_bins(LsjDev md, u32 *sbin) {
         sbin[i] = (u32)md.bin(md.sample[i]);
 }
 
-__global__ void k_split_points(LsjDev md, const u32 *sbin, const i64 *starts, const i64 *fbase, int nb, u64 *spv) {
+// sample index range [sr[b], se[b]) of every bin (bins are monotone over the
+// sorted sample)
+__global__ void k_split_ranges(LsjDev md, const u32 *sbin, int nb, i64 *sr, i64 *se) {
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
-        const i64 F = split_count(starts[b + 1] - starts[b]);
-        if (F < 2) continue;
-        // sample index range of bin b (bins are monotone over the sorted sample)
         i64 lo = 0, hi = md.nsample;
         while (lo < hi) {
             i64 mid = (lo + hi) >> 1;
             if ((sbin ? (int)sbin[mid] : md.bin(md.sample[mid])) < b) lo = mid + 1; else hi = mid;
         }
-        const i64 sb = lo;
+        sr[b] = lo;
         hi = md.nsample;
         while (lo < hi) {
             i64 mid = (lo + hi) >> 1;
             if ((sbin ? (int)sbin[mid] : md.bin(md.sample[mid])) <= b) lo = mid + 1; else hi = mid;
         }
-        const i64 se = lo, ns = se - sb;
-        // split KEYS at sample quantiles (distinct keys always separate, even
-        // where the model's placement y is flat); too few sample keys: the
-        // quantiles repeat (empty slices), none: one slice for the bucket
-        for (i64 j = 1; j < F; ++j)
-            spv[fbase[b] + j - 1] = ns > 0 ? md.sample[sb + (j * ns) / F < se ? sb + (j * ns) / F : se - 1] : ~0ULL;
+        se[b] = lo;
+    }
+}
+
+// split KEYS at sample quantiles, one thread per slot g of the slot space
+// (distinct keys always separate, even where the model's placement y is
+// flat); too few sample keys: the quantiles repeat (empty slices), none:
+// one slice for the bucket.  Bucket b's values: spv[fbase[b] + j - 1],
+// j in [1, F_b).
+__global__ void k_split_points(LsjDev md, const i64 *starts, const i64 *fbase, int nb, const i64 *sr,
+                               const i64 *se, u64 *spv) {
+    const i64 G = fbase[nb];
+    for (i64 g = blockIdx.x * (i64)blockDim.x + threadIdx.x; g < G; g += (i64)gridDim.x * blockDim.x) {
+        int lo = 0, hi = nb;  // bucket of slot g: last b with fbase[b] <= g
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (fbase[mid] <= g) lo = mid; else hi = mid;
+        }
+        const int b = lo;
+        const i64 F = split_count(starts[b + 1] - starts[b]), j = g - fbase[b] + 1;
+        if (F < 2 || j >= F) continue;
+        const i64 sb = sr[b], ns = se[b] - sb;
+        const i64 q = sb + (j * ns) / F;
+        spv[g] = ns > 0 ? md.sample[q < se[b] ? q : se[b] - 1] : ~0ULL;
     }
 }
 
@@ -1025,7 +1042,10 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
         // they fit, else evaluated inside the searches
         u32 *sbin = dev.nsample <= 2 * n ? reinterpret_cast<u32 *>(k1) : nullptr;
         if (sbin) k_sample_bins<<<grid_for(dev.nsample, 256, 8), 256, 0, st>>>(dev, sbin);
-        k_split_points<<<(int)((nb + 63) / 64), 64, 0, st>>>(dev, sbin, starts, fbase, (int)nb, spv);
+        // chunks / matc are free until k_chunk_plan: the bins' sample ranges
+        k_split_ranges<<<(int)((nb + 63) / 64), 64, 0, st>>>(dev, sbin, (int)nb, chunks, matc);
+        k_split_points<<<grid_for(max_subs(n, nb), 256, 8), 256, 0, st>>>(dev, starts, fbase, (int)nb, chunks, matc,
+                                                                         spv);
         LJ_CK_LAUNCH();
     }
     k_chunk_plan<<<(int)((nb + 256) / 256), 256, 0, st>>>(starts, fbase, (int)nb, chunks, matc);
