@@ -22,7 +22,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
                    "--expt-relaxed-constexpr", "-I", INCLUDE]
 SOURCES = ["lj_core.cu", "lj_grmi.cu", "lj_spline.cu", "lj_lsj.cu", "lj_spline_fit.cpp"]
-HEADERS = ["lj_common.cuh", "lj_part.cuh", "lj_probe_count.h"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 
 
 def _stale(target: str, deps: list[str]) -> bool:

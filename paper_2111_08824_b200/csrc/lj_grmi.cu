@@ -14,6 +14,7 @@
 
 #include "lj_common.cuh"
 #include "lj_part.cuh"
+#include "lj_keybin.cuh"
 #include "lj_part_est.cuh"
 #include "lj_pipe.cuh"
 #include "lj_probe_count.h"
@@ -721,6 +722,13 @@ __global__ void k_window_keys(const u64 *slots, int nwin, int wshift, u64 *wk) {
         wk[w] = slots[2 * ((i64)w << wshift)];
 }
 
+// key-range boundaries of the windows: B[j] = wk[j] + 1 (gapped keys are
+// never the reserved maximum key)
+__global__ void k_window_bounds(const u64 *wk, int nwin, u64 *lay) {
+    for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nwin; w += gridDim.x * blockDim.x)
+        lay[4 + w] = w ? wk[w] + 1 : 0;
+}
+
 static int slot_window_shift(i64 L) {
     int s = 0;
     // <= 2048 windows: blocks x bins open write lines (~148 x 2048 x 128 B)
@@ -948,7 +956,7 @@ int64_t lj_leaf_bucket_capacity(int64_t nk, int64_t L) {
 size_t lj_leaf_bucket_workspace_bytes(int64_t nk, int64_t L) {
     const int nwin = lj_leaf_bucket_bins(L);
     const size_t a = part_workspace_bytes(nk, nwin), b = est_workspace_bytes(nwin);
-    return (a > b ? a : b) + al(sizeof(u64) * (size_t)nwin);
+    return (a > b ? a : b) + al(sizeof(u64) * (size_t)nwin) + al(kb_bytes(nwin));
 }
 
 int lj_leaf_bucket(const LjGrmi *idx, const uint64_t *keys, const uint64_t *pay, int64_t nk, uint64_t *pairs_out,
@@ -972,9 +980,23 @@ int lj_leaf_bucket(const LjGrmi *idx, const uint64_t *keys, const uint64_t *pay,
     LJ_CK_LAUNCH();
     SoaSrc<SlotBin> src{keys, pay, f};
     static const bool exact_only = getenv("LJ_K4_EXACT") != nullptr;
+    static const bool model_bins = getenv("LJ_K4_MODEL_BINS") != nullptr;
     if (staged_ok(idx) && src.aligned16() && !exact_only) {
         // one pass into estimated-capacity regions (+ overflow), the layout
         // the staged probe reads
+        if (!model_bins && nwin <= KB_MAXBINS) {
+            // window = #{ j >= 1 : wk[j] < k } = #{ j : wk[j] + 1 <= k }:
+            // the same bins without a model evaluation per tuple
+            u64 *lay = reinterpret_cast<u64 *>((char *)ws + pws + al(sizeof(u64) * (size_t)nwin));
+            k_window_bounds<<<(nwin + 255) / 256, 256, 0, st>>>(f.wk, nwin, lay);
+            k_keybin_build<<<1, 1024, 0, st>>>(lay, nwin);
+            LJ_CK_LAUNCH();
+            KeyRangeBin kb;
+            kb.g = lay;
+            kb.nb = nwin;
+            SoaSrc<KeyRangeBin> ksrc{keys, pay, kb};
+            return run_partition_est(ksrc, nk, nwin, reinterpret_cast<ulonglong2 *>(pairs_out), reg_out, ws, pws, st);
+        }
         return run_partition_est(src, nk, nwin, reinterpret_cast<ulonglong2 *>(pairs_out), reg_out, ws, pws, st);
     }
     const int rc = run_partition(src, nk, nwin, reinterpret_cast<ulonglong2 *>(pairs_out), reg_out, ws, pws, st);

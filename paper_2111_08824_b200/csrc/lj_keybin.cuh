@@ -1,0 +1,158 @@
+// lj_keybin.cuh -- exact key-range bin function evaluated in shared memory.
+//
+// Every bin function the partition passes use is monotone in the key, so it
+// is a key-range function: bin(k) = #{ j in [1, nb) : B[j] <= k } for
+// non-decreasing boundary keys B.  K4's windows are key ranges by
+// definition (B[j] = gapped key at slot j*2^shift, plus one); LSJ's
+// equi-depth bins over the model's predicted positions are key ranges
+// because pos() is monotone (B[j] = the first key whose predicted position
+// reaches pb[j], found once per call by a 64-step search over the key
+// domain).  Evaluating the model per tuple costs a dependent leaf load from
+// L2 (plus, for LSJ, a bin-table load); this structure needs none: a radix
+// table over a monotone image t(k) of the key -- the key itself or a
+// log-like image (bit length, then the bits below the leading one) for
+// skewed keys, whichever leaves fewer boundaries per cell -- narrows the
+// boundary range to a few entries, and a short binary search over the
+// boundaries (both staged in shared memory, <= 32 KB) finishes it.
+//
+// Exactness: with cell() monotone, every boundary in a cell before k's is
+// < k and every boundary in a cell after k's is > k, so bin(k) lies in
+// [cells[c], cells[c+1]] (cells[c] = #{ j : cell(B[j]) < c }) and the
+// search over that range returns exactly #{ j : B[j] <= k }.
+//
+// Layout (u64 words, global and shared alike):
+//   [0] t0 (image of B[1])   [1] shift | log << 8   [2] nb   [3] 0
+//   [4 + j]  B[j], j in [1, nb)   (word 4 unused)
+//   then u16 cells[KB_CELLS + 1]
+#pragma once
+
+#include "lj_part.cuh"
+
+namespace lj {
+
+constexpr int KB_CELLS = 8192;
+constexpr int KB_MAXBINS = 2048;
+
+__host__ __device__ inline int kb_words(int nb) { return 4 + ((nb + 3) & ~3) + (KB_CELLS + 1 + 3) / 4; }
+inline size_t kb_bytes(int nb) { return (size_t)kb_words(nb) * 8; }
+
+// Monotone log-like image: bit length in the top 7 bits, then the bits
+// below the leading one (truncated to 57).  a <= b  =>  kb_lg(a) <= kb_lg(b).
+__device__ __forceinline__ u64 kb_lg(u64 k) {
+    if (k == 0) return 0;
+    const int z = __clzll((long long)k);
+    return ((u64)(64 - z) << 57) | (((k << z) << 1) >> 7);
+}
+
+__device__ __forceinline__ u64 kb_image(u64 k, int lg) { return lg ? kb_lg(k) : k; }
+
+__device__ __forceinline__ u32 kb_cell(u64 t, u64 t0, int shift) {
+    if (t < t0) return 0;
+    const u64 c = (t - t0) >> shift;
+    return c >= (u64)KB_CELLS ? (u32)(KB_CELLS - 1) : (u32)c;
+}
+
+struct KeyRangeBin {
+    const u64 *g;  // layout (global before staging, shared after)
+    int nb;
+    int shift = 0;  // code -> bin shift of the partition passes (code == bin)
+    __host__ __device__ int smem_words() const { return kb_words(nb); }
+    __device__ void stage(u64 *dst) const {
+        const int w = kb_words(nb);
+        for (int i = threadIdx.x; i < w; i += blockDim.x) dst[i] = g[i];
+    }
+    __device__ __forceinline__ KeyRangeBin at(u64 *tab) const {
+        KeyRangeBin c = *this;
+        c.g = tab;
+        return c;
+    }
+    __device__ __forceinline__ u32 code(u64 k) const {
+        const u64 t0 = g[0];
+        const u32 ctl = (u32)g[1];
+        const u64 *B = g + 4;
+        const u16 *cells = reinterpret_cast<const u16 *>(g + 4 + ((nb + 3) & ~3));
+        const u32 c = kb_cell(kb_image(k, (int)(ctl >> 8)), t0, (int)(ctl & 63));
+        int lo = cells[c], hi = cells[c + 1];
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (B[mid] <= k) lo = mid;
+            else hi = mid - 1;
+        }
+        return (u32)lo;
+    }
+};
+
+// One block of 1024 threads: header + cells from the boundaries already in
+// lay[4 + j], j in [1, nb).  Both images are tried; the one whose fullest
+// cell holds fewer boundaries wins (ties: the key itself).
+static __global__ void __launch_bounds__(1024) k_keybin_build(u64 *lay, int nb) {
+    __shared__ u32 worst[2];
+    __shared__ u64 s_t0[2];
+    __shared__ int s_shift[2];
+    __shared__ u64 pm[KB_MAXBINS];
+    u64 *B = lay + 4;
+    const int tid = threadIdx.x;
+    // the boundaries must be non-decreasing: a running maximum (a no-op
+    // for the monotone bin functions; it keeps the structure sound for any
+    // input)
+    for (int j = tid; j < nb; j += blockDim.x) pm[j] = j ? B[j] : 0;
+    __syncthreads();
+    for (int d = 1; d < nb; d <<= 1) {
+        u64 v[2];
+        for (int r = 0; r < 2; ++r) {
+            const int j = tid + r * (int)blockDim.x;
+            v[r] = (j < nb && j >= d && pm[j - d] > pm[j]) ? pm[j - d] : (j < nb ? pm[j] : 0);
+        }
+        __syncthreads();
+        for (int r = 0; r < 2; ++r) {
+            const int j = tid + r * (int)blockDim.x;
+            if (j < nb) pm[j] = v[r];
+        }
+        __syncthreads();
+    }
+    for (int j = tid; j < nb; j += blockDim.x) B[j] = pm[j];
+    __syncthreads();
+    if (tid < 2) {
+        worst[tid] = 0;
+        u64 t0 = 0, t1 = 0;
+        if (nb >= 2) {
+            t0 = kb_image(B[1], tid);
+            t1 = kb_image(B[nb - 1], tid);
+        }
+        int s = 0;
+        while (s < 63 && ((t1 - t0) >> s) >= (u64)KB_CELLS) ++s;
+        s_t0[tid] = t0;
+        s_shift[tid] = s;
+    }
+    __syncthreads();
+    // #{ j in [1, nb) : cell(B[j]) < c }  (cell() non-decreasing in j)
+    auto below = [&](int m, int c) {
+        int lo = 1, hi = nb;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if ((int)kb_cell(kb_image(B[mid], m), s_t0[m], s_shift[m]) < c) lo = mid + 1;
+            else hi = mid;
+        }
+        return lo - 1;
+    };
+    for (int m = 0; m < 2; ++m) {
+        u32 w = 0;
+        for (int c = tid; c < KB_CELLS; c += blockDim.x) {
+            const u32 d = (u32)(below(m, c + 1) - below(m, c));
+            w = d > w ? d : w;
+        }
+        atomicMax(&worst[m], w);
+    }
+    __syncthreads();
+    const int m = worst[1] < worst[0] ? 1 : 0;
+    u16 *cells = reinterpret_cast<u16 *>(lay + 4 + ((nb + 3) & ~3));
+    for (int c = tid; c <= KB_CELLS; c += blockDim.x) cells[c] = (u16)below(m, c);
+    if (tid == 0) {
+        lay[0] = s_t0[m];
+        lay[1] = (u64)s_shift[m] | ((u64)m << 8);
+        lay[2] = (u64)nb;
+        lay[3] = 0;
+    }
+}
+
+}  // namespace lj

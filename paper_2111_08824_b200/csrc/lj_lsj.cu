@@ -33,6 +33,7 @@
 #include <vector>
 
 #include "lj_common.cuh"
+#include "lj_keybin.cuh"
 #include "lj_part.cuh"
 
 namespace lj {
@@ -96,6 +97,31 @@ struct LsjBin : NoTable {
     __device__ __forceinline__ u32 code(u64 k) const { return (u32)d.bin(k); }
     __device__ __forceinline__ LsjBin at(u64 *) const { return *this; }
 };
+
+// Key boundaries of the bins: B[j] = the first key whose predicted position
+// reaches pb[j] (pos() is monotone in the key, so bin(k) = table[pos(k)] =
+// #{ j : pb[j] <= pos(k) } = #{ j : B[j] <= k }); a 64-step search over the
+// key domain per boundary.  Written as lay[4 + j] (lj_keybin.cuh).
+__global__ void k_lsj_key_bounds(LsjDev d, u64 *lay) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= d.nb) return;
+    if (j == 0) {
+        lay[4] = 0;
+        return;
+    }
+    const i64 target = d.pb[j];
+    u64 lo = 0, hi = ~0ULL;  // invariant: pos(hi) >= target or hi == max
+    if (d.pos(hi) < target) {
+        lay[4 + j] = hi;
+        return;
+    }
+    while (lo < hi) {
+        const u64 mid = lo + ((hi - lo) >> 1);
+        if (d.pos(mid) >= target) hi = mid;
+        else lo = mid + 1;
+    }
+    lay[4 + j] = lo;
+}
 
 // spos[i] = pos(sample[i]) (sample sorted -> spos non-decreasing)
 __global__ void k_sample_pos(RmiDev m, const u64 *sample, i64 total, i64 *spos) {
@@ -938,16 +964,37 @@ int lj_lsj_bins_from_bounds(const int64_t *pb, int64_t nbins, int64_t trained_le
     return LJ_OK;
 }
 
-size_t lj_lsj_partition_workspace_bytes(int64_t n, int64_t nbins) { return part_workspace_bytes(n, (int)nbins); }
+size_t lj_lsj_partition_workspace_bytes(int64_t n, int64_t nbins) {
+    return part_workspace_bytes(n, (int)nbins) + al(kb_bytes((int)nbins));
+}
 
 int lj_lsj_partition(const LjLsjModel *md, const uint64_t *keys, const uint64_t *pay, int64_t n, uint64_t *pairs,
                      int64_t *starts, void *ws, size_t ws_bytes, void *stream) {
     LJ_REQUIRE(md && md->table && md->pb && md->nbins >= 1, "model has no bins");
+    if (ws_bytes < lj_lsj_partition_workspace_bytes(n, md->nbins)) {
+        set_error("lj_lsj_partition: workspace too small");
+        return LJ_E_WORKSPACE;
+    }
+    cudaStream_t st = as_stream(stream);
+    const int nb = (int)md->nbins;
+    const size_t pws = part_workspace_bytes(n, nb);
+    static const bool model_bins = getenv("LJ_LSJ_MODEL_BINS") != nullptr;
+    if (!model_bins && nb <= KB_MAXBINS) {
+        // the model's bins as key ranges: no model evaluation per tuple
+        u64 *lay = reinterpret_cast<u64 *>((char *)ws + pws);
+        k_lsj_key_bounds<<<(nb + 127) / 128, 128, 0, st>>>(make_lsj(*md), lay);
+        k_keybin_build<<<1, 1024, 0, st>>>(lay, nb);
+        LJ_CK_LAUNCH();
+        KeyRangeBin kb;
+        kb.g = lay;
+        kb.nb = nb;
+        SoaSrc<KeyRangeBin> src{keys, pay, kb};
+        return run_partition(src, n, nb, reinterpret_cast<ulonglong2 *>(pairs), starts, ws, pws, st);
+    }
     LsjBin f;
     f.d = make_lsj(*md);
     SoaSrc<LsjBin> src{keys, pay, f};
-    return run_partition(src, n, (int)md->nbins, reinterpret_cast<ulonglong2 *>(pairs), starts, ws, ws_bytes,
-                         as_stream(stream));
+    return run_partition(src, n, nb, reinterpret_cast<ulonglong2 *>(pairs), starts, ws, pws, st);
 }
 
 static i64 max_subs(i64 n, i64 nbins) { return 2 * (n / SUB + nbins) + 2; }
