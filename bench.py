@@ -116,7 +116,7 @@ def build_index(inp):
     return None  # lsj builds nothing ahead of time: it is timed end to end
 
 
-DEFAULT_VARIANT = {"c1": "direct", "c2": "buffered", "c3": "direct"}
+DEFAULT_VARIANT = {"c1": "direct", "c2": "buffered", "c3": "buffered"}
 
 
 class Step:
@@ -149,10 +149,10 @@ def make_step(inp, index, variant="buffered"):
             scratch = index.bucket_scratch(n_s)
             parts = [("bucket", lambda out: index.bucket_records(keys, pays, scratch)),
                      ("probe", lambda out: index.probe_records(n_s, scratch, out))]
-            kern = "k_grmi_probe_staged" if grmi else "k_hash_probe<grouped>"
+            kern = "k_grmi_probe_staged" if grmi else "k_hash_probe_chunks"
             return Step(parts, "probe", 32 * n_s, kern,
-                        f"32 B/probe x {n_s} probes (16 B S record + 16 B R entry); the K4 bucketing "
-                        "(k_bin_hist_tma + k_bin_scatter_tma) runs before it in the step")
+                        f"32 B/probe x {n_s} probes (16 B S record + 16 B R entry); the one-pass bucketing "
+                        "(k_est_sample + k_bin_scatter_est) runs before it in the step")
         fn = (lambda out: index.join_checksum(keys, pays, out=out))
         return Step([("probe", fn)], "probe", 32 * n_s, "k_grmi_probe" if grmi else "k_hash_probe",
                     f"32 B/probe x {n_s} probes (16 B S record + 16 B R entry)")

@@ -250,6 +250,22 @@ int lj_spline_hash_bucket(const LjSplineHash *idx, const uint64_t *keys, const u
                           uint64_t *pairs_out, int64_t *starts_out, void *ws, size_t ws_bytes, void *stream);
 int lj_spline_hash_probe_grouped(const LjSplineHash *idx, const uint64_t *s_pairs, int64_t nk, uint64_t *out,
                                  int accumulate, void *stream);
+/* One-pass variant (the default of the buffered runner): S grouped by
+ * approximate-position window into est-capacity regions (lj_leaf_bucket's
+ * layout: reg[2*bins+2] = region starts, region ends, overflow count; gap
+ * records carry the reserved key 2^64-1); pairs_out holds
+ * lj_spline_hash_bucket_capacity(nk, n) records; columns 16-B aligned. */
+int64_t lj_spline_hash_bucket_bins(int64_t n);
+int64_t lj_spline_hash_bucket_capacity(int64_t nk, int64_t n);
+size_t lj_spline_hash_bucket_est_workspace_bytes(int64_t nk, int64_t n);
+int lj_spline_hash_bucket_est(const LjSplineHash *idx, const uint64_t *keys, const uint64_t *pay, int64_t nk,
+                              uint64_t *pairs_out, int64_t *reg_out, void *ws, size_t ws_bytes, void *stream);
+/* K5 over those regions, handed out to the CTAs in record order by a chunk
+ * counter (ws >= 8 bytes), so every SM works on the same few windows and
+ * their chain offsets and entries stay in L2. */
+int lj_spline_hash_probe_regions(const LjSplineHash *idx, const uint64_t *s_pairs, const int64_t *reg,
+                                 int64_t nbins, void *ws, size_t ws_bytes, uint64_t *out, int accumulate,
+                                 void *stream);
 int lj_spline_hash_count(const LjSplineHash *idx, const uint64_t *keys, int64_t nk,
                          int64_t *counts, void *stream);
 int lj_spline_hash_collect(const LjSplineHash *idx, const uint64_t *keys, int64_t nk,

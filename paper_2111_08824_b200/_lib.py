@@ -104,6 +104,11 @@ SIGNATURES = {
     "lj_spline_hash_bucket_workspace_bytes": (_size_t, [_i64, _i64]),
     "lj_spline_hash_bucket": (_int, [ctypes.POINTER(LjSplineHash), _P, _P, _i64, _P, _P, _P, _size_t, _P]),
     "lj_spline_hash_probe_grouped": (_int, [ctypes.POINTER(LjSplineHash), _P, _i64, _P, _int, _P]),
+    "lj_spline_hash_bucket_bins": (_i64, [_i64]),
+    "lj_spline_hash_bucket_capacity": (_i64, [_i64, _i64]),
+    "lj_spline_hash_bucket_est_workspace_bytes": (_size_t, [_i64, _i64]),
+    "lj_spline_hash_bucket_est": (_int, [ctypes.POINTER(LjSplineHash), _P, _P, _i64, _P, _P, _P, _size_t, _P]),
+    "lj_spline_hash_probe_regions": (_int, [ctypes.POINTER(LjSplineHash), _P, _P, _i64, _P, _size_t, _P, _int, _P]),
     "lj_spline_hash_count": (_int, [ctypes.POINTER(LjSplineHash), _P, _i64, _P, _P]),
     "lj_spline_hash_collect": (_int, [ctypes.POINTER(LjSplineHash), _P, _i64, _P, _P, _P, _P]),
     "lj_lsj_sample_workspace_bytes": (_size_t, [_i64]),

@@ -176,6 +176,60 @@ struct SlotMap {
     }
 };
 
+// ------------------------------------------------------------ L2 policies
+
+// Read-only loads of small, hot structures (models, tables): plain __ldg,
+// or with an L2 evict_last policy so a stream of random, touched-once
+// index lines (evict_first) does not push them out of L2.
+struct LdNc {
+    __device__ __forceinline__ u64 u(const u64 *p) const { return ldg(p); }
+    __device__ __forceinline__ u32 w(const u32 *p) const { return __ldg(p); }
+    __device__ __forceinline__ double d(const double *p) const { return __ldg(p); }
+};
+struct LdKeep {
+    u64 pol;
+    __device__ __forceinline__ static LdKeep make() {
+        LdKeep l;
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(l.pol));
+        return l;
+    }
+    __device__ __forceinline__ u64 u(const u64 *p) const {
+        u64 v;
+        asm volatile("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+        return v;
+    }
+    __device__ __forceinline__ u32 w(const u32 *p) const {
+        u32 v;
+        asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+        return v;
+    }
+    __device__ __forceinline__ double d(const double *p) const {
+        double v;
+        asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+        return v;
+    }
+};
+// touched-once random lines: evict_first in L2
+struct LdOnce {
+    u64 pol;
+    __device__ __forceinline__ static LdOnce make() {
+        LdOnce l;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(l.pol));
+        return l;
+    }
+    __device__ __forceinline__ u32 w(const u32 *p) const {
+        u32 v;
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+        return v;
+    }
+    __device__ __forceinline__ ulonglong2 q(const ulonglong2 *p) const {
+        ulonglong2 v;
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;"
+                     : "=l"(v.x), "=l"(v.y) : "l"(p), "l"(pol));
+        return v;
+    }
+};
+
 // ------------------------------------------------------------ RadixSpline
 
 struct SplineDev {
@@ -193,27 +247,29 @@ struct SplineDev {
 
     // first spline point of k's (sub-)radix bucket: a cheap, monotone
     // approximation of where k lands (no search, no division)
-    __device__ __forceinline__ i64 bucket_first_point(u64 k) const {
+    template <class L = LdNc>
+    __device__ __forceinline__ i64 bucket_first_point(u64 k, const L &ld = L()) const {
         if (K <= 1) return 0;
         const i64 rmax = ((i64)1 << radix_bits) - 1;
         const u64 raw = shift >= 64 ? 0 : (k >> shift);
         i64 lo;
-        const u64 ax = (aux && raw <= (u64)rmax) ? ldg(aux + raw) : 0;
+        const u64 ax = (aux && raw <= (u64)rmax) ? ld.u(aux + raw) : 0;
         if (ax & 0xFF) {
             const int bits = (int)(ax & 0xFF);
             const u64 q = (k >> (shift - (u64)bits)) & ((1ULL << bits) - 1ULL);
-            lo = (i64)__ldg(sub + (ax >> 8) + q);
+            lo = (i64)ld.w(sub + (ax >> 8) + q);
         } else {
-            lo = (i64)__ldg(radix + (raw > (u64)rmax ? rmax : (i64)raw));
+            lo = (i64)ld.w(radix + (raw > (u64)rmax ? rmax : (i64)raw));
         }
         return lo < 0 ? 0 : (lo > K - 1 ? K - 1 : lo);
     }
 
     // models.py:221-248 + _bounded_first_geq :263-282
-    __device__ __forceinline__ i64 pos(u64 k) const {
+    template <class L = LdNc>
+    __device__ __forceinline__ i64 pos(u64 k, const L &ld = L()) const {
         i64 p;
         if (K == 1) {
-            p = (i64)__ldg(ranks);
+            p = (i64)ld.d(ranks);
         } else {
             i64 rmax = ((i64)1 << radix_bits) - 1;
             // np.minimum((k >> shift).astype(int64), rmax); negative values
@@ -227,29 +283,29 @@ struct SplineDev {
             i64 lo, hi;
             const u64 raw = shift >= 64 ? 0 : (k >> shift);
             u64 ax = 0;
-            if (aux && raw <= (u64)rmax) ax = ldg(aux + raw);  // unclamped prefix: sub-table is exact
+            if (aux && raw <= (u64)rmax) ax = ld.u(aux + raw);  // unclamped prefix: sub-table is exact
             if (ax & 0xFF) {
                 const int bits = (int)(ax & 0xFF);
                 const u64 q = (k >> (shift - (u64)bits)) & ((1ULL << bits) - 1ULL);
                 const u32 *s = sub + (ax >> 8) + q;
-                lo = (i64)__ldg(s);
-                hi = (i64)__ldg(s + 1);
+                lo = (i64)ld.w(s);
+                hi = (i64)ld.w(s + 1);
             } else {
-                lo = (i64)__ldg(radix + (a < 0 ? 0 : a));
-                hi = (i64)__ldg(radix + (b < 0 ? 0 : b));
+                lo = (i64)ld.w(radix + (a < 0 ? 0 : a));
+                hi = (i64)ld.w(radix + (b < 0 ? 0 : b));
             }
             if (hi < lo) hi = lo;
             if (hi > K) hi = K;
             while (lo < hi) {
                 i64 mid = (lo + hi) >> 1;
-                if (ldg(keys + mid) < k) lo = mid + 1; else hi = mid;
+                if (ld.u(keys + mid) < k) lo = mid + 1; else hi = mid;
             }
             i64 j = clip_i64(lo, 1, K - 1 > 1 ? K - 1 : 1);
-            double x0 = u64_to_f64(ldg(keys + j - 1)), x1 = u64_to_f64(ldg(keys + j));
+            double x0 = u64_to_f64(ld.u(keys + j - 1)), x1 = u64_to_f64(ld.u(keys + j));
             double kf = u64_to_f64(k);
             double d = __dsub_rn(x1, x0);
             double t = clip_f64(__ddiv_rn(__dsub_rn(kf, x0), d > 1.0 ? d : 1.0), 0.0, 1.0);
-            double r0 = __ldg(ranks + j - 1), r1 = __ldg(ranks + j);
+            double r0 = ld.d(ranks + j - 1), r1 = ld.d(ranks + j);
             p = f64_to_i64(rint(__dadd_rn(r0, __dmul_rn(t, __dsub_rn(r1, r0)))));
         }
         return clip_i64(p, 0, n - 1);

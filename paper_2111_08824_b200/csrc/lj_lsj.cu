@@ -35,6 +35,7 @@
 #include "lj_common.cuh"
 #include "lj_keybin.cuh"
 #include "lj_part.cuh"
+#include "lj_part_est.cuh"
 
 namespace lj {
 
@@ -989,7 +990,7 @@ int lj_lsj_partition(const LjLsjModel *md, const uint64_t *keys, const uint64_t 
         kb.g = lay;
         kb.nb = nb;
         SoaSrc<KeyRangeBin> src{keys, pay, kb};
-        return run_partition(src, n, nb, reinterpret_cast<ulonglong2 *>(pairs), starts, ws, pws, st);
+        return run_partition_fast(src, n, nb, reinterpret_cast<ulonglong2 *>(pairs), starts, ws, pws, st);
     }
     LsjBin f;
     f.d = make_lsj(*md);

@@ -151,7 +151,7 @@ constexpr int PT_TILE_S = 4096;          // tuples per sorted scatter tile (long
 constexpr size_t PT_STAGE_H = sizeof(u64) * PT_TILE_H;
 constexpr size_t PT_STAGE_S = (size_t)PT_TILE_S * (8 + 8 + 2);
 constexpr int PT_MAXST = 6;
-constexpr int PT_SMEM_MAX = 220 * 1024;
+constexpr int PT_SMEM_MAX = 226 * 1024;  // + < 1 KB static, within the 227 KB opt-in
 
 // Pass 1, warp-specialised: the last warp issues the bulk copies, the other
 // 31 consume rows of 32 keys round-robin and release a stage on its `empty`
@@ -277,9 +277,11 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_tma(Src f, const u16 *
         for (int t = 0; t < min(nst - 1, ntiles); ++t) issue(t);
     }
     __syncthreads();
+    // Four barriers per tile (no barrier after the writes): the stage of
+    // tile t-1 is refilled once every warp has passed the first barrier of
+    // tile t.
     for (int t = 0; t < ntiles; ++t) {
         const int s = t % nst;
-        if (tid == 0 && t + nst - 1 < ntiles) issue(t + nst - 1);  // stage consumed in round t-1
         mbar_wait(&full[s], (unsigned)(t / nst) & 1u);
         const i64 base = lo + (i64)t * PT_TILE_S;
         const int cnt = (int)min((i64)PT_TILE_S, hi - base), nb = cnt & ~1, nb8 = cnt & ~7;
@@ -295,6 +297,7 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_tma(Src f, const u16 *
             rj[u] = bj[u] >= 0 ? (int)atomicAdd(thist + bj[u], 1u) : 0;
         }
         __syncthreads();
+        if (tid == 0 && t + nst - 1 < ntiles) issue(t + nst - 1);  // stage of tile t-1
         // (2) exclusive scan of the tile histogram (nbins <= 2 * PART2_NT)
         // -> run starts; reserve the runs in the block's segments
         {
@@ -352,7 +355,6 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_tma(Src f, const u16 *
                 out[at] = make_ulonglong2(k, p);
             }
         }
-        __syncthreads();
     }
 }
 

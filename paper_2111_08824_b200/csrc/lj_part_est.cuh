@@ -29,8 +29,9 @@ constexpr size_t EST_STAGE = (size_t)EST_TILE * 16;
 // capacity of the output (records) for n tuples in nb bins: regions + overflow
 inline i64 est_capacity(i64 n, int nb) { return n + n / 16 + (i64)nb * (EST_PAD + EST_STRIDE + 1) + 64 + n; }
 
+// per-bin counts of every `stride`-th tuple (stride 1: the exact histogram)
 template <class Src>
-__global__ void __launch_bounds__(256) k_est_sample(Src f0, i64 n, int nbins, u32 *est) {
+__global__ void __launch_bounds__(256) k_est_sample(Src f0, i64 n, int nbins, int stride, u32 *est) {
     extern __shared__ __align__(128) unsigned char smem_e[];
     u64 *tab = reinterpret_cast<u64 *>(smem_e);
     u32 *h = reinterpret_cast<u32 *>(smem_e + pt_table_bytes(f0.f.smem_words()));
@@ -40,18 +41,31 @@ __global__ void __launch_bounds__(256) k_est_sample(Src f0, i64 n, int nbins, u3
     for (int j = threadIdx.x; j < nbins; j += blockDim.x) h[j] = 0;
     __syncthreads();
     const int shift = f.f.shift;
-    for (i64 i = (blockIdx.x * (i64)blockDim.x + threadIdx.x) * EST_STRIDE; i < n;
-         i += (i64)gridDim.x * blockDim.x * EST_STRIDE)
-        atomicAdd(h + (f.code(ld_stream(f.keys + i)) >> shift), 1u);
+    const i64 step = (i64)gridDim.x * blockDim.x * stride;
+    i64 i = (blockIdx.x * (i64)blockDim.x + threadIdx.x) * stride;
+    for (; i + 3 * step < n; i += 4 * step) {  // four independent loads in flight
+        u64 k[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) k[u] = ld_stream(f.keys + i + u * step);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) atomicAdd(h + (f.code(k[u]) >> shift), 1u);
+    }
+    for (; i < n; i += step) atomicAdd(h + (f.code(ld_stream(f.keys + i)) >> shift), 1u);
     __syncthreads();
     for (int j = threadIdx.x; j < nbins; j += blockDim.x)
         if (h[j]) atomicAdd(est + j, h[j]);
 }
 
-__global__ void k_est_caps(const u32 *est, int nbins, i64 *cap) {
+// region capacity per bin: the exact count, or the sample estimate with
+// slack (est * 17/16 + pad)
+static __global__ void k_est_caps(const u32 *est, int nbins, int exact, i64 *cap) {
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b <= nbins; b += gridDim.x * blockDim.x) {
         if (b == nbins) {
             cap[b] = 0;
+            continue;
+        }
+        if (exact) {
+            cap[b] = (i64)est[b];
             continue;
         }
         const i64 e = (i64)est[b] * EST_STRIDE;
@@ -76,8 +90,8 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_est(Src f0, i64 n, i64
     u32 *gbase = tstart + nb4;                   // claimed position of the run in its bin
     i64 *srst = reinterpret_cast<i64 *>(gbase + nb4);  // region starts [nbins + 1]
     u16 *perm = reinterpret_cast<u16 *>(srst + nb4 + 32);
-    u16 *tbin = perm + EST_TILE;                 // bin of every tuple of the tile
-    unsigned char *ring = reinterpret_cast<unsigned char *>(perm) + ((EST_TILE * 4 + 127) & ~127);
+    u16 *tbin2 = perm + EST_TILE;                // bin of every tuple of the tile (double-buffered by tile parity)
+    unsigned char *ring = reinterpret_cast<unsigned char *>(perm) + ((EST_TILE * 6 + 127) & ~127);
     __shared__ __align__(8) uint64_t full[PT_MAXST];
     __shared__ u32 wsum[PART2_NT / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, shift = f.f.shift;
@@ -104,15 +118,20 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_est(Src f0, i64 n, i64
         for (int t = 0; t < min(nst - 1, ntiles); ++t) issue(t);
     }
     __syncthreads();
+    // Four barriers per tile: the tile's bins are double-buffered, so the
+    // next tile's binning (1) may start while slower warps still write this
+    // tile's runs (4); the run claims (global atomics) are issued before
+    // the scan and their results are stored only after the permutation,
+    // so their latency overlaps both.
     for (int t = 0; t < ntiles; ++t) {
         const int s = t % nst;
-        if (tid == 0 && t + nst - 1 < ntiles) issue(t + nst - 1);  // stage consumed in round t-1
         mbar_wait(&full[s], (unsigned)(t / nst) & 1u);
         const i64 base = lo + (i64)t * EST_TILE;
         const int cnt = (int)min((i64)EST_TILE, hi - base), nb = cnt & ~1;
         const unsigned char *st = ring + (size_t)s * EST_STAGE;
         const u64 *ks = reinterpret_cast<const u64 *>(st), *ps = ks + EST_TILE;
-        // (1) bin of every tuple (the model, once) and its rank in the tile's run
+        u16 *tbin = tbin2 + (t & 1) * EST_TILE;
+        // (1) bin of every tuple and its rank in the tile's run
         int bj[U], rj[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -125,10 +144,14 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_est(Src f0, i64 n, i64
             if (bj[u] >= 0) tbin[u * PART2_NT + tid] = (u16)bj[u];
         }
         __syncthreads();
-        // (2) scan of the tile histogram -> run starts; claim every run in
-        // its bin with one global atomic
+        // every warp is past tile t-1's writes: its stage may be refilled
+        if (tid == 0 && t + nst - 1 < ntiles) issue(t + nst - 1);
+        // (2) claim every run in its bin (one global atomic each), then the
+        // exclusive scan of the tile histogram -> run starts
+        const u32 v0 = 2 * tid < nbins ? thist[2 * tid] : 0, v1 = 2 * tid + 1 < nbins ? thist[2 * tid + 1] : 0;
+        const u32 g0 = v0 ? atomicAdd(gcur + 2 * tid, v0) : 0;
+        const u32 g1 = v1 ? atomicAdd(gcur + 2 * tid + 1, v1) : 0;
         {
-            u32 v0 = 2 * tid < nbins ? thist[2 * tid] : 0, v1 = 2 * tid + 1 < nbins ? thist[2 * tid + 1] : 0;
             const u32 tot = v0 + v1;
             u32 inc = tot;
 #pragma unroll
@@ -152,20 +175,20 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_est(Src f0, i64 n, i64
             const u32 r0 = wsum[warp] + inc - tot;
             if (2 * tid < nbins) {
                 tstart[2 * tid] = r0;
-                if (v0) gbase[2 * tid] = atomicAdd(gcur + 2 * tid, v0);
                 thist[2 * tid] = 0;
             }
             if (2 * tid + 1 < nbins) {
                 tstart[2 * tid + 1] = r0 + v0;
-                if (v1) gbase[2 * tid + 1] = atomicAdd(gcur + 2 * tid + 1, v1);
                 thist[2 * tid + 1] = 0;
             }
         }
         __syncthreads();
-        // (3) tile permutation sorted by bin
+        // (3) tile permutation sorted by bin; the claims land
 #pragma unroll
         for (int u = 0; u < U; ++u)
             if (bj[u] >= 0) perm[tstart[bj[u]] + rj[u]] = (u16)(u * PART2_NT + tid);
+        if (v0) gbase[2 * tid] = g0;
+        if (v1) gbase[2 * tid + 1] = g1;
         __syncthreads();
         // (4) write bin runs into their regions (overflow behind the regions)
 #pragma unroll
@@ -181,11 +204,10 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_est(Src f0, i64 n, i64
                 out[dst] = make_ulonglong2(k, p);
             }
         }
-        __syncthreads();
     }
 }
 
-__global__ void k_est_regions(const i64 *rstart, const u32 *gcur, const unsigned long long *ovf, int nbins,
+static __global__ void k_est_regions(const i64 *rstart, const u32 *gcur, const unsigned long long *ovf, int nbins,
                               i64 *reg) {
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b <= nbins; b += gridDim.x * blockDim.x) {
         reg[b] = rstart[b];
@@ -201,11 +223,17 @@ inline size_t est_workspace_bytes(int nbins) {
            part_align(sizeof(unsigned long long)) + part_align(t);
 }
 
-// One-pass partition of the n tuples of `f` into out (est_capacity records);
-// reg[2*nbins+2] as described above.
+// Partition of the n tuples of `f` into regions claimed run by run with
+// one global atomic per (tile, bin), so the open write frontiers are one
+// per bin, shared by all CTAs (per-CTA bin segments leave blocks x bins
+// half-written lines in L2; measured +22 % DRAM writes and reads).
+//   exact = 0: one pass; a 1/EST_STRIDE sample sizes the regions
+//              (est_capacity records, gaps, overflow), reg as above.
+//   exact = 1: an exact counting pass sizes them: out[n] grouped by bin,
+//              contiguous, reg[0..nbins] = bin starts (no overflow).
 template <class Src>
-int run_partition_est(const Src &f, i64 n, int nbins, ulonglong2 *out, i64 *reg, void *ws, size_t ws_bytes,
-                      cudaStream_t st) {
+int run_partition_claims(const Src &f, i64 n, int nbins, int exact, ulonglong2 *out, i64 *reg, void *ws,
+                         size_t ws_bytes, cudaStream_t st) {
     if (nbins < 1 || nbins > 2 * PART2_NT) {
         set_error("partition_est: nbins must be in [1, 2048]");
         return LJ_E_INVALID;
@@ -221,7 +249,7 @@ int run_partition_est(const Src &f, i64 n, int nbins, ulonglong2 *out, i64 *reg,
     q += part_align(sizeof(u32) * (size_t)nbins);
     i64 *cap = (i64 *)q;
     q += part_align(sizeof(i64) * (size_t)(nbins + 1));
-    i64 *rstart = (i64 *)q;
+    i64 *rstart = exact ? reg : (i64 *)q;
     q += part_align(sizeof(i64) * (size_t)(nbins + 1));
     unsigned long long *ovf = (unsigned long long *)q;
     q += part_align(sizeof(unsigned long long));
@@ -232,14 +260,16 @@ int run_partition_est(const Src &f, i64 n, int nbins, ulonglong2 *out, i64 *reg,
     static bool attr = false;
     if (!attr) {
         LJ_CK(cudaFuncSetAttribute(k_bin_scatter_est<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_SMEM_MAX));
+        LJ_CK(cudaFuncSetAttribute(k_est_sample<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_SMEM_MAX));
         attr = true;
     }
+    const int stride = exact ? 1 : EST_STRIDE;
     if (n > 0) {
-        k_est_sample<Src><<<grid_for((n + EST_STRIDE - 1) / EST_STRIDE, 256, 4), 256, tb + sizeof(u32) * nbins, st>>>(
-            f, n, nbins, est);
+        k_est_sample<Src><<<grid_for((n + stride - 1) / stride, 256, 4), 256, tb + sizeof(u32) * nbins, st>>>(
+            f, n, nbins, stride, est);
         LJ_CK_LAUNCH();
     }
-    k_est_caps<<<(nbins + 256) / 256, 256, 0, st>>>(est, nbins, cap);
+    k_est_caps<<<(nbins + 256) / 256, 256, 0, st>>>(est, nbins, exact, cap);
     LJ_CK_LAUNCH();
     size_t t = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, t, cap, rstart, (int64_t)(nbins + 1));
@@ -248,8 +278,8 @@ int run_partition_est(const Src &f, i64 n, int nbins, ulonglong2 *out, i64 *reg,
         const PartPlan p = part_plan(n, nbins);
         const size_t nb4 = (size_t)((nbins + 31) & ~31);
         const size_t fix = tb + 3 * nb4 * sizeof(u32) + (nb4 + 32) * sizeof(i64) +
-                           (((size_t)EST_TILE * 4 + 127) & ~(size_t)127);
-        const int nst = (int)min((size_t)PT_MAXST, (PT_SMEM_MAX - fix) / EST_STAGE);
+                           (((size_t)EST_TILE * 6 + 127) & ~(size_t)127);
+        const int nst = fix < (size_t)PT_SMEM_MAX ? (int)min((size_t)PT_MAXST, (PT_SMEM_MAX - fix) / EST_STAGE) : 0;
         if (nst < 2) {
             set_error("partition_est: shared memory too small for the ring");
             return LJ_E_INVALID;
@@ -258,9 +288,31 @@ int run_partition_est(const Src &f, i64 n, int nbins, ulonglong2 *out, i64 *reg,
                                                                                    gcur, ovf, out);
         LJ_CK_LAUNCH();
     }
-    k_est_regions<<<(nbins + 256) / 256, 256, 0, st>>>(rstart, gcur, ovf, nbins, reg);
-    LJ_CK_LAUNCH();
+    if (!exact) {
+        k_est_regions<<<(nbins + 256) / 256, 256, 0, st>>>(rstart, gcur, ovf, nbins, reg);
+        LJ_CK_LAUNCH();
+    }
     return LJ_OK;
+}
+
+// One pass into estimated-capacity regions (est_capacity records);
+// reg[2*nbins+2] as described above.
+template <class Src>
+int run_partition_est(const Src &f, i64 n, int nbins, ulonglong2 *out, i64 *reg, void *ws, size_t ws_bytes,
+                      cudaStream_t st) {
+    return run_partition_claims(f, n, nbins, 0, out, reg, ws, ws_bytes, st);
+}
+
+// Exact partition: out[n] grouped by bin, starts[nbins+1].  Bulk-copy
+// ring + shared frontiers when the columns are 16-B aligned and nbins <=
+// 2048, else the per-CTA-segment two-pass partition (lj_part.cuh).
+template <class Src>
+int run_partition_fast(const Src &f, i64 n, int nbins, ulonglong2 *out, i64 *starts, void *ws, size_t ws_bytes,
+                       cudaStream_t st) {
+    static const bool legacy = getenv("LJ_PART_SEGMENTS") != nullptr;
+    if (!legacy && f.aligned16() && nbins <= 2 * PART2_NT && n < (i64)0xFFFFFFFFLL)
+        return run_partition_claims(f, n, nbins, 1, out, starts, ws, ws_bytes, st);
+    return run_partition(f, n, nbins, out, starts, ws, ws_bytes, st);
 }
 
 }  // namespace lj

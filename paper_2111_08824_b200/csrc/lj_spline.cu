@@ -12,7 +12,9 @@
 #include <cub/cub.cuh>
 
 #include "lj_common.cuh"
+#include "lj_keybin.cuh"
 #include "lj_part.cuh"
+#include "lj_part_est.cuh"
 
 namespace lj {
 
@@ -25,9 +27,10 @@ struct HashDev {
     __host__ explicit HashDev(const LjSplineHash &h)
         : model(h.model), n(h.n), P(h.table_len), stride(h.stride), entries(h.entries), starts(h.starts),
           direct(h.model.n > 0 && h.table_len == h.stride * h.model.n) {}
-    __device__ __forceinline__ i64 slot_of(u64 k) const {
+    template <class L = LdNc>
+    __device__ __forceinline__ i64 slot_of(u64 k, const L &ld = L()) const {
         // models.py:297 clip(pos*P // n, 0, P-1) / stride; pos is in [0, n)
-        const i64 p = model.pos(k);
+        const i64 p = model.pos(k, ld);
         return direct ? p : scale_bucket(p, P, model.n) / stride;
     }
 };
@@ -131,6 +134,66 @@ __global__ void __launch_bounds__(NT) k_hash_probe(HashDev h, In in, i64 nk, u64
                 ++cnt;
                 sum += v;
                 x ^= v;
+            }
+        }
+    }
+    reduce_checksum(cnt, sum, x, 0, out);
+}
+
+// Grouped probe with ordered dynamic dispatch: each CTA takes the next
+// chunk of CH records from a global counter, so all SMs work on a sliding
+// stretch of ~(CTAs x CH) records -- a few windows, whose chain offsets and
+// entries stay in L2 (a grid-stride loop lets CTAs drift apart over
+// thousands of iterations and spread the working set over the table).
+// Records span [0, reg[nb] + reg[2 nb + 1]) (est regions + overflow); gap
+// records carry the reserved key ~0 (never a build key) and are skipped.
+template <int NT, int U, int R>
+__global__ void __launch_bounds__(NT) k_hash_probe_chunks(HashDev h, const ulonglong2 *__restrict__ rec,
+                                                          const i64 *reg, int nb, unsigned long long *ctr, u64 *out) {
+    constexpr i64 CH = (i64)NT * U * R;
+    __shared__ i64 s_c;
+    u64 cnt = 0, sum = 0, x = 0;
+    const LdKeep keep = LdKeep::make();
+    const i64 nk = reg[nb] + reg[2 * nb + 1];
+    for (;;) {
+        if (threadIdx.x == 0) s_c = (i64)atomicAdd(ctr, 1ULL) * CH;
+        __syncthreads();
+        const i64 c0 = s_c;
+        __syncthreads();
+        if (c0 >= nk) break;
+#pragma unroll 1
+        for (int r = 0; r < R; ++r) {
+            const i64 t0 = c0 + (i64)r * NT * U + threadIdx.x;
+            u64 k[U], ps[U];
+            i64 b[U];
+            u32 a[U], e[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const i64 t = t0 + u * NT;
+                k[u] = ps[u] = 0;
+                if (t < nk) {
+                    const ulonglong2 v = __ldcs(rec + t);
+                    k[u] = v.x;
+                    ps[u] = v.y;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) b[u] = (t0 + u * NT < nk && k[u] != ~0ULL) ? h.slot_of(k[u], keep) : -1;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                a[u] = b[u] >= 0 ? __ldg(h.starts + b[u]) : 0;
+                e[u] = b[u] >= 0 ? __ldg(h.starts + b[u] + 1) : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                for (u32 i = a[u]; i < e[u]; ++i) {
+                    const ulonglong2 en = __ldg(reinterpret_cast<const ulonglong2 *>(h.entries) + i);
+                    if (en.x != k[u]) continue;
+                    const u64 v = en.y + ps[u];
+                    ++cnt;
+                    sum += v;
+                    x ^= v;
+                }
             }
         }
     }
@@ -244,10 +307,20 @@ int lj_spline_hash_probe(const LjSplineHash *idx, const uint64_t *s_keys, const 
     if (nk <= 0 || idx->n == 0) return LJ_OK;
     constexpr int NT = 256;
     // 4 probes in flight per thread (measured: 125 ms vs 154 ms with 1 at C3)
+    // (L2 evict_last on the spline + evict_first on the chains measured
+    // 173 ms vs 118 ms at C3: plain loads)
     k_hash_probe<NT, 4, HashSoa, false><<<grid_for((nk + 3) / 4, NT, 8), NT, 0, st>>>(
         HashDev(*idx), HashSoa{s_keys, s_pay}, nk, out);
     LJ_CK_LAUNCH();
     return LJ_OK;
+}
+
+// est-region gaps [rend[b], rstart[b+1]) get the reserved key ~0 (skipped
+// by the probe)
+__global__ void k_fill_gaps(const i64 *reg, int nb, ulonglong2 *out) {
+    const int b = blockIdx.x;
+    const i64 lo = reg[nb + 1 + b], hi = reg[b + 1];
+    for (i64 i = lo + threadIdx.x; i < hi; i += blockDim.x) out[i] = make_ulonglong2(~0ULL, 0ULL);
 }
 
 // Request-Buffer analogue for the learned hash: group S by a window of
@@ -272,11 +345,38 @@ struct PosBin : NoTable {
 
 static int hash_bins(i64 n) { return (int)(n < 2048 ? (n < 1 ? 1 : n) : 2048); }
 
-size_t lj_spline_hash_bucket_workspace_bytes(int64_t nk, int64_t n) { return part_workspace_bytes(nk, hash_bins(n)); }
+size_t lj_spline_hash_bucket_workspace_bytes(int64_t nk, int64_t n) {
+    return part_workspace_bytes(nk, hash_bins(n)) + kb_bytes(hash_bins(n)) + 256;
+}
+
+// equi-depth key windows over the build side: B[j] = key of entry j*n/nb
+// (entries are grouped by predicted position, monotone in the key; the
+// layout build takes a running maximum)
+__global__ void k_hash_window_bounds(const u64 *entries, i64 n, int nb, u64 *lay) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nb; j += gridDim.x * blockDim.x)
+        lay[4 + j] = j ? entries[2 * (i64)(((unsigned __int128)j * (u64)n) / (u64)nb)] : 0;
+}
 
 int lj_spline_hash_bucket(const LjSplineHash *idx, const uint64_t *keys, const uint64_t *pay, int64_t nk,
                           uint64_t *pairs_out, int64_t *starts_out, void *ws, size_t ws_bytes, void *stream) {
     LJ_REQUIRE(idx && idx->n >= 1, "index is empty");
+    LJ_REQUIRE(ws_bytes >= lj_spline_hash_bucket_workspace_bytes(nk, idx->n), "workspace too small");
+    static const bool pos_bins = getenv("LJ_HASH_POS_BINS") != nullptr;
+    if (!pos_bins) {
+        // KEY windows, evaluated in shared memory (lj_keybin.cuh)
+        const int nb = hash_bins(idx->n);
+        const size_t pws = part_workspace_bytes(nk, nb);
+        u64 *lay = reinterpret_cast<u64 *>(((uintptr_t)ws + pws + 255) & ~(uintptr_t)255);
+        cudaStream_t st = as_stream(stream);
+        k_hash_window_bounds<<<(nb + 255) / 256, 256, 0, st>>>(idx->entries, idx->n, nb, lay);
+        k_keybin_build<<<1, 1024, 0, st>>>(lay, nb);
+        LJ_CK_LAUNCH();
+        KeyRangeBin kb;
+        kb.g = lay;
+        kb.nb = nb;
+        SoaSrc<KeyRangeBin> src{keys, pay, kb};
+        return run_partition_fast(src, nk, nb, reinterpret_cast<ulonglong2 *>(pairs_out), starts_out, ws, pws, st);
+    }
     PosBin f;
     f.m = SplineDev(idx->model);
     f.nb = hash_bins(idx->model.n);
@@ -296,6 +396,50 @@ int lj_spline_hash_probe_grouped(const LjSplineHash *idx, const uint64_t *s_pair
     constexpr int NT = 256;
     k_hash_probe<NT, 4, HashAos, true><<<grid_for((nk + 3) / 4, NT, 8), NT, 0, st>>>(
         HashDev(*idx), HashAos{reinterpret_cast<const ulonglong2 *>(s_pairs)}, nk, out);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+int64_t lj_spline_hash_bucket_bins(int64_t n) { return hash_bins(n); }
+
+int64_t lj_spline_hash_bucket_capacity(int64_t nk, int64_t n) { return est_capacity(nk < 0 ? 0 : nk, hash_bins(n)); }
+
+size_t lj_spline_hash_bucket_est_workspace_bytes(int64_t nk, int64_t n) {
+    (void)nk;
+    return est_workspace_bytes(hash_bins(n));
+}
+
+int lj_spline_hash_bucket_est(const LjSplineHash *idx, const uint64_t *keys, const uint64_t *pay, int64_t nk,
+                              uint64_t *pairs_out, int64_t *reg_out, void *ws, size_t ws_bytes, void *stream) {
+    LJ_REQUIRE(idx && idx->n >= 1, "index is empty");
+    LJ_REQUIRE(((uintptr_t)keys & 15) == 0 && ((uintptr_t)pay & 15) == 0, "key/payload columns must be 16-B aligned");
+    cudaStream_t st = as_stream(stream);
+    PosBin f;
+    f.m = SplineDev(idx->model);
+    f.nb = hash_bins(idx->model.n);
+    f.n = idx->model.n;
+    f.rn = (double)f.nb / (double)idx->model.n;
+    SoaSrc<PosBin> src{keys, pay, f};
+    const int rc = run_partition_est(src, nk, (int)f.nb, reinterpret_cast<ulonglong2 *>(pairs_out), reg_out, ws,
+                                     ws_bytes, st);
+    if (rc) return rc;
+    k_fill_gaps<<<(unsigned)f.nb, 256, 0, st>>>(reg_out, (int)f.nb, reinterpret_cast<ulonglong2 *>(pairs_out));
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+int lj_spline_hash_probe_regions(const LjSplineHash *idx, const uint64_t *s_pairs, const int64_t *reg, int64_t nbins,
+                                 void *ws, size_t ws_bytes, uint64_t *out, int accumulate, void *stream) {
+    LJ_REQUIRE(idx != nullptr && reg != nullptr, "null index or regions");
+    LJ_REQUIRE(ws != nullptr && ws_bytes >= 8, "workspace too small");
+    cudaStream_t st = as_stream(stream);
+    if (!accumulate) LJ_CK(cudaMemsetAsync(out, 0, 4 * sizeof(u64), st));
+    if (idx->n == 0) return LJ_OK;
+    unsigned long long *ctr = reinterpret_cast<unsigned long long *>(ws);
+    LJ_CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
+    constexpr int NT = 256;
+    k_hash_probe_chunks<NT, 4, 8><<<sm_count() * 3, NT, 0, st>>>(
+        HashDev(*idx), reinterpret_cast<const ulonglong2 *>(s_pairs), reg, (int)nbins, ctr, out);
     LJ_CK_LAUNCH();
     return LJ_OK;
 }

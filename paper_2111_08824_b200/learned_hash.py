@@ -102,9 +102,12 @@ class SplineHashIndex:
     def bucket_scratch(self, n: int, device=None) -> dict:
         lib = _lib.lib()
         dev = device or self.entries.device
-        return {"pairs": torch.empty(2 * max(n, 1), dtype=torch.int64, device=dev),
-                "starts": torch.empty(2049, dtype=torch.int64, device=dev),
-                "ws": _lib.workspace(lib.lj_spline_hash_bucket_workspace_bytes(n, self.model.trained_len), dev)}
+        tl = self.model.trained_len
+        cap = lib.lj_spline_hash_bucket_capacity(n, tl)
+        nb = lib.lj_spline_hash_bucket_bins(tl)
+        return {"pairs": torch.empty(2 * max(cap, 1), dtype=torch.int64, device=dev),
+                "reg": torch.empty(2 * nb + 2, dtype=torch.int64, device=dev), "nbins": nb,
+                "ws": _lib.workspace(max(lib.lj_spline_hash_bucket_est_workspace_bytes(n, tl), 8), dev)}
 
     def join_checksum_buffered(self, s_keys: torch.Tensor, s_payloads: torch.Tensor,
                                out: torch.Tensor | None = None, accumulate: bool = False, scratch: dict | None = None,
@@ -125,20 +128,27 @@ class SplineHashIndex:
         return out
 
     def bucket_records(self, s_keys: torch.Tensor, s_payloads: torch.Tensor, scratch: dict, stream=None) -> None:
-        """S grouped by predicted-position window into scratch["pairs"]."""
+        """S grouped by approximate-position window into scratch["pairs"]
+        (one pass, estimated-capacity regions; scratch["reg"] = layout)."""
         lib = _lib.lib()
         c = self.c_struct()
         ws = scratch["ws"]
-        _lib.check(lib.lj_spline_hash_bucket(ctypes.byref(c), _lib.ptr(s_keys), _lib.ptr(s_payloads), s_keys.numel(),
-                                             _lib.ptr(scratch["pairs"]), _lib.ptr(scratch["starts"]), _lib.ptr(ws),
-                                             ws.numel(), _lib.stream_ptr(stream)), "spline_hash_bucket")
+        if s_keys.data_ptr() % 16 or s_payloads.data_ptr() % 16:
+            s_keys, s_payloads = s_keys.clone(), s_payloads.clone()
+        _lib.check(lib.lj_spline_hash_bucket_est(ctypes.byref(c), _lib.ptr(s_keys), _lib.ptr(s_payloads),
+                                                 s_keys.numel(), _lib.ptr(scratch["pairs"]), _lib.ptr(scratch["reg"]),
+                                                 _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream)),
+                   "spline_hash_bucket_est")
 
     def probe_records(self, n: int, scratch: dict, out: torch.Tensor, accumulate: bool = False, stream=None) -> None:
-        """K5 over the n grouped records bucket_records left in scratch."""
+        """K5 over the grouped records bucket_records left in scratch (n is
+        implied by the regions)."""
         c = self.c_struct()
-        _lib.check(_lib.lib().lj_spline_hash_probe_grouped(ctypes.byref(c), _lib.ptr(scratch["pairs"]), n,
-                                                           _lib.ptr(out), int(bool(accumulate)),
-                                                           _lib.stream_ptr(stream)), "spline_hash_probe_grouped")
+        ws = scratch["ws"]
+        _lib.check(_lib.lib().lj_spline_hash_probe_regions(ctypes.byref(c), _lib.ptr(scratch["pairs"]),
+                                                           _lib.ptr(scratch["reg"]), scratch["nbins"], _lib.ptr(ws),
+                                                           ws.numel(), _lib.ptr(out), int(bool(accumulate)),
+                                                           _lib.stream_ptr(stream)), "spline_hash_probe_regions")
         return out
 
     def probe_batch(self, keys):

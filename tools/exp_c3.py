@@ -65,13 +65,18 @@ def main():
     n_s = len(inp.s)
     scratch = idx.bucket_scratch(n_s)
     res = {}
-    for g in (128, 64, 32):
-        res[f"l2fetch_{g}"] = set_l2_fetch(g)
+    for g in (128,):
         res[f"direct_{g}"] = timeit(lambda: idx.join_checksum(keys, pays, out=out), flush)
         res[f"bucket_{g}"] = timeit(lambda: idx.bucket_records(keys, pays, scratch), flush)
         res[f"grouped_probe_{g}"] = timeit(lambda: idx.probe_records(n_s, scratch, out), flush)
         print(json.dumps(res), flush=True)
-    set_l2_fetch(128)
+    o1 = torch.zeros(4, dtype=torch.int64, device="cuda")
+    o2 = torch.zeros(4, dtype=torch.int64, device="cuda")
+    idx.join_checksum(keys, pays, out=o1)
+    idx.bucket_records(keys, pays, scratch)
+    idx.probe_records(n_s, scratch, o2)
+    res["direct_words"] = o1.tolist()
+    res["grouped_words"] = o2.tolist()
     print(json.dumps(res), flush=True)
 
 
