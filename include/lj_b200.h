@@ -305,6 +305,15 @@ int lj_lsj_bins_from_bounds(const int64_t *pb, int64_t nbins, int64_t trained_le
 size_t lj_lsj_partition_workspace_bytes(int64_t n, int64_t nbins);
 int lj_lsj_partition(const LjLsjModel *model, const uint64_t *keys, const uint64_t *pay, int64_t n,
                      uint64_t *pairs, int64_t *starts, void *ws, size_t ws_bytes, void *stream);
+/* The exact key-range bin function the partition passes evaluate in
+ * shared memory (lj_keybin.cuh): bins[i] = #{ j in [1, nbins) :
+ * bounds[j] <= keys[i] } for non-decreasing bounds (bounds[0] ignored).
+ * lj_lsj_key_bounds: the model's bins as key boundaries (bounds[j] = first
+ * key whose predicted position reaches pb[j]).  ws >= lj_keybin_workspace_bytes. */
+size_t lj_keybin_workspace_bytes(int64_t nbins);
+int lj_keybin_eval(const uint64_t *bounds, int64_t nbins, const uint64_t *keys, int64_t nk, uint32_t *bins,
+                   void *ws, size_t ws_bytes, void *stream);
+int lj_lsj_key_bounds(const LjLsjModel *model, uint64_t *bounds, void *ws, size_t ws_bytes, void *stream);
 /* lsj.py:242-286 per-bucket sort (K8, model-placed, shared memory) from the
  * partitioned pairs_in into pairs_out (fully sorted, bucket ranges kept).
  * stats_host[4] = {oversized buckets, bitonic fallbacks, sub-buckets above

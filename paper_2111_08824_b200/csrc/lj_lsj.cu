@@ -34,6 +34,7 @@
 
 #include "lj_common.cuh"
 #include "lj_keybin.cuh"
+#include "lj_pipe.cuh"
 #include "lj_part.cuh"
 #include "lj_part_est.cuh"
 
@@ -548,14 +549,23 @@ __global__ void __launch_bounds__(SORT_NT, 2) k_lsj_sort(LsjDev md, Src src, con
     u16 *idx = slot + CAP;                                // placement [CAP]
     u16 *ord = idx + CAP;                                 // final order [CAP]
     __shared__ u32 warp_tot[SORT_NT / 32];
-    __shared__ i64 s_b;
+    __shared__ i64 s_b, s_bn;
     __shared__ int s_bad, s_nruns;
     __shared__ int2 s_runs[MAX_RUNS];
+    if (threadIdx.x == 0) s_bn = (i64)atomicAdd(&ctl->next, 1ULL);
     for (;;) {
         if (threadIdx.x == 0) {
-            s_b = (i64)atomicAdd(&ctl->next, 1ULL);
+            // take the bucket claimed one round ago and claim the next one,
+            // whose tuples stream into L2 (bulk prefetch) while this one sorts
+            s_b = s_bn;
+            s_bn = (i64)atomicAdd(&ctl->next, 1ULL);
             s_bad = 0;
             s_nruns = 0;
+            if (s_bn < nbuckets) {
+                const Bucket nx = src.get(s_bn);
+                if (!nx.point && nx.m > 1 && nx.m <= (i64)CAP)
+                    bulk_prefetch_l2(in + nx.in_base, (unsigned)(nx.m * sizeof(ulonglong2)));
+            }
         }
         __syncthreads();
         const i64 b = s_b;
@@ -816,6 +826,13 @@ __global__ void __launch_bounds__(JOIN_NT) k_lsj_join(const ulonglong2 *__restri
         const int ne = (int)(e - a);
         const i64 wlo = tb[2 * tile], whi = tb[2 * tile + 1], w = whi - wlo;
         const bool staged = w <= WCAP;
+        if (threadIdx.x == 0 && tile + gridDim.x < ntiles) {
+            // this CTA's next tile streams into L2 while this one merges
+            const i64 nt = tile + gridDim.x, na = nt * JOIN_T, nn = min((i64)JOIN_T, ns - na);
+            const i64 nlo = tb[2 * nt], nw = tb[2 * nt + 1] - nlo;
+            bulk_prefetch_l2(S + na, (unsigned)(nn * sizeof(ulonglong2)));
+            if (nw > 0 && nw <= WCAP) bulk_prefetch_l2(R + nlo, (unsigned)(nw * sizeof(ulonglong2)));
+        }
         if (staged) {
             for (int j = threadIdx.x; j < (int)w; j += JOIN_NT) wk[j] = R[wlo + j].x;
             if (threadIdx.x == 0) wk[w] = ~0ULL;  // sentinel above every key
@@ -961,6 +978,62 @@ int lj_lsj_bins(const LjRmi *model, const uint64_t *sample_sorted, int64_t total
 int lj_lsj_bins_from_bounds(const int64_t *pb, int64_t nbins, int64_t trained_len, uint32_t *table, void *stream) {
     LJ_REQUIRE(nbins >= 1 && nbins <= PART2_MAXBINS && trained_len >= 1, "bad bins");
     k_bin_table<<<grid_for(trained_len, 256, 8), 256, 0, as_stream(stream)>>>(pb, (int)nbins, trained_len, table);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+// ---- the key-range bin structure on its own (tests: exactness against a
+// plain search / the model's bins on arbitrary keys)
+static __global__ void k_keybin_eval(KeyRangeBin kb, const u64 *keys, i64 nk, u32 *bins) {
+    extern __shared__ __align__(16) u64 kb_s[];
+    kb.stage(kb_s);
+    __syncthreads();
+    const KeyRangeBin f = kb.at(kb_s);
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < nk; i += (i64)gridDim.x * blockDim.x)
+        bins[i] = f.code(keys[i]);
+}
+
+static __global__ void k_copy_bounds(const u64 *bounds, int nb, u64 *lay) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nb; j += gridDim.x * blockDim.x)
+        lay[4 + j] = j ? bounds[j] : 0;
+}
+
+static __global__ void k_read_bounds(const u64 *lay, int nb, u64 *bounds) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nb; j += gridDim.x * blockDim.x)
+        bounds[j] = j ? lay[4 + j] : 0;
+}
+
+size_t lj_keybin_workspace_bytes(int64_t nbins) { return kb_bytes((int)nbins); }
+
+int lj_keybin_eval(const uint64_t *bounds, int64_t nbins, const uint64_t *keys, int64_t nk, uint32_t *bins, void *ws,
+                   size_t ws_bytes, void *stream) {
+    LJ_REQUIRE(nbins >= 1 && nbins <= KB_MAXBINS, "need 1 <= nbins <= 2048");
+    LJ_REQUIRE(ws_bytes >= kb_bytes((int)nbins), "workspace too small");
+    cudaStream_t st = as_stream(stream);
+    u64 *lay = (u64 *)ws;
+    const int nb = (int)nbins;
+    k_copy_bounds<<<(nb + 255) / 256, 256, 0, st>>>(bounds, nb, lay);
+    k_keybin_build<<<1, 1024, 0, st>>>(lay, nb);
+    LJ_CK_LAUNCH();
+    if (nk > 0) {
+        KeyRangeBin kb;
+        kb.g = lay;
+        kb.nb = nb;
+        k_keybin_eval<<<grid_for(nk, 256, 4), 256, kb_bytes(nb), st>>>(kb, keys, nk, bins);
+        LJ_CK_LAUNCH();
+    }
+    return LJ_OK;
+}
+
+int lj_lsj_key_bounds(const LjLsjModel *md, uint64_t *bounds, void *ws, size_t ws_bytes, void *stream) {
+    LJ_REQUIRE(md && md->pb && md->nbins >= 1 && md->nbins <= KB_MAXBINS, "model has no bins (or > 2048)");
+    LJ_REQUIRE(ws_bytes >= kb_bytes((int)md->nbins), "workspace too small");
+    cudaStream_t st = as_stream(stream);
+    const int nb = (int)md->nbins;
+    u64 *lay = (u64 *)ws;
+    k_lsj_key_bounds<<<(nb + 127) / 128, 128, 0, st>>>(make_lsj(*md), lay);
+    k_keybin_build<<<1, 1024, 0, st>>>(lay, nb);
+    k_read_bounds<<<(nb + 255) / 256, 256, 0, st>>>(lay, nb, bounds);
     LJ_CK_LAUNCH();
     return LJ_OK;
 }

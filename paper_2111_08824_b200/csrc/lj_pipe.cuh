@@ -60,6 +60,12 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
         : "memory");
 }
 
+// bulk prefetch of [src, src + bytes) into L2 (bytes multiple of 16, src
+// 16-B aligned)
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 }  // namespace lj
 
 namespace lj {

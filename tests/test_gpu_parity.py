@@ -1,6 +1,8 @@
 """GPU parity: the CUDA path against the reference's golden vectors and the
 C oracle, through the C ABI.  Bit-exact for every integer output."""
 
+import ctypes
+
 import numpy as np
 import pytest
 import torch
@@ -448,3 +450,77 @@ def test_key_file_roundtrip_to_device_and_canonical(lj, tmp_path):
     assert np.array_equal(res.canonical(), want)
     dr, ds = res.canonical_device()
     assert np.array_equal(np.column_stack((_np(dr), _np(ds))), want)
+
+
+# ---- the key-range bin structure (lj_keybin.cuh) the partition passes use
+
+
+def _keybin(bounds, keys):
+    from paper_2111_08824_b200 import _lib
+
+    lib = _lib.lib()
+    nb = len(bounds)
+    b = torch.from_numpy(np.ascontiguousarray(bounds, np.uint64).view(np.int64)).cuda()
+    k = torch.from_numpy(np.ascontiguousarray(keys, np.uint64).view(np.int64)).cuda()
+    out = torch.empty(max(len(keys), 1), dtype=torch.int32, device="cuda")
+    ws = _lib.workspace(lib.lj_keybin_workspace_bytes(nb))
+    _lib.check(lib.lj_keybin_eval(_lib.ptr(b), nb, _lib.ptr(k), len(keys), _lib.ptr(out), _lib.ptr(ws), ws.numel(),
+                                  _lib.stream_ptr()), "keybin_eval")
+    return out[: len(keys)].cpu().numpy().astype(np.int64)
+
+
+def _dist_keys(rng, dist, n):
+    if dist == "uniform":
+        return rng.integers(0, 2**63, n, dtype=np.uint64)
+    if dist == "lognormal":
+        return np.floor(1e12 * rng.lognormal(0, 2, n)).astype(np.uint64)
+    if dist == "clusters":
+        c = rng.integers(0, 2**62, 64).astype(np.float64)
+        return np.clip(c[rng.integers(0, 64, n)] + rng.normal(0, 2.0**40, n), 0, 2.0**63 - 4096).astype(np.uint64)
+    if dist == "dups":
+        return rng.integers(0, 50, n, dtype=np.uint64) * np.uint64(1 << 40)
+    if dist == "dense":
+        return rng.integers(10**6, 10**6 + 5000, n, dtype=np.uint64)
+    return np.uint64(2**64 - 2) - rng.integers(0, 10**6, n, dtype=np.uint64)  # "top" of the key space
+
+
+@pytest.mark.parametrize("dist", ["uniform", "lognormal", "clusters", "dups", "dense", "top"])
+@pytest.mark.parametrize("nb", [1, 2, 37, 2048])
+def test_keybin_matches_search(lj, dist, nb):
+    """bin(k) = #{ j >= 1 : B[j] <= k } exactly, whichever key image the
+    table picks, on boundaries drawn from the distribution (repeats and all)
+    and keys on, next to and between them."""
+    rng = np.random.default_rng(nb * 7 + len(dist))
+    bounds = np.sort(_dist_keys(rng, dist, nb))
+    bounds[0] = 0
+    inner = bounds[1:]
+    keys = np.concatenate([_dist_keys(rng, dist, 20000), inner, inner - np.minimum(inner, 1),
+                           np.minimum(inner, np.uint64(2**64 - 3)) + np.uint64(1),
+                           np.array([0, 1, 2**63 - 1, 2**63, 2**64 - 2], dtype=np.uint64)])
+    want = np.searchsorted(inner, keys, side="right")
+    assert np.array_equal(_keybin(bounds, keys), want)
+
+
+@pytest.mark.parametrize("dist", ["uniform", "lognormal", "clusters", "dense"])
+def test_lsj_key_bounds_equal_model_bins(lj, dist):
+    """The partition's key-range bins are the model's bins table[pos(key)]
+    on every key (sample keys, draws, boundaries and their neighbours)."""
+    from paper_2111_08824_b200 import _lib, lsj
+
+    rng = np.random.default_rng(11)
+    rk = np.unique(_dist_keys(rng, dist, 300000))
+    r = lj.make_relation(rk, 3)
+    _, lm = lsj.prepare_model(r, 0.01, 5)
+    lib = _lib.lib()
+    bounds = torch.empty(lm.nbins, dtype=torch.int64, device="cuda")
+    ws = _lib.workspace(lib.lj_keybin_workspace_bytes(lm.nbins))
+    c = lm.c_struct()
+    _lib.check(lib.lj_lsj_key_bounds(ctypes.byref(c), _lib.ptr(bounds), _lib.ptr(ws), ws.numel(), _lib.stream_ptr()),
+               "lsj_key_bounds")
+    b = _np(bounds)
+    inner = b[1:]
+    keys = np.concatenate([rk, _dist_keys(rng, dist, 50000), inner, inner - np.minimum(inner, 1),
+                           np.array([0, 1, 2**63 - 1], dtype=np.uint64)])
+    pos = lm.rmi.predict_many(keys)[0]
+    model_bins = lm.table.long()[pos].cpu().numpy()
+    assert np.array_equal(_keybin(b, keys), model_bins)
