@@ -150,9 +150,11 @@ def make_step(inp, index, variant="buffered"):
             parts = [("bucket", lambda out: index.bucket_records(keys, pays, scratch)),
                      ("probe", lambda out: index.probe_records(n_s, scratch, out))]
             kern = "k_grmi_probe_staged" if grmi else "k_hash_probe_chunks"
-            return Step(parts, "probe", 32 * n_s, kern,
-                        f"32 B/probe x {n_s} probes (16 B S record + 16 B R entry); the one-pass bucketing "
-                        "(k_est_sample + k_bin_scatter_est) runs before it in the step")
+            st = Step(parts, "probe", 32 * n_s, kern,
+                      f"32 B/probe x {n_s} probes (16 B S record + 16 B R entry); the one-pass bucketing "
+                      "(k_est_sample + k_bin_scatter_est) runs before it in the step")
+            st.scratch = scratch  # reused by the e2e leg (C3's is ~66 GB)
+            return st
         fn = (lambda out: index.join_checksum(keys, pays, out=out))
         return Step([("probe", fn)], "probe", 32 * n_s, "k_grmi_probe" if grmi else "k_hash_probe",
                     f"32 B/probe x {n_s} probes (16 B S record + 16 B R entry)")
@@ -386,7 +388,7 @@ def run_b200(args):
 
     e2e = None
     if not args.no_e2e:
-        e2e = _e2e(args, inp, index, world)
+        e2e = _e2e(args, inp, index, world, run_step)
     line = None
     if rank == 0:
         cpu = None
@@ -407,7 +409,7 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
-def _e2e(args, inp, index, world):
+def _e2e(args, inp, index, world, run_step=None):
     """Same metric through the public API from pinned HOST buffers: every
     step copies S (INLJ) or R and S (LSJ) host->device into a validated
     Relation, runs the join and reads the 3-word result back."""
@@ -424,7 +426,7 @@ def _e2e(args, inp, index, world):
         h2d += 16 * len(inp.r)
         o = dict(lj.DEFAULT_OPTS, **inp.opts)
         cfg = lj.LsjConfig(workers=1, fanout=o["fanout"], sample_rate=o["sample_rate"], seed=o["seed"])
-    scratch = index.bucket_scratch(len(inp.s)) if (index is not None and args.variant == "buffered") else None
+    scratch = getattr(run_step, "scratch", None) if (index is not None and args.variant == "buffered") else None
     steps = max(1, min(args.steps, 3))
     times = []
     for i in range(steps + 1):

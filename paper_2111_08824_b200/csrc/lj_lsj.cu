@@ -821,17 +821,27 @@ __global__ void __launch_bounds__(JOIN_NT) k_lsj_join(const ulonglong2 *__restri
     __shared__ u64 sk[JOIN_T], sp[JOIN_T];
     u64 cnt = 0, sum = 0, x = 0;
     const i64 ntiles = (ns + JOIN_T - 1) / JOIN_T;
+    // the next tile's R range is loaded one tile ahead (its latency would
+    // otherwise open every tile), and its S tile and R range stream into L2
+    // (bulk prefetch) while this tile merges
+    i64 nlo = 0, nhi = 0;
+    if (blockIdx.x < ntiles) {
+        nlo = tb[2 * blockIdx.x];
+        nhi = tb[2 * blockIdx.x + 1];
+    }
     for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const i64 a = tile * JOIN_T, e = min(a + (i64)JOIN_T, ns);
         const int ne = (int)(e - a);
-        const i64 wlo = tb[2 * tile], whi = tb[2 * tile + 1], w = whi - wlo;
+        const i64 wlo = nlo, whi = nhi, w = whi - wlo;
         const bool staged = w <= WCAP;
-        if (threadIdx.x == 0 && tile + gridDim.x < ntiles) {
-            // this CTA's next tile streams into L2 while this one merges
-            const i64 nt = tile + gridDim.x, na = nt * JOIN_T, nn = min((i64)JOIN_T, ns - na);
-            const i64 nlo = tb[2 * nt], nw = tb[2 * nt + 1] - nlo;
-            bulk_prefetch_l2(S + na, (unsigned)(nn * sizeof(ulonglong2)));
-            if (nw > 0 && nw <= WCAP) bulk_prefetch_l2(R + nlo, (unsigned)(nw * sizeof(ulonglong2)));
+        const i64 nt = tile + gridDim.x;
+        if (nt < ntiles) {
+            nlo = tb[2 * nt];
+            nhi = tb[2 * nt + 1];
+            if (threadIdx.x == 0) {
+                const i64 na = nt * JOIN_T, nn = min((i64)JOIN_T, ns - na);
+                bulk_prefetch_l2(S + na, (unsigned)(nn * sizeof(ulonglong2)));
+            }
         }
         if (staged) {
             for (int j = threadIdx.x; j < (int)w; j += JOIN_NT) wk[j] = R[wlo + j].x;
@@ -878,6 +888,8 @@ __global__ void __launch_bounds__(JOIN_NT) k_lsj_join(const ulonglong2 *__restri
             }
             if (mode == 1) counts[i] = c;
         }
+        if (threadIdx.x == 0 && nt < ntiles && nhi - nlo > 0 && nhi - nlo <= WCAP)
+            bulk_prefetch_l2(R + nlo, (unsigned)((nhi - nlo) * sizeof(ulonglong2)));
         __syncthreads();
     }
     if (mode == 0) reduce_checksum(cnt, sum, x, 0, out);

@@ -438,7 +438,8 @@ int lj_spline_hash_probe_regions(const LjSplineHash *idx, const uint64_t *s_pair
     unsigned long long *ctr = reinterpret_cast<unsigned long long *>(ws);
     LJ_CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
     constexpr int NT = 256;
-    k_hash_probe_chunks<NT, 4, 8><<<sm_count() * 3, NT, 0, st>>>(
+    static const int per_sm = getenv("LJ_HASH_CTAS") ? atoi(getenv("LJ_HASH_CTAS")) : 4;
+    k_hash_probe_chunks<NT, 4, 8><<<sm_count() * per_sm, NT, 0, st>>>(
         HashDev(*idx), reinterpret_cast<const ulonglong2 *>(s_pairs), reg, (int)nbins, ctr, out);
     LJ_CK_LAUNCH();
     return LJ_OK;

@@ -1,0 +1,3 @@
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python tools/lsj_phases.py c4 > gpurun_out/lsj_phases14.log 2>&1
+for c in 3 4 6; do LJ_HASH_CTAS=$c timeout 900 python tools/exp_c3.py > gpurun_out/exp_c3_14_$c.log 2>&1; done
