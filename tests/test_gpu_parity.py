@@ -524,3 +524,25 @@ def test_lsj_key_bounds_equal_model_bins(lj, dist):
     pos = lm.rmi.predict_many(keys)[0]
     model_bins = lm.table.long()[pos].cpu().numpy()
     assert np.array_equal(_keybin(b, keys), model_bins)
+
+
+@pytest.mark.parametrize("buffered", [True, False])
+def test_join_checksum_host_streams_chunks(lj, buffered):
+    """Host-resident S streamed in chunks (copies overlapped with the join)
+    gives the same words as the device-resident join; the reserved key is
+    rejected."""
+    rng = np.random.default_rng(21)
+    rk = np.unique(rng.integers(0, 2**63, 50000, dtype=np.uint64))
+    sk = np.concatenate([rng.choice(rk, 90000), rng.integers(0, 2**63, 7000, dtype=np.uint64)])
+    r = lj.make_relation(rk, 1)
+    s = lj.make_relation(sk, 2)
+    hk, hp = s.keys.cpu(), s.payloads.cpu()
+    for idx in (lj.GappedRmiIndex(2.0, 256).fit(r), lj.SplineHashIndex(32, 18, 4.0).fit(r)):
+        want = idx.join_checksum(s.keys, s.payloads).cpu().tolist()
+        for chunk in (1000, 33333, 1 << 20):
+            got = lj.join_checksum_host(idx, hk, hp, buffered=buffered, chunk=chunk).cpu().tolist()
+            assert got == want, (type(idx).__name__, chunk)
+    bad = hk.clone()
+    bad[500] = -1
+    with pytest.raises(ValueError):
+        lj.join_checksum_host(idx, bad, hp, buffered=buffered, chunk=1000)
