@@ -40,12 +40,16 @@
 
 namespace lj {
 
-constexpr int SORT_NT = 512;     // two sort CTAs per SM (their barrier waits overlap)
-constexpr int CAP = 6144;         // largest bucket sorted in shared memory (108 KB per CTA)
+#ifndef LJ_SORT_CTAS
+#define LJ_SORT_CTAS 4
+#endif
+constexpr int SORT_CTAS = LJ_SORT_CTAS;  // sort CTAs per SM (their barrier waits overlap)
+constexpr int SORT_NT = 1024 / SORT_CTAS;
+constexpr int CAP = 12288 / SORT_CTAS;    // largest bucket sorted in shared memory (216 KB per SM)
 constexpr int RUN_SMALL = 64;     // equal-slot runs ranked element by element
 constexpr int MAX_RUNS = 64;      // longer mixed runs sorted block-wide per bucket
 constexpr int SORT_U = 4;         // tuples in flight per thread in the load / write-out phases
-constexpr int SUB = 3072;         // mean tuples per sub-bucket: sample-quantile slices
+constexpr int SUB = CAP / 2;      // mean tuples per sub-bucket: sample-quantile slices
                                   // (~61 sample keys each) stay below CAP
 constexpr int SPLIT_NT = 1024;
 constexpr int SPLIT_U = 4;        // tuple groups in flight per warp step
@@ -538,7 +542,7 @@ __device__ void block_sort_idx(u16 *idx, int base, int len, const u64 *K) {
 
 // K8: one CTA per bucket (dynamic work counter), model-placed in smem.
 template <class Src>
-__global__ void __launch_bounds__(SORT_NT, 2) k_lsj_sort(LsjDev md, Src src, const i64 *nbuckets_dev,
+__global__ void __launch_bounds__(SORT_NT, SORT_CTAS) k_lsj_sort(LsjDev md, Src src, const i64 *nbuckets_dev,
                                                          const ulonglong2 *__restrict__ in, ulonglong2 *out,
                                                          SortCtl *ctl, i64 *over_list) {
     const i64 nbuckets = *nbuckets_dev;
@@ -926,7 +930,7 @@ static int launch_sort(const LsjDev &md, const Src &src, const i64 *nb_dev, cons
         attr = true;
     }
     LJ_CK(cudaMemsetAsync(ctl, 0, sizeof(SortCtl), st));
-    k_lsj_sort<Src><<<sm_count() * 2, SORT_NT, sort_smem_bytes(), st>>>(md, src, nb_dev, in, out, ctl, over);
+    k_lsj_sort<Src><<<sm_count() * SORT_CTAS, SORT_NT, sort_smem_bytes(), st>>>(md, src, nb_dev, in, out, ctl, over);
     LJ_CK_LAUNCH();
     return LJ_OK;
 }
