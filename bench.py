@@ -99,10 +99,24 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def make_inputs(cfg: str, shard: int = 0):
+# configs whose relations are split across the ranks (BASELINE: C3's S is
+# sharded with R replicated; C5 range-shuffles both); the others run one
+# full-size workload per GPU (weak scaling)
+SHARDED = {"c3": ("s",), "c5": ("r", "s")}
+
+
+def make_inputs(cfg: str, shard: int = 0, shards: int = 1, scale=None):
+    import inspect
+
     from paper_2111_08824_b200 import configs
 
-    return configs.CONFIGS[cfg](shard=shard)
+    fn = configs.CONFIGS[cfg]
+    kw = {"shard": shard}
+    if "shards" in inspect.signature(fn).parameters:
+        kw["shards"] = shards
+    if scale is not None:
+        kw["scale"] = scale
+    return fn(**kw)
 
 
 def build_index(inp):
@@ -135,10 +149,12 @@ class Step:
         return out
 
 
-def make_step(inp, index, variant="buffered"):
+def make_step(inp, index, variant="buffered", world: int = 1, distributed: bool = False):
     """A step is one pass of the hot path over the whole S (INLJ, index
     prebuilt as in the reference, bench.py:138-144 of the reference) or the
     whole LSJ (sample, fit, partition, sort, join)."""
+    import torch
+
     import paper_2111_08824_b200 as lj
 
     n_r, n_s = len(inp.r), len(inp.s)
@@ -161,6 +177,24 @@ def make_step(inp, index, variant="buffered"):
     o = dict(lj.DEFAULT_OPTS, **inp.opts)
     cfg = lj.LsjConfig(workers=1, fanout=o["fanout"], sample_rate=o["sample_rate"], seed=o["seed"])
     holder = {}
+    if distributed:
+        # C5 across GPUs: shared model, range shuffle (NCCL all-to-all-v),
+        # local LSJ, 3-word reduction (dist.lsj_join); the words come back
+        # reduced on every rank
+        from paper_2111_08824_b200 import dist as ljdist
+
+        def dist_step(out):
+            (c, sm, x), ph = ljdist.lsj_join(inp.r.keys, inp.r.payloads, inp.s.keys, inp.s.payloads, cfg)
+            holder["phases"] = ph
+            sg = [v - (1 << 64) if v >= (1 << 63) else v for v in (c, sm, x, 0)]
+            out.copy_(torch.tensor(sg, dtype=torch.int64))
+            return out
+
+        st = Step([("lsj", dist_step)], "lsj", 80 * (n_r + n_s), "distributed LSJ step (partition, all-to-all, "
+                  "local LSJ)", f"80 B/tuple x {n_r + n_s} local tuples (partition 32, sort 32, merge 16)")
+        st.holder = holder
+        st.reduced = True
+        return st
 
     def lsj_step(out):
         res, br = lj.lsj_join(inp.r, inp.s, cfg)
@@ -296,7 +330,17 @@ def _config_block(args, inp):
     return {"workload": f"{args.config}: {inp.description}", "algorithm": inp.algorithm,
             "variant": getattr(args, "variant", None) if inp.algorithm != "lsj" else None,
             "n_r": len(inp.r), "n_s": len(inp.s), "l2": "inputs larger than L2 and L2 flushed between steps",
-            "parallelism": f"inlj-replicated-R x{args.gpus}"}
+            "parallelism": _parallelism(args.config, inp.algorithm, args.gpus)}
+
+
+def _parallelism(cfg, algorithm, n):
+    if cfg == "c5":
+        return f"lsj range shuffle over {n} GPU(s): shared model, NCCL all-to-all-v, local LSJ"
+    if algorithm == "lsj":
+        return f"lsj replicas x{n} (one full join per GPU)"
+    if cfg in SHARDED:
+        return f"inlj replicated R, S sharded 1/{n} per GPU"
+    return f"inlj replicated R, full S per GPU x{n}"
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -308,21 +352,35 @@ def run_b200(args):
 
     rank, world, local = _env_rank()
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    inp = make_inputs(args.config, shard=rank)
+    use_pg = world > 1 or args.config == "c5"  # C5 always runs the distributed LSJ
+    if use_pg:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local), rank=rank, world_size=world)
+    inp = make_inputs(args.config, shard=rank, shards=world, scale=args.scale)
     index = build_index(inp)
     dev = torch.device("cuda", local)
     variant = args.variant or DEFAULT_VARIANT.get(args.config, "direct")
     args.variant = variant
-    run_step = make_step(inp, index, variant)
+    run_step = make_step(inp, index, variant, world, distributed=args.config == "c5")
+    reduced = getattr(run_step, "reduced", False)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     out = torch.zeros(4, dtype=torch.int64, device=dev)
     xors = torch.zeros(world, dtype=torch.int64, device=dev)
+    # whole-job tuples: sharded relations summed over the ranks, replicated
+    # ones counted once (R of C3), per-GPU workloads N times (weak scaling)
+    sizes = torch.tensor([len(inp.r), len(inp.s)], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(sizes)
+    sh = SHARDED.get(args.config, ())
+    job_r = int(sizes[0]) if "r" in sh else (len(inp.r) if index is not None else world * len(inp.r))
+    job_s = int(sizes[1]) if "s" in sh else world * len(inp.s)
+    args.scaling = "strong" if sh else "weak"
+    args.job_tuples = job_r + job_s
 
     def step():
         run_step(out)
-        if world > 1:
+        if world > 1 and not reduced:
             dist.all_gather_into_tensor(xors, out[2:3].contiguous())
             dist.all_reduce(out, op=dist.ReduceOp.SUM)  # count, sum, steps (wrap mod 2^64)
 
@@ -348,10 +406,10 @@ def run_b200(args):
         dist.all_reduce(total, op=dist.ReduceOp.MAX)
     ms_per_step = float(total.item()) / args.steps
     n_r, n_s = len(inp.r), len(inp.s)
-    value = (n_r + world * n_s) / (ms_per_step / 1e3)
+    value = (job_r + job_s) / (ms_per_step / 1e3)
     w = out.cpu().tolist()
     xor_all = 0
-    if world > 1:
+    if world > 1 and not reduced:
         for v in xors.cpu().tolist():
             xor_all ^= v & (2**64 - 1)
     else:
@@ -399,13 +457,13 @@ def run_b200(args):
                 cpu = {"error": repr(exc)}
         line = {"metric": "join tuples/s ((|R|+|S|)/time)", "value": value, "unit": "tuples/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+                "scaling": args.scaling, "vs_baseline": None, "dtype": "u64", "data": "synthetic",
                 "config": _config_block(args, inp), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": (launches * args.steps) if launches is not None else None,
                 "clocks": clk.summary(),
                 "checksum": {"count": w[0], "sum": w[1] & (2**64 - 1), "xor": xor_all, "search_steps": w[3]}}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_pg:
         dist.destroy_process_group()
 
 
@@ -435,7 +493,13 @@ def _e2e(args, inp, index, world, run_step=None):
         if index is None:
             s = lj.Relation(hk.to("cuda", non_blocking=True), hp.to("cuda", non_blocking=True), validate=True)
             r = lj.Relation(rk.to("cuda", non_blocking=True), rp.to("cuda", non_blocking=True), validate=True)
-            res, _ = lj.lsj_join(r, s, cfg)
+            if args.config == "c5":
+                from paper_2111_08824_b200 import dist as ljdist
+
+                (c, sm, x), _ = ljdist.lsj_join(r.keys, r.payloads, s.keys, s.payloads, cfg)
+                res = lj.JoinResult(checksum=(c, sm, x))
+            else:
+                res, _ = lj.lsj_join(r, s, cfg)
             del s, r
         else:
             # S streamed from pinned host memory: chunk copies on a copy
@@ -450,7 +514,8 @@ def _e2e(args, inp, index, world, run_step=None):
     n_s = len(inp.s)
     how = ("R and S copied to the device, then lsj_join" if index is None else
            "lj.join_checksum_host: S in 2^25-tuple chunks, H2D on a copy stream overlapped with the join")
-    return {"value": (len(inp.r) + world * n_s) / t, "unit": "tuples/s", "h2d_bytes_per_step": h2d,
+    return {"value": getattr(args, "job_tuples", len(inp.r) + world * n_s) / t, "unit": "tuples/s",
+            "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": 4 * 8, "ms_per_step": t * 1e3, "steps": steps, "path": how}
 
 
@@ -475,6 +540,7 @@ def main():
                          "directly; default per config (c2 buffered, c1/c3 direct)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scale", type=int, default=None, help="config size shift (tests only; not a bench number)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3

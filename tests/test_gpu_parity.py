@@ -546,3 +546,24 @@ def test_join_checksum_host_streams_chunks(lj, buffered):
     bad[500] = -1
     with pytest.raises(ValueError):
         lj.join_checksum_host(idx, bad, hp, buffered=buffered, chunk=1000)
+
+
+def test_distributed_lsj_single_rank_nccl(lj, tmp_path):
+    """The C5 path (shared model, range partition, NCCL all-to-all-v, local
+    LSJ, 3-word reduction) on a one-rank NCCL group equals the oracle; the
+    exchange protocol at world 2 is covered with gloo in test_dist.py."""
+    import torch.distributed as dist
+
+    from paper_2111_08824_b200 import configs
+    from paper_2111_08824_b200 import dist as ljdist
+
+    inp = configs.config5(scale=12)
+    want = oracle.smj_checksum(*inp.r.numpy(), *inp.s.numpy())
+    dist.init_process_group("nccl", init_method=f"file://{tmp_path}/pg", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        (c, s, x), ph = ljdist.lsj_join(inp.r.keys, inp.r.payloads, inp.s.keys, inp.s.payloads,
+                                        lj.LsjConfig(fanout=4096, sample_rate=0.01))
+    finally:
+        dist.destroy_process_group()
+    assert (c, s, x) == tuple(want)
