@@ -31,7 +31,7 @@ inline i64 est_capacity(i64 n, int nb) { return n + n / 16 + (i64)nb * (EST_PAD 
 
 // per-bin counts of every `stride`-th tuple (stride 1: the exact histogram)
 template <class Src>
-__global__ void __launch_bounds__(256) k_est_sample(Src f0, i64 n, int nbins, int stride, u32 *est) {
+__global__ void __launch_bounds__(256) k_est_sample(Src f0, i64 n, int nbins, int stride, u32 *est, u16 *codes) {
     extern __shared__ __align__(128) unsigned char smem_e[];
     u64 *tab = reinterpret_cast<u64 *>(smem_e);
     u32 *h = reinterpret_cast<u32 *>(smem_e + pt_table_bytes(f0.f.smem_words()));
@@ -48,9 +48,17 @@ __global__ void __launch_bounds__(256) k_est_sample(Src f0, i64 n, int nbins, in
 #pragma unroll
         for (int u = 0; u < 4; ++u) k[u] = ld_stream(f.keys + i + u * step);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) atomicAdd(h + (f.code(k[u]) >> shift), 1u);
+        for (int u = 0; u < 4; ++u) {
+            const u32 b = f.code(k[u]) >> shift;
+            atomicAdd(h + b, 1u);
+            if (codes) codes[i + u * step] = (u16)b;  // stride 1 only
+        }
     }
-    for (; i < n; i += step) atomicAdd(h + (f.code(ld_stream(f.keys + i)) >> shift), 1u);
+    for (; i < n; i += step) {
+        const u32 b = f.code(ld_stream(f.keys + i)) >> shift;
+        atomicAdd(h + b, 1u);
+        if (codes) codes[i] = (u16)b;
+    }
     __syncthreads();
     for (int j = threadIdx.x; j < nbins; j += blockDim.x)
         if (h[j]) atomicAdd(est + j, h[j]);
@@ -73,17 +81,21 @@ static __global__ void k_est_caps(const u32 *est, int nbins, int exact, i64 *cap
     }
 }
 
-template <class Src>
+// STORED: the bins were written by the exact counting pass (u16 per tuple)
+// and arrive through the ring with the tuples (no bin evaluation, no table)
+template <class Src, bool STORED>
 __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_est(Src f0, i64 n, i64 chunk, int nbins, int nst,
                                                               const i64 *__restrict__ rstart, u32 *gcur,
-                                                              unsigned long long *ovf, ulonglong2 *out) {
+                                                              unsigned long long *ovf, ulonglong2 *out,
+                                                              const u16 *__restrict__ codes) {
     constexpr int U = EST_TILE / PART2_NT;
+    constexpr size_t STAGE = EST_STAGE + (STORED ? EST_TILE * 2 : 0);
     extern __shared__ __align__(128) unsigned char smem_s[];
     u64 *tab = reinterpret_cast<u64 *>(smem_s);
-    unsigned char *smem = smem_s + pt_table_bytes(f0.f.smem_words());
-    f0.f.stage(tab);
+    unsigned char *smem = smem_s + (STORED ? 0 : pt_table_bytes(f0.f.smem_words()));
+    if (!STORED) f0.f.stage(tab);
     Src f = f0;
-    f.f = f0.f.at(tab);
+    if (!STORED) f.f = f0.f.at(tab);
     const int nb4 = (nbins + 31) & ~31;
     u32 *thist = reinterpret_cast<u32 *>(smem);  // this tile's count per bin
     u32 *tstart = thist + nb4;                   // this tile's run start per bin
@@ -102,12 +114,17 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_est(Src f0, i64 n, i64
     auto issue = [&](int t) {
         const int s = t % nst;
         const i64 base = lo + (i64)t * EST_TILE;
-        const unsigned b8 = (unsigned)(min((i64)EST_TILE, hi - base) * 8) & ~15u;
-        unsigned char *st = ring + (size_t)s * EST_STAGE;
-        if (b8) {
-            mbar_arrive_expect_tx(&full[s], 2 * b8);
-            bulk_g2s(st, f.keys + base, b8, &full[s]);
-            bulk_g2s(st + EST_TILE * 8, f.pay + base, b8, &full[s]);
+        const int cnt = (int)min((i64)EST_TILE, hi - base);
+        const unsigned b8 = (unsigned)(cnt * 8) & ~15u;
+        const unsigned b2 = STORED ? ((unsigned)(cnt * 2) & ~15u) : 0u;
+        unsigned char *st = ring + (size_t)s * STAGE;
+        if (b8 + b2) {
+            mbar_arrive_expect_tx(&full[s], 2 * b8 + b2);
+            if (b8) {
+                bulk_g2s(st, f.keys + base, b8, &full[s]);
+                bulk_g2s(st + EST_TILE * 8, f.pay + base, b8, &full[s]);
+            }
+            if (b2) bulk_g2s(st + EST_TILE * 16, codes + base, b2, &full[s]);
         } else {
             mbar_arrive(&full[s]);
         }
@@ -127,16 +144,20 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_est(Src f0, i64 n, i64
         const int s = t % nst;
         mbar_wait(&full[s], (unsigned)(t / nst) & 1u);
         const i64 base = lo + (i64)t * EST_TILE;
-        const int cnt = (int)min((i64)EST_TILE, hi - base), nb = cnt & ~1;
-        const unsigned char *st = ring + (size_t)s * EST_STAGE;
+        const int cnt = (int)min((i64)EST_TILE, hi - base), nb = cnt & ~1, nb8 = cnt & ~7;
+        const unsigned char *st = ring + (size_t)s * STAGE;
         const u64 *ks = reinterpret_cast<const u64 *>(st), *ps = ks + EST_TILE;
+        const u16 *cs = reinterpret_cast<const u16 *>(st + EST_TILE * 16);
         u16 *tbin = tbin2 + (t & 1) * EST_TILE;
         // (1) bin of every tuple and its rank in the tile's run
         int bj[U], rj[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int j = u * PART2_NT + tid;
-            bj[u] = j < cnt ? (int)(f.code(j < nb ? ks[j] : ld_stream(f.keys + base + j)) >> shift) : -1;
+            if (STORED)
+                bj[u] = j < cnt ? (int)(j < nb8 ? cs[j] : codes[base + j]) : -1;
+            else
+                bj[u] = j < cnt ? (int)(f.code(j < nb ? ks[j] : ld_stream(f.keys + base + j)) >> shift) : -1;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -216,7 +237,7 @@ static __global__ void k_est_regions(const i64 *rstart, const u32 *gcur, const u
     }
 }
 
-inline size_t est_workspace_bytes(int nbins) {
+inline size_t est_workspace_bytes(int nbins) {  // (+ part_align(2 n) for stored bins)
     size_t t = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, t, (i64 *)nullptr, (i64 *)nullptr, (int64_t)(nbins + 1));
     return part_align(sizeof(u32) * (size_t)nbins) * 2 + part_align(sizeof(i64) * (size_t)(nbins + 1)) * 2 +
@@ -233,7 +254,7 @@ inline size_t est_workspace_bytes(int nbins) {
 //              contiguous, reg[0..nbins] = bin starts (no overflow).
 template <class Src>
 int run_partition_claims(const Src &f, i64 n, int nbins, int exact, ulonglong2 *out, i64 *reg, void *ws,
-                         size_t ws_bytes, cudaStream_t st) {
+                         size_t ws_bytes, cudaStream_t st, u16 *codes = nullptr) {
     if (nbins < 1 || nbins > 2 * PART2_NT) {
         set_error("partition_est: nbins must be in [1, 2048]");
         return LJ_E_INVALID;
@@ -259,14 +280,18 @@ int run_partition_claims(const Src &f, i64 n, int nbins, int exact, ulonglong2 *
     const size_t tb = pt_table_bytes(f.f.smem_words());
     static bool attr = false;
     if (!attr) {
-        LJ_CK(cudaFuncSetAttribute(k_bin_scatter_est<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_SMEM_MAX));
+        LJ_CK(cudaFuncSetAttribute(k_bin_scatter_est<Src, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   PT_SMEM_MAX));
+        LJ_CK(cudaFuncSetAttribute(k_bin_scatter_est<Src, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   PT_SMEM_MAX));
         LJ_CK(cudaFuncSetAttribute(k_est_sample<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_SMEM_MAX));
         attr = true;
     }
     const int stride = exact ? 1 : EST_STRIDE;
+    const bool stored = exact && codes != nullptr && nbins <= 65536;
     if (n > 0) {
         k_est_sample<Src><<<grid_for((n + stride - 1) / stride, 256, 4), 256, tb + sizeof(u32) * nbins, st>>>(
-            f, n, nbins, stride, est);
+            f, n, nbins, stride, est, stored ? codes : nullptr);
         LJ_CK_LAUNCH();
     }
     k_est_caps<<<(nbins + 256) / 256, 256, 0, st>>>(est, nbins, exact, cap);
@@ -277,15 +302,21 @@ int run_partition_claims(const Src &f, i64 n, int nbins, int exact, ulonglong2 *
     if (n > 0) {
         const PartPlan p = part_plan(n, nbins);
         const size_t nb4 = (size_t)((nbins + 31) & ~31);
-        const size_t fix = tb + 3 * nb4 * sizeof(u32) + (nb4 + 32) * sizeof(i64) +
+        const size_t fix = (stored ? 0 : tb) + 3 * nb4 * sizeof(u32) + (nb4 + 32) * sizeof(i64) +
                            (((size_t)EST_TILE * 6 + 127) & ~(size_t)127);
-        const int nst = fix < (size_t)PT_SMEM_MAX ? (int)min((size_t)PT_MAXST, (PT_SMEM_MAX - fix) / EST_STAGE) : 0;
+        const size_t stage = EST_STAGE + (stored ? EST_TILE * 2 : 0);
+        const int nst = fix < (size_t)PT_SMEM_MAX ? (int)min((size_t)PT_MAXST, (PT_SMEM_MAX - fix) / stage) : 0;
         if (nst < 2) {
             set_error("partition_est: shared memory too small for the ring");
             return LJ_E_INVALID;
         }
-        k_bin_scatter_est<Src><<<p.blocks, PART2_NT, fix + nst * EST_STAGE, st>>>(f, n, p.chunk, nbins, nst, rstart,
-                                                                                   gcur, ovf, out);
+        if (stored)
+            k_bin_scatter_est<Src, true><<<p.blocks, PART2_NT, fix + nst * stage, st>>>(f, n, p.chunk, nbins, nst,
+                                                                                        rstart, gcur, ovf, out, codes);
+        else
+            k_bin_scatter_est<Src, false><<<p.blocks, PART2_NT, fix + nst * stage, st>>>(f, n, p.chunk, nbins, nst,
+                                                                                         rstart, gcur, ovf, out,
+                                                                                         nullptr);
         LJ_CK_LAUNCH();
     }
     if (!exact) {
@@ -310,8 +341,16 @@ template <class Src>
 int run_partition_fast(const Src &f, i64 n, int nbins, ulonglong2 *out, i64 *starts, void *ws, size_t ws_bytes,
                        cudaStream_t st) {
     static const bool legacy = getenv("LJ_PART_SEGMENTS") != nullptr;
-    if (!legacy && f.aligned16() && nbins <= 2 * PART2_NT && n < (i64)0xFFFFFFFFLL)
-        return run_partition_claims(f, n, nbins, 1, out, starts, ws, ws_bytes, st);
+    static const bool recompute = getenv("LJ_PART_RECOMPUTE") != nullptr;
+    if (!legacy && f.aligned16() && nbins <= 2 * PART2_NT && n < (i64)0xFFFFFFFFLL) {
+        // the counting pass stores every tuple's bin (u16) when the workspace
+        // has room; the scatter then streams bins instead of evaluating them
+        const size_t eb = est_workspace_bytes(nbins);
+        u16 *codes = (!recompute && ws_bytes >= eb + part_align(sizeof(u16) * (size_t)n))
+                         ? reinterpret_cast<u16 *>((char *)ws + eb)
+                         : nullptr;
+        return run_partition_claims(f, n, nbins, 1, out, starts, ws, ws_bytes, st, codes);
+    }
     return run_partition(f, n, nbins, out, starts, ws, ws_bytes, st);
 }
 

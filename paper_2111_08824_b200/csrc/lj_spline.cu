@@ -405,8 +405,15 @@ int64_t lj_spline_hash_bucket_bins(int64_t n) { return hash_bins(n); }
 int64_t lj_spline_hash_bucket_capacity(int64_t nk, int64_t n) { return est_capacity(nk < 0 ? 0 : nk, hash_bins(n)); }
 
 size_t lj_spline_hash_bucket_est_workspace_bytes(int64_t nk, int64_t n) {
-    (void)nk;
-    return est_workspace_bytes(hash_bins(n));
+    return est_workspace_bytes(hash_bins(n)) + part_align(sizeof(u16) * (size_t)(nk < 0 ? 0 : nk));
+}
+
+// exact regions in lj_leaf_bucket's layout: ends = next starts, no overflow
+__global__ void k_exact_regions(int nb, i64 *reg) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += gridDim.x * blockDim.x) {
+        if (b < nb) reg[nb + 1 + b] = reg[b + 1];
+        else reg[2 * nb + 1] = 0;
+    }
 }
 
 int lj_spline_hash_bucket_est(const LjSplineHash *idx, const uint64_t *keys, const uint64_t *pay, int64_t nk,
@@ -420,6 +427,20 @@ int lj_spline_hash_bucket_est(const LjSplineHash *idx, const uint64_t *keys, con
     f.n = idx->model.n;
     f.rn = (double)f.nb / (double)idx->model.n;
     SoaSrc<PosBin> src{keys, pay, f};
+    // LJ_HASH_EXACT=1: a counting pass stores every probe's window (u16)
+    // and the claims scatter streams them (no gaps, no overflow); measured
+    // 42.4 ms vs 37.7 ms for the one-pass default at C3 (the counting pass
+    // pays the spline-table loads once more)
+    static const bool exact = getenv("LJ_HASH_EXACT") != nullptr;
+    const size_t eb = est_workspace_bytes((int)f.nb);
+    if (exact && ws_bytes >= eb + part_align(sizeof(u16) * (size_t)nk) && nk < (i64)0xFFFFFFFFLL) {
+        const int rc = run_partition_claims(src, nk, (int)f.nb, 1, reinterpret_cast<ulonglong2 *>(pairs_out), reg_out,
+                                            ws, ws_bytes, st, reinterpret_cast<u16 *>((char *)ws + eb));
+        if (rc) return rc;
+        k_exact_regions<<<((int)f.nb + 256) / 256, 256, 0, st>>>((int)f.nb, reg_out);
+        LJ_CK_LAUNCH();
+        return LJ_OK;
+    }
     const int rc = run_partition_est(src, nk, (int)f.nb, reinterpret_cast<ulonglong2 *>(pairs_out), reg_out, ws,
                                      ws_bytes, st);
     if (rc) return rc;
