@@ -23,7 +23,7 @@ from .models import (
     train_rmi,
 )
 from .results import JoinResult, LookupStats, PhaseBreakdown, SortStats
-from .streaming import join_checksum_host
+from .streaming import join_checksum_host, lsj_join_host
 from .util import SENTINEL_KEY, chunk_bounds
 
 __version__ = "0.1.0"

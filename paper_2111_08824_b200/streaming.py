@@ -76,3 +76,48 @@ def join_checksum_host(index, keys_host: torch.Tensor, payloads_host: torch.Tens
     if bool(bad):
         raise ValueError("keys may not contain the reserved maximum key")
     return out
+
+
+def lsj_join_host(r_keys_host: torch.Tensor, r_payloads_host: torch.Tensor, s_keys_host: torch.Tensor,
+                  s_payloads_host: torch.Tensor, config=None, device=None):
+    """`lsj_join` of host-resident R and S (lsj.py:373-405) with the copies
+    overlapped: R and then S are copied on a copy stream; R's side (sample,
+    fit, partition, sort) runs as soon as R has landed, while S is still
+    crossing PCIe; then S's side and the merge-join.  Same result as
+    `lsj_join` on the device-resident relations -> JoinResult."""
+    from . import lsj as L
+    from .data import Relation
+
+    config = config or L.LsjConfig()
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    comp = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    hs = [_pinned(t) for t in (r_keys_host, r_payloads_host, s_keys_host, s_payloads_host)]
+    ds = [torch.empty(t.shape, dtype=torch.int64, device=dev) for t in hs]
+    ev_r, ev_s = torch.cuda.Event(), torch.cuda.Event()
+    with torch.cuda.stream(copy):
+        for d, h in zip(ds[:2], hs[:2]):
+            d.copy_(h, non_blocking=True)
+        ev_r.record(copy)
+        for d, h in zip(ds[2:], hs[2:]):
+            d.copy_(h, non_blocking=True)
+        ev_s.record(copy)
+    comp.wait_event(ev_r)
+    r = Relation(ds[0], ds[1], validate=True)
+    if len(r) == 0:
+        comp.wait_event(ev_s)
+        return L.JoinResult()
+    scale = config.effective_fanout()
+    _, lr = L.prepare_model(r, config.sample_rate, config.seed, config.model_fanout)
+    pr, str_ = L._partition(r.keys, r.payloads, lr)
+    pr, dr = L._sort(pr, str_, lr, len(r))
+    comp.wait_event(ev_s)
+    s = Relation(ds[2], ds[3], validate=True)
+    if len(s) == 0:
+        return L.JoinResult()
+    _, ls = L.prepare_model(s, config.sample_rate, config.seed ^ 0x5DEECE66D, config.model_fanout)
+    ps, sts = L._partition(s.keys, s.payloads, ls)
+    ps, ds_ = L._sort(ps, sts, ls, len(s))
+    r_sorted = L.SortedRelation(pr[: 2 * len(r)], str_, lr, scale, (lr.tag, scale), diag=dr)
+    s_sorted = L.SortedRelation(ps[: 2 * len(s)], sts, ls, scale, (ls.tag, scale), diag=ds_)
+    return L.chunked_join(r_sorted, s_sorted, lr.rmi, scale, config.workers)

@@ -567,3 +567,14 @@ def test_distributed_lsj_single_rank_nccl(lj, tmp_path):
     finally:
         dist.destroy_process_group()
     assert (c, s, x) == tuple(want)
+
+
+def test_lsj_join_host_overlapped_equals_device(lj):
+    """lsj_join_host (R's side overlapped with S's H2D) == lsj_join == oracle."""
+    from paper_2111_08824_b200 import configs
+
+    inp = configs.config4(scale=10)
+    cfg = lj.LsjConfig(fanout=4096, sample_rate=0.01)
+    want, _ = lj.lsj_join(inp.r, inp.s, cfg)
+    got = lj.lsj_join_host(inp.r.keys.cpu(), inp.r.payloads.cpu(), inp.s.keys.cpu(), inp.s.payloads.cpu(), cfg)
+    assert got.checksum == want.checksum == tuple(oracle.smj_checksum(*inp.r.numpy(), *inp.s.numpy()))
