@@ -215,6 +215,16 @@ int lj_leaf_bucket(const LjGrmi *idx, const uint64_t *keys, const uint64_t *pay,
  * 8 bytes of device scratch (work counter). */
 int lj_grmi_probe_bucketed(const LjGrmi *idx, const uint64_t *s_pairs, const int64_t *reg, void *ws, uint64_t *out,
                            int accumulate, void *stream);
+/* The window staging of the probe above, precomputed once per index: for
+ * every window the compacted real keys, slot offsets, radix table and RMI
+ * leaves in the probe's shared-memory layout (+ a 32-B header), so a CTA
+ * stages a window with four bulk copies instead of rebuilding it.  0 bytes:
+ * the index is not probed through staged windows.  The image is derived
+ * from the index alone (rebuild it if the index changes). */
+size_t lj_grmi_stage_image_bytes(const LjGrmi *idx);
+int lj_grmi_stage_image_build(const LjGrmi *idx, void *img, size_t bytes, void *stream);
+int lj_grmi_probe_bucketed_img(const LjGrmi *idx, const uint64_t *s_pairs, const int64_t *reg, void *ws,
+                               const void *img, uint64_t *out, int accumulate, void *stream);
 /* K1 over interleaved {key, payload} probe records (e.g. bucketed S). */
 int lj_grmi_probe_pairs(const LjGrmi *idx, const uint64_t *s_pairs, int64_t nk, uint64_t *out, int accumulate,
                         void *stream);

@@ -93,6 +93,9 @@ SIGNATURES = {
     "lj_leaf_bucket_workspace_bytes": (_size_t, [_i64, _i64]),
     "lj_leaf_bucket": (_int, [ctypes.POINTER(LjGrmi), _P, _P, _i64, _P, _P, _P, _size_t, _P]),
     "lj_grmi_probe_bucketed": (_int, [ctypes.POINTER(LjGrmi), _P, _P, _P, _P, _int, _P]),
+    "lj_grmi_stage_image_bytes": (_size_t, [ctypes.POINTER(LjGrmi)]),
+    "lj_grmi_stage_image_build": (_int, [ctypes.POINTER(LjGrmi), _P, _size_t, _P]),
+    "lj_grmi_probe_bucketed_img": (_int, [ctypes.POINTER(LjGrmi), _P, _P, _P, _P, _P, _int, _P]),
     "lj_grmi_probe_pairs": (_int, [ctypes.POINTER(LjGrmi), _P, _i64, _P, _int, _P]),
     "lj_spline_fit_host": (_int, [_P, _i64, _i64, _i64, _P, _P, _P, _P, _P]),
     "lj_spline_aux_host": (_int, [_P, _i64, _P, _i64, _u64, _P, _P, _P]),

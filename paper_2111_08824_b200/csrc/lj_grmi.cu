@@ -319,10 +319,121 @@ __device__ __forceinline__ u32 block_exclusive_scan(u32 v, u32 *wsum, u32 *total
     return r;
 }
 
+// ---- staging of window [slo, shi) into (ck, cp, T, lc) -- shared memory in
+// the probe, global memory when building the staging image.  Every thread
+// of the CTA calls it.
+struct StageOut {
+    int n_c, lc_lo, lc_n;
+};
+struct StageHdr {  // 32 B per window in front of the image
+    int n_c, lc_lo, lc_n, smax;
+    i64 f0, pad;
+};
+__host__ __device__ inline size_t stage_hdr_bytes(int nwin) { return ((size_t)nwin * sizeof(StageHdr) + 255) & ~(size_t)255; }
+
+__device__ StageOut stage_window(const GrmiDev &g, i64 slo, i64 shi, int span, u64 *ck, u16 *cp, u16 *T, u32 *wb,
+                                 LjLeaf *lc, u32 *s_wsum, int *ps_max, i64 *ps_f0) {
+    const int tid = threadIdx.x;
+    int &s_max = *ps_max;
+    i64 &s_f0 = *ps_f0;
+    const i64 w0 = slo >> 5;
+    const int bo = (int)(slo & 31);  // staged slot i is bit i + bo of the range's words
+    const int nbw = (span + bo + 31) >> 5;
+    auto word = [&](int j) -> u32 {  // bitmap word j, bits outside [slo, shi) cleared
+        u32 v = __ldg(g.bitmap + w0 + j);
+        if (j == 0) v &= 0xffffffffu << bo;
+        const int top = span + bo - (j << 5);
+        if (top < 32) v &= (1u << top) - 1u;
+        return v;
+    };
+    u32 nc;
+    {
+        const int j0 = 2 * tid;  // nbw <= 2 * STAGE_NT words: two per thread
+        const u32 c0 = j0 < nbw ? __popc(word(j0)) : 0, c1 = j0 + 1 < nbw ? __popc(word(j0 + 1)) : 0;
+        const u32 pre = block_exclusive_scan<STAGE_NT>(c0 + c1, s_wsum, &nc);
+        if (j0 < nbw) wb[j0] = pre;
+        if (j0 + 1 < nbw) wb[j0 + 1] = pre + c0;
+    }
+    if (tid == 0) s_max = 0;
+    __syncthreads();
+    for (int i = tid; i < span; i += STAGE_NT) {
+        const int b = i + bo;
+        const u32 v = word(b >> 5);
+        if ((v >> (b & 31)) & 1u) {
+            const u32 idx = wb[b >> 5] + __popc(v & ((1u << (b & 31)) - 1u));
+            ck[idx] = ldg(g.slots + 2 * (slo + i));
+            cp[idx] = (u16)i;
+        }
+    }
+    const int n_c = (int)nc;
+    if (tid == 0) {
+        ck[n_c] = ~0ULL;  // sentinel: larger than every key (keys < 2^64 - 1)
+        cp[n_c] = (u16)span;
+        // window 0 with no entry: every slot copies entry 0 (gapped.py:250-252)
+        s_f0 = (slo == 0 && n_c == 0) ? g.next_real(shi) : -1;
+    }
+    __syncthreads();
+    const u64 kmin = n_c ? ck[0] : 0, kmax = n_c ? ck[n_c - 1] : 0;
+    const u64 krange = kmax - kmin;
+    const int sh = krange == 0 ? 0 : max(0, 64 - __clzll((long long)krange) - STAGE_TB);
+    for (int i = tid; i < n_c; i += STAGE_NT) {
+        const int p = (int)((ck[i] - kmin) >> sh);
+        const int pp = i == 0 ? -1 : (int)((ck[i - 1] - kmin) >> sh);
+        for (int q = pp + 1; q <= p; ++q) T[q] = (u16)i;
+    }
+    for (int q = (n_c ? (int)(krange >> sh) + 1 : 0) + tid; q <= STAGE_TBINS; q += STAGE_NT) T[q] = (u16)n_c;
+    // leaves the staged keys route to (+ a margin); probes routed elsewhere
+    // read their leaf from global memory
+    int lc_lo = 0, lc_n = 0;
+    if (n_c) {
+        const i64 l0 = max((i64)0, g.model.route(u64_to_f64(kmin)) - 8);
+        const i64 l1 = min(g.model.m - 1, g.model.route(u64_to_f64(kmax)) + 8);
+        lc_lo = (int)l0;
+        lc_n = (int)min(l1 - l0 + 1, (i64)STAGE_LEAVES);
+        for (int l = tid; l < lc_n; l += STAGE_NT) lc[l] = load_leaf(g.model.leaves, l0 + l);
+    }
+    __syncthreads();
+    {
+        int mb = 0;
+        for (int q = tid; q < STAGE_TBINS; q += STAGE_NT) mb = max(mb, (int)T[q + 1] - (int)T[q]);
+        mb = __reduce_max_sync(0xffffffffu, mb);
+        if ((tid & 31) == 0 && mb) atomicMax(&s_max, mb);
+    }
+    __syncthreads();
+    return StageOut{n_c, lc_lo, lc_n};
+}
+
+// staging image of every window (built once per index): header + the
+// shared-memory layout of each window
+__global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_stage_image(GrmiDev g, int nwin, int shift, unsigned char *img) {
+    __shared__ u32 s_wsum[STAGE_NT / 32 + 1];
+    __shared__ int s_max;
+    __shared__ i64 s_f0;
+    const int w = blockIdx.x;
+    const int span_max = (1 << shift) + 1;
+    const i64 slo = (i64)w << shift, shi = min(g.L, slo + span_max);
+    unsigned char *base = img + stage_hdr_bytes(nwin) + (size_t)w * SO_END;
+    const StageOut so = stage_window(g, slo, shi, (int)(shi - slo), reinterpret_cast<u64 *>(base + SO_CK),
+                                     reinterpret_cast<u16 *>(base + SO_CP), reinterpret_cast<u16 *>(base + SO_T),
+                                     reinterpret_cast<u32 *>(base + SO_WB), reinterpret_cast<LjLeaf *>(base + SO_LC),
+                                     s_wsum, &s_max, &s_f0);
+    if (threadIdx.x == 0) {
+        StageHdr h;
+        h.n_c = so.n_c;
+        h.lc_lo = so.lc_lo;
+        h.lc_n = so.lc_n;
+        h.smax = s_max;
+        h.f0 = s_f0;
+        h.pad = 0;
+        reinterpret_cast<StageHdr *>(img)[w] = h;
+    }
+}
+
 __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, const ulonglong2 *__restrict__ rec,
                                                                    const i64 *__restrict__ reg, int nwin, int shift,
                                                                    unsigned long long *work,
-                                                                   u64 *out, u64 *trace, i64 *dbg) {
+                                                                   u64 *out, u64 *trace, i64 *dbg,
+                                                                   const unsigned char *__restrict__ img) {
     extern __shared__ __align__(16) unsigned char smem[];
     u64 *ck = reinterpret_cast<u64 *>(smem + SO_CK);    // real keys of the staged range (+ sentinel)
     u16 *cp = reinterpret_cast<u16 *>(smem + SO_CP);    // their slot offsets (+ sentinel: span)
@@ -333,8 +444,15 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
     __shared__ int s_max;
     __shared__ u32 s_wsum[STAGE_NT / 32 + 1];
     __shared__ u32 s_small[2048 / 32];  // windows with < STAGE_MIN probes: global search
+    __shared__ StageHdr s_hdr;
+    __shared__ __align__(8) uint64_t s_bar;
+    unsigned s_phase = 0;
     const int tid = threadIdx.x;
     for (int j = tid; j < 2048 / 32; j += STAGE_NT) s_small[j] = 0;
+    if (img && tid == 0) {
+        mbar_init(&s_bar, 1);
+        mbar_init_fence();
+    }
     __syncthreads();
     // regions: window w's records are [reg[w], rend[w]); reg[nwin] = end of
     // the regions (the overflow area, probed separately, starts there)
@@ -373,70 +491,41 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
             const i64 slo = (i64)w << shift;
             const i64 shi = min(g.L, slo + span_max);
             const int span = (int)(shi - slo);
-            const i64 w0 = slo >> 5;
-            const int bo = (int)(slo & 31);  // staged slot i is bit i + bo of the range's words
-            const int nbw = (span + bo + 31) >> 5;
-            auto word = [&](int j) -> u32 {  // bitmap word j, bits outside [slo, shi) cleared
-                u32 v = __ldg(g.bitmap + w0 + j);
-                if (j == 0) v &= 0xffffffffu << bo;
-                const int top = span + bo - (j << 5);
-                if (top < 32) v &= (1u << top) - 1u;
-                return v;
-            };
-            u32 nc;
-            {
-                const int j0 = 2 * tid;  // nbw <= 2 * STAGE_NT words: two per thread
-                const u32 c0 = j0 < nbw ? __popc(word(j0)) : 0, c1 = j0 + 1 < nbw ? __popc(word(j0 + 1)) : 0;
-                const u32 pre = block_exclusive_scan<STAGE_NT>(c0 + c1, s_wsum, &nc);
-                if (j0 < nbw) wb[j0] = pre;
-                if (j0 + 1 < nbw) wb[j0 + 1] = pre + c0;
-            }
-            if (tid == 0) s_max = 0;
-            __syncthreads();
-            for (int i = tid; i < span; i += STAGE_NT) {
-                const int b = i + bo;
-                const u32 v = word(b >> 5);
-                if ((v >> (b & 31)) & 1u) {
-                    const u32 idx = wb[b >> 5] + __popc(v & ((1u << (b & 31)) - 1u));
-                    ck[idx] = ldg(g.slots + 2 * (slo + i));
-                    cp[idx] = (u16)i;
+            int n_c, lc_lo, lc_n;
+            if (img) {
+                // precomputed staging image of window w: four bulk copies
+                if (tid == 0) {
+                    const StageHdr h = reinterpret_cast<const StageHdr *>(img)[w];
+                    s_hdr = h;
+                    s_f0 = h.f0;
+                    s_max = h.smax;
+                    const unsigned bk = ((unsigned)(h.n_c + 1) * 8u + 15u) & ~15u;
+                    const unsigned bp = ((unsigned)(h.n_c + 1) * 2u + 15u) & ~15u;
+                    const unsigned bt = ((unsigned)(STAGE_TBINS + 1) * 2u + 15u) & ~15u;
+                    const unsigned bl = (unsigned)h.lc_n * 32u;
+                    const unsigned char *src = img + stage_hdr_bytes(nwin) + (size_t)w * SO_END;
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_arrive_expect_tx(&s_bar, bk + bp + bt + bl);
+                    bulk_g2s(smem + SO_CK, src + SO_CK, bk, &s_bar);
+                    bulk_g2s(smem + SO_CP, src + SO_CP, bp, &s_bar);
+                    bulk_g2s(smem + SO_T, src + SO_T, bt, &s_bar);
+                    if (bl) bulk_g2s(smem + SO_LC, src + SO_LC, bl, &s_bar);
                 }
+                __syncthreads();
+                mbar_wait(&s_bar, s_phase);
+                s_phase ^= 1u;
+                n_c = s_hdr.n_c;
+                lc_lo = s_hdr.lc_lo;
+                lc_n = s_hdr.lc_n;
+            } else {
+                const StageOut so = stage_window(g, slo, shi, span, ck, cp, T, wb, lc, s_wsum, &s_max, &s_f0);
+                n_c = so.n_c;
+                lc_lo = so.lc_lo;
+                lc_n = so.lc_n;
             }
-            const int n_c = (int)nc;
-            if (tid == 0) {
-                ck[n_c] = ~0ULL;  // sentinel: larger than every key (keys < 2^64 - 1)
-                cp[n_c] = (u16)span;
-                // window 0 with no entry: every slot copies entry 0 (gapped.py:250-252)
-                s_f0 = (slo == 0 && n_c == 0) ? g.next_real(shi) : -1;
-            }
-            __syncthreads();
             const u64 kmin = n_c ? ck[0] : 0, kmax = n_c ? ck[n_c - 1] : 0;
             const u64 krange = kmax - kmin;
             const int sh = krange == 0 ? 0 : max(0, 64 - __clzll((long long)krange) - STAGE_TB);
-            for (int i = tid; i < n_c; i += STAGE_NT) {
-                const int p = (int)((ck[i] - kmin) >> sh);
-                const int pp = i == 0 ? -1 : (int)((ck[i - 1] - kmin) >> sh);
-                for (int q = pp + 1; q <= p; ++q) T[q] = (u16)i;
-            }
-            for (int q = (n_c ? (int)(krange >> sh) + 1 : 0) + tid; q <= STAGE_TBINS; q += STAGE_NT) T[q] = (u16)n_c;
-            // leaves the staged keys route to (+ a margin); probes routed elsewhere
-            // read their leaf from global memory
-            int lc_lo = 0, lc_n = 0;
-            if (n_c) {
-                const i64 l0 = max((i64)0, g.model.route(u64_to_f64(kmin)) - 8);
-                const i64 l1 = min(g.model.m - 1, g.model.route(u64_to_f64(kmax)) + 8);
-                lc_lo = (int)l0;
-                lc_n = (int)min(l1 - l0 + 1, (i64)STAGE_LEAVES);
-                for (int l = tid; l < lc_n; l += STAGE_NT) lc[l] = load_leaf(g.model.leaves, l0 + l);
-            }
-            __syncthreads();
-            {
-                int mb = 0;
-                for (int q = tid; q < STAGE_TBINS; q += STAGE_NT) mb = max(mb, (int)T[q + 1] - (int)T[q]);
-                mb = __reduce_max_sync(0xffffffffu, mb);
-                if ((tid & 31) == 0 && mb) atomicMax(&s_max, mb);
-            }
-            __syncthreads();
             const int iters = 32 - __clz(s_max);  // lower-bound steps for the largest bucket
             if (trace && tid == 0) {
                 u64 t_now;
@@ -836,8 +925,42 @@ int lj_grmi_probe(const LjGrmi *idx, const uint64_t *s_keys, const uint64_t *s_p
     return LJ_OK;
 }
 
+static int probe_bucketed(const LjGrmi *idx, const uint64_t *s_pairs, const int64_t *reg, void *ws,
+                          const unsigned char *img, uint64_t *out, int accumulate, void *stream);
+
+size_t lj_grmi_stage_image_bytes(const LjGrmi *idx) {
+    if (!idx || idx->n == 0 || !staged_ok(idx)) return 0;
+    const int nwin = lj_leaf_bucket_bins(idx->L);
+    return stage_hdr_bytes(nwin) + (size_t)nwin * SO_END;
+}
+
+int lj_grmi_stage_image_build(const LjGrmi *idx, void *img, size_t bytes, void *stream) {
+    LJ_REQUIRE(idx != nullptr && img != nullptr, "null index or image");
+    const size_t need = lj_grmi_stage_image_bytes(idx);
+    LJ_REQUIRE(need > 0, "this index is not probed through staged windows");
+    if (bytes < need) {
+        set_error("lj_grmi_stage_image_build: buffer too small");
+        return LJ_E_WORKSPACE;
+    }
+    const int nwin = lj_leaf_bucket_bins(idx->L);
+    k_grmi_stage_image<<<nwin, STAGE_NT, 0, as_stream(stream)>>>(GrmiDev(*idx), nwin, slot_window_shift(idx->L),
+                                                                 (unsigned char *)img);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
 int lj_grmi_probe_bucketed(const LjGrmi *idx, const uint64_t *s_pairs, const int64_t *reg, void *ws, uint64_t *out,
                            int accumulate, void *stream) {
+    return probe_bucketed(idx, s_pairs, reg, ws, nullptr, out, accumulate, stream);
+}
+
+int lj_grmi_probe_bucketed_img(const LjGrmi *idx, const uint64_t *s_pairs, const int64_t *reg, void *ws,
+                               const void *img, uint64_t *out, int accumulate, void *stream) {
+    return probe_bucketed(idx, s_pairs, reg, ws, (const unsigned char *)img, out, accumulate, stream);
+}
+
+static int probe_bucketed(const LjGrmi *idx, const uint64_t *s_pairs, const int64_t *reg, void *ws,
+                          const unsigned char *img, uint64_t *out, int accumulate, void *stream) {
     LJ_REQUIRE(idx != nullptr, "null index");
     cudaStream_t st = as_stream(stream);
     if (!accumulate) LJ_CK(cudaMemsetAsync(out, 0, 4 * sizeof(u64), st));
@@ -883,7 +1006,7 @@ int lj_grmi_probe_bucketed(const LjGrmi *idx, const uint64_t *s_pairs, const int
         LJ_CK(cudaMemsetAsync(dbg, 0xff, (size_t)nk * 4 * sizeof(i64), st));
     }
     k_grmi_probe_staged<<<sm_count(), STAGE_NT, sm, st>>>(gd, reinterpret_cast<const ulonglong2 *>(s_pairs), reg,
-                                                          nwin, shift, work, out, trace, dbg);
+                                                          nwin, shift, work, out, trace, dbg, img);
     LJ_CK_LAUNCH();
     if (dbg) {
         std::vector<i64> h((size_t)nk * 4);

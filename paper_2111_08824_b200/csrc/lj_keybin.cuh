@@ -116,8 +116,8 @@ static __global__ void __launch_bounds__(1024) k_keybin_build(u64 *lay, int nb) 
         worst[tid] = 0;
         u64 t0 = 0, t1 = 0;
         if (nb >= 2) {
-            t0 = kb_image(B[1], tid);
-            t1 = kb_image(B[nb - 1], tid);
+            t0 = kb_image(pm[1], tid);
+            t1 = kb_image(pm[nb - 1], tid);
         }
         int s = 0;
         while (s < 63 && ((t1 - t0) >> s) >= (u64)KB_CELLS) ++s;
@@ -125,12 +125,13 @@ static __global__ void __launch_bounds__(1024) k_keybin_build(u64 *lay, int nb) 
         s_shift[tid] = s;
     }
     __syncthreads();
-    // #{ j in [1, nb) : cell(B[j]) < c }  (cell() non-decreasing in j)
+    // #{ j in [1, nb) : cell(B[j]) < c }  (cell() non-decreasing in j;
+    // searched in the shared-memory copy)
     auto below = [&](int m, int c) {
         int lo = 1, hi = nb;
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
-            if ((int)kb_cell(kb_image(B[mid], m), s_t0[m], s_shift[m]) < c) lo = mid + 1;
+            if ((int)kb_cell(kb_image(pm[mid], m), s_t0[m], s_shift[m]) < c) lo = mid + 1;
             else hi = mid;
         }
         return lo - 1;

@@ -41,20 +41,31 @@ __global__ void __launch_bounds__(256) k_est_sample(Src f0, i64 n, int nbins, in
     for (int j = threadIdx.x; j < nbins; j += blockDim.x) h[j] = 0;
     __syncthreads();
     const int shift = f.f.shift;
-    const i64 step = (i64)gridDim.x * blockDim.x * stride;
-    i64 i = (blockIdx.x * (i64)blockDim.x + threadIdx.x) * stride;
-    for (; i + 3 * step < n; i += 4 * step) {  // four independent loads in flight
+    // the sample is every stride-th block of 32 consecutive tuples (a warp
+    // reads whole sectors; a strided single-key sample wasted 3/4 of every
+    // 32-B sector it fetched); stride 1 visits every tuple
+    const i64 lane = threadIdx.x & 31;
+    const i64 ngrp = ((i64)gridDim.x * blockDim.x) >> 5, bs = 32 * (i64)stride;
+    i64 blk = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
+    for (; (blk + 3 * ngrp) * bs < n; blk += 4 * ngrp) {  // four independent loads in flight
         u64 k[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) k[u] = ld_stream(f.keys + i + u * step);
+        i64 i[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
+            i[u] = (blk + u * ngrp) * bs + lane;
+            k[u] = i[u] < n ? ld_stream(f.keys + i[u]) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (i[u] >= n) continue;
             const u32 b = f.code(k[u]) >> shift;
             atomicAdd(h + b, 1u);
-            if (codes) codes[i + u * step] = (u16)b;  // stride 1 only
+            if (codes) codes[i[u]] = (u16)b;  // stride 1 only
         }
     }
-    for (; i < n; i += step) {
+    for (; blk * bs < n; blk += ngrp) {
+        const i64 i = blk * bs + lane;
+        if (i >= n) continue;
         const u32 b = f.code(ld_stream(f.keys + i)) >> shift;
         atomicAdd(h + b, 1u);
         if (codes) codes[i] = (u16)b;

@@ -10,6 +10,7 @@ materialise pairs with the reference's exact per-probe semantics.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -137,13 +138,38 @@ class GappedRmiIndex:
                                       _lib.ptr(scratch["pairs"]), _lib.ptr(scratch["regions"]), _lib.ptr(ws),
                                       ws.numel(), _lib.stream_ptr(stream)), "leaf_bucket")
 
+    # staging image (lj_grmi_stage_image_build) for indexes at least this
+    # large: below it the 207 KB-per-window image costs more memory than the
+    # staging it saves
+    STAGE_IMAGE_MIN_SLOTS = 1 << 24
+
+    def stage_image(self, stream=None):
+        """The probe's per-window staging precomputed once (built on first
+        use; None when the index is not probed through staged windows or is
+        smaller than STAGE_IMAGE_MIN_SLOTS)."""
+        img = getattr(self, "_stage_img", False)
+        if img is not False:
+            return img
+        self._stage_img = None
+        if self.slot_count >= self.STAGE_IMAGE_MIN_SLOTS and not os.environ.get("LJ_NO_STAGE_IMAGE"):
+            lib = _lib.lib()
+            g = self.c_struct()
+            nbytes = lib.lj_grmi_stage_image_bytes(ctypes.byref(g))
+            if nbytes:
+                img = torch.empty(nbytes, dtype=torch.uint8, device=self.slots.device)
+                _lib.check(lib.lj_grmi_stage_image_build(ctypes.byref(g), _lib.ptr(img), nbytes,
+                                                         _lib.stream_ptr(stream)), "grmi_stage_image_build")
+                self._stage_img = img
+        return self._stage_img
+
     def probe_records(self, n: int, scratch: dict, out: torch.Tensor, accumulate: bool = False, stream=None) -> None:
         """Staged K1 over the n records bucket_records left in scratch."""
         g = self.c_struct()
-        _lib.check(_lib.lib().lj_grmi_probe_bucketed(ctypes.byref(g), _lib.ptr(scratch["pairs"]),
-                                                     _lib.ptr(scratch["regions"]), _lib.ptr(scratch["work"]),
-                                                     _lib.ptr(out), int(bool(accumulate)), _lib.stream_ptr(stream)),
-                   "grmi_probe_bucketed")
+        img = self.stage_image(stream)
+        _lib.check(_lib.lib().lj_grmi_probe_bucketed_img(ctypes.byref(g), _lib.ptr(scratch["pairs"]),
+                                                         _lib.ptr(scratch["regions"]), _lib.ptr(scratch["work"]),
+                                                         _lib.ptr(img), _lib.ptr(out), int(bool(accumulate)),
+                                                         _lib.stream_ptr(stream)), "grmi_probe_bucketed")
         return out
 
     def _predict_slots(self, keys: torch.Tensor) -> torch.Tensor:

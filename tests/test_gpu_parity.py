@@ -368,6 +368,11 @@ def test_buffered_staged_probe_duplicates_and_zero_payloads(lj):
     direct = idx.join_checksum(s.keys, s.payloads).cpu().tolist()
     buffered = idx.join_checksum_buffered(s.keys, s.payloads).cpu().tolist()
     assert buffered == direct
+    # the same through the precomputed staging image
+    idx.STAGE_IMAGE_MIN_SLOTS = 0
+    idx.__dict__.pop("_stage_img", None)  # drop the cached "no image" decision
+    assert idx.stage_image() is not None
+    assert idx.join_checksum_buffered(s.keys, s.payloads).cpu().tolist() == direct
     og = oracle.grmi_build(keys, pays, 2.0, 64, model=oracle.Rmi(
         idx.rmi.root_slope, idx.rmi.root_intercept, idx.rmi.trained_len, idx.rmi.leaf_slope, idx.rmi.leaf_intercept,
         idx.rmi.clamp_lo, idx.rmi.clamp_hi, idx.rmi.err_lo, idx.rmi.err_hi))
