@@ -1,5 +1,5 @@
 # round measurement: benches (all configs + reference arm), launch list, ncu --set full of the dominant kernels
-V=${V:-v5}
+V=${V:-v8}
 for c in c2 c1 c3 c4; do timeout 900 python bench.py --config $c > gpurun_out/bench_${c}_$V.json 2> gpurun_out/bench_${c}_$V.err; done
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_$V.json 2> gpurun_out/bench_ref_$V.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c2_$V.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch_$V.log 2>&1
