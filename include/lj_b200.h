@@ -99,6 +99,7 @@ typedef struct LjSpline {
      * index by construction (built by lj_spline_aux_host). */
     const uint64_t *aux;    /* [2^radix_bits] */
     const uint32_t *sub;
+    int64_t nsub;           /* length of sub (0 without the accelerator) */
 } LjSpline;
 
 /* Spline-keyed chained hash view (learned_hash.py:17-101). */
@@ -267,7 +268,7 @@ int lj_spline_hash_probe_grouped(const LjSplineHash *idx, const uint64_t *s_pair
  * lj_spline_hash_bucket_capacity(nk, n) records; columns 16-B aligned. */
 int64_t lj_spline_hash_bucket_bins(int64_t n);
 int64_t lj_spline_hash_bucket_capacity(int64_t nk, int64_t n);
-size_t lj_spline_hash_bucket_est_workspace_bytes(int64_t nk, int64_t n);
+size_t lj_spline_hash_bucket_est_workspace_bytes(const LjSplineHash *idx, int64_t nk);
 int lj_spline_hash_bucket_est(const LjSplineHash *idx, const uint64_t *keys, const uint64_t *pay, int64_t nk,
                               uint64_t *pairs_out, int64_t *reg_out, void *ws, size_t ws_bytes, void *stream);
 /* K5 over those regions, handed out to the CTAs in record order by a chunk

@@ -51,7 +51,7 @@ class LjGrmi(ctypes.Structure):
 class LjSpline(ctypes.Structure):
     _fields_ = [("npts", _i64), ("n", _i64), ("max_error", _i64), ("radix_bits", _i64), ("shift", _u64),
                 ("keys", _c_void_p), ("ranks", _c_void_p), ("radix", _c_void_p), ("aux", _c_void_p),
-                ("sub", _c_void_p)]
+                ("sub", _c_void_p), ("nsub", _i64)]
 
 
 class LjSplineHash(ctypes.Structure):
@@ -112,7 +112,7 @@ SIGNATURES = {
     "lj_lsj_key_bounds": (_int, [ctypes.POINTER(LjLsjModel), _P, _P, _size_t, _P]),
     "lj_spline_hash_bucket_bins": (_i64, [_i64]),
     "lj_spline_hash_bucket_capacity": (_i64, [_i64, _i64]),
-    "lj_spline_hash_bucket_est_workspace_bytes": (_size_t, [_i64, _i64]),
+    "lj_spline_hash_bucket_est_workspace_bytes": (_size_t, [ctypes.POINTER(LjSplineHash), _i64]),
     "lj_spline_hash_bucket_est": (_int, [ctypes.POINTER(LjSplineHash), _P, _P, _i64, _P, _P, _P, _size_t, _P]),
     "lj_spline_hash_probe_regions": (_int, [ctypes.POINTER(LjSplineHash), _P, _P, _i64, _P, _size_t, _P, _int, _P]),
     "lj_spline_hash_count": (_int, [ctypes.POINTER(LjSplineHash), _P, _i64, _P, _P]),

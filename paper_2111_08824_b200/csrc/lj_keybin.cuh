@@ -90,6 +90,7 @@ static __global__ void __launch_bounds__(1024) k_keybin_build(u64 *lay, int nb) 
     __shared__ u64 s_t0[2];
     __shared__ int s_shift[2];
     __shared__ u64 pm[KB_MAXBINS];
+    __shared__ u16 cand[KB_CELLS + 1];
     u64 *B = lay + 4;
     const int tid = threadIdx.x;
     // the boundaries must be non-decreasing: a running maximum (a no-op
@@ -125,29 +126,35 @@ static __global__ void __launch_bounds__(1024) k_keybin_build(u64 *lay, int nb) 
         s_shift[tid] = s;
     }
     __syncthreads();
-    // #{ j in [1, nb) : cell(B[j]) < c }  (cell() non-decreasing in j;
-    // searched in the shared-memory copy)
-    auto below = [&](int m, int c) {
-        int lo = 1, hi = nb;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if ((int)kb_cell(kb_image(pm[mid], m), s_t0[m], s_shift[m]) < c) lo = mid + 1;
-            else hi = mid;
-        }
-        return lo - 1;
+    // cells[c] = #{ j in [1, nb) : c_j < c } with c_j = cell(B[j])
+    // (non-decreasing in j): value j on (c_j, c_{j+1}], c_0 = -1,
+    // c_nb = KB_CELLS -- one thread per boundary fills its range
+    auto cellj = [&](int m, int j) -> int {
+        if (j <= 0) return -1;
+        if (j >= nb) return KB_CELLS;
+        return (int)kb_cell(kb_image(pm[j], m), s_t0[m], s_shift[m]);
     };
-    for (int m = 0; m < 2; ++m) {
+    auto fill = [&](int m) {
+        for (int j = tid; j < nb; j += blockDim.x) {
+            const int lo = cellj(m, j) + 1, hi = cellj(m, j + 1);
+            for (int c = lo; c <= hi; ++c) cand[c] = (u16)j;
+        }
+        __syncthreads();
+    };
+    for (int m = 1; m >= 0; --m) {  // mode 0 last: it stays in cand unless mode 1 wins
+        fill(m);
         u32 w = 0;
         for (int c = tid; c < KB_CELLS; c += blockDim.x) {
-            const u32 d = (u32)(below(m, c + 1) - below(m, c));
+            const u32 d = (u32)cand[c + 1] - (u32)cand[c];
             w = d > w ? d : w;
         }
         atomicMax(&worst[m], w);
+        __syncthreads();
     }
-    __syncthreads();
     const int m = worst[1] < worst[0] ? 1 : 0;
+    if (m == 1) fill(1);
     u16 *cells = reinterpret_cast<u16 *>(lay + 4 + ((nb + 3) & ~3));
-    for (int c = tid; c <= KB_CELLS; c += blockDim.x) cells[c] = (u16)below(m, c);
+    for (int c = tid; c <= KB_CELLS; c += blockDim.x) cells[c] = cand[c];
     if (tid == 0) {
         lay[0] = s_t0[m];
         lay[1] = (u64)s_shift[m] | ((u64)m << 8);

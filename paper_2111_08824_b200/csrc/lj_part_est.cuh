@@ -29,30 +29,6 @@ constexpr size_t EST_STAGE = (size_t)EST_TILE * 16;
 // capacity of the output (records) for n tuples in nb bins: regions + overflow
 inline i64 est_capacity(i64 n, int nb) { return n + n / 16 + (i64)nb * (EST_PAD + EST_STRIDE + 1) + 64 + n; }
 
-// +1 on h[b] for every lane with b >= 0; a warp whose lanes all carry the
-// same bin (runs of a hot key) adds 32 with one atomic instead of 32
-// serialised ones.  Every lane of the warp must call it.
-__device__ __forceinline__ void warp_count(u32 *h, int b) {
-    const int b0 = __shfl_sync(0xffffffffu, b, 0);
-    if (__all_sync(0xffffffffu, b == b0)) {
-        if ((threadIdx.x & 31) == 0 && b0 >= 0) atomicAdd(h + b0, 32u);
-    } else if (b >= 0) {
-        atomicAdd(h + b, 1u);
-    }
-}
-
-// rank of every lane's tuple in its bin's run (lanes with b < 0: 0); the
-// same warp aggregation for a warp on one bin
-__device__ __forceinline__ int warp_rank(u32 *h, int b) {
-    const int b0 = __shfl_sync(0xffffffffu, b, 0);
-    if (__all_sync(0xffffffffu, b == b0)) {
-        u32 r = 0;
-        if ((threadIdx.x & 31) == 0 && b0 >= 0) r = atomicAdd(h + b0, 32u);
-        return b0 >= 0 ? (int)(__shfl_sync(0xffffffffu, r, 0) + (threadIdx.x & 31)) : 0;
-    }
-    return b >= 0 ? (int)atomicAdd(h + b, 1u) : 0;
-}
-
 // per-bin counts of every `stride`-th tuple (stride 1: the exact histogram)
 template <class Src>
 __global__ void __launch_bounds__(256) k_est_sample(Src f0, i64 n, int nbins, int stride, u32 *est, u16 *codes) {
@@ -81,9 +57,10 @@ __global__ void __launch_bounds__(256) k_est_sample(Src f0, i64 n, int nbins, in
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const int b = i[u] < n ? (int)(f.code(k[u]) >> shift) : -1;
-            warp_count(h, b);
-            if (codes && b >= 0) codes[i[u]] = (u16)b;  // stride 1 only
+            if (i[u] >= n) continue;
+            const u32 b = f.code(k[u]) >> shift;
+            atomicAdd(h + b, 1u);
+            if (codes) codes[i[u]] = (u16)b;  // stride 1 only
         }
     }
     for (; blk * bs < n; blk += ngrp) {
@@ -195,7 +172,7 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_est(Src f0, i64 n, i64
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            rj[u] = warp_rank(thist, bj[u]);
+            rj[u] = bj[u] >= 0 ? (int)atomicAdd(thist + bj[u], 1u) : 0;
             if (bj[u] >= 0) tbin[u * PART2_NT + tid] = (u16)bj[u];
         }
         __syncthreads();

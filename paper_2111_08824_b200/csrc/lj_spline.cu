@@ -330,6 +330,42 @@ __global__ void k_fill_gaps(const i64 *reg, int nb, ulonglong2 *out) {
 // the exact bucket), and that rank is within one bucket's span of the
 // key's position, so a window's chains stay in one small stretch of the
 // table.  (The exact spline evaluation here cost 50 ms at C3.)
+// PosBin with the last two loads folded into precomputed tables: the window
+// of the first spline point of k's (sub-)radix bucket, per radix bucket
+// (wrad) and per sub-table entry (wsub) -- the same bin for every key, one
+// dependent load fewer (aux -> window instead of aux -> sub -> ranks).
+struct WinBin : NoTable {
+    const u64 *aux;
+    const u16 *wrad, *wsub;
+    u64 kshift;
+    u64 rmax;
+    int shift = 0;
+    __device__ __forceinline__ u32 code(u64 k) const {
+        const u64 raw = kshift >= 64 ? 0 : (k >> kshift);
+        const u64 ax = (aux && raw <= rmax) ? ldg(aux + raw) : 0;
+        if (ax & 0xFF) {
+            const int bits = (int)(ax & 0xFF);
+            const u64 q = (k >> (kshift - (u64)bits)) & ((1ULL << bits) - 1ULL);
+            return __ldg(wsub + (ax >> 8) + q);
+        }
+        return __ldg(wrad + (raw > rmax ? rmax : raw));
+    }
+    __device__ __forceinline__ WinBin at(u64 *) const { return *this; }
+};
+
+__device__ __forceinline__ u16 win_of_point(const SplineDev &m, i64 lo, i64 nb, double rn) {
+    lo = lo < 0 ? 0 : (lo > m.K - 1 ? m.K - 1 : lo);
+    const i64 b = (i64)(__ldg(m.ranks + lo) * rn);
+    return (u16)(b < 0 ? 0 : (b >= nb ? nb - 1 : b));
+}
+
+__global__ void k_win_tables(SplineDev m, i64 nb, double rn, u16 *wrad, i64 nrad, u16 *wsub, i64 nsub) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < nrad + nsub; i += (i64)gridDim.x * blockDim.x) {
+        if (i < nrad) wrad[i] = win_of_point(m, (i64)__ldg(m.radix + i), nb, rn);
+        else wsub[i - nrad] = win_of_point(m, (i64)__ldg(m.sub + (i - nrad)), nb, rn);
+    }
+}
+
 struct PosBin : NoTable {
     SplineDev m;
     i64 nb, n;
@@ -404,8 +440,17 @@ int64_t lj_spline_hash_bucket_bins(int64_t n) { return hash_bins(n); }
 
 int64_t lj_spline_hash_bucket_capacity(int64_t nk, int64_t n) { return est_capacity(nk < 0 ? 0 : nk, hash_bins(n)); }
 
-size_t lj_spline_hash_bucket_est_workspace_bytes(int64_t nk, int64_t n) {
-    return est_workspace_bytes(hash_bins(n)) + part_align(sizeof(u16) * (size_t)(nk < 0 ? 0 : nk));
+// window tables of the grouping (WinBin): u16 per radix bucket and per
+// sub-table entry
+static size_t win_tables_bytes(const LjSpline &m) {
+    if (m.npts <= 1 || m.radix_bits > 24) return 0;
+    return part_align(sizeof(u16) * ((size_t)1 << m.radix_bits)) + part_align(sizeof(u16) * (size_t)(m.nsub + 1));
+}
+
+size_t lj_spline_hash_bucket_est_workspace_bytes(const LjSplineHash *idx, int64_t nk) {
+    if (!idx) return 0;
+    const int nb = hash_bins(idx->model.n);
+    return est_workspace_bytes(nb) + part_align(sizeof(u16) * (size_t)(nk < 0 ? 0 : nk)) + win_tables_bytes(idx->model);
 }
 
 // exact regions in lj_leaf_bucket's layout: ends = next starts, no overflow
@@ -427,6 +472,30 @@ int lj_spline_hash_bucket_est(const LjSplineHash *idx, const uint64_t *keys, con
     f.n = idx->model.n;
     f.rn = (double)f.nb / (double)idx->model.n;
     SoaSrc<PosBin> src{keys, pay, f};
+    const size_t wtb = win_tables_bytes(idx->model);
+    static const bool no_win = getenv("LJ_HASH_POSBIN") != nullptr;
+    if (!no_win && wtb && idx->model.aux && ws_bytes >= est_workspace_bytes((int)f.nb) + wtb) {
+        // one pass with the window tables (last bytes of the workspace)
+        const size_t nrad = (size_t)1 << idx->model.radix_bits;
+        u16 *wrad = reinterpret_cast<u16 *>((char *)ws + ws_bytes - wtb);
+        u16 *wsub = reinterpret_cast<u16 *>((char *)wrad + part_align(sizeof(u16) * nrad));
+        k_win_tables<<<grid_for((i64)nrad + idx->model.nsub, 256, 4), 256, 0, st>>>(
+            f.m, f.nb, f.rn, wrad, (i64)nrad, wsub, idx->model.nsub);
+        LJ_CK_LAUNCH();
+        WinBin wb;
+        wb.aux = idx->model.aux;
+        wb.wrad = wrad;
+        wb.wsub = wsub;
+        wb.kshift = idx->model.shift;
+        wb.rmax = nrad - 1;
+        SoaSrc<WinBin> wsrc{keys, pay, wb};
+        const int rc = run_partition_est(wsrc, nk, (int)f.nb, reinterpret_cast<ulonglong2 *>(pairs_out), reg_out, ws,
+                                         ws_bytes - wtb, st);
+        if (rc) return rc;
+        k_fill_gaps<<<(unsigned)f.nb, 256, 0, st>>>(reg_out, (int)f.nb, reinterpret_cast<ulonglong2 *>(pairs_out));
+        LJ_CK_LAUNCH();
+        return LJ_OK;
+    }
     // LJ_HASH_EXACT=1: a counting pass stores every probe's window (u16)
     // and the claims scatter streams them (no gaps, no overflow); measured
     // 42.4 ms vs 37.7 ms for the one-pass default at C3 (the counting pass

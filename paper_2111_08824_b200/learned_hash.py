@@ -107,7 +107,8 @@ class SplineHashIndex:
         nb = lib.lj_spline_hash_bucket_bins(tl)
         return {"pairs": torch.empty(2 * max(cap, 1), dtype=torch.int64, device=dev),
                 "reg": torch.empty(2 * nb + 2, dtype=torch.int64, device=dev), "nbins": nb,
-                "ws": _lib.workspace(max(lib.lj_spline_hash_bucket_est_workspace_bytes(n, tl), 8), dev)}
+                "ws": _lib.workspace(max(lib.lj_spline_hash_bucket_est_workspace_bytes(ctypes.byref(self.c_struct()), n),
+                                         8), dev)}
 
     def join_checksum_buffered(self, s_keys: torch.Tensor, s_payloads: torch.Tensor,
                                out: torch.Tensor | None = None, accumulate: bool = False, scratch: dict | None = None,

@@ -250,7 +250,8 @@ class RadixSplineIndex:
         self._check_fitted()
         return _lib.LjSpline(self.spline_keys.size, self.trained_len, self.max_error, self.radix_bits,
                              int(self.shift), _lib.ptr(self._d_keys), _lib.ptr(self._d_ranks),
-                             _lib.ptr(self._d_radix), _lib.ptr(self._d_aux), _lib.ptr(self._d_sub))
+                             _lib.ptr(self._d_radix), _lib.ptr(self._d_aux), _lib.ptr(self._d_sub),
+                             0 if self._d_sub is None else self._d_sub.numel())
 
     def _check_fitted(self):
         if self.trained_len == 0:
