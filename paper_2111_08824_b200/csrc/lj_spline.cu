@@ -528,9 +528,17 @@ int lj_spline_hash_probe_regions(const LjSplineHash *idx, const uint64_t *s_pair
     unsigned long long *ctr = reinterpret_cast<unsigned long long *>(ws);
     LJ_CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
     constexpr int NT = 256;
-    static const int per_sm = getenv("LJ_HASH_CTAS") ? atoi(getenv("LJ_HASH_CTAS")) : 4;
-    k_hash_probe_chunks<NT, 4, 8><<<sm_count() * per_sm, NT, 0, st>>>(
-        HashDev(*idx), reinterpret_cast<const ulonglong2 *>(s_pairs), reg, (int)nbins, ctr, out);
+    // measured at C3 (ms): U=4 x 3 CTAs/SM 37.5, U=4 x 4 32.4, U=2 x 6 30.0, U=8 38.4
+    static const int per_sm = getenv("LJ_HASH_CTAS") ? atoi(getenv("LJ_HASH_CTAS")) : 6;
+    static const int u = getenv("LJ_HASH_U") ? atoi(getenv("LJ_HASH_U")) : 2;
+    const HashDev hd(*idx);
+    const ulonglong2 *rec = reinterpret_cast<const ulonglong2 *>(s_pairs);
+    if (u == 2)
+        k_hash_probe_chunks<NT, 2, 16><<<sm_count() * per_sm, NT, 0, st>>>(hd, rec, reg, (int)nbins, ctr, out);
+    else if (u == 8)
+        k_hash_probe_chunks<NT, 8, 4><<<sm_count() * per_sm, NT, 0, st>>>(hd, rec, reg, (int)nbins, ctr, out);
+    else
+        k_hash_probe_chunks<NT, 4, 8><<<sm_count() * per_sm, NT, 0, st>>>(hd, rec, reg, (int)nbins, ctr, out);
     LJ_CK_LAUNCH();
     return LJ_OK;
 }
