@@ -14,6 +14,9 @@ import torch
 
 from .build import LIB
 
+# diagnostics: load an alternative build of the same ABI (e.g. a tuning variant)
+LIB = os.environ.get("LJ_LIB", LIB)
+
 _c_void_p = ctypes.c_void_p
 _i64 = ctypes.c_int64
 _u64 = ctypes.c_uint64
