@@ -837,7 +837,6 @@ __global__ void __launch_bounds__(JOIN_NT) k_lsj_join(const ulonglong2 *__restri
         const i64 a = tile * JOIN_T, e = min(a + (i64)JOIN_T, ns);
         const int ne = (int)(e - a);
         const i64 wlo = nlo, whi = nhi, w = whi - wlo;
-        const bool staged = w <= WCAP;
         const i64 nt = tile + gridDim.x;
         if (nt < ntiles) {
             nlo = tb[2 * nt];
@@ -847,54 +846,70 @@ __global__ void __launch_bounds__(JOIN_NT) k_lsj_join(const ulonglong2 *__restri
                 bulk_prefetch_l2(S + na, (unsigned)(nn * sizeof(ulonglong2)));
             }
         }
-        if (staged) {
-            for (int j = threadIdx.x; j < (int)w; j += JOIN_NT) wk[j] = R[wlo + j].x;
-            if (threadIdx.x == 0) wk[w] = ~0ULL;  // sentinel above every key
-        }
         for (int j = threadIdx.x; j < ne; j += JOIN_NT) {
             const ulonglong2 v = S[a + j];
             sk[j] = v.x;
             sp[j] = v.y;
         }
-        __syncthreads();
+        // The R slice goes through shared memory in chunks of WCAP keys (one
+        // chunk for almost every tile; a sparse stretch of S -- the Zipf tail
+        // of C4 -- can face a slice of 10^4+ keys).  Each thread owns JOIN_PER
+        // consecutive (sorted) S keys and resolves, per chunk, those not
+        // above the chunk's last key: their lower bound lies in the chunk.
         const int j0 = threadIdx.x * JOIN_PER;
-        i64 pos = 0;  // lower bound of the previous S key, relative to wlo
-        for (int u = 0; u < JOIN_PER; ++u) {
-            const int j = j0 + u;
-            if (j >= ne) break;
-            const u64 k = sk[j];
-            if (u == 0 || !staged) {
-                i64 lo = u == 0 ? 0 : pos, hi = w;
-                while (lo < hi) {
-                    const i64 mid = (lo + hi) >> 1;
-                    if ((staged ? wk[mid] : R[wlo + mid].x) < k) lo = mid + 1; else hi = mid;
+        int un = 0;     // next unresolved key of this thread
+        int pos = 0;    // lower bound of the previous key, chunk-relative
+        for (i64 c0 = 0; c0 < w || (c0 == 0 && w == 0); c0 += WCAP) {
+            const int cl = (int)min((i64)WCAP, w - c0);
+            for (int j = threadIdx.x; j < cl; j += JOIN_NT) wk[j] = R[wlo + c0 + j].x;
+            if (threadIdx.x == 0) wk[cl] = ~0ULL;  // sentinel above every key
+            __syncthreads();
+            const u64 clast = cl > 0 ? wk[cl - 1] : 0;
+            const bool last_chunk = c0 + cl >= w;
+            bool fresh = true;  // first key resolved in this chunk: binary search
+            for (; un < JOIN_PER; ++un) {
+                const int j = j0 + un;
+                if (j >= ne) {
+                    un = JOIN_PER;
+                    break;
                 }
-                pos = lo;
-            } else {
-                while (wk[pos] < k) ++pos;  // S is sorted: lower bounds only grow
-            }
-            const i64 i = a + j;
-            i64 c = 0, o = mode == 2 ? offsets[i] : 0;
-            for (i64 q = pos; q < w; ++q) {
-                const u64 rk = staged ? wk[q] : R[wlo + q].x;
-                if (rk != k) break;
-                if (mode == 0) {
-                    const u64 v = R[wlo + q].y + sp[j];
-                    ++cnt;
-                    sum += v;
-                    x ^= v;
-                } else if (mode == 2) {
-                    opr[o] = R[wlo + q].y;
-                    ops[o] = sp[j];
-                    ++o;
+                const u64 k = sk[j];
+                if (!last_chunk && k > clast) break;  // lower bound in a later chunk
+                if (fresh) {
+                    int lo = 0, hi = cl;
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (wk[mid] < k) lo = mid + 1; else hi = mid;
+                    }
+                    pos = lo;
+                    fresh = false;
+                } else {
+                    while (wk[pos] < k) ++pos;  // S is sorted: lower bounds only grow
                 }
-                ++c;
+                const i64 i = a + j;
+                i64 c = 0, o = mode == 2 ? offsets[i] : 0;
+                for (i64 q = c0 + pos; q < w; ++q) {  // equal run (may run past the chunk)
+                    const u64 rk = q - c0 < cl ? wk[q - c0] : R[wlo + q].x;
+                    if (rk != k) break;
+                    if (mode == 0) {
+                        const u64 v = R[wlo + q].y + sp[j];
+                        ++cnt;
+                        sum += v;
+                        x ^= v;
+                    } else if (mode == 2) {
+                        opr[o] = R[wlo + q].y;
+                        ops[o] = sp[j];
+                        ++o;
+                    }
+                    ++c;
+                }
+                if (mode == 1) counts[i] = c;
             }
-            if (mode == 1) counts[i] = c;
+            __syncthreads();  // the chunk buffer is refilled next round
+            if (w == 0) break;
         }
         if (threadIdx.x == 0 && nt < ntiles && nhi - nlo > 0 && nhi - nlo <= WCAP)
             bulk_prefetch_l2(R + nlo, (unsigned)((nhi - nlo) * sizeof(ulonglong2)));
-        __syncthreads();
     }
     if (mode == 0) reduce_checksum(cnt, sum, x, 0, out);
 }

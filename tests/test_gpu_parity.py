@@ -583,3 +583,20 @@ def test_lsj_join_host_overlapped_equals_device(lj):
     want, _ = lj.lsj_join(inp.r, inp.s, cfg)
     got = lj.lsj_join_host(inp.r.keys.cpu(), inp.r.payloads.cpu(), inp.s.keys.cpu(), inp.s.payloads.cpu(), cfg)
     assert got.checksum == want.checksum == tuple(oracle.smj_checksum(*inp.r.numpy(), *inp.s.numpy()))
+
+
+def test_lsj_join_wide_r_slices(lj):
+    """A sparse S against a dense R: every S tile faces an R slice far wider
+    than one shared-memory chunk (and equal-key runs of R that cross chunk
+    boundaries): the chunked merge equals the oracle."""
+    rng = np.random.default_rng(23)
+    base = np.unique(rng.integers(0, 2**40, 400000, dtype=np.uint64))
+    reps = np.ones(base.size, dtype=np.int64)
+    reps[::50000] = 9000  # runs longer than a chunk
+    rk = np.repeat(base, reps)
+    sk = np.concatenate([rng.choice(base, 3000), base[::50000], rng.integers(0, 2**40, 500, dtype=np.uint64)])
+    r = lj.make_relation(rk, 5)
+    s = lj.make_relation(sk, 6)
+    for fanout in (64, 4096):
+        res, _ = lj.lsj_join(r, s, lj.LsjConfig(fanout=fanout, sample_rate=0.05))
+        assert res.checksum == tuple(oracle.smj_checksum(*r.numpy(), *s.numpy())), fanout
