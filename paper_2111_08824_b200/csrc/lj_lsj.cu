@@ -302,13 +302,45 @@ __device__ __forceinline__ int y_slice(double y, double ybase, double scale, int
     return f < 0.0 ? 0 : (f >= (double)(F - 1) ? F - 1 : (int)f);
 }
 
-// point-slice mode: slot = 2 * lower_bound(v, y) + (y == v[lb])
-// slot of key k among split keys v[0..K): 2i for keys in (v[i-1], v[i]),
-// 2i+1 for k == v[i] (a repeated hot key gets a slice of its own)
-__device__ __forceinline__ int point_slot(const u64 *v, int K, u64 k) {
-    int lo = 0, hi = K;
+// point-slice mode: slot of key k among split keys v[0..K): 2i for keys in
+// (v[i-1], v[i]), 2i+1 for k == v[i] (a repeated hot key gets a slice of
+// its own), i = lower_bound(v, k):
+// found through a radix table over the split keys (built per work
+// item in shared memory): cells[c] = #{ i : cell(v[i]) < c } bounds the
+// lower bound to [cells[c], cells[c+1]] (cell() monotone), so the search
+// runs over a cell's few keys instead of all K.
+constexpr int SPLIT_CELLS = 1024;
+struct SplitTab {
+    u64 v0;
+    int sh;
+};
+__device__ __forceinline__ int split_cell(const SplitTab &t, u64 k) {
+    if (k < t.v0) return 0;
+    const u64 c = (k - t.v0) >> t.sh;
+    return c >= (u64)SPLIT_CELLS ? SPLIT_CELLS - 1 : (int)c;
+}
+// all threads; v[0..K) staged and synced; returns the table parameters
+__device__ SplitTab split_tab_build(const u64 *v, int K, u16 *cells) {
+    SplitTab t;
+    t.v0 = K ? v[0] : 0;
+    const u64 span = K ? v[K - 1] - t.v0 : 0;
+    int sh = 0;
+    while (sh < 63 && (span >> sh) >= (u64)SPLIT_CELLS) ++sh;
+    t.sh = sh;
+    // value i on (c_{i-1}, c_i], c_{-1} = -1, c_K = SPLIT_CELLS
+    for (int i = threadIdx.x; i <= K; i += blockDim.x) {
+        const int lo = i == 0 ? 0 : split_cell(t, v[i - 1]) + 1;
+        const int hi = i == K ? SPLIT_CELLS : split_cell(t, v[i]);
+        for (int c = lo; c <= hi; ++c) cells[c] = (u16)i;
+    }
+    __syncthreads();
+    return t;
+}
+__device__ __forceinline__ int point_slot_tab(const u64 *v, int K, const u16 *cells, const SplitTab &t, u64 k) {
+    const int c = split_cell(t, k);
+    int lo = cells[c], hi = cells[c + 1];  // lower bound in [lo, hi]
     while (lo < hi) {
-        int mid = (lo + hi) >> 1;
+        const int mid = (lo + hi) >> 1;
         if (v[mid] < k) lo = mid + 1; else hi = mid;
     }
     return 2 * lo + ((lo < K && v[lo] == k) ? 1 : 0);
@@ -374,8 +406,9 @@ __device__ __forceinline__ SplitItem split_item(const LsjDev &md, const SplitCtx
     return it;
 }
 
-__device__ __forceinline__ int split_slot(const LsjDev &md, const SplitItem &it, const u64 *v, bool points, u64 k) {
-    return points ? point_slot(v, it.K, k) : y_slice(md.y(k), it.ybase, it.scale, it.F);
+__device__ __forceinline__ int split_slot(const LsjDev &md, const SplitItem &it, const u64 *v, bool points, u64 k,
+                                          const u16 *cells, const SplitTab &tab) {
+    return points ? point_slot_tab(v, it.K, cells, tab, k) : y_slice(md.y(k), it.ybase, it.scale, it.F);
 }
 
 // pass 1: mat[mbase[b] + s * chunks_b + c] = tuples of chunk c in slot s
@@ -383,6 +416,7 @@ __global__ void __launch_bounds__(SPLIT_NT) k_split_count(LsjDev md, SplitCtx cx
                                                           const i64 *nitems, u32 *mat, SortCtl *ctl) {
     __shared__ u32 h[2 * SPLIT_MAXF];
     __shared__ u64 v[SPLIT_MAXF];
+    __shared__ u16 cells[SPLIT_CELLS + 1];
     __shared__ i64 s_q;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool points = md.sample != nullptr;
@@ -396,12 +430,13 @@ __global__ void __launch_bounds__(SPLIT_NT) k_split_count(LsjDev md, SplitCtx cx
         for (int j = threadIdx.x; j < it.F; j += SPLIT_NT) h[j] = 0;
         for (int j = threadIdx.x; j < it.K; j += SPLIT_NT) v[j] = cx.spv[it.g0 + j];
         __syncthreads();
+        const SplitTab tab = points ? split_tab_build(v, it.K, cells) : SplitTab{0, 0};
         for (i64 base = it.a + (i64)warp * 32 * SPLIT_U; base < it.e; base += (i64)SPLIT_NT * SPLIT_U) {
             int s[SPLIT_U];
 #pragma unroll
             for (int u = 0; u < SPLIT_U; ++u) {
                 const i64 i = base + u * 32 + lane;
-                s[u] = i < it.e ? split_slot(md, it, v, points, A[i].x) : -1;
+                s[u] = i < it.e ? split_slot(md, it, v, points, A[i].x, cells, tab) : -1;
             }
 #pragma unroll
             for (int u = 0; u < SPLIT_U; ++u) {
@@ -468,6 +503,7 @@ __global__ void __launch_bounds__(SPLIT_NT) k_split_scatter(LsjDev md, SplitCtx 
                                                             ulonglong2 *B, ulonglong2 *Out, SortCtl *ctl) {
     __shared__ u32 cur[2 * SPLIT_MAXF];
     __shared__ u64 v[SPLIT_MAXF];
+    __shared__ u16 cells[SPLIT_CELLS + 1];
     __shared__ i64 s_q;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool points = md.sample != nullptr;
@@ -482,6 +518,7 @@ __global__ void __launch_bounds__(SPLIT_NT) k_split_scatter(LsjDev md, SplitCtx 
         for (int j = threadIdx.x; j < it.F; j += SPLIT_NT) cur[j] = (u32)(off[mb + (i64)j * it.chunks + it.c] - a0);
         for (int j = threadIdx.x; j < it.K; j += SPLIT_NT) v[j] = cx.spv[it.g0 + j];
         __syncthreads();
+        const SplitTab tab = points ? split_tab_build(v, it.K, cells) : SplitTab{0, 0};
         for (i64 base = it.a + (i64)warp * 32 * SPLIT_U; base < it.e; base += (i64)SPLIT_NT * SPLIT_U) {
             int s[SPLIT_U];
             ulonglong2 r[SPLIT_U];
@@ -489,7 +526,7 @@ __global__ void __launch_bounds__(SPLIT_NT) k_split_scatter(LsjDev md, SplitCtx 
             for (int u = 0; u < SPLIT_U; ++u) {
                 const i64 i = base + u * 32 + lane;
                 r[u] = i < it.e ? A[i] : make_ulonglong2(0, 0);
-                s[u] = i < it.e ? split_slot(md, it, v, points, r[u].x) : -1;
+                s[u] = i < it.e ? split_slot(md, it, v, points, r[u].x, cells, tab) : -1;
             }
 #pragma unroll
             for (int u = 0; u < SPLIT_U; ++u) {
