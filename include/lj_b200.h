@@ -236,6 +236,14 @@ int lj_grmi_probe_pairs(const LjGrmi *idx, const uint64_t *s_pairs, int64_t nk, 
 int lj_spline_fit_host(const uint64_t *sorted_keys_host, int64_t n, int64_t max_error,
                        int64_t radix_bits, uint64_t *keys_out_host, int64_t *ranks_out_host,
                        int64_t *radix_out_host, int64_t *npts_out, uint64_t *shift_out);
+/* The same fit on the DEVICE over device-sorted keys (speculative chunks
+ * spliced where they converge, repaired in order on the device when they do
+ * not): knot_keys/knot_ranks hold up to n entries, radix_out 2^r+1 (all
+ * device); *npts_out / *shift_out on the host.  Identical knots. */
+size_t lj_spline_fit_workspace_bytes(int64_t n);
+int lj_spline_fit(const uint64_t *sorted_keys, int64_t n, int64_t max_error, int64_t radix_bits,
+                  uint64_t *knot_keys, int64_t *knot_ranks, int64_t *radix_out, int64_t *npts_out,
+                  uint64_t *shift_out, void *ws, size_t ws_bytes, void *stream);
 /* Build the LjSpline.aux/sub accelerator on the host: every radix bucket
  * holding more than 8 spline points gets ceil(log2(count)) + 1 extra key
  * bits.  Call with sub_host = NULL to get the required sub length. */

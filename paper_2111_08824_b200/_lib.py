@@ -101,6 +101,8 @@ SIGNATURES = {
     "lj_grmi_probe_bucketed_img": (_int, [ctypes.POINTER(LjGrmi), _P, _P, _P, _P, _P, _int, _P]),
     "lj_grmi_probe_pairs": (_int, [ctypes.POINTER(LjGrmi), _P, _i64, _P, _int, _P]),
     "lj_spline_fit_host": (_int, [_P, _i64, _i64, _i64, _P, _P, _P, _P, _P]),
+    "lj_spline_fit_workspace_bytes": (_size_t, [_i64]),
+    "lj_spline_fit": (_int, [_P, _i64, _i64, _i64, _P, _P, _P, _P, _P, _P, _size_t, _P]),
     "lj_spline_aux_host": (_int, [_P, _i64, _P, _i64, _u64, _P, _P, _P]),
     "lj_spline_predict": (_int, [ctypes.POINTER(LjSpline), _P, _i64, _P, _P, _P, _P]),
     "lj_spline_partition_index": (_int, [ctypes.POINTER(LjSpline), _P, _i64, _i64, _P, _P]),

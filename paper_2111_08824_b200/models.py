@@ -11,6 +11,7 @@ the reference's numpy arithmetic (see csrc/lj_common.cuh).
 from __future__ import annotations
 
 import ctypes
+import os
 import uuid
 from typing import NamedTuple
 
@@ -181,6 +182,9 @@ class RadixSplineIndex:
         return {"max_error": self.max_error, "radix_bits": self.radix_bits}
 
     def fit(self, sorted_keys) -> "RadixSplineIndex":
+        if (isinstance(sorted_keys, torch.Tensor) and sorted_keys.is_cuda and sorted_keys.numel() > 0
+                and not os.environ.get("LJ_HOST_SPLINE_FIT")):
+            return self._fit_device(sorted_keys)
         if isinstance(sorted_keys, torch.Tensor):
             host = to_numpy_u64(sorted_keys)
         else:
@@ -203,6 +207,29 @@ class RadixSplineIndex:
         _lib.check(rc, "spline_fit")
         k = npts.value
         return self._adopt(sk[:k], sr[:k], rt, shift.value, n)
+
+    def _fit_device(self, keys: torch.Tensor) -> "RadixSplineIndex":
+        """models.py:171-219 on the device (lj_spline_fit): speculative
+        greedy runs per chunk, spliced where they converge -- the host
+        fit's knots exactly."""
+        k = keys.contiguous()
+        if bool((k == -1).any()):
+            raise ValueError("keys may not contain the reserved maximum key")
+        check_sorted(k)
+        n = k.numel()
+        dev = k.device
+        kk = torch.empty(n, dtype=torch.int64, device=dev)
+        rr = torch.empty(n, dtype=torch.int64, device=dev)
+        rt = torch.empty((1 << self.radix_bits) + 1, dtype=torch.int64, device=dev)
+        lib = _lib.lib()
+        ws = _lib.workspace(lib.lj_spline_fit_workspace_bytes(n), dev)
+        npts = ctypes.c_int64(0)
+        shift = ctypes.c_uint64(0)
+        _lib.check(lib.lj_spline_fit(_lib.ptr(k), n, self.max_error, self.radix_bits, _lib.ptr(kk), _lib.ptr(rr),
+                                     _lib.ptr(rt), ctypes.byref(npts), ctypes.byref(shift), _lib.ptr(ws), ws.numel(),
+                                     _lib.stream_ptr()), "spline_fit")
+        kn = npts.value
+        return self._adopt(to_numpy_u64(kk[:kn]), rr[:kn].cpu().numpy(), rt.cpu().numpy(), shift.value, n, device=dev)
 
     def _adopt(self, spline_keys, spline_ranks, radix_table, shift, trained_len, device=None):
         dev = device or "cuda"

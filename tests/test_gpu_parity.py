@@ -600,3 +600,53 @@ def test_lsj_join_wide_r_slices(lj):
     for fanout in (64, 4096):
         res, _ = lj.lsj_join(r, s, lj.LsjConfig(fanout=fanout, sample_rate=0.05))
         assert res.checksum == tuple(oracle.smj_checksum(*r.numpy(), *s.numpy())), fanout
+
+
+def _fit_both(lj, keys, err=32, bits=18, monkeypatch=None):
+    k = np.sort(np.asarray(keys, dtype=np.uint64))
+    dev = torch.from_numpy(k.view(np.int64)).cuda()
+    gpu = lj.RadixSplineIndex(err, bits).fit(dev)
+    monkeypatch.setenv("LJ_HOST_SPLINE_FIT", "1")
+    host = lj.RadixSplineIndex(err, bits).fit(dev)
+    monkeypatch.delenv("LJ_HOST_SPLINE_FIT")
+    return gpu, host
+
+
+@pytest.mark.parametrize("dist", ["uniform", "lognormal", "clusters", "dups", "dense", "linear", "collide53"])
+def test_spline_fit_on_device_equals_host(lj, dist, monkeypatch):
+    """The device greedy corridor (speculative chunks spliced where they
+    converge, repaired in order where they do not) gives the host fit's --
+    the reference's -- knots, ranks, radix table and shift exactly.
+    "linear" has chunks without any knot (the repair path); "collide53" has
+    distinct keys that round to the same float64."""
+    rng = np.random.default_rng(31)
+    n = 300_000
+    if dist == "linear":
+        keys = np.arange(n, dtype=np.uint64) * np.uint64(7919) + np.uint64(10**9)
+    elif dist == "collide53":
+        keys = np.uint64(2**60) + rng.integers(0, 2**12, n, dtype=np.uint64) * np.uint64(3)
+    else:
+        keys = _dist_keys(rng, dist, n)
+    for err, bits in ((32, 18), (4, 10), (1, 20)):
+        gpu, host = _fit_both(lj, keys, err, bits, monkeypatch)
+        assert np.array_equal(gpu.spline_keys, host.spline_keys), (dist, err)
+        assert np.array_equal(gpu.spline_ranks, host.spline_ranks), (dist, err)
+        assert np.array_equal(gpu.radix_table, host.radix_table), (dist, err)
+        assert int(gpu.shift) == int(host.shift)
+
+
+def test_spline_fit_on_device_matches_golden(golden, lj, monkeypatch):
+    """The reference-fitted splines of the golden vectors, refit on device."""
+    checked = 0
+    for name, d in golden("models").items():
+        if "sp_keys" not in d:
+            continue
+        k = np.sort(np.asarray(d["keys"], dtype=np.uint64))
+        dev = torch.from_numpy(k.view(np.int64)).cuda()
+        m = lj.RadixSplineIndex(int(d["sp_max_error"]), int(d["sp_radix_bits"])).fit(dev)
+        assert np.array_equal(m.spline_keys, np.asarray(d["sp_keys"], dtype=np.uint64)), name
+        assert np.array_equal(m.spline_ranks, np.asarray(d["sp_ranks"], dtype=np.int64)), name
+        assert np.array_equal(m.radix_table, np.asarray(d["sp_radix_table"], dtype=np.int64)), name
+        assert int(m.shift) == int(d["sp_shift"]), name
+        checked += 1
+    assert checked >= 5
