@@ -756,12 +756,40 @@ __global__ void k_big_list(const i64 *list, int nbig, const i64 *sub_starts, i64
     }
 }
 
-// flags[q] = 1 if sub-bucket q holds more than one distinct key
-__global__ void k_big_check(const ulonglong2 *B, const i64 *big, const i64 *boff, int nbig, i64 total, int *flags) {
-    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < total; t += (i64)gridDim.x * blockDim.x) {
-        const int q = find_big(boff, nbig, t);
-        const i64 a = big[2 * q];
-        if (B[a + (t - boff[q])].x != B[a].x) flags[q] = 1;
+// one block per big sub-bucket q: flags[q] = 1 if it holds more than one
+// distinct key, kr[q] = {min, max} of its keys (block reductions, no atomics)
+__global__ void k_big_scan(const ulonglong2 *B, const i64 *big, int nbig, int *flags, unsigned long long *kr) {
+    __shared__ u64 smin[32], smax[32];
+    for (int q = blockIdx.x; q < nbig; q += gridDim.x) {
+        const i64 a = big[2 * q], len = big[2 * q + 1];
+        const u64 k0 = B[a].x;
+        u64 mn = k0, mx = k0;
+        for (i64 t = threadIdx.x; t < len; t += blockDim.x) {
+            const u64 k = B[a + t].x;
+            mn = k < mn ? k : mn;
+            mx = k > mx ? k : mx;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const u64 a1 = __shfl_xor_sync(0xffffffffu, mn, o), b1 = __shfl_xor_sync(0xffffffffu, mx, o);
+            mn = a1 < mn ? a1 : mn;
+            mx = b1 > mx ? b1 : mx;
+        }
+        const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        if ((threadIdx.x & 31) == 0) {
+            smin[w] = mn;
+            smax[w] = mx;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int i = 1; i < nw; ++i) {
+                mn = smin[i] < mn ? smin[i] : mn;
+                mx = smax[i] > mx ? smax[i] : mx;
+            }
+            flags[q] = mn != mx;
+            kr[2 * q] = mn;
+            kr[2 * q + 1] = mx;
+        }
+        __syncthreads();
     }
 }
 
@@ -786,21 +814,23 @@ __device__ __forceinline__ int find_seg(const i64 *cum, int nseg, i64 t) {
     return lo;
 }
 
-__global__ void k_seg_gather(const ulonglong2 *B, const i64 *pos, const i64 *cum, int nseg, i64 total, u64 *k,
-                             u64 *v) {
+// keys enter the segmented sort relative to their segment's minimum (base),
+// so only the bits that vary inside a segment are sorted
+__global__ void k_seg_gather(const ulonglong2 *B, const i64 *pos, const i64 *cum, const u64 *base, int nseg, i64 total,
+                             u64 *k, u64 *v) {
     for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < total; t += (i64)gridDim.x * blockDim.x) {
         const int j = find_seg(cum, nseg, t);
         const ulonglong2 e = B[pos[j] + (t - cum[j])];
-        k[t] = e.x;
+        k[t] = e.x - base[j];
         v[t] = e.y;
     }
 }
 
-__global__ void k_seg_scatter(const u64 *k, const u64 *v, const i64 *pos, const i64 *cum, int nseg, i64 total,
-                              ulonglong2 *out) {
+__global__ void k_seg_scatter(const u64 *k, const u64 *v, const i64 *pos, const i64 *cum, const u64 *base, int nseg,
+                              i64 total, ulonglong2 *out) {
     for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < total; t += (i64)gridDim.x * blockDim.x) {
         const int j = find_seg(cum, nseg, t);
-        out[pos[j] + (t - cum[j])] = make_ulonglong2(k[t], v[t]);
+        out[pos[j] + (t - cum[j])] = make_ulonglong2(k[t] + base[j], v[t]);
     }
 }
 
@@ -1181,6 +1211,7 @@ size_t lj_lsj_sort_workspace_bytes(int64_t n, int64_t nbins) {
            al(sizeof(double) * (size_t)G) +                                  // split values
            al(sizeof(i64) * (size_t)nbig) + al(sizeof(i64) * 2 * (size_t)nbig) +  // big list, {start, len}
            al(sizeof(i64) * (size_t)(nbig + 1)) + al(sizeof(int) * (size_t)nbig) +  // offsets, flags
+           al(sizeof(u64) * 2 * (size_t)nbig) + al(sizeof(u64) * (size_t)nbig) +    // key ranges, bases
            4 * al(sizeof(u64) * (size_t)n) + al(t > sc ? t : sc);
 }
 
@@ -1222,6 +1253,8 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
     i64 *big = (i64 *)take(sizeof(i64) * 2 * (size_t)nbig_cap);
     i64 *boff = (i64 *)take(sizeof(i64) * (size_t)(nbig_cap + 1));
     int *flags = (int *)take(sizeof(int) * (size_t)nbig_cap);
+    unsigned long long *krange = (unsigned long long *)take(sizeof(u64) * 2 * (size_t)nbig_cap);
+    u64 *sbase = (u64 *)take(sizeof(u64) * (size_t)nbig_cap);
     u64 *k1 = (u64 *)take(sizeof(u64) * (size_t)n);
     u64 *v1 = (u64 *)take(sizeof(u64) * (size_t)n);
     u64 *k2 = (u64 *)take(sizeof(u64) * (size_t)n);
@@ -1301,18 +1334,20 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
     }
     hoff[nbig] = total;
     LJ_CK(cudaMemcpyAsync(boff, hoff.data(), sizeof(i64) * (nbig + 1), cudaMemcpyHostToDevice, st));
-    LJ_CK(cudaMemsetAsync(flags, 0, sizeof(int) * nbig, st));
-    k_big_check<<<grid_for(total, 256, 8), 256, 0, st>>>(B, big, boff, nbig, total, flags);
+    k_big_scan<<<nbig < 65535 ? nbig : 65535, 256, 0, st>>>(B, big, nbig, flags, krange);
     k_big_copy<<<grid_for(total, 256, 8), 256, 0, st>>>(B, big, boff, nbig, total, flags, out);
     LJ_CK_LAUNCH();
     std::vector<int> hf(nbig);
+    std::vector<u64> hkr(2 * (size_t)nbig);
     LJ_CK(cudaMemcpyAsync(hf.data(), flags, sizeof(int) * nbig, cudaMemcpyDeviceToHost, st));
+    LJ_CK(cudaMemcpyAsync(hkr.data(), krange, sizeof(u64) * 2 * nbig, cudaMemcpyDeviceToHost, st));
     LJ_CK(cudaStreamSynchronize(st));
     // the mixed ones: those above 2^16 tuples each get a device radix sort;
     // all smaller ones ONE segmented radix sort (block per segment): gather
     // -> sort -> scatter back, instead of a device sort per sub-bucket
     std::vector<i64> spos, scum(1, 0);
-    int nsorted = 0;
+    std::vector<u64> sbh;
+    int nsorted = 0, span_bits = 0;
     i64 mx = 0;
     for (int q = 0; q < nbig; ++q) {
         if (!hf[q]) continue;
@@ -1322,6 +1357,10 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
         if (len <= 65536) {
             spos.push_back(a);
             scum.push_back(scum.back() + len);
+            sbh.push_back(hkr[2 * q]);
+            int b = 0;
+            for (u64 d = hkr[2 * q + 1] - hkr[2 * q]; d; d >>= 1) ++b;
+            span_bits = std::max(span_bits, b);
             continue;
         }
         k_deinterleave<<<grid_for(len, 256, 8), 256, 0, st>>>(B + a, len, k1, v1);
@@ -1340,14 +1379,18 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
         i64 *d_cum = big + nseg;
         LJ_CK(cudaMemcpyAsync(d_pos, spos.data(), sizeof(i64) * nseg, cudaMemcpyHostToDevice, st));
         LJ_CK(cudaMemcpyAsync(d_cum, scum.data(), sizeof(i64) * (nseg + 1), cudaMemcpyHostToDevice, st));
-        k_seg_gather<<<grid_for(T, 256, 8), 256, 0, st>>>(B, d_pos, d_cum, nseg, T, k1, v1);
+        LJ_CK(cudaMemcpyAsync(sbase, sbh.data(), sizeof(u64) * nseg, cudaMemcpyHostToDevice, st));
+        k_seg_gather<<<grid_for(T, 256, 8), 256, 0, st>>>(B, d_pos, d_cum, sbase, nseg, T, k1, v1);
         LJ_CK_LAUNCH();
+        // only the low span_bits bits differ inside a segment (stable LSD
+        // radix over them == the full sort)
+        const int eb = span_bits < 1 ? 1 : span_bits;
         size_t tt = 0;
-        cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tt, k1, k2, v1, v2, (int)T, nseg, d_cum, d_cum + 1, 0, 64,
+        cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tt, k1, k2, v1, v2, (int)T, nseg, d_cum, d_cum + 1, 0, eb,
                                                  st);
         LJ_CK(cub::DeviceSegmentedRadixSort::SortPairs(cub_tmp, tt, k1, k2, v1, v2, (int)T, nseg, d_cum, d_cum + 1,
-                                                       0, 64, st));
-        k_seg_scatter<<<grid_for(T, 256, 8), 256, 0, st>>>(k2, v2, d_pos, d_cum, nseg, T, out);
+                                                       0, eb, st));
+        k_seg_scatter<<<grid_for(T, 256, 8), 256, 0, st>>>(k2, v2, d_pos, d_cum, sbase, nseg, T, out);
         LJ_CK_LAUNCH();
     }
     LJ_CK(cudaStreamSynchronize(st));
