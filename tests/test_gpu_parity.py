@@ -650,3 +650,25 @@ def test_spline_fit_on_device_matches_golden(golden, lj, monkeypatch):
         assert int(m.shift) == int(d["sp_shift"]), name
         checked += 1
     assert checked >= 5
+
+
+@pytest.mark.parametrize("keys", [[5], [5, 9], [5, 9, 11], [7] * 1000, [3] * 500 + [8] * 500,
+                                  [0, 2**63 - 1], list(range(70000))])
+def test_spline_fit_on_device_small_and_degenerate(lj, keys, monkeypatch):
+    """Device fit == host fit on one, two and three points, all-equal keys,
+    two distinct keys, the extremes of the key domain and a knot-free line
+    longer than two chunks."""
+    gpu, host = _fit_both(lj, keys, 32, 18, monkeypatch)
+    assert np.array_equal(gpu.spline_keys, host.spline_keys)
+    assert np.array_equal(gpu.spline_ranks, host.spline_ranks)
+    assert np.array_equal(gpu.radix_table, host.radix_table)
+    assert int(gpu.shift) == int(host.shift)
+
+
+def test_host_resident_entry_points_on_empty_inputs(lj):
+    r = lj.make_relation(np.arange(100, dtype=np.uint64) * 3, 1)
+    e = torch.empty(0, dtype=torch.int64)
+    idx = lj.GappedRmiIndex(2.0, 16).fit(r)
+    assert lj.join_checksum_host(idx, e, e).cpu().tolist() == [0, 0, 0, 0]
+    res = lj.lsj_join_host(r.keys.cpu(), r.payloads.cpu(), e, e)
+    assert res.checksum == (0, 0, 0)
