@@ -333,6 +333,17 @@ size_t lj_keybin_workspace_bytes(int64_t nbins);
 int lj_keybin_eval(const uint64_t *bounds, int64_t nbins, const uint64_t *keys, int64_t nk, uint32_t *bins,
                    void *ws, size_t ws_bytes, void *stream);
 int lj_lsj_key_bounds(const LjLsjModel *model, uint64_t *bounds, void *ws, size_t ws_bytes, void *stream);
+/* Range shuffle of the distributed LSJ fused with its partition (the
+ * shared model's nbins = destination ranks): _count -> exact counts[nbins+1]
+ * (device) and every tuple's destination kept in ws; _scatter (same ws) ->
+ * every tuple written to bases[dest] + its claimed position, bases[] =
+ * ABSOLUTE record indices (address / 16) of this rank's region in each
+ * destination's receive buffer (symmetric memory: NVLink P2P stores). */
+size_t lj_lsj_shuffle_workspace_bytes(int64_t n, int64_t nbins);
+int lj_lsj_shuffle_count(const LjLsjModel *model, const uint64_t *keys, const uint64_t *pay, int64_t n,
+                         int64_t *counts, void *ws, size_t ws_bytes, void *stream);
+int lj_lsj_shuffle_scatter(const LjLsjModel *model, const uint64_t *keys, const uint64_t *pay, int64_t n,
+                           const int64_t *bases, void *ws, size_t ws_bytes, void *stream);
 /* lsj.py:242-286 per-bucket sort (K8, model-placed, shared memory) from the
  * partitioned pairs_in into pairs_out (fully sorted, bucket ranges kept).
  * stats_host[4] = {oversized buckets, bitonic fallbacks, sub-buckets above

@@ -115,6 +115,9 @@ SIGNATURES = {
     "lj_keybin_workspace_bytes": (_size_t, [_i64]),
     "lj_keybin_eval": (_int, [_P, _i64, _P, _i64, _P, _P, _size_t, _P]),
     "lj_lsj_key_bounds": (_int, [ctypes.POINTER(LjLsjModel), _P, _P, _size_t, _P]),
+    "lj_lsj_shuffle_workspace_bytes": (_size_t, [_i64, _i64]),
+    "lj_lsj_shuffle_count": (_int, [ctypes.POINTER(LjLsjModel), _P, _P, _i64, _P, _P, _size_t, _P]),
+    "lj_lsj_shuffle_scatter": (_int, [ctypes.POINTER(LjLsjModel), _P, _P, _i64, _P, _P, _size_t, _P]),
     "lj_spline_hash_bucket_bins": (_i64, [_i64]),
     "lj_spline_hash_bucket_capacity": (_i64, [_i64, _i64]),
     "lj_spline_hash_bucket_est_workspace_bytes": (_size_t, [ctypes.POINTER(LjSplineHash), _i64]),

@@ -1134,6 +1134,52 @@ int lj_keybin_eval(const uint64_t *bounds, int64_t nbins, const uint64_t *keys, 
     return LJ_OK;
 }
 
+// ---- range shuffle of the distributed LSJ (dist.lsj_join): the shared
+// model's bins are the destination ranks
+size_t lj_lsj_shuffle_workspace_bytes(int64_t n, int64_t nbins) {
+    return est_workspace_bytes((int)nbins) + part_align(sizeof(u16) * (size_t)(n < 0 ? 0 : n)) +
+           al(kb_bytes((int)nbins));
+}
+
+static int shuffle_bins(const LjLsjModel *md, void *ws, size_t ws_bytes, int64_t n, KeyRangeBin &kb,
+                        cudaStream_t st) {
+    LJ_REQUIRE(md && md->pb && md->nbins >= 1 && md->nbins <= KB_MAXBINS, "model has no bins (or > 2048)");
+    if (ws_bytes < lj_lsj_shuffle_workspace_bytes(n, md->nbins)) {
+        set_error("lj_lsj_shuffle: workspace too small");
+        return LJ_E_WORKSPACE;
+    }
+    const int nb = (int)md->nbins;
+    u64 *lay = reinterpret_cast<u64 *>((char *)ws + ws_bytes - al(kb_bytes(nb)));
+    lay = reinterpret_cast<u64 *>((uintptr_t)lay & ~(uintptr_t)255);
+    kb.g = lay;
+    kb.nb = nb;
+    return LJ_OK;
+}
+
+int lj_lsj_shuffle_count(const LjLsjModel *md, const uint64_t *keys, const uint64_t *pay, int64_t n,
+                         int64_t *counts, void *ws, size_t ws_bytes, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    KeyRangeBin kb;
+    int rc = shuffle_bins(md, ws, ws_bytes, n, kb, st);
+    if (rc) return rc;
+    k_lsj_key_bounds<<<((int)md->nbins + 127) / 128, 128, 0, st>>>(make_lsj(*md), (u64 *)kb.g);
+    k_keybin_build<<<1, 1024, 0, st>>>((u64 *)kb.g, (int)md->nbins);
+    LJ_CK_LAUNCH();
+    SoaSrc<KeyRangeBin> src{keys, pay, kb};
+    return shuffle_count(src, n, (int)md->nbins, counts, ws, ws_bytes, st);
+}
+
+int lj_lsj_shuffle_scatter(const LjLsjModel *md, const uint64_t *keys, const uint64_t *pay, int64_t n,
+                           const int64_t *bases, void *ws, size_t ws_bytes, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    KeyRangeBin kb;
+    int rc = shuffle_bins(md, ws, ws_bytes, n, kb, st);
+    if (rc) return rc;
+    LJ_REQUIRE(((uintptr_t)keys & 15) == 0 && ((uintptr_t)pay & 15) == 0, "columns must be 16-B aligned");
+    SoaSrc<KeyRangeBin> src{keys, pay, kb};
+    return shuffle_scatter(src, n, (int)md->nbins, bases, ws, ws_bytes, st);
+}
+
 int lj_lsj_key_bounds(const LjLsjModel *md, uint64_t *bounds, void *ws, size_t ws_bytes, void *stream) {
     LJ_REQUIRE(md && md->pb && md->nbins >= 1 && md->nbins <= KB_MAXBINS, "model has no bins (or > 2048)");
     LJ_REQUIRE(ws_bytes >= kb_bytes((int)md->nbins), "workspace too small");

@@ -94,7 +94,11 @@ static __global__ void k_est_caps(const u32 *est, int nbins, int exact, i64 *cap
 
 // STORED: the bins were written by the exact counting pass (u16 per tuple)
 // and arrive through the ring with the tuples (no bin evaluation, no table)
-template <class Src, bool STORED>
+// PEER: regions are exact and rstart[b] is the ABSOLUTE record index (address
+// / 16) of bin b's region -- possibly in another GPU's memory (NVLink P2P
+// stores through a symmetric-memory pointer) -- so out is null and there
+// is no overflow check.
+template <class Src, bool STORED, bool PEER = false>
 __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_est(Src f0, i64 n, i64 chunk, int nbins, int nst,
                                                               const i64 *__restrict__ rstart, u32 *gcur,
                                                               unsigned long long *ovf, ulonglong2 *out,
@@ -232,8 +236,9 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_est(Src f0, i64 n, i64
                 const u64 p = j < nb ? ps[j] : ld_stream(f.pay + base + j);
                 const int b = tbin[j];
                 i64 dst = srst[b] + (i64)gbase[b] + (i - (int)tstart[b]);
-                if (dst >= srst[b + 1]) dst = srst[nbins] + (i64)atomicAdd(ovf, 1ULL);
-                out[dst] = make_ulonglong2(k, p);
+                if (!PEER && dst >= srst[b + 1]) dst = srst[nbins] + (i64)atomicAdd(ovf, 1ULL);
+                ulonglong2 *o = PEER ? reinterpret_cast<ulonglong2 *>((uintptr_t)dst << 4) : out + dst;
+                *o = make_ulonglong2(k, p);
             }
         }
     }
@@ -334,6 +339,69 @@ int run_partition_claims(const Src &f, i64 n, int nbins, int exact, ulonglong2 *
         k_est_regions<<<(nbins + 256) / 256, 256, 0, st>>>(rstart, gcur, ovf, nbins, reg);
         LJ_CK_LAUNCH();
     }
+    return LJ_OK;
+}
+
+// ---- the range shuffle of the distributed LSJ, fused with its partition:
+// (1) exact per-destination counts, every tuple's destination stored (u16);
+// (2) the claims scatter with the destinations' region bases (absolute
+// record indices) -- each source owns its region in every destination, so
+// no cross-GPU atomics.  ws: est_workspace_bytes(nbins) + 2 n bytes.
+template <class Src>
+int shuffle_count(const Src &f, i64 n, int nbins, i64 *counts, void *ws, size_t ws_bytes, cudaStream_t st) {
+    if (nbins < 1 || nbins > 2 * PART2_NT) {
+        set_error("shuffle: 1 <= destinations <= 2048");
+        return LJ_E_INVALID;
+    }
+    const size_t eb = est_workspace_bytes(nbins);
+    if (ws_bytes < eb + part_align(sizeof(u16) * (size_t)n)) {
+        set_error("shuffle: workspace too small");
+        return LJ_E_WORKSPACE;
+    }
+    u32 *est = (u32 *)ws;
+    u16 *codes = reinterpret_cast<u16 *>((char *)ws + eb);
+    LJ_CK(cudaMemsetAsync(est, 0, sizeof(u32) * (size_t)nbins, st));
+    const size_t tb = pt_table_bytes(f.f.smem_words());
+    static bool attr = false;
+    if (!attr) {
+        LJ_CK(cudaFuncSetAttribute(k_est_sample<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_SMEM_MAX));
+        LJ_CK(cudaFuncSetAttribute(k_bin_scatter_est<Src, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   PT_SMEM_MAX));
+        attr = true;
+    }
+    if (n > 0) {
+        k_est_sample<Src><<<grid_for(n, 256, 4), 256, tb + sizeof(u32) * nbins, st>>>(f, n, nbins, 1, est, codes);
+        LJ_CK_LAUNCH();
+    }
+    k_est_caps<<<(nbins + 256) / 256, 256, 0, st>>>(est, nbins, 1, counts);  // counts[b] = est[b], counts[nbins] = 0
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+template <class Src>
+int shuffle_scatter(const Src &f, i64 n, int nbins, const i64 *bases, void *ws, size_t ws_bytes, cudaStream_t st) {
+    const size_t eb = est_workspace_bytes(nbins);
+    if (ws_bytes < eb + part_align(sizeof(u16) * (size_t)n)) {
+        set_error("shuffle: workspace too small");
+        return LJ_E_WORKSPACE;
+    }
+    if (n <= 0) return LJ_OK;
+    char *q = (char *)ws;
+    q += part_align(sizeof(u32) * (size_t)nbins);
+    u32 *gcur = (u32 *)q;
+    q += part_align(sizeof(u32) * (size_t)nbins);
+    q += 2 * part_align(sizeof(i64) * (size_t)(nbins + 1));
+    unsigned long long *ovf = (unsigned long long *)q;
+    const u16 *codes = reinterpret_cast<const u16 *>((char *)ws + eb);
+    LJ_CK(cudaMemsetAsync(gcur, 0, sizeof(u32) * (size_t)nbins, st));
+    const PartPlan p = part_plan(n, nbins);
+    const size_t nb4 = (size_t)((nbins + 31) & ~31);
+    const size_t fix = 3 * nb4 * sizeof(u32) + (nb4 + 32) * sizeof(i64) + (((size_t)EST_TILE * 6 + 127) & ~(size_t)127);
+    const size_t stage = EST_STAGE + EST_TILE * 2;
+    const int nst = (int)min((size_t)PT_MAXST, (PT_SMEM_MAX - fix) / stage);
+    k_bin_scatter_est<Src, true, true><<<p.blocks, PART2_NT, fix + nst * stage, st>>>(
+        f, n, p.chunk, nbins, nst, bases, gcur, ovf, nullptr, codes);
+    LJ_CK_LAUNCH();
     return LJ_OK;
 }
 

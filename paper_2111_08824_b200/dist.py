@@ -21,6 +21,8 @@ CUDA library.
 
 from __future__ import annotations
 
+import ctypes
+import os
 import time
 
 import numpy as np
@@ -149,16 +151,100 @@ def _gpu_shared_model(r_keys: torch.Tensor, sample_rate: float, seed: int, world
     return LsjModel.from_sample(rmi, srt, world)
 
 
+def shuffle_plan(counts: np.ndarray, rank: int):
+    """Layout of the fused range shuffle.  counts[src, rel, dst] = tuples of
+    relation rel (0 = R, 1 = S) that rank src sends to rank dst.  Every
+    destination's receive buffer holds R from source 0, 1, ... then S from
+    source 0, 1, ...; each source owns its slice of every destination, so
+    the scatter needs no cross-GPU atomics.  Returns (recv_r[dst],
+    recv_s[dst], capacity in records (the same on every rank), this rank's
+    R offset in every destination, its S offset in every destination)."""
+    counts = np.asarray(counts, dtype=np.int64)
+    cr, cs = counts[:, 0, :], counts[:, 1, :]
+    recv_r, recv_s = cr.sum(axis=0), cs.sum(axis=0)
+    cap = int((recv_r + recv_s).max()) if counts.size else 0
+    off_r = cr[:rank].sum(axis=0)
+    off_s = recv_r + cs[:rank].sum(axis=0)
+    return recv_r, recv_s, cap, off_r, off_s
+
+
+_SYMM: dict = {}  # (device, group) -> (symmetric receive buffer, handle)
+
+
+def _pg(group):
+    return group if group is not None else dist.group.WORLD
+
+
+def fused_shuffle(r_keys, r_payloads, s_keys, s_payloads, model, group=None):
+    """The range shuffle fused with its partition (lj_lsj_shuffle_*): exact
+    per-destination counts (one all-gather of a 2 x G matrix), one symmetric-
+    memory receive buffer per rank, and ONE scatter kernel per relation that
+    writes every tuple straight into its destination's buffer -- NVLink P2P
+    stores through the peer pointers, the all-to-all overlapped with the
+    partition tile by tile.  Returns (R records [n, 2], S records [m, 2],
+    buffer handle) on this rank."""
+    import torch.distributed._symmetric_memory as symm
+
+    from . import _lib
+
+    rank, world = rank_world(group)
+    lib = _lib.lib()
+    dev = r_keys.device
+    c = model.c_struct()
+    rels = ((r_keys, r_payloads), (s_keys, s_payloads))
+    cnt = torch.zeros(2, world + 1, dtype=torch.int64, device=dev)
+    wss = []
+    for i, (k, p) in enumerate(rels):
+        n = k.numel()
+        ws = _lib.workspace(lib.lj_lsj_shuffle_workspace_bytes(n, world), dev)
+        _lib.check(lib.lj_lsj_shuffle_count(ctypes.byref(c), _lib.ptr(k), _lib.ptr(p), n, _lib.ptr(cnt[i]),
+                                            _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "lsj_shuffle_count")
+        wss.append(ws)
+    allc = torch.empty(world, 2, world + 1, dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_gather_into_tensor(allc, cnt.unsqueeze(0).contiguous(), group=group)
+    else:
+        allc.copy_(cnt.unsqueeze(0))
+    counts = allc[:, :, :world].cpu().numpy()
+    recv_r, recv_s, cap, off_r, off_s = shuffle_plan(counts, rank)
+    # the receive buffer is reused while it is large enough (cap is the same
+    # on every rank, so every rank takes the same decision)
+    key = (dev.index, id(_pg(group)))
+    got = _SYMM.get(key)
+    if got is None or got[0].numel() < 2 * max(cap, 1):
+        buf = symm.empty(2 * max(cap, 1) + (2 * max(cap, 1)) // 8, dtype=torch.int64, device=dev)
+        hdl = symm.rendezvous(buf, _pg(group))
+        _SYMM[key] = (buf, hdl)
+    buf, hdl = _SYMM[key]
+    ptrs = [int(v) for v in hdl.buffer_ptrs]
+    for i, (k, p) in enumerate(rels):
+        off = off_r if i == 0 else off_s
+        bases = torch.tensor([ptrs[d] // 16 + int(off[d]) for d in range(world)] + [0], dtype=torch.int64, device=dev)
+        _lib.check(lib.lj_lsj_shuffle_scatter(ctypes.byref(c), _lib.ptr(k), _lib.ptr(p), k.numel(), _lib.ptr(bases),
+                                              _lib.ptr(wss[i]), wss[i].numel(), _lib.stream_ptr()),
+                   "lsj_shuffle_scatter")
+    # every rank's scatter complete before any rank reads its buffer
+    torch.cuda.current_stream(dev).synchronize()
+    if world > 1:
+        dist.barrier(group=group)
+    rec = buf.view(-1, 2)
+    nr, ns = int(recv_r[rank]), int(recv_s[rank])
+    return rec[:nr], rec[nr:nr + ns], hdl
+
+
 def lsj_join(r_keys, r_payloads, s_keys, s_payloads, config=None, group=None, *, model_fn=None,
              partition_fn=None, local_join_fn=None):
     """Distributed LSJ over this rank's shards of R and S.  Returns
-    ((count, sum, xor), phases) -- the global checksum on every rank."""
+    ((count, sum, xor), phases) -- the global checksum on every rank.
+
+    On CUDA tensors the shuffle is `fused_shuffle` (partition + P2P stores
+    into symmetric memory); with injected partition functions (host tests)
+    or LJ_SHUFFLE=nccl, the partition is followed by an NCCL all-to-all-v."""
     from .lsj import LsjConfig
 
     config = config or LsjConfig()
     rank, world = rank_world(group)
     model_fn = model_fn or (lambda rk: _gpu_shared_model(rk, config.sample_rate, config.seed, world, group))
-    partition_fn = partition_fn or (lambda k, p, m: _gpu_partition(k, p, m, world))
     if local_join_fn is None:
         def local_join_fn(rrec, srec):
             from . import lsj as _lsj
@@ -173,18 +259,26 @@ def lsj_join(r_keys, r_payloads, s_keys, s_payloads, config=None, group=None, *,
                 list(res.checksum) + [0], dtype=torch.int64)
             return words
     phases = {}
+    fused = (partition_fn is None and r_keys.is_cuda and os.environ.get("LJ_SHUFFLE", "fused") == "fused")
     t0 = time.perf_counter()
     model = model_fn(r_keys)
     t1 = time.perf_counter()
-    r_rec, r_cnt = partition_fn(r_keys, r_payloads, model)
-    s_rec, s_cnt = partition_fn(s_keys, s_payloads, model)
-    t2 = time.perf_counter()
-    r_loc = exchange(r_rec, r_cnt, group)
-    s_loc = exchange(s_rec, s_cnt, group)
-    t3 = time.perf_counter()
+    hdl = None
+    if fused:
+        r_loc, s_loc, hdl = fused_shuffle(r_keys, r_payloads, s_keys, s_payloads, model, group)
+        t2 = t3 = time.perf_counter()
+    else:
+        partition_fn = partition_fn or (lambda k, p, m: _gpu_partition(k, p, m, world))
+        r_rec, r_cnt = partition_fn(r_keys, r_payloads, model)
+        s_rec, s_cnt = partition_fn(s_keys, s_payloads, model)
+        t2 = time.perf_counter()
+        r_loc = exchange(r_rec, r_cnt, group)
+        s_loc = exchange(s_rec, s_cnt, group)
+        t3 = time.perf_counter()
     words = local_join_fn(r_loc, s_loc)
     t4 = time.perf_counter()
+    del hdl  # the receive buffers stay alive until the local join is done
     res = reduce_checksum(words, group)
     phases.update(smpl=t1 - t0, part=t2 - t1, xchg=t3 - t2, local=t4 - t3, n_r_local=int(r_loc.shape[0]),
-                  n_s_local=int(s_loc.shape[0]))
+                  n_s_local=int(s_loc.shape[0]), shuffle="fused P2P" if fused else "partition + NCCL all-to-all-v")
     return res, phases

@@ -137,3 +137,28 @@ def test_shard_bounds_cover(n, world):
         assert lo == prev and hi >= lo
         prev = hi
     assert prev == n
+
+
+def test_shuffle_plan_tiles_every_destination():
+    """The fused shuffle's layout: for every destination, the slices the
+    sources write (R then S, in source order) are disjoint and cover its
+    receive buffer exactly; the capacity is the largest receive."""
+    import numpy as np
+
+    from paper_2111_08824_b200.dist import shuffle_plan
+
+    rng = np.random.default_rng(3)
+    for world in (1, 2, 3, 8):
+        counts = rng.integers(0, 1000, size=(world, 2, world))
+        counts[0, 1, :] = 0  # a source with nothing of S
+        plans = [shuffle_plan(counts, r) for r in range(world)]
+        recv_r, recv_s, cap = plans[0][0], plans[0][1], plans[0][2]
+        assert cap == int((recv_r + recv_s).max())
+        for d in range(world):
+            cover = np.zeros(int(recv_r[d] + recv_s[d]), dtype=np.int64)
+            for src in range(world):
+                _, _, c2, off_r, off_s = plans[src]
+                assert c2 == cap
+                cover[off_r[d]:off_r[d] + counts[src, 0, d]] += 1
+                cover[off_s[d]:off_s[d] + counts[src, 1, d]] += 1
+            assert (cover == 1).all()

@@ -553,10 +553,13 @@ def test_join_checksum_host_streams_chunks(lj, buffered):
         lj.join_checksum_host(idx, bad, hp, buffered=buffered, chunk=1000)
 
 
-def test_distributed_lsj_single_rank_nccl(lj, tmp_path):
-    """The C5 path (shared model, range partition, NCCL all-to-all-v, local
+@pytest.mark.parametrize("shuffle", ["fused", "nccl"])
+def test_distributed_lsj_single_rank_nccl(lj, tmp_path, monkeypatch, shuffle):
+    """The C5 path (shared model, range shuffle -- fused partition + P2P
+    stores into symmetric memory, or partition + NCCL all-to-all-v -- local
     LSJ, 3-word reduction) on a one-rank NCCL group equals the oracle; the
     exchange protocol at world 2 is covered with gloo in test_dist.py."""
+    monkeypatch.setenv("LJ_SHUFFLE", shuffle)
     import torch.distributed as dist
 
     from paper_2111_08824_b200 import configs
@@ -569,9 +572,11 @@ def test_distributed_lsj_single_rank_nccl(lj, tmp_path):
     try:
         (c, s, x), ph = ljdist.lsj_join(inp.r.keys, inp.r.payloads, inp.s.keys, inp.s.payloads,
                                         lj.LsjConfig(fanout=4096, sample_rate=0.01))
+        ljdist._SYMM.clear()
     finally:
         dist.destroy_process_group()
     assert (c, s, x) == tuple(want)
+    assert ph["shuffle"] == ("fused P2P" if shuffle == "fused" else "partition + NCCL all-to-all-v")
 
 
 def test_lsj_join_host_overlapped_equals_device(lj):
