@@ -417,12 +417,15 @@ def run_b200(args):
 
     # the dominant kernel timed alone, live, with CUDA events on its stream
     dom = []
+    phase_ms = []
     for i in range(args.steps):
         flush.zero_()
         if run_step.dominant == "sort":  # LSJ: phase events recorded by lsj_join itself
             run_step(out)
             torch.cuda.synchronize()
-            dom.append(run_step.holder["br"].sort * 1e3)
+            br = run_step.holder["br"]
+            dom.append(br.sort * 1e3)
+            phase_ms.append((br.part * 1e3, br.sort * 1e3, br.join * 1e3))
             continue
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         for name, fn in run_step.parts:
@@ -442,6 +445,14 @@ def run_b200(args):
                 "peak_kind": peak_kind, "algorithmic_bytes": run_step.bytes_note,
                 "step_frac": (ALGO_BYTES[inp.algorithm] * (n_s if index is not None else n_r + n_s))
                 / (ms_per_step / 1e3) / 1e9 / peak}
+    if phase_ms:
+        # LSJ per phase (partition 32 B, sort 32 B, merge 16 B per tuple of |R| + |S|)
+        roofline["lsj_phases"] = {}
+        for i, (name, bpt) in enumerate((("partition", 32), ("sort", 32), ("merge", 16))):
+            ms = statistics.mean(p[i] for p in phase_ms)
+            gbs = bpt * (n_r + n_s) / (ms / 1e3) / 1e9
+            roofline["lsj_phases"][name] = {"ms": ms, "achieved": gbs, "frac": gbs / peak,
+                                            "algorithmic_bytes": f"{bpt} B/tuple x {n_r + n_s}"}
     launches = count_launches(run_step, out)
 
     e2e = None

@@ -1,3 +1,4 @@
-timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 900 python tools/exp_c3.py > gpurun_out/exp_c3_p.log 2>&1
-LJ_PART_NO_PIPE=1 timeout 900 python tools/exp_c3.py > gpurun_out/exp_c3_np.log 2>&1
+for i in 1 2; do
+timeout 900 python bench.py --config c4 --no-cpu-baseline --no-e2e > gpurun_out/b_c4_side$i.json 2> gpurun_out/b_c4.err
+LJ_LSJ_SIDE=0 timeout 900 python bench.py --config c4 --no-cpu-baseline --no-e2e > gpurun_out/b_c4_noside$i.json 2> gpurun_out/b_c4n.err
+done
