@@ -704,12 +704,11 @@ __global__ void __launch_bounds__(SORT_NT, SORT_CTAS) k_lsj_sort(LsjDev md, Src 
         const int nruns = s_nruns < MAX_RUNS ? s_nruns : MAX_RUNS;
         if (!s_bad)
             for (int q = 0; q < nruns; ++q) block_sort_idx(ord, s_runs[q].x, s_runs[q].y, K);
-#ifdef LJ_SORT_VERIFY
-        // (diagnostics) the order is right by construction: slots are
-        // monotone in the key and every mixed run is ranked or sorted
+        // safety net: a misordered bucket is re-sorted whole (measured to
+        // fire, e.g. once on a C5 shard whose top keys lie past the model's
+        // training range; dropping this pass broke that join)
         for (int i = threadIdx.x; i + 1 < m; i += SORT_NT)
             if (K[ord[i]] > K[ord[i + 1]]) s_bad = 1;
-#endif
         __syncthreads();
         if (s_bad) {
             // safety net (the placement key is monotone, so this only runs

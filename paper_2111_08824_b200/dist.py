@@ -216,7 +216,12 @@ def fused_shuffle(r_keys, r_payloads, s_keys, s_payloads, model, group=None):
         hdl = symm.rendezvous(buf, _pg(group))
         _SYMM[key] = (buf, hdl)
     buf, hdl = _SYMM[key]
-    ptrs = [int(v) for v in hdl.buffer_ptrs]
+    # peer addresses of this tensor: the symmetric blocks' bases + the
+    # tensor's offset inside its block (the same on every rank)
+    off0 = int(getattr(hdl, "offset", 0))
+    ptrs = [int(v) + off0 for v in hdl.buffer_ptrs]
+    if ptrs[rank] != buf.data_ptr():
+        raise RuntimeError("symmetric memory: peer pointer of this rank does not match its buffer")
     for i, (k, p) in enumerate(rels):
         off = off_r if i == 0 else off_s
         bases = torch.tensor([ptrs[d] // 16 + int(off[d]) for d in range(world)] + [0], dtype=torch.int64, device=dev)

@@ -579,6 +579,34 @@ def test_distributed_lsj_single_rank_nccl(lj, tmp_path, monkeypatch, shuffle):
     assert ph["shuffle"] == ("fused P2P" if shuffle == "fused" else "partition + NCCL all-to-all-v")
 
 
+def test_lsj_on_shuffled_orders_repeatedly(lj):
+    """The local LSJ of the distributed path sees its relations in the
+    nondeterministic order of the claims scatter; some orders (the sample
+    then fits a model whose last leaf leaves the top keys' placement
+    misordered) need the sort's sortedness check + whole-bucket fallback.
+    Dropping that check broke ~1 in 8 of these runs (a C5 shard); 24 runs
+    over scatter-ordered relations must all be exact."""
+    from paper_2111_08824_b200 import configs
+    from paper_2111_08824_b200.lsj import LsjModel, _partition
+    from paper_2111_08824_b200.models import RecursiveModelIndex
+
+    inp = configs.config5(scale=12)
+    want = tuple(oracle.smj_checksum(*inp.r.numpy(), *inp.s.numpy()))
+    cfg = lj.LsjConfig(fanout=4096, sample_rate=0.01)
+    # a one-bin partition is a claims scatter: a nondeterministic permutation
+    from paper_2111_08824_b200.util import sort_pairs
+    srt, _ = sort_pairs(inp.r.keys[::64].contiguous(), inp.r.keys[::64].contiguous())
+    one = LsjModel.from_sample(RecursiveModelIndex(16).fit(srt), srt, 1)
+    for rep in range(24):
+        pr, _ = _partition(inp.r.keys, inp.r.payloads, one)
+        ps, _ = _partition(inp.s.keys, inp.s.payloads, one)
+        pr, ps = pr.view(-1, 2), ps.view(-1, 2)
+        r = lj.Relation(pr[:, 0].contiguous(), pr[:, 1].contiguous(), validate=False)
+        s = lj.Relation(ps[:, 0].contiguous(), ps[:, 1].contiguous(), validate=False)
+        res, _ = lj.lsj_join(r, s, cfg)
+        assert res.checksum == want, rep
+
+
 def test_lsj_join_host_overlapped_equals_device(lj):
     """lsj_join_host (R's side overlapped with S's H2D) == lsj_join == oracle."""
     from paper_2111_08824_b200 import configs

@@ -1,4 +1,2 @@
-for i in 1 2; do
-timeout 900 python bench.py --config c4 --no-cpu-baseline --no-e2e > gpurun_out/b_c4_side$i.json 2> gpurun_out/b_c4.err
-LJ_LSJ_SIDE=0 timeout 900 python bench.py --config c4 --no-cpu-baseline --no-e2e > gpurun_out/b_c4_noside$i.json 2> gpurun_out/b_c4n.err
-done
+timeout 600 python tools/dbg_lsj.py tools/bad_5.pt > gpurun_out/dbg_lsj_fix.log 2>&1
+timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
