@@ -1,2 +1,2 @@
-timeout 600 python tools/dbg_lsj.py tools/bad_5.pt > gpurun_out/dbg_lsj_fix.log 2>&1
-timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --config c1 --variant buffered --no-cpu-baseline --no-e2e > gpurun_out/b_c1b.json 2> gpurun_out/b_c1b.err
+timeout 600 python bench.py --config c1 --variant direct --no-cpu-baseline --no-e2e > gpurun_out/b_c1d.json 2> gpurun_out/b_c1d.err
