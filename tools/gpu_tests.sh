@@ -1,2 +1,2 @@
-timeout 600 python bench.py --config c1 --variant buffered --no-cpu-baseline --no-e2e > gpurun_out/b_c1b.json 2> gpurun_out/b_c1b.err
-timeout 600 python bench.py --config c1 --variant direct --no-cpu-baseline --no-e2e > gpurun_out/b_c1d.json 2> gpurun_out/b_c1d.err
+timeout 240 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "staged or buffered or config2 or registry" > gpurun_out/pytest_gpu_a.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_a.log
+timeout 200 python bench.py --config c2 --no-cpu-baseline --no-e2e > gpurun_out/b_c2w.json 2> gpurun_out/b_c2w.err
