@@ -1,2 +1,2 @@
-timeout 240 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "staged or buffered or config2 or registry" > gpurun_out/pytest_gpu_a.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_a.log
-timeout 200 python bench.py --config c2 --no-cpu-baseline --no-e2e > gpurun_out/b_c2w.json 2> gpurun_out/b_c2w.err
+timeout 400 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+for u in 1 2 4; do LJ_K1_ILP=$u timeout 200 python bench.py --config c1 --no-cpu-baseline --no-e2e > gpurun_out/b_c1_$u.json 2> gpurun_out/b_c1_$u.err; done
