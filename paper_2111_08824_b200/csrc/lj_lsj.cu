@@ -85,7 +85,11 @@ struct LsjDev {
         const double x = u64_to_f64(k);
         const LjLeaf lf = load_leaf(m.leaves, m.route(x));
         const double lo = i64_to_f64(lf.clamp_lo) - 0.5;
-        if (!(lf.slope > 0.0)) return lo;
+        // flat leaves sit at clamp_lo - 0.5, except at the top: an empty
+        // leaf past the last training key has its segment start clamped to
+        // n - 1 (models.py:87-93), and keys routed there (larger than every
+        // training key) must not sort below the last leaf's y <= n - 0.5
+        if (!(lf.slope > 0.0)) return lf.clamp_lo >= m.n - 1 ? i64_to_f64(m.n) - 0.5 : lo;
         const double raw = __dadd_rn(__dmul_rn(lf.slope, x), lf.icpt);
         const double hi = i64_to_f64(lf.clamp_hi) + 0.5;
         return raw < lo ? lo : (raw > hi ? hi : raw);
@@ -704,9 +708,9 @@ __global__ void __launch_bounds__(SORT_NT, SORT_CTAS) k_lsj_sort(LsjDev md, Src 
         const int nruns = s_nruns < MAX_RUNS ? s_nruns : MAX_RUNS;
         if (!s_bad)
             for (int q = 0; q < nruns; ++q) block_sort_idx(ord, s_runs[q].x, s_runs[q].y, K);
-        // safety net: a misordered bucket is re-sorted whole (measured to
-        // fire, e.g. once on a C5 shard whose top keys lie past the model's
-        // training range; dropping this pass broke that join)
+        // safety net: a misordered bucket is re-sorted whole (it fired on
+        // keys routed to empty leaves past the last training key before
+        // y() placed them at the top)
         for (int i = threadIdx.x; i + 1 < m; i += SORT_NT)
             if (K[ord[i]] > K[ord[i + 1]]) s_bad = 1;
         __syncthreads();

@@ -603,8 +603,11 @@ def test_lsj_on_shuffled_orders_repeatedly(lj):
         pr, ps = pr.view(-1, 2), ps.view(-1, 2)
         r = lj.Relation(pr[:, 0].contiguous(), pr[:, 1].contiguous(), validate=False)
         s = lj.Relation(ps[:, 0].contiguous(), ps[:, 1].contiguous(), validate=False)
-        res, _ = lj.lsj_join(r, s, cfg)
+        res, br = lj.lsj_join(r, s, cfg)
         assert res.checksum == want, rep
+        # placement is monotone (keys past the training range sort at the
+        # top): the whole-bucket fallback never has to fire
+        assert br.extra["r_bitonic_fallbacks"] == 0 and br.extra["s_bitonic_fallbacks"] == 0, rep
 
 
 def test_lsj_join_host_overlapped_equals_device(lj):
