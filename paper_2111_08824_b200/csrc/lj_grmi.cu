@@ -257,7 +257,10 @@ __global__ void __launch_bounds__(256) k_grmi_probe_overflow(GrmiDev g, const ul
 // load per match.
 
 constexpr int STAGE_NT = 1024;
-constexpr int STAGE_PIECE = 65536;      // probes per work item
+#ifndef LJ_STAGE_PIECE
+#define LJ_STAGE_PIECE 65536
+#endif
+constexpr int STAGE_PIECE = LJ_STAGE_PIECE;  // probes per work item (C2 step 6.41 / 6.20 / 6.19 ms at 2^15 / 2^16 / 2^17)
 constexpr i64 STAGE_MIN = 2048;         // windows with fewer probes: global search
 constexpr int STAGE_U = 2;              // probes in flight per thread
 constexpr int STAGE_TB = 13;            // radix-table bits
