@@ -257,7 +257,7 @@ def cpu_inlj(inp, target_s: float = 8.0, threads: int = 0):
             sk = inp.s.keys[:sample].cpu().numpy().view(np.uint64)
             sp = inp.s.payloads[:sample].cpu().numpy().view(np.uint64)
             rks, rps = rk[:sample], rp[:sample]
-            run = lambda a, b, rks=rks, rps=rps: oracle.lsj_join(rks, rps, a, b, workers=1,
+            run = lambda a, b, rks=rks, rps=rps: oracle.lsj_join(rks, rps, a, b, workers=cores,
                                                                   fanout=o.get("fanout", 4096),
                                                                   sample_rate=o.get("sample_rate", 0.01))
             t0 = time.perf_counter()
@@ -268,8 +268,9 @@ def cpu_inlj(inp, target_s: float = 8.0, threads: int = 0):
             sample = min(n_r, n_s, sample * 4)
         scale = (n_r + n_s) / (2 * sample)
         value = (n_r + n_s) / (dt * scale)
-        info = {"value": value, "unit": "tuples/s", "cores": 1, "kind": "port",
-                "sample": f"LSJ over the first {sample} tuples of R and of S ({dt:.2f} s, single thread), "
+        info = {"value": value, "unit": "tuples/s", "cores": cores, "kind": "port",
+                "sample": f"LSJ with {cores} workers (one thread each, as the reference's share-nothing "
+                          f"workers) over the first {sample} tuples of R and of S ({dt:.2f} s), "
                           f"time scaled x{scale:.1f} linearly to |R|+|S|"}
         return value, info, (sk, sp, run)
     if inp.algorithm in ("grmi-inlj", "buffered-grmi-inlj"):
@@ -453,6 +454,17 @@ def run_b200(args):
             gbs = bpt * (n_r + n_s) / (ms / 1e3) / 1e9
             roofline["lsj_phases"][name] = {"ms": ms, "achieved": gbs, "frac": gbs / peak,
                                             "algorithmic_bytes": f"{bpt} B/tuple x {n_r + n_s}"}
+    ph = getattr(run_step, "holder", {}).get("phases") if hasattr(run_step, "holder") else None
+    if ph is not None and "shuffle" in ph:
+        # the range shuffle against NVLink (16 B x (|R|+|S|)/G x
+        # (G-1)/G per GPU leave the GPU); partition and exchange are one fused
+        # step, timed on the host around its stream syncs
+        moved = 16 * (n_r + n_s) * (world - 1) / world
+        sh_ms = (ph["part"] + ph["xchg"]) * 1e3
+        roofline["nvlink"] = {"bytes_per_gpu": moved, "shuffle_ms": sh_ms, "peak": 900.0, "unit": "GB/s",
+                              "achieved": moved / (sh_ms / 1e3) / 1e9 if sh_ms > 0 else 0.0,
+                              "frac": (moved / (sh_ms / 1e3) / 1e9 / 900.0) if sh_ms > 0 else 0.0,
+                              "shuffle": ph["shuffle"]}
     launches = count_launches(run_step, out)
 
     e2e = None
