@@ -61,8 +61,14 @@ constexpr int SORT_U = LJ_SORT_U;  // tuples in flight per thread in the load / 
 constexpr int SUB = CAP / 2;      // mean tuples per sub-bucket: sample-quantile slices
                                   // (~61 sample keys each) stay below CAP
 constexpr int SPLIT_NT = 1024;
-constexpr int SPLIT_U = 4;        // tuple groups in flight per warp step
-constexpr i64 SPLIT_CH = 65536;   // tuples per split work item
+#ifndef LJ_SPLIT_U
+#define LJ_SPLIT_U 4
+#endif
+#ifndef LJ_SPLIT_CH
+#define LJ_SPLIT_CH 262144
+#endif
+constexpr int SPLIT_U = LJ_SPLIT_U;    // tuple groups in flight per warp step
+constexpr i64 SPLIT_CH = LJ_SPLIT_CH;  // tuples per split work item (C4 sort phase: 64 Ki 17.10, 128 Ki 16.90, 256 Ki 16.77, 512 Ki 16.95 ms)
 constexpr int SPLIT_MAXF = 2048;  // slices per coarse bucket (point mode: 2x-1 slots)
 constexpr int JOIN_T = 1024;
 constexpr int JOIN_NT = 256;
