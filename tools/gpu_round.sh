@@ -1,7 +1,8 @@
 # round measurement: benches (all configs + reference arm), launch list, ncu --set full of the dominant kernels
+V=${V:-v12}
+mkdir -p gpurun_out
 timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_$V.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_$V.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$V.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke_$V.log
-V=${V:-v12}
 for c in c2 c1 c3 c4; do timeout 900 python bench.py --config $c > gpurun_out/bench_${c}_$V.json 2> gpurun_out/bench_${c}_$V.err; done
 timeout 900 python bench.py --config c5 --scale 3 --no-cpu-baseline > gpurun_out/bench_c5s3_$V.json 2> gpurun_out/bench_c5s3_$V.err
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_$V.json 2> gpurun_out/bench_ref_$V.err
