@@ -129,6 +129,17 @@ int lj_fill_payloads(uint64_t *out, int64_t n, int64_t offset, uint64_t seed, vo
 int lj_fill_mix64(uint64_t *out, int64_t n, int64_t offset, uint64_t seed, void *stream);
 /* out[i] = src[mulhi64(mix64(seed ^ (offset+i)), src_n)]: uniform draw with
  * replacement from src (SURVEY 8d C3/C5 counter sampler). */
+/* Portable generator draws (include/lj_gen.h; bit-identical to the host
+ * generator oracle/lj_gen.c): out[i] = draw offset+i of stream `seed`.
+ * lj_fill_normal: standard normal (Box-Muller); lj_fill_lognormal:
+ * floor(scale * exp(sigma * normal)) clamped to [0, maxv]; lj_fill_cluster:
+ * centres[cluster] + sigma * normal truncated, -1 outside [0, maxv)
+ * (ncent a power of two, centres a device array). */
+int lj_fill_normal(double *out, int64_t n, int64_t offset, uint64_t seed, void *stream);
+int lj_fill_lognormal(int64_t *out, int64_t n, int64_t offset, uint64_t seed, double sigma, double scale,
+                      double maxv, void *stream);
+int lj_fill_cluster(int64_t *out, int64_t n, int64_t offset, uint64_t seed, const double *centres, int ncent,
+                    double sigma, double maxv, void *stream);
 int lj_gather_uniform(uint64_t *out, int64_t n, int64_t offset, uint64_t seed, const uint64_t *src,
                       int64_t src_n, void *stream);
 /* Stable device sort of (key, payload) pairs by key; used by index builds

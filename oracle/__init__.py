@@ -74,9 +74,10 @@ def build() -> str:
 def lib():
     global _lib
     if _lib is None:
-        if not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(
-            os.path.join(_HERE, "lj_oracle.c")
-        ):
+        srcs = [os.path.join(_HERE, f) for f in ("lj_oracle.c", "lj_gen.c")]
+        srcs.append(os.path.join(_HERE, "..", "include", "lj_gen.h"))
+        if not os.path.exists(_LIB_PATH) or any(os.path.getmtime(_LIB_PATH) < os.path.getmtime(f)
+                                                for f in srcs if os.path.exists(f)):
             build()
         _lib = ctypes.CDLL(_LIB_PATH)
         _lib.orc_mix64.restype = ctypes.c_uint64
@@ -383,7 +384,7 @@ def spline_hash_build(keys, payloads, max_error=32, radix_bits=18, table_factor=
     payloads = _u64(payloads)
     n = keys.size
     if model is None:
-        model = spline_fit(np.sort(keys), max_error, radix_bits)
+        model = spline_fit(sort_u64(keys), max_error, radix_bits)
     P = max(1, int(round(float(table_factor) * n)))
     ek = np.empty(n, np.uint64)
     ep = np.empty(n, np.uint64)
@@ -443,6 +444,14 @@ def lsj_join(rk, rp, sk, sp, workers=1, sample_rate=0.01, fanout=10000, seed=0x1
                        _i64(sk.size), ctypes.byref(cr), ctypes.byref(cs), _i64(workers),
                        _i64(fanout), _p(out, _u64p), _p(stats, _u64p))
     return tuple(int(v) for v in out), tuple(int(v) for v in stats)
+
+
+def sort_u64(keys) -> np.ndarray:
+    """np.sort of uint64 keys (parallel radix sort in C; a sorted copy)."""
+    out = np.array(keys, dtype=np.uint64, copy=True)
+    if out.size > 1:
+        lib().orc_sort_u64(_p(out, _u64p), _i64(out.size))
+    return out
 
 
 # ------------------------------------------------------- ground truth

@@ -76,6 +76,9 @@ SIGNATURES = {
     "lj_fill_payloads": (_int, [_P, _i64, _i64, _u64, _P]),
     "lj_fill_mix64": (_int, [_P, _i64, _i64, _u64, _P]),
     "lj_gather_uniform": (_int, [_P, _i64, _i64, _u64, _P, _i64, _P]),
+    "lj_fill_normal": (_int, [_P, _i64, _i64, _u64, _P]),
+    "lj_fill_lognormal": (_int, [_P, _i64, _i64, _u64, ctypes.c_double, ctypes.c_double, ctypes.c_double, _P]),
+    "lj_fill_cluster": (_int, [_P, _i64, _i64, _u64, _P, _int, ctypes.c_double, ctypes.c_double, _P]),
     "lj_sort_pairs_workspace_bytes": (_size_t, [_i64]),
     "lj_sort_pairs": (_int, [_P, _P, _P, _P, _i64, _int, _int, _P, _size_t, _P]),
     "lj_rmi_fit_workspace_bytes": (_size_t, [_i64, _i64]),

@@ -5,9 +5,11 @@ Size interpretations (pinned): "16M" = 2^24, "256M" = 2^28, "200M" =
 2*10^8, "2B" = 2*10^9.  Keys are uint64 < 2^63; payloads uint64.
 
 Integer parts use counter-based SplitMix64 draws (``mix64(seed ^ i)``),
-bit-identical anywhere.  The lognormal / normal draws use float64 on the
-device (Box-Muller on two counter draws), so the host never regenerates
-them: parity tests copy the device inputs to the CPU oracle.  Duplicates
+bit-identical anywhere.  The lognormal / normal draws (Box-Muller on two
+counter draws) use the portable float64 arithmetic of ``include/lj_gen.h``
+(IEEE + - * / sqrt only, no FMA), so the host generator ``oracle/gen.py``
+regenerates every configuration bit for bit without the CUDA library (the
+reference arm of bench.py does; ``tests/test_gpu_fullsize.py`` checks it).  Duplicates
 are removed keeping the first draw, then topped up from the continuing
 counter stream, and the draw order (already random) is kept.  A finite
 Zipf(s) over N ranks is sampled by exact inverse-CDF lookup in the float64
@@ -48,9 +50,38 @@ def uniform63(n: int, seed: int, offset: int = 0, device="cuda") -> torch.Tensor
 
 
 def normal(n: int, seed: int, offset: int = 0, device="cuda") -> torch.Tensor:
-    u1 = _unit(n, seed ^ 0xA5A5, offset, device)
-    u2 = _unit(n, seed ^ 0x5A5A, offset, device)
-    return torch.sqrt(-2.0 * torch.log(u1)) * torch.cos(2.0 * math.pi * u2)
+    """Standard normal draws offset .. offset+n-1 of stream ``seed``
+    (Box-Muller in the portable arithmetic of include/lj_gen.h: the host
+    generator oracle/gen.py reproduces the same bits)."""
+    out = torch.empty(int(n), dtype=torch.float64, device=device)
+    if n:
+        _lib.check(_lib.lib().lj_fill_normal(_lib.ptr(out), int(n), int(offset), int(seed) & (2**64 - 1),
+                                             _lib.stream_ptr()), "fill_normal")
+    return out
+
+
+MAXKEY_F = float(2**63 - 1024)  # largest generated key (exact in float64)
+
+
+def lognormal_keys(n: int, seed: int, offset: int, sigma: float, scale: float, device="cuda") -> torch.Tensor:
+    """floor(scale * exp(sigma * normal)) clamped to [0, 2^63 - 1024]."""
+    out = torch.empty(int(n), dtype=torch.int64, device=device)
+    if n:
+        _lib.check(_lib.lib().lj_fill_lognormal(_lib.ptr(out), int(n), int(offset), int(seed) & (2**64 - 1),
+                                                float(sigma), float(scale), MAXKEY_F, _lib.stream_ptr()),
+                   "fill_lognormal")
+    return out
+
+
+def cluster_keys(n: int, seed: int, offset: int, centres: torch.Tensor, sigma: float, device="cuda") -> torch.Tensor:
+    """centre[cluster] + sigma * normal, draws outside [0, 2^63 - 1024) dropped
+    (the kept draws stay in draw order)."""
+    out = torch.empty(int(n), dtype=torch.int64, device=device)
+    if n:
+        _lib.check(_lib.lib().lj_fill_cluster(_lib.ptr(out), int(n), int(offset), int(seed) & (2**64 - 1),
+                                              _lib.ptr(centres), centres.numel(), float(sigma), MAXKEY_F,
+                                              _lib.stream_ptr()), "fill_cluster")
+    return out[out >= 0]
 
 
 def distinct_first(draw, n: int, device="cuda") -> torch.Tensor:
@@ -162,8 +193,7 @@ def config2(scale: int = 0, device="cuda", seed: int = 0xC2, shard: int = 0) -> 
     leaves = (1 << 16) >> min(scale, 8)
 
     def draw(c, o):
-        v = torch.floor(1e12 * torch.exp(2.0 * normal(c, seed, o, device)))
-        return torch.clamp(v, 0, float(2**63 - 1024)).to(torch.int64)
+        return lognormal_keys(c, seed, o, 2.0, 1e12, device)
 
     rk = distinct_first(draw, nr, device)
     rp = fill_payloads(nr, seed ^ 0x11, device=device)
@@ -198,10 +228,7 @@ def config3(scale: int = 1, device="cuda", seed: int = 0xC3, shard: int = 0, sha
     centres = (uniform63(64, seed ^ 0x31, 0, device) >> 1).to(torch.float64)
 
     def draw(c, o):
-        cl = ((_mix(c, seed ^ 0x32, o, device) >> 58) & 63)
-        v = centres[cl] + float(2**40) * normal(c, seed ^ 0x33, o, device)
-        ok = (v >= 0) & (v < float(2**63 - 1024))
-        return v[ok].to(torch.int64)
+        return cluster_keys(c, seed, o, centres, float(2**40), device)
 
     rk = distinct_first(draw, nr, device)
     rp = fill_payloads(nr, seed ^ 0x34, device=device)
@@ -220,8 +247,7 @@ def config4(scale: int = 0, device="cuda", seed: int = 0xC4, shard: int = 0) -> 
     nr = ns = (1 << 28) >> scale
 
     def draw(c, o):
-        v = torch.floor(float(2**40) * torch.exp(1.5 * normal(c, seed, o, device)))
-        return torch.clamp(v, 0, float(2**63 - 1024)).to(torch.int64)
+        return lognormal_keys(c, seed, o, 1.5, float(2**40), device)
 
     rk = distinct_first(draw, nr, device)
     rp = fill_payloads(nr, seed ^ 0x41, device=device)

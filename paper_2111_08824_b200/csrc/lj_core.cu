@@ -7,6 +7,7 @@
 #include <mutex>
 
 #include "lj_common.cuh"
+#include "../../include/lj_gen.h"
 
 namespace lj {
 
@@ -58,6 +59,25 @@ __global__ void k_gather_uniform(u64 *out, i64 n, i64 offset, u64 seed, const u6
         u64 r = mix64(seed ^ (u64)(offset + i));
         out[i] = src[__umul64hi(r, (u64)src_n)];
     }
+}
+
+// portable normal / lognormal / cluster draws (include/lj_gen.h): the same
+// bits as the host generator oracle/lj_gen.c
+__global__ void k_fill_normal(double *out, i64 n, i64 offset, u64 seed) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+        out[i] = ljg_normal(seed, (u64)(offset + i));
+}
+
+__global__ void k_fill_lognormal(i64 *out, i64 n, i64 offset, u64 seed, double sigma, double scale, double maxv) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+        out[i] = ljg_lognormal_key(seed, (u64)(offset + i), sigma, scale, maxv);
+}
+
+// key = centre[cluster] + sigma * normal, or -1 when outside [0, maxv)
+__global__ void k_fill_cluster(i64 *out, i64 n, i64 offset, u64 seed, const double *centres, int ncent,
+                               double sigma, double maxv) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+        out[i] = ljg_cluster_key(seed, (u64)(offset + i), centres, ncent, sigma, maxv);
 }
 
 // ----------------------------------------------------------- RMI predict
@@ -398,6 +418,33 @@ int lj_fill_mix64(uint64_t *out, int64_t n, int64_t offset, uint64_t seed, void 
     LJ_REQUIRE(n >= 0, "n must be >= 0");
     if (n == 0) return LJ_OK;
     k_fill_mix64<<<grid_for(n, 256, 8), 256, 0, as_stream(stream)>>>(out, n, offset, seed);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+int lj_fill_normal(double *out, int64_t n, int64_t offset, uint64_t seed, void *stream) {
+    LJ_REQUIRE(n >= 0, "n must be >= 0");
+    if (n == 0) return LJ_OK;
+    k_fill_normal<<<grid_for(n, 256, 8), 256, 0, as_stream(stream)>>>(out, n, offset, seed);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+int lj_fill_lognormal(int64_t *out, int64_t n, int64_t offset, uint64_t seed, double sigma, double scale,
+                      double maxv, void *stream) {
+    LJ_REQUIRE(n >= 0, "n must be >= 0");
+    if (n == 0) return LJ_OK;
+    k_fill_lognormal<<<grid_for(n, 256, 8), 256, 0, as_stream(stream)>>>(out, n, offset, seed, sigma, scale, maxv);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+int lj_fill_cluster(int64_t *out, int64_t n, int64_t offset, uint64_t seed, const double *centres, int ncent,
+                    double sigma, double maxv, void *stream) {
+    LJ_REQUIRE(n >= 0 && ncent >= 1 && (ncent & (ncent - 1)) == 0, "need n >= 0 and a power-of-two centre count");
+    if (n == 0) return LJ_OK;
+    k_fill_cluster<<<grid_for(n, 256, 8), 256, 0, as_stream(stream)>>>(out, n, offset, seed, centres, ncent, sigma,
+                                                                        maxv);
     LJ_CK_LAUNCH();
     return LJ_OK;
 }

@@ -379,7 +379,12 @@ struct PosBin : NoTable {
     __device__ __forceinline__ PosBin at(u64 *) const { return *this; }
 };
 
-static int hash_bins(i64 n) { return (int)(n < 2048 ? (n < 1 ? 1 : n) : 2048); }
+static int hash_bins(i64 n) {
+    const char *e = getenv("LJ_HASH_BINS");  // diagnostic: window count of the grouping
+    const int want = e ? atoi(e) : 2048;
+    const int nb = want < 1 ? 1 : (want > 2048 ? 2048 : want);
+    return (int)(n < nb ? (n < 1 ? 1 : n) : nb);
+}
 
 size_t lj_spline_hash_bucket_workspace_bytes(int64_t nk, int64_t n) {
     return part_workspace_bytes(nk, hash_bins(n)) + kb_bytes(hash_bins(n)) + 256;
@@ -450,7 +455,8 @@ static size_t win_tables_bytes(const LjSpline &m) {
 size_t lj_spline_hash_bucket_est_workspace_bytes(const LjSplineHash *idx, int64_t nk) {
     if (!idx) return 0;
     const int nb = hash_bins(idx->model.n);
-    return est_workspace_bytes(nb) + part_align(sizeof(u16) * (size_t)(nk < 0 ? 0 : nk)) + win_tables_bytes(idx->model);
+    return est_workspace_bytes(nb) + part_align(sizeof(u16) * (size_t)(nk < 0 ? 0 : nk)) + win_tables_bytes(idx->model) +
+           kb_bytes(nb) + 256;
 }
 
 // exact regions in lj_leaf_bucket's layout: ends = next starts, no overflow
@@ -472,6 +478,27 @@ int lj_spline_hash_bucket_est(const LjSplineHash *idx, const uint64_t *keys, con
     f.n = idx->model.n;
     f.rn = (double)f.nb / (double)idx->model.n;
     SoaSrc<PosBin> src{keys, pay, f};
+    static const bool keybin = getenv("LJ_HASH_KEYBIN") != nullptr;
+    if (keybin) {
+        // equi-depth KEY windows over the build side, evaluated in shared
+        // memory (lj_keybin.cuh): no per-tuple global load
+        const int nb = (int)f.nb;
+        const size_t eb = est_workspace_bytes(nb);
+        LJ_REQUIRE(ws_bytes >= eb + kb_bytes(nb) + 256, "workspace too small");
+        u64 *lay = reinterpret_cast<u64 *>(((uintptr_t)ws + eb + 255) & ~(uintptr_t)255);
+        k_hash_window_bounds<<<(nb + 255) / 256, 256, 0, st>>>(idx->entries, idx->n, nb, lay);
+        k_keybin_build<<<1, 1024, 0, st>>>(lay, nb);
+        LJ_CK_LAUNCH();
+        KeyRangeBin kb;
+        kb.g = lay;
+        kb.nb = nb;
+        SoaSrc<KeyRangeBin> ksrc{keys, pay, kb};
+        const int rc = run_partition_est(ksrc, nk, nb, reinterpret_cast<ulonglong2 *>(pairs_out), reg_out, ws, eb, st);
+        if (rc) return rc;
+        k_fill_gaps<<<(unsigned)nb, 256, 0, st>>>(reg_out, nb, reinterpret_cast<ulonglong2 *>(pairs_out));
+        LJ_CK_LAUNCH();
+        return LJ_OK;
+    }
     const size_t wtb = win_tables_bytes(idx->model);
     static const bool no_win = getenv("LJ_HASH_POSBIN") != nullptr;
     if (!no_win && wtb && idx->model.aux && ws_bytes >= est_workspace_bytes((int)f.nb) + wtb) {
