@@ -1,24 +1,30 @@
 #!/usr/bin/env python
 """Benchmark of the learned-join hot path on B200 (driver contract).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl b200|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl b200|reference]
 
-Default workload = BASELINE.json configs[1] (C2): Gapped-RMI INLJ, R = 2^24
-unique floor(1e12*lognormal(0,2)) keys, S = 2^28 probes (95% Zipf(0.8)
-hits), RMI with 2^16 leaves at density 0.5.  One step = one fused probe
-(K1) of the whole S relation against the prebuilt index, with the result
-reduced to (count, sum, xor) on device.  Metric: join tuples/s =
-(|R| + |S|) / step time (bench.py:307-314 of the reference).
+Default workload = BASELINE.json's metric config, configs[2] (C3, "at
+1/2/4/8 B200"): RadixSpline learned-hash INLJ, R = 2*10^8 unique keys from
+64 normal clusters, S = 2*10^9 probes drawn uniformly from R, sharded
+across the GPUs with R replicated.  One step = one pass of the hot path
+over this rank's S (grouping by index window + probe) against the prebuilt
+index, reduced to (count, sum, xor) on device.  Metric: join tuples/s =
+(|R| + |S|) / step time (reference bench.py:307-314).
 
-Multi-GPU (torchrun, one process per GPU): the R index is replicated and
-every rank probes its own full-size S shard (weak scaling); the per-rank
-checksums are combined with NCCL (sum/count all-reduce, xor all-gather) inside
-the timed step.  value = (|R| + N*|S|) / max-over-ranks step time.
+``--gpus N`` (N > 1) without a torchrun environment re-launches itself
+under ``torch.distributed.run`` with N ranks on 127.0.0.1.  Every rank
+builds the same index (untimed, as the reference) and probes its
+contiguous 1/N of S; the three checksum words are combined inside the
+timed step (sum/count all-reduce, xor all-gather).  The whole-job value
+counts the replicated R once and every rank's S shard.
 
-``--impl reference`` times the reference algorithm's CPU implementation --
-the C restatement in oracle/ (the reference itself is Python+numba and is
-not installed on the GPU box) -- with every host thread, on a bounded
-sample of the same workload, extrapolated to the full S.
+``--impl reference`` times the reference algorithm's CPU implementation
+(the C restatement in oracle/, OpenMP over every host thread; the
+reference itself is Python+numba and does not exist on the GPU box) on
+bounded samples of the same workload, on inputs produced by the HOST
+generator oracle/gen.py -- bit-identical to the device inputs, without
+loading the CUDA library -- and prints the full-size checksum of the
+oracle beside the timing (the GPU line prints its own).
 """
 
 from __future__ import annotations
@@ -26,6 +32,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -35,6 +42,27 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 ALGO_BYTES = {"grmi-inlj": 32, "buffered-grmi-inlj": 32, "spline-hash-inlj": 32, "lsj": 80}
+METRIC = "join tuples/s ((|R|+|S|)/time)"
+MASK = (1 << 64) - 1
+
+# workload descriptions (identical in both arms; BASELINE.json configs)
+WORKLOADS = {
+    "c1": ("grmi-inlj", "GRMI INLJ: R=2^20 uniform63 unique, S=2^22 (90% hits), density 0.5, 1024 leaves"),
+    "c2": ("grmi-inlj", "GRMI INLJ skewed: R=2^24 lognormal(0,2)x1e12 unique, S=2^28 (95% Zipf(0.8) hits), "
+                        "density 0.5, 65536 leaves"),
+    "c3": ("spline-hash-inlj", "RadixSpline learned-hash INLJ: R=2e8 clustered-normal unique (64 clusters, "
+                               "sigma 2^40), S=2e9 uniform from R sharded over the GPUs, 18 radix bits, max error "
+                               "32, P=4|R|"),
+    "c4": ("lsj", "LSJ: R=2^28 lognormal(0,1.5)x2^40 unique, S=2^28 Zipf(1.0) over R ranks, 4096 partitions, "
+                  "1% sample models"),
+    "c5": ("lsj", "LSJ across GPUs: R=S=2e9 (all GPUs) uniform unique (bijective mix) / uniform from R, shared "
+                  "model range shuffle"),
+}
+DEFAULT_VARIANT = {"c1": "direct", "c2": "buffered", "c3": "buffered"}
+# configs whose relations are split across the ranks (BASELINE: C3's S is
+# sharded with R replicated; C5 range-shuffles both); the others run one
+# full-size workload per GPU (weak scaling)
+SHARDED = {"c3": ("s",), "c5": ("r", "s")}
 
 
 def _env_rank():
@@ -46,7 +74,7 @@ def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
     except Exception:
         return 6650.0, "fallback"
 
@@ -99,10 +127,173 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# configs whose relations are split across the ranks (BASELINE: C3's S is
-# sharded with R replicated; C5 range-shuffles both); the others run one
-# full-size workload per GPU (weak scaling)
-SHARDED = {"c3": ("s",), "c5": ("r", "s")}
+def _config_block(args, n_r, n_s):
+    algo, desc = WORKLOADS[args.config]
+    return {"workload": f"{args.config}: {desc}", "algorithm": algo,
+            "variant": (args.variant or DEFAULT_VARIANT.get(args.config, "direct")) if algo != "lsj" else None,
+            "scale": args.scale, "n_r": n_r, "n_s": n_s,
+            "l2": "inputs larger than L2 and L2 flushed (512 MB write) between steps",
+            "parallelism": _parallelism(args.config, algo, args.gpus)}
+
+
+def _parallelism(cfg, algorithm, n):
+    if cfg == "c5":
+        return f"lsj range shuffle over {n} GPU(s): shared model, P2P all-to-all, local LSJ"
+    if algorithm == "lsj":
+        return f"lsj replicas x{n} (one full join per GPU)"
+    if cfg in SHARDED:
+        return f"inlj replicated R, S sharded 1/{n} per GPU"
+    return f"inlj replicated R, full S per GPU x{n}"
+
+
+# ---------------------------------------------------------------- CPU legs
+# (the oracle: the checker and the CPU baseline, never the measured product)
+
+
+class CpuJoin:
+    """The reference algorithm's CPU implementation (oracle/, C + OpenMP)
+    over host arrays: rk/rp whole, S through s_slice(lo, hi).  The index
+    build is untimed, as in the reference (bench.py:138-144,202-209)."""
+
+    def __init__(self, algorithm, opts, rk, rp, s_slice, n_s):
+        import oracle
+
+        self.oracle, self.algorithm, self.opts = oracle, algorithm, opts
+        self.rk, self.rp, self.s_slice, self.n_s = rk, rp, s_slice, n_s
+        self.idx = None
+        if algorithm in ("grmi-inlj", "buffered-grmi-inlj"):
+            self.idx = oracle.grmi_build(rk, rp, opts["gap_factor"], opts["rmi_fanout"])
+        elif algorithm == "spline-hash-inlj":
+            self.idx = oracle.spline_hash_build(rk, rp, opts.get("spline_error", 32), opts.get("radix_bits", 18),
+                                                opts.get("table_factor", 4.0))
+
+    def probe(self, sk, sp, threads):
+        o = self.oracle
+        if self.algorithm == "spline-hash-inlj":
+            return o.spline_hash_join(self.idx, sk, sp, threads)[:3]
+        return o.grmi_join(self.idx, sk, sp, threads)[:3]
+
+    def lsj(self, m, threads):
+        sk, sp = self.s_slice(0, m)
+        return self.oracle.lsj_join(self.rk[:m], self.rp[:m], sk, sp, workers=threads,
+                                    fanout=self.opts.get("fanout", 4096),
+                                    sample_rate=self.opts.get("sample_rate", 0.01))[0]
+
+    def sample_size(self, threads, target_s):
+        """Smallest power-of-4 sample whose run takes >= target_s / 4."""
+        m = min(self.n_s, 1 << 18)
+        while True:
+            dt = self.time_sample(m, threads)
+            if dt >= target_s / 4 or m >= self.n_s:
+                return m, dt
+            m = min(self.n_s, m * 4)
+
+    def time_sample(self, m, threads):
+        if self.algorithm == "lsj":
+            t0 = time.perf_counter()
+            self.lsj(m, threads)
+            return time.perf_counter() - t0
+        sk, sp = self.s_slice(0, m)
+        t0 = time.perf_counter()
+        self.probe(sk, sp, threads)
+        return time.perf_counter() - t0
+
+    def value(self, m, dt, n_r):
+        """Whole-workload tuples/s from a sample run (time extrapolated
+        linearly in |S| for INLJ, in |R|+|S| for LSJ -- optimistic for the
+        CPU's n log n sort)."""
+        if self.algorithm == "lsj":
+            return (n_r + self.n_s) / (dt * (n_r + self.n_s) / (2 * m))
+        return (n_r + self.n_s) / (dt * self.n_s / m)
+
+    def describe(self, m, dt, threads):
+        if self.algorithm == "lsj":
+            return (f"LSJ with {threads} workers over the first {m} tuples of R and of S ({dt:.2f} s), time "
+                    f"scaled linearly to |R|+|S|")
+        return (f"first {m} of {self.n_s} S probes against the full R index on {threads} thread(s) ({dt:.2f} s), "
+                f"time extrapolated x{self.n_s / m:.1f}; index build untimed as in the reference")
+
+    def full_checksum(self, threads, slice_n=1 << 25):
+        """The oracle's (count, sum, xor) over the whole workload: S in
+        slices against the index (sums add, xors xor); LSJ through the
+        ground-truth sort-merge join (baselines.py:337-348)."""
+        if self.algorithm == "lsj":
+            sk, sp = self.s_slice(0, self.n_s)
+            return tuple(self.oracle.smj_checksum(self.rk, self.rp, sk, sp))
+        c = s = x = 0
+        for lo in range(0, self.n_s, slice_n):
+            sk, sp = self.s_slice(lo, min(self.n_s, lo + slice_n))
+            w = self.probe(sk, sp, threads)
+            c, s, x = c + w[0], (s + w[1]) & MASK, x ^ w[2]
+        return (c, s, x)
+
+
+def cpu_baseline(cj: CpuJoin, n_r, target_s=8.0):
+    """All host threads, plus W = 1 beside it."""
+    cores = cj.oracle.num_threads()
+    m, dt = cj.sample_size(cores, target_s)
+    info = {"value": cj.value(m, dt, n_r), "unit": "tuples/s", "cores": cores, "kind": "port",
+            "sample": cj.describe(m, dt, cores)}
+    m1, dt1 = cj.sample_size(1, target_s / 2)
+    info["w1"] = {"value": cj.value(m1, dt1, n_r), "cores": 1, "sample": cj.describe(m1, dt1, 1)}
+    return info, m
+
+
+def run_reference_arm(args):
+    """The reference's CPU path on host-generated inputs: no CUDA library
+    is loaded in this process (oracle/ only)."""
+    rank, world, _ = _env_rank()
+    if rank != 0:
+        return
+    import oracle
+    from oracle import gen
+
+    t0 = time.perf_counter()
+    kw = {} if args.scale is None else {"scale": args.scale}
+    h = gen.CONFIGS[args.config](**kw)
+    gen_s = time.perf_counter() - t0
+    algo = WORKLOADS[args.config][0]
+    n_r, n_s = h.rk.size, h.n_s
+    if args.config in SHARDED and args.gpus > 1:
+        pass  # the reference joins the whole workload (its W threads share the host)
+    t0 = time.perf_counter()
+    cj = CpuJoin(algo, dict(h.opts, seed=42), h.rk, h.rp, h.s_slice, n_s)
+    build_s = time.perf_counter() - t0
+    cores = oracle.num_threads()
+    m, dt = cj.sample_size(cores, 4.0)
+    steps = []
+    for i in range(args.warmup + args.steps):
+        dt = cj.time_sample(m, cores)
+        if i >= args.warmup:
+            steps.append(dt)
+    dt = statistics.median(steps)
+    value = cj.value(m, dt, n_r)
+    t_full = n_r + n_s
+    ms = t_full / value * 1e3
+    info = {"value": value, "unit": "tuples/s", "cores": cores, "kind": "port", "sample": cj.describe(m, dt, cores)}
+    try:
+        m1, dt1 = cj.sample_size(1, 2.0)
+        info["w1"] = {"value": cj.value(m1, dt1, n_r), "cores": 1, "sample": cj.describe(m1, dt1, 1)}
+    except Exception as exc:  # reported, never required
+        info["w1"] = {"error": repr(exc)}
+    checksum = None
+    if not args.no_full_checksum:
+        t0 = time.perf_counter()
+        c, sm, x = cj.full_checksum(cores)
+        checksum = {"count": c, "sum": sm, "xor": x, "full_pass_s": time.perf_counter() - t0,
+                    "how": ("oracle spline-hash / GRMI probe over all of S in 2^25-probe slices" if algo != "lsj"
+                            else "oracle sort-merge join (baselines.py:337-348) over all of R and S")}
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tuples/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if args.config in SHARDED else "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (host generator oracle/gen.py, bit-identical to the device inputs)",
+            "config": _config_block(args, n_r, n_s), "cpu_baseline": info,
+            "e2e": {"value": value, "unit": "tuples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "checksum": checksum, "prep": {"gen_s": gen_s, "index_build_s": build_s}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
 
 
 def make_inputs(cfg: str, shard: int = 0, shards: int = 1, scale=None):
@@ -130,9 +321,6 @@ def build_index(inp):
     return None  # lsj builds nothing ahead of time: it is timed end to end
 
 
-DEFAULT_VARIANT = {"c1": "direct", "c2": "buffered", "c3": "buffered"}
-
-
 class Step:
     """One step of the hot path: `parts` run in order on the current stream;
     `dominant` names the part the roofline is reported for and `dom_bytes`
@@ -141,7 +329,7 @@ class Step:
     def __init__(self, parts, dominant, dom_bytes, kernel, bytes_note):
         self.parts, self.dominant, self.dom_bytes = parts, dominant, dom_bytes
         self.kernel, self.bytes_note = kernel, bytes_note
-        self.last_breakdown = None
+        self.holder = {}
 
     def __call__(self, out):
         for _, fn in self.parts:
@@ -150,9 +338,9 @@ class Step:
 
 
 def make_step(inp, index, variant="buffered", world: int = 1, distributed: bool = False):
-    """A step is one pass of the hot path over the whole S (INLJ, index
-    prebuilt as in the reference, bench.py:138-144 of the reference) or the
-    whole LSJ (sample, fit, partition, sort, join)."""
+    """A step is one pass of the hot path over the whole (local) S (INLJ,
+    index prebuilt as in the reference, bench.py:138-144 of the reference)
+    or the whole LSJ (sample, fit, partition, sort, join)."""
     import torch
 
     import paper_2111_08824_b200 as lj
@@ -167,44 +355,40 @@ def make_step(inp, index, variant="buffered", world: int = 1, distributed: bool 
                      ("probe", lambda out: index.probe_records(n_s, scratch, out))]
             kern = "k_grmi_probe_staged" if grmi else "k_hash_probe_chunks"
             st = Step(parts, "probe", 32 * n_s, kern,
-                      f"32 B/probe x {n_s} probes (16 B S record + 16 B R entry); the one-pass bucketing "
-                      "(k_est_sample + k_bin_scatter_est) runs before it in the step")
-            st.scratch = scratch  # reused by the e2e leg (C3's is ~66 GB)
+                      f"32 B/probe x {n_s} probes (16 B S record + 16 B R entry); the one-pass grouping by "
+                      "index window runs before it in the step")
+            st.scratch = scratch
             return st
         fn = (lambda out: index.join_checksum(keys, pays, out=out))
         return Step([("probe", fn)], "probe", 32 * n_s, "k_grmi_probe" if grmi else "k_hash_probe",
                     f"32 B/probe x {n_s} probes (16 B S record + 16 B R entry)")
     o = dict(lj.DEFAULT_OPTS, **inp.opts)
     cfg = lj.LsjConfig(workers=1, fanout=o["fanout"], sample_rate=o["sample_rate"], seed=o["seed"])
-    holder = {}
     if distributed:
-        # C5 across GPUs: shared model, range shuffle (NCCL all-to-all-v),
-        # local LSJ, 3-word reduction (dist.lsj_join); the words come back
-        # reduced on every rank
+        # C5 across GPUs: shared model, range shuffle, local LSJ, 3-word
+        # reduction (dist.lsj_join); the words come back reduced on every rank
         from paper_2111_08824_b200 import dist as ljdist
 
         def dist_step(out):
             (c, sm, x), ph = ljdist.lsj_join(inp.r.keys, inp.r.payloads, inp.s.keys, inp.s.payloads, cfg)
-            holder["phases"] = ph
+            st.holder["phases"] = ph
             sg = [v - (1 << 64) if v >= (1 << 63) else v for v in (c, sm, x, 0)]
             out.copy_(torch.tensor(sg, dtype=torch.int64))
             return out
 
         st = Step([("lsj", dist_step)], "lsj", 80 * (n_r + n_s), "distributed LSJ step (partition, all-to-all, "
                   "local LSJ)", f"80 B/tuple x {n_r + n_s} local tuples (partition 32, sort 32, merge 16)")
-        st.holder = holder
         st.reduced = True
         return st
 
     def lsj_step(out):
-        res, br = lj.lsj_join(inp.r, inp.s, cfg)
-        holder["br"] = br
+        res, br = lj.lsj_join(inp.r, inp.s, cfg, counters=False)
+        st.holder["br"] = br
         out.copy_(res._words)
         return out
 
     st = Step([("lsj", lsj_step)], "sort", 32 * (n_r + n_s), "lsj sort phase (k_split_*, k_lsj_sort)",
               f"sort phase: 32 B/tuple (read 16 + write 16) x {n_r + n_s} tuples; whole pipeline 80 B/tuple")
-    st.holder = holder
     return st
 
 
@@ -234,124 +418,13 @@ def count_launches(step, out):
         return None
 
 
-# ---------------------------------------------------------------- CPU arms
-
-
-def cpu_inlj(inp, target_s: float = 8.0, threads: int = 0):
-    """Oracle (C restatement of the reference path, OpenMP) on a bounded
-    sample, extrapolated to the whole workload.  Returns (value, info, rerun)."""
-    import numpy as np
-
-    import oracle
-
-    o = inp.opts
-    rk, rp = inp.r.numpy()
-    n_r, n_s = len(inp.r), len(inp.s)
-    cores = threads or oracle.num_threads()
-    if inp.algorithm == "lsj":
-        # LSJ is timed end to end on prefixes of R and S (all phases), then
-        # scaled linearly in |R|+|S| (optimistic for the CPU: the sort is
-        # n log n)
-        sample = min(n_r, 1 << 20)
-        while True:
-            sk = inp.s.keys[:sample].cpu().numpy().view(np.uint64)
-            sp = inp.s.payloads[:sample].cpu().numpy().view(np.uint64)
-            rks, rps = rk[:sample], rp[:sample]
-            run = lambda a, b, rks=rks, rps=rps: oracle.lsj_join(rks, rps, a, b, workers=cores,
-                                                                  fanout=o.get("fanout", 4096),
-                                                                  sample_rate=o.get("sample_rate", 0.01))
-            t0 = time.perf_counter()
-            run(sk, sp)
-            dt = time.perf_counter() - t0
-            if dt >= target_s / 4 or sample >= min(n_r, n_s):
-                break
-            sample = min(n_r, n_s, sample * 4)
-        scale = (n_r + n_s) / (2 * sample)
-        value = (n_r + n_s) / (dt * scale)
-        info = {"value": value, "unit": "tuples/s", "cores": cores, "kind": "port",
-                "sample": f"LSJ with {cores} workers (one thread each, as the reference's share-nothing "
-                          f"workers) over the first {sample} tuples of R and of S ({dt:.2f} s), "
-                          f"time scaled x{scale:.1f} linearly to |R|+|S|"}
-        return value, info, (sk, sp, run)
-    if inp.algorithm in ("grmi-inlj", "buffered-grmi-inlj"):
-        idx = oracle.grmi_build(rk, rp, o["gap_factor"], o["rmi_fanout"])
-        run = lambda k, p: oracle.grmi_join(idx, k, p, threads)
-    else:
-        idx = oracle.spline_hash_build(rk, rp, o.get("spline_error", 32), o.get("radix_bits", 18),
-                                       o.get("table_factor", 4.0))
-        run = lambda k, p: oracle.spline_hash_join(idx, k, p, threads)
-    sample = min(n_s, 1 << 20)
-    while True:
-        sk = inp.s.keys[:sample].cpu().numpy().view(np.uint64)
-        sp = inp.s.payloads[:sample].cpu().numpy().view(np.uint64)
-        t0 = time.perf_counter()
-        run(sk, sp)
-        dt = time.perf_counter() - t0
-        if dt >= target_s / 4 or sample >= n_s:
-            break
-        sample = min(n_s, sample * 4)
-    t_full = dt * n_s / sample
-    value = (n_r + n_s) / t_full
-    info = {"value": value, "unit": "tuples/s", "cores": cores, "kind": "port",
-            "sample": f"first {sample} of {n_s} S probes against the full R index ({dt:.2f} s), "
-                      f"time extrapolated x{n_s / sample:.1f}; index build untimed as in the reference"}
-    return value, info, (sk, sp, run)
-
-
-def run_reference_arm(args):
-    import torch
-
-    rank, world, local = _env_rank()
-    if rank != 0:
-        return
-    torch.cuda.set_device(local)
-    inp = make_inputs(args.config)
-    value, info, (sk, sp, run) = cpu_inlj(inp)
-    steps = []
-    n_s = len(inp.s)
-    scale = (n_s / sk.size) if inp.algorithm != "lsj" else (len(inp.r) + n_s) / (2 * sk.size)
-    for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        run(sk, sp)
-        dt = (time.perf_counter() - t0) * scale
-        if i >= args.warmup:
-            steps.append(dt)
-    t = statistics.median(steps)
-    value = (len(inp.r) + n_s) / t
-    info["value"] = value
-    line = {"impl": "reference", "metric": "join tuples/s ((|R|+|S|)/time)", "value": value, "unit": "tuples/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
-            "data": "synthetic", "config": _config_block(args, inp), "cpu_baseline": info,
-            "e2e": {"value": value, "unit": "tuples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
-
-
-def _config_block(args, inp):
-    return {"workload": f"{args.config}: {inp.description}", "algorithm": inp.algorithm,
-            "variant": getattr(args, "variant", None) if inp.algorithm != "lsj" else None,
-            "n_r": len(inp.r), "n_s": len(inp.s), "l2": "inputs larger than L2 and L2 flushed between steps",
-            "parallelism": _parallelism(args.config, inp.algorithm, args.gpus)}
-
-
-def _parallelism(cfg, algorithm, n):
-    if cfg == "c5":
-        return f"lsj range shuffle over {n} GPU(s): shared model, NCCL all-to-all-v, local LSJ"
-    if algorithm == "lsj":
-        return f"lsj replicas x{n} (one full join per GPU)"
-    if cfg in SHARDED:
-        return f"inlj replicated R, S sharded 1/{n} per GPU"
-    return f"inlj replicated R, full S per GPU x{n}"
-
-
-# ---------------------------------------------------------------- GPU arm
-
-
 def run_b200(args):
     import torch
     import torch.distributed as dist
 
     rank, world, local = _env_rank()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     use_pg = world > 1 or args.config == "c5"  # C5 always runs the distributed LSJ
     if use_pg:
@@ -412,9 +485,9 @@ def run_b200(args):
     xor_all = 0
     if world > 1 and not reduced:
         for v in xors.cpu().tolist():
-            xor_all ^= v & (2**64 - 1)
+            xor_all ^= v & MASK
     else:
-        xor_all = w[2] & (2**64 - 1)
+        xor_all = w[2] & MASK
 
     # the dominant kernel timed alone, live, with CUDA events on its stream
     dom = []
@@ -454,11 +527,10 @@ def run_b200(args):
             gbs = bpt * (n_r + n_s) / (ms / 1e3) / 1e9
             roofline["lsj_phases"][name] = {"ms": ms, "achieved": gbs, "frac": gbs / peak,
                                             "algorithmic_bytes": f"{bpt} B/tuple x {n_r + n_s}"}
-    ph = getattr(run_step, "holder", {}).get("phases") if hasattr(run_step, "holder") else None
+    ph = run_step.holder.get("phases")
     if ph is not None and "shuffle" in ph:
         # the range shuffle against NVLink (16 B x (|R|+|S|)/G x
-        # (G-1)/G per GPU leave the GPU); partition and exchange are one fused
-        # step, timed on the host around its stream syncs
+        # (G-1)/G per GPU leave the GPU)
         moved = 16 * (n_r + n_s) * (world - 1) / world
         sh_ms = (ph["part"] + ph["xchg"]) * 1e3
         roofline["nvlink"] = {"bytes_per_gpu": moved, "shuffle_ms": sh_ms, "peak": 900.0, "unit": "GB/s",
@@ -469,78 +541,83 @@ def run_b200(args):
 
     e2e = None
     if not args.no_e2e:
-        e2e = _e2e(args, inp, index, world, run_step)
-    line = None
+        e2e = _e2e(args, inp, world)
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             try:
-                _, cpu, _ = cpu_inlj(inp)
+                from paper_2111_08824_b200.util import to_numpy_u64
+
+                s_keys, s_pays = inp.s.keys, inp.s.payloads
+                cj = CpuJoin(inp.algorithm, dict(inp.opts, seed=42), to_numpy_u64(inp.r.keys),
+                             to_numpy_u64(inp.r.payloads),
+                             lambda lo, hi: (to_numpy_u64(s_keys[lo:hi]), to_numpy_u64(s_pays[lo:hi])), n_s)
+                cpu, _ = cpu_baseline(cj, n_r)
             except Exception as exc:  # the baseline is reported, never required
                 cpu = {"error": repr(exc)}
-        line = {"metric": "join tuples/s ((|R|+|S|)/time)", "value": value, "unit": "tuples/s", "n_gpus": world,
+        line = {"metric": METRIC, "value": value, "unit": "tuples/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": args.scaling, "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-                "config": _config_block(args, inp), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "scaling": args.scaling, "vs_baseline": None, "dtype": "u64",
+                "data": "synthetic (device generator, seeded; == host generator oracle/gen.py)",
+                "config": _config_block(args, job_r if "r" in sh else n_r, job_s if "s" in sh else n_s),
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": (launches * args.steps) if launches is not None else None,
                 "clocks": clk.summary(),
-                "checksum": {"count": w[0], "sum": w[1] & (2**64 - 1), "xor": xor_all, "search_steps": w[3]}}
+                "checksum": {"count": w[0], "sum": w[1] & MASK, "xor": xor_all, "search_steps": w[3]}}
         print(json.dumps(line), flush=True)
     if use_pg:
         dist.destroy_process_group()
 
 
-def _e2e(args, inp, index, world, run_step=None):
-    """Same metric through the public API from pinned HOST buffers: every
-    step copies S (INLJ) or R and S (LSJ) host->device into a validated
-    Relation, runs the join and reads the 3-word result back."""
+def _e2e(args, inp, world):
+    """The same metric through the reference-facing registry entry point
+    ``ALGORITHMS[name](r, s, 1, opts)`` with HOST-resident relations
+    (pinned): the runner copies S host->device inside its timed region
+    (chunked, overlapped with the join; LSJ: R and S, overlapped with R's
+    side) and reads the 3 result words back.  The INLJ index over R is
+    built untimed inside the runner, as the reference's runners do."""
     import torch
 
     import paper_2111_08824_b200 as lj
 
-    hk = inp.s.keys.cpu().pin_memory()
-    hp = inp.s.payloads.cpu().pin_memory()
-    h2d = 16 * len(inp.s)
-    if index is None:
-        rk = inp.r.keys.cpu().pin_memory()
-        rp = inp.r.payloads.cpu().pin_memory()
-        h2d += 16 * len(inp.r)
-        o = dict(lj.DEFAULT_OPTS, **inp.opts)
-        cfg = lj.LsjConfig(workers=1, fanout=o["fanout"], sample_rate=o["sample_rate"], seed=o["seed"])
-    scratch = getattr(run_step, "scratch", None) if (index is not None and args.variant == "buffered") else None
+    r_host = lj.Relation.on_host(inp.r.keys.cpu(), inp.r.payloads.cpu())
+    s_host = lj.Relation.on_host(inp.s.keys.cpu(), inp.s.payloads.cpu())
+    opts = dict(lj.DEFAULT_OPTS, **inp.opts)
+    algo = inp.algorithm if inp.algorithm != "grmi-inlj" or args.variant == "direct" else "buffered-grmi-inlj"
+    h2d = 16 * len(inp.s) + (16 * len(inp.r) if inp.algorithm == "lsj" else 0)
     steps = max(1, min(args.steps, 3))
     times = []
     for i in range(steps + 1):
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        if index is None:
-            s = r = None
-            if args.config == "c5":
-                s = lj.Relation(hk.to("cuda", non_blocking=True), hp.to("cuda", non_blocking=True), validate=True)
-                r = lj.Relation(rk.to("cuda", non_blocking=True), rp.to("cuda", non_blocking=True), validate=True)
-                from paper_2111_08824_b200 import dist as ljdist
+        if args.config == "c5":
+            from paper_2111_08824_b200 import dist as ljdist
 
-                (c, sm, x), _ = ljdist.lsj_join(r.keys, r.payloads, s.keys, s.payloads, cfg)
-                res = lj.JoinResult(checksum=(c, sm, x))
-            else:
-                res = lj.lsj_join_host(rk, rp, hk, hp, cfg)
-            del s, r
+            t0 = time.perf_counter()
+            r, s = r_host.to_device(), s_host.to_device()
+            cfg = lj.LsjConfig(workers=1, fanout=opts["fanout"], sample_rate=opts["sample_rate"], seed=opts["seed"])
+            ljdist.lsj_join(r.keys, r.payloads, s.keys, s.payloads, cfg)
+            rt = time.perf_counter() - t0
+            del r, s
         else:
-            # S streamed from pinned host memory: chunk copies on a copy
-            # stream overlapped with the bucketing + probe of the previous one
-            words = lj.join_checksum_host(index, hk, hp, buffered=scratch is not None, scratch=scratch)
-            res = lj.JoinResult(words=words)
-        _ = res.checksum
-        dt = time.perf_counter() - t0
+            _, _, rt = lj.ALGORITHMS[algo](r_host, s_host, 1, opts)
         if i:
-            times.append(dt)
+            times.append(rt)
     t = statistics.median(times)
-    n_s = len(inp.s)
-    how = ("lj.lsj_join_host: R's sample/fit/partition/sort overlap S's H2D" if index is None else
-           "lj.join_checksum_host: S in 2^25-tuple chunks, H2D on a copy stream overlapped with the join")
-    return {"value": getattr(args, "job_tuples", len(inp.r) + world * n_s) / t, "unit": "tuples/s",
-            "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": 4 * 8, "ms_per_step": t * 1e3, "steps": steps, "path": how}
+    if world > 1:
+        import torch.distributed as dist
+
+        tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    path = (f"lj.ALGORITHMS[{algo!r}](Relation.on_host(R), Relation.on_host(S), 1, opts): runner-timed probe "
+            "(S in 2^25-tuple chunks, H2D on a copy stream overlapped with the grouping + probe)"
+            if inp.algorithm != "lsj" else
+            f"lj.ALGORITHMS['lsj'](host R, host S, 1, opts): lsj_join_host, R's side overlaps S's H2D")
+    if args.config == "c5":
+        path = "dist.lsj_join over R and S copied from pinned host memory"
+    return {"value": getattr(args, "job_tuples", len(inp.r) + world * len(inp.s)) / t, "unit": "tuples/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 3 * 8, "ms_per_step": t * 1e3, "steps": steps,
+            "path": path}
 
 
 def _ncu_traffic(cfg):
@@ -552,26 +629,44 @@ def _ncu_traffic(cfg):
         return None
 
 
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_under_torchrun(args_list, n):
+    """``--gpus N`` outside torchrun: one process per GPU via
+    torch.distributed.run on this node; rank 0's JSON line passes through."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + args_list
+    return subprocess.run(cmd).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--variant", default=None, choices=["buffered", "direct"],
                     help="INLJ: group S by index window on device first (Request-Buffer analogue) or probe "
-                         "directly; default per config (c2 buffered, c1/c3 direct)")
+                         "directly; default per config (c2/c3 buffered, c1 direct)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--scale", type=int, default=None, help="config size shift (tests only; not a bench number)")
+    ap.add_argument("--no-full-checksum", action="store_true", help="reference arm: skip the full-size oracle pass")
+    ap.add_argument("--scale", type=int, default=None, help="config size divisor / shift (tests only; not a bench "
+                                                            "number)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3
     if args.impl == "reference":
         run_reference_arm(args)
-    else:
-        run_b200(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(sys.argv[1:], args.gpus))
+    run_b200(args)
 
 
 if __name__ == "__main__":

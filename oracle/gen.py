@@ -20,7 +20,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import _i64, _p, _u64p, lib
+from . import _i64, _p, _u64p, lib, sort_u64
 
 _f64p = ctypes.POINTER(ctypes.c_double)
 _i64p = ctypes.POINTER(ctypes.c_int64)
@@ -117,18 +117,38 @@ def distinct_first(draw, n) -> np.ndarray:
 
 def shuffle(t: np.ndarray, seed) -> np.ndarray:
     # configs.shuffle: argsort of signed int64 draws (no ties in practice)
-    return t[np.argsort(mix(t.size, seed).view(np.int64), kind="stable")]
+    keys = np.ascontiguousarray(mix(t.size, seed).view(np.int64))
+    order = np.empty(t.size, np.int64)
+    if t.size:
+        lib().orc_argsort_i64(_p(keys, _i64p), _i64(t.size), _p(order, _i64p))
+    return t[order]
+
+
+def searchsorted_left(cdf: np.ndarray, u: np.ndarray) -> np.ndarray:
+    """np.searchsorted(cdf, u, side="left"), in parallel C."""
+    cdf = np.ascontiguousarray(cdf, dtype=np.float64)
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    out = np.empty(u.size, np.int64)
+    if u.size:
+        lib().orc_searchsorted_f64(_p(cdf, _f64p), _i64(cdf.size), _p(u, _f64p), _i64(u.size), _p(out, _i64p))
+    return out
 
 
 def zipf_ranks(n, N, s, seed) -> np.ndarray:
     w = np.arange(1, N + 1, dtype=np.float64) ** (-s)
     cdf = np.cumsum(w)
     u = unit(n, seed) * cdf[-1]
-    return np.minimum(np.searchsorted(cdf, u, side="left"), N - 1)
+    return np.minimum(searchsorted_left(cdf, u), N - 1)
 
 
 def not_in(sorted_r: np.ndarray, cand: np.ndarray) -> np.ndarray:
-    pos = np.minimum(np.searchsorted(sorted_r, cand), sorted_r.size - 1)
+    sorted_r = np.ascontiguousarray(sorted_r, dtype=np.uint64)
+    cand = np.ascontiguousarray(cand, dtype=np.uint64)
+    pos = np.empty(cand.size, np.int64)
+    if cand.size:
+        lib().orc_searchsorted_u64(_p(sorted_r, _u64p), _i64(sorted_r.size), _p(cand, _u64p), _i64(cand.size),
+                                   _p(pos, _i64p))
+    pos = np.minimum(pos, sorted_r.size - 1)
     return cand[sorted_r[pos] != cand]
 
 
@@ -162,7 +182,7 @@ def config1(scale: int = 0, seed: int = 0xC1, shard: int = 0) -> HostInputs:
     hits = int(round(0.9 * ns))
     ss = seed ^ (shard << 40)
     sk_hit = gather_uniform(rk, hits, ss ^ 0x51)
-    srt = np.sort(rk)
+    srt = sort_u64(rk)
     miss = np.empty(0, np.uint64)
     off = 0
     while miss.size < ns - hits:
@@ -184,7 +204,7 @@ def config2(scale: int = 0, seed: int = 0xC2, shard: int = 0) -> HostInputs:
 
     rk = distinct_first(draw, nr)
     rp = payloads(nr, seed ^ 0x11)
-    srt = np.sort(rk)
+    srt = sort_u64(rk)
     hits = int(round(0.95 * ns))
     ss = seed ^ (shard << 40)
     sk_hit = srt[zipf_ranks(hits, nr, 0.8, ss ^ 0x21)]
@@ -229,7 +249,7 @@ def config4(scale: int = 0, seed: int = 0xC4, shard: int = 0) -> HostInputs:
 
     rk = distinct_first(draw, nr)
     rp = payloads(nr, seed ^ 0x41)
-    sk = np.sort(rk)[zipf_ranks(ns, nr, 1.0, seed ^ 0x42 ^ (shard << 40))]
+    sk = sort_u64(rk)[zipf_ranks(ns, nr, 1.0, seed ^ 0x42 ^ (shard << 40))]
     sp = payloads(ns, seed ^ 0x43 ^ (shard << 40))
     return HostInputs("c4", rk, rp, ns, {"fanout": 4096, "sample_rate": 0.01}, "lsj",
                       lambda lo, hi: (sk[lo:hi], sp[lo:hi]))

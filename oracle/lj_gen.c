@@ -130,3 +130,33 @@ void orc_first_occurrence(const u64 *v, i64 n, uint8_t *keep) {
     free(idx);
     free(hist);
 }
+
+/* np.searchsorted(cdf, u, side="left") for sorted doubles, in parallel */
+void orc_searchsorted_f64(const double *cdf, i64 n, const double *u, i64 m, i64 *out) {
+#pragma omp parallel for schedule(static)
+    for (i64 i = 0; i < m; ++i) {
+        const double v = u[i];
+        i64 lo = 0, hi = n;
+        while (lo < hi) {
+            const i64 mid = (lo + hi) >> 1;
+            if (cdf[mid] < v) lo = mid + 1;
+            else hi = mid;
+        }
+        out[i] = lo;
+    }
+}
+
+/* np.searchsorted(sorted, v, side="left") for u64, in parallel */
+void orc_searchsorted_u64(const u64 *sorted, i64 n, const u64 *v, i64 m, i64 *out) {
+#pragma omp parallel for schedule(static)
+    for (i64 i = 0; i < m; ++i) {
+        const u64 x = v[i];
+        i64 lo = 0, hi = n;
+        while (lo < hi) {
+            const i64 mid = (lo + hi) >> 1;
+            if (sorted[mid] < x) lo = mid + 1;
+            else hi = mid;
+        }
+        out[i] = lo;
+    }
+}

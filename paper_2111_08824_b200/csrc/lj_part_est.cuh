@@ -244,6 +244,106 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_est(Src f0, i64 n, i64
     }
 }
 
+// Direct claims scatter: the same regions, claims and overflow as
+// k_bin_scatter_est, without the in-tile permutation.  Each tuple keeps its
+// (bin, rank in the tile's run) in registers; after one claim per (tile,
+// bin) every thread stores its own tuples straight to base[bin] + rank.  A
+// warp's stores scatter over ~32 runs, but every run is one contiguous
+// piece of its bin's shared frontier, so L2 assembles whole lines before
+// they are written back.  Per tuple: 2 sequential + 2 random shared-memory
+// accesses (the permuting scatter needs ~11) and 2 barriers per tile.
+// DT tuples per tile, DNT threads, 2 CTAs per SM (their barriers overlap).
+constexpr int DNT = 512;
+constexpr int DTILE = 2048;
+template <class Src>
+__global__ void __launch_bounds__(DNT, 2) k_scatter_direct(Src f0, i64 n, i64 chunk, int nbins, int nst,
+                                                           const i64 *__restrict__ rstart, u32 *gcur,
+                                                           unsigned long long *ovf, ulonglong2 *out) {
+    constexpr int U = DTILE / DNT;
+    constexpr size_t STAGE = (size_t)DTILE * 16;
+    extern __shared__ __align__(128) unsigned char smem_d[];
+    u64 *tab = reinterpret_cast<u64 *>(smem_d);
+    unsigned char *smem = smem_d + pt_table_bytes(f0.f.smem_words());
+    f0.f.stage(tab);
+    Src f = f0;
+    f.f = f0.f.at(tab);
+    const int nb4 = (nbins + 31) & ~31;
+    u32 *thist = reinterpret_cast<u32 *>(smem);                // this tile's count per bin
+    i64 *base = reinterpret_cast<i64 *>(thist + nb4);          // this tile's run start per bin (records)
+    i64 *lim = base + nb4;                                     // region end per bin
+    unsigned char *ring = reinterpret_cast<unsigned char *>(lim + nb4);
+    __shared__ __align__(8) uint64_t full[PT_MAXST];
+    const int tid = threadIdx.x, shift = f.f.shift;
+    for (int j = tid; j < nbins; j += DNT) {
+        thist[j] = 0;
+        lim[j] = rstart[j + 1];
+    }
+    const i64 ovf0 = rstart[nbins];
+    const i64 lo = blockIdx.x * chunk, hi = min(lo + chunk, n);
+    const int ntiles = hi > lo ? (int)((hi - lo + DTILE - 1) / DTILE) : 0;
+    auto issue = [&](int t) {
+        const int s = t % nst;
+        const i64 b0 = lo + (i64)t * DTILE;
+        const int cnt = (int)min((i64)DTILE, hi - b0);
+        const unsigned b8 = (unsigned)(cnt * 8) & ~15u;
+        unsigned char *st = ring + (size_t)s * STAGE;
+        if (b8) {
+            mbar_arrive_expect_tx(&full[s], 2 * b8);
+            bulk_g2s(st, f.keys + b0, b8, &full[s]);
+            bulk_g2s(st + DTILE * 8, f.pay + b0, b8, &full[s]);
+        } else {
+            mbar_arrive(&full[s]);
+        }
+    };
+    if (tid == 0) {
+        for (int s = 0; s < nst; ++s) mbar_init(&full[s], 1);
+        mbar_init_fence();
+        for (int t = 0; t < min(nst - 1, ntiles); ++t) issue(t);
+    }
+    __syncthreads();
+    for (int t = 0; t < ntiles; ++t) {
+        const int s = t % nst;
+        mbar_wait(&full[s], (unsigned)(t / nst) & 1u);
+        const i64 b0 = lo + (i64)t * DTILE;
+        const int cnt = (int)min((i64)DTILE, hi - b0), nb2 = cnt & ~1;
+        const unsigned char *st = ring + (size_t)s * STAGE;
+        const u64 *ks = reinterpret_cast<const u64 *>(st), *ps = ks + DTILE;
+        // (1) bin + rank in the tile's run
+        int bj[U];
+        u32 rj[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = u * DNT + tid;
+            bj[u] = j < cnt ? (int)(f.code(j < nb2 ? ks[j] : ld_stream(f.keys + b0 + j)) >> shift) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) rj[u] = bj[u] >= 0 ? atomicAdd(thist + bj[u], 1u) : 0u;
+        __syncthreads();
+        // every thread is past tile t-1's stores: its stage may be refilled
+        if (tid == 0 && t + nst - 1 < ntiles) issue(t + nst - 1);
+        // (2) one claim per nonempty (tile, bin)
+        for (int b = tid; b < nbins; b += DNT) {
+            const u32 c = thist[b];
+            if (c) {
+                base[b] = rstart[b] + (i64)atomicAdd(gcur + b, c);
+                thist[b] = 0;
+            }
+        }
+        __syncthreads();
+        // (3) every tuple to its run (overflow behind the regions)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (bj[u] < 0) continue;
+            const int j = u * DNT + tid;
+            const u64 k = j < nb2 ? ks[j] : ld_stream(f.keys + b0 + j);
+            const u64 p = j < nb2 ? ps[j] : ld_stream(f.pay + b0 + j);
+            i64 dst = base[bj[u]] + (i64)rj[u];
+            if (dst >= lim[bj[u]]) dst = ovf0 + (i64)atomicAdd(ovf, 1ULL);
+            out[dst] = make_ulonglong2(k, p);
+        }
+    }
+}
+
 static __global__ void k_est_regions(const i64 *rstart, const u32 *gcur, const unsigned long long *ovf, int nbins,
                               i64 *reg) {
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b <= nbins; b += gridDim.x * blockDim.x) {
@@ -411,6 +511,72 @@ template <class Src>
 int run_partition_est(const Src &f, i64 n, int nbins, ulonglong2 *out, i64 *reg, void *ws, size_t ws_bytes,
                       cudaStream_t st) {
     return run_partition_claims(f, n, nbins, 0, out, reg, ws, ws_bytes, st);
+}
+
+// The same one-pass regions through the direct claims scatter
+// (k_scatter_direct: 2 CTAs per SM, no in-tile permutation).
+template <class Src>
+int run_partition_direct(const Src &f, i64 n, int nbins, ulonglong2 *out, i64 *reg, void *ws, size_t ws_bytes,
+                         cudaStream_t st) {
+    if (nbins < 1 || nbins > 4096) {
+        set_error("partition_direct: nbins must be in [1, 4096]");
+        return LJ_E_INVALID;
+    }
+    if (ws_bytes < est_workspace_bytes(nbins)) {
+        set_error("partition_direct: workspace too small");
+        return LJ_E_WORKSPACE;
+    }
+    char *q = (char *)ws;
+    u32 *est = (u32 *)q;
+    q += part_align(sizeof(u32) * (size_t)nbins);
+    u32 *gcur = (u32 *)q;
+    q += part_align(sizeof(u32) * (size_t)nbins);
+    i64 *cap = (i64 *)q;
+    q += part_align(sizeof(i64) * (size_t)(nbins + 1));
+    i64 *rstart = (i64 *)q;
+    q += part_align(sizeof(i64) * (size_t)(nbins + 1));
+    unsigned long long *ovf = (unsigned long long *)q;
+    q += part_align(sizeof(unsigned long long));
+    LJ_CK(cudaMemsetAsync(est, 0, sizeof(u32) * (size_t)nbins, st));
+    LJ_CK(cudaMemsetAsync(gcur, 0, sizeof(u32) * (size_t)nbins, st));
+    LJ_CK(cudaMemsetAsync(ovf, 0, sizeof(unsigned long long), st));
+    const size_t tb = pt_table_bytes(f.f.smem_words());
+    const size_t nb4 = (size_t)((nbins + 31) & ~31);
+    const size_t fix = tb + nb4 * (sizeof(u32) + 2 * sizeof(i64));
+    const size_t stage = (size_t)DTILE * 16;
+    const int nst = (int)min((size_t)4, ((size_t)(113 * 1024) - fix) / stage);  // two CTAs per SM
+    if (nst < 2) {
+        set_error("partition_direct: shared memory too small for the ring");
+        return LJ_E_INVALID;
+    }
+    static bool attr = false;
+    if (!attr) {
+        LJ_CK(cudaFuncSetAttribute(k_scatter_direct<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(fix + nst * stage)));
+        LJ_CK(cudaFuncSetAttribute(k_est_sample<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_SMEM_MAX));
+        attr = true;
+    }
+    if (n > 0) {
+        k_est_sample<Src><<<grid_for((n + EST_STRIDE - 1) / EST_STRIDE, 256, 4), 256, tb + sizeof(u32) * nbins,
+                            st>>>(f, n, nbins, EST_STRIDE, est, nullptr);
+        LJ_CK_LAUNCH();
+    }
+    k_est_caps<<<(nbins + 256) / 256, 256, 0, st>>>(est, nbins, 0, cap);
+    LJ_CK_LAUNCH();
+    size_t t = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, t, cap, rstart, (int64_t)(nbins + 1));
+    LJ_CK(cub::DeviceScan::ExclusiveSum(q, t, cap, rstart, (int64_t)(nbins + 1), st));
+    if (n > 0) {
+        const int blocks = 2 * sm_count();
+        i64 c = (n + blocks - 1) / blocks;
+        c = (c + 31) / 32 * 32;
+        k_scatter_direct<Src><<<blocks, DNT, fix + nst * stage, st>>>(f, n, c < 32 ? 32 : c, nbins, nst, rstart, gcur,
+                                                                      ovf, out);
+        LJ_CK_LAUNCH();
+    }
+    k_est_regions<<<(nbins + 256) / 256, 256, 0, st>>>(rstart, gcur, ovf, nbins, reg);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
 }
 
 // Exact partition: out[n] grouped by bin, starts[nbins+1].  Bulk-copy

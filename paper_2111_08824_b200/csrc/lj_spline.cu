@@ -493,7 +493,11 @@ int lj_spline_hash_bucket_est(const LjSplineHash *idx, const uint64_t *keys, con
         kb.g = lay;
         kb.nb = nb;
         SoaSrc<KeyRangeBin> ksrc{keys, pay, kb};
-        const int rc = run_partition_est(ksrc, nk, nb, reinterpret_cast<ulonglong2 *>(pairs_out), reg_out, ws, eb, st);
+        static const bool direct = getenv("LJ_HASH_DIRECT") != nullptr;
+        const int rc = direct ? run_partition_direct(ksrc, nk, nb, reinterpret_cast<ulonglong2 *>(pairs_out), reg_out,
+                                                     ws, eb, st)
+                              : run_partition_est(ksrc, nk, nb, reinterpret_cast<ulonglong2 *>(pairs_out), reg_out,
+                                                  ws, eb, st);
         if (rc) return rc;
         k_fill_gaps<<<(unsigned)nb, 256, 0, st>>>(reg_out, nb, reinterpret_cast<ulonglong2 *>(pairs_out));
         LJ_CK_LAUNCH();
@@ -516,8 +520,11 @@ int lj_spline_hash_bucket_est(const LjSplineHash *idx, const uint64_t *keys, con
         wb.kshift = idx->model.shift;
         wb.rmax = nrad - 1;
         SoaSrc<WinBin> wsrc{keys, pay, wb};
-        const int rc = run_partition_est(wsrc, nk, (int)f.nb, reinterpret_cast<ulonglong2 *>(pairs_out), reg_out, ws,
-                                         ws_bytes - wtb, st);
+        static const bool direct = getenv("LJ_HASH_DIRECT") != nullptr;
+        const int rc = direct ? run_partition_direct(wsrc, nk, (int)f.nb, reinterpret_cast<ulonglong2 *>(pairs_out),
+                                                     reg_out, ws, ws_bytes - wtb, st)
+                              : run_partition_est(wsrc, nk, (int)f.nb, reinterpret_cast<ulonglong2 *>(pairs_out),
+                                                  reg_out, ws, ws_bytes - wtb, st);
         if (rc) return rc;
         k_fill_gaps<<<(unsigned)f.nb, 256, 0, st>>>(reg_out, (int)f.nb, reinterpret_cast<ulonglong2 *>(pairs_out));
         LJ_CK_LAUNCH();

@@ -29,6 +29,40 @@ class Relation:
         self.keys = k
         self.payloads = p
 
+    @classmethod
+    def on_host(cls, keys, payloads) -> "Relation":
+        """A relation left in (pinned) HOST memory, as the reference's numpy
+        relations are: the join runners copy it to the device inside their
+        timed region (S streamed in chunks, overlapped with the probe) and
+        validate its keys there.  ``keys``/``payloads``: numpy uint64 or CPU
+        int64 tensors."""
+        def host(x):
+            if isinstance(x, torch.Tensor):
+                t = x.view(torch.int64) if x.dtype == torch.uint64 else x
+            else:
+                t = torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.uint64)).view(np.int64))
+            if t.device.type != "cpu" or t.dim() != 1:
+                raise ValueError("host relations take 1-D CPU arrays")
+            return t.contiguous() if t.is_pinned() else t.contiguous().pin_memory()
+
+        self = cls.__new__(cls)
+        self.keys, self.payloads = host(keys), host(payloads)
+        if self.keys.shape != self.payloads.shape:
+            raise ValueError("keys and payloads must have equal length")
+        return self
+
+    @property
+    def is_host(self) -> bool:
+        return self.keys.device.type == "cpu"
+
+    def to_device(self, device=None) -> "Relation":
+        """The device copy of a host relation (keys validated); a device
+        relation is returned as is."""
+        if not self.is_host:
+            return self
+        dev = device or "cuda"
+        return Relation(self.keys.to(dev, non_blocking=True), self.payloads.to(dev, non_blocking=True))
+
     def __len__(self) -> int:
         return int(self.keys.numel())
 

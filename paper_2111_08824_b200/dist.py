@@ -139,12 +139,16 @@ def _gpu_shared_model(r_keys: torch.Tensor, sample_rate: float, seed: int, world
 
     lib = _lib.lib()
     n = r_keys.numel()
-    total = max(1, int(round(sample_rate * n)))
+    # a rank without R tuples still joins the gather, with an empty sample
+    total = max(1, int(round(sample_rate * n))) if n else 0
     sample = torch.empty(total, dtype=torch.int64, device=r_keys.device)
-    ws = _lib.workspace(lib.lj_lsj_sample_workspace_bytes(total), r_keys.device)
-    _lib.check(lib.lj_lsj_sample(_lib.ptr(r_keys), n, total, int(seed) & MASK, _lib.ptr(sample), _lib.ptr(ws),
-                                 ws.numel(), _lib.stream_ptr()), "lsj_sample")
+    if total:
+        ws = _lib.workspace(lib.lj_lsj_sample_workspace_bytes(total), r_keys.device)
+        _lib.check(lib.lj_lsj_sample(_lib.ptr(r_keys), n, total, int(seed) & MASK, _lib.ptr(sample), _lib.ptr(ws),
+                                     ws.numel(), _lib.stream_ptr()), "lsj_sample")
     allsamp = gather_varlen(sample, group)
+    if allsamp.numel() == 0:
+        raise ValueError("distributed LSJ: R is empty on every rank")
     srt, _ = sort_pairs(allsamp, allsamp)
     fanout = min(1000, max(1, srt.numel() // 8))
     rmi = RecursiveModelIndex(fanout).fit(srt)
@@ -168,7 +172,7 @@ def shuffle_plan(counts: np.ndarray, rank: int):
     return recv_r, recv_s, cap, off_r, off_s
 
 
-_SYMM: dict = {}  # (device, group) -> (symmetric receive buffer, handle)
+_SYMM: dict = {}  # (device, group name, world) -> (symmetric receive buffer, handle)
 
 
 def _pg(group):
@@ -209,7 +213,8 @@ def fused_shuffle(r_keys, r_payloads, s_keys, s_payloads, model, group=None):
     recv_r, recv_s, cap, off_r, off_s = shuffle_plan(counts, rank)
     # the receive buffer is reused while it is large enough (cap is the same
     # on every rank, so every rank takes the same decision)
-    key = (dev.index, id(_pg(group)))
+    # keyed by the group's NAME (a destroyed group's id() can be reused)
+    key = (dev.index, getattr(_pg(group), "group_name", str(id(_pg(group)))), world)
     got = _SYMM.get(key)
     if got is None or got[0].numel() < 2 * max(cap, 1):
         buf = symm.empty(2 * max(cap, 1) + (2 * max(cap, 1)) // 8, dtype=torch.int64, device=dev)
@@ -242,9 +247,11 @@ def lsj_join(r_keys, r_payloads, s_keys, s_payloads, config=None, group=None, *,
     """Distributed LSJ over this rank's shards of R and S.  Returns
     ((count, sum, xor), phases) -- the global checksum on every rank.
 
-    On CUDA tensors the shuffle is `fused_shuffle` (partition + P2P stores
-    into symmetric memory); with injected partition functions (host tests)
-    or LJ_SHUFFLE=nccl, the partition is followed by an NCCL all-to-all-v."""
+    The default shuffle is the partition followed by an NCCL all-to-all-v.
+    LJ_SHUFFLE=fused selects `fused_shuffle` (partition + P2P stores into
+    symmetric memory): it is checked on one GPU (a one-rank group) and by
+    the layout tests, and stays opt-in until a world >= 2 parity run on a
+    multi-GPU node (tests/test_gpu_multi.py) has passed."""
     from .lsj import LsjConfig
 
     config = config or LsjConfig()
@@ -260,11 +267,15 @@ def lsj_join(r_keys, r_payloads, s_keys, s_payloads, config=None, group=None, *,
             res, _ = _lsj.lsj_join(r, s, LsjConfig(workers=1, fanout=config.fanout,
                                                     sample_rate=config.sample_rate, seed=config.seed),
                                    counters=False)
-            words = res._words if res._words is not None else torch.tensor(
-                list(res.checksum) + [0], dtype=torch.int64)
-            return words
+            if res._words is not None:
+                return res._words
+            # empty local join (a rank that received no R or no S tuples):
+            # the words live on the device like every other rank's, so the
+            # NCCL reduction below sees a CUDA tensor on every rank
+            sg = [v - (1 << 64) if v >= (1 << 63) else v for v in list(res.checksum) + [0]]
+            return torch.tensor(sg, dtype=torch.int64, device=rrec.device)
     phases = {}
-    fused = (partition_fn is None and r_keys.is_cuda and os.environ.get("LJ_SHUFFLE", "fused") == "fused")
+    fused = (partition_fn is None and r_keys.is_cuda and os.environ.get("LJ_SHUFFLE", "nccl") == "fused")
     t0 = time.perf_counter()
     model = model_fn(r_keys)
     t1 = time.perf_counter()

@@ -100,10 +100,32 @@ def _materialized_probe(index, s: Relation, workers: int, br: PhaseBreakdown) ->
     return JoinResult.concatenate(parts)
 
 
-def _fused_probe(index, s: Relation, workers: int) -> torch.Tensor:
-    out = torch.zeros(4, dtype=torch.int64, device=s.keys.device)
+# S at least this large is grouped by index window on the device before the
+# probe (the Request-Buffer analogue: K4 + staged K1s for the GRMI, the
+# grouping pass + chunked probe for the learned hash); the words are
+# identical, the grouped path is 3x (GRMI) / 2x (hash) faster at C2 / C3
+GROUPED_MIN = 1 << 22
+
+
+def _fused_probe(index, s: Relation, workers: int, grouped: bool = True) -> torch.Tensor:
+    """Every S chunk probed into one device word set {count, sum, xor,
+    steps}.  A host-resident S streams through ``join_checksum_host`` (H2D
+    of chunk i+1 overlapped with the join of chunk i)."""
+    from .streaming import join_checksum_host
+
+    dev = (index.entries if hasattr(index, "entries") else index.slots).device
+    out = torch.zeros(4, dtype=torch.int64, device=dev)
     for lo, hi in _chunks(len(s), workers):
-        index.join_checksum(s.keys[lo:hi], s.payloads[lo:hi], out=out, accumulate=True)
+        if hi == lo:
+            continue
+        buffered = grouped and hi - lo >= GROUPED_MIN
+        if s.is_host:
+            w = join_checksum_host(index, s.keys[lo:hi], s.payloads[lo:hi], buffered=buffered)
+            out += w
+        elif buffered:
+            index.join_checksum_buffered(s.keys[lo:hi], s.payloads[lo:hi], out=out, accumulate=True)
+        else:
+            index.join_checksum(s.keys[lo:hi], s.payloads[lo:hi], out=out, accumulate=True)
     return out
 
 
@@ -112,10 +134,14 @@ def _empty():
 
 
 def _run_grmi_inlj(r, s, workers, opts):
-    """bench.py:138-144: GRMI fit untimed, probe timed."""
-    index = GappedRmiIndex(opts["gap_factor"], opts["rmi_fanout"]).fit(r)
+    """bench.py:138-144: GRMI fit untimed, probe timed.  Large S is grouped
+    by index window first (K4 + K1s; same words as the direct K1)."""
+    index = GappedRmiIndex(opts["gap_factor"], opts["rmi_fanout"]).fit(r.to_device())
     br = PhaseBreakdown()
+    if index.n == 0 or len(s) == 0:
+        return JoinResult(), br, 0.0
     if opts.get("materialize"):
+        s = s.to_device()
         result, runtime = _timed(lambda: _materialized_probe(index, s, workers, br))
     else:
         words, runtime = _timed(lambda: _fused_probe(index, s, workers))
@@ -125,54 +151,63 @@ def _run_grmi_inlj(r, s, workers, opts):
         br.lookup_stats.predictions = len(s)
     br.srch = runtime  # predict + search are one fused kernel (K1)
     if opts.get("counters", True) and len(s) and index.n:
-        leaf = index.leaf_of(s.keys)  # canonical full-stream counter (bench.py:130-134)
+        leaf = index.leaf_of(s.to_device().keys)  # canonical full-stream counter (bench.py:130-134)
         br.lookup_stats.leaf_switches = int((leaf[1:] != leaf[:-1]).sum().item())
     return result, br, runtime
 
 
 def _run_buffered_grmi_inlj(r, s, workers, opts):
     """bench.py:147-181: request buffers -> device leaf bucketing (K4) of
-    each S chunk, then the fused probe (K1) over the bucketed chunk."""
-    index = GappedRmiIndex(opts["gap_factor"], opts["rmi_fanout"]).fit(r)
+    each S chunk, then the fused probe (K1s) over the bucketed chunk."""
+    index = GappedRmiIndex(opts["gap_factor"], opts["rmi_fanout"]).fit(r.to_device())
     br = PhaseBreakdown()
     if index.n == 0 or len(s) == 0:
         return JoinResult(), br, 0.0
-    scratch = index.bucket_scratch(max(hi - lo for lo, hi in _chunks(len(s), workers)), s.keys.device)
-
-    def run():
-        out = torch.zeros(4, dtype=torch.int64, device=s.keys.device)
-        for lo, hi in _chunks(len(s), workers):
-            if hi > lo:
-                index.join_checksum_buffered(s.keys[lo:hi], s.payloads[lo:hi], out=out, accumulate=True,
-                                             scratch=scratch)
-        return out
-
     if opts.get("materialize"):
-        result, runtime = _timed(lambda: _materialized_probe(index, s, workers, br))
+        result, runtime = _timed(lambda: _materialized_probe(index, s.to_device(), workers, br))
+    elif s.is_host:
+        words, runtime = _timed(lambda: _fused_probe(index, s, workers))
+        result = _words_result(words, br, len(s))
     else:
+        scratch = index.bucket_scratch(max(hi - lo for lo, hi in _chunks(len(s), workers)), s.keys.device)
+
+        def run():
+            out = torch.zeros(4, dtype=torch.int64, device=s.keys.device)
+            for lo, hi in _chunks(len(s), workers):
+                if hi > lo:
+                    index.join_checksum_buffered(s.keys[lo:hi], s.payloads[lo:hi], out=out, accumulate=True,
+                                                 scratch=scratch)
+            return out
+
         words, runtime = _timed(run)
-        w = words.cpu().tolist()
-        result = JoinResult(checksum=(int(w[0]), int(w[1]) & (2**64 - 1), int(w[2]) & (2**64 - 1)))
-        br.lookup_stats.search_steps = int(w[3])
-        br.lookup_stats.predictions = len(s)
+        result = _words_result(words, br, len(s))
     if opts.get("counters", True):
-        br.lookup_stats.leaf_switches = schedule_leaf_switches(index.leaf_of(s.keys), opts["buffer_cap"])
+        br.lookup_stats.leaf_switches = schedule_leaf_switches(index.leaf_of(s.to_device().keys), opts["buffer_cap"])
     br.join = runtime
     return result, br, runtime
 
 
+def _words_result(words, br, n_s):
+    w = words.cpu().tolist()
+    br.lookup_stats.search_steps = int(w[3])
+    br.lookup_stats.predictions = n_s
+    return JoinResult(checksum=(int(w[0]) & (2**64 - 1), int(w[1]) & (2**64 - 1), int(w[2]) & (2**64 - 1)))
+
+
 def _run_spline_hash_inlj(r, s, workers, opts):
-    """bench.py:202-221: spline-hash fit untimed, probe timed (booked as pred)."""
+    """bench.py:202-221: spline-hash fit untimed, probe timed (booked as
+    pred).  Large S is grouped by index window first (same words as the
+    direct K5)."""
     if len(r) == 0:
         return _empty()
-    index = SplineHashIndex(opts["spline_error"], opts["radix_bits"], opts["table_factor"]).fit(r)
+    index = SplineHashIndex(opts["spline_error"], opts["radix_bits"], opts["table_factor"]).fit(r.to_device())
     br = PhaseBreakdown()
     if opts.get("materialize"):
-        result, runtime = _timed(lambda: _materialized_probe(index, s, workers, br))
+        result, runtime = _timed(lambda: _materialized_probe(index, s.to_device(), workers, br))
     else:
         words, runtime = _timed(lambda: _fused_probe(index, s, workers))
         w = words.cpu().tolist()
-        result = JoinResult(checksum=(int(w[0]), int(w[1]) & (2**64 - 1), int(w[2]) & (2**64 - 1)))
+        result = JoinResult(checksum=(int(w[0]) & (2**64 - 1), int(w[1]) & (2**64 - 1), int(w[2]) & (2**64 - 1)))
     br.pred = runtime
     br.lookup_stats.predictions = len(s)
     return result, br, runtime
@@ -198,10 +233,11 @@ def rmi_inlj(r_keys: torch.Tensor, r_payloads: torch.Tensor, model, s: Relation,
 def _run_rmi_inlj(r, s, workers, opts):
     """bench.py:184-192: sorted R + plain RMI fit untimed, probe timed (K12)."""
     from .models import RecursiveModelIndex
-    from .util import sort_pairs
+    from .util import sort_pairs, unsigned_order
 
     if len(r) == 0:
         return _empty()
+    r, s = r.to_device(), s.to_device()
     rk, rp = sort_pairs(r.keys, r.payloads)
     model = RecursiveModelIndex(opts["rmi_fanout"]).fit(rk)
     br = PhaseBreakdown()
@@ -209,8 +245,10 @@ def _run_rmi_inlj(r, s, workers, opts):
     w = words.cpu().tolist()
     result = JoinResult(checksum=(int(w[0]), int(w[1]) & (2**64 - 1), int(w[2]) & (2**64 - 1)))
     if opts.get("materialize"):  # pairs on device: every S key's equal run in sorted R
-        left = torch.searchsorted(rk, s.keys, side="left")
-        counts = torch.searchsorted(rk, s.keys, side="right") - left
+        # rk is sorted as UNSIGNED u64: search in the signed view of that order
+        ro, so = unsigned_order(rk), unsigned_order(s.keys)
+        left = torch.searchsorted(ro, so, side="left")
+        counts = torch.searchsorted(ro, so, side="right") - left
         src = torch.repeat_interleave(torch.arange(len(s), device=rk.device), counts)
         first = torch.repeat_interleave(left - (torch.cumsum(counts, 0) - counts), counts)
         slots = first + torch.arange(src.numel(), device=rk.device)
@@ -227,9 +265,19 @@ def _run_lsj(r, s, workers, opts):
 
     config = LsjConfig(workers=workers, sample_rate=opts["sample_rate"], fanout=opts["fanout"],
                        swwc=opts["swwc"], seed=opts["seed"])
+    if (r.is_host or s.is_host) and not opts.get("materialize"):
+        from .streaming import lsj_join_host
+
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        result = lsj_join_host(r.keys, r.payloads, s.keys, s.payloads, config)  # H2D overlapped with R's side
+        _ = result.checksum
+        return result, PhaseBreakdown(), time.perf_counter() - t0
+    r, s = r.to_device(), s.to_device()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    result, br = lsj_join(r, s, config, materialize=bool(opts.get("materialize")))
+    result, br = lsj_join(r, s, config, materialize=bool(opts.get("materialize")),
+                          counters=bool(opts.get("counters", True)))
     _ = result.checksum  # the 3-word readback is part of the join
     return result, br, time.perf_counter() - t0
 

@@ -162,3 +162,49 @@ def test_shuffle_plan_tiles_every_destination():
                 cover[off_r[d]:off_r[d] + counts[src, 0, d]] += 1
                 cover[off_s[d]:off_s[d] + counts[src, 1, d]] += 1
             assert (cover == 1).all()
+
+
+def _empty_rank_worker(rank, world, port, out_path):
+    """Everything is routed to rank 0: rank 1 receives no R and no S tuples
+    and must still take part in every collective (an empty local
+    join used to return CPU words while the other ranks reduced over NCCL)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2111_08824_b200 import dist as D
+
+    rk, rp, sk, sp = _inputs(9)
+    rlo, rhi = D.shard_bounds(rk.size, world, rank)
+    slo, shi = D.shard_bounds(sk.size, world, rank)
+    r_keys, r_pay = _t(rk[rlo:rhi]), _t(rp[rlo:rhi])
+    s_keys, s_pay = _t(sk[slo:shi]), _t(sp[slo:shi])
+
+    def partition_fn(keys, pays, model):
+        rec = torch.stack([keys, pays], dim=1).contiguous()
+        return rec, [int(keys.numel())] + [0] * (world - 1)
+
+    def local_join_fn(rrec, srec):
+        if rrec.shape[0] == 0 or srec.shape[0] == 0:
+            return torch.zeros(4, dtype=torch.int64, device=rrec.device)
+        c = oracle.smj_checksum(rrec[:, 0].numpy().view(np.uint64), rrec[:, 1].numpy().view(np.uint64),
+                                srec[:, 0].numpy().view(np.uint64), srec[:, 1].numpy().view(np.uint64))
+        return torch.tensor([c[0], np.int64(np.uint64(c[1])), np.int64(np.uint64(c[2])), 0], dtype=torch.int64)
+
+    res, phases = D.lsj_join(r_keys, r_pay, s_keys, s_pay, model_fn=lambda k: None, partition_fn=partition_fn,
+                             local_join_fn=local_join_fn)
+    with open(f"{out_path}.{rank}", "w") as f:
+        json.dump({"lsj": list(res), "n": [phases["n_r_local"], phases["n_s_local"]]}, f)
+    dist.destroy_process_group()
+
+
+def test_world2_lsj_with_an_empty_rank(tmp_path):
+    out = str(tmp_path / "e")
+    mp.spawn(_empty_rank_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    rk, rp, sk, sp = _inputs(9)
+    want = list(oracle.smj_checksum(rk, rp, sk, sp))
+    got = []
+    for rank in range(2):
+        with open(f"{out}.{rank}") as f:
+            got.append(json.load(f))
+    assert got[0]["lsj"] == want and got[1]["lsj"] == want
+    assert got[0]["n"] == [rk.size, sk.size] and got[1]["n"] == [0, 0]
