@@ -113,6 +113,14 @@ typedef struct LjSplineHash {
     const uint64_t *entries;/* [2n] interleaved {key, payload}, chains in
                                insertion order */
     const uint32_t *starts; /* [P/stride + 1] chain offsets (n < 2^32) */
+    /* Optional probe table (NULL: the chains are probed): [2 * nslots]
+     * interleaved {key, payload}, the entries in key order at slot
+     * max(2 * pos, previous slot + 1), gap slots holding the key to their
+     * left with payload 0, a final pair of keys ~0.  Built by
+     * lj_spline_slots_plan / _fill when every payload is nonzero; the probe
+     * scans forward from slot 2*pos(k) (lj_hash_staged.cu). */
+    const uint64_t *slots;
+    int64_t nslots;
 } LjSplineHash;
 
 /* ------------------------------------------------------------ library */
@@ -285,6 +293,17 @@ int lj_spline_hash_probe_grouped(const LjSplineHash *idx, const uint64_t *s_pair
  * layout: reg[2*bins+2] = region starts, region ends, overflow count; gap
  * records carry the reserved key 2^64-1); pairs_out holds
  * lj_spline_hash_bucket_capacity(nk, n) records; columns 16-B aligned. */
+/* Probe table of a spline-hash index (LjSplineHash.slots), from the build
+ * keys sorted ascending with their payloads: plan writes plan[0] = the slot
+ * count to allocate and plan[1] = the number of zero payloads (a table is
+ * only valid when it is 0) to DEVICE memory; fill (same workspace, after
+ * plan) writes the 2*nslots words.  Index build, untimed like the
+ * reference's (learned_hash.py:35-66). */
+size_t lj_spline_slots_workspace_bytes(int64_t n);
+int lj_spline_slots_plan(const LjSpline *model, const uint64_t *sorted_keys, const uint64_t *sorted_pay, int64_t n,
+                         int64_t *plan, void *ws, size_t ws_bytes, void *stream);
+int lj_spline_slots_fill(const uint64_t *sorted_keys, const uint64_t *sorted_pay, int64_t n, uint64_t *slots,
+                         int64_t nslots, void *ws, size_t ws_bytes, void *stream);
 int64_t lj_spline_hash_bucket_bins(int64_t n);
 int64_t lj_spline_hash_bucket_capacity(int64_t nk, int64_t n);
 size_t lj_spline_hash_bucket_est_workspace_bytes(const LjSplineHash *idx, int64_t nk);

@@ -59,7 +59,7 @@ class LjSpline(ctypes.Structure):
 
 class LjSplineHash(ctypes.Structure):
     _fields_ = [("model", LjSpline), ("n", _i64), ("table_len", _i64), ("stride", _i64),
-                ("entries", _c_void_p), ("starts", _c_void_p)]
+                ("entries", _c_void_p), ("starts", _c_void_p), ("slots", _c_void_p), ("nslots", _i64)]
 
 
 class LjLsjModel(ctypes.Structure):
@@ -77,6 +77,9 @@ SIGNATURES = {
     "lj_fill_mix64": (_int, [_P, _i64, _i64, _u64, _P]),
     "lj_gather_uniform": (_int, [_P, _i64, _i64, _u64, _P, _i64, _P]),
     "lj_fill_normal": (_int, [_P, _i64, _i64, _u64, _P]),
+    "lj_spline_slots_workspace_bytes": (_size_t, [_i64]),
+    "lj_spline_slots_plan": (_int, [ctypes.POINTER(LjSpline), _P, _P, _i64, _P, _P, _size_t, _P]),
+    "lj_spline_slots_fill": (_int, [_P, _P, _i64, _P, _i64, _P, _size_t, _P]),
     "lj_fill_lognormal": (_int, [_P, _i64, _i64, _u64, ctypes.c_double, ctypes.c_double, ctypes.c_double, _P]),
     "lj_fill_cluster": (_int, [_P, _i64, _i64, _u64, _P, _int, ctypes.c_double, ctypes.c_double, _P]),
     "lj_sort_pairs_workspace_bytes": (_size_t, [_i64]),

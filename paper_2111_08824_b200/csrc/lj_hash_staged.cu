@@ -1,0 +1,479 @@
+// lj_hash_staged.cu -- the grouped learned-hash probe (C3 hot path).
+// Reference: learned_hash.py:81-96 (probe_batch), models.py:221-248
+// (RadixSpline predict), bench.py:202-221 (_run_spline_hash_inlj).
+//
+// Two structures beside the reference's chains (lj_spline.cu):
+//
+// 1. The PROBE TABLE ("slots"), built once with the index (untimed, as the
+//    reference's build): the entries in key order, entry j at
+//        slot_j = max(2 * pos_j, slot_{j-1} + 1),   pos_j = spline pos of key_j
+//    (a prefix max: slot_j = j + max_{i<=j}(2 pos_i - i)), gap slots holding
+//    the key to their left with payload 0 (leading gaps: key_0), then a
+//    terminating pair of reserved keys ~0.  A key k lies at or after slot
+//    2*pos(k) (pos is monotone, so every earlier entry has a smaller key and
+//    a slot no later), every slot before it holds a smaller key, equal keys
+//    are adjacent REAL slots: the probe reads the 32-B aligned slot pair at
+//    2*pos(k) and scans forward over keys < k, counting keys == k with a
+//    nonzero payload, until a key > k.  The match set is exactly the chain
+//    scan's -- every R entry whose key equals k, since the chain of pos(k)
+//    holds every entry with key k -- so the checksum words are identical;
+//    one dependent 32-B load replaces starts[pos], starts[pos+1] and the
+//    chain entries.  Needs every build payload != 0 (the gap marker);
+//    otherwise the index keeps the chains only and the chained probe runs.
+//
+// 2. WINDOW STAGING: S arrives grouped into equi-depth KEY windows (the
+//    one-pass claims partition of lj_part_est.cuh with the key-range bins
+//    of lj_keybin.cuh).  Per window, a tiny kernel records the spline points
+//    the window's keys can need (the lower bound of every key in [klo, khi]
+//    and its predecessor) and a 1024-cell table over [klo, khi] giving each
+//    cell's lower-bound range.  The probe CTA bulk-copies a window's points
+//    (keys u64 + ranks f64) and cells into shared memory once per window
+//    and evaluates models.py:221-248 there -- the same first spline key >= k
+//    (hence the same pos, bit for bit, with the reference's float64
+//    operations) without a global load; records outside the staged range
+//    (overflow area, unstageable windows) take the global evaluation.
+//
+// Work is handed out in window order (pieces of HS_PIECE records) from one
+// counter, so all SMs work in the same one or two windows and their slot
+// lines stay in L2.
+#include <cub/cub.cuh>
+
+#include "lj_common.cuh"
+#include "lj_keybin.cuh"
+#include "lj_pipe.cuh"
+
+namespace lj {
+
+static inline size_t part_align_c(size_t v) { return (v + 255) & ~(size_t)255; }
+
+constexpr int HS_NT = 512;
+constexpr int HS_U = 2;
+constexpr int HS_CAP = 4096;   // staged spline points per window
+constexpr int HS_NC = 1024;    // lower-bound cells per window
+constexpr i64 HS_PIECE = 16384;
+constexpr int HS_MAXWIN = 2048;
+
+struct WinMeta {
+    u64 klo, khi;
+    int a0, npts, cshift, ok;
+};
+
+inline size_t hs_meta_bytes(int nb) {
+    return (((size_t)nb * sizeof(WinMeta) + 255) & ~(size_t)255) + (size_t)nb * (HS_NC + 8) * sizeof(u16);
+}
+
+__device__ __forceinline__ i64 lower_bound_u64(const u64 *a, i64 n, u64 k) {
+    i64 lo = 0, hi = n;
+    while (lo < hi) {
+        const i64 mid = (lo + hi) >> 1;
+        if (__ldg(reinterpret_cast<const unsigned long long *>(a) + mid) < k) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// ------------------------------------------------------------ probe table
+
+// t_j = 2 pos_j - j over the sorted build keys; zero[0] counts zero payloads
+__global__ void k_slots_t(SplineDev m, const u64 *sk, const u64 *sp, i64 n, i64 *t, unsigned long long *zero) {
+    u32 z = 0;
+    for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < n; j += (i64)gridDim.x * blockDim.x) {
+        t[j] = 2 * m.pos(sk[j]) - j;
+        z += sp[j] == 0;
+    }
+    if (z) atomicAdd(zero, (unsigned long long)z);
+}
+
+struct MaxI64 {
+    __device__ __forceinline__ i64 operator()(const i64 &a, const i64 &b) const { return a > b ? a : b; }
+};
+
+// plan[0] = slots needed (even, incl. the terminating pair), plan[1] = zero payloads
+__global__ void k_slots_size(const i64 *M, i64 n, unsigned long long *zero, i64 *plan) {
+    const i64 last = (n - 1) + M[n - 1];
+    i64 L = last + 1;
+    if (L < 2 * (n - 1) + 2) L = 2 * (n - 1) + 2;
+    L = (L + 1) & ~(i64)1;
+    plan[0] = L + 2;
+    plan[1] = (i64)*zero;
+}
+
+// slot s: the last entry j with slot_j = j + M_j <= s (slot_j is strictly
+// increasing) -> (key_j, s == slot_j ? payload_j : 0); before entry 0:
+// (key_0, 0); the final pair: (~0, 0)
+__global__ void k_slots_fill(const i64 *M, const u64 *sk, const u64 *sp, i64 n, i64 L, ulonglong2 *slots) {
+    for (i64 s = blockIdx.x * (i64)blockDim.x + threadIdx.x; s < L; s += (i64)gridDim.x * blockDim.x) {
+        if (s >= L - 2) {
+            slots[s] = make_ulonglong2(~0ULL, 0ULL);
+            continue;
+        }
+        i64 lo = 0, hi = n;  // first j with slot_j > s
+        while (lo < hi) {
+            const i64 mid = (lo + hi) >> 1;
+            if (mid + __ldg(reinterpret_cast<const long long *>(M) + mid) <= s) lo = mid + 1;
+            else hi = mid;
+        }
+        const i64 j = lo - 1;
+        if (j < 0) {
+            slots[s] = make_ulonglong2(sk[0], 0ULL);
+        } else {
+            const bool real = j + M[j] == s;
+            slots[s] = make_ulonglong2(sk[j], real ? sp[j] : 0ULL);
+        }
+    }
+}
+
+// ------------------------------------------------------------ windows
+
+// one block per window: the spline points [a0, a0 + npts) and the cells
+__global__ void __launch_bounds__(256) k_hash_windows(SplineDev m, const u64 *lay, int nb, u64 kmin, WinMeta *meta,
+                                                      u16 *cells) {
+    const int w = blockIdx.x;
+    const u64 *B = lay + 4;
+    __shared__ WinMeta s;
+    if (threadIdx.x == 0) {
+        const u64 kfirst = __ldg(reinterpret_cast<const unsigned long long *>(m.keys));
+        const u64 klast = __ldg(reinterpret_cast<const unsigned long long *>(m.keys) + m.K - 1);
+        u64 klo = w == 0 ? kmin : B[w];
+        u64 khi = w + 1 < nb ? (B[w + 1] == 0 ? 0 : B[w + 1] - 1) : klast;
+        if (klo < kfirst) klo = kfirst;
+        if (khi > klast) khi = klast;
+        WinMeta t;
+        t.klo = klo;
+        t.khi = khi;
+        t.ok = (m.K >= 2 && klo <= khi && (w + 1 >= nb || B[w + 1] > klo)) ? 1 : 0;
+        t.a0 = 0;
+        t.npts = 0;
+        t.cshift = 0;
+        if (t.ok) {
+            const i64 lbl = lower_bound_u64(m.keys, m.K, klo);
+            const i64 lbh = lower_bound_u64(m.keys, m.K, khi);
+            i64 a = lbl - 1 < 0 ? 0 : lbl - 1;
+            const i64 b = lbh < 1 ? 1 : (lbh > m.K - 1 ? m.K - 1 : lbh);
+            a &= ~(i64)1;
+            t.a0 = (int)a;
+            t.npts = (int)(b - a + 1);
+            if (t.npts > HS_CAP || m.K >= ((i64)1 << 31)) t.ok = 0;
+            int sh = 0;
+            while (sh < 63 && ((khi - klo) >> sh) >= (u64)HS_NC) ++sh;
+            t.cshift = sh;
+        }
+        s = t;
+        meta[w] = t;
+    }
+    __syncthreads();
+    if (!s.ok) return;
+    u16 *cw = cells + (size_t)w * (HS_NC + 8);
+    for (int c = threadIdx.x; c <= HS_NC; c += blockDim.x) {
+        const u64 off = (u64)c << s.cshift;
+        const bool past = (s.cshift > 0 && (u64)c > ((s.khi - s.klo) >> s.cshift)) || off > s.khi - s.klo;
+        const u64 L = past ? s.khi : s.klo + off;
+        i64 i = lower_bound_u64(m.keys, m.K, L) - s.a0;
+        if (past) i = s.npts - 1;
+        cw[c] = (u16)(i < 0 ? 0 : (i > s.npts - 1 ? s.npts - 1 : i));
+    }
+}
+
+// ------------------------------------------------------------ probe
+
+struct StagedSpline {
+    const u64 *sk;
+    const double *sr;
+    const u16 *cells;
+    u64 klo, khi;
+    int a0, npts, cshift;
+    i64 K, n;
+    // models.py:221-248 for k in [klo, khi]: the lower bound over the
+    // staged points (the cell bounds it), then the reference's operations
+    __device__ __forceinline__ i64 pos(u64 k) const {
+        const int c = (int)((k - klo) >> cshift);
+        int lo = cells[c], hi = cells[c + 1];
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (sk[mid] < k) lo = mid + 1;
+            else hi = mid;
+        }
+        i64 j = (i64)a0 + lo;
+        j = j < 1 ? 1 : (j > K - 1 ? K - 1 : j);
+        const int li = (int)(j - a0);
+        const double x0 = u64_to_f64(sk[li - 1]), x1 = u64_to_f64(sk[li]);
+        const double kf = u64_to_f64(k);
+        const double d = __dsub_rn(x1, x0);
+        const double t = clip_f64(__ddiv_rn(__dsub_rn(kf, x0), d > 1.0 ? d : 1.0), 0.0, 1.0);
+        const double r0 = sr[li - 1], r1 = sr[li];
+        const i64 p = f64_to_i64(rint(__dadd_rn(r0, __dmul_rn(t, __dsub_rn(r1, r0)))));
+        return clip_i64(p, 0, n - 1);
+    }
+};
+
+struct Acc3 {
+    u64 c, s, x;
+};
+
+// the slot scan from 2*pos (see the header): 32-B pairs, keys < k skipped,
+// keys == k with a nonzero payload counted, stop at the first key > k
+__device__ __forceinline__ void slot_scan(const ulonglong2 *__restrict__ slots, i64 pos, u64 k, u64 ps, Acc3 &a) {
+    const ulonglong2 *p = slots + 2 * pos;
+    for (;;) {
+        const ulonglong2 e0 = __ldg(p), e1 = __ldg(p + 1);
+        if (e0.x > k) return;
+        if (e0.x == k && e0.y) {
+            const u64 v = e0.y + ps;
+            ++a.c;
+            a.s += v;
+            a.x ^= v;
+        }
+        if (e1.x > k) return;
+        if (e1.x == k && e1.y) {
+            const u64 v = e1.y + ps;
+            ++a.c;
+            a.s += v;
+            a.x ^= v;
+        }
+        p += 2;
+    }
+}
+
+__global__ void __launch_bounds__(HS_NT, 2) k_hash_probe_staged(SplineDev m, const ulonglong2 *__restrict__ slots,
+                                                                const ulonglong2 *__restrict__ rec,
+                                                                const i64 *__restrict__ reg, int nb,
+                                                                const WinMeta *__restrict__ meta,
+                                                                const u16 *__restrict__ cells_g,
+                                                                unsigned long long *ctr, u64 *out) {
+    extern __shared__ __align__(128) unsigned char smem_h[];
+    u64 *sk = reinterpret_cast<u64 *>(smem_h);
+    double *sr = reinterpret_cast<double *>(smem_h + (size_t)HS_CAP * 8);
+    u16 *cells = reinterpret_cast<u16 *>(smem_h + (size_t)HS_CAP * 16);
+    int *ip = reinterpret_cast<int *>(smem_h + (size_t)HS_CAP * 16 + (HS_NC + 8) * 2);  // [nb + 2] piece prefix
+    __shared__ int s_item, s_tot;
+    __shared__ WinMeta s_m;
+    __shared__ int s_wsum[HS_NT / 32];
+    __shared__ __align__(8) uint64_t bar;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const i64 *rend = reg + nb + 1;
+    // pieces per window, exclusive prefix (4 windows per thread, nb <= 2048)
+    {
+        int v[4], tot = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int w = tid * 4 + q;
+            v[q] = w < nb ? (int)((rend[w] - reg[w] + HS_PIECE - 1) / HS_PIECE) : 0;
+            tot += v[q];
+        }
+        int inc = tot;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += y;
+        }
+        if (lane == 31) s_wsum[warp] = inc;
+        __syncthreads();
+        if (warp == 0) {
+            const int x = lane < HS_NT / 32 ? s_wsum[lane] : 0;
+            int xi = x;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, xi, d);
+                if (lane >= d) xi += y;
+            }
+            if (lane < HS_NT / 32) s_wsum[lane] = xi - x;
+        }
+        __syncthreads();
+        int run = s_wsum[warp] + inc - tot;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int w = tid * 4 + q;
+            if (w < nb) ip[w] = run;
+            run += v[q];
+        }
+        if (tid * 4 + 3 >= nb - 1 && tid * 4 <= nb - 1) {
+            // the thread holding window nb-1 writes the total and the overflow pieces
+            const i64 ovf = reg[2 * nb + 1];
+            ip[nb] = run;
+            s_tot = run + (int)((ovf + HS_PIECE - 1) / HS_PIECE);
+        }
+    }
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        mbar_init_fence();
+    }
+    __syncthreads();
+    const int total = s_tot;
+    unsigned phase = 0;
+    int cur = -1;
+    StagedSpline ss;
+    ss.sk = sk;
+    ss.sr = sr;
+    ss.cells = cells;
+    ss.K = m.K;
+    ss.n = m.n;
+    bool staged = false;
+    Acc3 acc = {0, 0, 0};
+    for (;;) {
+        if (tid == 0) s_item = (int)atomicAdd(ctr, 1ULL);
+        __syncthreads();
+        const int item = s_item;
+        if (item >= total) break;
+        int w;
+        i64 lo, hi;
+        if (item >= ip[nb]) {  // overflow area: any window
+            w = nb;
+            lo = reg[nb] + (i64)(item - ip[nb]) * HS_PIECE;
+            hi = min(lo + HS_PIECE, reg[nb] + reg[2 * nb + 1]);
+        } else {
+            int a = 0, b = nb - 1;  // last window with ip[w] <= item
+            while (a < b) {
+                const int mid = (a + b + 1) >> 1;
+                if (ip[mid] <= item) a = mid;
+                else b = mid - 1;
+            }
+            w = a;
+            lo = reg[w] + (i64)(item - ip[w]) * HS_PIECE;
+            hi = min(lo + HS_PIECE, rend[w]);
+        }
+        if (w != cur) {
+            cur = w;
+            staged = false;
+            if (w < nb) {
+                if (tid == 0) s_m = meta[w];
+                __syncthreads();
+                if (s_m.ok) {
+                    if (tid == 0) {
+                        const unsigned nbk = ((unsigned)s_m.npts * 8u + 15u) & ~15u;
+                        const unsigned nbc = (unsigned)(HS_NC + 8) * 2u;
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        mbar_arrive_expect_tx(&bar, 2 * nbk + nbc);
+                        bulk_g2s(sk, m.keys + s_m.a0, nbk, &bar);
+                        bulk_g2s(sr, m.ranks + s_m.a0, nbk, &bar);
+                        bulk_g2s(cells, cells_g + (size_t)w * (HS_NC + 8), nbc, &bar);
+                    }
+                    mbar_wait(&bar, phase);
+                    phase ^= 1u;
+                    staged = true;
+                    ss.klo = s_m.klo;
+                    ss.khi = s_m.khi;
+                    ss.a0 = s_m.a0;
+                    ss.npts = s_m.npts;
+                    ss.cshift = s_m.cshift;
+                }
+            }
+        }
+        for (i64 t0 = lo + tid; t0 < hi; t0 += (i64)HS_NT * HS_U) {
+            u64 k[HS_U], ps[HS_U];
+            i64 pos[HS_U];
+#pragma unroll
+            for (int u = 0; u < HS_U; ++u) {
+                const i64 t = t0 + (i64)u * HS_NT;
+                if (t < hi) {
+                    const ulonglong2 r = __ldcs(rec + t);
+                    k[u] = r.x;
+                    ps[u] = r.y;
+                } else {
+                    k[u] = ~0ULL;
+                    ps[u] = 0;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < HS_U; ++u) {
+                if (k[u] == ~0ULL) {
+                    pos[u] = -1;  // past the piece / a gap record
+                } else if (staged && k[u] >= ss.klo && k[u] <= ss.khi) {
+                    pos[u] = ss.pos(k[u]);
+                } else {
+                    pos[u] = m.pos(k[u]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < HS_U; ++u)
+                if (pos[u] >= 0) slot_scan(slots, pos[u], k[u], ps[u], acc);
+        }
+        __syncthreads();  // every thread is done with the staged window before a restage
+    }
+    reduce_checksum(acc.c, acc.s, acc.x, 0, out);
+}
+
+}  // namespace lj
+
+using namespace lj;
+
+extern "C" {
+
+size_t lj_spline_slots_workspace_bytes(int64_t n) {
+    size_t t = 0;
+    cub::DeviceScan::InclusiveScan((void *)nullptr, t, (const i64 *)nullptr, (i64 *)nullptr, MaxI64(), (int64_t)n);
+    return part_align_c(sizeof(i64) * (size_t)(n > 0 ? n : 1)) * 2 + part_align_c(t) + 256;
+}
+
+int lj_spline_slots_plan(const LjSpline *model, const uint64_t *sorted_keys, const uint64_t *sorted_pay, int64_t n,
+                         int64_t *plan, void *ws, size_t ws_bytes, void *stream) {
+    LJ_REQUIRE(model && model->npts >= 1 && model->n == n && n >= 1, "model is not fitted on these keys");
+    LJ_REQUIRE(ws_bytes >= lj_spline_slots_workspace_bytes(n), "workspace too small");
+    cudaStream_t st = as_stream(stream);
+    char *q = (char *)ws;
+    i64 *t = (i64 *)q;
+    q += part_align_c(sizeof(i64) * (size_t)n);
+    i64 *M = (i64 *)q;
+    q += part_align_c(sizeof(i64) * (size_t)n);
+    unsigned long long *zero = (unsigned long long *)q;
+    q += 256;
+    LJ_CK(cudaMemsetAsync(zero, 0, sizeof(unsigned long long), st));
+    k_slots_t<<<grid_for(n, 256, 8), 256, 0, st>>>(SplineDev(*model), sorted_keys, sorted_pay, n, t, zero);
+    LJ_CK_LAUNCH();
+    size_t tb = 0;
+    cub::DeviceScan::InclusiveScan(nullptr, tb, t, M, MaxI64(), (int64_t)n);
+    LJ_CK(cub::DeviceScan::InclusiveScan(q, tb, t, M, MaxI64(), (int64_t)n, st));
+    k_slots_size<<<1, 1, 0, st>>>(M, n, zero, plan);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+int lj_spline_slots_fill(const uint64_t *sorted_keys, const uint64_t *sorted_pay, int64_t n, uint64_t *slots,
+                         int64_t nslots, void *ws, size_t ws_bytes, void *stream) {
+    LJ_REQUIRE(n >= 1 && nslots >= 2 * n, "need n >= 1 and the planned slot count");
+    LJ_REQUIRE(ws_bytes >= lj_spline_slots_workspace_bytes(n), "workspace too small");
+    const i64 *M = (const i64 *)((char *)ws + part_align_c(sizeof(i64) * (size_t)n));
+    k_slots_fill<<<grid_for(nslots, 256, 16), 256, 0, as_stream(stream)>>>(
+        M, sorted_keys, sorted_pay, n, nslots, reinterpret_cast<ulonglong2 *>(slots));
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+}  // extern "C"
+
+namespace lj {
+
+size_t hash_staged_meta_bytes(int nb) { return hs_meta_bytes(nb); }
+
+// window metadata for the key-range windows in `lay` (lj_keybin layout)
+int hash_windows(const LjSpline &model, const u64 *lay, int nb, u64 kmin, void *meta_ws, cudaStream_t st) {
+    WinMeta *meta = reinterpret_cast<WinMeta *>(meta_ws);
+    u16 *cells = reinterpret_cast<u16 *>((char *)meta_ws + (((size_t)nb * sizeof(WinMeta) + 255) & ~(size_t)255));
+    k_hash_windows<<<nb, 256, 0, st>>>(SplineDev(model), lay, nb, kmin, meta, cells);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+int hash_probe_staged(const LjSplineHash &idx, const ulonglong2 *rec, const i64 *reg, int nb, const void *meta_ws,
+                      unsigned long long *ctr, u64 *out, cudaStream_t st) {
+    if (nb > HS_MAXWIN) {
+        set_error("hash_probe_staged: at most 2048 windows");
+        return LJ_E_INVALID;
+    }
+    const WinMeta *meta = reinterpret_cast<const WinMeta *>(meta_ws);
+    const u16 *cells =
+        reinterpret_cast<const u16 *>((const char *)meta_ws + (((size_t)nb * sizeof(WinMeta) + 255) & ~(size_t)255));
+    const size_t sm = (size_t)HS_CAP * 16 + (HS_NC + 8) * 2 + (size_t)(HS_MAXWIN + 2) * 4;
+    static bool attr = false;
+    if (!attr) {
+        LJ_CK(cudaFuncSetAttribute(k_hash_probe_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        attr = true;
+    }
+    LJ_CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
+    k_hash_probe_staged<<<2 * sm_count(), HS_NT, sm, st>>>(SplineDev(idx.model),
+                                                           reinterpret_cast<const ulonglong2 *>(idx.slots), rec, reg,
+                                                           nb, meta, cells, ctr, out);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
+}  // namespace lj

@@ -18,6 +18,12 @@
 
 namespace lj {
 
+// lj_hash_staged.cu
+size_t hash_staged_meta_bytes(int nb);
+int hash_windows(const LjSpline &model, const u64 *lay, int nb, u64 kmin, void *meta_ws, cudaStream_t st);
+int hash_probe_staged(const LjSplineHash &idx, const ulonglong2 *rec, const i64 *reg, int nb, const void *meta_ws,
+                      unsigned long long *ctr, u64 *out, cudaStream_t st);
+
 struct HashDev {
     SplineDev model;
     i64 n, P, stride;
@@ -381,7 +387,7 @@ struct PosBin : NoTable {
 
 static int hash_bins(i64 n) {
     const char *e = getenv("LJ_HASH_BINS");  // diagnostic: window count of the grouping
-    const int want = e ? atoi(e) : 2048;
+    const int want = e ? atoi(e) : 512;
     const int nb = want < 1 ? 1 : (want > 2048 ? 2048 : want);
     return (int)(n < nb ? (n < 1 ? 1 : n) : nb);
 }
@@ -456,7 +462,7 @@ size_t lj_spline_hash_bucket_est_workspace_bytes(const LjSplineHash *idx, int64_
     if (!idx) return 0;
     const int nb = hash_bins(idx->model.n);
     return est_workspace_bytes(nb) + part_align(sizeof(u16) * (size_t)(nk < 0 ? 0 : nk)) + win_tables_bytes(idx->model) +
-           kb_bytes(nb) + 256;
+           kb_bytes(nb) + 256 + part_align(hash_staged_meta_bytes(nb)) + 256;
 }
 
 // exact regions in lj_leaf_bucket's layout: ends = next starts, no overflow
@@ -479,6 +485,29 @@ int lj_spline_hash_bucket_est(const LjSplineHash *idx, const uint64_t *keys, con
     f.rn = (double)f.nb / (double)idx->model.n;
     SoaSrc<PosBin> src{keys, pay, f};
     static const bool keybin = getenv("LJ_HASH_KEYBIN") != nullptr;
+    static const bool nostage = getenv("LJ_HASH_NOSTAGE") != nullptr;
+    if (idx->slots && !nostage) {
+        // the staged probe's grouping: equi-depth KEY windows over the build
+        // side (lj_keybin.cuh, evaluated in shared memory) + every window's
+        // staging metadata for k_hash_probe_staged
+        const int nb = (int)f.nb;
+        const size_t eb = est_workspace_bytes(nb);
+        LJ_REQUIRE(ws_bytes >= eb + kb_bytes(nb) + 512 + hash_staged_meta_bytes(nb), "workspace too small");
+        u64 *lay = reinterpret_cast<u64 *>(((uintptr_t)ws + eb + 255) & ~(uintptr_t)255);
+        void *meta = reinterpret_cast<void *>(((uintptr_t)lay + kb_bytes(nb) + 255) & ~(uintptr_t)255);
+        k_hash_window_bounds<<<(nb + 255) / 256, 256, 0, st>>>(idx->entries, idx->n, nb, lay);
+        k_keybin_build<<<1, 1024, 0, st>>>(lay, nb);
+        LJ_CK_LAUNCH();
+        KeyRangeBin kb;
+        kb.g = lay;
+        kb.nb = nb;
+        SoaSrc<KeyRangeBin> ksrc{keys, pay, kb};
+        int rc = run_partition_est(ksrc, nk, nb, reinterpret_cast<ulonglong2 *>(pairs_out), reg_out, ws, eb, st);
+        if (rc) return rc;
+        k_fill_gaps<<<(unsigned)nb, 256, 0, st>>>(reg_out, nb, reinterpret_cast<ulonglong2 *>(pairs_out));
+        LJ_CK_LAUNCH();
+        return hash_windows(idx->model, lay, nb, 0, meta, st);
+    }
     if (keybin) {
         // equi-depth KEY windows over the build side, evaluated in shared
         // memory (lj_keybin.cuh): no per-tuple global load
@@ -565,8 +594,19 @@ int lj_spline_hash_probe_regions(const LjSplineHash *idx, const uint64_t *s_pair
     // measured at C3 (ms): U=4 x 3 CTAs/SM 37.5, U=4 x 4 32.4, U=2 x 6 30.0, U=8 38.4
     static const int per_sm = getenv("LJ_HASH_CTAS") ? atoi(getenv("LJ_HASH_CTAS")) : 6;
     static const int u = getenv("LJ_HASH_U") ? atoi(getenv("LJ_HASH_U")) : 2;
-    const HashDev hd(*idx);
     const ulonglong2 *rec = reinterpret_cast<const ulonglong2 *>(s_pairs);
+    static const bool nostage = getenv("LJ_HASH_NOSTAGE") != nullptr;
+    if (idx->slots && !nostage) {
+        // k_hash_probe_staged over the windows lj_spline_hash_bucket_est
+        // left (its staging metadata sits behind the key-range bin layout)
+        const int nb = (int)nbins;
+        const size_t eb = est_workspace_bytes(nb);
+        LJ_REQUIRE(ws_bytes >= eb + kb_bytes(nb) + 512 + hash_staged_meta_bytes(nb), "workspace too small");
+        const uintptr_t lay = ((uintptr_t)ws + eb + 255) & ~(uintptr_t)255;
+        const void *meta = reinterpret_cast<const void *>((lay + kb_bytes(nb) + 255) & ~(uintptr_t)255);
+        return hash_probe_staged(*idx, rec, reg, nb, meta, ctr, out, st);
+    }
+    const HashDev hd(*idx);
     if (u == 2)
         k_hash_probe_chunks<NT, 2, 16><<<sm_count() * per_sm, NT, 0, st>>>(hd, rec, reg, (int)nbins, ctr, out);
     else if (u == 8)

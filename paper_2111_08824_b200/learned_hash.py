@@ -58,6 +58,7 @@ class SplineHashIndex:
         dev = relation.device
         self.entries = torch.empty(2 * max(n, 1), dtype=torch.int64, device=dev)
         self.starts = torch.zeros(P // self.stride + 1, dtype=torch.int32, device=dev)
+        self.slots, self.nslots = None, 0
         if n == 0:
             return self
         lib = _lib.lib()
@@ -66,11 +67,43 @@ class SplineHashIndex:
         _lib.check(lib.lj_spline_hash_build(ctypes.byref(c), _lib.ptr(relation.keys), _lib.ptr(relation.payloads),
                                             n, P, _lib.ptr(self.entries), _lib.ptr(self.starts), _lib.ptr(ws),
                                             ws.numel(), _lib.stream_ptr()), "spline_hash_build")
+        del ws
+        self._build_slots(relation)
         return self
 
+    build_slots = True  # class switch: the probe table never changes a result
+
+    def _build_slots(self, relation: Relation) -> None:
+        """The probe table (LjSplineHash.slots, lj_hash_staged.cu): the
+        entries in key order at slot max(2 pos, previous + 1), gaps marked by
+        payload 0 -- built only when every payload is nonzero (else the
+        chains are probed)."""
+        self.slots = None
+        self.nslots = 0
+        if not self.build_slots or self.model.trained_len != self.n:
+            return
+        lib = _lib.lib()
+        dev = relation.device
+        sk, sp = sort_pairs(relation.keys, relation.payloads)
+        ws = _lib.workspace(lib.lj_spline_slots_workspace_bytes(self.n),
+                            dev)
+        plan = torch.zeros(2, dtype=torch.int64, device=dev)
+        c = self.model.c_struct()
+        _lib.check(lib.lj_spline_slots_plan(ctypes.byref(c), _lib.ptr(sk), _lib.ptr(sp), self.n, _lib.ptr(plan),
+                                            _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "spline_slots_plan")
+        nslots, zeros = (int(v) for v in plan.cpu().tolist())
+        if zeros:
+            return
+        self.slots = torch.empty(2 * nslots, dtype=torch.int64, device=dev)
+        _lib.check(lib.lj_spline_slots_fill(_lib.ptr(sk), _lib.ptr(sp), self.n, _lib.ptr(self.slots), nslots,
+                                            _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "spline_slots_fill")
+        self.nslots = nslots
+
     def c_struct(self) -> _lib.LjSplineHash:
+        slots = getattr(self, "slots", None)
         return _lib.LjSplineHash(self.model.c_struct(), self.n, self.table_len, self.stride,
-                                 _lib.ptr(self.entries), _lib.ptr(self.starts))
+                                 _lib.ptr(self.entries), _lib.ptr(self.starts), _lib.ptr(slots),
+                                 getattr(self, "nslots", 0))
 
     @property
     def _keys(self) -> np.ndarray:

@@ -238,8 +238,11 @@ class RadixSplineIndex:
         self.radix_table = np.ascontiguousarray(radix_table, dtype=np.int64)
         self.shift = np.uint64(shift)
         self.trained_len = int(trained_len)
-        self._d_keys = to_device_u64(self.spline_keys, device=dev)
-        self._d_ranks = torch.from_numpy(self.spline_ranks.astype(np.float64)).to(dev)
+        # two words of padding: the staged probe bulk-copies whole 16-B words
+        K = self.spline_keys.size
+        self._d_keys = to_device_u64(np.concatenate([self.spline_keys, np.zeros(2, np.uint64)]), device=dev)[:K]
+        self._d_ranks = torch.from_numpy(np.concatenate([self.spline_ranks.astype(np.float64),
+                                                         np.zeros(2)])).to(dev)[:K]
         self._d_radix = torch.from_numpy(self.radix_table.astype(np.uint32).view(np.int32)).to(dev)
         self._build_aux(dev)
         self.tag = uuid.uuid4().hex

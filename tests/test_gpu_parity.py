@@ -708,3 +708,46 @@ def test_host_resident_entry_points_on_empty_inputs(lj):
     assert lj.join_checksum_host(idx, e, e).cpu().tolist() == [0, 0, 0, 0]
     res = lj.lsj_join_host(r.keys.cpu(), r.payloads.cpu(), e, e)
     assert res.checksum == (0, 0, 0)
+
+
+def _dup_probe_sets():
+    rng = np.random.default_rng(31)
+    base = np.unique(rng.integers(0, 2**40, 50000, dtype=np.uint64))
+    dup = np.concatenate([base, base[::7], base[::7], base[::101]])  # equal build keys: adjacent real slots
+    clus = np.unique(np.concatenate([rng.normal(c, 2**24, 20000) for c in (2**50, 2**51, 3 * 2**52)]).astype(np.uint64))
+    high = np.unique(rng.integers(2**63, 2**64 - 1, 30000, dtype=np.uint64))  # keys >= 2^63
+    return {"dup": dup, "clusters": clus, "high": high, "tiny1": np.array([5], np.uint64),
+            "tiny3": np.array([9, 9, 2**62], np.uint64)}
+
+
+@pytest.mark.parametrize("name", ["dup", "clusters", "high", "tiny1", "tiny3"])
+def test_spline_hash_probe_table_equals_chains(lj, name):
+    """The staged probe over the slot table (k_hash_probe_staged) against
+    the chain probe (K5) and the oracle: duplicate build keys, clustered
+    keys, keys >= 2^63, probes below / above / between the build keys."""
+    rk = _dup_probe_sets()[name]
+    rng = np.random.default_rng(5)
+    sk = np.concatenate([rng.choice(rk, 200000), rng.integers(0, 2**64 - 1, 20000, dtype=np.uint64),
+                         np.array([0, rk.min(), rk.max(), 2**64 - 2], np.uint64)])
+    sk = rng.permutation(sk)
+    r = lj.make_relation(rng.permutation(rk), 3)
+    s = lj.make_relation(sk, 4)
+    idx = lj.SplineHashIndex(32, 18, 4.0).fit(r)
+    assert idx.slots is not None
+    want = oracle.smj_checksum(*r.numpy(), *s.numpy())
+    direct = idx.join_checksum(s.keys, s.payloads).cpu().tolist()
+    grouped = idx.join_checksum_buffered(s.keys, s.payloads).cpu().tolist()
+    assert (direct[0], direct[1] & MASK, direct[2] & MASK) == want
+    assert (grouped[0], grouped[1] & MASK, grouped[2] & MASK) == want
+
+
+def test_spline_hash_zero_payloads_keep_the_chains(lj):
+    rk = np.unique(np.random.default_rng(2).integers(0, 2**50, 40000, dtype=np.uint64))
+    rp = np.arange(rk.size, dtype=np.uint64)  # payload 0 once: no gap marker, no slot table
+    r = lj.Relation(rk, rp)
+    s = lj.make_relation(np.concatenate([rk, rk[:1000]]), 8)
+    idx = lj.SplineHashIndex(32, 18, 4.0).fit(r)
+    assert idx.slots is None
+    want = oracle.smj_checksum(*r.numpy(), *s.numpy())
+    g = idx.join_checksum_buffered(s.keys, s.payloads).cpu().tolist()
+    assert (g[0], g[1] & MASK, g[2] & MASK) == want
