@@ -47,10 +47,12 @@ namespace lj {
 static inline size_t part_align_c(size_t v) { return (v + 255) & ~(size_t)255; }
 
 constexpr int HS_NT = 512;
-constexpr int HS_U = 2;
-constexpr int HS_CAP = 4096;   // staged spline points per window
-constexpr int HS_NC = 1024;    // lower-bound cells per window
-constexpr i64 HS_PIECE = 16384;
+constexpr int HS_U = 4;
+constexpr int HS_TT = HS_NT * HS_U;  // records per ring tile (32 KB)
+constexpr int HS_NST = 2;            // ring stages
+constexpr int HS_CAP = 2048;         // staged spline points per window
+constexpr int HS_NC = 1024;          // lower-bound cells per window
+constexpr i64 HS_PIECE = 16384;      // records per work item (8 tiles)
 constexpr int HS_MAXWIN = 2048;
 
 struct WinMeta {
@@ -208,31 +210,36 @@ struct StagedSpline {
 
 struct Acc3 {
     u64 c, s, x;
+    __device__ __forceinline__ void add(u64 pr, u64 ps) {
+        const u64 v = pr + ps;
+        ++c;
+        s += v;
+        x ^= v;
+    }
 };
 
-// the slot scan from 2*pos (see the header): 32-B pairs, keys < k skipped,
-// keys == k with a nonzero payload counted, stop at the first key > k
-__device__ __forceinline__ void slot_scan(const ulonglong2 *__restrict__ slots, i64 pos, u64 k, u64 ps, Acc3 &a) {
-    const ulonglong2 *p = slots + 2 * pos;
-    for (;;) {
+// the rest of a slot scan whose first pair did not decide it: pairs from
+// slot 2*pos + 2 on, keys < k skipped, keys == k with a nonzero payload
+// counted, stop at the first key > k
+__device__ __noinline__ void slot_scan_tail(const ulonglong2 *__restrict__ p, u64 k, u64 ps, Acc3 &a) {
+    for (;; p += 2) {
         const ulonglong2 e0 = __ldg(p), e1 = __ldg(p + 1);
         if (e0.x > k) return;
-        if (e0.x == k && e0.y) {
-            const u64 v = e0.y + ps;
-            ++a.c;
-            a.s += v;
-            a.x ^= v;
-        }
+        if (e0.x == k && e0.y) a.add(e0.y, ps);
         if (e1.x > k) return;
-        if (e1.x == k && e1.y) {
-            const u64 v = e1.y + ps;
-            ++a.c;
-            a.s += v;
-            a.x ^= v;
-        }
-        p += 2;
+        if (e1.x == k && e1.y) a.add(e1.y, ps);
     }
 }
+
+// record tiles of the probe's ring: HS_TT records each, with their window
+struct TileMeta {
+    i64 lo;
+    int w, cnt;
+};
+
+// global (unstaged) evaluation, kept out of line: the overflow area and
+// windows whose points exceed the staging capacity
+__device__ __noinline__ i64 spline_pos_global(const SplineDev &m, u64 k) { return m.pos(k); }
 
 __global__ void __launch_bounds__(HS_NT, 2) k_hash_probe_staged(SplineDev m, const ulonglong2 *__restrict__ slots,
                                                                 const ulonglong2 *__restrict__ rec,
@@ -241,14 +248,16 @@ __global__ void __launch_bounds__(HS_NT, 2) k_hash_probe_staged(SplineDev m, con
                                                                 const u16 *__restrict__ cells_g,
                                                                 unsigned long long *ctr, u64 *out) {
     extern __shared__ __align__(128) unsigned char smem_h[];
-    u64 *sk = reinterpret_cast<u64 *>(smem_h);
-    double *sr = reinterpret_cast<double *>(smem_h + (size_t)HS_CAP * 8);
-    u16 *cells = reinterpret_cast<u16 *>(smem_h + (size_t)HS_CAP * 16);
-    int *ip = reinterpret_cast<int *>(smem_h + (size_t)HS_CAP * 16 + (HS_NC + 8) * 2);  // [nb + 2] piece prefix
-    __shared__ int s_item, s_tot;
+    ulonglong2 *ring = reinterpret_cast<ulonglong2 *>(smem_h);                        // [HS_NST][HS_TT]
+    u64 *sk = reinterpret_cast<u64 *>(smem_h + (size_t)HS_NST * HS_TT * 16);
+    double *sr = reinterpret_cast<double *>(reinterpret_cast<unsigned char *>(sk) + (size_t)HS_CAP * 8);
+    u16 *cells = reinterpret_cast<u16 *>(reinterpret_cast<unsigned char *>(sr) + (size_t)HS_CAP * 8);
+    int *ip = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(cells) + (HS_NC + 8) * 2);  // [nb + 1]
+    __shared__ TileMeta tm[HS_NST];
+    __shared__ int s_tot;
     __shared__ WinMeta s_m;
     __shared__ int s_wsum[HS_NT / 32];
-    __shared__ __align__(8) uint64_t bar;
+    __shared__ __align__(8) uint64_t full[HS_NST], sbar;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const i64 *rend = reg + nb + 1;
     // pieces per window, exclusive prefix (4 windows per thread, nb <= 2048)
@@ -286,52 +295,77 @@ __global__ void __launch_bounds__(HS_NT, 2) k_hash_probe_staged(SplineDev m, con
             if (w < nb) ip[w] = run;
             run += v[q];
         }
-        if (tid * 4 + 3 >= nb - 1 && tid * 4 <= nb - 1) {
-            // the thread holding window nb-1 writes the total and the overflow pieces
-            const i64 ovf = reg[2 * nb + 1];
+        if (tid * 4 <= nb - 1 && nb - 1 <= tid * 4 + 3) {
             ip[nb] = run;
-            s_tot = run + (int)((ovf + HS_PIECE - 1) / HS_PIECE);
+            s_tot = run + (int)((reg[2 * nb + 1] + HS_PIECE - 1) / HS_PIECE);
         }
     }
+    // producer state (thread 0 only): the current work item's remaining records
+    int p_w = -1;
+    i64 p_lo = 0, p_hi = 0;
+    bool p_done = false;
+    auto issue = [&](int s) {  // thread 0: the next tile into stage s
+        while (!p_done && p_lo >= p_hi) {
+            const int item = (int)atomicAdd(ctr, 1ULL);
+            if (item >= s_tot) {
+                p_done = true;
+                break;
+            }
+            if (item >= ip[nb]) {  // overflow area: any window
+                p_w = nb;
+                p_lo = reg[nb] + (i64)(item - ip[nb]) * HS_PIECE;
+                p_hi = min(p_lo + HS_PIECE, reg[nb] + reg[2 * nb + 1]);
+            } else {
+                int a = 0, b = nb - 1;  // last window with ip[w] <= item
+                while (a < b) {
+                    const int mid = (a + b + 1) >> 1;
+                    if (ip[mid] <= item) a = mid;
+                    else b = mid - 1;
+                }
+                p_w = a;
+                p_lo = reg[a] + (i64)(item - ip[a]) * HS_PIECE;
+                p_hi = min(p_lo + HS_PIECE, rend[a]);
+            }
+        }
+        if (p_done) {
+            tm[s].w = -1;
+            tm[s].cnt = 0;
+            mbar_arrive(&full[s]);
+            return;
+        }
+        const int cnt = (int)min((i64)HS_TT, p_hi - p_lo);
+        tm[s].w = p_w;
+        tm[s].lo = p_lo;
+        tm[s].cnt = cnt;
+        mbar_arrive_expect_tx(&full[s], (unsigned)cnt * 16u);
+        bulk_g2s(ring + (size_t)s * HS_TT, rec + p_lo, (unsigned)cnt * 16u, &full[s]);
+        p_lo += cnt;
+    };
     if (tid == 0) {
-        mbar_init(&bar, 1);
+        for (int s = 0; s < HS_NST; ++s) mbar_init(&full[s], 1);
+        mbar_init(&sbar, 1);
         mbar_init_fence();
     }
     __syncthreads();
-    const int total = s_tot;
-    unsigned phase = 0;
+    if (tid == 0)
+        for (int s = 0; s < HS_NST - 1; ++s) issue(s);
+    unsigned sphase = 0;
     int cur = -1;
+    bool staged = false;
     StagedSpline ss;
     ss.sk = sk;
     ss.sr = sr;
     ss.cells = cells;
     ss.K = m.K;
     ss.n = m.n;
-    bool staged = false;
     Acc3 acc = {0, 0, 0};
-    for (;;) {
-        if (tid == 0) s_item = (int)atomicAdd(ctr, 1ULL);
-        __syncthreads();
-        const int item = s_item;
-        if (item >= total) break;
-        int w;
-        i64 lo, hi;
-        if (item >= ip[nb]) {  // overflow area: any window
-            w = nb;
-            lo = reg[nb] + (i64)(item - ip[nb]) * HS_PIECE;
-            hi = min(lo + HS_PIECE, reg[nb] + reg[2 * nb + 1]);
-        } else {
-            int a = 0, b = nb - 1;  // last window with ip[w] <= item
-            while (a < b) {
-                const int mid = (a + b + 1) >> 1;
-                if (ip[mid] <= item) a = mid;
-                else b = mid - 1;
-            }
-            w = a;
-            lo = reg[w] + (i64)(item - ip[w]) * HS_PIECE;
-            hi = min(lo + HS_PIECE, rend[w]);
-        }
+    for (int t = 0;; ++t) {
+        const int s = t % HS_NST;
+        mbar_wait(&full[s], (unsigned)(t / HS_NST) & 1u);
+        const int w = tm[s].w, cnt = tm[s].cnt;
+        if (cnt == 0) break;  // the producer ran out of work (every thread sees the same)
         if (w != cur) {
+            // restage: every thread is past the previous tile (barrier below)
             cur = w;
             staged = false;
             if (w < nb) {
@@ -342,13 +376,13 @@ __global__ void __launch_bounds__(HS_NT, 2) k_hash_probe_staged(SplineDev m, con
                         const unsigned nbk = ((unsigned)s_m.npts * 8u + 15u) & ~15u;
                         const unsigned nbc = (unsigned)(HS_NC + 8) * 2u;
                         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                        mbar_arrive_expect_tx(&bar, 2 * nbk + nbc);
-                        bulk_g2s(sk, m.keys + s_m.a0, nbk, &bar);
-                        bulk_g2s(sr, m.ranks + s_m.a0, nbk, &bar);
-                        bulk_g2s(cells, cells_g + (size_t)w * (HS_NC + 8), nbc, &bar);
+                        mbar_arrive_expect_tx(&sbar, 2 * nbk + nbc);
+                        bulk_g2s(sk, m.keys + s_m.a0, nbk, &sbar);
+                        bulk_g2s(sr, m.ranks + s_m.a0, nbk, &sbar);
+                        bulk_g2s(cells, cells_g + (size_t)w * (HS_NC + 8), nbc, &sbar);
                     }
-                    mbar_wait(&bar, phase);
-                    phase ^= 1u;
+                    mbar_wait(&sbar, sphase);
+                    sphase ^= 1u;
                     staged = true;
                     ss.klo = s_m.klo;
                     ss.khi = s_m.khi;
@@ -358,36 +392,48 @@ __global__ void __launch_bounds__(HS_NT, 2) k_hash_probe_staged(SplineDev m, con
                 }
             }
         }
-        for (i64 t0 = lo + tid; t0 < hi; t0 += (i64)HS_NT * HS_U) {
-            u64 k[HS_U], ps[HS_U];
-            i64 pos[HS_U];
+        const ulonglong2 *tile = ring + (size_t)s * HS_TT;
+        u64 k[HS_U], ps[HS_U];
+        i64 pos[HS_U];
 #pragma unroll
-            for (int u = 0; u < HS_U; ++u) {
-                const i64 t = t0 + (i64)u * HS_NT;
-                if (t < hi) {
-                    const ulonglong2 r = __ldcs(rec + t);
-                    k[u] = r.x;
-                    ps[u] = r.y;
-                } else {
-                    k[u] = ~0ULL;
-                    ps[u] = 0;
-                }
+        for (int u = 0; u < HS_U; ++u) {
+            const int j = u * HS_NT + tid;
+            if (j < cnt) {
+                const ulonglong2 r = tile[j];
+                k[u] = r.x;
+                ps[u] = r.y;
+            } else {
+                k[u] = ~0ULL;
+                ps[u] = 0;
             }
-#pragma unroll
-            for (int u = 0; u < HS_U; ++u) {
-                if (k[u] == ~0ULL) {
-                    pos[u] = -1;  // past the piece / a gap record
-                } else if (staged && k[u] >= ss.klo && k[u] <= ss.khi) {
-                    pos[u] = ss.pos(k[u]);
-                } else {
-                    pos[u] = m.pos(k[u]);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < HS_U; ++u)
-                if (pos[u] >= 0) slot_scan(slots, pos[u], k[u], ps[u], acc);
         }
-        __syncthreads();  // every thread is done with the staged window before a restage
+#pragma unroll
+        for (int u = 0; u < HS_U; ++u) {
+            if (k[u] == ~0ULL) pos[u] = -1;  // past the tile / a gap record
+            else if (staged && k[u] >= ss.klo && k[u] <= ss.khi) pos[u] = ss.pos(k[u]);
+            else pos[u] = spline_pos_global(m, k[u]);
+        }
+        // every probe's first slot pair in flight at once
+        ulonglong2 e0[HS_U], e1[HS_U];
+#pragma unroll
+        for (int u = 0; u < HS_U; ++u) {
+            if (pos[u] >= 0) {
+                e0[u] = __ldg(slots + 2 * pos[u]);
+                e1[u] = __ldg(slots + 2 * pos[u] + 1);
+            } else {
+                e0[u] = e1[u] = make_ulonglong2(~0ULL, 0ULL);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < HS_U; ++u) {
+            if (pos[u] < 0 || e0[u].x > k[u]) continue;
+            if (e0[u].x == k[u] && e0[u].y) acc.add(e0[u].y, ps[u]);
+            if (e1[u].x > k[u]) continue;
+            if (e1[u].x == k[u] && e1[u].y) acc.add(e1[u].y, ps[u]);
+            slot_scan_tail(slots + 2 * pos[u] + 2, k[u], ps[u], acc);
+        }
+        __syncthreads();  // every thread is done with stage s (and the staged window)
+        if (tid == 0) issue((t + HS_NST - 1) % HS_NST);
     }
     reduce_checksum(acc.c, acc.s, acc.x, 0, out);
 }
@@ -462,7 +508,7 @@ int hash_probe_staged(const LjSplineHash &idx, const ulonglong2 *rec, const i64 
     const WinMeta *meta = reinterpret_cast<const WinMeta *>(meta_ws);
     const u16 *cells =
         reinterpret_cast<const u16 *>((const char *)meta_ws + (((size_t)nb * sizeof(WinMeta) + 255) & ~(size_t)255));
-    const size_t sm = (size_t)HS_CAP * 16 + (HS_NC + 8) * 2 + (size_t)(HS_MAXWIN + 2) * 4;
+    const size_t sm = (size_t)HS_NST * HS_TT * 16 + (size_t)HS_CAP * 16 + (HS_NC + 8) * 2 + (size_t)(nb + 2) * 4;
     static bool attr = false;
     if (!attr) {
         LJ_CK(cudaFuncSetAttribute(k_hash_probe_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
