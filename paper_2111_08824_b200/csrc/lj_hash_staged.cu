@@ -46,11 +46,12 @@ namespace lj {
 
 static inline size_t part_align_c(size_t v) { return (v + 255) & ~(size_t)255; }
 
-constexpr int HS_NT = 512;
+constexpr int HS_NT = 256;
+constexpr int HS_CTAS = 3;           // CTAs per SM
 constexpr int HS_U = 4;
-constexpr int HS_TT = HS_NT * HS_U;  // records per ring tile (32 KB)
-constexpr int HS_NST = 2;            // ring stages
-constexpr int HS_CAP = 2048;         // staged spline points per window
+constexpr int HS_TT = HS_NT * HS_U;  // records per ring tile (16 KB)
+constexpr int HS_NST = 3;            // ring stages
+constexpr int HS_CAP = 1024;         // staged spline points per window
 constexpr int HS_NC = 1024;          // lower-bound cells per window
 constexpr i64 HS_PIECE = 16384;      // records per work item (8 tiles)
 constexpr int HS_MAXWIN = 2048;
@@ -221,7 +222,7 @@ struct Acc3 {
 // the rest of a slot scan whose first pair did not decide it: pairs from
 // slot 2*pos + 2 on, keys < k skipped, keys == k with a nonzero payload
 // counted, stop at the first key > k
-__device__ __noinline__ void slot_scan_tail(const ulonglong2 *__restrict__ p, u64 k, u64 ps, Acc3 &a) {
+__device__ __forceinline__ void slot_scan_tail(const ulonglong2 *__restrict__ p, u64 k, u64 ps, Acc3 &a) {
     for (;; p += 2) {
         const ulonglong2 e0 = __ldg(p), e1 = __ldg(p + 1);
         if (e0.x > k) return;
@@ -239,9 +240,9 @@ struct TileMeta {
 
 // global (unstaged) evaluation, kept out of line: the overflow area and
 // windows whose points exceed the staging capacity
-__device__ __noinline__ i64 spline_pos_global(const SplineDev &m, u64 k) { return m.pos(k); }
+__device__ __forceinline__ i64 spline_pos_global(const SplineDev &m, u64 k) { return m.pos(k); }
 
-__global__ void __launch_bounds__(HS_NT, 2) k_hash_probe_staged(SplineDev m, const ulonglong2 *__restrict__ slots,
+__global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev m, const ulonglong2 *__restrict__ slots,
                                                                 const ulonglong2 *__restrict__ rec,
                                                                 const i64 *__restrict__ reg, int nb,
                                                                 const WinMeta *__restrict__ meta,
@@ -260,12 +261,12 @@ __global__ void __launch_bounds__(HS_NT, 2) k_hash_probe_staged(SplineDev m, con
     __shared__ __align__(8) uint64_t full[HS_NST], sbar;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const i64 *rend = reg + nb + 1;
-    // pieces per window, exclusive prefix (4 windows per thread, nb <= 2048)
+    // pieces per window, exclusive prefix (8 windows per thread, nb <= 2048)
     {
-        int v[4], tot = 0;
+        int v[8], tot = 0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int w = tid * 4 + q;
+        for (int q = 0; q < 8; ++q) {
+            const int w = tid * 8 + q;
             v[q] = w < nb ? (int)((rend[w] - reg[w] + HS_PIECE - 1) / HS_PIECE) : 0;
             tot += v[q];
         }
@@ -290,12 +291,12 @@ __global__ void __launch_bounds__(HS_NT, 2) k_hash_probe_staged(SplineDev m, con
         __syncthreads();
         int run = s_wsum[warp] + inc - tot;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int w = tid * 4 + q;
+        for (int q = 0; q < 8; ++q) {
+            const int w = tid * 8 + q;
             if (w < nb) ip[w] = run;
             run += v[q];
         }
-        if (tid * 4 <= nb - 1 && nb - 1 <= tid * 4 + 3) {
+        if (tid * 8 <= nb - 1 && nb - 1 <= tid * 8 + 7) {
             ip[nb] = run;
             s_tot = run + (int)((reg[2 * nb + 1] + HS_PIECE - 1) / HS_PIECE);
         }
@@ -515,7 +516,7 @@ int hash_probe_staged(const LjSplineHash &idx, const ulonglong2 *rec, const i64 
         attr = true;
     }
     LJ_CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
-    k_hash_probe_staged<<<2 * sm_count(), HS_NT, sm, st>>>(SplineDev(idx.model),
+    k_hash_probe_staged<<<HS_CTAS * sm_count(), HS_NT, sm, st>>>(SplineDev(idx.model),
                                                            reinterpret_cast<const ulonglong2 *>(idx.slots), rec, reg,
                                                            nb, meta, cells, ctr, out);
     LJ_CK_LAUNCH();
