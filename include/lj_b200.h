@@ -121,6 +121,9 @@ typedef struct LjSplineHash {
      * scans forward from slot 2*pos(k) (lj_hash_staged.cu). */
     const uint64_t *slots;
     int64_t nslots;
+    int32_t slots_unique;   /* 1 if no two build keys are equal: the probe
+                               stops at the first match */
+    int32_t _pad;
 } LjSplineHash;
 
 /* ------------------------------------------------------------ library */

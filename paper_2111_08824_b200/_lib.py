@@ -59,7 +59,8 @@ class LjSpline(ctypes.Structure):
 
 class LjSplineHash(ctypes.Structure):
     _fields_ = [("model", LjSpline), ("n", _i64), ("table_len", _i64), ("stride", _i64),
-                ("entries", _c_void_p), ("starts", _c_void_p), ("slots", _c_void_p), ("nslots", _i64)]
+                ("entries", _c_void_p), ("starts", _c_void_p), ("slots", _c_void_p), ("nslots", _i64),
+                ("slots_unique", ctypes.c_int32), ("_pad", ctypes.c_int32)]
 
 
 class LjLsjModel(ctypes.Structure):

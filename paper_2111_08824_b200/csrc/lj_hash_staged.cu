@@ -46,15 +46,16 @@ namespace lj {
 
 static inline size_t part_align_c(size_t v) { return (v + 255) & ~(size_t)255; }
 
-constexpr int HS_NT = 256;
-constexpr int HS_CTAS = 3;           // CTAs per SM
-constexpr int HS_U = 4;
-constexpr int HS_TT = HS_NT * HS_U;  // records per ring tile (16 KB)
-constexpr int HS_NST = 3;            // ring stages
+constexpr int HS_NT = 512;
+constexpr int HS_CTAS = 2;           // CTAs per SM
+constexpr int HS_U = 4;              // probes per thread per iteration
+constexpr int HS_D = 2;              // iterations of records in flight (cp.async)
+constexpr int HS_TT = HS_NT * HS_U;  // records per iteration
 constexpr int HS_CAP = 1024;         // staged spline points per window
 constexpr int HS_NC = 1024;          // lower-bound cells per window
-constexpr i64 HS_PIECE = 16384;      // records per work item (8 tiles)
+constexpr i64 HS_PIECE = 65536;      // records per work item
 constexpr int HS_MAXWIN = 2048;
+constexpr int HS_WPT = HS_MAXWIN / HS_NT;  // windows per thread in the piece prefix
 
 struct WinMeta {
     u64 klo, khi;
@@ -77,28 +78,33 @@ __device__ __forceinline__ i64 lower_bound_u64(const u64 *a, i64 n, u64 k) {
 
 // ------------------------------------------------------------ probe table
 
-// t_j = 2 pos_j - j over the sorted build keys; zero[0] counts zero payloads
-__global__ void k_slots_t(SplineDev m, const u64 *sk, const u64 *sp, i64 n, i64 *t, unsigned long long *zero) {
-    u32 z = 0;
+// t_j = 2 pos_j - j over the sorted build keys; cnt[0] counts zero
+// payloads, cnt[1] equal adjacent keys
+__global__ void k_slots_t(SplineDev m, const u64 *sk, const u64 *sp, i64 n, i64 *t, unsigned long long *cnt) {
+    u32 z = 0, d = 0;
     for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < n; j += (i64)gridDim.x * blockDim.x) {
         t[j] = 2 * m.pos(sk[j]) - j;
         z += sp[j] == 0;
+        d += j > 0 && sk[j] == sk[j - 1];
     }
-    if (z) atomicAdd(zero, (unsigned long long)z);
+    if (z) atomicAdd(cnt, (unsigned long long)z);
+    if (d) atomicAdd(cnt + 1, (unsigned long long)d);
 }
 
 struct MaxI64 {
     __device__ __forceinline__ i64 operator()(const i64 &a, const i64 &b) const { return a > b ? a : b; }
 };
 
-// plan[0] = slots needed (even, incl. the terminating pair), plan[1] = zero payloads
+// plan[0] = slots needed (even, incl. the terminating pair), plan[1] = zero
+// payloads, plan[2] = duplicate build keys
 __global__ void k_slots_size(const i64 *M, i64 n, unsigned long long *zero, i64 *plan) {
     const i64 last = (n - 1) + M[n - 1];
     i64 L = last + 1;
     if (L < 2 * (n - 1) + 2) L = 2 * (n - 1) + 2;
     L = (L + 1) & ~(i64)1;
     plan[0] = L + 2;
-    plan[1] = (i64)*zero;
+    plan[1] = (i64)zero[0];
+    plan[2] = (i64)zero[1];
 }
 
 // slot s: the last entry j with slot_j = j + M_j <= s (slot_j is strictly
@@ -219,54 +225,40 @@ struct Acc3 {
     }
 };
 
-// the rest of a slot scan whose first pair did not decide it: pairs from
-// slot 2*pos + 2 on, keys < k skipped, keys == k with a nonzero payload
-// counted, stop at the first key > k
-__device__ __forceinline__ void slot_scan_tail(const ulonglong2 *__restrict__ p, u64 k, u64 ps, Acc3 &a) {
-    for (;; p += 2) {
-        const ulonglong2 e0 = __ldg(p), e1 = __ldg(p + 1);
-        if (e0.x > k) return;
-        if (e0.x == k && e0.y) a.add(e0.y, ps);
-        if (e1.x > k) return;
-        if (e1.x == k && e1.y) a.add(e1.y, ps);
-    }
-}
-
-// record tiles of the probe's ring: HS_TT records each, with their window
-struct TileMeta {
-    i64 lo;
-    int w, cnt;
-};
-
-// global (unstaged) evaluation, kept out of line: the overflow area and
-// windows whose points exceed the staging capacity
+// global (unstaged) evaluation: the overflow area and windows whose points
+// exceed the staging capacity
 __device__ __forceinline__ i64 spline_pos_global(const SplineDev &m, u64 k) { return m.pos(k); }
 
+// Per thread, a software pipeline over iterations of HS_U records (one
+// per HS_NT-strided lane position): the records of iteration i + HS_D - 1
+// are copied into this thread's own shared-memory slots (cp.async, 16 B,
+// coalesced across the warp) while iteration i is probed, so no barrier
+// is needed inside a work item; every probe's first slot is loaded before
+// any is compared (HS_U independent L2 loads in flight per thread).
 __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev m, const ulonglong2 *__restrict__ slots,
-                                                                const ulonglong2 *__restrict__ rec,
-                                                                const i64 *__restrict__ reg, int nb,
-                                                                const WinMeta *__restrict__ meta,
-                                                                const u16 *__restrict__ cells_g,
-                                                                unsigned long long *ctr, u64 *out) {
+                                                                     int unique, const ulonglong2 *__restrict__ rec,
+                                                                     const i64 *__restrict__ reg, int nb,
+                                                                     const WinMeta *__restrict__ meta,
+                                                                     const u16 *__restrict__ cells_g,
+                                                                     unsigned long long *ctr, u64 *out) {
     extern __shared__ __align__(128) unsigned char smem_h[];
-    ulonglong2 *ring = reinterpret_cast<ulonglong2 *>(smem_h);                        // [HS_NST][HS_TT]
-    u64 *sk = reinterpret_cast<u64 *>(smem_h + (size_t)HS_NST * HS_TT * 16);
+    ulonglong2 *rbuf = reinterpret_cast<ulonglong2 *>(smem_h);  // [HS_D][HS_U][HS_NT]
+    u64 *sk = reinterpret_cast<u64 *>(smem_h + (size_t)HS_D * HS_U * HS_NT * 16);
     double *sr = reinterpret_cast<double *>(reinterpret_cast<unsigned char *>(sk) + (size_t)HS_CAP * 8);
     u16 *cells = reinterpret_cast<u16 *>(reinterpret_cast<unsigned char *>(sr) + (size_t)HS_CAP * 8);
     int *ip = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(cells) + (HS_NC + 8) * 2);  // [nb + 1]
-    __shared__ TileMeta tm[HS_NST];
-    __shared__ int s_tot;
+    __shared__ int s_item[2], s_tot;
     __shared__ WinMeta s_m;
     __shared__ int s_wsum[HS_NT / 32];
-    __shared__ __align__(8) uint64_t full[HS_NST], sbar;
+    __shared__ __align__(8) uint64_t sbar;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const i64 *rend = reg + nb + 1;
-    // pieces per window, exclusive prefix (8 windows per thread, nb <= 2048)
+    // pieces per window, exclusive prefix (HS_WPT windows per thread)
     {
-        int v[8], tot = 0;
+        int v[HS_WPT], tot = 0;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int w = tid * 8 + q;
+        for (int q = 0; q < HS_WPT; ++q) {
+            const int w = tid * HS_WPT + q;
             v[q] = w < nb ? (int)((rend[w] - reg[w] + HS_PIECE - 1) / HS_PIECE) : 0;
             tot += v[q];
         }
@@ -291,65 +283,22 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
         __syncthreads();
         int run = s_wsum[warp] + inc - tot;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int w = tid * 8 + q;
+        for (int q = 0; q < HS_WPT; ++q) {
+            const int w = tid * HS_WPT + q;
             if (w < nb) ip[w] = run;
             run += v[q];
         }
-        if (tid * 8 <= nb - 1 && nb - 1 <= tid * 8 + 7) {
+        if (tid * HS_WPT <= nb - 1 && nb - 1 < tid * HS_WPT + HS_WPT) {
             ip[nb] = run;
             s_tot = run + (int)((reg[2 * nb + 1] + HS_PIECE - 1) / HS_PIECE);
         }
     }
-    // producer state (thread 0 only): the current work item's remaining records
-    int p_w = -1;
-    i64 p_lo = 0, p_hi = 0;
-    bool p_done = false;
-    auto issue = [&](int s) {  // thread 0: the next tile into stage s
-        while (!p_done && p_lo >= p_hi) {
-            const int item = (int)atomicAdd(ctr, 1ULL);
-            if (item >= s_tot) {
-                p_done = true;
-                break;
-            }
-            if (item >= ip[nb]) {  // overflow area: any window
-                p_w = nb;
-                p_lo = reg[nb] + (i64)(item - ip[nb]) * HS_PIECE;
-                p_hi = min(p_lo + HS_PIECE, reg[nb] + reg[2 * nb + 1]);
-            } else {
-                int a = 0, b = nb - 1;  // last window with ip[w] <= item
-                while (a < b) {
-                    const int mid = (a + b + 1) >> 1;
-                    if (ip[mid] <= item) a = mid;
-                    else b = mid - 1;
-                }
-                p_w = a;
-                p_lo = reg[a] + (i64)(item - ip[a]) * HS_PIECE;
-                p_hi = min(p_lo + HS_PIECE, rend[a]);
-            }
-        }
-        if (p_done) {
-            tm[s].w = -1;
-            tm[s].cnt = 0;
-            mbar_arrive(&full[s]);
-            return;
-        }
-        const int cnt = (int)min((i64)HS_TT, p_hi - p_lo);
-        tm[s].w = p_w;
-        tm[s].lo = p_lo;
-        tm[s].cnt = cnt;
-        mbar_arrive_expect_tx(&full[s], (unsigned)cnt * 16u);
-        bulk_g2s(ring + (size_t)s * HS_TT, rec + p_lo, (unsigned)cnt * 16u, &full[s]);
-        p_lo += cnt;
-    };
     if (tid == 0) {
-        for (int s = 0; s < HS_NST; ++s) mbar_init(&full[s], 1);
         mbar_init(&sbar, 1);
         mbar_init_fence();
     }
     __syncthreads();
-    if (tid == 0)
-        for (int s = 0; s < HS_NST - 1; ++s) issue(s);
+    const int total = s_tot;
     unsigned sphase = 0;
     int cur = -1;
     bool staged = false;
@@ -360,81 +309,113 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
     ss.K = m.K;
     ss.n = m.n;
     Acc3 acc = {0, 0, 0};
-    for (int t = 0;; ++t) {
-        const int s = t % HS_NST;
-        mbar_wait(&full[s], (unsigned)(t / HS_NST) & 1u);
-        const int w = tm[s].w, cnt = tm[s].cnt;
-        if (cnt == 0) break;  // the producer ran out of work (every thread sees the same)
+    for (int it = 0;; ++it) {
+        if (tid == 0) s_item[it & 1] = (int)atomicAdd(ctr, 1ULL);
+        __syncthreads();
+        const int item = s_item[it & 1];
+        if (item >= total) break;
+        int w;
+        i64 lo, hi;
+        if (item >= ip[nb]) {  // overflow area: any window
+            w = nb;
+            lo = reg[nb] + (i64)(item - ip[nb]) * HS_PIECE;
+            hi = min(lo + HS_PIECE, reg[nb] + reg[2 * nb + 1]);
+        } else {
+            int a = 0, b = nb - 1;  // last window with ip[w] <= item
+            while (a < b) {
+                const int mid = (a + b + 1) >> 1;
+                if (ip[mid] <= item) a = mid;
+                else b = mid - 1;
+            }
+            w = a;
+            lo = reg[w] + (i64)(item - ip[w]) * HS_PIECE;
+            hi = min(lo + HS_PIECE, rend[w]);
+        }
         if (w != cur) {
-            // restage: every thread is past the previous tile (barrier below)
+            // restage (every thread is past the previous item: barrier above)
             cur = w;
             staged = false;
             if (w < nb) {
-                if (tid == 0) s_m = meta[w];
-                __syncthreads();
-                if (s_m.ok) {
+                const WinMeta mw = meta[w];
+                if (mw.ok) {
                     if (tid == 0) {
-                        const unsigned nbk = ((unsigned)s_m.npts * 8u + 15u) & ~15u;
+                        const unsigned nbk = ((unsigned)mw.npts * 8u + 15u) & ~15u;
                         const unsigned nbc = (unsigned)(HS_NC + 8) * 2u;
                         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                         mbar_arrive_expect_tx(&sbar, 2 * nbk + nbc);
-                        bulk_g2s(sk, m.keys + s_m.a0, nbk, &sbar);
-                        bulk_g2s(sr, m.ranks + s_m.a0, nbk, &sbar);
+                        bulk_g2s(sk, m.keys + mw.a0, nbk, &sbar);
+                        bulk_g2s(sr, m.ranks + mw.a0, nbk, &sbar);
                         bulk_g2s(cells, cells_g + (size_t)w * (HS_NC + 8), nbc, &sbar);
                     }
                     mbar_wait(&sbar, sphase);
                     sphase ^= 1u;
                     staged = true;
-                    ss.klo = s_m.klo;
-                    ss.khi = s_m.khi;
-                    ss.a0 = s_m.a0;
-                    ss.npts = s_m.npts;
-                    ss.cshift = s_m.cshift;
+                    ss.klo = mw.klo;
+                    ss.khi = mw.khi;
+                    ss.a0 = mw.a0;
+                    ss.npts = mw.npts;
+                    ss.cshift = mw.cshift;
                 }
             }
         }
-        const ulonglong2 *tile = ring + (size_t)s * HS_TT;
-        u64 k[HS_U], ps[HS_U];
-        i64 pos[HS_U];
+        const int niter = (int)((hi - lo + HS_TT - 1) / HS_TT);
+        auto fetch = [&](int i) {
+            if (i < niter) {
 #pragma unroll
-        for (int u = 0; u < HS_U; ++u) {
-            const int j = u * HS_NT + tid;
-            if (j < cnt) {
-                const ulonglong2 r = tile[j];
-                k[u] = r.x;
-                ps[u] = r.y;
-            } else {
-                k[u] = ~0ULL;
-                ps[u] = 0;
+                for (int u = 0; u < HS_U; ++u) {
+                    const i64 j = lo + (i64)i * HS_TT + u * HS_NT + tid;
+                    if (j < hi) cp_async16(rbuf + ((size_t)(i % HS_D) * HS_U + u) * HS_NT + tid, rec + j);
+                }
+            }
+            cp_async_commit();
+        };
+#pragma unroll
+        for (int i = 0; i < HS_D - 1; ++i) fetch(i);
+        for (int i = 0; i < niter; ++i) {
+            fetch(i + HS_D - 1);
+            asm volatile("cp.async.wait_group %0;" ::"n"(HS_D - 1) : "memory");
+            u64 k[HS_U], ps[HS_U];
+            i64 s0[HS_U];
+#pragma unroll
+            for (int u = 0; u < HS_U; ++u) {
+                const i64 j = lo + (i64)i * HS_TT + u * HS_NT + tid;
+                if (j < hi) {
+                    const ulonglong2 r = rbuf[((size_t)(i % HS_D) * HS_U + u) * HS_NT + tid];
+                    k[u] = r.x;
+                    ps[u] = r.y;
+                } else {
+                    k[u] = ~0ULL;
+                    ps[u] = 0;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < HS_U; ++u) {
+                if (k[u] == ~0ULL) s0[u] = -1;  // past the item / a gap record
+                else if (staged && k[u] >= ss.klo && k[u] <= ss.khi) s0[u] = 2 * ss.pos(k[u]);
+                else s0[u] = 2 * spline_pos_global(m, k[u]);
+            }
+            ulonglong2 e[HS_U];
+#pragma unroll
+            for (int u = 0; u < HS_U; ++u) e[u] = s0[u] >= 0 ? __ldg(slots + s0[u]) : make_ulonglong2(~0ULL, 0ULL);
+            // the slot scan (see the header): keys < k skipped, keys == k
+            // with a nonzero payload counted (unique build keys: the first
+            // is the only one), stop at the first key > k
+#pragma unroll
+            for (int u = 0; u < HS_U; ++u) {
+                if (s0[u] < 0) continue;
+                i64 sl = s0[u];
+                ulonglong2 ev = e[u];
+                for (;;) {
+                    if (ev.x > k[u]) break;
+                    if (ev.x == k[u] && ev.y) {
+                        acc.add(ev.y, ps[u]);
+                        if (unique) break;
+                    }
+                    ev = __ldg(slots + ++sl);
+                }
             }
         }
-#pragma unroll
-        for (int u = 0; u < HS_U; ++u) {
-            if (k[u] == ~0ULL) pos[u] = -1;  // past the tile / a gap record
-            else if (staged && k[u] >= ss.klo && k[u] <= ss.khi) pos[u] = ss.pos(k[u]);
-            else pos[u] = spline_pos_global(m, k[u]);
-        }
-        // every probe's first slot pair in flight at once
-        ulonglong2 e0[HS_U], e1[HS_U];
-#pragma unroll
-        for (int u = 0; u < HS_U; ++u) {
-            if (pos[u] >= 0) {
-                e0[u] = __ldg(slots + 2 * pos[u]);
-                e1[u] = __ldg(slots + 2 * pos[u] + 1);
-            } else {
-                e0[u] = e1[u] = make_ulonglong2(~0ULL, 0ULL);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < HS_U; ++u) {
-            if (pos[u] < 0 || e0[u].x > k[u]) continue;
-            if (e0[u].x == k[u] && e0[u].y) acc.add(e0[u].y, ps[u]);
-            if (e1[u].x > k[u]) continue;
-            if (e1[u].x == k[u] && e1[u].y) acc.add(e1[u].y, ps[u]);
-            slot_scan_tail(slots + 2 * pos[u] + 2, k[u], ps[u], acc);
-        }
-        __syncthreads();  // every thread is done with stage s (and the staged window)
-        if (tid == 0) issue((t + HS_NST - 1) % HS_NST);
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     reduce_checksum(acc.c, acc.s, acc.x, 0, out);
 }
@@ -463,7 +444,7 @@ int lj_spline_slots_plan(const LjSpline *model, const uint64_t *sorted_keys, con
     q += part_align_c(sizeof(i64) * (size_t)n);
     unsigned long long *zero = (unsigned long long *)q;
     q += 256;
-    LJ_CK(cudaMemsetAsync(zero, 0, sizeof(unsigned long long), st));
+    LJ_CK(cudaMemsetAsync(zero, 0, 2 * sizeof(unsigned long long), st));
     k_slots_t<<<grid_for(n, 256, 8), 256, 0, st>>>(SplineDev(*model), sorted_keys, sorted_pay, n, t, zero);
     LJ_CK_LAUNCH();
     size_t tb = 0;
@@ -509,16 +490,18 @@ int hash_probe_staged(const LjSplineHash &idx, const ulonglong2 *rec, const i64 
     const WinMeta *meta = reinterpret_cast<const WinMeta *>(meta_ws);
     const u16 *cells =
         reinterpret_cast<const u16 *>((const char *)meta_ws + (((size_t)nb * sizeof(WinMeta) + 255) & ~(size_t)255));
-    const size_t sm = (size_t)HS_NST * HS_TT * 16 + (size_t)HS_CAP * 16 + (HS_NC + 8) * 2 + (size_t)(nb + 2) * 4;
+    const size_t sm = (size_t)HS_D * HS_U * HS_NT * 16 + (size_t)HS_CAP * 16 + (HS_NC + 8) * 2 + (size_t)(nb + 2) * 4;
     static bool attr = false;
     if (!attr) {
-        LJ_CK(cudaFuncSetAttribute(k_hash_probe_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        LJ_CK(cudaFuncSetAttribute(k_hash_probe_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)((size_t)HS_D * HS_U * HS_NT * 16 + (size_t)HS_CAP * 16 + (HS_NC + 8) * 2 +
+                                         (size_t)(HS_MAXWIN + 2) * 4)));
         attr = true;
     }
     LJ_CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
-    k_hash_probe_staged<<<HS_CTAS * sm_count(), HS_NT, sm, st>>>(SplineDev(idx.model),
-                                                           reinterpret_cast<const ulonglong2 *>(idx.slots), rec, reg,
-                                                           nb, meta, cells, ctr, out);
+    k_hash_probe_staged<<<HS_CTAS * sm_count(), HS_NT, sm, st>>>(
+        SplineDev(idx.model), reinterpret_cast<const ulonglong2 *>(idx.slots), idx.slots_unique, rec, reg, nb, meta, cells,
+        ctr, out);
     LJ_CK_LAUNCH();
     return LJ_OK;
 }

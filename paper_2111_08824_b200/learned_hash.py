@@ -87,13 +87,14 @@ class SplineHashIndex:
         sk, sp = sort_pairs(relation.keys, relation.payloads)
         ws = _lib.workspace(lib.lj_spline_slots_workspace_bytes(self.n),
                             dev)
-        plan = torch.zeros(2, dtype=torch.int64, device=dev)
+        plan = torch.zeros(3, dtype=torch.int64, device=dev)
         c = self.model.c_struct()
         _lib.check(lib.lj_spline_slots_plan(ctypes.byref(c), _lib.ptr(sk), _lib.ptr(sp), self.n, _lib.ptr(plan),
                                             _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "spline_slots_plan")
-        nslots, zeros = (int(v) for v in plan.cpu().tolist())
+        nslots, zeros, dups = (int(v) for v in plan.cpu().tolist())
         if zeros:
             return
+        self.slots_unique = int(dups == 0)
         self.slots = torch.empty(2 * nslots, dtype=torch.int64, device=dev)
         _lib.check(lib.lj_spline_slots_fill(_lib.ptr(sk), _lib.ptr(sp), self.n, _lib.ptr(self.slots), nslots,
                                             _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "spline_slots_fill")
@@ -103,7 +104,7 @@ class SplineHashIndex:
         slots = getattr(self, "slots", None)
         return _lib.LjSplineHash(self.model.c_struct(), self.n, self.table_len, self.stride,
                                  _lib.ptr(self.entries), _lib.ptr(self.starts), _lib.ptr(slots),
-                                 getattr(self, "nslots", 0))
+                                 getattr(self, "nslots", 0), getattr(self, "slots_unique", 0), 0)
 
     @property
     def _keys(self) -> np.ndarray:
