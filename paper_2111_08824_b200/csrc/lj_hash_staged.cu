@@ -46,16 +46,16 @@ namespace lj {
 
 static inline size_t part_align_c(size_t v) { return (v + 255) & ~(size_t)255; }
 
-constexpr int HS_NT = 512;
+constexpr int HS_NT = 384;
 constexpr int HS_CTAS = 2;           // CTAs per SM
 constexpr int HS_U = 4;              // probes per thread per iteration
 constexpr int HS_D = 2;              // iterations of records in flight (cp.async)
 constexpr int HS_TT = HS_NT * HS_U;  // records per iteration
 constexpr int HS_CAP = 1024;         // staged spline points per window
 constexpr int HS_NC = 1024;          // lower-bound cells per window
-constexpr i64 HS_PIECE = 65536;      // records per work item
+constexpr i64 HS_PIECE = 16384;      // records per work item
 constexpr int HS_MAXWIN = 2048;
-constexpr int HS_WPT = HS_MAXWIN / HS_NT;  // windows per thread in the piece prefix
+constexpr int HS_WPT = (HS_MAXWIN + HS_NT - 1) / HS_NT;  // windows per thread in the piece prefix
 
 struct WinMeta {
     u64 klo, khi;
@@ -225,6 +225,12 @@ struct Acc3 {
     }
 };
 
+// 16-B asynchronous global -> shared copy with an L2 cache policy
+__device__ __forceinline__ void cp_async16_ef(void *dst, const void *src, u64 pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "l"(pol)
+                 : "memory");
+}
+
 // global (unstaged) evaluation: the overflow area and windows whose points
 // exceed the staging capacity
 __device__ __forceinline__ i64 spline_pos_global(const SplineDev &m, u64 k) { return m.pos(k); }
@@ -309,6 +315,8 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
     ss.K = m.K;
     ss.n = m.n;
     Acc3 acc = {0, 0, 0};
+    u64 pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     for (int it = 0;; ++it) {
         if (tid == 0) s_item[it & 1] = (int)atomicAdd(ctr, 1ULL);
         __syncthreads();
@@ -359,20 +367,31 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
             }
         }
         const int niter = (int)((hi - lo + HS_TT - 1) / HS_TT);
-        auto fetch = [&](int i) {
+        // records of iteration i -> this thread's slots of stage i % HS_D
+        // (evict-first in L2: read once; the slot lines are what L2 keeps)
+#pragma unroll
+        for (int i = 0; i < HS_D - 1; ++i) {
             if (i < niter) {
 #pragma unroll
                 for (int u = 0; u < HS_U; ++u) {
                     const i64 j = lo + (i64)i * HS_TT + u * HS_NT + tid;
-                    if (j < hi) cp_async16(rbuf + ((size_t)(i % HS_D) * HS_U + u) * HS_NT + tid, rec + j);
+                    if (j < hi) cp_async16_ef(rbuf + ((size_t)(i % HS_D) * HS_U + u) * HS_NT + tid, rec + j, pol);
                 }
             }
             cp_async_commit();
-        };
-#pragma unroll
-        for (int i = 0; i < HS_D - 1; ++i) fetch(i);
+        }
         for (int i = 0; i < niter; ++i) {
-            fetch(i + HS_D - 1);
+            {
+                const int f = i + HS_D - 1;
+                if (f < niter) {
+#pragma unroll
+                    for (int u = 0; u < HS_U; ++u) {
+                        const i64 j = lo + (i64)f * HS_TT + u * HS_NT + tid;
+                        if (j < hi) cp_async16_ef(rbuf + ((size_t)(f % HS_D) * HS_U + u) * HS_NT + tid, rec + j, pol);
+                    }
+                }
+                cp_async_commit();
+            }
             asm volatile("cp.async.wait_group %0;" ::"n"(HS_D - 1) : "memory");
             u64 k[HS_U], ps[HS_U];
             i64 s0[HS_U];
@@ -394,24 +413,41 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
                 else if (staged && k[u] >= ss.klo && k[u] <= ss.khi) s0[u] = 2 * ss.pos(k[u]);
                 else s0[u] = 2 * spline_pos_global(m, k[u]);
             }
-            ulonglong2 e[HS_U];
+            // every probe's first slot PAIR (32 B, aligned: one sector) in flight at once
+            u64 e[HS_U][4];
 #pragma unroll
-            for (int u = 0; u < HS_U; ++u) e[u] = s0[u] >= 0 ? __ldg(slots + s0[u]) : make_ulonglong2(~0ULL, 0ULL);
+            for (int u = 0; u < HS_U; ++u) {
+                if (s0[u] >= 0) {
+                    asm volatile("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+                                 : "=l"(e[u][0]), "=l"(e[u][1]), "=l"(e[u][2]), "=l"(e[u][3])
+                                 : "l"(slots + s0[u]));
+                } else {
+                    e[u][0] = e[u][2] = ~0ULL;
+                    e[u][1] = e[u][3] = 0;
+                }
+            }
             // the slot scan (see the header): keys < k skipped, keys == k
             // with a nonzero payload counted (unique build keys: the first
             // is the only one), stop at the first key > k
 #pragma unroll
             for (int u = 0; u < HS_U; ++u) {
-                if (s0[u] < 0) continue;
-                i64 sl = s0[u];
-                ulonglong2 ev = e[u];
-                for (;;) {
+                if (s0[u] < 0 || e[u][0] > k[u]) continue;
+                if (e[u][0] == k[u] && e[u][1]) {
+                    acc.add(e[u][1], ps[u]);
+                    if (unique) continue;
+                }
+                if (e[u][2] > k[u]) continue;
+                if (e[u][2] == k[u] && e[u][3]) {
+                    acc.add(e[u][3], ps[u]);
+                    if (unique) continue;
+                }
+                for (i64 sl = s0[u] + 2;; ++sl) {
+                    const ulonglong2 ev = __ldg(slots + sl);
                     if (ev.x > k[u]) break;
                     if (ev.x == k[u] && ev.y) {
                         acc.add(ev.y, ps[u]);
                         if (unique) break;
                     }
-                    ev = __ldg(slots + ++sl);
                 }
             }
         }
