@@ -185,15 +185,30 @@ __global__ void __launch_bounds__(256) k_hash_windows(SplineDev m, const u64 *la
 
 // ------------------------------------------------------------ probe
 
+// One staged spline segment [point li-1, point li]: the operands of
+// models.py:240-244 -- x0 = float64(key[li-1]), inv = RN(1 / max(x1 - x0, 1)),
+// r0 = rank[li-1], dr = RN(r1 - r0) -- precomputed per window in shared
+// memory.
+struct Seg {
+    double x0, inv, r0, dr;
+};
+
 struct StagedSpline {
     const u64 *sk;
-    const double *sr;
+    const Seg *seg;
     const u16 *cells;
     u64 klo, khi;
     int a0, npts, cshift;
     i64 K, n;
-    // models.py:221-248 for k in [klo, khi]: the lower bound over the
-    // staged points (the cell bounds it), then the reference's operations
+    double guard;  // (n + 1) * 2^-49: see pos()
+    // models.py:221-248 for k in [klo, khi]: the first spline key >= k over
+    // the staged points (the cell bounds its range), then the reference's
+    // operations.  t = (k - x0) / d is taken as (k - x0) * RN(1/d): both are
+    // within 3.01 * 2^-53 of the true quotient (t <= 1), so the two values of
+    // r0 + t*dr differ by at most 2^-50 * (r1 + 1) <= 2^-50 * (n + 1); rint
+    // only jumps at half-integers, so unless the fast value lies within
+    // `guard` (twice that) of one, both round to the same integer -- else
+    // the reference's division runs.
     __device__ __forceinline__ i64 pos(u64 k) const {
         const int c = (int)((k - klo) >> cshift);
         int lo = cells[c], hi = cells[c + 1];
@@ -205,12 +220,18 @@ struct StagedSpline {
         i64 j = (i64)a0 + lo;
         j = j < 1 ? 1 : (j > K - 1 ? K - 1 : j);
         const int li = (int)(j - a0);
-        const double x0 = u64_to_f64(sk[li - 1]), x1 = u64_to_f64(sk[li]);
+        const Seg g = seg[li];
         const double kf = u64_to_f64(k);
-        const double d = __dsub_rn(x1, x0);
-        const double t = clip_f64(__ddiv_rn(__dsub_rn(kf, x0), d > 1.0 ? d : 1.0), 0.0, 1.0);
-        const double r0 = sr[li - 1], r1 = sr[li];
-        const i64 p = f64_to_i64(rint(__dadd_rn(r0, __dmul_rn(t, __dsub_rn(r1, r0)))));
+        const double a = __dsub_rn(kf, g.x0);
+        double t = clip_f64(__dmul_rn(a, g.inv), 0.0, 1.0);
+        double z = __dadd_rn(g.r0, __dmul_rn(t, g.dr));
+        if (fabs(__dsub_rn(__dsub_rn(z, floor(z)), 0.5)) <= guard) {
+            const double x1 = u64_to_f64(sk[li]);
+            const double d = __dsub_rn(x1, g.x0);
+            t = clip_f64(__ddiv_rn(a, d > 1.0 ? d : 1.0), 0.0, 1.0);
+            z = __dadd_rn(g.r0, __dmul_rn(t, g.dr));
+        }
+        const i64 p = f64_to_i64(rint(z));
         return clip_i64(p, 0, n - 1);
     }
 };
@@ -251,7 +272,8 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
     ulonglong2 *rbuf = reinterpret_cast<ulonglong2 *>(smem_h);  // [HS_D][HS_U][HS_NT]
     u64 *sk = reinterpret_cast<u64 *>(smem_h + (size_t)HS_D * HS_U * HS_NT * 16);
     double *sr = reinterpret_cast<double *>(reinterpret_cast<unsigned char *>(sk) + (size_t)HS_CAP * 8);
-    u16 *cells = reinterpret_cast<u16 *>(reinterpret_cast<unsigned char *>(sr) + (size_t)HS_CAP * 8);
+    Seg *seg = reinterpret_cast<Seg *>(reinterpret_cast<unsigned char *>(sr) + (size_t)HS_CAP * 8);
+    u16 *cells = reinterpret_cast<u16 *>(reinterpret_cast<unsigned char *>(seg) + (size_t)HS_CAP * sizeof(Seg));
     int *ip = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(cells) + (HS_NC + 8) * 2);  // [nb + 1]
     __shared__ int s_item[2], s_tot;
     __shared__ WinMeta s_m;
@@ -310,10 +332,11 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
     bool staged = false;
     StagedSpline ss;
     ss.sk = sk;
-    ss.sr = sr;
+    ss.seg = seg;
     ss.cells = cells;
     ss.K = m.K;
     ss.n = m.n;
+    ss.guard = ((double)m.n + 1.0) * 1.7763568394002505e-15;  // 2^-49
     Acc3 acc = {0, 0, 0};
     u64 pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -357,6 +380,16 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
                     }
                     mbar_wait(&sbar, sphase);
                     sphase ^= 1u;
+                    for (int li = tid + 1; li < mw.npts; li += HS_NT) {
+                        Seg g;
+                        g.x0 = u64_to_f64(sk[li - 1]);
+                        const double d = __dsub_rn(u64_to_f64(sk[li]), g.x0);
+                        g.inv = __drcp_rn(d > 1.0 ? d : 1.0);
+                        g.r0 = sr[li - 1];
+                        g.dr = __dsub_rn(sr[li], g.r0);
+                        seg[li] = g;
+                    }
+                    __syncthreads();
                     staged = true;
                     ss.klo = mw.klo;
                     ss.khi = mw.khi;
@@ -526,12 +559,13 @@ int hash_probe_staged(const LjSplineHash &idx, const ulonglong2 *rec, const i64 
     const WinMeta *meta = reinterpret_cast<const WinMeta *>(meta_ws);
     const u16 *cells =
         reinterpret_cast<const u16 *>((const char *)meta_ws + (((size_t)nb * sizeof(WinMeta) + 255) & ~(size_t)255));
-    const size_t sm = (size_t)HS_D * HS_U * HS_NT * 16 + (size_t)HS_CAP * 16 + (HS_NC + 8) * 2 + (size_t)(nb + 2) * 4;
+    const size_t sm = (size_t)HS_D * HS_U * HS_NT * 16 + (size_t)HS_CAP * (16 + sizeof(Seg)) + (HS_NC + 8) * 2 +
+                      (size_t)(nb + 2) * 4;
     static bool attr = false;
     if (!attr) {
         LJ_CK(cudaFuncSetAttribute(k_hash_probe_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)((size_t)HS_D * HS_U * HS_NT * 16 + (size_t)HS_CAP * 16 + (HS_NC + 8) * 2 +
-                                         (size_t)(HS_MAXWIN + 2) * 4)));
+                                   (int)((size_t)HS_D * HS_U * HS_NT * 16 + (size_t)HS_CAP * (16 + sizeof(Seg)) +
+                                         (HS_NC + 8) * 2 + (size_t)(HS_MAXWIN + 2) * 4)));
         attr = true;
     }
     LJ_CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
