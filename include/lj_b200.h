@@ -124,6 +124,10 @@ typedef struct LjSplineHash {
     int32_t slots_unique;   /* 1 if no two build keys are equal: the probe
                                stops at the first match */
     int32_t _pad;
+    const double *segs;     /* [4 * model.npts] per spline point li >= 1:
+                               {x0 = f64(key[li-1]), RN(1/max(f64(key[li]) - x0, 1)),
+                                rank[li-1], RN(rank[li] - rank[li-1])}
+                               (lj_spline_segments); required with slots */
 } LjSplineHash;
 
 /* ------------------------------------------------------------ library */
@@ -303,6 +307,7 @@ int lj_spline_hash_probe_grouped(const LjSplineHash *idx, const uint64_t *s_pair
  * plan) writes the 2*nslots words.  Index build, untimed like the
  * reference's (learned_hash.py:35-66). */
 size_t lj_spline_slots_workspace_bytes(int64_t n);
+int lj_spline_segments(const LjSpline *model, double *segs, void *stream);
 int lj_spline_slots_plan(const LjSpline *model, const uint64_t *sorted_keys, const uint64_t *sorted_pay, int64_t n,
                          int64_t *plan, void *ws, size_t ws_bytes, void *stream);
 int lj_spline_slots_fill(const uint64_t *sorted_keys, const uint64_t *sorted_pay, int64_t n, uint64_t *slots,

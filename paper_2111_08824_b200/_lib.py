@@ -60,7 +60,7 @@ class LjSpline(ctypes.Structure):
 class LjSplineHash(ctypes.Structure):
     _fields_ = [("model", LjSpline), ("n", _i64), ("table_len", _i64), ("stride", _i64),
                 ("entries", _c_void_p), ("starts", _c_void_p), ("slots", _c_void_p), ("nslots", _i64),
-                ("slots_unique", ctypes.c_int32), ("_pad", ctypes.c_int32)]
+                ("slots_unique", ctypes.c_int32), ("_pad", ctypes.c_int32), ("segs", _c_void_p)]
 
 
 class LjLsjModel(ctypes.Structure):
@@ -79,6 +79,7 @@ SIGNATURES = {
     "lj_gather_uniform": (_int, [_P, _i64, _i64, _u64, _P, _i64, _P]),
     "lj_fill_normal": (_int, [_P, _i64, _i64, _u64, _P]),
     "lj_spline_slots_workspace_bytes": (_size_t, [_i64]),
+    "lj_spline_segments": (_int, [ctypes.POINTER(LjSpline), _P, _P]),
     "lj_spline_slots_plan": (_int, [ctypes.POINTER(LjSpline), _P, _P, _i64, _P, _P, _size_t, _P]),
     "lj_spline_slots_fill": (_int, [_P, _P, _i64, _P, _i64, _P, _size_t, _P]),
     "lj_fill_lognormal": (_int, [_P, _i64, _i64, _u64, ctypes.c_double, ctypes.c_double, ctypes.c_double, _P]),

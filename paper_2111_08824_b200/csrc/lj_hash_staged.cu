@@ -53,7 +53,7 @@ constexpr int HS_D = 2;              // iterations of records in flight (cp.asyn
 constexpr int HS_TT = HS_NT * HS_U;  // records per iteration
 constexpr int HS_CAP = 1024;         // staged spline points per window
 constexpr int HS_NC = 1024;          // lower-bound cells per window
-constexpr i64 HS_PIECE = 16384;      // records per work item
+constexpr i64 HS_PIECE = 32768;      // records per work item
 constexpr int HS_MAXWIN = 2048;
 constexpr int HS_WPT = (HS_MAXWIN + HS_NT - 1) / HS_NT;  // windows per thread in the piece prefix
 
@@ -267,12 +267,12 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
                                                                      const i64 *__restrict__ reg, int nb,
                                                                      const WinMeta *__restrict__ meta,
                                                                      const u16 *__restrict__ cells_g,
+                                                                     const Seg *__restrict__ segs_g,
                                                                      unsigned long long *ctr, u64 *out) {
     extern __shared__ __align__(128) unsigned char smem_h[];
     ulonglong2 *rbuf = reinterpret_cast<ulonglong2 *>(smem_h);  // [HS_D][HS_U][HS_NT]
     u64 *sk = reinterpret_cast<u64 *>(smem_h + (size_t)HS_D * HS_U * HS_NT * 16);
-    double *sr = reinterpret_cast<double *>(reinterpret_cast<unsigned char *>(sk) + (size_t)HS_CAP * 8);
-    Seg *seg = reinterpret_cast<Seg *>(reinterpret_cast<unsigned char *>(sr) + (size_t)HS_CAP * 8);
+    Seg *seg = reinterpret_cast<Seg *>(reinterpret_cast<unsigned char *>(sk) + (size_t)HS_CAP * 8);
     u16 *cells = reinterpret_cast<u16 *>(reinterpret_cast<unsigned char *>(seg) + (size_t)HS_CAP * sizeof(Seg));
     int *ip = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(cells) + (HS_NC + 8) * 2);  // [nb + 1]
     __shared__ int s_item[2], s_tot;
@@ -371,25 +371,16 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
                 if (mw.ok) {
                     if (tid == 0) {
                         const unsigned nbk = ((unsigned)mw.npts * 8u + 15u) & ~15u;
+                        const unsigned nbs = (unsigned)mw.npts * (unsigned)sizeof(Seg);
                         const unsigned nbc = (unsigned)(HS_NC + 8) * 2u;
                         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                        mbar_arrive_expect_tx(&sbar, 2 * nbk + nbc);
+                        mbar_arrive_expect_tx(&sbar, nbk + nbs + nbc);
                         bulk_g2s(sk, m.keys + mw.a0, nbk, &sbar);
-                        bulk_g2s(sr, m.ranks + mw.a0, nbk, &sbar);
+                        bulk_g2s(seg, segs_g + mw.a0, nbs, &sbar);
                         bulk_g2s(cells, cells_g + (size_t)w * (HS_NC + 8), nbc, &sbar);
                     }
                     mbar_wait(&sbar, sphase);
                     sphase ^= 1u;
-                    for (int li = tid + 1; li < mw.npts; li += HS_NT) {
-                        Seg g;
-                        g.x0 = u64_to_f64(sk[li - 1]);
-                        const double d = __dsub_rn(u64_to_f64(sk[li]), g.x0);
-                        g.inv = __drcp_rn(d > 1.0 ? d : 1.0);
-                        g.r0 = sr[li - 1];
-                        g.dr = __dsub_rn(sr[li], g.r0);
-                        seg[li] = g;
-                    }
-                    __syncthreads();
                     staged = true;
                     ss.klo = mw.klo;
                     ss.khi = mw.khi;
@@ -535,6 +526,32 @@ int lj_spline_slots_fill(const uint64_t *sorted_keys, const uint64_t *sorted_pay
     return LJ_OK;
 }
 
+// per spline point li >= 1: Seg{x0, RN(1/max(x1 - x0, 1)), r0, RN(r1 - r0)}
+// of the segment ending at li (seg[0] unused)
+__global__ void k_spline_segs(SplineDev m, Seg *seg) {
+    for (i64 li = blockIdx.x * (i64)blockDim.x + threadIdx.x; li < m.K; li += (i64)gridDim.x * blockDim.x) {
+        Seg g;
+        if (li == 0) {
+            g.x0 = g.inv = g.r0 = g.dr = 0.0;
+        } else {
+            g.x0 = u64_to_f64(m.keys[li - 1]);
+            const double d = __dsub_rn(u64_to_f64(m.keys[li]), g.x0);
+            g.inv = __drcp_rn(d > 1.0 ? d : 1.0);
+            g.r0 = m.ranks[li - 1];
+            g.dr = __dsub_rn(m.ranks[li], g.r0);
+        }
+        seg[li] = g;
+    }
+}
+
+int lj_spline_segments(const LjSpline *model, double *segs, void *stream) {
+    LJ_REQUIRE(model && model->npts >= 1, "model is not fitted");
+    k_spline_segs<<<grid_for(model->npts, 256, 4), 256, 0, as_stream(stream)>>>(SplineDev(*model),
+                                                                                reinterpret_cast<Seg *>(segs));
+    LJ_CK_LAUNCH();
+    return LJ_OK;
+}
+
 }  // extern "C"
 
 namespace lj {
@@ -552,6 +569,10 @@ int hash_windows(const LjSpline &model, const u64 *lay, int nb, u64 kmin, void *
 
 int hash_probe_staged(const LjSplineHash &idx, const ulonglong2 *rec, const i64 *reg, int nb, const void *meta_ws,
                       unsigned long long *ctr, u64 *out, cudaStream_t st) {
+    if (!idx.segs) {
+        set_error("hash_probe_staged: the index has no segment table");
+        return LJ_E_INVALID;
+    }
     if (nb > HS_MAXWIN) {
         set_error("hash_probe_staged: at most 2048 windows");
         return LJ_E_INVALID;
@@ -559,19 +580,19 @@ int hash_probe_staged(const LjSplineHash &idx, const ulonglong2 *rec, const i64 
     const WinMeta *meta = reinterpret_cast<const WinMeta *>(meta_ws);
     const u16 *cells =
         reinterpret_cast<const u16 *>((const char *)meta_ws + (((size_t)nb * sizeof(WinMeta) + 255) & ~(size_t)255));
-    const size_t sm = (size_t)HS_D * HS_U * HS_NT * 16 + (size_t)HS_CAP * (16 + sizeof(Seg)) + (HS_NC + 8) * 2 +
+    const size_t sm = (size_t)HS_D * HS_U * HS_NT * 16 + (size_t)HS_CAP * (8 + sizeof(Seg)) + (HS_NC + 8) * 2 +
                       (size_t)(nb + 2) * 4;
     static bool attr = false;
     if (!attr) {
         LJ_CK(cudaFuncSetAttribute(k_hash_probe_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)((size_t)HS_D * HS_U * HS_NT * 16 + (size_t)HS_CAP * (16 + sizeof(Seg)) +
+                                   (int)((size_t)HS_D * HS_U * HS_NT * 16 + (size_t)HS_CAP * (8 + sizeof(Seg)) +
                                          (HS_NC + 8) * 2 + (size_t)(HS_MAXWIN + 2) * 4)));
         attr = true;
     }
     LJ_CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
     k_hash_probe_staged<<<HS_CTAS * sm_count(), HS_NT, sm, st>>>(
         SplineDev(idx.model), reinterpret_cast<const ulonglong2 *>(idx.slots), idx.slots_unique, rec, reg, nb, meta, cells,
-        ctr, out);
+        reinterpret_cast<const Seg *>(idx.segs), ctr, out);
     LJ_CK_LAUNCH();
     return LJ_OK;
 }

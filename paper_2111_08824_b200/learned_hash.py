@@ -79,6 +79,7 @@ class SplineHashIndex:
         payload 0 -- built only when every payload is nonzero (else the
         chains are probed)."""
         self.slots = None
+        self.segs = None
         self.nslots = 0
         if not self.build_slots or self.model.trained_len != self.n:
             return
@@ -95,6 +96,8 @@ class SplineHashIndex:
         if zeros:
             return
         self.slots_unique = int(dups == 0)
+        self.segs = torch.empty(4 * self.model.spline_keys.size + 8, dtype=torch.float64, device=dev)
+        _lib.check(lib.lj_spline_segments(ctypes.byref(c), _lib.ptr(self.segs), _lib.stream_ptr()), "spline_segments")
         self.slots = torch.empty(2 * nslots, dtype=torch.int64, device=dev)
         _lib.check(lib.lj_spline_slots_fill(_lib.ptr(sk), _lib.ptr(sp), self.n, _lib.ptr(self.slots), nslots,
                                             _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "spline_slots_fill")
@@ -104,7 +107,8 @@ class SplineHashIndex:
         slots = getattr(self, "slots", None)
         return _lib.LjSplineHash(self.model.c_struct(), self.n, self.table_len, self.stride,
                                  _lib.ptr(self.entries), _lib.ptr(self.starts), _lib.ptr(slots),
-                                 getattr(self, "nslots", 0), getattr(self, "slots_unique", 0), 0)
+                                 getattr(self, "nslots", 0), getattr(self, "slots_unique", 0), 0,
+                                 _lib.ptr(getattr(self, "segs", None)) if slots is not None else None)
 
     @property
     def _keys(self) -> np.ndarray:
