@@ -353,7 +353,7 @@ def make_step(inp, index, variant="buffered", world: int = 1, distributed: bool 
             scratch = index.bucket_scratch(n_s)
             parts = [("bucket", lambda out: index.bucket_records(keys, pays, scratch)),
                      ("probe", lambda out: index.probe_records(n_s, scratch, out))]
-            kern = "k_grmi_probe_staged" if grmi else "k_hash_probe_chunks"
+            kern = "k_grmi_probe_staged" if grmi else "k_hash_probe_staged"
             st = Step(parts, "probe", 32 * n_s, kern,
                       f"32 B/probe x {n_s} probes (16 B S record + 16 B R entry); the one-pass grouping by "
                       "index window runs before it in the step")
