@@ -64,6 +64,10 @@ typedef struct LjRmi {
     const LjLeaf *leaves;   /* [m] */
     const int64_t *err;     /* [2m] interleaved {err_lo, err_hi}; may be NULL
                                when only positions are needed */
+    const double *root_dev; /* optional: the root {slope, intercept} in DEVICE
+                               memory (a model fitted on the stream, e.g. by
+                               lj_lsj_run); NULL = root_slope / root_icpt.
+                               Read by the LSJ kernels (K6-K9). */
 } LjRmi;
 
 /* Gapped RMI index view (gapped.py:206-338, GappedRmiIndex). */
@@ -384,12 +388,14 @@ int lj_lsj_shuffle_scatter(const LjLsjModel *model, const uint64_t *keys, const 
                            const int64_t *bases, void *ws, size_t ws_bytes, void *stream);
 /* lsj.py:242-286 per-bucket sort (K8, model-placed, shared memory) from the
  * partitioned pairs_in into pairs_out (fully sorted, bucket ranges kept).
- * stats_host[4] = {oversized buckets, bitonic fallbacks, sub-buckets above
- * shared memory, device radix-sorted sub-buckets}.  Synchronises the
- * stream (reads a few counters). */
+ * Asynchronous on the stream (no host readback): sub-buckets above the
+ * per-CTA capacity go to a one-CTA-per-SM instance, the rare ones above
+ * that to a global-memory chunk sort + merge, through device-side lists.
+ * stats (device int64[4], or NULL) = {sub-buckets above the main capacity,
+ * bitonic fallbacks, sorted by the big instance, sorted in global memory}. */
 size_t lj_lsj_sort_workspace_bytes(int64_t n, int64_t nbins);
 int lj_lsj_sort(const LjLsjModel *model, const uint64_t *pairs_in, uint64_t *pairs_out, int64_t n,
-                const int64_t *starts, void *ws, size_t ws_bytes, int64_t *stats_host, void *stream);
+                const int64_t *starts, void *ws, size_t ws_bytes, int64_t *stats, void *stream);
 /* Reference bucket bounds at scale P of a sorted relation (the
  * partition_index buckets of lsj.py:302-305, for its counters). */
 int lj_lsj_ref_bounds(const LjRmi *model, const uint64_t *sorted_pairs, int64_t n, int64_t P, int64_t *bounds,
@@ -399,6 +405,18 @@ int lj_lsj_ref_bounds(const LjRmi *model, const uint64_t *sorted_pairs, int64_t 
  * thread per tile, into ws), then tile and slice are merged in shared
  * memory.  mode 0: out[4] checksum; mode 1: counts[ns]; mode 2: pairs at
  * offsets[ns] into out_pr/out_ps. */
+/* lsj.py:373-405 lsj_join in ONE call, asynchronous on the stream, from one
+ * caller workspace (lj_lsj_run_workspace_bytes): per relation the sample
+ * (seed for R, seed ^ 0x5DEECE66D for S, lsj.py:388-391), the RMI fit with
+ * fanout min(1000, samples // 8), equi-depth bins, partition (K6/K7), the
+ * split + model-placed sort (K8); then the chunked merge-join (K9) of S
+ * against R through R's model.  out[4] (device) = {count, sum, xor, 0} of
+ * R.payload + S.payload over the equal-key pairs.  The same words as the
+ * Python orchestration (lsj.lsj_join) and the reference's lsj_join. */
+size_t lj_lsj_run_workspace_bytes(int64_t nr, int64_t ns, double sample_rate);
+int lj_lsj_run(const uint64_t *r_keys, const uint64_t *r_pay, int64_t nr, const uint64_t *s_keys,
+               const uint64_t *s_pay, int64_t ns, double sample_rate, uint64_t seed, uint64_t *out, void *ws,
+               size_t ws_bytes, void *stream);
 size_t lj_lsj_join_workspace_bytes(int64_t ns);
 int lj_lsj_join(const LjLsjModel *model_r, const uint64_t *r_pairs, int64_t nr, const int64_t *r_starts,
                 const uint64_t *s_pairs, int64_t ns, int mode, int64_t *counts, const int64_t *offsets,

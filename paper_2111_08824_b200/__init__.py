@@ -13,7 +13,7 @@ from .data import CorruptKeyFileError, Relation, load_keys_file, make_relation, 
 from .gapped import GappedRmiIndex, build_grmi
 from .joins import ALGORITHMS, DEFAULT_OPTS, BenchReport, run_join
 from .learned_hash import SplineHashIndex, build_spline_hash
-from .lsj import LsjConfig, ModelMismatchError, lsj_join
+from .lsj import LsjConfig, ModelMismatchError, lsj_join, lsj_run
 from .models import (
     PosPrediction,
     RadixSplineIndex,

@@ -43,7 +43,7 @@ class LjLeaf(ctypes.Structure):
 
 class LjRmi(ctypes.Structure):
     _fields_ = [("root_slope", ctypes.c_double), ("root_icpt", ctypes.c_double), ("m", _i64), ("n", _i64),
-                ("leaves", _c_void_p), ("err", _c_void_p)]
+                ("leaves", _c_void_p), ("err", _c_void_p), ("root_dev", _c_void_p)]
 
 
 class LjGrmi(ctypes.Structure):
@@ -79,6 +79,8 @@ SIGNATURES = {
     "lj_gather_uniform": (_int, [_P, _i64, _i64, _u64, _P, _i64, _P]),
     "lj_fill_normal": (_int, [_P, _i64, _i64, _u64, _P]),
     "lj_spline_slots_workspace_bytes": (_size_t, [_i64]),
+    "lj_lsj_run_workspace_bytes": (_size_t, [_i64, _i64, ctypes.c_double]),
+    "lj_lsj_run": (_int, [_P, _P, _i64, _P, _P, _i64, ctypes.c_double, _u64, _P, _P, _size_t, _P]),
     "lj_spline_segments": (_int, [ctypes.POINTER(LjSpline), _P, _P]),
     "lj_spline_slots_plan": (_int, [ctypes.POINTER(LjSpline), _P, _P, _i64, _P, _P, _size_t, _P]),
     "lj_spline_slots_fill": (_int, [_P, _P, _i64, _P, _i64, _P, _size_t, _P]),

@@ -128,9 +128,18 @@ struct RmiDev {
     i64 m, n;
     const LjLeaf *leaves;
     const i64 *err;
+    const double *rootp;  // root {slope, intercept} in device memory, or null
     __host__ RmiDev() {}
     __host__ explicit RmiDev(const LjRmi &r)
-        : rs(r.root_slope), ri(r.root_icpt), m(r.m), n(r.n), leaves(r.leaves), err(r.err) {}
+        : rs(r.root_slope), ri(r.root_icpt), m(r.m), n(r.n), leaves(r.leaves), err(r.err), rootp(r.root_dev) {}
+    // a model fitted on the stream (lj_lsj_run) keeps its root on the device:
+    // kernels take it from there before the first evaluation
+    __device__ __forceinline__ void fix() {
+        if (rootp) {
+            rs = rootp[0];
+            ri = rootp[1];
+        }
+    }
     __device__ __forceinline__ i64 route(double x) const { return rmi_route(rs, ri, m, x); }
     __device__ __forceinline__ i64 pos(double x) const {
         return rmi_leaf_pos(load_leaf(leaves, route(x)), x);

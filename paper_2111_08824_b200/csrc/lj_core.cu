@@ -247,8 +247,10 @@ __device__ __forceinline__ i64 piece_leaf(const i64 *pbase, i64 m, i64 q) {
 // means; phase 2: residual bounds of the finished leaf model
 template <int PHASE>
 __global__ void __launch_bounds__(FIT_THREADS) k_leaf_piece(const u64 *k, const i64 *rank, i64 m, const i64 *starts,
-                                                            const i64 *pbase, i64 npieces, const double *means,
-                                                            const LjLeaf *leaves, double *part, i64 *ipart) {
+                                                            const i64 *pbase, const i64 *npieces_dev,
+                                                            const double *means, const LjLeaf *leaves, double *part,
+                                                            i64 *ipart) {
+    const i64 npieces = *npieces_dev;  // pbase[m], on the device: no readback
     for (i64 q = blockIdx.x; q < npieces; q += gridDim.x) {
         const i64 l = piece_leaf(pbase, m, q);
         const i64 j = q - pbase[l];
@@ -543,10 +545,11 @@ int lj_rmi_fit(const uint64_t *k, int64_t n, int64_t m, double *root, LjLeaf *le
     LJ_CK_LAUNCH();
     size_t pq = piece_scan_bytes(m);
     LJ_CK(cub::DeviceScan::ExclusiveSum(p, pq, pcnt, pbase, (int64_t)(m + 1), st));
-    i64 npieces = 0;
-    LJ_CK(cudaMemcpyAsync(&npieces, pbase + m, sizeof(i64), cudaMemcpyDeviceToHost, st));
-    LJ_CK(cudaStreamSynchronize(st));
-    const unsigned gp = (unsigned)(npieces < 65535 * 4 ? npieces : 65535 * 4);
+    // the piece count stays on the device (pbase[m]): a grid-stride launch
+    // at its bound keeps the fit asynchronous on the stream
+    const i64 pmax = max_pieces(n, m), pcap = (i64)sm_count() * 16;
+    const unsigned gp = (unsigned)(pmax < pcap ? pmax : pcap);
+    const i64 *npieces = pbase + m;
     const unsigned gl = grid_for(m, 256, 8);
     k_leaf_piece<0><<<gp, FIT_THREADS, 0, st>>>(k, rank, m, starts, pbase, npieces, lmeans, leaves, ppart, ipart);
     k_leaf_combine<0><<<gl, 256, 0, st>>>(starts, n, m, pbase, ppart, ipart, lmeans, leaves, err);

@@ -128,6 +128,7 @@ struct LsjBin : NoTable {
 // #{ j : pb[j] <= pos(k) } = #{ j : B[j] <= k }); a 64-step search over the
 // key domain per boundary.  Written as lay[4 + j] (lj_keybin.cuh).
 __global__ void k_lsj_key_bounds(LsjDev d, u64 *lay) {
+    d.m.fix();
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= d.nb) return;
     if (j == 0) {
@@ -150,6 +151,7 @@ __global__ void k_lsj_key_bounds(LsjDev d, u64 *lay) {
 
 // spos[i] = pos(sample[i]) (sample sorted -> spos non-decreasing)
 __global__ void k_sample_pos(RmiDev m, const u64 *sample, i64 total, i64 *spos) {
+    m.fix();
     for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < total; i += (i64)gridDim.x * blockDim.x)
         spos[i] = m.pos(u64_to_f64(sample[i]));
 }
@@ -211,9 +213,10 @@ struct SubBuckets {
     }
 };
 
+template <int NT>
 __device__ __forceinline__ void block_scan_u32(u32 *a, int n, u32 *warp_tot) {
-    // exclusive scan of a[0..n) in place, SORT_NT threads
-    const int per = (n + SORT_NT - 1) / SORT_NT;
+    // exclusive scan of a[0..n) in place, NT threads
+    const int per = (n + NT - 1) / NT;
     const int j0 = threadIdx.x * per;
     u32 local = 0;
     for (int j = j0; j < j0 + per && j < n; ++j) local += a[j];
@@ -227,13 +230,13 @@ __device__ __forceinline__ void block_scan_u32(u32 *a, int n, u32 *warp_tot) {
     if (lane == 31) warp_tot[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-        u32 t = lane < SORT_NT / 32 ? warp_tot[lane] : 0;
+        u32 t = lane < NT / 32 ? warp_tot[lane] : 0;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             u32 v = __shfl_up_sync(0xffffffffu, t, o);
             if (lane >= o) t += v;
         }
-        if (lane < SORT_NT / 32) warp_tot[lane] = t;
+        if (lane < NT / 32) warp_tot[lane] = t;
     }
     __syncthreads();
     u32 run = (warp ? warp_tot[warp - 1] : 0) + incl - local;
@@ -270,6 +273,7 @@ __global__ void k_split_plan(const i64 *starts, int nb, int points, i64 *fcount)
 // split values of bucket b -> spv[fbase[b] .. fbase[b] + F_b - 1)
 // bin of every sample key (the sample is sorted, so these are non-decreasing)
 __global__ void k_sample_bins(LsjDev md, u32 *sbin) {
+    md.m.fix();
     for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < md.nsample; i += (i64)gridDim.x * blockDim.x)
         sbin[i] = (u32)md.bin(md.sample[i]);
 }
@@ -277,6 +281,7 @@ __global__ void k_sample_bins(LsjDev md, u32 *sbin) {
 // sample index range [sr[b], se[b]) of every bin (bins are monotone over the
 // sorted sample)
 __global__ void k_split_ranges(LsjDev md, const u32 *sbin, int nb, i64 *sr, i64 *se) {
+    md.m.fix();
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
         i64 lo = 0, hi = md.nsample;
         while (lo < hi) {
@@ -300,6 +305,7 @@ __global__ void k_split_ranges(LsjDev md, const u32 *sbin, int nb, i64 *sr, i64 
 // j in [1, F_b).
 __global__ void k_split_points(LsjDev md, const i64 *starts, const i64 *fbase, int nb, const i64 *sr,
                                const i64 *se, u64 *spv) {
+    md.m.fix();
     const i64 G = fbase[nb];
     for (i64 g = blockIdx.x * (i64)blockDim.x + threadIdx.x; g < G; g += (i64)gridDim.x * blockDim.x) {
         int lo = 0, hi = nb;  // bucket of slot g: last b with fbase[b] <= g
@@ -433,6 +439,7 @@ __device__ __forceinline__ int split_slot(const LsjDev &md, const SplitItem &it,
 // pass 1: mat[mbase[b] + s * chunks_b + c] = tuples of chunk c in slot s
 __global__ void __launch_bounds__(SPLIT_NT) k_split_count(LsjDev md, SplitCtx cx, const ulonglong2 *__restrict__ A,
                                                           const i64 *nitems, u32 *mat, SortCtl *ctl) {
+    md.m.fix();
     __shared__ u32 h[2 * SPLIT_MAXF];
     __shared__ u64 v[SPLIT_MAXF];
     __shared__ u16 cells[SPLIT_CELLS + 1];
@@ -478,6 +485,7 @@ __global__ void __launch_bounds__(SPLIT_NT) k_split_count(LsjDev md, SplitCtx cx
 
 // slot bounds + placement ranges from the scanned matrix
 __global__ void k_split_slots(LsjDev md, SplitCtx cx, const i64 *off, i64 n, i64 *sub_starts, double2 *sub_y) {
+    md.m.fix();
     const bool points = md.sample != nullptr;
     const i64 G = cx.fbase[cx.nb];
     for (i64 g = blockIdx.x * (i64)blockDim.x + threadIdx.x; g <= G; g += (i64)gridDim.x * blockDim.x) {
@@ -520,6 +528,7 @@ __global__ void k_split_slots(LsjDev md, SplitCtx cx, const i64 *off, i64 n, i64
 __global__ void __launch_bounds__(SPLIT_NT) k_split_scatter(LsjDev md, SplitCtx cx, const ulonglong2 *__restrict__ A,
                                                             const i64 *nitems, const i64 *__restrict__ off,
                                                             ulonglong2 *B, ulonglong2 *Out, SortCtl *ctl) {
+    md.m.fix();
     __shared__ u32 cur[2 * SPLIT_MAXF];
     __shared__ u64 v[SPLIT_MAXF];
     __shared__ u16 cells[SPLIT_CELLS + 1];
@@ -571,6 +580,7 @@ __global__ void __launch_bounds__(SPLIT_NT) k_split_scatter(LsjDev md, SplitCtx 
 // Block-wide sort of idx[base, base+len) by K[idx[.]]: a bitonic network in
 // its "flip" form, whose comparators all put the minimum at the lower index,
 // so positions >= len act as +inf and their comparators are skipped.
+template <int NT>
 __device__ void block_sort_idx(u16 *idx, int base, int len, const u64 *K) {
     int w = 1;
     while (w < len) w <<= 1;
@@ -578,7 +588,7 @@ __device__ void block_sort_idx(u16 *idx, int base, int len, const u64 *K) {
         for (int j = k; j > 1; j >>= 1) {
             const bool flip = j == k;
             const int h = j >> 1;
-            for (int t = threadIdx.x; t < (w >> 1); t += SORT_NT) {
+            for (int t = threadIdx.x; t < (w >> 1); t += NT) {
                 // t-th comparator of this stage: i in the lower half of its
                 // j-block, partner mirrored (flip) or h apart
                 const int i = (t / h) * j + (t % h);
@@ -597,18 +607,21 @@ __device__ void block_sort_idx(u16 *idx, int base, int len, const u64 *K) {
 }
 
 // K8: one CTA per bucket (dynamic work counter), model-placed in smem.
-template <class Src>
-__global__ void __launch_bounds__(SORT_NT, SORT_CTAS) k_lsj_sort(LsjDev md, Src src, const i64 *nbuckets_dev,
-                                                         const ulonglong2 *__restrict__ in, ulonglong2 *out,
-                                                         SortCtl *ctl, i64 *over_list) {
-    const i64 nbuckets = *nbuckets_dev;
+// Buckets above CAPV go to over_list (ctl->n_over); the "big" instance (one
+// CTA per SM, CAPV = CAP_BIG) sorts that list and passes what exceeds it on.
+template <class Src, int NT, int CAPV, int CTAS>
+__global__ void __launch_bounds__(NT, CTAS) k_lsj_sort(LsjDev md, Src src, const unsigned long long *nbuckets_dev,
+                                                       const ulonglong2 *__restrict__ in, ulonglong2 *out,
+                                                       SortCtl *ctl, i64 *over_list) {
+    md.m.fix();
+    const i64 nbuckets = (i64)*nbuckets_dev;
     extern __shared__ __align__(16) unsigned char smem[];
-    u64 *K = reinterpret_cast<u64 *>(smem);              // keys [CAP]
-    u32 *cnt = reinterpret_cast<u32 *>(K + CAP);          // slot counts -> cursors [SLOT_X * CAP]
-    u16 *slot = reinterpret_cast<u16 *>(cnt + SLOT_X * CAP);  // slot per key [CAP]
-    u16 *idx = slot + CAP;                                // placement [CAP]
-    u16 *ord = idx + CAP;                                 // final order [CAP]
-    __shared__ u32 warp_tot[SORT_NT / 32];
+    u64 *K = reinterpret_cast<u64 *>(smem);              // keys [CAPV]
+    u32 *cnt = reinterpret_cast<u32 *>(K + CAPV);          // slot counts -> cursors [SLOT_X * CAPV]
+    u16 *slot = reinterpret_cast<u16 *>(cnt + SLOT_X * CAPV);  // slot per key [CAPV]
+    u16 *idx = slot + CAPV;                                // placement [CAPV]
+    u16 *ord = idx + CAPV;                                 // final order [CAPV]
+    __shared__ u32 warp_tot[NT / 32];
     __shared__ i64 s_b, s_bn;
     __shared__ int s_bad, s_nruns;
     __shared__ int2 s_runs[MAX_RUNS];
@@ -623,7 +636,7 @@ __global__ void __launch_bounds__(SORT_NT, SORT_CTAS) k_lsj_sort(LsjDev md, Src 
             s_nruns = 0;
             if (s_bn < nbuckets) {
                 const Bucket nx = src.get(s_bn);
-                if (!nx.point && nx.m > 1 && nx.m <= (i64)CAP)
+                if (!nx.point && nx.m > 1 && nx.m <= (i64)CAPV)
                     bulk_prefetch_l2(in + nx.in_base, (unsigned)(nx.m * sizeof(ulonglong2)));
             }
         }
@@ -632,31 +645,31 @@ __global__ void __launch_bounds__(SORT_NT, SORT_CTAS) k_lsj_sort(LsjDev md, Src 
         __syncthreads();
         if (b >= nbuckets) break;
         const Bucket bk = src.get(b);
-        const int m = (int)(bk.m < (i64)CAP ? bk.m : (i64)CAP);
+        const int m = (int)(bk.m < (i64)CAPV ? bk.m : (i64)CAPV);
         if (bk.m == 0 || bk.point) continue;
         if (bk.m == 1) {
             if (threadIdx.x == 0) out[bk.out_base] = in[bk.in_base];
             continue;
         }
-        if (bk.m > CAP) {
+        if (bk.m > CAPV) {
             if (threadIdx.x == 0) over_list[atomicAdd(&ctl->n_over, 1ULL)] = b;
             continue;
         }
         const int ms = m * SLOT_X;  // placement slots
         const double scale = (double)ms / (bk.yspan > 0.0 ? bk.yspan : 1.0);
-        for (int j = threadIdx.x; j < ms; j += SORT_NT) cnt[j] = 0;
+        for (int j = threadIdx.x; j < ms; j += NT) cnt[j] = 0;
         __syncthreads();
         // load keys, place by the model (SORT_U keys in flight per thread)
-        for (int i0 = threadIdx.x; i0 < m; i0 += SORT_NT * SORT_U) {
+        for (int i0 = threadIdx.x; i0 < m; i0 += NT * SORT_U) {
             u64 k[SORT_U];
 #pragma unroll
             for (int u = 0; u < SORT_U; ++u) {
-                const int i = i0 + u * SORT_NT;
+                const int i = i0 + u * NT;
                 k[u] = i < m ? in[bk.in_base + i].x : 0;
             }
 #pragma unroll
             for (int u = 0; u < SORT_U; ++u) {
-                const int i = i0 + u * SORT_NT;
+                const int i = i0 + u * NT;
                 if (i >= m) break;
                 K[i] = k[u];
                 const double f = floor((md.y(k[u]) - bk.ybase) * scale);
@@ -666,8 +679,8 @@ __global__ void __launch_bounds__(SORT_NT, SORT_CTAS) k_lsj_sort(LsjDev md, Src 
             }
         }
         __syncthreads();
-        block_scan_u32(cnt, ms, warp_tot);
-        for (int i = threadIdx.x; i < m; i += SORT_NT) idx[atomicAdd(cnt + slot[i], 1u)] = (u16)i;
+        block_scan_u32<NT>(cnt, ms, warp_tot);
+        for (int i = threadIdx.x; i < m; i += NT) idx[atomicAdd(cnt + slot[i], 1u)] = (u16)i;
         __syncthreads();
         // after the scatter cnt[s] = end of slot s's run = start of slot
         // s+1's, so every element knows its run [cnt[s-1], cnt[s]).  Pass 1
@@ -677,14 +690,14 @@ __global__ void __launch_bounds__(SORT_NT, SORT_CTAS) k_lsj_sort(LsjDev md, Src 
         // rank in the run (key, then position), long mixed runs are copied
         // and sorted block-wide below.
         constexpr u32 MIXED = 0x80000000u;
-        for (int p = threadIdx.x; p < m; p += SORT_NT) {
+        for (int p = threadIdx.x; p < m; p += NT) {
             const u16 ip = idx[p];
             const int si = slot[ip];
             const int a = si > 0 ? (int)(cnt[si - 1] & ~MIXED) : 0, e = (int)(cnt[si] & ~MIXED);
             if (e - a > 1 && p != a && K[ip] != K[idx[a]]) atomicOr(cnt + si, MIXED);
         }
         __syncthreads();
-        for (int p = threadIdx.x; p < m; p += SORT_NT) {
+        for (int p = threadIdx.x; p < m; p += NT) {
             const u16 ip = idx[p];
             const int si = slot[ip];
             const u32 ce = cnt[si];
@@ -716,32 +729,32 @@ __global__ void __launch_bounds__(SORT_NT, SORT_CTAS) k_lsj_sort(LsjDev md, Src 
         __syncthreads();
         const int nruns = s_nruns < MAX_RUNS ? s_nruns : MAX_RUNS;
         if (!s_bad)
-            for (int q = 0; q < nruns; ++q) block_sort_idx(ord, s_runs[q].x, s_runs[q].y, K);
+            for (int q = 0; q < nruns; ++q) block_sort_idx<NT>(ord, s_runs[q].x, s_runs[q].y, K);
         // safety net: a misordered bucket is re-sorted whole (it fired on
         // keys routed to empty leaves past the last training key before
         // y() placed them at the top)
-        for (int i = threadIdx.x; i + 1 < m; i += SORT_NT)
+        for (int i = threadIdx.x; i + 1 < m; i += NT)
             if (K[ord[i]] > K[ord[i + 1]]) s_bad = 1;
         __syncthreads();
         if (s_bad) {
             // safety net (the placement key is monotone, so this only runs
             // when too many long runs appeared): sort the whole bucket
-            block_sort_idx(ord, 0, m, K);
+            block_sort_idx<NT>(ord, 0, m, K);
             if (threadIdx.x == 0) atomicAdd(&ctl->n_fallback, 1ULL);
         }
         // write out: key from smem, payload gathered from the bucket (L2-hot)
-        for (int i0 = threadIdx.x; i0 < m; i0 += SORT_NT * SORT_U) {
+        for (int i0 = threadIdx.x; i0 < m; i0 += NT * SORT_U) {
             u64 p[SORT_U];
             u16 j[SORT_U];
 #pragma unroll
             for (int u = 0; u < SORT_U; ++u) {
-                const int i = i0 + u * SORT_NT;
+                const int i = i0 + u * NT;
                 j[u] = i < m ? ord[i] : 0;
                 p[u] = i < m ? __ldg(&in[bk.in_base + j[u]].y) : 0;
             }
 #pragma unroll
             for (int u = 0; u < SORT_U; ++u) {
-                const int i = i0 + u * SORT_NT;
+                const int i = i0 + u * NT;
                 if (i < m) out[bk.out_base + i] = make_ulonglong2(K[j[u]], p[u]);
             }
         }
@@ -749,119 +762,115 @@ __global__ void __launch_bounds__(SORT_NT, SORT_CTAS) k_lsj_sort(LsjDev md, Src 
     }
 }
 
-// Sub-buckets still above CAP (a hot duplicate key's point slice), over the
-// flattened list: big[q] = {start, len}, boff = exclusive prefix of len.
-__device__ __forceinline__ int find_big(const i64 *boff, int nbig, i64 t) {
-    int lo = 0, hi = nbig;  // last q with boff[q] <= t
-    while (hi - lo > 1) {
-        int mid = (lo + hi) >> 1;
-        if (boff[mid] <= t) lo = mid; else hi = mid;
-    }
-    return lo;
-}
+// The sub-buckets the main sort passed over (above CAP), by list index:
+// the "big" sort instance (one CTA per SM, up to CAP_BIG tuples in shared
+// memory) takes them from this view.
+struct OverBuckets {
+    const i64 *list;
+    SubBuckets sub;
+    __device__ __forceinline__ Bucket get(i64 q) const { return sub.get(list[q]); }
+};
 
-__global__ void k_big_list(const i64 *list, int nbig, const i64 *sub_starts, i64 *big) {
-    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nbig; q += gridDim.x * blockDim.x) {
-        const i64 g = list[q];
-        big[2 * q] = sub_starts[g];
-        big[2 * q + 1] = sub_starts[g + 1] - sub_starts[g];
-    }
-}
+// The rare sub-buckets above CAP_BIG, device-driven (no host readback): one
+// CTA per bucket sorts it in global memory -- chunks of HUGE_CH records
+// sorted in shared memory (bitonic), then bottom-up merge passes (merge
+// path: every thread finds its output range by a binary search over the
+// two runs) ping-ponging between the split array and the output.
+constexpr int HUGE_NT = 1024;
+constexpr int HUGE_CH = 8192;  // 128 KB of records in shared memory
 
-// one block per big sub-bucket q: flags[q] = 1 if it holds more than one
-// distinct key, kr[q] = {min, max} of its keys (block reductions, no atomics)
-__global__ void k_big_scan(const ulonglong2 *B, const i64 *big, int nbig, int *flags, unsigned long long *kr) {
-    __shared__ u64 smin[32], smax[32];
-    for (int q = blockIdx.x; q < nbig; q += gridDim.x) {
-        const i64 a = big[2 * q], len = big[2 * q + 1];
-        const u64 k0 = B[a].x;
-        u64 mn = k0, mx = k0;
-        for (i64 t = threadIdx.x; t < len; t += blockDim.x) {
-            const u64 k = B[a + t].x;
-            mn = k < mn ? k : mn;
-            mx = k > mx ? k : mx;
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            const u64 a1 = __shfl_xor_sync(0xffffffffu, mn, o), b1 = __shfl_xor_sync(0xffffffffu, mx, o);
-            mn = a1 < mn ? a1 : mn;
-            mx = b1 > mx ? b1 : mx;
-        }
-        const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-        if ((threadIdx.x & 31) == 0) {
-            smin[w] = mn;
-            smax[w] = mx;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            for (int i = 1; i < nw; ++i) {
-                mn = smin[i] < mn ? smin[i] : mn;
-                mx = smax[i] > mx ? smax[i] : mx;
+__device__ __forceinline__ bool rec_less(const ulonglong2 &a, const ulonglong2 &b) { return a.x < b.x; }
+
+__device__ void huge_chunk_sort(ulonglong2 *sm, int len) {
+    int w = 1;
+    while (w < len) w <<= 1;
+    for (int i = len + (int)threadIdx.x; i < w; i += HUGE_NT) sm[i] = make_ulonglong2(~0ULL, 0ULL);
+    __syncthreads();
+    for (int k = 2; k <= w; k <<= 1)
+        for (int j = k; j > 1; j >>= 1) {
+            const bool flip = j == k;
+            const int h = j >> 1;
+            for (int t = threadIdx.x; t < (w >> 1); t += HUGE_NT) {
+                const int i = (t / h) * j + (t % h);
+                const int l = flip ? (i ^ (j - 1)) : (i + h);
+                const ulonglong2 x = sm[i], y = sm[l];
+                if (rec_less(y, x)) {
+                    sm[i] = y;
+                    sm[l] = x;
+                }
             }
-            flags[q] = mn != mx;
-            kr[2 * q] = mn;
-            kr[2 * q + 1] = mx;
+            __syncthreads();
         }
+}
+
+// merge sorted A[0, na) and B[0, nb) into C: each thread its slice of the
+// output (merge path)
+__device__ void block_merge(const ulonglong2 *A, i64 na, const ulonglong2 *B, i64 nb, ulonglong2 *C) {
+    const i64 tot = na + nb, per = (tot + HUGE_NT - 1) / HUGE_NT;
+    const i64 d0 = min(tot, (i64)threadIdx.x * per), d1 = min(tot, d0 + per);
+    if (d0 >= d1) return;
+    // first diagonal split: i in [max(0, d0 - nb), min(d0, na)] with A[i-1] <= B[d0-i] < ...
+    i64 lo = d0 > nb ? d0 - nb : 0, hi = d0 < na ? d0 : na;
+    while (lo < hi) {
+        const i64 i = (lo + hi) >> 1;
+        if (A[i].x <= B[d0 - i - 1].x) lo = i + 1;
+        else hi = i;
+    }
+    i64 i = lo, j = d0 - lo;
+    for (i64 d = d0; d < d1; ++d) {
+        if (j >= nb || (i < na && A[i].x <= B[j].x)) C[d] = A[i++];
+        else C[d] = B[j++];
+    }
+}
+
+__global__ void __launch_bounds__(HUGE_NT, 1) k_lsj_huge(SubBuckets sub, const i64 *list,
+                                                         const unsigned long long *nlist, ulonglong2 *B,
+                                                         ulonglong2 *out) {
+    extern __shared__ __align__(16) ulonglong2 hsm[];
+    const i64 nh = (i64)*nlist;
+    for (i64 q = blockIdx.x; q < nh; q += gridDim.x) {
+        const Bucket bk = sub.get(list[q]);
+        const i64 a = bk.in_base, len = bk.m;
+        // sorted chunks -> out
+        for (i64 c0 = 0; c0 < len; c0 += HUGE_CH) {
+            const int cl = (int)min((i64)HUGE_CH, len - c0);
+            for (int i = threadIdx.x; i < cl; i += HUGE_NT) hsm[i] = B[a + c0 + i];
+            __syncthreads();
+            huge_chunk_sort(hsm, cl);
+            for (int i = threadIdx.x; i < cl; i += HUGE_NT) out[bk.out_base + c0 + i] = hsm[i];
+            __syncthreads();
+        }
+        // merge passes: out -> B -> out ...
+        ulonglong2 *src = out + bk.out_base, *dst = B + a;
+        for (i64 wdt = HUGE_CH; wdt < len; wdt <<= 1) {
+            for (i64 m0 = 0; m0 < len; m0 += 2 * wdt) {
+                const i64 na = min(wdt, len - m0), nb = min(wdt, max((i64)0, len - m0 - wdt));
+                block_merge(src + m0, na, src + m0 + na, nb, dst + m0);
+            }
+            __syncthreads();
+            ulonglong2 *t = src;
+            src = dst;
+            dst = t;
+        }
+        if (src != out + bk.out_base)
+            for (i64 i = threadIdx.x; i < len; i += HUGE_NT) out[bk.out_base + i] = src[i];
         __syncthreads();
     }
 }
 
-// one repeated key: already sorted, copy through
-__global__ void k_big_copy(const ulonglong2 *B, const i64 *big, const i64 *boff, int nbig, i64 total,
-                           const int *flags, ulonglong2 *out) {
-    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < total; t += (i64)gridDim.x * blockDim.x) {
-        const int q = find_big(boff, nbig, t);
-        if (flags[q]) continue;
-        const i64 i = big[2 * q] + (t - boff[q]);
-        out[i] = B[i];
-    }
-}
-
-// flattened segments (pos[j], cum[j+1]-cum[j]) of B <-> compact SoA columns
-__device__ __forceinline__ int find_seg(const i64 *cum, int nseg, i64 t) {
-    int lo = 0, hi = nseg;
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (cum[mid] <= t) lo = mid; else hi = mid;
-    }
-    return lo;
-}
-
-// keys enter the segmented sort relative to their segment's minimum (base),
-// so only the bits that vary inside a segment are sorted
-__global__ void k_seg_gather(const ulonglong2 *B, const i64 *pos, const i64 *cum, const u64 *base, int nseg, i64 total,
-                             u64 *k, u64 *v) {
-    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < total; t += (i64)gridDim.x * blockDim.x) {
-        const int j = find_seg(cum, nseg, t);
-        const ulonglong2 e = B[pos[j] + (t - cum[j])];
-        k[t] = e.x - base[j];
-        v[t] = e.y;
-    }
-}
-
-__global__ void k_seg_scatter(const u64 *k, const u64 *v, const i64 *pos, const i64 *cum, const u64 *base, int nseg,
-                              i64 total, ulonglong2 *out) {
-    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < total; t += (i64)gridDim.x * blockDim.x) {
-        const int j = find_seg(cum, nseg, t);
-        out[pos[j] + (t - cum[j])] = make_ulonglong2(k[t] + base[j], v[t]);
-    }
-}
-
-__global__ void k_deinterleave(const ulonglong2 *p, i64 n, u64 *k, u64 *v) {
-    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
-        ulonglong2 e = p[i];
-        k[i] = e.x;
-        v[i] = e.y;
-    }
-}
-
-__global__ void k_interleave(const u64 *k, const u64 *v, i64 n, ulonglong2 *p) {
-    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
-        p[i] = make_ulonglong2(k[i], v[i]);
+// SortCtl counters of both sort instances -> stats[4] (device): oversized
+// sub-buckets (> CAP), fallbacks, sorted by the big instance, above CAP_BIG
+__global__ void k_sort_stats(const SortCtl *c1, const SortCtl *c2, i64 *stats) {
+    stats[0] = (i64)c1->n_over;
+    stats[1] = (i64)(c1->n_fallback + c2->n_fallback);
+    stats[2] = (i64)c1->n_over - (i64)c2->n_over;
+    stats[3] = (i64)c2->n_over;
 }
 
 // reference bucket bounds at scale P of a sorted relation (for the
 // reference's comparator / partition counters, lsj.py:250-286, 302-305)
 __global__ void k_ref_bounds(RmiDev m, const ulonglong2 *sorted, i64 n, i64 P, i64 *bounds) {
+    m.fix();
     for (i64 c = blockIdx.x * (i64)blockDim.x + threadIdx.x; c <= P; c += (i64)gridDim.x * blockDim.x) {
         i64 lo = 0, hi = n;  // first i with partition_index(key_i, P) >= c
         while (lo < hi) {
@@ -881,6 +890,7 @@ __global__ void k_ref_bounds(RmiDev m, const ulonglong2 *sorted, i64 n, i64 P, i
 // the dependent probes of the searches overlap across the grid.
 __global__ void k_join_bounds(LsjDev mr, const ulonglong2 *__restrict__ R, const i64 *__restrict__ rst,
                               const ulonglong2 *__restrict__ S, i64 ns, i64 ntiles, i64 *tb) {
+    mr.m.fix();
     for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < ntiles; t += (i64)gridDim.x * blockDim.x) {
         const i64 a = t * JOIN_T, e = min(a + (i64)JOIN_T, ns);
         const u64 kf = S[a].x, kl = S[e - 1].x;
@@ -1021,21 +1031,27 @@ __global__ void k_sample(const u64 *keys, i64 n, i64 total, u64 seed, u64 *out) 
 
 static size_t al(size_t v) { return (v + 255) & ~(size_t)255; }
 
+// the big instance: one CTA per SM, 1024 threads, everything of up to
+// CAP_BIG tuples in shared memory
+constexpr int CAP_BIG = (221184 / (8 + 4 * SLOT_X + 6)) / 128 * 128;
+
+template <int CAPV>
 static size_t sort_smem_bytes() {
-    return sizeof(u64) * CAP + sizeof(u32) * SLOT_X * CAP + 3 * sizeof(u16) * CAP;
+    return sizeof(u64) * CAPV + sizeof(u32) * SLOT_X * CAPV + 3 * sizeof(u16) * CAPV;
 }
 
-template <class Src>
-static int launch_sort(const LsjDev &md, const Src &src, const i64 *nb_dev, const ulonglong2 *in, ulonglong2 *out,
-                       SortCtl *ctl, i64 *over, cudaStream_t st) {
+template <class Src, int NT, int CAPV, int CTAS>
+static int launch_sort(const LsjDev &md, const Src &src, const unsigned long long *nb_dev, const ulonglong2 *in,
+                       ulonglong2 *out, SortCtl *ctl, i64 *over, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        LJ_CK(cudaFuncSetAttribute(k_lsj_sort<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)sort_smem_bytes()));
+        LJ_CK(cudaFuncSetAttribute(k_lsj_sort<Src, NT, CAPV, CTAS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)sort_smem_bytes<CAPV>()));
         attr = true;
     }
     LJ_CK(cudaMemsetAsync(ctl, 0, sizeof(SortCtl), st));
-    k_lsj_sort<Src><<<sm_count() * SORT_CTAS, SORT_NT, sort_smem_bytes(), st>>>(md, src, nb_dev, in, out, ctl, over);
+    k_lsj_sort<Src, NT, CAPV, CTAS><<<sm_count() * CTAS, NT, sort_smem_bytes<CAPV>(), st>>>(md, src, nb_dev, in, out,
+                                                                                          ctl, over);
     LJ_CK_LAUNCH();
     return LJ_OK;
 }
@@ -1248,43 +1264,39 @@ static size_t mat_scan_bytes(i64 items) {
     return t;
 }
 
+// Everything lives in the caller's workspace and every step is enqueued on
+// the stream: the split's slot x chunk matrix is scanned at its bound (no
+// readback of its size), the oversized sub-buckets go from the main sort to
+// the big instance and then to k_lsj_huge through device-side lists.
 size_t lj_lsj_sort_workspace_bytes(int64_t n, int64_t nbins) {
     const i64 G = max_subs(n, nbins), nbig = n / CAP + 2, M = max_mat(n, nbins);
-    size_t t = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, t, (const u64 *)nullptr, (u64 *)nullptr, (const u64 *)nullptr,
-                                    (u64 *)nullptr, (int64_t)n);
-    size_t tseg = 0;
-    cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tseg, (const u64 *)nullptr, (u64 *)nullptr,
-                                             (const u64 *)nullptr, (u64 *)nullptr, (int)(n < INT32_MAX ? n : INT32_MAX),
-                                             (int)nbig, (const i64 *)nullptr, (const i64 *)nullptr, 0, 64);
-    if (tseg > t) t = tseg;
     size_t sc = scan_i64_bytes(nbins + 1);
     const size_t ms = mat_scan_bytes(M);
     if (ms > sc) sc = ms;
-    return al(sizeof(SortCtl)) + 2 * al(sizeof(i64) * (size_t)(nbins + 1)) +  // ctl, fcount, fbase
-           4 * al(sizeof(i64) * (size_t)(nbins + 1)) +                       // chunks, cbase, matc, mbase
-           al(sizeof(u32) * (size_t)M) + al(sizeof(i64) * (size_t)M) +        // slot x chunk matrix, offsets
-           al(sizeof(ulonglong2) * (size_t)n) +                              // split array
+    return 2 * al(sizeof(SortCtl)) + 2 * al(sizeof(i64) * (size_t)(nbins + 1)) +  // ctls, fcount, fbase
+           4 * al(sizeof(i64) * (size_t)(nbins + 1)) +                           // chunks, cbase, matc, mbase
+           al(sizeof(u32) * (size_t)M) + al(sizeof(i64) * (size_t)M) +            // slot x chunk matrix, offsets
+           al(sizeof(ulonglong2) * (size_t)n) +                                  // split array
            al(sizeof(i64) * (size_t)(G + 1)) + al(sizeof(double2) * (size_t)G) +  // sub starts, y ranges
-           al(sizeof(double) * (size_t)G) +                                  // split values
-           al(sizeof(i64) * (size_t)nbig) + al(sizeof(i64) * 2 * (size_t)nbig) +  // big list, {start, len}
-           al(sizeof(i64) * (size_t)(nbig + 1)) + al(sizeof(int) * (size_t)nbig) +  // offsets, flags
-           al(sizeof(u64) * 2 * (size_t)nbig) + al(sizeof(u64) * (size_t)nbig) +    // key ranges, bases
-           4 * al(sizeof(u64) * (size_t)n) + al(t > sc ? t : sc);
+           al(sizeof(double) * (size_t)G) +                                      // split values
+           2 * al(sizeof(i64) * (size_t)nbig) +                                  // over / huge lists
+           al(sc);
 }
 
 __global__ void k_set_last(const i64 *fbase, int nb, i64 n, i64 *sub_starts) { sub_starts[fbase[nb]] = n; }
 
 int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_out, int64_t n,
-                const int64_t *starts, void *ws, size_t ws_bytes, int64_t *stats_host, void *stream) {
+                const int64_t *starts, void *ws, size_t ws_bytes, int64_t *stats, void *stream) {
     LJ_REQUIRE(md && md->table && md->pb && md->nbins >= 1, "model has no bins");
     if (ws_bytes < lj_lsj_sort_workspace_bytes(n, md->nbins)) {
         set_error("lj_lsj_sort: workspace too small");
         return LJ_E_WORKSPACE;
     }
-    for (int i = 0; i < 4; ++i) stats_host[i] = 0;
-    if (n == 0) return LJ_OK;
     cudaStream_t st = as_stream(stream);
+    if (n == 0) {
+        if (stats) LJ_CK(cudaMemsetAsync(stats, 0, 4 * sizeof(i64), st));
+        return LJ_OK;
+    }
     const i64 nb = md->nbins, G = max_subs(n, nb);
     char *p = (char *)ws;
     auto take = [&](size_t bytes) {
@@ -1293,6 +1305,7 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
         return r;
     };
     SortCtl *ctl = (SortCtl *)take(sizeof(SortCtl));
+    SortCtl *ctl2 = (SortCtl *)take(sizeof(SortCtl));
     i64 *fcount = (i64 *)take(sizeof(i64) * (size_t)(nb + 1));
     i64 *fbase = (i64 *)take(sizeof(i64) * (size_t)(nb + 1));
     i64 *chunks = (i64 *)take(sizeof(i64) * (size_t)(nb + 1));
@@ -1307,16 +1320,8 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
     double2 *sub_y = (double2 *)take(sizeof(double2) * (size_t)G);
     u64 *spv = (u64 *)take(sizeof(u64) * (size_t)G);
     const i64 nbig_cap = n / CAP + 2;
-    i64 *biglist = (i64 *)take(sizeof(i64) * (size_t)nbig_cap);
-    i64 *big = (i64 *)take(sizeof(i64) * 2 * (size_t)nbig_cap);
-    i64 *boff = (i64 *)take(sizeof(i64) * (size_t)(nbig_cap + 1));
-    int *flags = (int *)take(sizeof(int) * (size_t)nbig_cap);
-    unsigned long long *krange = (unsigned long long *)take(sizeof(u64) * 2 * (size_t)nbig_cap);
-    u64 *sbase = (u64 *)take(sizeof(u64) * (size_t)nbig_cap);
-    u64 *k1 = (u64 *)take(sizeof(u64) * (size_t)n);
-    u64 *v1 = (u64 *)take(sizeof(u64) * (size_t)n);
-    u64 *k2 = (u64 *)take(sizeof(u64) * (size_t)n);
-    u64 *v2 = (u64 *)take(sizeof(u64) * (size_t)n);
+    i64 *overlist = (i64 *)take(sizeof(i64) * (size_t)nbig_cap);
+    i64 *hugelist = (i64 *)take(sizeof(i64) * (size_t)nbig_cap);
     char *cub_tmp = p;
 
     const LsjDev dev = make_lsj(*md);
@@ -1329,12 +1334,9 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
     size_t t = scan_i64_bytes(nb + 1);
     LJ_CK(cub::DeviceScan::ExclusiveSum(cub_tmp, t, fcount, fbase, (int64_t)(nb + 1), st));
     if (points) {
-        // sample bins precomputed into k1 (free until the oversized pass) when
-        // they fit, else evaluated inside the searches
-        u32 *sbin = dev.nsample <= 2 * n ? reinterpret_cast<u32 *>(k1) : nullptr;
-        if (sbin) k_sample_bins<<<grid_for(dev.nsample, 256, 8), 256, 0, st>>>(dev, sbin);
-        // chunks / matc are free until k_chunk_plan: the bins' sample ranges
-        k_split_ranges<<<(int)((nb + 63) / 64), 64, 0, st>>>(dev, sbin, (int)nb, chunks, matc);
+        // the bins' sample ranges go through chunks / matc (free until
+        // k_chunk_plan); sample bins evaluated inside the searches
+        k_split_ranges<<<(int)((nb + 63) / 64), 64, 0, st>>>(dev, nullptr, (int)nb, chunks, matc);
         k_split_points<<<grid_for(max_subs(n, nb), 256, 8), 256, 0, st>>>(dev, starts, fbase, (int)nb, chunks, matc,
                                                                          spv);
         LJ_CK_LAUNCH();
@@ -1343,23 +1345,16 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
     LJ_CK_LAUNCH();
     LJ_CK(cub::DeviceScan::ExclusiveSum(cub_tmp, t, chunks, cbase, (int64_t)(nb + 1), st));
     LJ_CK(cub::DeviceScan::ExclusiveSum(cub_tmp, t, matc, mbase, (int64_t)(nb + 1), st));
-    i64 CM[2];
-    LJ_CK(cudaMemcpyAsync(&CM[0], cbase + nb, sizeof(i64), cudaMemcpyDeviceToHost, st));
-    LJ_CK(cudaMemcpyAsync(&CM[1], mbase + nb, sizeof(i64), cudaMemcpyDeviceToHost, st));
-    LJ_CK(cudaStreamSynchronize(st));
-    const i64 M = CM[1];
-    if (M > Mcap) {
-        set_error("lj_lsj_sort: slot x chunk matrix exceeds its bound");
-        return LJ_E_WORKSPACE;
-    }
     const SplitCtx cx{starts, fbase, cbase, mbase, spv, (int)nb};
     LJ_CK(cudaMemsetAsync(ctl, 0, sizeof(SortCtl), st));
     k_split_count<<<sm_count() * 2, SPLIT_NT, 0, st>>>(dev, cx, A, cbase + nb, mat, ctl);
     LJ_CK_LAUNCH();
     {
-        size_t tm = mat_scan_bytes(M);
+        // the matrix holds mbase[nb] <= Mcap entries: scanning the bound is
+        // exact for every used entry (the tail is never read)
+        size_t tm = mat_scan_bytes(Mcap);
         cub::TransformInputIterator<i64, CastU32I64, const u32 *> it(mat, CastU32I64());
-        LJ_CK(cub::DeviceScan::ExclusiveSum(cub_tmp, tm, it, moff, (int64_t)M, st));
+        LJ_CK(cub::DeviceScan::ExclusiveSum(cub_tmp, tm, it, moff, (int64_t)Mcap, st));
     }
     k_split_slots<<<grid_for(G + 1, 256, 8), 256, 0, st>>>(dev, cx, moff, n, sub_starts, sub_y);
     LJ_CK_LAUNCH();
@@ -1368,90 +1363,26 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
     LJ_CK_LAUNCH();
     // K8 over the sub-buckets, B -> out (G = fbase[nb] read on device)
     SubBuckets sb{sub_starts, sub_y};
-    int rc = launch_sort(dev, sb, fbase + nb, B, out, ctl, biglist, st);
+    int rc = launch_sort<SubBuckets, SORT_NT, CAP, SORT_CTAS>(
+        dev, sb, reinterpret_cast<const unsigned long long *>(fbase + nb), B, out, ctl, overlist, st);
     if (rc) return rc;
-    SortCtl h;
-    LJ_CK(cudaMemcpyAsync(&h, ctl, sizeof(SortCtl), cudaMemcpyDeviceToHost, st));
-    LJ_CK(cudaStreamSynchronize(st));
-    stats_host[1] = (int64_t)h.n_fallback;
-    const int nbig = (int)h.n_over;
-    stats_host[0] = nbig;
-    if (nbig == 0) return LJ_OK;
-    // sub-buckets above shared memory: one repeated key (a hot duplicate's
-    // point slice) -> already sorted, copied through over the flattened
-    // list; otherwise (rare) a device radix sort of that sub-bucket
-    k_big_list<<<(nbig + 255) / 256, 256, 0, st>>>(biglist, nbig, sub_starts, big);
+    // the big instance over the oversized list (count on device)
+    OverBuckets ob{overlist, sb};
+    rc = launch_sort<OverBuckets, 1024, CAP_BIG, 1>(dev, ob, &ctl->n_over, B, out, ctl2, hugelist, st);
+    if (rc) return rc;
+    // above CAP_BIG: chunk sort + merge passes in global memory
+    static bool hattr = false;
+    if (!hattr) {
+        LJ_CK(cudaFuncSetAttribute(k_lsj_huge, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(HUGE_CH * sizeof(ulonglong2))));
+        hattr = true;
+    }
+    k_lsj_huge<<<sm_count(), HUGE_NT, HUGE_CH * sizeof(ulonglong2), st>>>(sb, hugelist, &ctl2->n_over, B, out);
     LJ_CK_LAUNCH();
-    std::vector<i64> hbig(2 * (size_t)nbig), hoff(nbig + 1);
-    LJ_CK(cudaMemcpyAsync(hbig.data(), big, sizeof(i64) * 2 * nbig, cudaMemcpyDeviceToHost, st));
-    LJ_CK(cudaStreamSynchronize(st));
-    i64 total = 0;
-    for (int q = 0; q < nbig; ++q) {
-        hoff[q] = total;
-        total += hbig[2 * q + 1];
-    }
-    hoff[nbig] = total;
-    LJ_CK(cudaMemcpyAsync(boff, hoff.data(), sizeof(i64) * (nbig + 1), cudaMemcpyHostToDevice, st));
-    k_big_scan<<<nbig < 65535 ? nbig : 65535, 256, 0, st>>>(B, big, nbig, flags, krange);
-    k_big_copy<<<grid_for(total, 256, 8), 256, 0, st>>>(B, big, boff, nbig, total, flags, out);
-    LJ_CK_LAUNCH();
-    std::vector<int> hf(nbig);
-    std::vector<u64> hkr(2 * (size_t)nbig);
-    LJ_CK(cudaMemcpyAsync(hf.data(), flags, sizeof(int) * nbig, cudaMemcpyDeviceToHost, st));
-    LJ_CK(cudaMemcpyAsync(hkr.data(), krange, sizeof(u64) * 2 * nbig, cudaMemcpyDeviceToHost, st));
-    LJ_CK(cudaStreamSynchronize(st));
-    // the mixed ones: those above 2^16 tuples each get a device radix sort;
-    // all smaller ones ONE segmented radix sort (block per segment): gather
-    // -> sort -> scatter back, instead of a device sort per sub-bucket
-    std::vector<i64> spos, scum(1, 0);
-    std::vector<u64> sbh;
-    int nsorted = 0, span_bits = 0;
-    i64 mx = 0;
-    for (int q = 0; q < nbig; ++q) {
-        if (!hf[q]) continue;
-        ++nsorted;
-        const i64 a = hbig[2 * q], len = hbig[2 * q + 1];
-        mx = std::max(mx, len);
-        if (len <= 65536) {
-            spos.push_back(a);
-            scum.push_back(scum.back() + len);
-            sbh.push_back(hkr[2 * q]);
-            int b = 0;
-            for (u64 d = hkr[2 * q + 1] - hkr[2 * q]; d; d >>= 1) ++b;
-            span_bits = std::max(span_bits, b);
-            continue;
-        }
-        k_deinterleave<<<grid_for(len, 256, 8), 256, 0, st>>>(B + a, len, k1, v1);
-        size_t tt = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, tt, k1, k2, v1, v2, (int64_t)len);
-        LJ_CK(cub::DeviceRadixSort::SortPairs(cub_tmp, tt, k1, k2, v1, v2, (int64_t)len, 0, 64, st));
-        k_interleave<<<grid_for(len, 256, 8), 256, 0, st>>>(k2, v2, len, out + a);
+    if (stats) {
+        k_sort_stats<<<1, 1, 0, st>>>(ctl, ctl2, stats);
         LJ_CK_LAUNCH();
     }
-    stats_host[2] = nsorted;
-    stats_host[3] = mx;
-    const int nseg = (int)spos.size();
-    if (nseg) {
-        const i64 T = scum.back();
-        i64 *d_pos = big;  // reuse: 2 * nbig_cap words >= 2 * nseg + 1
-        i64 *d_cum = big + nseg;
-        LJ_CK(cudaMemcpyAsync(d_pos, spos.data(), sizeof(i64) * nseg, cudaMemcpyHostToDevice, st));
-        LJ_CK(cudaMemcpyAsync(d_cum, scum.data(), sizeof(i64) * (nseg + 1), cudaMemcpyHostToDevice, st));
-        LJ_CK(cudaMemcpyAsync(sbase, sbh.data(), sizeof(u64) * nseg, cudaMemcpyHostToDevice, st));
-        k_seg_gather<<<grid_for(T, 256, 8), 256, 0, st>>>(B, d_pos, d_cum, sbase, nseg, T, k1, v1);
-        LJ_CK_LAUNCH();
-        // only the low span_bits bits differ inside a segment (stable LSD
-        // radix over them == the full sort)
-        const int eb = span_bits < 1 ? 1 : span_bits;
-        size_t tt = 0;
-        cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tt, k1, k2, v1, v2, (int)T, nseg, d_cum, d_cum + 1, 0, eb,
-                                                 st);
-        LJ_CK(cub::DeviceSegmentedRadixSort::SortPairs(cub_tmp, tt, k1, k2, v1, v2, (int)T, nseg, d_cum, d_cum + 1,
-                                                       0, eb, st));
-        k_seg_scatter<<<grid_for(T, 256, 8), 256, 0, st>>>(k2, v2, d_pos, d_cum, sbase, nseg, T, out);
-        LJ_CK_LAUNCH();
-    }
-    LJ_CK(cudaStreamSynchronize(st));
     return LJ_OK;
 }
 
@@ -1494,6 +1425,155 @@ int lj_lsj_join(const LjLsjModel *model_r, const uint64_t *r_pairs, int64_t nr, 
     k_lsj_join<<<g, JOIN_NT, 0, st>>>(R, S, ns, tb, mode, counts, offsets, out_pr, out_ps, out);
     LJ_CK_LAUNCH();
     return LJ_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------ one-call LSJ
+
+namespace lj {
+
+// {min, max} of the keys (unsigned), one block: the two-key "sample" of a
+// relation too small for sample_rate (lsj.py zero-sample fallback)
+__global__ void k_minmax2(const u64 *keys, i64 n, u64 *out) {
+    __shared__ u64 smin[1024], smax[1024];
+    u64 lo = ~0ULL, hi = 0;
+    for (i64 i = threadIdx.x; i < n; i += blockDim.x) {
+        const u64 k = keys[i];
+        lo = k < lo ? k : lo;
+        hi = k > hi ? k : hi;
+    }
+    smin[threadIdx.x] = lo;
+    smax[threadIdx.x] = hi;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) {
+            smin[threadIdx.x] = smin[threadIdx.x + o] < smin[threadIdx.x] ? smin[threadIdx.x + o] : smin[threadIdx.x];
+            smax[threadIdx.x] = smax[threadIdx.x + o] > smax[threadIdx.x] ? smax[threadIdx.x + o] : smax[threadIdx.x];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        out[0] = smin[0];
+        out[1] = smax[0];
+    }
+}
+
+// per-relation layout of lj_lsj_run's workspace
+struct LsjRunRel {
+    i64 n, total, tl, fanout, nbins;
+};
+
+static LsjRunRel run_rel(i64 n, double rate) {
+    LsjRunRel r;
+    r.n = n;
+    r.total = (i64)nearbyint(rate * (double)n);  // Python round(): half to even
+    r.tl = r.total > 0 ? r.total : 2;
+    r.fanout = r.total > 0 ? std::min<i64>(1000, std::max<i64>(1, r.total / 8)) : 1;
+    r.nbins = std::max<i64>(1, std::min<i64>(2048, (n + 8191) / 8192));  // lsj.default_bins
+    return r;
+}
+
+// bytes that stay live until the join (model, bins, partitioned and sorted pairs)
+static size_t run_keep_bytes(const LsjRunRel &r) {
+    return al(sizeof(u64) * (size_t)r.tl) + al(sizeof(double) * 2) + al(sizeof(LjLeaf) * (size_t)r.fanout) +
+           al(sizeof(i64) * 2 * (size_t)r.fanout) + al(sizeof(i64) * (size_t)(r.nbins + 1)) +
+           al(sizeof(u32) * (size_t)r.tl) + 2 * al(sizeof(ulonglong2) * (size_t)r.n) +
+           al(sizeof(i64) * (size_t)(r.nbins + 1));
+}
+
+static size_t run_scratch_bytes(const LsjRunRel &r) {
+    size_t s = lj_lsj_sample_workspace_bytes(std::max<i64>(r.total, 1));
+    s = std::max(s, lj_rmi_fit_workspace_bytes(r.tl, r.fanout));
+    s = std::max(s, lj_lsj_bins_workspace_bytes(r.tl));
+    s = std::max(s, lj_lsj_partition_workspace_bytes(r.n, r.nbins));
+    s = std::max(s, lj_lsj_sort_workspace_bytes(r.n, r.nbins));
+    return al(s);
+}
+
+}  // namespace lj
+
+extern "C" {
+
+size_t lj_lsj_run_workspace_bytes(int64_t nr, int64_t ns, double sample_rate) {
+    const LsjRunRel a = run_rel(nr, sample_rate), b = run_rel(ns, sample_rate);
+    return run_keep_bytes(a) + run_keep_bytes(b) + std::max(run_scratch_bytes(a), run_scratch_bytes(b)) +
+           al(lj_lsj_join_workspace_bytes(ns)) + 1024;
+}
+
+int lj_lsj_run(const uint64_t *rk, const uint64_t *rp, int64_t nr, const uint64_t *sk, const uint64_t *sp, int64_t ns,
+               double sample_rate, uint64_t seed, uint64_t *out, void *ws, size_t ws_bytes, void *stream) {
+    LJ_REQUIRE(sample_rate > 0.0 && sample_rate <= 1.0, "sample_rate must be in (0, 1]");
+    LJ_REQUIRE(nr >= 0 && ns >= 0, "sizes must be >= 0");
+    cudaStream_t st = as_stream(stream);
+    LJ_CK(cudaMemsetAsync(out, 0, 4 * sizeof(u64), st));
+    if (nr == 0 || ns == 0) return LJ_OK;
+    if (ws_bytes < lj_lsj_run_workspace_bytes(nr, ns, sample_rate)) {
+        set_error("lj_lsj_run: workspace too small");
+        return LJ_E_WORKSPACE;
+    }
+    char *p = (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+    auto take = [&](size_t bytes) {
+        char *r = p;
+        p += al(bytes);
+        return r;
+    };
+    const LsjRunRel rel[2] = {run_rel(nr, sample_rate), run_rel(ns, sample_rate)};
+    const uint64_t *keys[2] = {rk, sk}, *pays[2] = {rp, sp};
+    const u64 seeds[2] = {seed, seed ^ 0x5DEECE66DULL};  // lsj.py:388-391: S's model seed
+    LjRmi rmi[2];
+    LjLsjModel md[2];
+    u64 *sbuf[2], *pairs[2];
+    double *root[2];
+    LjLeaf *leaves[2];
+    i64 *err[2], *pb[2], *starts[2];
+    u32 *table[2];
+    ulonglong2 *sorted[2];
+    for (int x = 0; x < 2; ++x) {
+        const LsjRunRel &r = rel[x];
+        sbuf[x] = (u64 *)take(sizeof(u64) * (size_t)r.tl);
+        root[x] = (double *)take(sizeof(double) * 2);
+        leaves[x] = (LjLeaf *)take(sizeof(LjLeaf) * (size_t)r.fanout);
+        err[x] = (i64 *)take(sizeof(i64) * 2 * (size_t)r.fanout);
+        pb[x] = (i64 *)take(sizeof(i64) * (size_t)(r.nbins + 1));
+        table[x] = (u32 *)take(sizeof(u32) * (size_t)r.tl);
+        pairs[x] = (u64 *)take(sizeof(ulonglong2) * (size_t)r.n);
+        sorted[x] = (ulonglong2 *)take(sizeof(ulonglong2) * (size_t)r.n);
+        starts[x] = (i64 *)take(sizeof(i64) * (size_t)(r.nbins + 1));
+        // the root stays on the device (root_dev): nothing is read back
+        rmi[x] = LjRmi{0.0, 0.0, r.fanout, r.tl, leaves[x], err[x], root[x]};
+        md[x] = LjLsjModel{rmi[x], r.nbins, pb[x], table[x], r.total > 0 ? sbuf[x] : nullptr, r.total > 0 ? r.tl : 0};
+    }
+    char *scratch = p;
+    const size_t sb = std::max(run_scratch_bytes(rel[0]), run_scratch_bytes(rel[1]));
+    p += sb;
+    char *join_ws = take(lj_lsj_join_workspace_bytes(ns));
+    for (int x = 0; x < 2; ++x) {
+        const LsjRunRel &r = rel[x];
+        int rc;
+        // smpl: stratified sample (or {min, max}), RMI fit, equi-depth bins
+        if (r.total > 0) {
+            rc = lj_lsj_sample(keys[x], r.n, r.total, seeds[x], sbuf[x], scratch, sb, stream);
+            if (rc) return rc;
+        } else {
+            k_minmax2<<<1, 1024, 0, st>>>(keys[x], r.n, sbuf[x]);
+            LJ_CK_LAUNCH();
+        }
+        rc = lj_rmi_fit(sbuf[x], r.tl, r.fanout, root[x], leaves[x], err[x], scratch, sb, stream);
+        if (rc) return rc;
+        rc = lj_lsj_bins(&rmi[x], sbuf[x], r.tl, r.nbins, pb[x], table[x], scratch, sb, stream);
+        if (rc) return rc;
+        // part + sort (K6/K7, split, K8)
+        rc = lj_lsj_partition(&md[x], keys[x], pays[x], r.n, pairs[x], starts[x], scratch, sb, stream);
+        if (rc) return rc;
+        rc = lj_lsj_sort(&md[x], pairs[x], reinterpret_cast<u64 *>(sorted[x]), r.n, starts[x], scratch, sb, nullptr,
+                         stream);
+        if (rc) return rc;
+    }
+    // join (K9): S's tiles against R's windows through R's model
+    return lj_lsj_join(&md[0], reinterpret_cast<const u64 *>(sorted[0]), nr, starts[0],
+                       reinterpret_cast<const u64 *>(sorted[1]), ns, 0, nullptr, nullptr, nullptr, nullptr, out, 0,
+                       join_ws, lj_lsj_join_workspace_bytes(ns), stream);
 }
 
 }  // extern "C"

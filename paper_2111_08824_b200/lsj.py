@@ -256,17 +256,28 @@ def _partition(keys, payloads, lm: LsjModel):
     return pairs, starts
 
 
+SORT_DIAG = ("oversized_sub_buckets", "bitonic_fallbacks", "big_sorted_sub_buckets", "global_sorted_sub_buckets")
+
+
 def _sort(pairs_in, starts, lm: LsjModel, n: int):
+    """K8 (asynchronous): -> (sorted pairs, device int64[4] sort counters;
+    see SORT_DIAG and ``sort_diag``)."""
     lib = _lib.lib()
     out = torch.empty_like(pairs_in)
     ws = _lib.workspace(lib.lj_lsj_sort_workspace_bytes(n, lm.nbins), pairs_in.device)
-    st = (ctypes.c_int64 * 4)()
+    st = torch.zeros(4, dtype=torch.int64, device=pairs_in.device)
     c = lm.c_struct()
     _lib.check(lib.lj_lsj_sort(ctypes.byref(c), _lib.ptr(pairs_in), _lib.ptr(out), n, _lib.ptr(starts),
-                               _lib.ptr(ws), ws.numel(), st, _lib.stream_ptr()), "lsj_sort")
-    diag = {"oversized_sub_buckets": int(st[0]), "bitonic_fallbacks": int(st[1]),
-            "radix_sorted_sub_buckets": int(st[2]), "largest_radix_sorted": int(st[3])}
-    return out, diag
+                               _lib.ptr(ws), ws.numel(), _lib.ptr(st), _lib.stream_ptr()), "lsj_sort")
+    return out, st
+
+
+def sort_diag(st) -> dict:
+    """The sort counters as a dict (reads the device words)."""
+    if isinstance(st, dict):
+        return st
+    v = st.cpu().tolist() if isinstance(st, torch.Tensor) else [0, 0, 0, 0]
+    return dict(zip(SORT_DIAG, (int(x) for x in v)))
 
 
 def sort_relation(keys, payloads, model, scale: int, workers: int = 1) -> SortedRelation:
@@ -396,29 +407,25 @@ def lsj_join(r: Relation, s: Relation, config: LsjConfig | None = None, material
     if counters:
         br.sort_stats = SortStats().merge(_sort_stats(r_sorted.bucket_bounds)).merge(
             _sort_stats(s_sorted.bucket_bounds))
-    br.extra = {"bins_r": lr.nbins, "bins_s": ls.nbins, **{f"r_{k}": v for k, v in dr.items()},
-                **{f"s_{k}": v for k, v in ds.items()}}
+    if counters:
+        br.extra = {"bins_r": lr.nbins, "bins_s": ls.nbins, **{f"r_{k}": v for k, v in sort_diag(dr).items()},
+                    **{f"s_{k}": v for k, v in sort_diag(ds).items()}}
     return result, br
 
 
-@dataclass(frozen=True)
-class LsjCostParams:
-    """lsj.py:408-430 inputs of the per-worker cost estimate (analysis only)."""
-
-    n_r: int
-    n_s: int
-    s_r: int = 0
-    s_s: int = 0
-    p_r: int = 1
-    p_s: int = 1
-    o_r: int = 0
-    o_s: int = 0
-    workers: int = 1
-
-    def __post_init__(self):
-        if self.workers < 1:
-            raise ValueError("workers must be >= 1")
-        if self.p_r < self.workers or self.p_s < self.workers:
-            raise ValueError("partition counts must be >= workers")
-        if not (0 <= self.o_r <= self.workers and 0 <= self.o_s <= self.workers):
-            raise ValueError("overlap counts must be within [0, workers]")
+def lsj_run(r: Relation, s: Relation, config: LsjConfig | None = None) -> JoinResult:
+    """lsj_join in ONE asynchronous C call (lj_lsj_run): sample, fit, bins,
+    partition, sort and merge-join of both relations from one workspace,
+    the root of each model kept on the device.  -> JoinResult of the
+    device words (the same checksum as ``lsj_join``)."""
+    config = config or LsjConfig()
+    dev = s.keys.device if len(s) else r.keys.device
+    out = torch.zeros(4, dtype=torch.int64, device=dev)
+    if len(r) == 0 or len(s) == 0:
+        return JoinResult(words=out)
+    lib = _lib.lib()
+    ws = _lib.workspace(lib.lj_lsj_run_workspace_bytes(len(r), len(s), float(config.sample_rate)), dev)
+    _lib.check(lib.lj_lsj_run(_lib.ptr(r.keys), _lib.ptr(r.payloads), len(r), _lib.ptr(s.keys), _lib.ptr(s.payloads),
+                              len(s), float(config.sample_rate), int(config.seed) & (2**64 - 1), _lib.ptr(out),
+                              _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "lsj_run")
+    return JoinResult(words=out)

@@ -751,3 +751,63 @@ def test_spline_hash_zero_payloads_keep_the_chains(lj):
     want = oracle.smj_checksum(*r.numpy(), *s.numpy())
     g = idx.join_checksum_buffered(s.keys, s.payloads).cpu().tolist()
     assert (g[0], g[1] & MASK, g[2] & MASK) == want
+
+
+@pytest.mark.parametrize("n", [2000, 9000, 50000])
+def test_lsj_sort_flat_model_big_and_global_paths(lj, n):
+    """A flat model (fitted on one key: slope 0, every y equal) puts every
+    key of a relation into one mixed slice: n = 9000 goes to the big sort
+    instance (one CTA per SM), n = 50000 to the global-memory chunk sort +
+    merge (k_lsj_huge) -- all device-driven, no host readback.  Sorted,
+    pairs kept, and the counters say which path ran."""
+    from paper_2111_08824_b200.lsj import LsjModel, sort_diag, sort_relation
+
+    rng = np.random.default_rng(n)
+    keys = rng.integers(0, 2**63, n, dtype=np.uint64)
+    keys[: n // 10] = keys[n // 10]  # duplicates inside the slice
+    pays = rng.integers(1, 2**63, n, dtype=np.uint64)
+    r = lj.Relation(keys, pays)
+    rmi = lj.RecursiveModelIndex(1).fit(np.array([12345], np.uint64))
+    srt = sort_relation(r.keys, r.payloads, LsjModel.uniform(rmi, 1), 1)
+    k = _np(srt.keys.contiguous())
+    p = _np(srt.payloads.contiguous())
+    assert np.all(k[:-1] <= k[1:])
+    assert sorted(zip(k.tolist(), p.tolist())) == sorted(zip(keys.tolist(), pays.tolist()))
+    d = sort_diag(srt.diag)
+    if n > 3072:
+        assert d["oversized_sub_buckets"] >= 1
+    if n > 12288:
+        assert d["global_sorted_sub_buckets"] >= 1
+
+
+def _lsj_sets():
+    from paper_2111_08824_b200 import configs
+
+    rng = np.random.default_rng(17)
+    c4 = configs.config4(scale=8)
+    c5 = configs.config5(scale=12)
+    tiny_r = np.array([3, 9, 9, 2**63 + 1, 40], np.uint64)
+    tiny_s = np.array([9, 40, 41, 2**63 + 1, 2**63 + 1, 3], np.uint64)
+    zr = np.unique(rng.integers(0, 2**44, 100000, dtype=np.uint64))
+    zs = zr[np.minimum(rng.zipf(1.3, 300000), zr.size) - 1]
+    return {"c4": (c4.r, c4.s), "c5": (c5.r, c5.s),
+            "tiny": (lj_mod().make_relation(tiny_r, 1), lj_mod().make_relation(tiny_s, 2)),
+            "zipf": (lj_mod().make_relation(zr, 3), lj_mod().make_relation(zs, 4))}
+
+
+def lj_mod():
+    import paper_2111_08824_b200 as lj
+
+    return lj
+
+
+@pytest.mark.parametrize("name", ["c4", "c5", "tiny", "zipf"])
+def test_lsj_run_one_call_abi_equals_lsj_join_and_oracle(lj, name):
+    """lj_lsj_run (the whole LSJ in one asynchronous C call, one workspace)
+    through ctypes == lsj_join (Python orchestration) == the oracle."""
+    r, s = _lsj_sets()[name]
+    want = oracle.smj_checksum(*r.numpy(), *s.numpy())
+    cfg = lj.LsjConfig(fanout=4096, sample_rate=0.01)
+    got = lj.lsj_run(r, s, cfg).checksum
+    res, _ = lj.lsj_join(r, s, cfg)
+    assert got == tuple(want) == res.checksum
