@@ -823,7 +823,9 @@ __device__ void block_merge(const ulonglong2 *A, i64 na, const ulonglong2 *B, i6
     }
 }
 
-__global__ void __launch_bounds__(HUGE_NT, 1) k_lsj_huge(SubBuckets sub, const i64 *list,
+// list[q] indexes the big instance's bucket space (OverBuckets): the big
+// instance passed on its own bucket numbers
+__global__ void __launch_bounds__(HUGE_NT, 1) k_lsj_huge(OverBuckets sub, const i64 *list,
                                                          const unsigned long long *nlist, ulonglong2 *B,
                                                          ulonglong2 *out) {
     extern __shared__ __align__(16) ulonglong2 hsm[];
@@ -1377,7 +1379,7 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
                                    (int)(HUGE_CH * sizeof(ulonglong2))));
         hattr = true;
     }
-    k_lsj_huge<<<sm_count(), HUGE_NT, HUGE_CH * sizeof(ulonglong2), st>>>(sb, hugelist, &ctl2->n_over, B, out);
+    k_lsj_huge<<<sm_count(), HUGE_NT, HUGE_CH * sizeof(ulonglong2), st>>>(ob, hugelist, &ctl2->n_over, B, out);
     LJ_CK_LAUNCH();
     if (stats) {
         k_sort_stats<<<1, 1, 0, st>>>(ctl, ctl2, stats);
