@@ -423,6 +423,37 @@ int lj_lsj_join(const LjLsjModel *model_r, const uint64_t *r_pairs, int64_t nr, 
                 uint64_t *out_pr, uint64_t *out_ps, uint64_t *out, int accumulate, void *ws, size_t ws_bytes,
                 void *stream);
 
+/* ---------------------------------------------- multi-GPU (one process)
+ * Single-process calls over ndev devices with one NCCL communicator and one
+ * stream per device (ncclComm_t / cudaStream_t passed as void*); NCCL is
+ * bound at run time (dlopen libnccl.so.2, the copy already loaded in the
+ * process if any).  lj_nccl_available() = 1 if it was found. */
+int lj_nccl_available(void);
+/* ncclCommInitAll over devs (comms[ndev] out) / ncclCommDestroy. */
+int lj_nccl_comm_init_all(int ndev, const int *devs, void **comms);
+int lj_nccl_comm_destroy(void *comm);
+/* The checksum reduction: words[d] = device int64[4]
+ * {count, sum, xor, ...} of device d; afterwards every words[d] holds the
+ * global {count, sum mod 2^64, xor}.  ws[d] >= lj_reduce_sums_workspace_bytes(nranks). */
+size_t lj_reduce_sums_workspace_bytes(int nranks);
+int lj_reduce_sums(int ndev, const int *devs, void *const *comms, void *const *streams, uint64_t *const *words,
+                   void *const *ws);
+/* The distributed learned sort-join (lsj.py:373-405, workers = devices):
+ * R / S shards per device, a shared model on the union of the R samples,
+ * range partition, ncclSend/ncclRecv exchange, lj_lsj_run per device,
+ * lj_reduce_sums.  cap_r / cap_s bound the tuples a device receives (the
+ * workspace is sized by them); recv_counts (host int64[2*ndev] or NULL)
+ * reports what each device received -- LJ_E_WORKSPACE when above the caps.
+ * Reads the partition counts back once (NCCL's exchange sizes are host
+ * values).  out[d] = device int64[4]: the global checksum on every device. */
+size_t lj_lsj_run_multi_workspace_bytes(int ndev, int64_t nr_local, int64_t ns_local, int64_t nr_total,
+                                        int64_t cap_r, int64_t cap_s, double sample_rate);
+int lj_lsj_run_multi(int ndev, const int *devs, void *const *comms, void *const *streams,
+                     const uint64_t *const *r_keys, const uint64_t *const *r_pay, const int64_t *nr,
+                     const uint64_t *const *s_keys, const uint64_t *const *s_pay, const int64_t *ns,
+                     int64_t cap_r, int64_t cap_s, double sample_rate, uint64_t seed, uint64_t *const *out,
+                     void *const *ws, const size_t *ws_bytes, int64_t *recv_counts);
+
 #ifdef __cplusplus
 }
 #endif

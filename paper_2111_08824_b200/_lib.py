@@ -80,6 +80,14 @@ SIGNATURES = {
     "lj_fill_normal": (_int, [_P, _i64, _i64, _u64, _P]),
     "lj_spline_slots_workspace_bytes": (_size_t, [_i64]),
     "lj_lsj_run_workspace_bytes": (_size_t, [_i64, _i64, ctypes.c_double]),
+    "lj_nccl_available": (_int, []),
+    "lj_nccl_comm_init_all": (_int, [_int, _P, _P]),
+    "lj_nccl_comm_destroy": (_int, [_P]),
+    "lj_reduce_sums_workspace_bytes": (_size_t, [_int]),
+    "lj_reduce_sums": (_int, [_int, _P, _P, _P, _P, _P]),
+    "lj_lsj_run_multi_workspace_bytes": (_size_t, [_int, _i64, _i64, _i64, _i64, _i64, ctypes.c_double]),
+    "lj_lsj_run_multi": (_int, [_int, _P, _P, _P, _P, _P, _P, _P, _P, _P, _i64, _i64, ctypes.c_double, _u64, _P, _P,
+                                _P, _P]),
     "lj_lsj_run": (_int, [_P, _P, _i64, _P, _P, _i64, ctypes.c_double, _u64, _P, _P, _size_t, _P]),
     "lj_spline_segments": (_int, [ctypes.POINTER(LjSpline), _P, _P]),
     "lj_spline_slots_plan": (_int, [ctypes.POINTER(LjSpline), _P, _P, _i64, _P, _P, _size_t, _P]),

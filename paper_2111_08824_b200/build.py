@@ -21,7 +21,7 @@ CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
                    "--expt-relaxed-constexpr", "-I", INCLUDE]
-SOURCES = ["lj_core.cu", "lj_grmi.cu", "lj_spline.cu", "lj_hash_staged.cu", "lj_spline_fit.cu", "lj_lsj.cu", "lj_spline_fit.cpp"]
+SOURCES = ["lj_core.cu", "lj_grmi.cu", "lj_spline.cu", "lj_hash_staged.cu", "lj_spline_fit.cu", "lj_lsj.cu", "lj_multi.cu", "lj_spline_fit.cpp"]
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 
 

@@ -42,6 +42,17 @@ int cuda_fail(cudaError_t e, const char *what, const char *file, int line);
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// True the first time it is called for the current device (bit in `mask`):
+// kernel attributes (dynamic shared memory) are set per device.
+inline bool once_per_device(unsigned long long &mask) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ULL << (dev & 63);
+    if (mask & bit) return false;
+    mask |= bit;
+    return true;
+}
+
 // Number of SMs of the current device (cached per process).
 int sm_count();
 // Grid for a grid-stride kernel: enough blocks to fill every SM

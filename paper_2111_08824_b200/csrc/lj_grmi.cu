@@ -984,10 +984,9 @@ static int probe_bucketed(const LjGrmi *idx, const uint64_t *s_pairs, const int6
         LJ_CK(cudaStreamSynchronize(st));
         return lj_grmi_probe_pairs(idx, s_pairs, nk, out, 1, stream);
     }
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;  // one bit per device
+    if (once_per_device(attr)) {
         LJ_CK(cudaFuncSetAttribute(k_grmi_probe_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        attr = true;
     }
     unsigned long long *work = reinterpret_cast<unsigned long long *>(ws);
     LJ_CK(cudaMemsetAsync(work, 0, sizeof(unsigned long long), st));

@@ -582,12 +582,11 @@ int hash_probe_staged(const LjSplineHash &idx, const ulonglong2 *rec, const i64 
         reinterpret_cast<const u16 *>((const char *)meta_ws + (((size_t)nb * sizeof(WinMeta) + 255) & ~(size_t)255));
     const size_t sm = (size_t)HS_D * HS_U * HS_NT * 16 + (size_t)HS_CAP * (8 + sizeof(Seg)) + (HS_NC + 8) * 2 +
                       (size_t)(nb + 2) * 4;
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;  // one bit per device
+    if (once_per_device(attr)) {
         LJ_CK(cudaFuncSetAttribute(k_hash_probe_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)((size_t)HS_D * HS_U * HS_NT * 16 + (size_t)HS_CAP * (8 + sizeof(Seg)) +
                                          (HS_NC + 8) * 2 + (size_t)(HS_MAXWIN + 2) * 4)));
-        attr = true;
     }
     LJ_CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
     k_hash_probe_staged<<<HS_CTAS * sm_count(), HS_NT, sm, st>>>(

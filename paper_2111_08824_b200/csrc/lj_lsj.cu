@@ -1045,11 +1045,10 @@ static size_t sort_smem_bytes() {
 template <class Src, int NT, int CAPV, int CTAS>
 static int launch_sort(const LsjDev &md, const Src &src, const unsigned long long *nb_dev, const ulonglong2 *in,
                        ulonglong2 *out, SortCtl *ctl, i64 *over, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;  // one bit per device
+    if (once_per_device(attr)) {
         LJ_CK(cudaFuncSetAttribute(k_lsj_sort<Src, NT, CAPV, CTAS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)sort_smem_bytes<CAPV>()));
-        attr = true;
     }
     LJ_CK(cudaMemsetAsync(ctl, 0, sizeof(SortCtl), st));
     k_lsj_sort<Src, NT, CAPV, CTAS><<<sm_count() * CTAS, NT, sort_smem_bytes<CAPV>(), st>>>(md, src, nb_dev, in, out,
@@ -1373,11 +1372,10 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
     rc = launch_sort<OverBuckets, 1024, CAP_BIG, 1>(dev, ob, &ctl->n_over, B, out, ctl2, hugelist, st);
     if (rc) return rc;
     // above CAP_BIG: chunk sort + merge passes in global memory
-    static bool hattr = false;
-    if (!hattr) {
+    static unsigned long long hattr = 0;  // one bit per device
+    if (once_per_device(hattr)) {
         LJ_CK(cudaFuncSetAttribute(k_lsj_huge, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)(HUGE_CH * sizeof(ulonglong2))));
-        hattr = true;
     }
     k_lsj_huge<<<sm_count(), HUGE_NT, HUGE_CH * sizeof(ulonglong2), st>>>(ob, hugelist, &ctl2->n_over, B, out);
     LJ_CK_LAUNCH();

@@ -420,13 +420,12 @@ int run_partition(const Src &f, i64 n, int nbins, ulonglong2 *out, i64 *starts, 
     u16 *bins = (u16 *)q;  // pass-1 bins for the pipelined pass 2
     q += part_align(sizeof(u16) * (size_t)n);
     const size_t sm_h = sizeof(u32) * (size_t)nbins * p.hc, sm_s = sizeof(u32) * (size_t)nbins;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static unsigned long long attr_set = 0;  // one bit per device
+    if (once_per_device(attr_set)) {
         LJ_CK(cudaFuncSetAttribute(k_bin_hist<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_SMEM_MAX));
         LJ_CK(cudaFuncSetAttribute(k_bin_scatter<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_SMEM_MAX));
         LJ_CK(cudaFuncSetAttribute(k_bin_hist_tma<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_SMEM_MAX));
         LJ_CK(cudaFuncSetAttribute(k_bin_scatter_tma<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_SMEM_MAX));
-        attr_set = true;
     }
     // bulk-copy rings: 16-B aligned columns, >= 2 stages next to the counters
     static const bool no_tma = getenv("LJ_PART_NO_TMA") != nullptr;

@@ -394,14 +394,13 @@ int run_partition_claims(const Src &f, i64 n, int nbins, int exact, ulonglong2 *
     LJ_CK(cudaMemsetAsync(gcur, 0, sizeof(u32) * (size_t)nbins, st));
     LJ_CK(cudaMemsetAsync(ovf, 0, sizeof(unsigned long long), st));
     const size_t tb = pt_table_bytes(f.f.smem_words());
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;  // one bit per device
+    if (once_per_device(attr)) {
         LJ_CK(cudaFuncSetAttribute(k_bin_scatter_est<Src, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    PT_SMEM_MAX));
         LJ_CK(cudaFuncSetAttribute(k_bin_scatter_est<Src, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    PT_SMEM_MAX));
         LJ_CK(cudaFuncSetAttribute(k_est_sample<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_SMEM_MAX));
-        attr = true;
     }
     const int stride = exact ? 1 : EST_STRIDE;
     const bool stored = exact && codes != nullptr && nbins <= 65536;
@@ -462,12 +461,11 @@ int shuffle_count(const Src &f, i64 n, int nbins, i64 *counts, void *ws, size_t 
     u16 *codes = reinterpret_cast<u16 *>((char *)ws + eb);
     LJ_CK(cudaMemsetAsync(est, 0, sizeof(u32) * (size_t)nbins, st));
     const size_t tb = pt_table_bytes(f.f.smem_words());
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;  // one bit per device
+    if (once_per_device(attr)) {
         LJ_CK(cudaFuncSetAttribute(k_est_sample<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_SMEM_MAX));
         LJ_CK(cudaFuncSetAttribute(k_bin_scatter_est<Src, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    PT_SMEM_MAX));
-        attr = true;
     }
     if (n > 0) {
         k_est_sample<Src><<<grid_for(n, 256, 4), 256, tb + sizeof(u32) * nbins, st>>>(f, n, nbins, 1, est, codes);
@@ -549,12 +547,11 @@ int run_partition_direct(const Src &f, i64 n, int nbins, ulonglong2 *out, i64 *r
         set_error("partition_direct: shared memory too small for the ring");
         return LJ_E_INVALID;
     }
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;  // one bit per device
+    if (once_per_device(attr)) {
         LJ_CK(cudaFuncSetAttribute(k_scatter_direct<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)(fix + nst * stage)));
         LJ_CK(cudaFuncSetAttribute(k_est_sample<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_SMEM_MAX));
-        attr = true;
     }
     if (n > 0) {
         k_est_sample<Src><<<grid_for((n + EST_STRIDE - 1) / EST_STRIDE, 256, 4), 256, tb + sizeof(u32) * nbins,

@@ -298,3 +298,91 @@ def lsj_join(r_keys, r_payloads, s_keys, s_payloads, config=None, group=None, *,
     phases.update(smpl=t1 - t0, part=t2 - t1, xchg=t3 - t2, local=t4 - t3, n_r_local=int(r_loc.shape[0]),
                   n_s_local=int(s_loc.shape[0]), shuffle="fused P2P" if fused else "partition + NCCL all-to-all-v")
     return res, phases
+
+
+# ------------------------------------------- single-process multi-GPU (C ABI)
+# The same distributed LSJ as one call over several devices of this process
+# (lj_lsj_run_multi: NCCL communicators from ncclCommInitAll, one stream per
+# device) -- the drop-in for the reference's `workers` when the workers are
+# GPUs driven from one host thread.
+
+_NCCL_COMMS: dict = {}
+
+
+def _ptrs(vals, ctype=ctypes.c_void_p):
+    return (ctype * len(vals))(*vals)
+
+
+def nccl_comms(devices) -> list:
+    """One NCCL communicator per device (cached per device tuple)."""
+    from . import _lib
+
+    key = tuple(int(d) for d in devices)
+    if key not in _NCCL_COMMS:
+        lib = _lib.lib()
+        if lib.lj_nccl_available() != 1:
+            raise RuntimeError("NCCL (libnccl.so.2) is not available")
+        arr = (ctypes.c_void_p * len(key))()
+        _lib.check(lib.lj_nccl_comm_init_all(len(key), _ptrs(key, ctypes.c_int), arr), "nccl_comm_init_all")
+        _NCCL_COMMS[key] = [int(a) for a in arr]
+    return _NCCL_COMMS[key]
+
+
+def reduce_sums_multi(words: list) -> tuple[int, int, int]:
+    """lj_reduce_sums over the devices of this process: words[d] (device
+    int64[4]) all become the global (count, sum, xor)."""
+    from . import _lib
+
+    devs = [w.device.index for w in words]
+    comms = nccl_comms(devs)
+    lib = _lib.lib()
+    ws = [torch.empty(lib.lj_reduce_sums_workspace_bytes(len(devs)), dtype=torch.uint8, device=w.device)
+          for w in words]
+    streams = [torch.cuda.current_stream(w.device).cuda_stream for w in words]
+    _lib.check(lib.lj_reduce_sums(len(devs), _ptrs(devs, ctypes.c_int), _ptrs(comms), _ptrs(streams),
+                                  _ptrs([w.data_ptr() for w in words]), _ptrs([t.data_ptr() for t in ws])),
+               "reduce_sums")
+    v = words[0].cpu().tolist()
+    return int(v[0]), int(v[1]) & MASK, int(v[2]) & MASK
+
+
+def lsj_run_multi(r_parts: list, s_parts: list, config=None, cap_factor: float = 1.5):
+    """The distributed LSJ over this process's devices in one C call:
+    r_parts[d] / s_parts[d] are the shards (Relations) on device d.
+    -> (count, sum, xor)."""
+    from . import _lib
+    from .lsj import LsjConfig
+
+    config = config or LsjConfig()
+    lib = _lib.lib()
+    n = len(r_parts)
+    devs = [p.keys.device.index for p in r_parts]
+    comms = nccl_comms(devs)
+    nr = [len(p) for p in r_parts]
+    ns = [len(p) for p in s_parts]
+    nr_t, ns_t = sum(nr), sum(ns)
+    cap_r = min(nr_t, int(cap_factor * nr_t / n) + 4096)
+    cap_s = min(ns_t, int(cap_factor * ns_t / n) + 4096)
+    outs = [torch.zeros(4, dtype=torch.int64, device=p.keys.device) for p in r_parts]
+    streams = [torch.cuda.current_stream(p.keys.device).cuda_stream for p in r_parts]
+    for _ in range(2):
+        wsb = [lib.lj_lsj_run_multi_workspace_bytes(n, nr[d], ns[d], nr_t, max(cap_r, 1), max(cap_s, 1),
+                                                    float(config.sample_rate)) for d in range(n)]
+        ws = [torch.empty(b, dtype=torch.uint8, device=p.keys.device) for b, p in zip(wsb, r_parts)]
+        recv = (ctypes.c_int64 * (2 * n))()
+        rc = lib.lj_lsj_run_multi(n, _ptrs(devs, ctypes.c_int), _ptrs(comms), _ptrs(streams),
+                                  _ptrs([p.keys.data_ptr() for p in r_parts]),
+                                  _ptrs([p.payloads.data_ptr() for p in r_parts]), _ptrs(nr, ctypes.c_int64),
+                                  _ptrs([p.keys.data_ptr() for p in s_parts]),
+                                  _ptrs([p.payloads.data_ptr() for p in s_parts]), _ptrs(ns, ctypes.c_int64),
+                                  max(cap_r, 1), max(cap_s, 1), float(config.sample_rate),
+                                  int(config.seed) & MASK, _ptrs([o.data_ptr() for o in outs]),
+                                  _ptrs([w.data_ptr() for w in ws]), _ptrs(wsb, ctypes.c_size_t), recv)
+        if rc == _lib.LJ_E_WORKSPACE and any(recv):
+            cap_r = max(cap_r, max(recv[2 * d] for d in range(n)))
+            cap_s = max(cap_s, max(recv[2 * d + 1] for d in range(n)))
+            continue
+        _lib.check(rc, "lsj_run_multi")
+        break
+    v = outs[0].cpu().tolist()
+    return int(v[0]), int(v[1]) & MASK, int(v[2]) & MASK

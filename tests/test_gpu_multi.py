@@ -65,3 +65,34 @@ def test_world2_distributed_lsj_equals_oracle(tmp_path, shuffle):
         with open(f"{out}.{rank}") as f:
             r = json.load(f)
         assert r["lsj"] == want
+
+
+@pytest.mark.parametrize("ndev", [1, 2])
+def test_lsj_run_multi_single_process_equals_oracle(ndev):
+    """lj_lsj_run_multi (one process, ndev devices, ncclCommInitAll, grouped
+    send/recv exchange, lj_lsj_run per device, lj_reduce_sums) == the
+    oracle; ndev = 1 runs the whole protocol on one device."""
+    if torch.cuda.device_count() < ndev:
+        pytest.skip("needs %d GPUs" % ndev)
+    import paper_2111_08824_b200 as lj
+    from oracle import gen
+    from paper_2111_08824_b200 import configs
+    from paper_2111_08824_b200 import dist as D
+
+    parts = []
+    for d in range(ndev):
+        with torch.cuda.device(d):
+            parts.append(configs.config5(scale=10, shard=d, shards=ndev, device=f"cuda:{d}"))
+    got = D.lsj_run_multi([p.r for p in parts], [p.s for p in parts], lj.LsjConfig(fanout=4096, sample_rate=0.01))
+    hs = [gen.config5(scale=10, shard=d, shards=ndev) for d in range(ndev)]
+    ss = [h.s() for h in hs]
+    want = oracle.smj_checksum(np.concatenate([h.rk for h in hs]), np.concatenate([h.rp for h in hs]),
+                               np.concatenate([a for a, _ in ss]), np.concatenate([b for _, b in ss]))
+    assert got == tuple(want)
+
+
+def test_reduce_sums_single_device():
+    from paper_2111_08824_b200 import dist as D
+
+    w = torch.tensor([5, -3, 0x0F, 0], dtype=torch.int64, device="cuda")
+    assert D.reduce_sums_multi([w]) == (5, (2**64 - 3), 0x0F)
