@@ -46,14 +46,33 @@ namespace lj {
 
 static inline size_t part_align_c(size_t v) { return (v + 255) & ~(size_t)255; }
 
-constexpr int HS_NT = 384;
-constexpr int HS_CTAS = 2;           // CTAs per SM
-constexpr int HS_U = 4;              // probes per thread per iteration
-constexpr int HS_D = 2;              // iterations of records in flight (cp.async)
+// tuning constants (build-time; tools/gpu_hash_variants.sh measures variants)
+#ifndef LJ_HS_NT
+#define LJ_HS_NT 384
+#endif
+#ifndef LJ_HS_CTAS
+#define LJ_HS_CTAS 2
+#endif
+#ifndef LJ_HS_U
+#define LJ_HS_U 4
+#endif
+#ifndef LJ_HS_D
+#define LJ_HS_D 2
+#endif
+#ifndef LJ_HS_PIECE
+#define LJ_HS_PIECE 32768
+#endif
+#ifndef LJ_HS_NC
+#define LJ_HS_NC 1024
+#endif
+constexpr int HS_NT = LJ_HS_NT;
+constexpr int HS_CTAS = LJ_HS_CTAS;  // CTAs per SM
+constexpr int HS_U = LJ_HS_U;        // probes per thread per iteration
+constexpr int HS_D = LJ_HS_D;        // iterations of records in flight (cp.async)
 constexpr int HS_TT = HS_NT * HS_U;  // records per iteration
 constexpr int HS_CAP = 1024;         // staged spline points per window
-constexpr int HS_NC = 1024;          // lower-bound cells per window
-constexpr i64 HS_PIECE = 32768;      // records per work item
+constexpr int HS_NC = LJ_HS_NC;      // lower-bound cells per window
+constexpr i64 HS_PIECE = LJ_HS_PIECE;  // records per work item
 constexpr int HS_MAXWIN = 2048;
 constexpr int HS_WPT = (HS_MAXWIN + HS_NT - 1) / HS_NT;  // windows per thread in the piece prefix
 
