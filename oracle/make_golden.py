@@ -246,6 +246,34 @@ def make_algos(lj):
     return out
 
 
+def make_c01(lj):
+    """The reference acceptance criterion c01's sweep (test_acceptance.py:73-94:
+    kinds x n in {1e3, 1e4} x dup in {0, 0.25, 0.5}, plus n = 1e5 at dup 0.5;
+    the full n = 1e5 row would triple the fixture) through the
+    reference's ALGORITHMS registry: inputs, NLJ truth checksum and every
+    runner's counters at workers 1 and 4."""
+    from learned_joins.bench import ALGORITHMS, DEFAULT_OPTS, make_join_inputs
+
+    out = {}
+    for kind in ("seq_h", "unif", "lognorm"):
+        for n, dup in [(n, d) for n in (10**3, 10**4) for d in (0.0, 0.25, 0.5)] + [(10**5, 0.5)]:
+            if True:  # n = 1e5 at the largest duplicate share only (fixture size)
+                r, s, _ = make_join_inputs(kind, n, 42, dup_frac=dup)
+                truth = checksum(lj.nlj_oracle(r, s))
+                key = f"{kind}_{n}_{dup}"
+                out[key] = {"r_keys": r.keys, "r_payloads": r.payloads, "s_keys": s.keys,
+                            "s_payloads": s.payloads, "checksum": truth}
+                for algo in ("grmi-inlj", "buffered-grmi-inlj", "spline-hash-inlj", "lsj", "rmi-inlj"):
+                    for workers in (1, 4):
+                        res, br, _ = ALGORITHMS[algo](r, s, workers, dict(DEFAULT_OPTS))
+                        assert np.array_equal(checksum(res), truth), (algo, kind, n, dup)
+                        ctr = br.counters()
+                        out[key][f"{algo}_w{workers}_counters"] = np.array(
+                            [ctr["search_steps"], ctr["predictions"], ctr["leaf_switches"],
+                             ctr["comparator_count"], ctr["partitions_sorted"]], np.int64)
+    return out
+
+
 def make_util(lj):
     from learned_joins.util import chunk_bounds, mix64
 
@@ -281,6 +309,9 @@ def main():
     if len(sys.argv) > 1 and sys.argv[1] == "algos":
         save("algos.npz", make_algos(lj))
         return
+    if len(sys.argv) > 1 and sys.argv[1] == "c01":
+        save("c01.npz", make_c01(lj))
+        return
     sets = key_sets(lj)
     save("util.npz", make_util(lj))
     save("models.npz", make_models(lj, sets))
@@ -288,6 +319,7 @@ def main():
     save("spline_hash.npz", make_spline_hash(lj, sets))
     save("lsj.npz", make_lsj(lj))
     save("algos.npz", make_algos(lj))
+    save("c01.npz", make_c01(lj))
 
 
 if __name__ == "__main__":

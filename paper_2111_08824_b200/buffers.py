@@ -116,7 +116,13 @@ def buffered_probe(index, keys, plan: BufferPlan, sink, *, collect: str = "first
     """buffers.py:103-150: probe ``keys`` flush by flush through per-leaf
     request buffers; ``sink`` receives (tags, payloads, found) with
     collect="first" or (tags, payloads) with collect="all" (host arrays).
-    The delivered multiset equals unbuffered lookups for any cap >= 1."""
+    The delivered multiset equals unbuffered lookups for any cap >= 1.
+
+    The flush schedule is computed on the device, all flushes are searched
+    in ONE device call over the keys in flush order (each flush is a
+    contiguous slice of it), and the per-flush results are cut out of that
+    on the host for the sink -- instead of a few small device calls and
+    copies per flush."""
     from .results import LookupStats
     from .util import to_numpy_u64
 
@@ -133,23 +139,28 @@ def buffered_probe(index, keys, plan: BufferPlan, sink, *, collect: str = "first
         else:
             sink(np.empty(0, dtype=np.int64), np.empty(0, dtype=np.uint64))
         return stats
-    prev = -1
-    for leaf, tags_t in flush_schedule(index.leaf_of(k), plan.cap):
-        if prev >= 0 and leaf != prev:
-            stats.leaf_switches += 1
-        prev = leaf
-        sub = LookupStats()
-        pays, src, found = index.search_from(None, k[tags_t], sub)
-        stats.search_steps += sub.search_steps
-        stats.predictions += sub.predictions
-        tags = tags_t.cpu().numpy()
-        pays_h = to_numpy_u64(pays)
-        src_h = src.cpu().numpy()
+    batches = flush_schedule(index.leaf_of(k), plan.cap)
+    leaves = [lf for lf, _ in batches]
+    stats.leaf_switches = sum(1 for a, b in zip(leaves, leaves[1:]) if a != b)
+    order = torch.cat([t for _, t in batches])
+    sub = LookupStats()
+    pays, src, found = index.search_from(None, k[order], sub)
+    stats.search_steps += sub.search_steps
+    stats.predictions += sub.predictions
+    tags_all = order.cpu().numpy()
+    pays_h = to_numpy_u64(pays)
+    src_h = src.cpu().numpy()  # non-decreasing: every probe's matches in probe order
+    found_h = found.cpu().numpy()
+    bounds = np.cumsum([0] + [t.numel() for _, t in batches])
+    cut = np.searchsorted(src_h, bounds)  # each flush's slice of the matches
+    if collect == "first":
+        first = np.zeros(tags_all.size, dtype=np.uint64)
+        probe, at = np.unique(src_h, return_index=True)
+        first[probe] = pays_h[at]
+    for b in range(len(batches)):
+        lo, hi = int(bounds[b]), int(bounds[b + 1])
         if collect == "first":
-            first = np.zeros(tags.size, dtype=np.uint64)
-            probe, at = np.unique(src_h, return_index=True)
-            first[probe] = pays_h[at]
-            sink(tags, first, found.cpu().numpy())
+            sink(tags_all[lo:hi], first[lo:hi], found_h[lo:hi])
         else:
-            sink(tags[src_h], pays_h)
+            sink(tags_all[src_h[cut[b]:cut[b + 1]]], pays_h[cut[b]:cut[b + 1]])
     return stats

@@ -45,6 +45,7 @@ DEFAULT_OPTS = {
     # GPU-only knobs (absent from the reference)
     "materialize": False,
     "counters": True,
+    "lsj_sampler": "device",  # "reference": numpy Generator.choice positions -> the reference's bucket counters
 }
 
 
@@ -277,7 +278,7 @@ def _run_lsj(r, s, workers, opts):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     result, br = lsj_join(r, s, config, materialize=bool(opts.get("materialize")),
-                          counters=bool(opts.get("counters", True)))
+                          counters=bool(opts.get("counters", True)), sampler=opts.get("lsj_sampler", "device"))
     _ = result.checksum  # the 3-word readback is part of the join
     return result, br, time.perf_counter() - t0
 

@@ -196,13 +196,28 @@ def _sort_stats(bounds: torch.Tensor) -> SortStats:
     return SortStats(comparator_count=comps, partitions_sorted=int(nz.numel()))
 
 
-def _sample_sorted(relation: Relation, sample_rate: float, seed: int) -> torch.Tensor:
+SAMPLERS = ("device", "reference")
+
+
+def _sample_sorted(relation: Relation, sample_rate: float, seed: int, sampler: str = "device") -> torch.Tensor:
+    """The sorted model-fit sample.  "device": one key per stratum at a
+    counter-drawn offset (lj_lsj_sample).  "reference": the reference's own
+    positions, numpy default_rng(seed).choice(n, total, replace=False)
+    (lsj.py:119-120) drawn on the host and gathered on the device -- the
+    reference's model, hence its bucket counters (comparator_count,
+    partitions_sorted); the join result is the same with either."""
+    if sampler not in SAMPLERS:
+        raise ValueError(f"sampler must be one of {SAMPLERS}")
     n = len(relation)
     total = int(round(sample_rate * n))
     if total == 0:
         o = unsigned_order(relation.keys)
         lo, hi = torch.aminmax(o)
         return torch.stack([lo, hi]) ^ (-(2**63))
+    if sampler == "reference":
+        pos = np.random.default_rng(seed).choice(n, size=total, replace=False)
+        picked = relation.keys[torch.from_numpy(pos.astype(np.int64)).to(relation.device)]
+        return unsigned_order(torch.sort(unsigned_order(picked)).values)
     lib = _lib.lib()
     sample = torch.empty(total, dtype=torch.int64, device=relation.device)
     ws = _lib.workspace(lib.lj_lsj_sample_workspace_bytes(total), relation.device)
@@ -221,13 +236,13 @@ def sample_train(relation: Relation, sample_rate: float, workers: int, seed: int
 
 
 def prepare_model(relation: Relation, sample_rate: float, seed: int, fanout: int | None = None,
-                  nbins: int | None = None) -> tuple[RecursiveModelIndex, LsjModel]:
+                  nbins: int | None = None, sampler: str = "device") -> tuple[RecursiveModelIndex, LsjModel]:
     n = len(relation)
     if n == 0:
         raise ValueError("cannot sample an empty relation")
     if not 0.0 < sample_rate <= 1.0:
         raise ValueError("sample_rate must be in (0, 1]")
-    sample = _sample_sorted(relation, sample_rate, seed)
+    sample = _sample_sorted(relation, sample_rate, seed, sampler)
     total = int(round(sample_rate * n))
     if total == 0:
         rmi = RecursiveModelIndex(fanout=1).fit(sample)
@@ -307,16 +322,33 @@ def sort_relation(keys, payloads, model, scale: int, workers: int = 1) -> Sorted
 def range_partition(relation: Relation, model: RecursiveModelIndex, workers: int,
                     config: LsjConfig) -> PartitionedRelation:
     """lsj.py:133-209: worker of a key = partition_index(model, key, p_eff)
-    // (p_eff / workers) == partition_index(model, key, workers); order inside
-    a worker range is unspecified (the multiset is the reference's)."""
+    // (p_eff / workers) == partition_index(model, key, workers) (nested
+    floor division); one device partition into the worker ranges.  The
+    histogram is the reference's workers x workers matrix (input chunk w,
+    chunk_bounds semantics, by target t), prefix_sums its write offsets;
+    the order inside a range is unspecified (the multiset is the
+    reference's, and so are the ranges)."""
+    from .models import partition_index
+    from .util import chunk_bounds
+
     n = len(relation)
     lm = LsjModel.uniform(model, workers)
     pairs, starts = _partition(relation.keys, relation.payloads, lm)
     st = starts.cpu().tolist()
     ranges = [(int(st[w]), int(st[w + 1])) for w in range(workers)]
-    hist = np.diff(np.asarray(st, dtype=np.int64)).reshape(1, workers)
+    hist = np.zeros((workers, workers), dtype=np.int64)
+    if n:
+        target = partition_index(model, relation.keys, workers)
+        b = chunk_bounds(n, workers)
+        chunk = torch.repeat_interleave(torch.arange(workers, device=target.device),
+                                        torch.as_tensor(np.diff(b), device=target.device))
+        hist = torch.bincount(chunk * workers + target, minlength=workers * workers).reshape(workers, workers)
+        hist = hist.cpu().numpy().astype(np.int64)
+    totals = hist.sum(axis=0)
+    target_starts = np.concatenate(([0], np.cumsum(totals)))[:-1]
+    offsets = target_starts + np.cumsum(hist, axis=0) - hist
     return PartitionedRelation(pairs[0 : 2 * n : 2].contiguous(), pairs[1 : 2 * n : 2].contiguous(), ranges, hist,
-                               np.asarray(st[:-1], dtype=np.int64).reshape(1, workers))
+                               offsets)
 
 
 def cdf_bitonic_sort(keys, payloads, model, num_partitions: int):
@@ -369,7 +401,7 @@ def _join(r_sorted: SortedRelation, s_sorted: SortedRelation, materialize: bool)
 
 
 def lsj_join(r: Relation, s: Relation, config: LsjConfig | None = None, materialize: bool = False,
-             models: tuple | None = None, counters: bool = True):
+             models: tuple | None = None, counters: bool = True, sampler: str = "device"):
     """lsj.py:373-405: the full learned sort-join -> (JoinResult,
     PhaseBreakdown).  Phase times are CUDA-event times on the stream.
     ``models`` = (model_r, model_s) RMIs fitted elsewhere (e.g. the
@@ -383,8 +415,9 @@ def lsj_join(r: Relation, s: Relation, config: LsjConfig | None = None, material
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
     ev[0].record()
     if models is None:
-        _, lr = prepare_model(r, config.sample_rate, config.seed, config.model_fanout)
-        _, ls = prepare_model(s, config.sample_rate, config.seed ^ 0x5DEECE66D, config.model_fanout)
+        _, lr = prepare_model(r, config.sample_rate, config.seed, config.model_fanout, sampler=sampler)
+        _, ls = prepare_model(s, config.sample_rate, config.seed ^ 0x5DEECE66D, config.model_fanout,
+                              sampler=sampler)
     else:
         lr = _as_lsj_model(models[0], len(r))
         ls = _as_lsj_model(models[1], len(s))
