@@ -123,6 +123,19 @@ __device__ __forceinline__ i64 rmi_leaf_pos(const LjLeaf &lf, double x) {
     return clip_i64(p, lf.clamp_lo, lf.clamp_hi);
 }
 
+// The same position with a SATURATING cast: a raw prediction beyond the
+// int64 range clamps to the leaf's bound instead of the x86 cast's
+// INT64_MIN (which sends keys far above the training range to clamp_lo).
+// Monotone in the key everywhere; the LSJ's internal bins use it (any
+// monotone bin function gives the same join), the reference-facing
+// predictions keep the reference's cast.
+__device__ __forceinline__ i64 rmi_leaf_pos_sat(const LjLeaf &lf, double x) {
+    const double raw = __dadd_rn(__dmul_rn(lf.slope, x), lf.icpt);
+    if (raw >= 9223372036854775808.0) return lf.clamp_hi;
+    if (!(raw >= -9223372036854775808.0)) return lf.clamp_lo;
+    return clip_i64(__double2ll_rn(raw), lf.clamp_lo, lf.clamp_hi);
+}
+
 __device__ __forceinline__ LjLeaf load_leaf(const LjLeaf *leaves, i64 l) {
     const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(leaves + l);
     ulonglong2 a = __ldg(p), b = __ldg(p + 1);
@@ -154,6 +167,9 @@ struct RmiDev {
     __device__ __forceinline__ i64 route(double x) const { return rmi_route(rs, ri, m, x); }
     __device__ __forceinline__ i64 pos(double x) const {
         return rmi_leaf_pos(load_leaf(leaves, route(x)), x);
+    }
+    __device__ __forceinline__ i64 pos_sat(double x) const {
+        return rmi_leaf_pos_sat(load_leaf(leaves, route(x)), x);
     }
 };
 

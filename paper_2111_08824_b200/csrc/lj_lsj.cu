@@ -84,7 +84,10 @@ struct LsjDev {
     int nb;
     const u64 *sample;  // sorted fit sample (split points) or nullptr
     i64 nsample;
-    __device__ __forceinline__ i64 pos(u64 k) const { return m.pos(u64_to_f64(k)); }
+    // monotone over the whole key domain (saturating cast, lj_common.cuh):
+    // the key-range bounds found by search, the partition and the join's
+    // window lookup all see the same bins
+    __device__ __forceinline__ i64 pos(u64 k) const { return m.pos_sat(u64_to_f64(k)); }
     __device__ __forceinline__ int bin(u64 k) const { return (int)__ldg(table + pos(k)); }
     // Unrounded placement key y in [pos-0.5, pos+0.5], monotone in the key:
     // within a leaf slope*x + icpt is non-decreasing; clamping to the leaf's
@@ -153,7 +156,7 @@ __global__ void k_lsj_key_bounds(LsjDev d, u64 *lay) {
 __global__ void k_sample_pos(RmiDev m, const u64 *sample, i64 total, i64 *spos) {
     m.fix();
     for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < total; i += (i64)gridDim.x * blockDim.x)
-        spos[i] = m.pos(u64_to_f64(sample[i]));
+        spos[i] = m.pos_sat(u64_to_f64(sample[i]));
 }
 
 // pb[0] = 0, pb[j] = spos[floor(j*S/nb)], pb[nb] = trained_len
