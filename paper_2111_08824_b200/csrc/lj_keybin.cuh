@@ -20,10 +20,19 @@
 // [cells[c], cells[c+1]] (cells[c] = #{ j : cell(B[j]) < c }) and the
 // search over that range returns exactly #{ j : B[j] <= k }.
 //
+// Crowded cells (clustered keys put a cluster's boundaries into one cell)
+// get a second level: up to kb_nsub(nb) of them carry a sub-table of
+// KB_SUBN sub-cells spanning just their own boundaries' image range [base,
+// base + (KB_SUBN << sh)), with the same exactness argument one level down
+// (sub-cell monotone in the image, clamped at both ends).
+//
 // Layout (u64 words, global and shared alike):
-//   [0] t0 (image of B[1])   [1] shift | log << 8   [2] nb   [3] 0
+//   [0] t0 (image of B[1])   [1] shift | log << 8   [2] nb   [3] sub-tables used
 //   [4 + j]  B[j], j in [1, nb)   (word 4 unused)
-//   then u16 cells[KB_CELLS + 1]
+//   u16 cells[KB_CELLS + 1]
+//   u8  sidx[KB_CELLS]            sub-table of a cell, 0xFF = none
+//   u64 sbase[nsub], u64 sshift[nsub]
+//   u16 subs[nsub][KB_SUBN + 1]
 #pragma once
 
 #include "lj_part.cuh"
@@ -32,8 +41,16 @@ namespace lj {
 
 constexpr int KB_CELLS = 8192;
 constexpr int KB_MAXBINS = 2048;
+constexpr int KB_SUBN = 64;
 
-__host__ __device__ inline int kb_words(int nb) { return 4 + ((nb + 3) & ~3) + (KB_CELLS + 1 + 3) / 4; }
+// sub-tables: only next to small boundary sets (the partition kernels keep
+// two ring stages beside the staged table)
+__host__ __device__ inline int kb_nsub(int nb) { return nb <= 1024 ? 64 : 0; }
+__host__ __device__ inline int kb_cells_words() { return (KB_CELLS + 1 + 3) / 4; }
+__host__ __device__ inline int kb_words(int nb) {
+    const int ns = kb_nsub(nb);
+    return 4 + ((nb + 3) & ~3) + kb_cells_words() + (ns ? KB_CELLS / 8 + 2 * ns + (ns * (KB_SUBN + 1) + 3) / 4 : 0);
+}
 inline size_t kb_bytes(int nb) { return (size_t)kb_words(nb) * 8; }
 
 // Monotone log-like image: bit length in the top 7 bits, then the bits
@@ -70,9 +87,25 @@ struct KeyRangeBin {
         const u64 t0 = g[0];
         const u32 ctl = (u32)g[1];
         const u64 *B = g + 4;
-        const u16 *cells = reinterpret_cast<const u16 *>(g + 4 + ((nb + 3) & ~3));
-        const u32 c = kb_cell(kb_image(k, (int)(ctl >> 8)), t0, (int)(ctl & 63));
+        const u64 *cw = g + 4 + ((nb + 3) & ~3);
+        const u16 *cells = reinterpret_cast<const u16 *>(cw);
+        const u64 t = kb_image(k, (int)(ctl >> 8));
+        const u32 c = kb_cell(t, t0, (int)(ctl & 63));
         int lo = cells[c], hi = cells[c + 1];
+        const int ns = kb_nsub(nb);
+        if (ns) {
+            const u64 *sw = cw + kb_cells_words();
+            const int q = reinterpret_cast<const unsigned char *>(sw)[c];
+            if (q != 0xFF) {
+                const u64 *sbase = sw + KB_CELLS / 8, *sshift = sbase + ns;
+                const u16 *subs = reinterpret_cast<const u16 *>(sshift + ns) + q * (KB_SUBN + 1);
+                const u64 b = sbase[q];
+                const u64 d = t > b ? (t - b) >> sshift[q] : 0;
+                const int sc = d >= (u64)KB_SUBN ? KB_SUBN - 1 : (int)d;
+                lo = subs[sc];
+                hi = subs[sc + 1];
+            }
+        }
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
             if (B[mid] <= k) lo = mid;
@@ -153,14 +186,61 @@ static __global__ void __launch_bounds__(1024) k_keybin_build(u64 *lay, int nb) 
     }
     const int m = worst[1] < worst[0] ? 1 : 0;
     if (m == 1) fill(1);
-    u16 *cells = reinterpret_cast<u16 *>(lay + 4 + ((nb + 3) & ~3));
+    u64 *cw = lay + 4 + ((nb + 3) & ~3);
+    u16 *cells = reinterpret_cast<u16 *>(cw);
     for (int c = tid; c <= KB_CELLS; c += blockDim.x) cells[c] = cand[c];
+    __shared__ int s_nsub;
+    const int ns = kb_nsub(nb);
     if (tid == 0) {
         lay[0] = s_t0[m];
         lay[1] = (u64)s_shift[m] | ((u64)m << 8);
         lay[2] = (u64)nb;
-        lay[3] = 0;
+        s_nsub = 0;
     }
+    __syncthreads();
+    if (ns) {
+        // second level for the crowded cells (> 2 boundaries), first come
+        // first served up to the budget (any choice is exact)
+        u64 *sw = cw + kb_cells_words();
+        unsigned char *sidx = reinterpret_cast<unsigned char *>(sw);
+        u64 *sbase = sw + KB_CELLS / 8, *sshift = sbase + ns;
+        u16 *subs = reinterpret_cast<u16 *>(sshift + ns);
+        const u64 t0 = s_t0[m];
+        const int sh0 = s_shift[m];
+        for (int c = tid; c < KB_CELLS; c += blockDim.x) {
+            int q = 0xFF;
+            if ((int)cand[c + 1] - (int)cand[c] > 2) {
+                const int got = atomicAdd(&s_nsub, 1);
+                if (got < ns) q = got;
+            }
+            sidx[c] = (unsigned char)q;
+            if (q == 0xFF) continue;
+            const int a = cand[c], e = cand[c + 1];  // boundaries j in (a, e] lie in cell c
+            const u64 b = kb_image(pm[a + 1], m), last = kb_image(pm[e], m);
+            int sh = 0;
+            while (sh < 63 && ((last - b) >> sh) >= (u64)KB_SUBN) ++sh;
+            sbase[q] = b;
+            sshift[q] = (u64)sh;
+            u16 *st = subs + q * (KB_SUBN + 1);
+            // st[s] = a + #{ j in (a, e] : subcell(B[j]) < s }: the search in
+            // sub-cell s runs over (st[s], st[s + 1]] like the cells above
+            int j = a + 1;
+            for (int sc = 0; sc <= KB_SUBN; ++sc) {
+                while (j <= e) {
+                    const u64 tj = kb_image(pm[j], m);
+                    const u64 d = tj > b ? (tj - b) >> sh : 0;
+                    const int scj = d >= (u64)KB_SUBN ? KB_SUBN - 1 : (int)d;
+                    if (scj < sc) ++j;
+                    else break;
+                }
+                st[sc] = (u16)(sc == KB_SUBN ? e : j - 1);
+            }
+        }
+        (void)t0;
+        (void)sh0;
+    }
+    __syncthreads();
+    if (tid == 0) lay[3] = (u64)(s_nsub < ns ? s_nsub : ns);
 }
 
 }  // namespace lj

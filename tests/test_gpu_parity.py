@@ -490,7 +490,7 @@ def _dist_keys(rng, dist, n):
 
 
 @pytest.mark.parametrize("dist", ["uniform", "lognormal", "clusters", "dups", "dense", "top"])
-@pytest.mark.parametrize("nb", [1, 2, 37, 2048])
+@pytest.mark.parametrize("nb", [1, 2, 37, 512, 1000, 2048])
 def test_keybin_matches_search(lj, dist, nb):
     """bin(k) = #{ j >= 1 : B[j] <= k } exactly, whichever key image the
     table picks, on boundaries drawn from the distribution (repeats and all)
