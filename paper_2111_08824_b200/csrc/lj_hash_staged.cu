@@ -65,6 +65,9 @@ static inline size_t part_align_c(size_t v) { return (v + 255) & ~(size_t)255; }
 #ifndef LJ_HS_NC
 #define LJ_HS_NC 1024
 #endif
+#ifndef LJ_HS_ROUNDS
+#define LJ_HS_ROUNDS 1  // forward slot scan in rounds of one pair per unfinished probe (0: slot by slot)
+#endif
 constexpr int HS_NT = LJ_HS_NT;
 constexpr int HS_CTAS = LJ_HS_CTAS;  // CTAs per SM
 constexpr int HS_U = LJ_HS_U;        // probes per thread per iteration
@@ -216,19 +219,23 @@ struct StagedSpline {
     const u64 *sk;
     const Seg *seg;
     const u16 *cells;
-    u64 klo, khi;
-    int a0, npts, cshift;
-    i64 K, n;
-    double guard;  // (n + 1) * 2^-49: see pos()
-    // models.py:221-248 for k in [klo, khi]: the first spline key >= k over
-    // the staged points (the cell bounds its range), then the reference's
-    // operations.  t = (k - x0) / d is taken as (k - x0) * RN(1/d): both are
-    // within 3.01 * 2^-53 of the true quotient (t <= 1), so the two values of
-    // r0 + t*dr differ by at most 2^-50 * (r1 + 1) <= 2^-50 * (n + 1); rint
-    // only jumps at half-integers, so unless the fast value lies within
-    // `guard` (twice that) of one, both round to the same integer -- else
-    // the reference's division runs.
-    __device__ __forceinline__ i64 pos(u64 k) const {
+    u64 klo, span;  // staged key range [klo, klo + span]
+    int cshift;
+    int li_lo, li_hi;  // the staged image of clamping the point index to [1, K-1]
+    int nm1;           // n - 1 (the staged path needs n < 2^31)
+    double guard;      // 0.5 - (n + 1) * 2^-49: see pos()
+    // models.py:221-248 for k in [klo, klo + span]: the first spline key >= k
+    // over the staged points (the cell bounds its range), then the
+    // reference's operations.  t = (k - x0) / d is taken as (k - x0) *
+    // RN(1/d): both are within 3.01 * 2^-53 of the true quotient (t <= 1), so
+    // the two values of r0 + t*dr differ by at most 2^-50 * (r1 + 1) <=
+    // 2^-50 * (n + 1); rint only jumps at half-integers, so unless the fast
+    // value lies within (n + 1) * 2^-49 (twice that) of one, both round to
+    // the same integer -- else the reference's division runs.  Every operand
+    // is finite and t in [0, 1] keeps z in [0, n), so np.clip's NaN rule and
+    // the cast's range rule never apply; z is within 0.5 of the rounded p, so
+    // "near a half-integer" is |z - p| >= guard.
+    __device__ __forceinline__ int pos(u64 k) const {
         const int c = (int)((k - klo) >> cshift);
         int lo = cells[c], hi = cells[c + 1];
         while (lo < hi) {
@@ -236,22 +243,17 @@ struct StagedSpline {
             if (sk[mid] < k) lo = mid + 1;
             else hi = mid;
         }
-        i64 j = (i64)a0 + lo;
-        j = j < 1 ? 1 : (j > K - 1 ? K - 1 : j);
-        const int li = (int)(j - a0);
+        const int li = min(max(lo, li_lo), li_hi);
         const Seg g = seg[li];
-        const double kf = u64_to_f64(k);
-        const double a = __dsub_rn(kf, g.x0);
-        double t = clip_f64(__dmul_rn(a, g.inv), 0.0, 1.0);
-        double z = __dadd_rn(g.r0, __dmul_rn(t, g.dr));
-        if (fabs(__dsub_rn(__dsub_rn(z, floor(z)), 0.5)) <= guard) {
-            const double x1 = u64_to_f64(sk[li]);
-            const double d = __dsub_rn(x1, g.x0);
-            t = clip_f64(__ddiv_rn(a, d > 1.0 ? d : 1.0), 0.0, 1.0);
-            z = __dadd_rn(g.r0, __dmul_rn(t, g.dr));
+        const double a = __dsub_rn(u64_to_f64(k), g.x0);
+        double z = __dadd_rn(g.r0, __dmul_rn(fmin(fmax(__dmul_rn(a, g.inv), 0.0), 1.0), g.dr));
+        int p = __double2int_rn(z);
+        if (fabs(__dsub_rn(z, (double)p)) >= guard) {
+            const double d = __dsub_rn(u64_to_f64(sk[li]), g.x0);
+            z = __dadd_rn(g.r0, __dmul_rn(fmin(fmax(__ddiv_rn(a, d > 1.0 ? d : 1.0), 0.0), 1.0), g.dr));
+            p = __double2int_rn(z);
         }
-        const i64 p = f64_to_i64(rint(z));
-        return clip_i64(p, 0, n - 1);
+        return min(max(p, 0), nm1);
     }
 };
 
@@ -264,6 +266,26 @@ struct Acc3 {
         x ^= v;
     }
 };
+
+// One aligned slot pair {key0, pay0, key1, pay1} of a probe for key k; slot
+// keys are non-decreasing.  Matches (key == k, payload != 0) are added;
+// returns true when the scan must go on to the next pair (no key > k seen
+// and, with unique build keys, no match yet).  UNIQUE is branch-free: at
+// most one slot matches, its payload is selected and added under one
+// predicate.
+template <bool UNIQUE>
+__device__ __forceinline__ bool pair_scan(const u64 (&e)[4], u64 k, u64 ps, Acc3 &acc) {
+    if (UNIQUE) {
+        const u64 h = (e[0] == k && e[1]) ? e[1] : ((e[2] == k && e[3]) ? e[3] : 0ULL);
+        if (h) acc.add(h, ps);
+        return h == 0 && e[2] <= k;
+    }
+    if (e[0] > k) return false;
+    if (e[0] == k && e[1]) acc.add(e[1], ps);
+    if (e[2] > k) return false;
+    if (e[2] == k && e[3]) acc.add(e[3], ps);
+    return true;
+}
 
 // 16-B asynchronous global -> shared copy with an L2 cache policy
 __device__ __forceinline__ void cp_async16_ef(void *dst, const void *src, u64 pol) {
@@ -281,8 +303,9 @@ __device__ __forceinline__ i64 spline_pos_global(const SplineDev &m, u64 k) { re
 // coalesced across the warp) while iteration i is probed, so no barrier
 // is needed inside a work item; every probe's first slot is loaded before
 // any is compared (HS_U independent L2 loads in flight per thread).
+template <bool UNIQUE>
 __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev m, const ulonglong2 *__restrict__ slots,
-                                                                     int unique, const ulonglong2 *__restrict__ rec,
+                                                                     const ulonglong2 *__restrict__ rec,
                                                                      const i64 *__restrict__ reg, int nb,
                                                                      const WinMeta *__restrict__ meta,
                                                                      const u16 *__restrict__ cells_g,
@@ -353,9 +376,8 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
     ss.sk = sk;
     ss.seg = seg;
     ss.cells = cells;
-    ss.K = m.K;
-    ss.n = m.n;
-    ss.guard = ((double)m.n + 1.0) * 1.7763568394002505e-15;  // 2^-49
+    ss.nm1 = (int)(m.n - 1);
+    ss.guard = 0.5 - ((double)m.n + 1.0) * 1.7763568394002505e-15;  // 2^-49
     Acc3 acc = {0, 0, 0};
     u64 pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -402,10 +424,11 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
                     sphase ^= 1u;
                     staged = true;
                     ss.klo = mw.klo;
-                    ss.khi = mw.khi;
-                    ss.a0 = mw.a0;
-                    ss.npts = mw.npts;
+                    ss.span = mw.khi - mw.klo;
                     ss.cshift = mw.cshift;
+                    // point index j = a0 + lo clamped to [1, K-1], staged-relative
+                    ss.li_lo = mw.a0 >= 1 ? 0 : 1;
+                    ss.li_hi = (int)min((i64)mw.npts, m.K - 1 - (i64)mw.a0);
                 }
             }
         }
@@ -452,8 +475,10 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
             }
 #pragma unroll
             for (int u = 0; u < HS_U; ++u) {
-                if (k[u] == ~0ULL) s0[u] = -1;  // past the item / a gap record
-                else if (staged && k[u] >= ss.klo && k[u] <= ss.khi) s0[u] = 2 * ss.pos(k[u]);
+                // (one unsigned compare covers klo <= k <= khi; the reserved
+                // key of gap records / past the item lies outside every window)
+                if (staged && k[u] - ss.klo <= ss.span) s0[u] = 2 * (i64)ss.pos(k[u]);
+                else if (k[u] == ~0ULL) s0[u] = -1;
                 else s0[u] = 2 * spline_pos_global(m, k[u]);
             }
             // every probe's first slot PAIR (32 B, aligned: one sector) in flight at once
@@ -471,25 +496,47 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
             }
             // the slot scan (see the header): keys < k skipped, keys == k
             // with a nonzero payload counted (unique build keys: the first
-            // is the only one), stop at the first key > k
+            // is the only one), stop at the first key > k.  About a quarter
+            // of the probes go past their first pair (crowded positions push
+            // entries forward); their following pairs are fetched in rounds
+            // -- one more pair for EVERY unfinished probe of the thread in
+            // flight at once -- instead of one dependent 16-B load at a time.
+            unsigned need = 0;
 #pragma unroll
             for (int u = 0; u < HS_U; ++u) {
-                if (s0[u] < 0 || e[u][0] > k[u]) continue;
-                if (e[u][0] == k[u] && e[u][1]) {
-                    acc.add(e[u][1], ps[u]);
-                    if (unique) continue;
-                }
-                if (e[u][2] > k[u]) continue;
-                if (e[u][2] == k[u] && e[u][3]) {
-                    acc.add(e[u][3], ps[u]);
-                    if (unique) continue;
-                }
+                // (a skipped probe's pair {~0, 0, ~0, 0} matches nothing)
+                need |= (unsigned)(pair_scan<UNIQUE>(e[u], k[u], ps[u], acc) && s0[u] >= 0) << u;
+            }
+#if LJ_HS_ROUNDS == 0
+            // (ablation) one dependent 16-B slot at a time, probe by probe
+#pragma unroll
+            for (int u = 0; u < HS_U; ++u) {
+                if (!(need >> u & 1u)) continue;
                 for (i64 sl = s0[u] + 2;; ++sl) {
                     const ulonglong2 ev = __ldg(slots + sl);
                     if (ev.x > k[u]) break;
                     if (ev.x == k[u] && ev.y) {
                         acc.add(ev.y, ps[u]);
-                        if (unique) break;
+                        if (UNIQUE) break;
+                    }
+                }
+            }
+            need = 0;
+#endif
+#pragma unroll 1
+            for (int r = 1; need; ++r) {
+#pragma unroll
+                for (int u = 0; u < HS_U; ++u) {
+                    if (need >> u & 1u) {
+                        asm volatile("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+                                     : "=l"(e[u][0]), "=l"(e[u][1]), "=l"(e[u][2]), "=l"(e[u][3])
+                                     : "l"(slots + s0[u] + 2 * r));
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < HS_U; ++u) {
+                    if (need >> u & 1u) {
+                        if (!pair_scan<UNIQUE>(e[u], k[u], ps[u], acc)) need &= ~(1u << u);
                     }
                 }
             }
@@ -601,16 +648,26 @@ int hash_probe_staged(const LjSplineHash &idx, const ulonglong2 *rec, const i64 
         reinterpret_cast<const u16 *>((const char *)meta_ws + (((size_t)nb * sizeof(WinMeta) + 255) & ~(size_t)255));
     const size_t sm = (size_t)HS_D * HS_U * HS_NT * 16 + (size_t)HS_CAP * (8 + sizeof(Seg)) + (HS_NC + 8) * 2 +
                       (size_t)(nb + 2) * 4;
+    if (idx.model.n >= ((i64)1 << 31)) {
+        set_error("hash_probe_staged: at most 2^31 - 1 build keys");
+        return LJ_E_INVALID;
+    }
     static unsigned long long attr = 0;  // one bit per device
     if (once_per_device(attr)) {
-        LJ_CK(cudaFuncSetAttribute(k_hash_probe_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)((size_t)HS_D * HS_U * HS_NT * 16 + (size_t)HS_CAP * (8 + sizeof(Seg)) +
-                                         (HS_NC + 8) * 2 + (size_t)(HS_MAXWIN + 2) * 4)));
+        const int mx = (int)((size_t)HS_D * HS_U * HS_NT * 16 + (size_t)HS_CAP * (8 + sizeof(Seg)) + (HS_NC + 8) * 2 +
+                             (size_t)(HS_MAXWIN + 2) * 4);
+        LJ_CK(cudaFuncSetAttribute(k_hash_probe_staged<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        LJ_CK(cudaFuncSetAttribute(k_hash_probe_staged<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     }
     LJ_CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
-    k_hash_probe_staged<<<HS_CTAS * sm_count(), HS_NT, sm, st>>>(
-        SplineDev(idx.model), reinterpret_cast<const ulonglong2 *>(idx.slots), idx.slots_unique, rec, reg, nb, meta, cells,
-        reinterpret_cast<const Seg *>(idx.segs), ctr, out);
+    if (idx.slots_unique)
+        k_hash_probe_staged<true><<<HS_CTAS * sm_count(), HS_NT, sm, st>>>(
+            SplineDev(idx.model), reinterpret_cast<const ulonglong2 *>(idx.slots), rec, reg, nb, meta, cells,
+            reinterpret_cast<const Seg *>(idx.segs), ctr, out);
+    else
+        k_hash_probe_staged<false><<<HS_CTAS * sm_count(), HS_NT, sm, st>>>(
+            SplineDev(idx.model), reinterpret_cast<const ulonglong2 *>(idx.slots), rec, reg, nb, meta, cells,
+            reinterpret_cast<const Seg *>(idx.segs), ctr, out);
     LJ_CK_LAUNCH();
     return LJ_OK;
 }

@@ -10,8 +10,9 @@
 // domain).  Evaluating the model per tuple costs a dependent leaf load from
 // L2 (plus, for LSJ, a bin-table load); this structure needs none: a radix
 // table over a monotone image t(k) of the key -- the key itself or a
-// log-like image (bit length, then the bits below the leading one) for
-// skewed keys, whichever leaves fewer boundaries per cell -- narrows the
+// log-like image (the key's float bit pattern: bit length, then the bits
+// below the leading one) for skewed keys, whichever leaves fewer boundaries
+// per cell -- narrows the
 // boundary range to a few entries, and a short binary search over the
 // boundaries (both staged in shared memory, <= 32 KB) finishes it.
 //
@@ -53,13 +54,11 @@ __host__ __device__ inline int kb_words(int nb) {
 }
 inline size_t kb_bytes(int nb) { return (size_t)kb_words(nb) * 8; }
 
-// Monotone log-like image: bit length in the top 7 bits, then the bits
-// below the leading one (truncated to 57).  a <= b  =>  kb_lg(a) <= kb_lg(b).
-__device__ __forceinline__ u64 kb_lg(u64 k) {
-    if (k == 0) return 0;
-    const int z = __clzll((long long)k);
-    return ((u64)(64 - z) << 57) | (((k << z) << 1) >> 7);
-}
+// Monotone log-like image: the bit pattern of the key converted to float
+// with truncation -- the exponent (bit length), then the 23 bits below the
+// leading one; one conversion instruction.  a <= b  =>  kb_lg(a) <= kb_lg(b)
+// (truncation is monotone, and non-negative floats order like their bits).
+__device__ __forceinline__ u64 kb_lg(u64 k) { return (u64)__float_as_uint(__ull2float_rz(k)); }
 
 __device__ __forceinline__ u64 kb_image(u64 k, int lg) { return lg ? kb_lg(k) : k; }
 
@@ -73,6 +72,10 @@ struct KeyRangeBin {
     const u64 *g;  // layout (global before staging, shared after)
     int nb;
     int shift = 0;  // code -> bin shift of the partition passes (code == bin)
+    // header words, cached in registers by at() (read from the global layout,
+    // so no barrier is needed before them)
+    u64 t0 = 0;
+    u32 ctl = 0;
     __host__ __device__ int smem_words() const { return kb_words(nb); }
     __device__ void stage(u64 *dst) const {
         const int w = kb_words(nb);
@@ -80,12 +83,13 @@ struct KeyRangeBin {
     }
     __device__ __forceinline__ KeyRangeBin at(u64 *tab) const {
         KeyRangeBin c = *this;
+        c.t0 = g[0];
+        c.ctl = (u32)g[1];
         c.g = tab;
         return c;
     }
+    // only on the copy at() returns
     __device__ __forceinline__ u32 code(u64 k) const {
-        const u64 t0 = g[0];
-        const u32 ctl = (u32)g[1];
         const u64 *B = g + 4;
         const u64 *cw = g + 4 + ((nb + 3) & ~3);
         const u16 *cells = reinterpret_cast<const u16 *>(cw);
@@ -105,6 +109,16 @@ struct KeyRangeBin {
                 lo = subs[sc];
                 hi = subs[sc + 1];
             }
+        }
+        // two unconditional, branch-free steps settle every range of <= 3
+        // boundaries (a step on lo == hi is a no-op: B[lo] <= k there, B[0] =
+        // 0), so consecutive evaluations overlap; longer ranges finish in the loop
+#pragma unroll
+        for (int it = 0; it < 2; ++it) {
+            const int mid = (lo + hi + 1) >> 1;
+            const bool ge = B[mid] <= k;
+            lo = ge ? mid : lo;
+            hi = ge ? hi : mid - 1;
         }
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;

@@ -41,25 +41,31 @@
 namespace lj {
 
 #ifndef LJ_SORT_CTAS
-#define LJ_SORT_CTAS 4
+#define LJ_SORT_CTAS 5
+#endif
+#ifndef LJ_SORT_NT
+#define LJ_SORT_NT 256
+#endif
+#ifndef LJ_SORT_E
+#define LJ_SORT_E 8
 #endif
 constexpr int SORT_CTAS = LJ_SORT_CTAS;  // sort CTAs per SM (their barrier waits overlap)
-constexpr int SORT_NT = 1024 / SORT_CTAS;
-#ifndef LJ_SLOT_X
-#define LJ_SLOT_X 1
-#endif
-constexpr int SLOT_X = LJ_SLOT_X;  // placement slots per tuple (2: 17.9 vs 17.3 ms sort phase at C4)
-// largest bucket sorted in shared memory: 216 KB per SM over the CTAs
-// (8 B key + 4 B per slot counter + 3 u16 per tuple), a multiple of 128
-constexpr int CAP = (221184 / SORT_CTAS / (8 + 4 * SLOT_X + 6)) / 128 * 128;
+constexpr int SORT_NT = LJ_SORT_NT;
+// largest bucket sorted in shared memory by the main instance: every thread
+// owns LJ_SORT_E tuples (keys and slots in registers); 14 B of shared memory
+// per tuple (8 B key + 4 B slot counter + u16 index)
+constexpr int CAP = SORT_NT * LJ_SORT_E;
+static_assert((size_t)CAP * 14 * SORT_CTAS + 1024 * SORT_CTAS <= 233472, "sort CTAs exceed the SM's shared memory");
 constexpr int RUN_SMALL = 64;     // equal-slot runs ranked element by element
 constexpr int MAX_RUNS = 64;      // longer mixed runs sorted block-wide per bucket
 #ifndef LJ_SORT_U
 #define LJ_SORT_U 4
 #endif
 constexpr int SORT_U = LJ_SORT_U;  // tuples in flight per thread in the load / write-out phases (8: -0.6 %, 12: +0.6 %)
-constexpr int SUB = CAP / 2;      // mean tuples per sub-bucket: sample-quantile slices
-                                  // (~61 sample keys each) stay below CAP
+#ifndef LJ_SUB_DIV
+#define LJ_SUB_DIV 2
+#endif
+constexpr int SUB = CAP / LJ_SUB_DIV;  // mean tuples per sub-bucket: sample-quantile slices stay below CAP
 constexpr int SPLIT_NT = 1024;
 #ifndef LJ_SPLIT_U
 #define LJ_SPLIT_U 4
@@ -580,11 +586,12 @@ __global__ void __launch_bounds__(SPLIT_NT) k_split_scatter(LsjDev md, SplitCtx 
     }
 }
 
-// Block-wide sort of idx[base, base+len) by K[idx[.]]: a bitonic network in
-// its "flip" form, whose comparators all put the minimum at the lower index,
-// so positions >= len act as +inf and their comparators are skipped.
+// Block-wide sort of the pairs (K[i], X[i]), i in [base, base+len), by key: a
+// bitonic network in its "flip" form, whose comparators all put the minimum
+// at the lower index, so positions >= len act as +inf and their comparators
+// are skipped.
 template <int NT>
-__device__ void block_sort_idx(u16 *idx, int base, int len, const u64 *K) {
+__device__ void block_sort_pairs(u64 *K, u16 *X, int base, int len) {
     int w = 1;
     while (w < len) w <<= 1;
     for (int k = 2; k <= w; k <<= 1) {
@@ -597,10 +604,13 @@ __device__ void block_sort_idx(u16 *idx, int base, int len, const u64 *K) {
                 const int i = (t / h) * j + (t % h);
                 const int l = flip ? (i ^ (j - 1)) : (i + h);
                 if (l < len) {
-                    const u16 a = idx[base + i], c = idx[base + l];
-                    if (K[a] > K[c]) {
-                        idx[base + i] = c;
-                        idx[base + l] = a;
+                    const u64 a = K[base + i], c = K[base + l];
+                    if (a > c) {
+                        K[base + i] = c;
+                        K[base + l] = a;
+                        const u16 x = X[base + i];
+                        X[base + i] = X[base + l];
+                        X[base + l] = x;
                     }
                 }
             }
@@ -609,159 +619,202 @@ __device__ void block_sort_idx(u16 *idx, int base, int len, const u64 *K) {
     }
 }
 
-// K8: one CTA per bucket (dynamic work counter), model-placed in smem.
-// Buckets above CAPV go to over_list (ctl->n_over); the "big" instance (one
-// CTA per SM, CAPV = CAP_BIG) sorts that list and passes what exceeds it on.
+// number of keys of the run KP[a, e) that sort before (k at placement p):
+// smaller keys, and equal keys placed earlier
+__device__ __forceinline__ int run_rank(const u64 *KP, int a, int e, int p, u64 k) {
+    int r = 0;
+    for (int q = a; q < e; ++q) {
+        const u64 kq = KP[q];
+        r += (kq < k || (kq == k && q < p)) ? 1 : 0;
+    }
+    return r;
+}
+
+// K8: one CTA per bucket (dynamic work counter), model-placed in shared
+// memory.  Every thread OWNS E = CAPV / NT tuples of the bucket (tuple
+// e * NT + tid) and keeps their keys and (slot, position) in registers:
+//   1. load the keys (E loads in flight), slot = floor((y - ybase) * m /
+//      yspan) in [0, m), count the slots;
+//   2. exclusive scan of the counts;
+//   3. claim a position in the slot's run (shared atomic), key -> KP[pos]:
+//      keys in PLACEMENT order, misordered only inside a slot's run;
+//   4. rank inside the run: runs of <= RUN_DIRECT keys by scanning the run
+//      (one shared load per step); longer runs are first classified -- an
+//      owner whose key differs from the run's first marks the run MIXED --
+//      constant runs (one repeated key) keep their placement order, mixed
+//      runs of <= RUN_SMALL are ranked by scanning, longer ones are queued
+//      for a block-wide bitonic sort;
+//   5. key -> KP[final] (the placement array is dead after the ranking),
+//      tuple index -> IDX[final];
+//   6. write-out in final order, coalesced: key from shared memory, payload
+//      gathered from the bucket (L2-hot), with a sortedness check on the way
+//      (a misordered bucket is re-sorted whole and rewritten: a safety net
+//      that the monotone placement never needs).
+// 14 B of shared memory per tuple.  Buckets above CAPV go to over_list
+// (ctl->n_over); the "big" instance (one CTA per SM, CAPV = CAP_BIG) sorts
+// that list and passes what exceeds it on.
+constexpr int RUN_DIRECT = 8;
 template <class Src, int NT, int CAPV, int CTAS>
 __global__ void __launch_bounds__(NT, CTAS) k_lsj_sort(LsjDev md, Src src, const unsigned long long *nbuckets_dev,
                                                        const ulonglong2 *__restrict__ in, ulonglong2 *out,
                                                        SortCtl *ctl, i64 *over_list) {
+    constexpr int E = CAPV / NT;
+    static_assert(CAPV % NT == 0 && CAPV <= 65536, "tuples per thread / u16 indices");
     md.m.fix();
     const i64 nbuckets = (i64)*nbuckets_dev;
     extern __shared__ __align__(16) unsigned char smem[];
-    u64 *K = reinterpret_cast<u64 *>(smem);              // keys [CAPV]
-    u32 *cnt = reinterpret_cast<u32 *>(K + CAPV);          // slot counts -> cursors [SLOT_X * CAPV]
-    u16 *slot = reinterpret_cast<u16 *>(cnt + SLOT_X * CAPV);  // slot per key [CAPV]
-    u16 *idx = slot + CAPV;                                // placement [CAPV]
-    u16 *ord = idx + CAPV;                                 // final order [CAPV]
+    u64 *KP = reinterpret_cast<u64 *>(smem);           // keys: placement order, then final order [CAPV]
+    u32 *cnt = reinterpret_cast<u32 *>(KP + CAPV);       // slot counts -> cursors -> run ends [CAPV]
+    u16 *IDX = reinterpret_cast<u16 *>(cnt + CAPV);      // tuple of every final position [CAPV]
     __shared__ u32 warp_tot[NT / 32];
-    __shared__ i64 s_b, s_bn;
-    __shared__ int s_bad, s_nruns;
+    __shared__ i64 s_q[2];
+    __shared__ int s_nruns;
     __shared__ int2 s_runs[MAX_RUNS];
-    if (threadIdx.x == 0) s_bn = (i64)atomicAdd(&ctl->next, 1ULL);
-    for (;;) {
-        if (threadIdx.x == 0) {
-            // take the bucket claimed one round ago and claim the next one,
-            // whose tuples stream into L2 (bulk prefetch) while this one sorts
-            s_b = s_bn;
-            s_bn = (i64)atomicAdd(&ctl->next, 1ULL);
-            s_bad = 0;
-            s_nruns = 0;
-            if (s_bn < nbuckets) {
-                const Bucket nx = src.get(s_bn);
-                if (!nx.point && nx.m > 1 && nx.m <= (i64)CAPV)
-                    bulk_prefetch_l2(in + nx.in_base, (unsigned)(nx.m * sizeof(ulonglong2)));
-            }
-        }
-        __syncthreads();
-        const i64 b = s_b;
-        __syncthreads();
+    constexpr u32 MIXED = 0x80000000u;
+    const int tid = threadIdx.x;
+    for (int j = tid; j < CAPV; j += NT) cnt[j] = 0;
+    if (tid == 0) s_q[0] = (i64)atomicAdd(&ctl->next, 1ULL);
+    __syncthreads();
+    for (int par = 0;; par ^= 1) {
+        const i64 b = s_q[par];
         if (b >= nbuckets) break;
+        if (tid == 0) {
+            // claim the next bucket now: its tuples stream into L2 (bulk
+            // prefetch) while this one sorts
+            const i64 nx = (i64)atomicAdd(&ctl->next, 1ULL);
+            s_q[par ^ 1] = nx;
+            s_nruns = 0;
+            if (nx < nbuckets) {
+                const Bucket nk = src.get(nx);
+                if (!nk.point && nk.m > 1 && nk.m <= (i64)CAPV)
+                    bulk_prefetch_l2(in + nk.in_base, (unsigned)(nk.m * sizeof(ulonglong2)));
+            }
+        }
         const Bucket bk = src.get(b);
-        const int m = (int)(bk.m < (i64)CAPV ? bk.m : (i64)CAPV);
-        if (bk.m == 0 || bk.point) continue;
-        if (bk.m == 1) {
-            if (threadIdx.x == 0) out[bk.out_base] = in[bk.in_base];
+        if (bk.m <= 1 || bk.point || bk.m > (i64)CAPV) {
+            if (tid == 0 && !bk.point) {
+                if (bk.m == 1) out[bk.out_base] = in[bk.in_base];
+                if (bk.m > (i64)CAPV) over_list[atomicAdd(&ctl->n_over, 1ULL)] = b;
+            }
+            __syncthreads();
             continue;
         }
-        if (bk.m > CAPV) {
-            if (threadIdx.x == 0) over_list[atomicAdd(&ctl->n_over, 1ULL)] = b;
-            continue;
-        }
-        const int ms = m * SLOT_X;  // placement slots
-        const double scale = (double)ms / (bk.yspan > 0.0 ? bk.yspan : 1.0);
-        for (int j = threadIdx.x; j < ms; j += NT) cnt[j] = 0;
-        __syncthreads();
-        // load keys, place by the model (SORT_U keys in flight per thread)
-        for (int i0 = threadIdx.x; i0 < m; i0 += NT * SORT_U) {
-            u64 k[SORT_U];
+        const int m = (int)bk.m;
+        const ulonglong2 *src_rec = in + bk.in_base;
+        const double scale = (double)m / (bk.yspan > 0.0 ? bk.yspan : 1.0);
+        // 1. keys, slots, slot counts
+        u64 k[E];
+        u32 sp[E];  // slot | position << 16
 #pragma unroll
-            for (int u = 0; u < SORT_U; ++u) {
-                const int i = i0 + u * NT;
-                k[u] = i < m ? in[bk.in_base + i].x : 0;
-            }
+        for (int e = 0; e < E; ++e) {
+            const int i = e * NT + tid;
+            k[e] = i < m ? src_rec[i].x : 0;
+        }
 #pragma unroll
-            for (int u = 0; u < SORT_U; ++u) {
-                const int i = i0 + u * NT;
-                if (i >= m) break;
-                K[i] = k[u];
-                const double f = floor((md.y(k[u]) - bk.ybase) * scale);
-                const int s = f < 0.0 ? 0 : (f >= (double)(ms - 1) ? ms - 1 : (int)f);
-                slot[i] = (u16)s;
-                atomicAdd(cnt + s, 1u);
+        for (int e = 0; e < E; ++e) {
+            const int i = e * NT + tid;
+            if (i < m) {
+                const double f = floor((md.y(k[e]) - bk.ybase) * scale);
+                const int sl = f < 0.0 ? 0 : (f >= (double)(m - 1) ? m - 1 : (int)f);
+                sp[e] = (u32)sl;
+                atomicAdd(cnt + sl, 1u);
             }
         }
         __syncthreads();
-        block_scan_u32<NT>(cnt, ms, warp_tot);
-        for (int i = threadIdx.x; i < m; i += NT) idx[atomicAdd(cnt + slot[i], 1u)] = (u16)i;
-        __syncthreads();
-        // after the scatter cnt[s] = end of slot s's run = start of slot
-        // s+1's, so every element knows its run [cnt[s-1], cnt[s]).  Pass 1
-        // flags mixed runs (an element differing from the run's first key
-        // sets bit 31 of cnt[s]); pass 2: singletons and constant runs copy
-        // through, short mixed runs (<= RUN_SMALL) place each element at its
-        // rank in the run (key, then position), long mixed runs are copied
-        // and sorted block-wide below.
-        constexpr u32 MIXED = 0x80000000u;
-        for (int p = threadIdx.x; p < m; p += NT) {
-            const u16 ip = idx[p];
-            const int si = slot[ip];
-            const int a = si > 0 ? (int)(cnt[si - 1] & ~MIXED) : 0, e = (int)(cnt[si] & ~MIXED);
-            if (e - a > 1 && p != a && K[ip] != K[idx[a]]) atomicOr(cnt + si, MIXED);
+        // 2. run starts
+        block_scan_u32<NT>(cnt, m, warp_tot);
+        // 3. placement: afterwards cnt[s] = end of slot s's run = start of slot s+1's
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int i = e * NT + tid;
+            if (i < m) {
+                const u32 p = atomicAdd(cnt + sp[e], 1u);
+                KP[p] = k[e];
+                sp[e] |= p << 16;
+            }
         }
         __syncthreads();
-        for (int p = threadIdx.x; p < m; p += NT) {
-            const u16 ip = idx[p];
-            const int si = slot[ip];
-            const u32 ce = cnt[si];
-            const int a = si > 0 ? (int)(cnt[si - 1] & ~MIXED) : 0, e = (int)(ce & ~MIXED);
-            if (!(ce & MIXED)) {  // singleton or one repeated key
-                ord[p] = ip;
-                continue;
-            }
-            if (e - a <= RUN_SMALL) {
-                const u64 kv = K[ip];
-                int r = 0;
-                for (int q = a; q < e; ++q) {
-                    const u64 kq = K[idx[q]];
-                    r += (kq < kv || (kq == kv && q < p)) ? 1 : 0;
-                }
-                ord[a + r] = ip;
-                continue;
-            }
-            ord[p] = ip;  // long mixed run: copied, queued by its first element
-            if (p == a) {
-                const int q = atomicAdd(&s_nruns, 1);
-                if (q < MAX_RUNS) {
-                    s_runs[q] = make_int2(p, e - p);
-                } else {
-                    s_bad = 1;
+        // 4. rank in the run -> final position (kept in sp's upper half)
+        int need_long = 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int i = e * NT + tid;
+            if (i < m) {
+                const int sl = (int)(sp[e] & 0xFFFFu), p = (int)(sp[e] >> 16);
+                const int a = sl > 0 ? (int)(cnt[sl - 1] & ~MIXED) : 0, en = (int)(cnt[sl] & ~MIXED);
+                if (en - a > RUN_DIRECT) {
+                    need_long = 1;
+                    if (k[e] != KP[a]) atomicOr(cnt + sl, MIXED);
+                } else if (en - a > 1) {
+                    sp[e] = (u32)sl | ((u32)(a + run_rank(KP, a, en, p, k[e])) << 16);
                 }
             }
         }
-        __syncthreads();
-        const int nruns = s_nruns < MAX_RUNS ? s_nruns : MAX_RUNS;
-        if (!s_bad)
-            for (int q = 0; q < nruns; ++q) block_sort_idx<NT>(ord, s_runs[q].x, s_runs[q].y, K);
-        // safety net: a misordered bucket is re-sorted whole (it fired on
-        // keys routed to empty leaves past the last training key before
-        // y() placed them at the top)
-        for (int i = threadIdx.x; i + 1 < m; i += NT)
-            if (K[ord[i]] > K[ord[i + 1]]) s_bad = 1;
-        __syncthreads();
-        if (s_bad) {
-            // safety net (the placement key is monotone, so this only runs
-            // when too many long runs appeared): sort the whole bucket
-            block_sort_idx<NT>(ord, 0, m, K);
-            if (threadIdx.x == 0) atomicAdd(&ctl->n_fallback, 1ULL);
-        }
-        // write out: key from smem, payload gathered from the bucket (L2-hot)
-        for (int i0 = threadIdx.x; i0 < m; i0 += NT * SORT_U) {
-            u64 p[SORT_U];
-            u16 j[SORT_U];
+        if (__syncthreads_or(need_long)) {
 #pragma unroll
-            for (int u = 0; u < SORT_U; ++u) {
-                const int i = i0 + u * NT;
-                j[u] = i < m ? ord[i] : 0;
-                p[u] = i < m ? __ldg(&in[bk.in_base + j[u]].y) : 0;
+            for (int e = 0; e < E; ++e) {
+                const int i = e * NT + tid;
+                if (i < m) {
+                    const int sl = (int)(sp[e] & 0xFFFFu), p = (int)(sp[e] >> 16);
+                    const u32 ce = cnt[sl];
+                    const int a = sl > 0 ? (int)(cnt[sl - 1] & ~MIXED) : 0, en = (int)(ce & ~MIXED);
+                    if (en - a > RUN_DIRECT && (ce & MIXED)) {
+                        if (en - a <= RUN_SMALL) {
+                            sp[e] = (u32)sl | ((u32)(a + run_rank(KP, a, en, p, k[e])) << 16);
+                        } else if (p == a) {  // long mixed run: sorted block-wide below
+                            const int q = atomicAdd(&s_nruns, 1);
+                            if (q < MAX_RUNS) s_runs[q] = make_int2(a, en - a);
+                        }
+                    }
+                }
             }
+            __syncthreads();
+        }
+        // 5. final order (the ranking's reads of KP are done)
 #pragma unroll
-            for (int u = 0; u < SORT_U; ++u) {
-                const int i = i0 + u * NT;
-                if (i < m) out[bk.out_base + i] = make_ulonglong2(K[j[u]], p[u]);
+        for (int e = 0; e < E; ++e) {
+            const int i = e * NT + tid;
+            if (i < m) {
+                const int f = (int)(sp[e] >> 16);
+                KP[f] = k[e];
+                IDX[f] = (u16)i;
             }
         }
         __syncthreads();
+        const int nruns = s_nruns;
+        if (nruns > MAX_RUNS) {
+            block_sort_pairs<NT>(KP, IDX, 0, m);
+        } else {
+            for (int q = 0; q < nruns; ++q) block_sort_pairs<NT>(KP, IDX, s_runs[q].x, s_runs[q].y);
+        }
+        // 6. write out: key from smem, payload gathered from the bucket
+        // (L2-hot); the slot counters are cleared for the next bucket
+        for (int pass = 0;; ++pass) {
+            int bad = 0;
+            for (int i0 = tid; i0 < m; i0 += NT * SORT_U) {
+                u64 kf[SORT_U], py[SORT_U];
+#pragma unroll
+                for (int u = 0; u < SORT_U; ++u) {
+                    const int i = i0 + u * NT;
+                    kf[u] = i < m ? KP[i] : 0;
+                    py[u] = i < m ? __ldg(&src_rec[IDX[i]].y) : 0;
+                    if (i + 1 < m && kf[u] > KP[i + 1]) bad = 1;
+                }
+#pragma unroll
+                for (int u = 0; u < SORT_U; ++u) {
+                    const int i = i0 + u * NT;
+                    if (i < m) {
+                        out[bk.out_base + i] = make_ulonglong2(kf[u], py[u]);
+                        cnt[i] = 0;
+                    }
+                }
+            }
+            if (!__syncthreads_or(bad)) break;
+            // safety net: the placement key is monotone, so a bucket is
+            // never misordered here; if it is, sort it whole and rewrite
+            block_sort_pairs<NT>(KP, IDX, 0, m);
+            if (tid == 0 && pass == 0) atomicAdd(&ctl->n_fallback, 1ULL);
+        }
     }
 }
 
@@ -1038,11 +1091,11 @@ static size_t al(size_t v) { return (v + 255) & ~(size_t)255; }
 
 // the big instance: one CTA per SM, 1024 threads, everything of up to
 // CAP_BIG tuples in shared memory
-constexpr int CAP_BIG = (221184 / (8 + 4 * SLOT_X + 6)) / 128 * 128;
+constexpr int CAP_BIG = 12288;  // 12 tuples per thread, 168 KB
 
 template <int CAPV>
 static size_t sort_smem_bytes() {
-    return sizeof(u64) * CAPV + sizeof(u32) * SLOT_X * CAPV + 3 * sizeof(u16) * CAPV;
+    return (sizeof(u64) + sizeof(u32) + sizeof(u16)) * CAPV;
 }
 
 template <class Src, int NT, int CAPV, int CTAS>

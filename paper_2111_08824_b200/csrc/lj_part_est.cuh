@@ -26,6 +26,13 @@ constexpr i64 EST_PAD = 4096;
 constexpr int EST_TILE = 4096;
 constexpr size_t EST_STAGE = (size_t)EST_TILE * 16;
 
+// shared memory of the claims scatter beside the bin table and the ring:
+// tile histogram, run starts (u32), region starts, output deltas (i64),
+// the tile permutation (u32)
+inline size_t est_fix_bytes(size_t nb4) {
+    return 2 * nb4 * sizeof(u32) + (nb4 + 32) * sizeof(i64) + nb4 * sizeof(i64) + (size_t)EST_TILE * 4;
+}
+
 // capacity of the output (records) for n tuples in nb bins: regions + overflow
 inline i64 est_capacity(i64 n, int nb) { return n + n / 16 + (i64)nb * (EST_PAD + EST_STRIDE + 1) + 64 + n; }
 
@@ -99,7 +106,7 @@ static __global__ void k_est_caps(const u32 *est, int nbins, int exact, i64 *cap
 // stores through a symmetric-memory pointer) -- so out is null and there
 // is no overflow check.
 template <class Src, bool STORED, bool PEER = false>
-__global__ void __launch_bounds__(PART2_NT) k_bin_scatter_est(Src f0, i64 n, i64 chunk, int nbins, int nst,
+__global__ void __launch_bounds__(PART2_NT, 1) k_bin_scatter_est(Src f0, i64 n, i64 chunk, int nbins, int nst,
                                                               const i64 *__restrict__ rstart, u32 *gcur,
                                                               unsigned long long *ovf, ulonglong2 *out,
                                                               const u16 *__restrict__ codes) {
@@ -114,11 +121,13 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_est(Src f0, i64 n, i64
     const int nb4 = (nbins + 31) & ~31;
     u32 *thist = reinterpret_cast<u32 *>(smem);  // this tile's count per bin
     u32 *tstart = thist + nb4;                   // this tile's run start per bin
-    u32 *gbase = tstart + nb4;                   // claimed position of the run in its bin
-    i64 *srst = reinterpret_cast<i64 *>(gbase + nb4);  // region starts [nbins + 1]
-    u16 *perm = reinterpret_cast<u16 *>(srst + nb4 + 32);
-    u16 *tbin2 = perm + EST_TILE;                // bin of every tuple of the tile (double-buffered by tile parity)
-    unsigned char *ring = reinterpret_cast<unsigned char *>(perm) + ((EST_TILE * 6 + 127) & ~127);
+    i64 *srst = reinterpret_cast<i64 *>(tstart + nb4);  // region starts [nbins + 1]
+    // output position of the tile-sorted tuple i of bin b = dlt[b] + i
+    // (region start + claimed position of the run - the run's start in the tile)
+    i64 *dlt = srst + nb4 + 32;
+    // tile permutation sorted by bin: tile index | bin << 16
+    u32 *perm = reinterpret_cast<u32 *>(dlt + nb4);
+    unsigned char *ring = reinterpret_cast<unsigned char *>(perm) + EST_TILE * 4;
     __shared__ __align__(8) uint64_t full[PT_MAXST];
     __shared__ u32 wsum[PART2_NT / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, shift = f.f.shift;
@@ -126,8 +135,7 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_est(Src f0, i64 n, i64
     for (int j = tid; j <= nbins; j += PART2_NT) srst[j] = rstart[j];
     const i64 lo = blockIdx.x * chunk, hi = min(lo + chunk, n);
     const int ntiles = hi > lo ? (int)((hi - lo + EST_TILE - 1) / EST_TILE) : 0;
-    auto issue = [&](int t) {
-        const int s = t % nst;
+    auto issue = [&](int t, int s) {
         const i64 base = lo + (i64)t * EST_TILE;
         const int cnt = (int)min((i64)EST_TILE, hi - base);
         const unsigned b8 = (unsigned)(cnt * 8) & ~15u;
@@ -147,23 +155,24 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_est(Src f0, i64 n, i64
     if (tid == 0) {
         for (int s = 0; s < nst; ++s) mbar_init(&full[s], 1);
         mbar_init_fence();
-        for (int t = 0; t < min(nst - 1, ntiles); ++t) issue(t);
+        for (int t = 0; t < min(nst - 1, ntiles); ++t) issue(t, t);
     }
     __syncthreads();
-    // Four barriers per tile: the tile's bins are double-buffered, so the
-    // next tile's binning (1) may start while slower warps still write this
-    // tile's runs (4); the run claims (global atomics) are issued before
-    // the scan and their results are stored only after the permutation,
-    // so their latency overlaps both.
+    // Four barriers per tile.  The next tile's binning (1) may start while
+    // slower warps still write this tile's runs (4): (1) writes only the
+    // tile histogram, which (4) does not read.  The run claims (global
+    // atomics) are issued before the scan and their results are used only
+    // after it, so their latency overlaps the scan.
+    int s = 0;           // ring stage of tile t
+    unsigned phase = 0;  // its mbarrier phase
+    int sn = nst - 1;    // stage refilled during tile t (tile t + nst - 1)
     for (int t = 0; t < ntiles; ++t) {
-        const int s = t % nst;
-        mbar_wait(&full[s], (unsigned)(t / nst) & 1u);
+        mbar_wait(&full[s], phase);
         const i64 base = lo + (i64)t * EST_TILE;
         const int cnt = (int)min((i64)EST_TILE, hi - base), nb = cnt & ~1, nb8 = cnt & ~7;
         const unsigned char *st = ring + (size_t)s * STAGE;
         const u64 *ks = reinterpret_cast<const u64 *>(st), *ps = ks + EST_TILE;
         const u16 *cs = reinterpret_cast<const u16 *>(st + EST_TILE * 16);
-        u16 *tbin = tbin2 + (t & 1) * EST_TILE;
         // (1) bin of every tuple and its rank in the tile's run
         int bj[U], rj[U];
 #pragma unroll
@@ -175,18 +184,16 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_est(Src f0, i64 n, i64
                 bj[u] = j < cnt ? (int)(f.code(j < nb ? ks[j] : ld_stream(f.keys + base + j)) >> shift) : -1;
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            rj[u] = bj[u] >= 0 ? (int)atomicAdd(thist + bj[u], 1u) : 0;
-            if (bj[u] >= 0) tbin[u * PART2_NT + tid] = (u16)bj[u];
-        }
+        for (int u = 0; u < U; ++u) rj[u] = bj[u] >= 0 ? (int)atomicAdd(thist + bj[u], 1u) : 0;
         __syncthreads();
         // every warp is past tile t-1's writes: its stage may be refilled
-        if (tid == 0 && t + nst - 1 < ntiles) issue(t + nst - 1);
+        if (tid == 0 && t + nst - 1 < ntiles) issue(t + nst - 1, sn);
         // (2) claim every run in its bin (one global atomic each), then the
         // exclusive scan of the tile histogram -> run starts
         const u32 v0 = 2 * tid < nbins ? thist[2 * tid] : 0, v1 = 2 * tid + 1 < nbins ? thist[2 * tid + 1] : 0;
         const u32 g0 = v0 ? atomicAdd(gcur + 2 * tid, v0) : 0;
         const u32 g1 = v1 ? atomicAdd(gcur + 2 * tid + 1, v1) : 0;
+        u32 r0;
         {
             const u32 tot = v0 + v1;
             u32 inc = tot;
@@ -208,7 +215,7 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_est(Src f0, i64 n, i64
                 wsum[lane] = wi - w;
             }
             __syncthreads();
-            const u32 r0 = wsum[warp] + inc - tot;
+            r0 = wsum[warp] + inc - tot;
             if (2 * tid < nbins) {
                 tstart[2 * tid] = r0;
                 thist[2 * tid] = 0;
@@ -222,25 +229,30 @@ __global__ void __launch_bounds__(PART2_NT) k_bin_scatter_est(Src f0, i64 n, i64
         // (3) tile permutation sorted by bin; the claims land
 #pragma unroll
         for (int u = 0; u < U; ++u)
-            if (bj[u] >= 0) perm[tstart[bj[u]] + rj[u]] = (u16)(u * PART2_NT + tid);
-        if (v0) gbase[2 * tid] = g0;
-        if (v1) gbase[2 * tid + 1] = g1;
+            if (bj[u] >= 0) perm[tstart[bj[u]] + rj[u]] = (u32)(u * PART2_NT + tid) | ((u32)bj[u] << 16);
+        if (v0) dlt[2 * tid] = srst[2 * tid] + (i64)g0 - (i64)r0;
+        if (v1) dlt[2 * tid + 1] = srst[2 * tid + 1] + (i64)g1 - (i64)(r0 + v0);
         __syncthreads();
         // (4) write bin runs into their regions (overflow behind the regions)
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int i = u * PART2_NT + tid;
             if (i < cnt) {
-                const int j = perm[i];
+                const u32 pj = perm[i];
+                const int j = (int)(pj & 0xFFFFu), b = (int)(pj >> 16);
                 const u64 k = j < nb ? ks[j] : ld_stream(f.keys + base + j);
                 const u64 p = j < nb ? ps[j] : ld_stream(f.pay + base + j);
-                const int b = tbin[j];
-                i64 dst = srst[b] + (i64)gbase[b] + (i - (int)tstart[b]);
-                if (!PEER && dst >= srst[b + 1]) dst = srst[nbins] + (i64)atomicAdd(ovf, 1ULL);
+                i64 dst = dlt[b] + i;
+                if (!PEER && !STORED && dst >= srst[b + 1]) dst = srst[nbins] + (i64)atomicAdd(ovf, 1ULL);
                 ulonglong2 *o = PEER ? reinterpret_cast<ulonglong2 *>((uintptr_t)dst << 4) : out + dst;
                 *o = make_ulonglong2(k, p);
             }
         }
+        if (++s == nst) {
+            s = 0;
+            phase ^= 1u;
+        }
+        if (++sn == nst) sn = 0;
     }
 }
 
@@ -417,8 +429,7 @@ int run_partition_claims(const Src &f, i64 n, int nbins, int exact, ulonglong2 *
     if (n > 0) {
         const PartPlan p = part_plan(n, nbins);
         const size_t nb4 = (size_t)((nbins + 31) & ~31);
-        const size_t fix = (stored ? 0 : tb) + 3 * nb4 * sizeof(u32) + (nb4 + 32) * sizeof(i64) +
-                           (((size_t)EST_TILE * 6 + 127) & ~(size_t)127);
+        const size_t fix = (stored ? 0 : tb) + est_fix_bytes(nb4);
         const size_t stage = EST_STAGE + (stored ? EST_TILE * 2 : 0);
         const int nst = fix < (size_t)PT_SMEM_MAX ? (int)min((size_t)PT_MAXST, (PT_SMEM_MAX - fix) / stage) : 0;
         if (nst < 2) {
@@ -494,7 +505,7 @@ int shuffle_scatter(const Src &f, i64 n, int nbins, const i64 *bases, void *ws, 
     LJ_CK(cudaMemsetAsync(gcur, 0, sizeof(u32) * (size_t)nbins, st));
     const PartPlan p = part_plan(n, nbins);
     const size_t nb4 = (size_t)((nbins + 31) & ~31);
-    const size_t fix = 3 * nb4 * sizeof(u32) + (nb4 + 32) * sizeof(i64) + (((size_t)EST_TILE * 6 + 127) & ~(size_t)127);
+    const size_t fix = est_fix_bytes(nb4);
     const size_t stage = EST_STAGE + EST_TILE * 2;
     const int nst = (int)min((size_t)PT_MAXST, (PT_SMEM_MAX - fix) / stage);
     k_bin_scatter_est<Src, true, true><<<p.blocks, PART2_NT, fix + nst * stage, st>>>(

@@ -1,0 +1,10 @@
+O=gpurun_out/exp3
+mkdir -p $O
+rm -rf gpurun_out/var
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+python tools/kprof.py c4 > $O/kprof_c4.txt 2>&1
+python tools/kprof.py c2 > $O/kprof_c2.txt 2>&1
+python tools/kprof.py c3 > $O/kprof_c3.txt 2>&1
+bash tools/gpu_variants.sh lj_lsj.cu "python tools/kprof.py c4" "-DLJ_SORT_CTAS=5" "-DLJ_SORT_E=8 -DLJ_SORT_NT=384" "-DLJ_SORT_E=6 -DLJ_SORT_NT=512 -DLJ_SORT_CTAS=2" "-DLJ_SORT_E=8 -DLJ_SORT_NT=256 -DLJ_SORT_CTAS=5"
+cp gpurun_out/var/out.txt $O/variants.txt; cp gpurun_out/var/err.txt $O/variants.err
