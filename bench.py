@@ -519,6 +519,28 @@ def run_b200(args):
                 "peak_kind": peak_kind, "algorithmic_bytes": run_step.bytes_note,
                 "step_frac": (ALGO_BYTES[inp.algorithm] * (n_s if index is not None else n_r + n_s))
                 / (ms_per_step / 1e3) / 1e9 / peak}
+    if run_step.kernel == "k_grmi_probe_staged" and hasattr(index, "probe_records"):
+        # ablation: the staged probe without the reference's probe counter
+        # (search_steps): the staged search never uses the model's prediction,
+        # so its evaluation goes with the counter; the checksum is unchanged
+        nc = []
+        o2 = torch.zeros(4, dtype=torch.int64, device=dev)
+        for i in range(args.steps):
+            flush.zero_()
+            run_step.parts[0][1](o2)  # regroup S (the probe consumes the grouped records)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            index.probe_records(n_s, run_step.scratch, o2, count_steps=False)
+            e1.record()
+            torch.cuda.synchronize()
+            nc.append(e0.elapsed_time(e1))
+        nc_ms = statistics.mean(nc)
+        w2 = o2.cpu().tolist()
+        roofline["no_probe_counter"] = {
+            "kernel_ms": nc_ms, "achieved": run_step.dom_bytes / (nc_ms / 1e3) / 1e9,
+            "frac": run_step.dom_bytes / (nc_ms / 1e3) / 1e9 / peak,
+            "same_checksum": [v & MASK for v in w2[:3]] == [w[0] & MASK, w[1] & MASK, xor_all],
+            "note": "probe_records(count_steps=False): no search_steps, no model evaluation"}
     if phase_ms:
         # LSJ per phase (partition 32 B, sort 32 B, merge 16 B per tuple of |R| + |S|)
         roofline["lsj_phases"] = {}

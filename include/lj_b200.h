@@ -243,7 +243,10 @@ int lj_leaf_bucket(const LjGrmi *idx, const uint64_t *keys, const uint64_t *pay,
  * entries in shared memory and searches there, the overflow records take the
  * plain K1; results and search_steps equal lj_grmi_probe's (the reference's
  * probe count follows from the predicted slot and the key's position).  ws:
- * 8 bytes of device scratch (work counter). */
+ * 8 bytes of device scratch (work counter).  accumulate: bit 0 = add to out
+ * instead of overwriting it; bit 1 = leave the reference's probe counter
+ * (out[3]) and with it the model evaluation out (the staged search finds
+ * the lower bound through the window's radix table; an ablation). */
 int lj_grmi_probe_bucketed(const LjGrmi *idx, const uint64_t *s_pairs, const int64_t *reg, void *ws, uint64_t *out,
                            int accumulate, void *stream);
 /* The window staging of the probe above, precomputed once per index: for

@@ -432,6 +432,13 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_stage_image(GrmiDev g, int
     }
 }
 
+// COUNT: also reproduce the reference's probe counter (search_steps,
+// gapped.py:86-160): the model's predicted slot of every probe and the
+// closed-form count from (predicted slot, lower bound, run end).  The staged
+// search itself never needs the prediction -- the window's radix table
+// finds the lower bound -- so without the counter the model evaluation goes
+// too (out[3] stays 0).
+template <bool COUNT>
 __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, const ulonglong2 *__restrict__ rec,
                                                                    const i64 *__restrict__ reg, int nwin, int shift,
                                                                    unsigned long long *work,
@@ -557,6 +564,10 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
                 }
 #pragma unroll
                 for (int u = 0; u < STAGE_U; ++u) {
+                    if (!COUNT) {
+                        start[u] = 0;
+                        continue;
+                    }
                     // models.py:112-124 + gapped.py:258-261, the leaf from smem
                     // the same operations as RmiDev::pos + SlotMap in 32-bit
                     // integers (n <= L < 2^30 on this path; saturating
@@ -626,7 +637,7 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
                             x ^= t2;
                         }
                         const int re0 = ja == f0 ? 0 : (int)ja;  // absent (k < entry 0): [0, 0)
-                        steps += (u64)ref_probe_count(start[u], 0, re0, lim, zero);
+                        if (COUNT) steps += (u64)ref_probe_count(start[u], 0, re0, lim, zero);
                         continue;
                     }
                     int iu = il;
@@ -659,7 +670,7 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
                         }
                         re = (int)(ja - slo);
                     }
-                    steps += (u64)ref_probe_count(start[u], lb, re, lim, zero);
+                    if (COUNT) steps += (u64)ref_probe_count(start[u], lb, re, lim, zero);
                     if (dbg) {
                         i64 *dp = dbg + 4 * (a + t0 + u * STAGE_NT);
                         dp[0] = lb + slo;
@@ -966,6 +977,10 @@ static int probe_bucketed(const LjGrmi *idx, const uint64_t *s_pairs, const int6
                           const unsigned char *img, uint64_t *out, int accumulate, void *stream) {
     LJ_REQUIRE(idx != nullptr, "null index");
     cudaStream_t st = as_stream(stream);
+    // accumulate: bit 0 = add to out instead of overwriting it; bit 1
+    // (LJ_PROBE_NO_STEPS) = skip the reference's probe counter
+    const bool count_steps = !(accumulate & 2);
+    accumulate &= 1;
     if (!accumulate) LJ_CK(cudaMemsetAsync(out, 0, 4 * sizeof(u64), st));
     if (idx->n == 0) return LJ_OK;
     const int shift = slot_window_shift(idx->L);
@@ -986,7 +1001,10 @@ static int probe_bucketed(const LjGrmi *idx, const uint64_t *s_pairs, const int6
     }
     static unsigned long long attr = 0;  // one bit per device
     if (once_per_device(attr)) {
-        LJ_CK(cudaFuncSetAttribute(k_grmi_probe_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        LJ_CK(cudaFuncSetAttribute(k_grmi_probe_staged<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   220 * 1024));
+        LJ_CK(cudaFuncSetAttribute(k_grmi_probe_staged<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   220 * 1024));
     }
     unsigned long long *work = reinterpret_cast<unsigned long long *>(ws);
     LJ_CK(cudaMemsetAsync(work, 0, sizeof(unsigned long long), st));
@@ -1007,8 +1025,12 @@ static int probe_bucketed(const LjGrmi *idx, const uint64_t *s_pairs, const int6
         LJ_CK(cudaMalloc(&dbg, (size_t)nk * 4 * sizeof(i64)));
         LJ_CK(cudaMemsetAsync(dbg, 0xff, (size_t)nk * 4 * sizeof(i64), st));
     }
-    k_grmi_probe_staged<<<sm_count(), STAGE_NT, sm, st>>>(gd, reinterpret_cast<const ulonglong2 *>(s_pairs), reg,
-                                                          nwin, shift, work, out, trace, dbg, img);
+    if (count_steps)
+        k_grmi_probe_staged<true><<<sm_count(), STAGE_NT, sm, st>>>(gd, reinterpret_cast<const ulonglong2 *>(s_pairs),
+                                                                    reg, nwin, shift, work, out, trace, dbg, img);
+    else
+        k_grmi_probe_staged<false><<<sm_count(), STAGE_NT, sm, st>>>(gd, reinterpret_cast<const ulonglong2 *>(s_pairs),
+                                                                     reg, nwin, shift, work, out, trace, dbg, img);
     LJ_CK_LAUNCH();
     if (dbg) {
         std::vector<i64> h((size_t)nk * 4);

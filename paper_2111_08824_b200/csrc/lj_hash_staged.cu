@@ -65,6 +65,9 @@ static inline size_t part_align_c(size_t v) { return (v + 255) & ~(size_t)255; }
 #ifndef LJ_HS_NC
 #define LJ_HS_NC 1024
 #endif
+#ifndef LJ_HS_SPREAD
+#define LJ_HS_SPREAD 2  // probe-table slots per position (the first slot of a position is even: one 32-B pair)
+#endif
 #ifndef LJ_HS_ROUNDS
 #define LJ_HS_ROUNDS 1  // forward slot scan in rounds of one pair per unfinished probe (0: slot by slot)
 #endif
@@ -78,6 +81,9 @@ constexpr int HS_NC = LJ_HS_NC;      // lower-bound cells per window
 constexpr i64 HS_PIECE = LJ_HS_PIECE;  // records per work item
 constexpr int HS_MAXWIN = 2048;
 constexpr int HS_WPT = (HS_MAXWIN + HS_NT - 1) / HS_NT;  // windows per thread in the piece prefix
+
+// first slot of position p in the probe table (monotone, even)
+__host__ __device__ __forceinline__ i64 slot_of_pos(i64 p) { return (p * LJ_HS_SPREAD) & ~(i64)1; }
 
 struct WinMeta {
     u64 klo, khi;
@@ -105,7 +111,7 @@ __device__ __forceinline__ i64 lower_bound_u64(const u64 *a, i64 n, u64 k) {
 __global__ void k_slots_t(SplineDev m, const u64 *sk, const u64 *sp, i64 n, i64 *t, unsigned long long *cnt) {
     u32 z = 0, d = 0;
     for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < n; j += (i64)gridDim.x * blockDim.x) {
-        t[j] = 2 * m.pos(sk[j]) - j;
+        t[j] = slot_of_pos(m.pos(sk[j])) - j;
         z += sp[j] == 0;
         d += j > 0 && sk[j] == sk[j - 1];
     }
@@ -122,7 +128,7 @@ struct MaxI64 {
 __global__ void k_slots_size(const i64 *M, i64 n, unsigned long long *zero, i64 *plan) {
     const i64 last = (n - 1) + M[n - 1];
     i64 L = last + 1;
-    if (L < 2 * (n - 1) + 2) L = 2 * (n - 1) + 2;
+    if (L < slot_of_pos(n - 1) + 2) L = slot_of_pos(n - 1) + 2;
     L = (L + 1) & ~(i64)1;
     plan[0] = L + 2;
     plan[1] = (i64)zero[0];
@@ -477,9 +483,9 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
             for (int u = 0; u < HS_U; ++u) {
                 // (one unsigned compare covers klo <= k <= khi; the reserved
                 // key of gap records / past the item lies outside every window)
-                if (staged && k[u] - ss.klo <= ss.span) s0[u] = 2 * (i64)ss.pos(k[u]);
+                if (staged && k[u] - ss.klo <= ss.span) s0[u] = slot_of_pos((i64)ss.pos(k[u]));
                 else if (k[u] == ~0ULL) s0[u] = -1;
-                else s0[u] = 2 * spline_pos_global(m, k[u]);
+                else s0[u] = slot_of_pos(spline_pos_global(m, k[u]));
             }
             // every probe's first slot PAIR (32 B, aligned: one sector) in flight at once
             u64 e[HS_U][4];

@@ -93,7 +93,7 @@ struct KeyRangeBin {
         const u64 *B = g + 4;
         const u64 *cw = g + 4 + ((nb + 3) & ~3);
         const u16 *cells = reinterpret_cast<const u16 *>(cw);
-        const u64 t = kb_image(k, (int)(ctl >> 8));
+        const u64 t = kb_image(k, (int)(ctl >> 8) & 1);
         const u32 c = kb_cell(t, t0, (int)(ctl & 63));
         int lo = cells[c], hi = cells[c + 1];
         const int ns = kb_nsub(nb);
@@ -113,12 +113,14 @@ struct KeyRangeBin {
         // two unconditional, branch-free steps settle every range of <= 3
         // boundaries (a step on lo == hi is a no-op: B[lo] <= k there, B[0] =
         // 0), so consecutive evaluations overlap; longer ranges finish in the loop
+        if (ctl & 0x10000u) {  // dense boundary sets only (most cells non-empty ranges)
 #pragma unroll
-        for (int it = 0; it < 2; ++it) {
-            const int mid = (lo + hi + 1) >> 1;
-            const bool ge = B[mid] <= k;
-            lo = ge ? mid : lo;
-            hi = ge ? hi : mid - 1;
+            for (int it = 0; it < 2; ++it) {
+                const int mid = (lo + hi + 1) >> 1;
+                const bool ge = B[mid] <= k;
+                lo = ge ? mid : lo;
+                hi = ge ? hi : mid - 1;
+            }
         }
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
@@ -207,7 +209,9 @@ static __global__ void __launch_bounds__(1024) k_keybin_build(u64 *lay, int nb) 
     const int ns = kb_nsub(nb);
     if (tid == 0) {
         lay[0] = s_t0[m];
-        lay[1] = (u64)s_shift[m] | ((u64)m << 8);
+        // bit 16: the search starts with two unconditional steps (sets with a
+        // boundary for at least every eighth cell)
+        lay[1] = (u64)s_shift[m] | ((u64)m << 8) | ((u64)(nb * 8 >= KB_CELLS ? 1 : 0) << 16);
         lay[2] = (u64)nb;
         s_nsub = 0;
     }

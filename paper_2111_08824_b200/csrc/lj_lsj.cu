@@ -165,12 +165,34 @@ __global__ void k_sample_pos(RmiDev m, const u64 *sample, i64 total, i64 *spos) 
         spos[i] = m.pos_sat(u64_to_f64(sample[i]));
 }
 
-// pb[0] = 0, pb[j] = spos[floor(j*S/nb)], pb[nb] = trained_len
+// pb[0] = 0, pb[j] = spos[floor(j*S/nb)], pb[nb] = trained_len.  A key
+// repeated so often that it spans several sample quantiles repeats its
+// position v as a boundary; the repeats move to v + 1 (capped by the next
+// distinct boundary), so the bin that starts at v holds position v alone --
+// the hot key -- and the keys after it get a bin of ordinary size instead of
+// sharing one giant bucket, where the split's slice cap left them in slices
+// far above the sort's capacity (C4's S: 13 M tuples through the big
+// instance).  Still non-decreasing; the bins in between are empty.
 __global__ void k_bin_bounds(const i64 *spos, i64 total, int nb, i64 tl, i64 *pb) {
+    auto raw = [&](int j) -> i64 {
+        if (j <= 0) return 0;
+        if (j >= nb) return tl;
+        return spos[(i64)(((unsigned __int128)j * (u64)total) / (u64)nb)];
+    };
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= nb; j += gridDim.x * blockDim.x) {
-        if (j == 0) pb[j] = 0;
-        else if (j == nb) pb[j] = tl;
-        else pb[j] = spos[(i64)(((unsigned __int128)j * (u64)total) / (u64)nb)];
+        i64 v = raw(j);
+        if (j >= 1 && j < nb && raw(j - 1) == v) {
+            i64 nx = tl;
+            for (int q = j + 1; q < nb; ++q) {
+                const i64 r = raw(q);
+                if (r > v) {
+                    nx = r;
+                    break;
+                }
+            }
+            v = v + 1 < nx ? v + 1 : nx;
+        }
+        pb[j] = v;
     }
 }
 
@@ -670,6 +692,7 @@ __global__ void __launch_bounds__(NT, CTAS) k_lsj_sort(LsjDev md, Src src, const
     __shared__ i64 s_q[2];
     __shared__ int s_nruns;
     __shared__ int2 s_runs[MAX_RUNS];
+    __shared__ u64 s_mm[2 * (NT / 32)];  // per-warp key min / max (flat-model buckets)
     constexpr u32 MIXED = 0x80000000u;
     const int tid = threadIdx.x;
     for (int j = tid; j < CAPV; j += NT) cnt[j] = 0;
@@ -694,7 +717,12 @@ __global__ void __launch_bounds__(NT, CTAS) k_lsj_sort(LsjDev md, Src src, const
         if (bk.m <= 1 || bk.point || bk.m > (i64)CAPV) {
             if (tid == 0 && !bk.point) {
                 if (bk.m == 1) out[bk.out_base] = in[bk.in_base];
-                if (bk.m > (i64)CAPV) over_list[atomicAdd(&ctl->n_over, 1ULL)] = b;
+                if (bk.m > (i64)CAPV) {
+                    over_list[atomicAdd(&ctl->n_over, 1ULL)] = b;
+#ifdef LJ_SORT_DIAG
+                    printf("over %d %lld %lld %f %f\n", CAPV, (long long)b, (long long)bk.m, bk.ybase, bk.yspan);
+#endif
+                }
             }
             __syncthreads();
             continue;
@@ -710,11 +738,48 @@ __global__ void __launch_bounds__(NT, CTAS) k_lsj_sort(LsjDev md, Src src, const
             const int i = e * NT + tid;
             k[e] = i < m ? src_rec[i].x : 0;
         }
+        // A bucket over which the model is FLAT (keys clamped to one leaf
+        // bound: C4's S has 12 M such tuples) would put every key into one
+        // slot and be bitonic-sorted whole: it is placed by linear
+        // interpolation over its own key range instead (monotone in the key
+        // like the model, so everything after is unchanged).
+        const bool flat = !(bk.yspan > 0.0);
+        u64 kmin = 0;
+        double sc = scale;
+        if (flat) {
+            u64 kmax = 0;
+            kmin = ~0ULL;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                if (e * NT + tid < m) {
+                    kmin = k[e] < kmin ? k[e] : kmin;
+                    kmax = k[e] > kmax ? k[e] : kmax;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const u64 a = __shfl_xor_sync(0xffffffffu, kmin, o), c = __shfl_xor_sync(0xffffffffu, kmax, o);
+                kmin = a < kmin ? a : kmin;
+                kmax = c > kmax ? c : kmax;
+            }
+            if ((tid & 31) == 0) {
+                s_mm[2 * (tid >> 5)] = kmin;
+                s_mm[2 * (tid >> 5) + 1] = kmax;
+            }
+            __syncthreads();
+#pragma unroll 1
+            for (int w = 0; w < NT / 32; ++w) {
+                kmin = s_mm[2 * w] < kmin ? s_mm[2 * w] : kmin;
+                kmax = s_mm[2 * w + 1] > kmax ? s_mm[2 * w + 1] : kmax;
+            }
+            sc = (double)m / (u64_to_f64(kmax - kmin) + 1.0);
+        }
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const int i = e * NT + tid;
             if (i < m) {
-                const double f = floor((md.y(k[e]) - bk.ybase) * scale);
+                const double v = flat ? u64_to_f64(k[e] - kmin) : md.y(k[e]) - bk.ybase;
+                const double f = floor(v * sc);
                 const int sl = f < 0.0 ? 0 : (f >= (double)(m - 1) ? m - 1 : (int)f);
                 sp[e] = (u32)sl;
                 atomicAdd(cnt + sl, 1u);

@@ -233,10 +233,16 @@ def fused_shuffle(r_keys, r_payloads, s_keys, s_payloads, model, group=None):
         _lib.check(lib.lj_lsj_shuffle_scatter(ctypes.byref(c), _lib.ptr(k), _lib.ptr(p), k.numel(), _lib.ptr(bases),
                                               _lib.ptr(wss[i]), wss[i].numel(), _lib.stream_ptr()),
                    "lsj_shuffle_scatter")
-    # every rank's scatter complete before any rank reads its buffer
-    torch.cuda.current_stream(dev).synchronize()
-    if world > 1:
-        dist.barrier(group=group)
+    # every rank's scatter complete before any rank reads its buffer: the
+    # symmetric-memory barrier is a device-side signal / wait over the peers'
+    # signal pads, ordered on the stream after the scatters (no host
+    # synchronize); older handles fall back to a host sync + group barrier
+    if hasattr(hdl, "barrier") and os.environ.get("LJ_SHUFFLE_HOST_BARRIER") is None:
+        hdl.barrier()
+    else:
+        torch.cuda.current_stream(dev).synchronize()
+        if world > 1:
+            dist.barrier(group=group)
     rec = buf.view(-1, 2)
     nr, ns = int(recv_r[rank]), int(recv_s[rank])
     return rec[:nr], rec[nr:nr + ns], hdl

@@ -162,13 +162,19 @@ class GappedRmiIndex:
                 self._stage_img = img
         return self._stage_img
 
-    def probe_records(self, n: int, scratch: dict, out: torch.Tensor, accumulate: bool = False, stream=None) -> None:
-        """Staged K1 over the n records bucket_records left in scratch."""
+    def probe_records(self, n: int, scratch: dict, out: torch.Tensor, accumulate: bool = False, stream=None,
+                      count_steps: bool = True) -> None:
+        """Staged K1 over the n records bucket_records left in scratch.
+        ``count_steps=False`` leaves the reference's probe counter
+        (search_steps, out[3]) out: the staged search never needs the model's
+        prediction, so its evaluation goes with the counter (ablation; the
+        checksum words are unchanged)."""
         g = self.c_struct()
         img = self.stage_image(stream)
+        flags = int(bool(accumulate)) | (0 if count_steps else 2)
         _lib.check(_lib.lib().lj_grmi_probe_bucketed_img(ctypes.byref(g), _lib.ptr(scratch["pairs"]),
                                                          _lib.ptr(scratch["regions"]), _lib.ptr(scratch["work"]),
-                                                         _lib.ptr(img), _lib.ptr(out), int(bool(accumulate)),
+                                                         _lib.ptr(img), _lib.ptr(out), flags,
                                                          _lib.stream_ptr(stream)), "grmi_probe_bucketed")
         return out
 
