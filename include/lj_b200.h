@@ -369,6 +369,22 @@ int lj_lsj_bins_from_bounds(const int64_t *pb, int64_t nbins, int64_t trained_le
 size_t lj_lsj_partition_workspace_bytes(int64_t n, int64_t nbins);
 int lj_lsj_partition(const LjLsjModel *model, const uint64_t *keys, const uint64_t *pay, int64_t n,
                      uint64_t *pairs, int64_t *starts, void *ws, size_t ws_bytes, void *stream);
+/* The same partition in ONE pass (no exact counting pass): a 1/16 strided
+ * sample of the keys sizes a region per bin (estimate * 17/16 + 4096), the
+ * scatter claims run by run.  pairs: lj_lsj_partition_regions_capacity(n,
+ * nbins) records; reg[2 nbins + 2]: bin b = records [reg[b], reg[nbins + 1 +
+ * b]) of pairs (gaps between the bins), reg[2 nbins + 1] = 0.  Should a
+ * region overflow (the slack is many standard deviations of the estimate),
+ * the exact two-pass partition runs over the same buffer instead -- its
+ * kernels are always enqueued and return at once otherwise, so the decision
+ * stays on the device.  Needs 16-B aligned columns, nbins <= 2048, n < 2^32.
+ * lj_lsj_sort_regions sorts such regions into the dense pairs_out and
+ * returns the bins' dense starts[nbins+1] (what lj_lsj_partition's starts
+ * are for lj_lsj_sort; lj_lsj_join takes them as r_starts). */
+int64_t lj_lsj_partition_regions_capacity(int64_t n, int64_t nbins);
+size_t lj_lsj_partition_regions_workspace_bytes(int64_t n, int64_t nbins);
+int lj_lsj_partition_regions(const LjLsjModel *model, const uint64_t *keys, const uint64_t *pay, int64_t n,
+                             uint64_t *pairs, int64_t *reg, void *ws, size_t ws_bytes, void *stream);
 /* The exact key-range bin function the partition passes evaluate in
  * shared memory (lj_keybin.cuh): bins[i] = #{ j in [1, nbins) :
  * bounds[j] <= keys[i] } for non-decreasing bounds (bounds[0] ignored).
@@ -399,6 +415,9 @@ int lj_lsj_shuffle_scatter(const LjLsjModel *model, const uint64_t *keys, const 
 size_t lj_lsj_sort_workspace_bytes(int64_t n, int64_t nbins);
 int lj_lsj_sort(const LjLsjModel *model, const uint64_t *pairs_in, uint64_t *pairs_out, int64_t n,
                 const int64_t *starts, void *ws, size_t ws_bytes, int64_t *stats, void *stream);
+int lj_lsj_sort_regions(const LjLsjModel *model, const uint64_t *pairs_in, uint64_t *pairs_out, int64_t n,
+                        const int64_t *reg, int64_t *starts_out, void *ws, size_t ws_bytes, int64_t *stats,
+                        void *stream);
 /* Reference bucket bounds at scale P of a sorted relation (the
  * partition_index buckets of lsj.py:302-305, for its counters). */
 int lj_lsj_ref_bounds(const LjRmi *model, const uint64_t *sorted_pairs, int64_t n, int64_t P, int64_t *bounds,

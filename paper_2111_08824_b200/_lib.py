@@ -152,6 +152,10 @@ SIGNATURES = {
     "lj_lsj_partition": (_int, [ctypes.POINTER(LjLsjModel), _P, _P, _i64, _P, _P, _P, _size_t, _P]),
     "lj_lsj_sort_workspace_bytes": (_size_t, [_i64, _i64]),
     "lj_lsj_sort": (_int, [ctypes.POINTER(LjLsjModel), _P, _P, _i64, _P, _P, _size_t, _P, _P]),
+    "lj_lsj_sort_regions": (_int, [ctypes.POINTER(LjLsjModel), _P, _P, _i64, _P, _P, _P, _size_t, _P, _P]),
+    "lj_lsj_partition_regions": (_int, [ctypes.POINTER(LjLsjModel), _P, _P, _i64, _P, _P, _P, _size_t, _P]),
+    "lj_lsj_partition_regions_capacity": (_i64, [_i64, _i64]),
+    "lj_lsj_partition_regions_workspace_bytes": (_size_t, [_i64, _i64]),
     "lj_lsj_ref_bounds": (_int, [ctypes.POINTER(LjRmi), _P, _i64, _i64, _P, _P]),
     "lj_lsj_join_workspace_bytes": (_size_t, [_i64]),
     "lj_lsj_join": (_int, [ctypes.POINTER(LjLsjModel), _P, _i64, _P, _P, _i64, _int, _P, _P, _P, _P, _P, _int,

@@ -73,12 +73,24 @@ constexpr int SPLIT_NT = 1024;
 #ifndef LJ_SPLIT_CH
 #define LJ_SPLIT_CH 262144
 #endif
+#ifndef LJ_SPLIT_MINB
+#define LJ_SPLIT_MINB 1  // resident split-scatter CTAs per SM the register budget allows
+#endif
 constexpr int SPLIT_U = LJ_SPLIT_U;    // tuple groups in flight per warp step
 constexpr i64 SPLIT_CH = LJ_SPLIT_CH;  // tuples per split work item (C4 sort phase: 64 Ki 17.10, 128 Ki 16.90, 256 Ki 16.77, 512 Ki 16.95 ms)
 constexpr int SPLIT_MAXF = 2048;  // slices per coarse bucket (point mode: 2x-1 slots)
-constexpr int JOIN_T = 1024;
-constexpr int JOIN_NT = 256;
-constexpr int WCAP = 3840;  // R slice keys staged per tile (+ the S tile: < 48 KB static)
+#ifndef LJ_JOIN_T
+#define LJ_JOIN_T 1024
+#endif
+#ifndef LJ_JOIN_WCAP
+#define LJ_JOIN_WCAP 3840
+#endif
+#ifndef LJ_JOIN_NT
+#define LJ_JOIN_NT 256
+#endif
+constexpr int JOIN_T = LJ_JOIN_T;
+constexpr int JOIN_NT = LJ_JOIN_NT;
+constexpr int WCAP = LJ_JOIN_WCAP;  // R slice keys staged per tile (+ the S tile: < 48 KB static)
 
 // ------------------------------------------------------------------ model
 
@@ -290,13 +302,13 @@ __device__ __forceinline__ i64 split_count(i64 m) {
     return m == 0 ? 0 : (f < 1 ? 1 : (f > SPLIT_MAXF ? SPLIT_MAXF : f));
 }
 
-__global__ void k_split_plan(const i64 *starts, int nb, int points, i64 *fcount) {
+__global__ void k_split_plan(const i64 *bstart, const i64 *bend, int nb, int points, i64 *fcount) {
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += gridDim.x * blockDim.x) {
         if (b == nb) {
             fcount[b] = 0;
             continue;
         }
-        const i64 f = split_count(starts[b + 1] - starts[b]);
+        const i64 f = split_count(bend[b] - bstart[b]);
         fcount[b] = points && f > 0 ? 2 * f - 1 : f;
     }
 }
@@ -334,7 +346,7 @@ __global__ void k_split_ranges(LsjDev md, const u32 *sbin, int nb, i64 *sr, i64 
 // flat); too few sample keys: the quantiles repeat (empty slices), none:
 // one slice for the bucket.  Bucket b's values: spv[fbase[b] + j - 1],
 // j in [1, F_b).
-__global__ void k_split_points(LsjDev md, const i64 *starts, const i64 *fbase, int nb, const i64 *sr,
+__global__ void k_split_points(LsjDev md, const i64 *bstart, const i64 *bend, const i64 *fbase, int nb, const i64 *sr,
                                const i64 *se, u64 *spv) {
     md.m.fix();
     const i64 G = fbase[nb];
@@ -345,7 +357,7 @@ __global__ void k_split_points(LsjDev md, const i64 *starts, const i64 *fbase, i
             if (fbase[mid] <= g) lo = mid; else hi = mid;
         }
         const int b = lo;
-        const i64 F = split_count(starts[b + 1] - starts[b]), j = g - fbase[b] + 1;
+        const i64 F = split_count(bend[b] - bstart[b]), j = g - fbase[b] + 1;
         if (F < 2 || j >= F) continue;
         const i64 sb = sr[b], ns = se[b] - sb;
         const i64 q = sb + (j * ns) / F;
@@ -412,7 +424,8 @@ __device__ __forceinline__ int point_slot_tab(const u64 *v, int K, const u16 *ce
 // shared-memory cursors.  A chunk keeps <= 4095 write frontiers open.
 
 struct SplitCtx {  // per-bucket layout shared by the split kernels
-    const i64 *starts;  // [nb+1] coarse bucket bounds
+    const i64 *bstart;  // [nb] coarse bucket b = records [bstart[b], bend[b]) of the input
+    const i64 *bend;    // (contiguous bins: bend = bstart + 1; one-pass regions leave gaps)
     const i64 *fbase;   // [nb+1] first slot of each bucket
     const i64 *cbase;   // [nb+1] first chunk of each bucket
     const i64 *mbase;   // [nb+1] first matrix entry of each bucket
@@ -420,13 +433,13 @@ struct SplitCtx {  // per-bucket layout shared by the split kernels
     int nb;
 };
 
-__global__ void k_chunk_plan(const i64 *starts, const i64 *fbase, int nb, i64 *chunks, i64 *matc) {
+__global__ void k_chunk_plan(const i64 *bstart, const i64 *bend, const i64 *fbase, int nb, i64 *chunks, i64 *matc) {
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += gridDim.x * blockDim.x) {
         if (b == nb) {
             chunks[b] = matc[b] = 0;
             continue;
         }
-        const i64 m = starts[b + 1] - starts[b];
+        const i64 m = bend[b] - bstart[b];
         const i64 c = (m + SPLIT_CH - 1) / SPLIT_CH;
         chunks[b] = c;
         matc[b] = c * (fbase[b + 1] - fbase[b]);
@@ -449,7 +462,7 @@ __device__ __forceinline__ SplitItem split_item(const LsjDev &md, const SplitCtx
     it.b = lo;
     it.c = q - cx.cbase[lo];
     it.chunks = cx.cbase[lo + 1] - cx.cbase[lo];
-    const i64 a0 = cx.starts[lo], e0 = cx.starts[lo + 1];
+    const i64 a0 = cx.bstart[lo], e0 = cx.bend[lo];
     it.a = a0 + it.c * SPLIT_CH;
     it.e = min(it.a + (i64)SPLIT_CH, e0);
     it.g0 = cx.fbase[lo];
@@ -556,7 +569,7 @@ __global__ void k_split_slots(LsjDev md, SplitCtx cx, const i64 *off, i64 n, i64
 }
 
 // pass 2: scatter every chunk through shared-memory cursors
-__global__ void __launch_bounds__(SPLIT_NT) k_split_scatter(LsjDev md, SplitCtx cx, const ulonglong2 *__restrict__ A,
+__global__ void __launch_bounds__(SPLIT_NT, LJ_SPLIT_MINB) k_split_scatter(LsjDev md, SplitCtx cx, const ulonglong2 *__restrict__ A,
                                                             const i64 *nitems, const i64 *__restrict__ off,
                                                             ulonglong2 *B, ulonglong2 *Out, SortCtl *ctl) {
     md.m.fix();
@@ -573,7 +586,9 @@ __global__ void __launch_bounds__(SPLIT_NT) k_split_scatter(LsjDev md, SplitCtx 
         const i64 q = s_q;
         if (q >= total) break;
         const SplitItem it = split_item(md, cx, q, points);
-        const i64 a0 = cx.starts[it.b], mb = cx.mbase[it.b];
+        // a0: the bucket's start in the OUTPUT (dense: the scanned matrix is
+        // bucket-major, so its first entry is the tuples of all earlier buckets)
+        const i64 mb = cx.mbase[it.b], a0 = off[mb];
         for (int j = threadIdx.x; j < it.F; j += SPLIT_NT) cur[j] = (u32)(off[mb + (i64)j * it.chunks + it.c] - a0);
         for (int j = threadIdx.x; j < it.K; j += SPLIT_NT) v[j] = cx.spv[it.g0 + j];
         __syncthreads();
@@ -1111,20 +1126,43 @@ __global__ void __launch_bounds__(JOIN_NT) k_lsj_join(const ulonglong2 *__restri
                 }
                 const i64 i = a + j;
                 i64 c = 0, o = mode == 2 ? offsets[i] : 0;
-                for (i64 q = c0 + pos; q < w; ++q) {  // equal run (may run past the chunk)
-                    const u64 rk = q - c0 < cl ? wk[q - c0] : R[wlo + q].x;
-                    if (rk != k) break;
-                    if (mode == 0) {
-                        const u64 v = R[wlo + q].y + sp[j];
-                        ++cnt;
-                        sum += v;
-                        x ^= v;
-                    } else if (mode == 2) {
-                        opr[o] = R[wlo + q].y;
-                        ops[o] = sp[j];
-                        ++o;
+                // equal run: from the staged keys (unique build keys: one
+                // compare, one payload load), past the chunk from global
+                int p2 = pos;
+                if (p2 < cl && wk[p2] == k) {
+                    const ulonglong2 *rr = R + wlo + c0;
+                    const u64 spj = sp[j];
+                    do {
+                        const u64 pr = rr[p2].y;
+                        if (mode == 0) {
+                            const u64 v = pr + spj;
+                            ++cnt;
+                            sum += v;
+                            x ^= v;
+                        } else if (mode == 2) {
+                            opr[o] = pr;
+                            ops[o] = spj;
+                            ++o;
+                        }
+                        ++c;
+                        ++p2;
+                    } while (p2 < cl && wk[p2] == k);
+                    if (p2 == cl) {
+                        for (i64 q = c0 + cl; q < w && R[wlo + q].x == k; ++q) {
+                            const u64 pr = R[wlo + q].y;
+                            if (mode == 0) {
+                                const u64 v = pr + spj;
+                                ++cnt;
+                                sum += v;
+                                x ^= v;
+                            } else if (mode == 2) {
+                                opr[o] = pr;
+                                ops[o] = spj;
+                                ++o;
+                            }
+                            ++c;
+                        }
                     }
-                    ++c;
                 }
                 if (mode == 1) counts[i] = c;
             }
@@ -1376,6 +1414,41 @@ int lj_lsj_partition(const LjLsjModel *md, const uint64_t *keys, const uint64_t 
     return run_partition(src, n, nb, reinterpret_cast<ulonglong2 *>(pairs), starts, ws, pws, st);
 }
 
+// One pass into estimated-capacity regions (lj_part_est.cuh): no exact
+// counting pass.  pairs: lj_lsj_partition_regions_capacity records; reg[2
+// nbins + 2]: bin b = records [reg[b], reg[nbins + 1 + b]) of pairs (gaps
+// between the bins).  An overflow of any region (practically never) makes
+// the exact two-pass partition run instead, decided on the device.
+int64_t lj_lsj_partition_regions_capacity(int64_t n, int64_t nbins) { return est_capacity(n, (int)nbins); }
+
+size_t lj_lsj_partition_regions_workspace_bytes(int64_t n, int64_t nbins) {
+    (void)n;
+    return est_exact_workspace_bytes((int)nbins) + al(kb_bytes((int)nbins));
+}
+
+int lj_lsj_partition_regions(const LjLsjModel *md, const uint64_t *keys, const uint64_t *pay, int64_t n,
+                             uint64_t *pairs, int64_t *reg, void *ws, size_t ws_bytes, void *stream) {
+    LJ_REQUIRE(md && md->table && md->pb && md->nbins >= 1 && md->nbins <= KB_MAXBINS, "model has no bins / > 2048 bins");
+    LJ_REQUIRE(((uintptr_t)keys & 15) == 0 && ((uintptr_t)pay & 15) == 0 && n < (i64)0xFFFFFFFFLL,
+               "columns must be 16-B aligned, n < 2^32");
+    if (ws_bytes < lj_lsj_partition_regions_workspace_bytes(n, md->nbins)) {
+        set_error("lj_lsj_partition_regions: workspace too small");
+        return LJ_E_WORKSPACE;
+    }
+    cudaStream_t st = as_stream(stream);
+    const int nb = (int)md->nbins;
+    const size_t pws = est_exact_workspace_bytes(nb);
+    u64 *lay = reinterpret_cast<u64 *>((char *)ws + pws);
+    k_lsj_key_bounds<<<(nb + 127) / 128, 128, 0, st>>>(make_lsj(*md), lay);
+    k_keybin_build<<<1, 1024, 0, st>>>(lay, nb);
+    LJ_CK_LAUNCH();
+    KeyRangeBin kb;
+    kb.g = lay;
+    kb.nb = nb;
+    SoaSrc<KeyRangeBin> src{keys, pay, kb};
+    return run_partition_est_or_exact(src, n, nb, reinterpret_cast<ulonglong2 *>(pairs), reg, ws, pws, st);
+}
+
 static i64 max_subs(i64 n, i64 nbins) { return 2 * (n / SUB + nbins) + 2; }
 static i64 max_mat(i64 n, i64 nbins) { return (i64)(2 * SPLIT_MAXF) * (n / SPLIT_CH + nbins + 1); }
 
@@ -1407,8 +1480,33 @@ size_t lj_lsj_sort_workspace_bytes(int64_t n, int64_t nbins) {
 
 __global__ void k_set_last(const i64 *fbase, int nb, i64 n, i64 *sub_starts) { sub_starts[fbase[nb]] = n; }
 
+// dense bucket starts of the sorted output: the scanned matrix's first entry
+// of every bucket (empty trailing buckets: n)
+__global__ void k_dense_starts(const i64 *mbase, const i64 *off, int nb, i64 n, i64 *dstarts) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += gridDim.x * blockDim.x)
+        dstarts[b] = (b < nb && mbase[b] < mbase[nb]) ? off[mbase[b]] : n;
+}
+
+static int lsj_sort_impl(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_out, int64_t n,
+                         const int64_t *bstart, const int64_t *bend, int64_t *dense_starts, void *ws, size_t ws_bytes,
+                         int64_t *stats, void *stream);
+
 int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_out, int64_t n,
                 const int64_t *starts, void *ws, size_t ws_bytes, int64_t *stats, void *stream) {
+    return lsj_sort_impl(md, pairs_in, pairs_out, n, starts, starts + 1, nullptr, ws, ws_bytes, stats, stream);
+}
+
+int lj_lsj_sort_regions(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_out, int64_t n,
+                        const int64_t *reg, int64_t *starts_out, void *ws, size_t ws_bytes, int64_t *stats,
+                        void *stream) {
+    LJ_REQUIRE(md && md->nbins >= 1 && reg && starts_out, "null regions / starts");
+    return lsj_sort_impl(md, pairs_in, pairs_out, n, reg, reg + md->nbins + 1, starts_out, ws, ws_bytes, stats,
+                         stream);
+}
+
+static int lsj_sort_impl(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_out, int64_t n,
+                         const int64_t *bstart, const int64_t *bend, int64_t *dense_starts, void *ws, size_t ws_bytes,
+                         int64_t *stats, void *stream) {
     LJ_REQUIRE(md && md->table && md->pb && md->nbins >= 1, "model has no bins");
     if (ws_bytes < lj_lsj_sort_workspace_bytes(n, md->nbins)) {
         set_error("lj_lsj_sort: workspace too small");
@@ -1417,6 +1515,7 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
     cudaStream_t st = as_stream(stream);
     if (n == 0) {
         if (stats) LJ_CK(cudaMemsetAsync(stats, 0, 4 * sizeof(i64), st));
+        if (dense_starts) LJ_CK(cudaMemsetAsync(dense_starts, 0, sizeof(i64) * (size_t)(md->nbins + 1), st));
         return LJ_OK;
     }
     const i64 nb = md->nbins, G = max_subs(n, nb);
@@ -1451,7 +1550,7 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
     ulonglong2 *out = reinterpret_cast<ulonglong2 *>(pairs_out);
     // level 2: slices of ~SUB tuples per coarse bucket (segmented, chunked)
     const int points = dev.sample != nullptr && dev.nsample > 0;
-    k_split_plan<<<(int)((nb + 256) / 256), 256, 0, st>>>(starts, (int)nb, points, fcount);
+    k_split_plan<<<(int)((nb + 256) / 256), 256, 0, st>>>(bstart, bend, (int)nb, points, fcount);
     LJ_CK_LAUNCH();
     size_t t = scan_i64_bytes(nb + 1);
     LJ_CK(cub::DeviceScan::ExclusiveSum(cub_tmp, t, fcount, fbase, (int64_t)(nb + 1), st));
@@ -1459,15 +1558,15 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
         // the bins' sample ranges go through chunks / matc (free until
         // k_chunk_plan); sample bins evaluated inside the searches
         k_split_ranges<<<(int)((nb + 63) / 64), 64, 0, st>>>(dev, nullptr, (int)nb, chunks, matc);
-        k_split_points<<<grid_for(max_subs(n, nb), 256, 8), 256, 0, st>>>(dev, starts, fbase, (int)nb, chunks, matc,
-                                                                         spv);
+        k_split_points<<<grid_for(max_subs(n, nb), 256, 8), 256, 0, st>>>(dev, bstart, bend, fbase, (int)nb, chunks,
+                                                                         matc, spv);
         LJ_CK_LAUNCH();
     }
-    k_chunk_plan<<<(int)((nb + 256) / 256), 256, 0, st>>>(starts, fbase, (int)nb, chunks, matc);
+    k_chunk_plan<<<(int)((nb + 256) / 256), 256, 0, st>>>(bstart, bend, fbase, (int)nb, chunks, matc);
     LJ_CK_LAUNCH();
     LJ_CK(cub::DeviceScan::ExclusiveSum(cub_tmp, t, chunks, cbase, (int64_t)(nb + 1), st));
     LJ_CK(cub::DeviceScan::ExclusiveSum(cub_tmp, t, matc, mbase, (int64_t)(nb + 1), st));
-    const SplitCtx cx{starts, fbase, cbase, mbase, spv, (int)nb};
+    const SplitCtx cx{bstart, bend, fbase, cbase, mbase, spv, (int)nb};
     LJ_CK(cudaMemsetAsync(ctl, 0, sizeof(SortCtl), st));
     k_split_count<<<sm_count() * 2, SPLIT_NT, 0, st>>>(dev, cx, A, cbase + nb, mat, ctl);
     LJ_CK_LAUNCH();
@@ -1479,6 +1578,7 @@ int lj_lsj_sort(const LjLsjModel *md, const uint64_t *pairs_in, uint64_t *pairs_
         LJ_CK(cub::DeviceScan::ExclusiveSum(cub_tmp, tm, it, moff, (int64_t)Mcap, st));
     }
     k_split_slots<<<grid_for(G + 1, 256, 8), 256, 0, st>>>(dev, cx, moff, n, sub_starts, sub_y);
+    if (dense_starts) k_dense_starts<<<(int)((nb + 256) / 256), 256, 0, st>>>(mbase, moff, (int)nb, n, dense_starts);
     LJ_CK_LAUNCH();
     LJ_CK(cudaMemsetAsync(ctl, 0, sizeof(SortCtl), st));
     k_split_scatter<<<sm_count() * 2, SPLIT_NT, 0, st>>>(dev, cx, A, cbase + nb, moff, B, out, ctl);
@@ -1542,7 +1642,11 @@ int lj_lsj_join(const LjLsjModel *model_r, const uint64_t *r_pairs, int64_t nr, 
     const ulonglong2 *S = reinterpret_cast<const ulonglong2 *>(s_pairs);
     k_join_bounds<<<grid_for(ntiles, 128, 16), 128, 0, st>>>(make_lsj(*model_r), R, r_starts, S, ns, ntiles, tb);
     LJ_CK_LAUNCH();
-    const unsigned g = (unsigned)(ntiles < (i64)sm_count() * 8 ? ntiles : (i64)sm_count() * 8);
+    // one wave of resident CTAs (the tile loop strides by the grid)
+    int per_sm = 0;
+    LJ_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lsj_join, JOIN_NT, 0));
+    const i64 wave = (i64)sm_count() * (per_sm > 0 ? per_sm : 1);
+    const unsigned g = (unsigned)(ntiles < wave ? ntiles : wave);
     k_lsj_join<<<g, JOIN_NT, 0, st>>>(R, S, ns, tb, mode, counts, offsets, out_pr, out_ps, out);
     LJ_CK_LAUNCH();
     return LJ_OK;
@@ -1599,8 +1703,15 @@ static LsjRunRel run_rel(i64 n, double rate) {
 static size_t run_keep_bytes(const LsjRunRel &r) {
     return al(sizeof(u64) * (size_t)r.tl) + al(sizeof(double) * 2) + al(sizeof(LjLeaf) * (size_t)r.fanout) +
            al(sizeof(i64) * 2 * (size_t)r.fanout) + al(sizeof(i64) * (size_t)(r.nbins + 1)) +
-           al(sizeof(u32) * (size_t)r.tl) + 2 * al(sizeof(ulonglong2) * (size_t)r.n) +
-           al(sizeof(i64) * (size_t)(r.nbins + 1));
+           al(sizeof(u32) * (size_t)r.tl) + al(sizeof(ulonglong2) * (size_t)r.n) +
+           al(sizeof(i64) * (size_t)(r.nbins + 1)) + al(sizeof(i64) * (size_t)(2 * r.nbins + 2));
+}
+
+// the partition buffer both relations go through, one after the other:
+// one-pass regions (gaps between the bins) for the larger relation
+static size_t run_part_bytes(const LsjRunRel &a, const LsjRunRel &b) {
+    const i64 ca = lj_lsj_partition_regions_capacity(a.n, a.nbins), cb = lj_lsj_partition_regions_capacity(b.n, b.nbins);
+    return al(sizeof(ulonglong2) * (size_t)std::max(ca, cb));
 }
 
 static size_t run_scratch_bytes(const LsjRunRel &r) {
@@ -1608,6 +1719,7 @@ static size_t run_scratch_bytes(const LsjRunRel &r) {
     s = std::max(s, lj_rmi_fit_workspace_bytes(r.tl, r.fanout));
     s = std::max(s, lj_lsj_bins_workspace_bytes(r.tl));
     s = std::max(s, lj_lsj_partition_workspace_bytes(r.n, r.nbins));
+    s = std::max(s, lj_lsj_partition_regions_workspace_bytes(r.n, r.nbins));
     s = std::max(s, lj_lsj_sort_workspace_bytes(r.n, r.nbins));
     return al(s);
 }
@@ -1618,7 +1730,8 @@ extern "C" {
 
 size_t lj_lsj_run_workspace_bytes(int64_t nr, int64_t ns, double sample_rate) {
     const LsjRunRel a = run_rel(nr, sample_rate), b = run_rel(ns, sample_rate);
-    return run_keep_bytes(a) + run_keep_bytes(b) + std::max(run_scratch_bytes(a), run_scratch_bytes(b)) +
+    return run_keep_bytes(a) + run_keep_bytes(b) + run_part_bytes(a, b) +
+           std::max(run_scratch_bytes(a), run_scratch_bytes(b)) +
            al(lj_lsj_join_workspace_bytes(ns)) + 1024;
 }
 
@@ -1644,7 +1757,8 @@ int lj_lsj_run(const uint64_t *rk, const uint64_t *rp, int64_t nr, const uint64_
     const u64 seeds[2] = {seed, seed ^ 0x5DEECE66DULL};  // lsj.py:388-391: S's model seed
     LjRmi rmi[2];
     LjLsjModel md[2];
-    u64 *sbuf[2], *pairs[2];
+    u64 *sbuf[2];
+    i64 *reg[2];
     double *root[2];
     LjLeaf *leaves[2];
     i64 *err[2], *pb[2], *starts[2];
@@ -1658,13 +1772,14 @@ int lj_lsj_run(const uint64_t *rk, const uint64_t *rp, int64_t nr, const uint64_
         err[x] = (i64 *)take(sizeof(i64) * 2 * (size_t)r.fanout);
         pb[x] = (i64 *)take(sizeof(i64) * (size_t)(r.nbins + 1));
         table[x] = (u32 *)take(sizeof(u32) * (size_t)r.tl);
-        pairs[x] = (u64 *)take(sizeof(ulonglong2) * (size_t)r.n);
         sorted[x] = (ulonglong2 *)take(sizeof(ulonglong2) * (size_t)r.n);
         starts[x] = (i64 *)take(sizeof(i64) * (size_t)(r.nbins + 1));
+        reg[x] = (i64 *)take(sizeof(i64) * (size_t)(2 * r.nbins + 2));
         // the root stays on the device (root_dev): nothing is read back
         rmi[x] = LjRmi{0.0, 0.0, r.fanout, r.tl, leaves[x], err[x], root[x]};
         md[x] = LjLsjModel{rmi[x], r.nbins, pb[x], table[x], r.total > 0 ? sbuf[x] : nullptr, r.total > 0 ? r.tl : 0};
     }
+    u64 *pairs = (u64 *)take(run_part_bytes(rel[0], rel[1]));
     char *scratch = p;
     const size_t sb = std::max(run_scratch_bytes(rel[0]), run_scratch_bytes(rel[1]));
     p += sb;
@@ -1684,11 +1799,20 @@ int lj_lsj_run(const uint64_t *rk, const uint64_t *rp, int64_t nr, const uint64_
         if (rc) return rc;
         rc = lj_lsj_bins(&rmi[x], sbuf[x], r.tl, r.nbins, pb[x], table[x], scratch, sb, stream);
         if (rc) return rc;
-        // part + sort (K6/K7, split, K8)
-        rc = lj_lsj_partition(&md[x], keys[x], pays[x], r.n, pairs[x], starts[x], scratch, sb, stream);
-        if (rc) return rc;
-        rc = lj_lsj_sort(&md[x], pairs[x], reinterpret_cast<u64 *>(sorted[x]), r.n, starts[x], scratch, sb, nullptr,
-                         stream);
+        // part + sort (K6/K7, split, K8): one-pass regions when the columns
+        // allow the bulk-copy ring, else the exact partition
+        if (r.nbins <= KB_MAXBINS && ((uintptr_t)keys[x] & 15) == 0 && ((uintptr_t)pays[x] & 15) == 0 &&
+            r.n < (i64)0xFFFFFFFFLL) {
+            rc = lj_lsj_partition_regions(&md[x], keys[x], pays[x], r.n, pairs, reg[x], scratch, sb, stream);
+            if (rc) return rc;
+            rc = lj_lsj_sort_regions(&md[x], pairs, reinterpret_cast<u64 *>(sorted[x]), r.n, reg[x], starts[x], scratch,
+                                     sb, nullptr, stream);
+        } else {
+            rc = lj_lsj_partition(&md[x], keys[x], pays[x], r.n, pairs, starts[x], scratch, sb, stream);
+            if (rc) return rc;
+            rc = lj_lsj_sort(&md[x], pairs, reinterpret_cast<u64 *>(sorted[x]), r.n, starts[x], scratch, sb, nullptr,
+                             stream);
+        }
         if (rc) return rc;
     }
     // join (K9): S's tiles against R's windows through R's model

@@ -38,7 +38,9 @@ inline i64 est_capacity(i64 n, int nb) { return n + n / 16 + (i64)nb * (EST_PAD 
 
 // per-bin counts of every `stride`-th tuple (stride 1: the exact histogram)
 template <class Src>
-__global__ void __launch_bounds__(256) k_est_sample(Src f0, i64 n, int nbins, int stride, u32 *est, u16 *codes) {
+__global__ void __launch_bounds__(256) k_est_sample(Src f0, i64 n, int nbins, int stride, u32 *est, u16 *codes,
+                                                    const unsigned long long *run_if = nullptr) {
+    if (run_if && *run_if == 0) return;  // a fallback pass that is not needed
     extern __shared__ __align__(128) unsigned char smem_e[];
     u64 *tab = reinterpret_cast<u64 *>(smem_e);
     u32 *h = reinterpret_cast<u32 *>(smem_e + pt_table_bytes(f0.f.smem_words()));
@@ -84,7 +86,7 @@ __global__ void __launch_bounds__(256) k_est_sample(Src f0, i64 n, int nbins, in
 
 // region capacity per bin: the exact count, or the sample estimate with
 // slack (est * 17/16 + pad)
-static __global__ void k_est_caps(const u32 *est, int nbins, int exact, i64 *cap) {
+static __global__ void k_est_caps(const u32 *est, int nbins, int exact, i64 *cap, int tight = 0) {
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b <= nbins; b += gridDim.x * blockDim.x) {
         if (b == nbins) {
             cap[b] = 0;
@@ -95,7 +97,7 @@ static __global__ void k_est_caps(const u32 *est, int nbins, int exact, i64 *cap
             continue;
         }
         const i64 e = (i64)est[b] * EST_STRIDE;
-        cap[b] = e + e / 16 + EST_PAD + EST_STRIDE;
+        cap[b] = tight ? e : e + e / 16 + EST_PAD + EST_STRIDE;  // tight (LJ_EST_TIGHT): tests force overflow
     }
 }
 
@@ -109,7 +111,9 @@ template <class Src, bool STORED, bool PEER = false>
 __global__ void __launch_bounds__(PART2_NT, 1) k_bin_scatter_est(Src f0, i64 n, i64 chunk, int nbins, int nst,
                                                               const i64 *__restrict__ rstart, u32 *gcur,
                                                               unsigned long long *ovf, ulonglong2 *out,
-                                                              const u16 *__restrict__ codes) {
+                                                              const u16 *__restrict__ codes,
+                                                              const unsigned long long *run_if = nullptr) {
+    if (run_if && *run_if == 0) return;  // a fallback pass that is not needed
     constexpr int U = EST_TILE / PART2_NT;
     constexpr size_t STAGE = EST_STAGE + (STORED ? EST_TILE * 2 : 0);
     extern __shared__ __align__(128) unsigned char smem_s[];
@@ -382,7 +386,8 @@ inline size_t est_workspace_bytes(int nbins) {  // (+ part_align(2 n) for stored
 //              contiguous, reg[0..nbins] = bin starts (no overflow).
 template <class Src>
 int run_partition_claims(const Src &f, i64 n, int nbins, int exact, ulonglong2 *out, i64 *reg, void *ws,
-                         size_t ws_bytes, cudaStream_t st, u16 *codes = nullptr) {
+                         size_t ws_bytes, cudaStream_t st, u16 *codes = nullptr,
+                         const unsigned long long *run_if = nullptr) {
     if (nbins < 1 || nbins > 2 * PART2_NT) {
         set_error("partition_est: nbins must be in [1, 2048]");
         return LJ_E_INVALID;
@@ -418,10 +423,10 @@ int run_partition_claims(const Src &f, i64 n, int nbins, int exact, ulonglong2 *
     const bool stored = exact && codes != nullptr && nbins <= 65536;
     if (n > 0) {
         k_est_sample<Src><<<grid_for((n + stride - 1) / stride, 256, 4), 256, tb + sizeof(u32) * nbins, st>>>(
-            f, n, nbins, stride, est, stored ? codes : nullptr);
+            f, n, nbins, stride, est, stored ? codes : nullptr, run_if);
         LJ_CK_LAUNCH();
     }
-    k_est_caps<<<(nbins + 256) / 256, 256, 0, st>>>(est, nbins, exact, cap);
+    k_est_caps<<<(nbins + 256) / 256, 256, 0, st>>>(est, nbins, exact, cap, getenv("LJ_EST_TIGHT") != nullptr);
     LJ_CK_LAUNCH();
     size_t t = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, t, cap, rstart, (int64_t)(nbins + 1));
@@ -437,12 +442,11 @@ int run_partition_claims(const Src &f, i64 n, int nbins, int exact, ulonglong2 *
             return LJ_E_INVALID;
         }
         if (stored)
-            k_bin_scatter_est<Src, true><<<p.blocks, PART2_NT, fix + nst * stage, st>>>(f, n, p.chunk, nbins, nst,
-                                                                                        rstart, gcur, ovf, out, codes);
+            k_bin_scatter_est<Src, true><<<p.blocks, PART2_NT, fix + nst * stage, st>>>(
+                f, n, p.chunk, nbins, nst, rstart, gcur, ovf, out, codes, run_if);
         else
-            k_bin_scatter_est<Src, false><<<p.blocks, PART2_NT, fix + nst * stage, st>>>(f, n, p.chunk, nbins, nst,
-                                                                                         rstart, gcur, ovf, out,
-                                                                                         nullptr);
+            k_bin_scatter_est<Src, false><<<p.blocks, PART2_NT, fix + nst * stage, st>>>(
+                f, n, p.chunk, nbins, nst, rstart, gcur, ovf, out, nullptr, run_if);
         LJ_CK_LAUNCH();
     }
     if (!exact) {
@@ -520,6 +524,47 @@ template <class Src>
 int run_partition_est(const Src &f, i64 n, int nbins, ulonglong2 *out, i64 *reg, void *ws, size_t ws_bytes,
                       cudaStream_t st) {
     return run_partition_claims(f, n, nbins, 0, out, reg, ws, ws_bytes, st);
+}
+
+// a fallback partition ran (*cond != 0): its contiguous bins as regions
+static __global__ void k_cond_regions(unsigned long long *cond, const i64 *starts, int nbins, i64 *reg) {
+    const bool ran = *cond != 0;
+    __syncthreads();
+    if (!ran) return;
+    for (int b = threadIdx.x; b <= nbins; b += blockDim.x) {
+        reg[b] = starts[b];
+        if (b < nbins) reg[nbins + 1 + b] = starts[b + 1];
+    }
+    if (threadIdx.x == 0) reg[2 * nbins + 1] = 0;
+}
+
+inline size_t est_exact_workspace_bytes(int nbins) {
+    return est_workspace_bytes(nbins) + part_align(sizeof(i64) * (size_t)(nbins + 1));
+}
+
+// One pass into estimated-capacity regions with NO overflow area for the
+// consumer: if any record overflowed (practically never: the slack is many
+// standard deviations of the sample estimate), the exact two-pass partition
+// runs over the same output instead.  Its kernels are always enqueued and
+// return at once when the overflow count is zero, so the decision stays on
+// the device (no readback).  reg as run_partition_est, reg[2 nbins + 1] = 0.
+template <class Src>
+int run_partition_est_or_exact(const Src &f, i64 n, int nbins, ulonglong2 *out, i64 *reg, void *ws, size_t ws_bytes,
+                               cudaStream_t st) {
+    if (ws_bytes < est_exact_workspace_bytes(nbins)) {
+        set_error("partition_est: workspace too small");
+        return LJ_E_WORKSPACE;
+    }
+    const size_t eb = est_workspace_bytes(nbins);
+    i64 *starts = reinterpret_cast<i64 *>((char *)ws + eb);
+    int rc = run_partition_claims(f, n, nbins, 0, out, reg, ws, eb, st);
+    if (rc) return rc;
+    unsigned long long *cond = reinterpret_cast<unsigned long long *>(reg + 2 * nbins + 1);
+    rc = run_partition_claims(f, n, nbins, 1, out, starts, ws, eb, st, nullptr, cond);
+    if (rc) return rc;
+    k_cond_regions<<<1, 1024, 0, st>>>(cond, starts, nbins, reg);
+    LJ_CK_LAUNCH();
+    return LJ_OK;
 }
 
 // The same one-pass regions through the direct claims scatter

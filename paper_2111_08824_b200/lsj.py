@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -271,6 +272,56 @@ def _partition(keys, payloads, lm: LsjModel):
     return pairs, starts
 
 
+def _regions_ok(keys, payloads, lm: LsjModel) -> bool:
+    """The one-pass partition needs the bulk-copy ring (16-B aligned columns)
+    and the key-range bins in shared memory (<= 2048 bins)."""
+    return (lm.nbins <= 2048 and keys.numel() < 0xFFFFFFFF and keys.data_ptr() % 16 == 0
+            and payloads.data_ptr() % 16 == 0 and not os.environ.get("LJ_LSJ_EXACT_PARTITION"))
+
+
+def _partition_regions(keys, payloads, lm: LsjModel):
+    """lj_lsj_partition_regions: ONE pass into estimated-capacity regions
+    (no exact counting pass) -> (pairs with gaps, reg[2 nbins + 2])."""
+    lib = _lib.lib()
+    n = keys.numel()
+    cap = lib.lj_lsj_partition_regions_capacity(n, lm.nbins)
+    pairs = torch.empty(2 * max(cap, 1), dtype=torch.int64, device=keys.device)
+    reg = torch.empty(2 * lm.nbins + 2, dtype=torch.int64, device=keys.device)
+    ws = _lib.workspace(lib.lj_lsj_partition_regions_workspace_bytes(n, lm.nbins), keys.device)
+    c = lm.c_struct()
+    _lib.check(lib.lj_lsj_partition_regions(ctypes.byref(c), _lib.ptr(keys), _lib.ptr(payloads), n, _lib.ptr(pairs),
+                                            _lib.ptr(reg), _lib.ptr(ws), ws.numel(), _lib.stream_ptr()),
+               "lsj_partition_regions")
+    return pairs, reg
+
+
+def _sort_regions(pairs_in, reg, lm: LsjModel, n: int):
+    """K8 over one-pass regions -> (sorted pairs [2n], dense bin starts
+    [nbins + 1], device sort counters)."""
+    lib = _lib.lib()
+    out = torch.empty(2 * max(n, 1), dtype=torch.int64, device=pairs_in.device)
+    starts = torch.empty(lm.nbins + 1, dtype=torch.int64, device=pairs_in.device)
+    ws = _lib.workspace(lib.lj_lsj_sort_workspace_bytes(n, lm.nbins), pairs_in.device)
+    st = torch.zeros(4, dtype=torch.int64, device=pairs_in.device)
+    c = lm.c_struct()
+    _lib.check(lib.lj_lsj_sort_regions(ctypes.byref(c), _lib.ptr(pairs_in), _lib.ptr(out), n, _lib.ptr(reg),
+                                       _lib.ptr(starts), _lib.ptr(ws), ws.numel(), _lib.ptr(st), _lib.stream_ptr()),
+               "lsj_sort_regions")
+    return out, starts, st
+
+
+def _partition_sort(keys, payloads, lm: LsjModel, n: int):
+    """Partition + per-bucket sort of one relation -> (sorted pairs, dense
+    bin starts, sort counters): the one-pass regions when the columns allow
+    them, else the exact partition."""
+    if _regions_ok(keys, payloads, lm):
+        pairs, reg = _partition_regions(keys, payloads, lm)
+        return _sort_regions(pairs, reg, lm, n)
+    pairs, starts = _partition(keys, payloads, lm)
+    out, st = _sort(pairs, starts, lm, n)
+    return out, starts, st
+
+
 SORT_DIAG = ("oversized_sub_buckets", "bitonic_fallbacks", "big_sorted_sub_buckets", "global_sorted_sub_buckets")
 
 
@@ -422,11 +473,20 @@ def lsj_join(r: Relation, s: Relation, config: LsjConfig | None = None, material
         lr = _as_lsj_model(models[0], len(r))
         ls = _as_lsj_model(models[1], len(s))
     ev[1].record()
-    pr, str_ = _partition(r.keys, r.payloads, lr)
-    ps, sts = _partition(s.keys, s.payloads, ls)
+    # partition: one pass into estimated-capacity regions (no exact counting
+    # pass) when the columns allow it, else the exact K6/K7
+    fast_r, fast_s = _regions_ok(r.keys, r.payloads, lr), _regions_ok(s.keys, s.payloads, ls)
+    pr, str_ = (_partition_regions if fast_r else _partition)(r.keys, r.payloads, lr)
+    ps, sts = (_partition_regions if fast_s else _partition)(s.keys, s.payloads, ls)
     ev[2].record()
-    pr, dr = _sort(pr, str_, lr, len(r))
-    ps, ds = _sort(ps, sts, ls, len(s))
+    if fast_r:
+        pr, str_, dr = _sort_regions(pr, str_, lr, len(r))
+    else:
+        pr, dr = _sort(pr, str_, lr, len(r))
+    if fast_s:
+        ps, sts, ds = _sort_regions(ps, sts, ls, len(s))
+    else:
+        ps, ds = _sort(ps, sts, ls, len(s))
     r_sorted = SortedRelation(pr[: 2 * len(r)], str_, lr, scale, (lr.tag, scale), diag=dr)
     s_sorted = SortedRelation(ps[: 2 * len(s)], sts, ls, scale, (ls.tag, scale), diag=ds)
     ev[3].record()

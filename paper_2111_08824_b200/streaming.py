@@ -109,15 +109,13 @@ def lsj_join_host(r_keys_host: torch.Tensor, r_payloads_host: torch.Tensor, s_ke
         return L.JoinResult()
     scale = config.effective_fanout()
     _, lr = L.prepare_model(r, config.sample_rate, config.seed, config.model_fanout)
-    pr, str_ = L._partition(r.keys, r.payloads, lr)
-    pr, dr = L._sort(pr, str_, lr, len(r))
+    pr, str_, dr = L._partition_sort(r.keys, r.payloads, lr, len(r))
     comp.wait_event(ev_s)
     s = Relation(ds[2], ds[3], validate=True)
     if len(s) == 0:
         return L.JoinResult()
     _, ls = L.prepare_model(s, config.sample_rate, config.seed ^ 0x5DEECE66D, config.model_fanout)
-    ps, sts = L._partition(s.keys, s.payloads, ls)
-    ps, ds_ = L._sort(ps, sts, ls, len(s))
+    ps, sts, ds_ = L._partition_sort(s.keys, s.payloads, ls, len(s))
     r_sorted = L.SortedRelation(pr[: 2 * len(r)], str_, lr, scale, (lr.tag, scale), diag=dr)
     s_sorted = L.SortedRelation(ps[: 2 * len(s)], sts, ls, scale, (ls.tag, scale), diag=ds_)
     return L.chunked_join(r_sorted, s_sorted, lr.rmi, scale, config.workers)

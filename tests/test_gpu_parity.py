@@ -813,6 +813,31 @@ def test_lsj_run_one_call_abi_equals_lsj_join_and_oracle(lj, name):
     assert got == tuple(want) == res.checksum
 
 
+@pytest.mark.parametrize("name", ["c4", "zipf"])
+def test_lsj_one_pass_partition_equals_exact_and_overflow_falls_back(lj, name, monkeypatch):
+    """LSJ's partition in ONE pass (sample-sized regions with gaps,
+    lj_lsj_partition_regions + lj_lsj_sort_regions) == the exact two-pass
+    partition == the oracle; with the regions' slack taken away
+    (LJ_EST_TIGHT: about half of the bins overflow) the device-side
+    fallback to the exact partition gives the same join, through both the
+    Python orchestration and the one-call ABI."""
+    r, s = _lsj_sets()[name]
+    want = tuple(oracle.smj_checksum(*r.numpy(), *s.numpy()))
+    cfg = lj.LsjConfig(fanout=4096, sample_rate=0.01)
+    res, br = lj.lsj_join(r, s, cfg)
+    assert res.checksum == want
+    monkeypatch.setenv("LJ_LSJ_EXACT_PARTITION", "1")
+    exact, br2 = lj.lsj_join(r, s, cfg)
+    assert exact.checksum == want
+    assert br.sort_stats == br2.sort_stats  # the reference counters: the same sorted relations
+    monkeypatch.delenv("LJ_LSJ_EXACT_PARTITION")
+    monkeypatch.setenv("LJ_EST_TIGHT", "1")
+    tight, br3 = lj.lsj_join(r, s, cfg)
+    assert tight.checksum == want
+    assert br3.sort_stats == br2.sort_stats
+    assert lj.lsj_run(r, s, cfg).checksum == want
+
+
 C01_ALGOS = ["grmi-inlj", "buffered-grmi-inlj", "spline-hash-inlj", "lsj", "rmi-inlj"]
 
 
