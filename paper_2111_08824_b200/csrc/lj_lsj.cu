@@ -80,13 +80,13 @@ constexpr int SPLIT_U = LJ_SPLIT_U;    // tuple groups in flight per warp step
 constexpr i64 SPLIT_CH = LJ_SPLIT_CH;  // tuples per split work item (C4 sort phase: 64 Ki 17.10, 128 Ki 16.90, 256 Ki 16.77, 512 Ki 16.95 ms)
 constexpr int SPLIT_MAXF = 2048;  // slices per coarse bucket (point mode: 2x-1 slots)
 #ifndef LJ_JOIN_T
-#define LJ_JOIN_T 1024
+#define LJ_JOIN_T 512
 #endif
 #ifndef LJ_JOIN_WCAP
-#define LJ_JOIN_WCAP 3840
+#define LJ_JOIN_WCAP 1920
 #endif
 #ifndef LJ_JOIN_NT
-#define LJ_JOIN_NT 256
+#define LJ_JOIN_NT 128
 #endif
 constexpr int JOIN_T = LJ_JOIN_T;
 constexpr int JOIN_NT = LJ_JOIN_NT;
@@ -503,6 +503,13 @@ __global__ void __launch_bounds__(SPLIT_NT) k_split_count(LsjDev md, SplitCtx cx
         const SplitTab tab = points ? split_tab_build(v, it.K, cells) : SplitTab{0, 0};
         for (i64 base = it.a + (i64)warp * 32 * SPLIT_U; base < it.e; base += (i64)SPLIT_NT * SPLIT_U) {
             int s[SPLIT_U];
+            if ((lane & 7) == 0) {
+#pragma unroll
+                for (int u = 0; u < SPLIT_U; ++u) {
+                    const i64 ip = base + 2 * (i64)SPLIT_NT * SPLIT_U + u * 32 + lane;
+                    if (ip < it.e) asm volatile("prefetch.global.L2 [%0];" ::"l"(A + ip));
+                }
+            }
 #pragma unroll
             for (int u = 0; u < SPLIT_U; ++u) {
                 const i64 i = base + u * 32 + lane;
@@ -596,6 +603,16 @@ __global__ void __launch_bounds__(SPLIT_NT, LJ_SPLIT_MINB) k_split_scatter(LsjDe
         for (i64 base = it.a + (i64)warp * 32 * SPLIT_U; base < it.e; base += (i64)SPLIT_NT * SPLIT_U) {
             int s[SPLIT_U];
             ulonglong2 r[SPLIT_U];
+            if ((lane & 7) == 0) {
+                // the records of two steps ahead start their way into L2 (one
+                // prefetch per 128-B line): more bytes in flight than the
+                // registers hold
+#pragma unroll
+                for (int u = 0; u < SPLIT_U; ++u) {
+                    const i64 ip = base + 2 * (i64)SPLIT_NT * SPLIT_U + u * 32 + lane;
+                    if (ip < it.e) asm volatile("prefetch.global.L2 [%0];" ::"l"(A + ip));
+                }
+            }
 #pragma unroll
             for (int u = 0; u < SPLIT_U; ++u) {
                 const i64 i = base + u * 32 + lane;
@@ -1419,7 +1436,10 @@ int lj_lsj_partition(const LjLsjModel *md, const uint64_t *keys, const uint64_t 
 // nbins + 2]: bin b = records [reg[b], reg[nbins + 1 + b]) of pairs (gaps
 // between the bins).  An overflow of any region (practically never) makes
 // the exact two-pass partition run instead, decided on the device.
-int64_t lj_lsj_partition_regions_capacity(int64_t n, int64_t nbins) { return est_capacity(n, (int)nbins); }
+int64_t lj_lsj_partition_regions_capacity(int64_t n, int64_t nbins) {
+    const i64 c = est_capacity_regions(n, (int)nbins);
+    return c > n ? c : n;
+}
 
 size_t lj_lsj_partition_regions_workspace_bytes(int64_t n, int64_t nbins) {
     (void)n;

@@ -35,6 +35,8 @@ inline size_t est_fix_bytes(size_t nb4) {
 
 // capacity of the output (records) for n tuples in nb bins: regions + overflow
 inline i64 est_capacity(i64 n, int nb) { return n + n / 16 + (i64)nb * (EST_PAD + EST_STRIDE + 1) + 64 + n; }
+// ... without the overflow area (run_partition_est_or_exact drops overflowing records)
+inline i64 est_capacity_regions(i64 n, int nb) { return n + n / 16 + (i64)nb * (EST_PAD + EST_STRIDE + 1) + 64; }
 
 // per-bin counts of every `stride`-th tuple (stride 1: the exact histogram)
 template <class Src>
@@ -112,7 +114,8 @@ __global__ void __launch_bounds__(PART2_NT, 1) k_bin_scatter_est(Src f0, i64 n, 
                                                               const i64 *__restrict__ rstart, u32 *gcur,
                                                               unsigned long long *ovf, ulonglong2 *out,
                                                               const u16 *__restrict__ codes,
-                                                              const unsigned long long *run_if = nullptr) {
+                                                              const unsigned long long *run_if = nullptr,
+                                                              int drop = 0) {
     if (run_if && *run_if == 0) return;  // a fallback pass that is not needed
     constexpr int U = EST_TILE / PART2_NT;
     constexpr size_t STAGE = EST_STAGE + (STORED ? EST_TILE * 2 : 0);
@@ -247,7 +250,14 @@ __global__ void __launch_bounds__(PART2_NT, 1) k_bin_scatter_est(Src f0, i64 n, 
                 const u64 k = j < nb ? ks[j] : ld_stream(f.keys + base + j);
                 const u64 p = j < nb ? ps[j] : ld_stream(f.pay + base + j);
                 i64 dst = dlt[b] + i;
-                if (!PEER && !STORED && dst >= srst[b + 1]) dst = srst[nbins] + (i64)atomicAdd(ovf, 1ULL);
+                if (!PEER && !STORED && dst >= srst[b + 1]) {
+                    // past the bin's region: the overflow area behind the regions
+                    // -- or only counted (drop: the consumer redoes the partition
+                    // exactly when the count is not zero, so the area need not exist)
+                    const i64 q = (i64)atomicAdd(ovf, 1ULL);
+                    if (drop) continue;
+                    dst = srst[nbins] + q;
+                }
                 ulonglong2 *o = PEER ? reinterpret_cast<ulonglong2 *>((uintptr_t)dst << 4) : out + dst;
                 *o = make_ulonglong2(k, p);
             }
@@ -387,7 +397,7 @@ inline size_t est_workspace_bytes(int nbins) {  // (+ part_align(2 n) for stored
 template <class Src>
 int run_partition_claims(const Src &f, i64 n, int nbins, int exact, ulonglong2 *out, i64 *reg, void *ws,
                          size_t ws_bytes, cudaStream_t st, u16 *codes = nullptr,
-                         const unsigned long long *run_if = nullptr) {
+                         const unsigned long long *run_if = nullptr, int drop_overflow = 0) {
     if (nbins < 1 || nbins > 2 * PART2_NT) {
         set_error("partition_est: nbins must be in [1, 2048]");
         return LJ_E_INVALID;
@@ -446,7 +456,7 @@ int run_partition_claims(const Src &f, i64 n, int nbins, int exact, ulonglong2 *
                 f, n, p.chunk, nbins, nst, rstart, gcur, ovf, out, codes, run_if);
         else
             k_bin_scatter_est<Src, false><<<p.blocks, PART2_NT, fix + nst * stage, st>>>(
-                f, n, p.chunk, nbins, nst, rstart, gcur, ovf, out, nullptr, run_if);
+                f, n, p.chunk, nbins, nst, rstart, gcur, ovf, out, nullptr, run_if, drop_overflow);
         LJ_CK_LAUNCH();
     }
     if (!exact) {
@@ -547,7 +557,8 @@ inline size_t est_exact_workspace_bytes(int nbins) {
 // standard deviations of the sample estimate), the exact two-pass partition
 // runs over the same output instead.  Its kernels are always enqueued and
 // return at once when the overflow count is zero, so the decision stays on
-// the device (no readback).  reg as run_partition_est, reg[2 nbins + 1] = 0.
+// the device (no readback).  reg as run_partition_est, reg[2 nbins + 1] = 0;
+// out: est_capacity_regions records (overflowing records are only counted).
 template <class Src>
 int run_partition_est_or_exact(const Src &f, i64 n, int nbins, ulonglong2 *out, i64 *reg, void *ws, size_t ws_bytes,
                                cudaStream_t st) {
@@ -557,7 +568,7 @@ int run_partition_est_or_exact(const Src &f, i64 n, int nbins, ulonglong2 *out, 
     }
     const size_t eb = est_workspace_bytes(nbins);
     i64 *starts = reinterpret_cast<i64 *>((char *)ws + eb);
-    int rc = run_partition_claims(f, n, nbins, 0, out, reg, ws, eb, st);
+    int rc = run_partition_claims(f, n, nbins, 0, out, reg, ws, eb, st, nullptr, nullptr, 1);
     if (rc) return rc;
     unsigned long long *cond = reinterpret_cast<unsigned long long *>(reg + 2 * nbins + 1);
     rc = run_partition_claims(f, n, nbins, 1, out, starts, ws, eb, st, nullptr, cond);

@@ -21,7 +21,7 @@ python tools/ncu_sum.py $O/full_c3.ncu-rep > $O/sum_c3.txt 2>&1
 timeout 900 $NCU -k regex:"k_grmi_probe_staged|k_bin_scatter_est|k_est_sample" -c 3 -o $O/full_c2 python tools/one_step.py c2 buffered 1 > $O/full_c2.log 2>&1
 python tools/ncu_export.py $O/full_c2.ncu-rep c2 r02_ncu_full_c2 k_grmi_probe_staged $O
 python tools/ncu_sum.py $O/full_c2.ncu-rep > $O/sum_c2.txt 2>&1
-timeout 1200 $NCU -k regex:"k_lsj_sort|k_split_count|k_split_scatter|k_bin_scatter_est|k_est_sample|k_lsj_join" -c 12 -o $O/full_c4 python tools/one_step.py c4 x 1 > $O/full_c4.log 2>&1
+timeout 1200 $NCU -k regex:"k_lsj_sort|k_split_count|k_split_scatter|k_bin_scatter_est|k_est_sample|k_lsj_join" -c 20 -o $O/full_c4 python tools/one_step.py c4 x 1 > $O/full_c4.log 2>&1
 python tools/ncu_export.py $O/full_c4.ncu-rep c4 r02_ncu_full_c4 k_lsj_sort $O
 python tools/ncu_sum.py $O/full_c4.ncu-rep > $O/sum_c4.txt 2>&1
 rm -f $O/full_c4.ncu-rep $O/full_c2.ncu-rep
