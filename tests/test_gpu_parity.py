@@ -838,6 +838,37 @@ def test_lsj_one_pass_partition_equals_exact_and_overflow_falls_back(lj, name, m
     assert lj.lsj_run(r, s, cfg).checksum == want
 
 
+def test_lsj_run_replays_as_a_cuda_graph(lj):
+    """lj_lsj_run enqueues everything on the stream (no host readback, the
+    partition's overflow fallback decided on the device), so the whole
+    learned sort-join captures into ONE CUDA graph; replays on fresh
+    result words equal the oracle."""
+    r, s = _lsj_sets()["c4"]
+    want = tuple(oracle.smj_checksum(*r.numpy(), *s.numpy()))
+    cfg = lj.LsjConfig(fanout=4096, sample_rate=0.01)
+    assert lj.lsj_run(r, s, cfg).checksum == want  # warm-up: kernel attributes are set outside the capture
+    from paper_2111_08824_b200 import _lib
+
+    lib = _lib.lib()
+    dev = r.keys.device
+    out = torch.zeros(4, dtype=torch.int64, device=dev)
+    ws = _lib.workspace(lib.lj_lsj_run_workspace_bytes(len(r), len(s), float(cfg.sample_rate)), dev)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(g, stream=side):
+            _lib.check(lib.lj_lsj_run(_lib.ptr(r.keys), _lib.ptr(r.payloads), len(r), _lib.ptr(s.keys),
+                                      _lib.ptr(s.payloads), len(s), float(cfg.sample_rate),
+                                      int(cfg.seed) & (2**64 - 1), _lib.ptr(out), _lib.ptr(ws), ws.numel(),
+                                      _lib.stream_ptr()), "lsj_run")
+    for _ in range(3):
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert tuple(int(v) & MASK for v in out.cpu().tolist()[:3]) == want
+
+
 C01_ALGOS = ["grmi-inlj", "buffered-grmi-inlj", "spline-hash-inlj", "lsj", "rmi-inlj"]
 
 
