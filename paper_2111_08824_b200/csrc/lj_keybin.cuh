@@ -30,10 +30,12 @@
 // Layout (u64 words, global and shared alike):
 //   [0] t0 (image of B[1])   [1] shift | log << 8   [2] nb   [3] sub-tables used
 //   [4 + j]  B[j], j in [1, nb)   (word 4 unused)
-//   u16 cells[KB_CELLS + 1]
-//   u8  sidx[KB_CELLS]            sub-table of a cell, 0xFF = none
-//   u64 sbase[nsub], u64 sshift[nsub]
-//   u16 subs[nsub][KB_SUBN + 1]
+//   sets of > 1024 boundaries:   u16 cells[KB_CELLS + 1]
+//   sets of <= 1024 boundaries (with sub-tables), packed so the lookup is
+//   one load per level:
+//     u32 cell32[KB_CELLS]        lo | (hi - lo) << 12 | sub-table << 24 (0xFF = none)
+//     {u64 base, u64 shift} shdr[nsub]
+//     u32 sub32[nsub][KB_SUBN]    lo | hi << 16 of every sub-cell
 #pragma once
 
 #include "lj_part.cuh"
@@ -50,7 +52,7 @@ __host__ __device__ inline int kb_nsub(int nb) { return nb <= 1024 ? 64 : 0; }
 __host__ __device__ inline int kb_cells_words() { return (KB_CELLS + 1 + 3) / 4; }
 __host__ __device__ inline int kb_words(int nb) {
     const int ns = kb_nsub(nb);
-    return 4 + ((nb + 3) & ~3) + kb_cells_words() + (ns ? KB_CELLS / 8 + 2 * ns + (ns * (KB_SUBN + 1) + 3) / 4 : 0);
+    return 4 + ((nb + 3) & ~3) + (ns ? KB_CELLS / 2 + 2 * ns + ns * KB_SUBN / 2 : kb_cells_words());
 }
 inline size_t kb_bytes(int nb) { return (size_t)kb_words(nb) * 8; }
 
@@ -92,23 +94,28 @@ struct KeyRangeBin {
     __device__ __forceinline__ u32 code(u64 k) const {
         const u64 *B = g + 4;
         const u64 *cw = g + 4 + ((nb + 3) & ~3);
-        const u16 *cells = reinterpret_cast<const u16 *>(cw);
         const u64 t = kb_image(k, (int)(ctl >> 8) & 1);
         const u32 c = kb_cell(t, t0, (int)(ctl & 63));
-        int lo = cells[c], hi = cells[c + 1];
+        int lo, hi;
         const int ns = kb_nsub(nb);
         if (ns) {
-            const u64 *sw = cw + kb_cells_words();
-            const int q = reinterpret_cast<const unsigned char *>(sw)[c];
-            if (q != 0xFF) {
-                const u64 *sbase = sw + KB_CELLS / 8, *sshift = sbase + ns;
-                const u16 *subs = reinterpret_cast<const u16 *>(sshift + ns) + q * (KB_SUBN + 1);
-                const u64 b = sbase[q];
-                const u64 d = t > b ? (t - b) >> sshift[q] : 0;
-                const int sc = d >= (u64)KB_SUBN ? KB_SUBN - 1 : (int)d;
-                lo = subs[sc];
-                hi = subs[sc + 1];
+            // packed: one load per level
+            const u32 e = reinterpret_cast<const u32 *>(cw)[c];
+            lo = (int)(e & 0xFFFu);
+            hi = lo + (int)((e >> 12) & 0xFFFu);
+            const u32 q = e >> 24;
+            if (q != 0xFFu) {
+                const ulonglong2 h = reinterpret_cast<const ulonglong2 *>(cw + KB_CELLS / 2)[q];  // {base, shift}
+                const u64 d = t > h.x ? (t - h.x) >> h.y : 0;
+                const u32 sc = d >= (u64)KB_SUBN ? (u32)(KB_SUBN - 1) : (u32)d;
+                const u32 p = reinterpret_cast<const u32 *>(cw + KB_CELLS / 2 + 2 * ns)[q * KB_SUBN + sc];
+                lo = (int)(p & 0xFFFFu);
+                hi = (int)(p >> 16);
             }
+        } else {
+            const u16 *cells = reinterpret_cast<const u16 *>(cw);
+            lo = cells[c];
+            hi = cells[c + 1];
         }
         // two unconditional, branch-free steps settle every range of <= 3
         // boundaries (a step on lo == hi is a no-op: B[lo] <= k there, B[0] =
@@ -203,10 +210,12 @@ static __global__ void __launch_bounds__(1024) k_keybin_build(u64 *lay, int nb) 
     const int m = worst[1] < worst[0] ? 1 : 0;
     if (m == 1) fill(1);
     u64 *cw = lay + 4 + ((nb + 3) & ~3);
-    u16 *cells = reinterpret_cast<u16 *>(cw);
-    for (int c = tid; c <= KB_CELLS; c += blockDim.x) cells[c] = cand[c];
     __shared__ int s_nsub;
     const int ns = kb_nsub(nb);
+    if (!ns) {
+        u16 *cells = reinterpret_cast<u16 *>(cw);
+        for (int c = tid; c <= KB_CELLS; c += blockDim.x) cells[c] = cand[c];
+    }
     if (tid == 0) {
         lay[0] = s_t0[m];
         // bit 16: the search starts with two unconditional steps (sets with a
@@ -219,10 +228,9 @@ static __global__ void __launch_bounds__(1024) k_keybin_build(u64 *lay, int nb) 
     if (ns) {
         // second level for the crowded cells (> 2 boundaries), first come
         // first served up to the budget (any choice is exact)
-        u64 *sw = cw + kb_cells_words();
-        unsigned char *sidx = reinterpret_cast<unsigned char *>(sw);
-        u64 *sbase = sw + KB_CELLS / 8, *sshift = sbase + ns;
-        u16 *subs = reinterpret_cast<u16 *>(sshift + ns);
+        u32 *cell32 = reinterpret_cast<u32 *>(cw);
+        u64 *shdr = cw + KB_CELLS / 2;
+        u32 *sub32 = reinterpret_cast<u32 *>(shdr + 2 * ns);
         const u64 t0 = s_t0[m];
         const int sh0 = s_shift[m];
         for (int c = tid; c < KB_CELLS; c += blockDim.x) {
@@ -231,18 +239,20 @@ static __global__ void __launch_bounds__(1024) k_keybin_build(u64 *lay, int nb) 
                 const int got = atomicAdd(&s_nsub, 1);
                 if (got < ns) q = got;
             }
-            sidx[c] = (unsigned char)q;
+            cell32[c] = (u32)cand[c] | ((u32)(cand[c + 1] - cand[c]) << 12) | ((u32)q << 24);
             if (q == 0xFF) continue;
             const int a = cand[c], e = cand[c + 1];  // boundaries j in (a, e] lie in cell c
             const u64 b = kb_image(pm[a + 1], m), last = kb_image(pm[e], m);
             int sh = 0;
             while (sh < 63 && ((last - b) >> sh) >= (u64)KB_SUBN) ++sh;
-            sbase[q] = b;
-            sshift[q] = (u64)sh;
-            u16 *st = subs + q * (KB_SUBN + 1);
-            // st[s] = a + #{ j in (a, e] : subcell(B[j]) < s }: the search in
-            // sub-cell s runs over (st[s], st[s + 1]] like the cells above
+            shdr[2 * q] = b;
+            shdr[2 * q + 1] = (u64)sh;
+            u32 *st = sub32 + q * KB_SUBN;
+            // s_sc = a + #{ j in (a, e] : subcell(B[j]) < sc }: the search in
+            // sub-cell sc runs over (s_sc, s_{sc+1}] like the cells above;
+            // st[sc] = s_sc | s_{sc+1} << 16
             int j = a + 1;
+            u32 prev = 0;
             for (int sc = 0; sc <= KB_SUBN; ++sc) {
                 while (j <= e) {
                     const u64 tj = kb_image(pm[j], m);
@@ -251,7 +261,9 @@ static __global__ void __launch_bounds__(1024) k_keybin_build(u64 *lay, int nb) 
                     if (scj < sc) ++j;
                     else break;
                 }
-                st[sc] = (u16)(sc == KB_SUBN ? e : j - 1);
+                const u32 cur = (u32)(sc == KB_SUBN ? e : j - 1);
+                if (sc > 0) st[sc - 1] = prev | (cur << 16);
+                prev = cur;
             }
         }
         (void)t0;

@@ -1401,6 +1401,9 @@ int lj_keybin_eval(const uint64_t *bounds, int64_t nbins, const uint64_t *keys, 
         KeyRangeBin kb;
         kb.g = lay;
         kb.nb = nb;
+        static unsigned long long attr = 0;  // one bit per device (the packed layout exceeds 48 KB)
+        if (once_per_device(attr))
+            LJ_CK(cudaFuncSetAttribute(k_keybin_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
         k_keybin_eval<<<grid_for(nk, 256, 4), 256, kb_bytes(nb), st>>>(kb, keys, nk, bins);
         LJ_CK_LAUNCH();
     }

@@ -140,7 +140,12 @@ __global__ void __launch_bounds__(PART2_NT, 1) k_bin_scatter_est(Src f0, i64 n, 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, shift = f.f.shift;
     for (int j = tid; j < nbins; j += PART2_NT) thist[j] = 0;
     for (int j = tid; j <= nbins; j += PART2_NT) srst[j] = rstart[j];
-    const i64 lo = blockIdx.x * chunk, hi = min(lo + chunk, n);
+    // The tiles cover [0, n_main): whole 16-B units of every column (chunks are
+    // multiples of 32 tuples), so a tile never has a tail outside its ring
+    // stage; the last n - n_main < 8 tuples are placed one by one by a single
+    // thread below.
+    const i64 n_main = STORED ? (n & ~(i64)7) : (n & ~(i64)1);
+    const i64 lo = blockIdx.x * chunk, hi = min(lo + chunk, n_main);
     const int ntiles = hi > lo ? (int)((hi - lo + EST_TILE - 1) / EST_TILE) : 0;
     auto issue = [&](int t, int s) {
         const i64 base = lo + (i64)t * EST_TILE;
@@ -165,6 +170,20 @@ __global__ void __launch_bounds__(PART2_NT, 1) k_bin_scatter_est(Src f0, i64 n, 
         for (int t = 0; t < min(nst - 1, ntiles); ++t) issue(t, t);
     }
     __syncthreads();
+    if (blockIdx.x == 0 && tid == 0) {
+        for (i64 i = n_main; i < n; ++i) {
+            const u64 k = f.keys[i], p = f.pay[i];
+            const int b = STORED ? (int)codes[i] : (int)(f.code(k) >> shift);
+            i64 dst = rstart[b] + (i64)atomicAdd(gcur + b, 1u);
+            if (!PEER && !STORED && dst >= rstart[b + 1]) {
+                const i64 q = (i64)atomicAdd(ovf, 1ULL);
+                if (drop) continue;
+                dst = rstart[nbins] + q;
+            }
+            ulonglong2 *o = PEER ? reinterpret_cast<ulonglong2 *>((uintptr_t)dst << 4) : out + dst;
+            *o = make_ulonglong2(k, p);
+        }
+    }
     // Four barriers per tile.  The next tile's binning (1) may start while
     // slower warps still write this tile's runs (4): (1) writes only the
     // tile histogram, which (4) does not read.  The run claims (global
@@ -176,7 +195,7 @@ __global__ void __launch_bounds__(PART2_NT, 1) k_bin_scatter_est(Src f0, i64 n, 
     for (int t = 0; t < ntiles; ++t) {
         mbar_wait(&full[s], phase);
         const i64 base = lo + (i64)t * EST_TILE;
-        const int cnt = (int)min((i64)EST_TILE, hi - base), nb = cnt & ~1, nb8 = cnt & ~7;
+        const int cnt = (int)min((i64)EST_TILE, hi - base);
         const unsigned char *st = ring + (size_t)s * STAGE;
         const u64 *ks = reinterpret_cast<const u64 *>(st), *ps = ks + EST_TILE;
         const u16 *cs = reinterpret_cast<const u16 *>(st + EST_TILE * 16);
@@ -185,10 +204,8 @@ __global__ void __launch_bounds__(PART2_NT, 1) k_bin_scatter_est(Src f0, i64 n, 
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int j = u * PART2_NT + tid;
-            if (STORED)
-                bj[u] = j < cnt ? (int)(j < nb8 ? cs[j] : codes[base + j]) : -1;
-            else
-                bj[u] = j < cnt ? (int)(f.code(j < nb ? ks[j] : ld_stream(f.keys + base + j)) >> shift) : -1;
+            if (STORED) bj[u] = j < cnt ? (int)cs[j] : -1;
+            else bj[u] = j < cnt ? (int)(f.code(ks[j]) >> shift) : -1;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) rj[u] = bj[u] >= 0 ? (int)atomicAdd(thist + bj[u], 1u) : 0;
@@ -247,8 +264,7 @@ __global__ void __launch_bounds__(PART2_NT, 1) k_bin_scatter_est(Src f0, i64 n, 
             if (i < cnt) {
                 const u32 pj = perm[i];
                 const int j = (int)(pj & 0xFFFFu), b = (int)(pj >> 16);
-                const u64 k = j < nb ? ks[j] : ld_stream(f.keys + base + j);
-                const u64 p = j < nb ? ps[j] : ld_stream(f.pay + base + j);
+                const u64 k = ks[j], p = ps[j];
                 i64 dst = dlt[b] + i;
                 if (!PEER && !STORED && dst >= srst[b + 1]) {
                     // past the bin's region: the overflow area behind the regions
