@@ -343,6 +343,9 @@ int lj_spline_hash_collect(const LjSplineHash *idx, const uint64_t *keys, int64_
 size_t lj_lsj_sample_workspace_bytes(int64_t total);
 int lj_lsj_sample(const uint64_t *keys, int64_t n, int64_t total, uint64_t seed, uint64_t *sample_sorted,
                   void *ws, size_t ws_bytes, void *stream);
+/* ... over keys[i * stride] (stride 2: interleaved {key, payload} records). */
+int lj_lsj_sample_strided(const uint64_t *keys, int64_t stride, int64_t n, int64_t total, uint64_t seed,
+                          uint64_t *sample_sorted, void *ws, size_t ws_bytes, void *stream);
 /* An LSJ relation model: the sample-fitted RMI plus equi-depth bins over its
  * predicted positions: bin(key) = table[pos(key)], pb[j] = first predicted
  * position of bin j (pb[nbins] = trained_len).  Monotone in the key. */
@@ -385,6 +388,12 @@ int64_t lj_lsj_partition_regions_capacity(int64_t n, int64_t nbins);
 size_t lj_lsj_partition_regions_workspace_bytes(int64_t n, int64_t nbins);
 int lj_lsj_partition_regions(const LjLsjModel *model, const uint64_t *keys, const uint64_t *pay, int64_t n,
                              uint64_t *pairs, int64_t *reg, void *ws, size_t ws_bytes, void *stream);
+/* ... reading the relation as n interleaved 16-B records {key, payload}
+ * (16-B aligned) in place -- the form the range shuffle of the distributed
+ * LSJ delivers (lsj.py:161-173: the per-worker ranges are contiguous record
+ * runs); same output, capacity and workspace. */
+int lj_lsj_partition_regions_rec(const LjLsjModel *model, const uint64_t *records, int64_t n, uint64_t *pairs,
+                                 int64_t *reg, void *ws, size_t ws_bytes, void *stream);
 /* The exact key-range bin function the partition passes evaluate in
  * shared memory (lj_keybin.cuh): bins[i] = #{ j in [1, nbins) :
  * bounds[j] <= keys[i] } for non-decreasing bounds (bounds[0] ignored).

@@ -9,7 +9,7 @@ fallback.
 """
 
 from .buffers import BufferPlan, analytic_buffer_size, buffered_probe, plan_buffers
-from .data import CorruptKeyFileError, Relation, load_keys_file, make_relation, relation_from_keys_file, write_keys_file
+from .data import CorruptKeyFileError, RecordRelation, Relation, load_keys_file, make_relation, relation_from_keys_file, write_keys_file
 from .gapped import GappedRmiIndex, build_grmi
 from .joins import ALGORITHMS, DEFAULT_OPTS, BenchReport, run_join
 from .learned_hash import SplineHashIndex, build_spline_hash

@@ -145,6 +145,7 @@ SIGNATURES = {
     "lj_spline_hash_collect": (_int, [ctypes.POINTER(LjSplineHash), _P, _i64, _P, _P, _P, _P]),
     "lj_lsj_sample_workspace_bytes": (_size_t, [_i64]),
     "lj_lsj_sample": (_int, [_P, _i64, _i64, _u64, _P, _P, _size_t, _P]),
+    "lj_lsj_sample_strided": (_int, [_P, _i64, _i64, _i64, _u64, _P, _P, _size_t, _P]),
     "lj_lsj_bins_workspace_bytes": (_size_t, [_i64]),
     "lj_lsj_bins": (_int, [ctypes.POINTER(LjRmi), _P, _i64, _i64, _P, _P, _P, _size_t, _P]),
     "lj_lsj_bins_from_bounds": (_int, [_P, _i64, _i64, _P, _P]),
@@ -154,6 +155,7 @@ SIGNATURES = {
     "lj_lsj_sort": (_int, [ctypes.POINTER(LjLsjModel), _P, _P, _i64, _P, _P, _size_t, _P, _P]),
     "lj_lsj_sort_regions": (_int, [ctypes.POINTER(LjLsjModel), _P, _P, _i64, _P, _P, _P, _size_t, _P, _P]),
     "lj_lsj_partition_regions": (_int, [ctypes.POINTER(LjLsjModel), _P, _P, _i64, _P, _P, _P, _size_t, _P]),
+    "lj_lsj_partition_regions_rec": (_int, [ctypes.POINTER(LjLsjModel), _P, _i64, _P, _P, _P, _size_t, _P]),
     "lj_lsj_partition_regions_capacity": (_i64, [_i64, _i64]),
     "lj_lsj_partition_regions_workspace_bytes": (_size_t, [_i64, _i64]),
     "lj_lsj_ref_bounds": (_int, [ctypes.POINTER(LjRmi), _P, _i64, _i64, _P, _P]),

@@ -88,6 +88,9 @@ constexpr int SPLIT_MAXF = 2048;  // slices per coarse bucket (point mode: 2x-1 
 #ifndef LJ_JOIN_NT
 #define LJ_JOIN_NT 128
 #endif
+#ifndef LJ_JOIN_MINB
+#define LJ_JOIN_MINB 1  // resident join CTAs per SM the register budget must allow
+#endif
 constexpr int JOIN_T = LJ_JOIN_T;
 constexpr int JOIN_NT = LJ_JOIN_NT;
 constexpr int WCAP = LJ_JOIN_WCAP;  // R slice keys staged per tile (+ the S tile: < 48 KB static)
@@ -1140,7 +1143,7 @@ __global__ void k_join_bounds(LsjDev mr, const ulonglong2 *__restrict__ R, const
 // mode 0: checksum; mode 1: counts[ns]; mode 2: pairs at offsets[ns].
 constexpr int JOIN_PER = JOIN_T / JOIN_NT;
 
-__global__ void __launch_bounds__(JOIN_NT) k_lsj_join(const ulonglong2 *__restrict__ R,
+__global__ void __launch_bounds__(JOIN_NT, LJ_JOIN_MINB) k_lsj_join(const ulonglong2 *__restrict__ R,
                                                       const ulonglong2 *__restrict__ S, i64 ns, const i64 *tb,
                                                       int mode, i64 *counts, const i64 *offsets, u64 *opr, u64 *ops,
                                                       u64 *out) {
@@ -1265,13 +1268,14 @@ __global__ void __launch_bounds__(JOIN_NT) k_lsj_join(const ulonglong2 *__restri
 // Stratified sample without replacement: one position per stratum
 // [j*n/total, (j+1)*n/total), offset by a counter draw (results-neutral;
 // the reference draws with numpy's Generator.choice, lsj.py:119-120).
-__global__ void k_sample(const u64 *keys, i64 n, i64 total, u64 seed, u64 *out) {
+// (stride: keys[i * stride], 2 for interleaved {key, payload} records)
+__global__ void k_sample(const u64 *keys, i64 stride, i64 n, i64 total, u64 seed, u64 *out) {
     for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < total; j += (i64)gridDim.x * blockDim.x) {
         i64 lo = (i64)(((unsigned __int128)j * (u64)n) / (u64)total);
         i64 hi = (i64)(((unsigned __int128)(j + 1) * (u64)n) / (u64)total);
         i64 w = hi > lo ? hi - lo : 1;
         i64 p = lo + (i64)__umul64hi(mix64(seed ^ (u64)j), (u64)w);
-        out[j] = keys[p < n ? p : n - 1];
+        out[j] = keys[(p < n ? p : n - 1) * stride];
     }
 }
 
@@ -1321,7 +1325,12 @@ size_t lj_lsj_sample_workspace_bytes(int64_t total) {
 
 int lj_lsj_sample(const uint64_t *keys, int64_t n, int64_t total, uint64_t seed, uint64_t *sample_sorted, void *ws,
                   size_t ws_bytes, void *stream) {
-    LJ_REQUIRE(n >= 1 && total >= 1 && total <= n, "need 1 <= total <= n");
+    return lj_lsj_sample_strided(keys, 1, n, total, seed, sample_sorted, ws, ws_bytes, stream);
+}
+
+int lj_lsj_sample_strided(const uint64_t *keys, int64_t stride, int64_t n, int64_t total, uint64_t seed,
+                          uint64_t *sample_sorted, void *ws, size_t ws_bytes, void *stream) {
+    LJ_REQUIRE(n >= 1 && total >= 1 && total <= n && stride >= 1, "need 1 <= total <= n, stride >= 1");
     if (ws_bytes < lj_lsj_sample_workspace_bytes(total)) {
         set_error("lj_lsj_sample: workspace too small");
         return LJ_E_WORKSPACE;
@@ -1331,7 +1340,7 @@ int lj_lsj_sample(const uint64_t *keys, int64_t n, int64_t total, uint64_t seed,
     char *cub_tmp = (char *)ws + al(sizeof(u64) * (size_t)total);
     size_t t = 0;
     cub::DeviceRadixSort::SortKeys(nullptr, t, (const u64 *)tmp, sample_sorted, (int64_t)total);
-    k_sample<<<grid_for(total, 256, 8), 256, 0, st>>>(keys, n, total, seed, tmp);
+    k_sample<<<grid_for(total, 256, 8), 256, 0, st>>>(keys, stride, n, total, seed, tmp);
     LJ_CK_LAUNCH();
     LJ_CK(cub::DeviceRadixSort::SortKeys(cub_tmp, t, (const u64 *)tmp, sample_sorted, (int64_t)total, 0, 64, st));
     return LJ_OK;
@@ -1537,6 +1546,30 @@ int lj_lsj_partition_regions(const LjLsjModel *md, const uint64_t *keys, const u
     kb.g = lay;
     kb.nb = nb;
     SoaSrc<KeyRangeBin> src{keys, pay, kb};
+    return run_partition_est_or_exact(src, n, nb, reinterpret_cast<ulonglong2 *>(pairs), reg, ws, pws, st);
+}
+
+// ... from interleaved 16-B records {key, payload} (the receive buffer of the
+// distributed LSJ's range shuffle): read in place, no conversion to columns.
+int lj_lsj_partition_regions_rec(const LjLsjModel *md, const uint64_t *records, int64_t n, uint64_t *pairs,
+                                 int64_t *reg, void *ws, size_t ws_bytes, void *stream) {
+    LJ_REQUIRE(md && md->table && md->pb && md->nbins >= 1 && md->nbins <= KB_MAXBINS, "model has no bins / > 2048 bins");
+    LJ_REQUIRE(((uintptr_t)records & 15) == 0 && n < (i64)0xFFFFFFFFLL, "records must be 16-B aligned, n < 2^32");
+    if (ws_bytes < lj_lsj_partition_regions_workspace_bytes(n, md->nbins)) {
+        set_error("lj_lsj_partition_regions_rec: workspace too small");
+        return LJ_E_WORKSPACE;
+    }
+    cudaStream_t st = as_stream(stream);
+    const int nb = (int)md->nbins;
+    const size_t pws = est_exact_workspace_bytes(nb);
+    u64 *lay = reinterpret_cast<u64 *>((char *)ws + pws);
+    k_lsj_key_bounds<<<(nb + 127) / 128, 128, 0, st>>>(make_lsj(*md), lay);
+    k_keybin_build<<<1, 1024, 0, st>>>(lay, nb);
+    LJ_CK_LAUNCH();
+    KeyRangeBin kb;
+    kb.g = lay;
+    kb.nb = nb;
+    AosSrc<KeyRangeBin> src{records, kb};
     return run_partition_est_or_exact(src, n, nb, reinterpret_cast<ulonglong2 *>(pairs), reg, ws, pws, st);
 }
 

@@ -61,6 +61,7 @@ struct NoTable {
 };
 template <class BinF>
 struct SoaSrc {
+    static constexpr bool AOS = false;
     const u64 *__restrict__ keys;
     const u64 *__restrict__ pay;
     BinF f;
@@ -68,6 +69,22 @@ struct SoaSrc {
         return ((uintptr_t)keys & 15) == 0 && ((uintptr_t)pay & 15) == 0;
     }
     __device__ __forceinline__ u32 code(u64 k) const { return f.code(k); }
+    __device__ __forceinline__ const u64 *key_ptr(i64 i) const { return keys + i; }
+    __device__ __forceinline__ const u64 *pay_ptr(i64 i) const { return pay + i; }
+};
+
+// The same relation as interleaved 16-B records {key, payload} (what the
+// range shuffle of the distributed LSJ delivers): the claims scatter and its
+// sample read them in place -- no conversion back to columns.
+template <class BinF>
+struct AosSrc {
+    static constexpr bool AOS = true;
+    const u64 *__restrict__ rec;
+    BinF f;
+    __host__ bool aligned16() const { return ((uintptr_t)rec & 15) == 0; }
+    __device__ __forceinline__ u32 code(u64 k) const { return f.code(k); }
+    __device__ __forceinline__ const u64 *key_ptr(i64 i) const { return rec + 2 * i; }
+    __device__ __forceinline__ const u64 *pay_ptr(i64 i) const { return rec + 2 * i + 1; }
 };
 
 // histogram copies -> mat[bin * blocks + block]

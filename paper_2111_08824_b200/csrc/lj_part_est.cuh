@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(256) k_est_sample(Src f0, i64 n, int nbins, in
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             i[u] = (blk + u * ngrp) * bs + lane;
-            k[u] = i[u] < n ? ld_stream(f.keys + i[u]) : 0;
+            k[u] = i[u] < n ? ld_stream(f.key_ptr(i[u])) : 0;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(256) k_est_sample(Src f0, i64 n, int nbins, in
     for (; blk * bs < n; blk += ngrp) {
         const i64 i = blk * bs + lane;
         if (i >= n) continue;
-        const u32 b = f.code(ld_stream(f.keys + i)) >> shift;
+        const u32 b = f.code(ld_stream(f.key_ptr(i))) >> shift;
         atomicAdd(h + b, 1u);
         if (codes) codes[i] = (u16)b;
     }
@@ -144,20 +144,26 @@ __global__ void __launch_bounds__(PART2_NT, 1) k_bin_scatter_est(Src f0, i64 n, 
     // multiples of 32 tuples), so a tile never has a tail outside its ring
     // stage; the last n - n_main < 8 tuples are placed one by one by a single
     // thread below.
-    const i64 n_main = STORED ? (n & ~(i64)7) : (n & ~(i64)1);
+    // (interleaved records: every record is a 16-B unit of its own)
+    constexpr bool AOS = Src::AOS;
+    const i64 n_main = STORED ? (n & ~(i64)7) : (AOS ? n : (n & ~(i64)1));
     const i64 lo = blockIdx.x * chunk, hi = min(lo + chunk, n_main);
     const int ntiles = hi > lo ? (int)((hi - lo + EST_TILE - 1) / EST_TILE) : 0;
     auto issue = [&](int t, int s) {
         const i64 base = lo + (i64)t * EST_TILE;
         const int cnt = (int)min((i64)EST_TILE, hi - base);
-        const unsigned b8 = (unsigned)(cnt * 8) & ~15u;
+        const unsigned b8 = AOS ? (unsigned)(cnt * 8) : ((unsigned)(cnt * 8) & ~15u);
         const unsigned b2 = STORED ? ((unsigned)(cnt * 2) & ~15u) : 0u;
         unsigned char *st = ring + (size_t)s * STAGE;
         if (b8 + b2) {
             mbar_arrive_expect_tx(&full[s], 2 * b8 + b2);
             if (b8) {
-                bulk_g2s(st, f.keys + base, b8, &full[s]);
-                bulk_g2s(st + EST_TILE * 8, f.pay + base, b8, &full[s]);
+                if constexpr (AOS) {
+                    bulk_g2s(st, f.key_ptr(base), 2 * b8, &full[s]);
+                } else {
+                    bulk_g2s(st, f.key_ptr(base), b8, &full[s]);
+                    bulk_g2s(st + EST_TILE * 8, f.pay_ptr(base), b8, &full[s]);
+                }
             }
             if (b2) bulk_g2s(st + EST_TILE * 16, codes + base, b2, &full[s]);
         } else {
@@ -172,7 +178,7 @@ __global__ void __launch_bounds__(PART2_NT, 1) k_bin_scatter_est(Src f0, i64 n, 
     __syncthreads();
     if (blockIdx.x == 0 && tid == 0) {
         for (i64 i = n_main; i < n; ++i) {
-            const u64 k = f.keys[i], p = f.pay[i];
+            const u64 k = *f.key_ptr(i), p = *f.pay_ptr(i);
             const int b = STORED ? (int)codes[i] : (int)(f.code(k) >> shift);
             i64 dst = rstart[b] + (i64)atomicAdd(gcur + b, 1u);
             if (!PEER && !STORED && dst >= rstart[b + 1]) {
@@ -205,7 +211,7 @@ __global__ void __launch_bounds__(PART2_NT, 1) k_bin_scatter_est(Src f0, i64 n, 
         for (int u = 0; u < U; ++u) {
             const int j = u * PART2_NT + tid;
             if (STORED) bj[u] = j < cnt ? (int)cs[j] : -1;
-            else bj[u] = j < cnt ? (int)(f.code(ks[j]) >> shift) : -1;
+            else bj[u] = j < cnt ? (int)(f.code(AOS ? ks[2 * j] : ks[j]) >> shift) : -1;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) rj[u] = bj[u] >= 0 ? (int)atomicAdd(thist + bj[u], 1u) : 0;
@@ -264,7 +270,15 @@ __global__ void __launch_bounds__(PART2_NT, 1) k_bin_scatter_est(Src f0, i64 n, 
             if (i < cnt) {
                 const u32 pj = perm[i];
                 const int j = (int)(pj & 0xFFFFu), b = (int)(pj >> 16);
-                const u64 k = ks[j], p = ps[j];
+                u64 k, p;
+                if constexpr (AOS) {
+                    const ulonglong2 r = reinterpret_cast<const ulonglong2 *>(st)[j];
+                    k = r.x;
+                    p = r.y;
+                } else {
+                    k = ks[j];
+                    p = ps[j];
+                }
                 i64 dst = dlt[b] + i;
                 if (!PEER && !STORED && dst >= srst[b + 1]) {
                     // past the bin's region: the overflow area behind the regions

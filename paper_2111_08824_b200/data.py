@@ -94,6 +94,39 @@ def fill_payloads(n: int, seed: int, offset: int = 0, device=None, stream=None) 
     return out
 
 
+class RecordRelation:
+    """A relation held as n interleaved 16-B records {key, payload} on the
+    GPU (an int64 [n, 2] tensor) -- what the range shuffle of the
+    distributed LSJ delivers.  ``lsj_join`` partitions it in place
+    (lj_lsj_partition_regions_rec); ``keys`` / ``payloads`` are strided views,
+    ``columns()`` the contiguous copy every other consumer takes."""
+
+    __slots__ = ("records",)
+
+    def __init__(self, records: torch.Tensor):
+        if records.dim() != 2 or records.shape[1] != 2 or records.dtype != torch.int64 or not records.is_cuda:
+            raise ValueError("records must be a CUDA int64 [n, 2] tensor")
+        self.records = records.contiguous()
+
+    @property
+    def keys(self) -> torch.Tensor:
+        return self.records[:, 0]
+
+    @property
+    def payloads(self) -> torch.Tensor:
+        return self.records[:, 1]
+
+    def __len__(self) -> int:
+        return int(self.records.shape[0])
+
+    @property
+    def device(self):
+        return self.records.device
+
+    def columns(self) -> "Relation":
+        return Relation(self.records[:, 0].contiguous(), self.records[:, 1].contiguous(), validate=False)
+
+
 def make_relation(keys, seed: int) -> Relation:
     """Attach the reference's deterministic nonzero payloads to ``keys``."""
     k = as_key_tensor(keys)

@@ -266,10 +266,10 @@ def lsj_join(r_keys, r_payloads, s_keys, s_payloads, config=None, group=None, *,
     if local_join_fn is None:
         def local_join_fn(rrec, srec):
             from . import lsj as _lsj
-            from .data import Relation
+            from .data import RecordRelation
 
-            r = Relation(rrec[:, 0].contiguous(), rrec[:, 1].contiguous(), validate=False)
-            s = Relation(srec[:, 0].contiguous(), srec[:, 1].contiguous(), validate=False)
+            # the received records are partitioned in place (no copy back to columns)
+            r, s = RecordRelation(rrec), RecordRelation(srec)
             res, _ = _lsj.lsj_join(r, s, LsjConfig(workers=1, fanout=config.fanout,
                                                     sample_rate=config.sample_rate, seed=config.seed),
                                    counters=False)

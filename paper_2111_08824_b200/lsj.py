@@ -31,13 +31,14 @@ import numpy as np
 import torch
 
 from . import _lib
-from .data import Relation
+from .data import RecordRelation, Relation
 from .models import RecursiveModelIndex
 from .results import JoinResult, PhaseBreakdown, SortStats
 from .util import exclusive_offsets, to_device_u64, unsigned_order
 
 BUCKET_TARGET = 8192  # mean tuples per sort unit (the shared-memory sort holds <= 12288)
-MAX_BINS = 2048       # coarse bins of the grid-wide partition (open write lines stay in L2)
+# coarse bins of the grid-wide partition (open write lines stay in L2); LJ_LSJ_MAX_BINS: tuning experiments
+MAX_BINS = min(2048, max(1, int(os.environ.get("LJ_LSJ_MAX_BINS", "2048"))))
 
 
 class ModelMismatchError(ValueError):
@@ -222,8 +223,10 @@ def _sample_sorted(relation: Relation, sample_rate: float, seed: int, sampler: s
     lib = _lib.lib()
     sample = torch.empty(total, dtype=torch.int64, device=relation.device)
     ws = _lib.workspace(lib.lj_lsj_sample_workspace_bytes(total), relation.device)
-    _lib.check(lib.lj_lsj_sample(_lib.ptr(relation.keys), n, total, int(seed) & (2**64 - 1), _lib.ptr(sample),
-                                 _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "lsj_sample")
+    # (interleaved records: the keys are every second word)
+    base, stride = (relation.records, 2) if isinstance(relation, RecordRelation) else (relation.keys, 1)
+    _lib.check(lib.lj_lsj_sample_strided(_lib.ptr(base), stride, n, total, int(seed) & (2**64 - 1), _lib.ptr(sample),
+                                         _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "lsj_sample")
     return sample
 
 
@@ -292,6 +295,27 @@ def _partition_regions(keys, payloads, lm: LsjModel):
     _lib.check(lib.lj_lsj_partition_regions(ctypes.byref(c), _lib.ptr(keys), _lib.ptr(payloads), n, _lib.ptr(pairs),
                                             _lib.ptr(reg), _lib.ptr(ws), ws.numel(), _lib.stream_ptr()),
                "lsj_partition_regions")
+    return pairs, reg
+
+
+def _records_ok(rel: RecordRelation, lm: LsjModel) -> bool:
+    return (lm.nbins <= 2048 and len(rel) < 0xFFFFFFFF and rel.records.data_ptr() % 16 == 0
+            and not os.environ.get("LJ_LSJ_EXACT_PARTITION"))
+
+
+def _partition_regions_rec(records, lm: LsjModel):
+    """lj_lsj_partition_regions_rec: the one-pass regions straight from
+    interleaved records (no conversion to columns)."""
+    lib = _lib.lib()
+    n = records.shape[0]
+    cap = lib.lj_lsj_partition_regions_capacity(n, lm.nbins)
+    pairs = torch.empty(2 * max(cap, 1), dtype=torch.int64, device=records.device)
+    reg = torch.empty(2 * lm.nbins + 2, dtype=torch.int64, device=records.device)
+    ws = _lib.workspace(lib.lj_lsj_partition_regions_workspace_bytes(n, lm.nbins), records.device)
+    c = lm.c_struct()
+    _lib.check(lib.lj_lsj_partition_regions_rec(ctypes.byref(c), _lib.ptr(records), n, _lib.ptr(pairs), _lib.ptr(reg),
+                                                _lib.ptr(ws), ws.numel(), _lib.stream_ptr()),
+               "lsj_partition_regions_rec")
     return pairs, reg
 
 
@@ -451,10 +475,12 @@ def _join(r_sorted: SortedRelation, s_sorted: SortedRelation, materialize: bool)
     return JoinResult(pr, ps)
 
 
-def lsj_join(r: Relation, s: Relation, config: LsjConfig | None = None, materialize: bool = False,
-             models: tuple | None = None, counters: bool = True, sampler: str = "device"):
+def lsj_join(r: Relation | RecordRelation, s: Relation | RecordRelation, config: LsjConfig | None = None,
+             materialize: bool = False, models: tuple | None = None, counters: bool = True, sampler: str = "device"):
     """lsj.py:373-405: the full learned sort-join -> (JoinResult,
     PhaseBreakdown).  Phase times are CUDA-event times on the stream.
+    A ``RecordRelation`` (interleaved records, e.g. a shuffle's receive
+    buffer) is sampled and partitioned in place.
     ``models`` = (model_r, model_s) RMIs fitted elsewhere (e.g. the
     reference's): they are then bucketed at the reference's uniform scale."""
     config = config or LsjConfig()
@@ -475,9 +501,16 @@ def lsj_join(r: Relation, s: Relation, config: LsjConfig | None = None, material
     ev[1].record()
     # partition: one pass into estimated-capacity regions (no exact counting
     # pass) when the columns allow it, else the exact K6/K7
-    fast_r, fast_s = _regions_ok(r.keys, r.payloads, lr), _regions_ok(s.keys, s.payloads, ls)
-    pr, str_ = (_partition_regions if fast_r else _partition)(r.keys, r.payloads, lr)
-    ps, sts = (_partition_regions if fast_s else _partition)(s.keys, s.payloads, ls)
+    def part(rel, lm):
+        if isinstance(rel, RecordRelation):
+            if _records_ok(rel, lm):
+                return True, _partition_regions_rec(rel.records, lm)
+            rel = rel.columns()
+        fast = _regions_ok(rel.keys, rel.payloads, lm)
+        return fast, (_partition_regions if fast else _partition)(rel.keys, rel.payloads, lm)
+
+    fast_r, (pr, str_) = part(r, lr)
+    fast_s, (ps, sts) = part(s, ls)
     ev[2].record()
     if fast_r:
         pr, str_, dr = _sort_regions(pr, str_, lr, len(r))

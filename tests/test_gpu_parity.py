@@ -838,6 +838,69 @@ def test_lsj_one_pass_partition_equals_exact_and_overflow_falls_back(lj, name, m
     assert lj.lsj_run(r, s, cfg).checksum == want
 
 
+@pytest.mark.parametrize("name", ["c4", "zipf"])
+def test_lsj_from_interleaved_records_equals_columns_and_oracle(lj, name, monkeypatch):
+    """A RecordRelation (interleaved 16-B records, the distributed LSJ's
+    receive buffer) is sampled and partitioned in place
+    (lj_lsj_sample_strided, lj_lsj_partition_regions_rec): every bin holds
+    the same multiset as the column partition's, the join equals the column
+    join and the oracle -- also through the overflow fallback (LJ_EST_TIGHT)
+    and with the exact partition forced (records copied to columns)."""
+    r, s = _lsj_sets()[name]
+    want = tuple(oracle.smj_checksum(*r.numpy(), *s.numpy()))
+    cfg = lj.LsjConfig(fanout=4096, sample_rate=0.01)
+    rr = lj.RecordRelation(torch.stack([r.keys, r.payloads], dim=1))
+    sr = lj.RecordRelation(torch.stack([s.keys, s.payloads], dim=1))
+    assert torch.equal(rr.keys, r.keys) and torch.equal(sr.payloads, s.payloads)
+    from paper_2111_08824_b200 import lsj as L
+
+    _, lm = L.prepare_model(r, cfg.sample_rate, cfg.seed)
+    _, lm2 = L.prepare_model(rr, cfg.sample_rate, cfg.seed)
+    assert torch.equal(lm.pb, lm2.pb)  # the strided sample draws the same keys
+    pc, regc = L._partition_regions(r.keys, r.payloads, lm)
+    pr, regr = L._partition_regions_rec(rr.records, lm)
+    assert torch.equal(regc, regr)
+    nb = lm.nbins
+    reg = regc.cpu().tolist()
+    for b in sorted({0, 1, nb // 2, nb - 1}):
+        a, e = reg[b], reg[nb + 1 + b]
+        kc, kr = pc[2 * a:2 * e:2], pr[2 * a:2 * e:2]
+        oc, orr = torch.argsort(kc), torch.argsort(kr)
+        assert torch.equal(kc[oc], kr[orr])
+        assert torch.equal(pc[2 * a + 1:2 * e:2][oc].sort().values, pr[2 * a + 1:2 * e:2][orr].sort().values)
+    res, br = lj.lsj_join(rr, sr, cfg)
+    ref, br0 = lj.lsj_join(r, s, cfg)
+    assert res.checksum == want == ref.checksum
+    assert br.sort_stats == br0.sort_stats
+    mixed, _ = lj.lsj_join(r, sr, cfg)  # one side as records
+    assert mixed.checksum == want
+    monkeypatch.setenv("LJ_EST_TIGHT", "1")
+    assert lj.lsj_join(rr, sr, cfg)[0].checksum == want
+    monkeypatch.delenv("LJ_EST_TIGHT")
+    monkeypatch.setenv("LJ_LSJ_EXACT_PARTITION", "1")
+    assert lj.lsj_join(rr, sr, cfg)[0].checksum == want
+
+
+def test_record_relation_edge_cases(lj):
+    """Odd sizes (tiles with a tail), tiny relations (the zero-sample
+    fallback) and an empty side through the record path."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    for n in (1, 2, 7, 4097, 100003):
+        k = torch.randperm(4 * n, generator=g, device="cuda")[:n].to(torch.int64) * 977 + 13
+        p = k * 3 + 1
+        sk = k[torch.randint(0, n, (2 * n + 1,), generator=g, device="cuda")]
+        sp = sk ^ 0x55
+        want = tuple(oracle.smj_checksum(k.cpu().numpy().view("u8"), p.cpu().numpy().view("u8"),
+                                         sk.cpu().numpy().view("u8"), sp.cpu().numpy().view("u8")))
+        rr = lj.RecordRelation(torch.stack([k, p], dim=1))
+        sr = lj.RecordRelation(torch.stack([sk, sp], dim=1))
+        assert lj.lsj_join(rr, sr, lj.LsjConfig(sample_rate=0.01))[0].checksum == want
+    empty = lj.RecordRelation(torch.empty((0, 2), dtype=torch.int64, device="cuda"))
+    assert lj.lsj_join(empty, sr)[0].checksum == (0, 0, 0)
+    with pytest.raises(ValueError):
+        lj.RecordRelation(torch.zeros(4, dtype=torch.int64, device="cuda"))
+
+
 def test_lsj_run_replays_as_a_cuda_graph(lj):
     """lj_lsj_run enqueues everything on the stream (no host readback, the
     partition's overflow fallback decided on the device), so the whole
