@@ -22,6 +22,12 @@
 namespace lj {
 
 constexpr int EST_STRIDE = 16;
+constexpr int EST_STRIDE_MAX = 64;
+// The sample is every stride-th block of 32 tuples.  Above 2^30 tuples one
+// block in 64 keeps >= 8192 sampled tuples per bin at 2048 bins (C4's count
+// at 2^28 and stride 16), so the regions' 1/16 slack stays > 8 sigma of the
+// estimate; C3's 2 * 10^9 probes: sample pass 0.57 -> 0.15 ms.
+inline int est_stride(i64 n) { return n >= ((i64)1 << 30) ? EST_STRIDE_MAX : EST_STRIDE; }
 constexpr i64 EST_PAD = 4096;
 constexpr int EST_TILE = 4096;
 constexpr size_t EST_STAGE = (size_t)EST_TILE * 16;
@@ -34,9 +40,12 @@ inline size_t est_fix_bytes(size_t nb4) {
 }
 
 // capacity of the output (records) for n tuples in nb bins: regions + overflow
-inline i64 est_capacity(i64 n, int nb) { return n + n / 16 + (i64)nb * (EST_PAD + EST_STRIDE + 1) + 64 + n; }
-// ... without the overflow area (run_partition_est_or_exact drops overflowing records)
-inline i64 est_capacity_regions(i64 n, int nb) { return n + n / 16 + (i64)nb * (EST_PAD + EST_STRIDE + 1) + 64; }
+// (the estimates sum to at most n + 32 * stride: the last sampled block; 17/16 of that + the per-bin pads)
+inline i64 est_capacity_regions(i64 n, int nb) {
+    return n + n / 16 + (i64)nb * (EST_PAD + EST_STRIDE_MAX + 1) + 34 * EST_STRIDE_MAX + 64;
+}
+inline i64 est_capacity(i64 n, int nb) { return est_capacity_regions(n, nb) + n; }
+// ... est_capacity_regions: without the overflow area (run_partition_est_or_exact drops overflowing records)
 
 // per-bin counts of every `stride`-th tuple (stride 1: the exact histogram)
 template <class Src>
@@ -88,7 +97,8 @@ __global__ void __launch_bounds__(256) k_est_sample(Src f0, i64 n, int nbins, in
 
 // region capacity per bin: the exact count, or the sample estimate with
 // slack (est * 17/16 + pad)
-static __global__ void k_est_caps(const u32 *est, int nbins, int exact, i64 *cap, int tight = 0) {
+static __global__ void k_est_caps(const u32 *est, int nbins, int exact, i64 *cap, int tight = 0,
+                                  int stride = EST_STRIDE) {
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b <= nbins; b += gridDim.x * blockDim.x) {
         if (b == nbins) {
             cap[b] = 0;
@@ -98,8 +108,8 @@ static __global__ void k_est_caps(const u32 *est, int nbins, int exact, i64 *cap
             cap[b] = (i64)est[b];
             continue;
         }
-        const i64 e = (i64)est[b] * EST_STRIDE;
-        cap[b] = tight ? e : e + e / 16 + EST_PAD + EST_STRIDE;  // tight (LJ_EST_TIGHT): tests force overflow
+        const i64 e = (i64)est[b] * stride;
+        cap[b] = tight ? e : e + e / 16 + EST_PAD + stride;  // tight (LJ_EST_TIGHT): tests force overflow
     }
 }
 
@@ -459,14 +469,14 @@ int run_partition_claims(const Src &f, i64 n, int nbins, int exact, ulonglong2 *
                                    PT_SMEM_MAX));
         LJ_CK(cudaFuncSetAttribute(k_est_sample<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_SMEM_MAX));
     }
-    const int stride = exact ? 1 : EST_STRIDE;
+    const int stride = exact ? 1 : est_stride(n);
     const bool stored = exact && codes != nullptr && nbins <= 65536;
     if (n > 0) {
         k_est_sample<Src><<<grid_for((n + stride - 1) / stride, 256, 4), 256, tb + sizeof(u32) * nbins, st>>>(
             f, n, nbins, stride, est, stored ? codes : nullptr, run_if);
         LJ_CK_LAUNCH();
     }
-    k_est_caps<<<(nbins + 256) / 256, 256, 0, st>>>(est, nbins, exact, cap, getenv("LJ_EST_TIGHT") != nullptr);
+    k_est_caps<<<(nbins + 256) / 256, 256, 0, st>>>(est, nbins, exact, cap, getenv("LJ_EST_TIGHT") != nullptr, stride);
     LJ_CK_LAUNCH();
     size_t t = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, t, cap, rstart, (int64_t)(nbins + 1));

@@ -504,8 +504,8 @@ int lj_spline_hash_bucket_est(const LjSplineHash *idx, const uint64_t *keys, con
         SoaSrc<KeyRangeBin> ksrc{keys, pay, kb};
         int rc = run_partition_est(ksrc, nk, nb, reinterpret_cast<ulonglong2 *>(pairs_out), reg_out, ws, eb, st);
         if (rc) return rc;
-        k_fill_gaps<<<(unsigned)nb, 256, 0, st>>>(reg_out, nb, reinterpret_cast<ulonglong2 *>(pairs_out));
-        LJ_CK_LAUNCH();
+        // (the staged probe reads only the filled part [reg[w], reg[nb + 1 + w]) of
+        // every region: the gaps behind the fills need no reserved-key records)
         return hash_windows(idx->model, lay, nb, 0, meta, st);
     }
     if (keybin) {
