@@ -381,14 +381,49 @@ def make_step(inp, index, variant="buffered", world: int = 1, distributed: bool 
         st.reduced = True
         return st
 
-    def lsj_step(out):
+    def lsj_phases(out):
+        # the same LSJ through the Python orchestration (one C call per
+        # phase), which records the phase events
         res, br = lj.lsj_join(inp.r, inp.s, cfg, counters=False)
         st.holder["br"] = br
         out.copy_(res._words)
         return out
 
+    # The step: the whole LSJ as ONE asynchronous C call (lj_lsj_run: sample,
+    # fit, bins, partition, sort, join of both relations from one workspace;
+    # no host readback, the partition's overflow fallback decided on the
+    # device), captured into a CUDA graph on first use and replayed.
+    from paper_2111_08824_b200 import _lib
+
+    lib = _lib.lib()
+    dev = inp.r.keys.device
+    ws = _lib.workspace(lib.lj_lsj_run_workspace_bytes(n_r, n_s, float(o["sample_rate"])), dev)
+    cap = {}
+
+    def one_call(out):
+        _lib.check(lib.lj_lsj_run(_lib.ptr(inp.r.keys), _lib.ptr(inp.r.payloads), n_r, _lib.ptr(inp.s.keys),
+                                  _lib.ptr(inp.s.payloads), n_s, float(o["sample_rate"]), int(o["seed"]) & MASK,
+                                  _lib.ptr(out), _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "lsj_run")
+
+    def lsj_step(out):
+        if cap.get("ptr") != out.data_ptr():
+            one_call(out)  # kernel attributes are set outside the capture
+            torch.cuda.synchronize()
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(graph, stream=side):
+                    one_call(out)
+            torch.cuda.current_stream().wait_stream(side)
+            cap.update(ptr=out.data_ptr(), graph=graph)
+        cap["graph"].replay()
+        return out
+
     st = Step([("lsj", lsj_step)], "sort", 32 * (n_r + n_s), "lsj sort phase (k_split_*, k_lsj_sort)",
               f"sort phase: 32 B/tuple (read 16 + write 16) x {n_r + n_s} tuples; whole pipeline 80 B/tuple")
+    st.phases = lsj_phases
+    st.path = "lj_lsj_run (one C call) replayed as a CUDA graph"
     return st
 
 
@@ -495,7 +530,7 @@ def run_b200(args):
     for i in range(args.steps):
         flush.zero_()
         if run_step.dominant == "sort":  # LSJ: phase events recorded by lsj_join itself
-            run_step(out)
+            getattr(run_step, "phases", run_step)(out)
             torch.cuda.synchronize()
             br = run_step.holder["br"]
             dom.append(br.sort * 1e3)
@@ -549,51 +584,25 @@ def run_b200(args):
             gbs = bpt * (n_r + n_s) / (ms / 1e3) / 1e9
             roofline["lsj_phases"][name] = {"ms": ms, "achieved": gbs, "frac": gbs / peak,
                                             "algorithmic_bytes": f"{bpt} B/tuple x {n_r + n_s}"}
-    if phase_ms and args.config == "c4":
-        # the whole LSJ as ONE asynchronous C call (lj_lsj_run: no host readback,
-        # the partition's overflow fallback decided on the device) captured into
-        # a CUDA graph and replayed: no launch gaps, no Python between kernels
-        try:
-            import paper_2111_08824_b200 as lj
-            from paper_2111_08824_b200 import _lib
-
-            o = dict(lj.DEFAULT_OPTS, **inp.opts)
-            lib = _lib.lib()
-            o3 = torch.zeros(4, dtype=torch.int64, device=dev)
-            ws = _lib.workspace(lib.lj_lsj_run_workspace_bytes(n_r, n_s, float(o["sample_rate"])), dev)
-
-            def one_call():
-                _lib.check(lib.lj_lsj_run(_lib.ptr(inp.r.keys), _lib.ptr(inp.r.payloads), n_r, _lib.ptr(inp.s.keys),
-                                          _lib.ptr(inp.s.payloads), n_s, float(o["sample_rate"]),
-                                          int(o["seed"]) & MASK, _lib.ptr(o3), _lib.ptr(ws), ws.numel(),
-                                          _lib.stream_ptr()), "lsj_run")
-
-            one_call()  # kernel attributes are set outside the capture
+    if phase_ms and hasattr(run_step, "phases"):
+        # the step is lj_lsj_run replayed as one CUDA graph; the phase times
+        # above come from the same LSJ run phase by phase from Python
+        pm = []
+        o3 = torch.zeros(4, dtype=torch.int64, device=dev)
+        for i in range(args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            run_step.phases(o3)
+            e1.record()
             torch.cuda.synchronize()
-            side = torch.cuda.Stream()
-            side.wait_stream(torch.cuda.current_stream())
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.stream(side):
-                with torch.cuda.graph(graph, stream=side):
-                    one_call()
-            gms = []
-            for i in range(args.steps):
-                flush.zero_()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                graph.replay()
-                e1.record()
-                torch.cuda.synchronize()
-                gms.append(e0.elapsed_time(e1))
-            w3 = o3.cpu().tolist()
-            roofline["one_call_graph"] = {
-                "ms_per_step": statistics.mean(gms),
-                "same_checksum": [v & MASK for v in w3[:3]] == [w[0] & MASK, w[1] & MASK, xor_all],
-                "note": "lj_lsj_run (sample, fit, partition, sort, join of both relations) captured once into a "
-                        "CUDA graph, replayed per step"}
-            del ws, graph
-        except Exception as exc:  # diagnostics only: the step above is the measurement
-            roofline["one_call_graph"] = {"error": repr(exc)}
+            pm.append(e0.elapsed_time(e1))
+        w3 = o3.cpu().tolist()
+        roofline["step_path"] = run_step.path
+        roofline["python_orchestration"] = {
+            "ms_per_step": statistics.mean(pm),
+            "same_checksum": [v & MASK for v in w3[:3]] == [w[0] & MASK, w[1] & MASK, xor_all],
+            "note": "lsj_join: one C call per phase with CUDA events between them (the source of lsj_phases)"}
     ph = run_step.holder.get("phases")
     if ph is not None and "shuffle" in ph:
         # the range shuffle against NVLink (16 B x (|R|+|S|)/G x
