@@ -1838,6 +1838,41 @@ static size_t run_part_bytes(const LsjRunRel &a, const LsjRunRel &b) {
     return al(sizeof(ulonglong2) * (size_t)std::max(ca, cb));
 }
 
+// scratch of the sample / fit / bins steps alone (S's run on a side stream
+// while R is partitioned and sorted, so they need their own)
+static size_t run_smpl_scratch_bytes(const LsjRunRel &r) {
+    size_t s = lj_lsj_sample_workspace_bytes(std::max<i64>(r.total, 1));
+    s = std::max(s, lj_rmi_fit_workspace_bytes(r.tl, r.fanout));
+    s = std::max(s, lj_lsj_bins_workspace_bytes(r.tl));
+    return al(s);
+}
+
+// A side stream and fork / join events per (host thread, device): S's model
+// steps are a chain of small kernels that leave the GPU mostly idle, so they
+// run beside R's partition and sort.  Event record / wait on the caller's
+// stream keeps the whole call asynchronous and capturable (the side stream
+// joins the capture through the fork event and leaves it at the join event).
+struct SideStream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+static SideStream *side_stream() {
+    thread_local SideStream tab[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    SideStream &t = tab[dev & 63];
+    if (!t.s) {
+        if (cudaStreamCreateWithFlags(&t.s, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&t.fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&t.join, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            t.s = nullptr;
+            return nullptr;  // no side stream: everything on the caller's stream
+        }
+    }
+    return &t;
+}
+
 static size_t run_scratch_bytes(const LsjRunRel &r) {
     size_t s = lj_lsj_sample_workspace_bytes(std::max<i64>(r.total, 1));
     s = std::max(s, lj_rmi_fit_workspace_bytes(r.tl, r.fanout));
@@ -1855,7 +1890,7 @@ extern "C" {
 size_t lj_lsj_run_workspace_bytes(int64_t nr, int64_t ns, double sample_rate) {
     const LsjRunRel a = run_rel(nr, sample_rate), b = run_rel(ns, sample_rate);
     return run_keep_bytes(a) + run_keep_bytes(b) + run_part_bytes(a, b) +
-           std::max(run_scratch_bytes(a), run_scratch_bytes(b)) +
+           std::max(run_scratch_bytes(a), run_scratch_bytes(b)) + run_smpl_scratch_bytes(b) +
            al(lj_lsj_join_workspace_bytes(ns)) + 1024;
 }
 
@@ -1908,21 +1943,46 @@ int lj_lsj_run(const uint64_t *rk, const uint64_t *rp, int64_t nr, const uint64_
     const size_t sb = std::max(run_scratch_bytes(rel[0]), run_scratch_bytes(rel[1]));
     p += sb;
     char *join_ws = take(lj_lsj_join_workspace_bytes(ns));
+    const size_t ssb = run_smpl_scratch_bytes(rel[1]);
+    char *smpl_scratch = take(ssb);
+    // smpl: stratified sample (or {min, max}), RMI fit, equi-depth bins
+    auto smpl = [&](int x, char *scr, size_t scr_bytes, void *strm) -> int {
+        const LsjRunRel &r = rel[x];
+        int rc;
+        if (r.total > 0) {
+            rc = lj_lsj_sample(keys[x], r.n, r.total, seeds[x], sbuf[x], scr, scr_bytes, strm);
+            if (rc) return rc;
+        } else {
+            k_minmax2<<<1, 1024, 0, as_stream(strm)>>>(keys[x], r.n, sbuf[x]);
+            LJ_CK_LAUNCH();
+        }
+        rc = lj_rmi_fit(sbuf[x], r.tl, r.fanout, root[x], leaves[x], err[x], scr, scr_bytes, strm);
+        if (rc) return rc;
+        return lj_lsj_bins(&rmi[x], sbuf[x], r.tl, r.nbins, pb[x], table[x], scr, scr_bytes, strm);
+    };
+    // S's model on the side stream, beside R's partition and sort
+    static const bool one_stream = getenv("LJ_LSJ_ONE_STREAM") != nullptr;
+    SideStream *side = one_stream ? nullptr : side_stream();
+    if (side) {
+        LJ_CK(cudaEventRecord(side->fork, st));
+        LJ_CK(cudaStreamWaitEvent(side->s, side->fork, 0));
+        const int rc = smpl(1, smpl_scratch, ssb, side->s);
+        // (join the side stream even on an error: a capture must not be left forked)
+        LJ_CK(cudaEventRecord(side->join, side->s));
+        if (rc) {
+            cudaStreamWaitEvent(st, side->join, 0);
+            return rc;
+        }
+    }
     for (int x = 0; x < 2; ++x) {
         const LsjRunRel &r = rel[x];
         int rc;
-        // smpl: stratified sample (or {min, max}), RMI fit, equi-depth bins
-        if (r.total > 0) {
-            rc = lj_lsj_sample(keys[x], r.n, r.total, seeds[x], sbuf[x], scratch, sb, stream);
+        if (x == 0 || !side) {
+            rc = smpl(x, scratch, sb, stream);
             if (rc) return rc;
         } else {
-            k_minmax2<<<1, 1024, 0, st>>>(keys[x], r.n, sbuf[x]);
-            LJ_CK_LAUNCH();
+            LJ_CK(cudaStreamWaitEvent(st, side->join, 0));
         }
-        rc = lj_rmi_fit(sbuf[x], r.tl, r.fanout, root[x], leaves[x], err[x], scratch, sb, stream);
-        if (rc) return rc;
-        rc = lj_lsj_bins(&rmi[x], sbuf[x], r.tl, r.nbins, pb[x], table[x], scratch, sb, stream);
-        if (rc) return rc;
         // part + sort (K6/K7, split, K8): one-pass regions when the columns
         // allow the bulk-copy ring, else the exact partition
         if (r.nbins <= KB_MAXBINS && ((uintptr_t)keys[x] & 15) == 0 && ((uintptr_t)pays[x] & 15) == 0 &&

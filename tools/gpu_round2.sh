@@ -1,6 +1,6 @@
 # round-2 measurement: GPU tests, smoke, bench lines (all configs + reference arm),
 # launch list of the default bench, ncu --set full of the dominant kernels
-V=${V:-r2b}
+V=${V:-r2d}
 O=gpurun_out/$V
 mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
