@@ -448,6 +448,11 @@ size_t lj_lsj_run_workspace_bytes(int64_t nr, int64_t ns, double sample_rate);
 int lj_lsj_run(const uint64_t *r_keys, const uint64_t *r_pay, int64_t nr, const uint64_t *s_keys,
                const uint64_t *s_pay, int64_t ns, double sample_rate, uint64_t seed, uint64_t *out, void *ws,
                size_t ws_bytes, void *stream);
+/* ... with both relations held as interleaved 16-B records {key, payload}
+ * (16-B aligned, < 2^32 - 1 each): what a range shuffle delivers; same
+ * workspace, same result words. */
+int lj_lsj_run_rec(const uint64_t *r_records, int64_t nr, const uint64_t *s_records, int64_t ns, double sample_rate,
+                   uint64_t seed, uint64_t *out, void *ws, size_t ws_bytes, void *stream);
 size_t lj_lsj_join_workspace_bytes(int64_t ns);
 int lj_lsj_join(const LjLsjModel *model_r, const uint64_t *r_pairs, int64_t nr, const int64_t *r_starts,
                 const uint64_t *s_pairs, int64_t ns, int mode, int64_t *counts, const int64_t *offsets,

@@ -89,6 +89,7 @@ SIGNATURES = {
     "lj_lsj_run_multi": (_int, [_int, _P, _P, _P, _P, _P, _P, _P, _P, _P, _i64, _i64, ctypes.c_double, _u64, _P, _P,
                                 _P, _P]),
     "lj_lsj_run": (_int, [_P, _P, _i64, _P, _P, _i64, ctypes.c_double, _u64, _P, _P, _size_t, _P]),
+    "lj_lsj_run_rec": (_int, [_P, _i64, _P, _i64, ctypes.c_double, _u64, _P, _P, _size_t, _P]),
     "lj_spline_segments": (_int, [ctypes.POINTER(LjSpline), _P, _P]),
     "lj_spline_slots_plan": (_int, [ctypes.POINTER(LjSpline), _P, _P, _i64, _P, _P, _size_t, _P]),
     "lj_spline_slots_fill": (_int, [_P, _P, _i64, _P, _i64, _P, _size_t, _P]),

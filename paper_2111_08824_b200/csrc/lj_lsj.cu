@@ -1784,11 +1784,11 @@ namespace lj {
 
 // {min, max} of the keys (unsigned), one block: the two-key "sample" of a
 // relation too small for sample_rate (lsj.py zero-sample fallback)
-__global__ void k_minmax2(const u64 *keys, i64 n, u64 *out) {
+__global__ void k_minmax2(const u64 *keys, i64 stride, i64 n, u64 *out) {
     __shared__ u64 smin[1024], smax[1024];
     u64 lo = ~0ULL, hi = 0;
     for (i64 i = threadIdx.x; i < n; i += blockDim.x) {
-        const u64 k = keys[i];
+        const u64 k = keys[i * stride];
         lo = k < lo ? k : lo;
         hi = k > hi ? k : hi;
     }
@@ -1894,8 +1894,10 @@ size_t lj_lsj_run_workspace_bytes(int64_t nr, int64_t ns, double sample_rate) {
            al(lj_lsj_join_workspace_bytes(ns)) + 1024;
 }
 
-int lj_lsj_run(const uint64_t *rk, const uint64_t *rp, int64_t nr, const uint64_t *sk, const uint64_t *sp, int64_t ns,
-               double sample_rate, uint64_t seed, uint64_t *out, void *ws, size_t ws_bytes, void *stream) {
+// records = true: rk / sk point at n interleaved {key, payload} records (rp / sp unused)
+static int lsj_run_impl(bool records, const uint64_t *rk, const uint64_t *rp, int64_t nr, const uint64_t *sk,
+                        const uint64_t *sp, int64_t ns, double sample_rate, uint64_t seed, uint64_t *out, void *ws,
+                        size_t ws_bytes, void *stream) {
     LJ_REQUIRE(sample_rate > 0.0 && sample_rate <= 1.0, "sample_rate must be in (0, 1]");
     LJ_REQUIRE(nr >= 0 && ns >= 0, "sizes must be >= 0");
     cudaStream_t st = as_stream(stream);
@@ -1950,10 +1952,10 @@ int lj_lsj_run(const uint64_t *rk, const uint64_t *rp, int64_t nr, const uint64_
         const LsjRunRel &r = rel[x];
         int rc;
         if (r.total > 0) {
-            rc = lj_lsj_sample(keys[x], r.n, r.total, seeds[x], sbuf[x], scr, scr_bytes, strm);
+            rc = lj_lsj_sample_strided(keys[x], records ? 2 : 1, r.n, r.total, seeds[x], sbuf[x], scr, scr_bytes, strm);
             if (rc) return rc;
         } else {
-            k_minmax2<<<1, 1024, 0, as_stream(strm)>>>(keys[x], r.n, sbuf[x]);
+            k_minmax2<<<1, 1024, 0, as_stream(strm)>>>(keys[x], records ? 2 : 1, r.n, sbuf[x]);
             LJ_CK_LAUNCH();
         }
         rc = lj_rmi_fit(sbuf[x], r.tl, r.fanout, root[x], leaves[x], err[x], scr, scr_bytes, strm);
@@ -1985,8 +1987,13 @@ int lj_lsj_run(const uint64_t *rk, const uint64_t *rp, int64_t nr, const uint64_
         }
         // part + sort (K6/K7, split, K8): one-pass regions when the columns
         // allow the bulk-copy ring, else the exact partition
-        if (r.nbins <= KB_MAXBINS && ((uintptr_t)keys[x] & 15) == 0 && ((uintptr_t)pays[x] & 15) == 0 &&
-            r.n < (i64)0xFFFFFFFFLL) {
+        if (records) {
+            rc = lj_lsj_partition_regions_rec(&md[x], keys[x], r.n, pairs, reg[x], scratch, sb, stream);
+            if (rc) return rc;
+            rc = lj_lsj_sort_regions(&md[x], pairs, reinterpret_cast<u64 *>(sorted[x]), r.n, reg[x], starts[x], scratch,
+                                     sb, nullptr, stream);
+        } else if (r.nbins <= KB_MAXBINS && ((uintptr_t)keys[x] & 15) == 0 && ((uintptr_t)pays[x] & 15) == 0 &&
+                   r.n < (i64)0xFFFFFFFFLL) {
             rc = lj_lsj_partition_regions(&md[x], keys[x], pays[x], r.n, pairs, reg[x], scratch, sb, stream);
             if (rc) return rc;
             rc = lj_lsj_sort_regions(&md[x], pairs, reinterpret_cast<u64 *>(sorted[x]), r.n, reg[x], starts[x], scratch,
@@ -2003,6 +2010,20 @@ int lj_lsj_run(const uint64_t *rk, const uint64_t *rp, int64_t nr, const uint64_
     return lj_lsj_join(&md[0], reinterpret_cast<const u64 *>(sorted[0]), nr, starts[0],
                        reinterpret_cast<const u64 *>(sorted[1]), ns, 0, nullptr, nullptr, nullptr, nullptr, out, 0,
                        join_ws, lj_lsj_join_workspace_bytes(ns), stream);
+}
+
+int lj_lsj_run(const uint64_t *rk, const uint64_t *rp, int64_t nr, const uint64_t *sk, const uint64_t *sp, int64_t ns,
+               double sample_rate, uint64_t seed, uint64_t *out, void *ws, size_t ws_bytes, void *stream) {
+    return lsj_run_impl(false, rk, rp, nr, sk, sp, ns, sample_rate, seed, out, ws, ws_bytes, stream);
+}
+
+int lj_lsj_run_rec(const uint64_t *r_records, int64_t nr, const uint64_t *s_records, int64_t ns, double sample_rate,
+                   uint64_t seed, uint64_t *out, void *ws, size_t ws_bytes, void *stream) {
+    LJ_REQUIRE((((uintptr_t)r_records | (uintptr_t)s_records) & 15) == 0 && nr < (i64)0xFFFFFFFFLL &&
+                   ns < (i64)0xFFFFFFFFLL,
+               "records must be 16-B aligned, fewer than 2^32 - 1 per relation");
+    return lsj_run_impl(true, r_records, nullptr, nr, s_records, nullptr, ns, sample_rate, seed, out, ws, ws_bytes,
+                        stream);
 }
 
 }  // extern "C"

@@ -93,14 +93,6 @@ __global__ void k_fold_xor(const u64 *xs, int nranks, u64 *words) {
     words[2] = x;
 }
 
-__global__ void k_deinterleave2(const ulonglong2 *p, i64 n, u64 *k, u64 *v) {
-    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
-        const ulonglong2 e = p[i];
-        k[i] = e.x;
-        v[i] = e.y;
-    }
-}
-
 struct DevGuard {
     int prev = 0;
     DevGuard() { cudaGetDevice(&prev); }
@@ -187,7 +179,6 @@ size_t lj_lsj_run_multi_workspace_bytes(int ndev, int64_t nr_local, int64_t ns_l
            alm(16 * (size_t)std::max<int64_t>(nr_local, 1)) + alm(16 * (size_t)std::max<int64_t>(ns_local, 1)) +
            2 * alm(sizeof(i64) * (size_t)(ndev + 1)) +                                   // partitioned + starts
            alm(16 * (size_t)cap_r) + alm(16 * (size_t)cap_s) +                            // received runs
-           alm(16 * (size_t)cap_r) + alm(16 * (size_t)cap_s) +                            // their SoA columns
            alm(scr) + alm(lj_lsj_run_workspace_bytes(cap_r, cap_s, sample_rate)) +
            lj_reduce_sums_workspace_bytes(ndev) + 1024;
 }
@@ -224,7 +215,6 @@ int lj_lsj_run_multi(int ndev, const int *devs, void *const *comms, void *const 
         u64 *pr, *ps;
         i64 *str, *sts;
         ulonglong2 *rr, *rs;
-        u64 *rk, *rp, *sk, *sp;
         char *scr, *run, *red;
         size_t scr_b, run_b;
     };
@@ -258,10 +248,6 @@ int lj_lsj_run_multi(int ndev, const int *devs, void *const *comms, void *const 
         l.sts = (i64 *)take(sizeof(i64) * (size_t)(ndev + 1));
         l.rr = (ulonglong2 *)take(16 * (size_t)cap_r);
         l.rs = (ulonglong2 *)take(16 * (size_t)cap_s);
-        l.rk = (u64 *)take(8 * (size_t)cap_r);
-        l.rp = (u64 *)take(8 * (size_t)cap_r);
-        l.sk = (u64 *)take(8 * (size_t)cap_s);
-        l.sp = (u64 *)take(8 * (size_t)cap_s);
         l.red = take(lj_reduce_sums_workspace_bytes(ndev));
         l.run_b = lj_lsj_run_workspace_bytes(cap_r, cap_s, sample_rate);
         l.run = take(l.run_b);
@@ -370,13 +356,11 @@ int lj_lsj_run_multi(int ndev, const int *devs, void *const *comms, void *const 
         LJ_CK(cudaSetDevice(devs[d]));
         Lay &l = L[(size_t)d];
         cudaStream_t st = as_stream(streams[d]);
-        if (rin[(size_t)d])
-            k_deinterleave2<<<grid_for(rin[(size_t)d], 256, 8), 256, 0, st>>>(l.rr, rin[(size_t)d], l.rk, l.rp);
-        if (sin[(size_t)d])
-            k_deinterleave2<<<grid_for(sin[(size_t)d], 256, 8), 256, 0, st>>>(l.rs, sin[(size_t)d], l.sk, l.sp);
-        LJ_CK_LAUNCH();
-        const int rc = lj_lsj_run(l.rk, l.rp, rin[(size_t)d], l.sk, l.sp, sin[(size_t)d], sample_rate, seed, out[d],
-                                  l.run, l.run_b, streams[d]);
+        // the received records are sampled and partitioned in place (no copy back to columns)
+        (void)st;
+        const int rc = lj_lsj_run_rec(reinterpret_cast<const u64 *>(l.rr), rin[(size_t)d],
+                                      reinterpret_cast<const u64 *>(l.rs), sin[(size_t)d], sample_rate, seed, out[d],
+                                      l.run, l.run_b, streams[d]);
         if (rc) return rc;
         words[(size_t)d] = out[d];
         red[(size_t)d] = l.red;

@@ -539,7 +539,8 @@ def lsj_join(r: Relation | RecordRelation, s: Relation | RecordRelation, config:
     return result, br
 
 
-def lsj_run(r: Relation, s: Relation, config: LsjConfig | None = None) -> JoinResult:
+def lsj_run(r: Relation | RecordRelation, s: Relation | RecordRelation,
+            config: LsjConfig | None = None) -> JoinResult:
     """lsj_join in ONE asynchronous C call (lj_lsj_run): sample, fit, bins,
     partition, sort and merge-join of both relations from one workspace,
     the root of each model kept on the device.  -> JoinResult of the
@@ -551,6 +552,14 @@ def lsj_run(r: Relation, s: Relation, config: LsjConfig | None = None) -> JoinRe
         return JoinResult(words=out)
     lib = _lib.lib()
     ws = _lib.workspace(lib.lj_lsj_run_workspace_bytes(len(r), len(s), float(config.sample_rate)), dev)
+    if isinstance(r, RecordRelation) or isinstance(s, RecordRelation):
+        # lj_lsj_run_rec: both sides as interleaved records, read in place
+        rr = r.records if isinstance(r, RecordRelation) else torch.stack([r.keys, r.payloads], dim=1)
+        sr = s.records if isinstance(s, RecordRelation) else torch.stack([s.keys, s.payloads], dim=1)
+        _lib.check(lib.lj_lsj_run_rec(_lib.ptr(rr), len(r), _lib.ptr(sr), len(s), float(config.sample_rate),
+                                      int(config.seed) & (2**64 - 1), _lib.ptr(out), _lib.ptr(ws), ws.numel(),
+                                      _lib.stream_ptr()), "lsj_run_rec")
+        return JoinResult(words=out)
     _lib.check(lib.lj_lsj_run(_lib.ptr(r.keys), _lib.ptr(r.payloads), len(r), _lib.ptr(s.keys), _lib.ptr(s.payloads),
                               len(s), float(config.sample_rate), int(config.seed) & (2**64 - 1), _lib.ptr(out),
                               _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "lsj_run")

@@ -874,6 +874,8 @@ def test_lsj_from_interleaved_records_equals_columns_and_oracle(lj, name, monkey
     assert br.sort_stats == br0.sort_stats
     mixed, _ = lj.lsj_join(r, sr, cfg)  # one side as records
     assert mixed.checksum == want
+    assert lj.lsj_run(rr, sr, cfg).checksum == want  # lj_lsj_run_rec: the one-call ABI over records
+    assert lj.lsj_run(rr, s, cfg).checksum == want
     monkeypatch.setenv("LJ_EST_TIGHT", "1")
     assert lj.lsj_join(rr, sr, cfg)[0].checksum == want
     monkeypatch.delenv("LJ_EST_TIGHT")
@@ -895,6 +897,7 @@ def test_record_relation_edge_cases(lj):
         rr = lj.RecordRelation(torch.stack([k, p], dim=1))
         sr = lj.RecordRelation(torch.stack([sk, sp], dim=1))
         assert lj.lsj_join(rr, sr, lj.LsjConfig(sample_rate=0.01))[0].checksum == want
+        assert lj.lsj_run(rr, sr, lj.LsjConfig(sample_rate=0.01)).checksum == want
     empty = lj.RecordRelation(torch.empty((0, 2), dtype=torch.int64, device="cuda"))
     assert lj.lsj_join(empty, sr)[0].checksum == (0, 0, 0)
     with pytest.raises(ValueError):
