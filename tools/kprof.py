@@ -39,3 +39,4 @@ tot = sum(v[0] for v in agg.values())
 print(f"{cfg} {variant}: {tot / steps / 1000:.3f} ms of kernels per step")
 for name, (t, c) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:28]:
     print(f"{t / steps / 1000:9.3f} ms  x{c / steps:5.1f}  {name}")
+print("words", [int(v) & ((1 << 64) - 1) for v in out.cpu().tolist()])
