@@ -838,7 +838,7 @@ def test_lsj_one_pass_partition_equals_exact_and_overflow_falls_back(lj, name, m
     assert lj.lsj_run(r, s, cfg).checksum == want
 
 
-@pytest.mark.parametrize("name", ["c4", "zipf"])
+@pytest.mark.parametrize("name", ["c4", "zipf", "tiny", "c5"])
 def test_lsj_from_interleaved_records_equals_columns_and_oracle(lj, name, monkeypatch):
     """A RecordRelation (interleaved 16-B records, the distributed LSJ's
     receive buffer) is sampled and partitioned in place
@@ -862,7 +862,7 @@ def test_lsj_from_interleaved_records_equals_columns_and_oracle(lj, name, monkey
     assert torch.equal(regc, regr)
     nb = lm.nbins
     reg = regc.cpu().tolist()
-    for b in sorted({0, 1, nb // 2, nb - 1}):
+    for b in sorted({0, min(1, nb - 1), nb // 2, nb - 1}):
         a, e = reg[b], reg[nb + 1 + b]
         kc, kr = pc[2 * a:2 * e:2], pr[2 * a:2 * e:2]
         oc, orr = torch.argsort(kc), torch.argsort(kr)
