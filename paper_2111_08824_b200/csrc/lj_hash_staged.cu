@@ -60,18 +60,28 @@ static inline size_t part_align_c(size_t v) { return (v + 255) & ~(size_t)255; }
 #define LJ_HS_D 2
 #endif
 #ifndef LJ_HS_PIECE
-#define LJ_HS_PIECE 32768
+#define LJ_HS_PIECE 49152  // a multiple of HS_NT * HS_U: no partly filled last iteration (32768: 22.07, 49152: 21.84 ms)
 #endif
 #ifndef LJ_HS_NC
-#define LJ_HS_NC 1024
+#define LJ_HS_NC 2048
 #endif
 #ifndef LJ_HS_SPREAD
 #define LJ_HS_SPREAD 2  // probe-table slots per position (the first slot of a position is even: one 32-B pair)
 #endif
 #ifndef LJ_HS_ROUNDS
-#define LJ_HS_ROUNDS 1  // forward slot scan: 2 = unfinished probes compacted across the warp (29.9 vs 23.1 ms: a lane's
-                        // dependent loads no longer overlap), 1 = rounds of one pair per
-                        // unfinished probe of the thread, 0 = slot by slot
+#define LJ_HS_ROUNDS 3  // forward slot scan: 3 = one pair per LANE per round (the lane's first unfinished probe selected
+                        // into one register set and followed to its end: a round is one pair scan, not one per probe
+                        // position u at 3-9 active lanes; 22.07 ms with 2048 cells), 1 = one pair per unfinished probe
+                        // of the thread per round (22.84 ms), 2 = unfinished probes compacted across the warp (29.9 ms: a
+                        // lane's dependent loads no longer overlap), 0 = slot by slot
+#endif
+#ifndef LJ_HS_LAYOUT
+#define LJ_HS_LAYOUT 0  // probe table: 0 = entries pushed forward in key order; 1 (ablation) = home pairs + tails: no
+                        // displacement, but 18.4 % of C3's probes go on to a tail (chains >= 3, rank >= 1) against 16.1 %
+                        // past the first pair here, and a tail is another line: 23.6 vs 22.8 ms
+#endif
+#if LJ_HS_LAYOUT == 1 && ((LJ_HS_ROUNDS != 1 && LJ_HS_ROUNDS != 3) || LJ_HS_SPREAD != 2)
+#error "the home-pair probe table is probed in rounds of pairs at two slots per position"
 #endif
 constexpr int HS_NT = LJ_HS_NT;
 constexpr int HS_CTAS = LJ_HS_CTAS;  // CTAs per SM
@@ -116,6 +126,7 @@ __device__ __forceinline__ i64 lower_bound_u64(const u64 *a, i64 n, u64 k) {
 
 // ------------------------------------------------------------ probe table
 
+#if LJ_HS_LAYOUT == 0
 // t_j = 2 pos_j - j over the sorted build keys; cnt[0] counts zero
 // payloads, cnt[1] equal adjacent keys
 __global__ void k_slots_t(SplineDev m, const u64 *sk, const u64 *sp, i64 n, i64 *t, unsigned long long *cnt) {
@@ -132,6 +143,7 @@ __global__ void k_slots_t(SplineDev m, const u64 *sk, const u64 *sp, i64 n, i64 
 struct MaxI64 {
     __device__ __forceinline__ i64 operator()(const i64 &a, const i64 &b) const { return a > b ? a : b; }
 };
+using SlotScanOp = MaxI64;
 
 // plan[0] = slots needed (even, incl. the terminating pair), plan[1] = zero
 // payloads, plan[2] = duplicate build keys
@@ -169,6 +181,100 @@ __global__ void k_slots_fill(const i64 *M, const u64 *sk, const u64 *sp, i64 n, 
         }
     }
 }
+#else
+// Home pairs + tails (layout 1).  All entries with key k share pos(k), so a
+// probe needs the chain of ITS position only (learned_hash.py:81-96).  Chain
+// C_p = the entries of position p in key order (contiguous in the sorted
+// build keys):
+//   |C_p| <= 2: the home pair (slots 2p, 2p + 1) holds the chain, empty slots
+//               are {~0, 0};
+//   |C_p| >= 3: slot 2p = the first entry, slot 2p + 1 = {~0, tail} with
+//               tail the (even, >= 2n) slot where entries 1.. of the chain
+//               follow in key order, closed by at least one {~0, 0} and
+//               padded to whole pairs.
+// No entry is displaced by its neighbours' chains: a probe whose key is
+// among the first two of its chain (or absent from a short chain) is done
+// after ONE 32-B load; the others continue at the tail.  P[j] = pos of the
+// sorted build key j; cnt as in layout 0.
+__global__ void k_slots_t(SplineDev m, const u64 *sk, const u64 *sp, i64 n, i64 *P, unsigned long long *cnt) {
+    u32 z = 0, d = 0;
+    for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < n; j += (i64)gridDim.x * blockDim.x) {
+        P[j] = m.pos(sk[j]);
+        z += sp[j] == 0;
+        d += j > 0 && sk[j] == sk[j - 1];
+    }
+    if (z) atomicAdd(cnt, (unsigned long long)z);
+    if (d) atomicAdd(cnt + 1, (unsigned long long)d);
+}
+
+__device__ __forceinline__ i64 first_pos_geq(const i64 *P, i64 n, i64 p) {
+    i64 lo = 0, hi = n;
+    while (lo < hi) {
+        const i64 mid = (lo + hi) >> 1;
+        if (__ldg(reinterpret_cast<const long long *>(P) + mid) < p) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// A[j] = tail slots of the chain headed by entry j (0 unless j heads a chain
+// of >= 3): its |C| - 1 further entries + a closing {~0, 0}, rounded up to pairs
+__global__ void k_slots_tail(const i64 *P, i64 n, i64 *A) {
+    for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < n; j += (i64)gridDim.x * blockDim.x) {
+        const i64 p = P[j];
+        i64 a = 0;
+        if ((j == 0 || P[j - 1] != p) && j + 2 < n && P[j + 2] == p) {
+            const i64 c = first_pos_geq(P, n, p + 1) - j;
+            a = (c + 1) & ~(i64)1;
+        }
+        A[j] = a;
+    }
+}
+
+struct SumI64 {
+    __device__ __forceinline__ i64 operator()(const i64 &a, const i64 &b) const { return a + b; }
+};
+using SlotScanOp = SumI64;  // the plan's scan: inclusive tail-slot sums M[j]
+
+// plan[0] = slots needed: 2n home slots + the tails + a closing pair
+__global__ void k_slots_size(const i64 *M, i64 n, unsigned long long *zero, i64 *plan) {
+    plan[0] = 2 * n + M[n - 1] + 2;
+    plan[1] = (i64)zero[0];
+    plan[2] = (i64)zero[1];
+}
+
+__global__ void k_slots_fill(const i64 *M, const i64 *P, const u64 *sk, const u64 *sp, i64 n, i64 L,
+                             ulonglong2 *slots) {
+    const ulonglong2 none = make_ulonglong2(~0ULL, 0ULL);
+    for (i64 s = blockIdx.x * (i64)blockDim.x + threadIdx.x; s < L; s += (i64)gridDim.x * blockDim.x) {
+        if (s < 2 * n) {
+            const i64 p = s >> 1;
+            const i64 h = first_pos_geq(P, n, p);
+            ulonglong2 v = none;
+            if (h < n && P[h] == p) {
+                if (!(s & 1)) v = make_ulonglong2(sk[h], sp[h]);
+                else if (h + 2 < n && P[h + 2] == p) v = make_ulonglong2(~0ULL, (u64)(2 * n + (h > 0 ? M[h - 1] : 0)));
+                else if (h + 1 < n && P[h + 1] == p) v = make_ulonglong2(sk[h + 1], sp[h + 1]);
+            }
+            slots[s] = v;
+            continue;
+        }
+        const i64 t = s - 2 * n;
+        ulonglong2 v = none;
+        if (t < M[n - 1]) {
+            i64 lo = 0, hi = n;  // the head h whose tail [M[h-1], M[h]) holds t: first j with M[j] > t
+            while (lo < hi) {
+                const i64 mid = (lo + hi) >> 1;
+                if (__ldg(reinterpret_cast<const long long *>(M) + mid) <= t) lo = mid + 1;
+                else hi = mid;
+            }
+            const i64 h = lo, j = h + 1 + (t - (h > 0 ? M[h - 1] : 0));
+            if (j < n && P[j] == P[h]) v = make_ulonglong2(sk[j], sp[j]);
+        }
+        slots[s] = v;
+    }
+}
+#endif
 
 // ------------------------------------------------------------ windows
 
@@ -302,6 +408,26 @@ __device__ __forceinline__ bool pair_scan(const u64 (&e)[4], u64 k, u64 ps, Acc3
     if (e[2] == k && e[3]) acc.add(e[3], ps);
     return true;
 }
+
+#if LJ_HS_LAYOUT == 1
+// The HOME pair of a probe for key k (layout 1): its chain's first two
+// entries, or the first entry and {~0, tail}.  Matches are added; returns
+// true when the chain goes on in its tail (e[3]) and may still hold k (the
+// tail's keys are >= e[0]; with unique build keys a match ends the probe).
+template <bool UNIQUE>
+__device__ __forceinline__ bool pair_first(const u64 (&e)[4], u64 k, u64 ps, Acc3 &acc) {
+    const bool tail = e[2] == ~0ULL && e[3] != 0;
+    if (UNIQUE) {
+        const u64 h = (e[0] == k && e[1]) ? e[1] : ((e[2] == k && e[3]) ? e[3] : 0ULL);
+        if (h) acc.add(h, ps);
+        return tail && e[0] < k;
+    }
+    if (e[0] == k && e[1]) acc.add(e[1], ps);
+    if (tail) return e[0] <= k;
+    if (e[2] == k && e[3]) acc.add(e[3], ps);
+    return false;
+}
+#endif
 
 // 16-B asynchronous global -> shared copy with an L2 cache policy
 __device__ __forceinline__ void cp_async16_ef(void *dst, const void *src, u64 pol) {
@@ -526,7 +652,13 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
 #pragma unroll
             for (int u = 0; u < HS_U; ++u) {
                 // (a skipped probe's pair {~0, 0, ~0, 0} matches nothing)
+#if LJ_HS_LAYOUT == 1
+                const bool go = pair_first<UNIQUE>(e[u], k[u], ps[u], acc) && s0[u] >= 0;
+                if (go) s0[u] = (i64)e[u][3] - 2;  // round r reads the tail pair r - 1
+                need |= (unsigned)go << u;
+#else
                 need |= (unsigned)(pair_scan<UNIQUE>(e[u], k[u], ps[u], acc) && s0[u] >= 0) << u;
+#endif
             }
 #if LJ_HS_ROUNDS == 0
             // (ablation) one dependent 16-B slot at a time, probe by probe
@@ -582,6 +714,35 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
                 need = 0;
             }
 #endif
+#if LJ_HS_ROUNDS == 3
+            // One pair per LANE per round: the lane's first unfinished probe
+            // is selected into (kq, pq, sq) and followed to its end, then the
+            // next -- a round costs one pair scan instead of one per probe
+            // position u (whose blocks run at 3-9 active lanes each).
+            {
+                u64 kq = 0, pq = 0;
+                i64 sq = 0;
+                bool fresh = true;
+#pragma unroll 1
+                while (need) {
+                    if (fresh) {
+                        const int u0 = __ffs(need) - 1;
+                        kq = k[0], pq = ps[0], sq = s0[0];
+#pragma unroll
+                        for (int u = 1; u < HS_U; ++u) {
+                            if (u0 == u) kq = k[u], pq = ps[u], sq = s0[u];
+                        }
+                    }
+                    sq += 2;
+                    u64 ee[4];
+                    asm volatile("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+                                 : "=l"(ee[0]), "=l"(ee[1]), "=l"(ee[2]), "=l"(ee[3])
+                                 : "l"(slots + sq));
+                    fresh = !pair_scan<UNIQUE>(ee, kq, pq, acc);
+                    if (fresh) need &= need - 1u;
+                }
+            }
+#endif
 #pragma unroll 1
             for (int r = 1; need; ++r) {
 #pragma unroll
@@ -613,7 +774,7 @@ extern "C" {
 
 size_t lj_spline_slots_workspace_bytes(int64_t n) {
     size_t t = 0;
-    cub::DeviceScan::InclusiveScan((void *)nullptr, t, (const i64 *)nullptr, (i64 *)nullptr, MaxI64(), (int64_t)n);
+    cub::DeviceScan::InclusiveScan((void *)nullptr, t, (const i64 *)nullptr, (i64 *)nullptr, SlotScanOp(), (int64_t)n);
     return part_align_c(sizeof(i64) * (size_t)(n > 0 ? n : 1)) * 2 + part_align_c(t) + 256;
 }
 
@@ -632,9 +793,15 @@ int lj_spline_slots_plan(const LjSpline *model, const uint64_t *sorted_keys, con
     LJ_CK(cudaMemsetAsync(zero, 0, 2 * sizeof(unsigned long long), st));
     k_slots_t<<<grid_for(n, 256, 8), 256, 0, st>>>(SplineDev(*model), sorted_keys, sorted_pay, n, t, zero);
     LJ_CK_LAUNCH();
+#if LJ_HS_LAYOUT == 1
+    // t = P (positions) stays for the fill; the tail sizes are scanned in place in M
+    k_slots_tail<<<grid_for(n, 256, 8), 256, 0, st>>>(t, n, M);
+    LJ_CK_LAUNCH();
+    t = M;
+#endif
     size_t tb = 0;
-    cub::DeviceScan::InclusiveScan(nullptr, tb, t, M, MaxI64(), (int64_t)n);
-    LJ_CK(cub::DeviceScan::InclusiveScan(q, tb, t, M, MaxI64(), (int64_t)n, st));
+    cub::DeviceScan::InclusiveScan(nullptr, tb, t, M, SlotScanOp(), (int64_t)n);
+    LJ_CK(cub::DeviceScan::InclusiveScan(q, tb, t, M, SlotScanOp(), (int64_t)n, st));
     k_slots_size<<<1, 1, 0, st>>>(M, n, zero, plan);
     LJ_CK_LAUNCH();
     return LJ_OK;
@@ -645,8 +812,13 @@ int lj_spline_slots_fill(const uint64_t *sorted_keys, const uint64_t *sorted_pay
     LJ_REQUIRE(n >= 1 && nslots >= 2 * n, "need n >= 1 and the planned slot count");
     LJ_REQUIRE(ws_bytes >= lj_spline_slots_workspace_bytes(n), "workspace too small");
     const i64 *M = (const i64 *)((char *)ws + part_align_c(sizeof(i64) * (size_t)n));
+#if LJ_HS_LAYOUT == 1
+    k_slots_fill<<<grid_for(nslots, 256, 16), 256, 0, as_stream(stream)>>>(
+        M, (const i64 *)ws, sorted_keys, sorted_pay, n, nslots, reinterpret_cast<ulonglong2 *>(slots));
+#else
     k_slots_fill<<<grid_for(nslots, 256, 16), 256, 0, as_stream(stream)>>>(
         M, sorted_keys, sorted_pay, n, nslots, reinterpret_cast<ulonglong2 *>(slots));
+#endif
     LJ_CK_LAUNCH();
     return LJ_OK;
 }

@@ -9,7 +9,7 @@ ARCH="-gencode arch=compute_100a,code=sm_100a"
 FL="-O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-ffp-contract=off --expt-relaxed-constexpr -I include"
 OBJS=$(ls $C/build/*.o | grep -v "$SRC")
 for v in "$@"; do
-  tag=$(echo "$SRC $v" | tr ' =.' '_--')
+  tag=$(echo "$SRC $v" | tr ' =.' '___')
   mkdir -p /tmp/var_$tag
   nvcc $ARCH $FL $v -c $C/$SRC -o /tmp/var_$tag/v.o >> $O/build.log 2>&1
   nvcc $ARCH -shared -o /tmp/var_$tag/lib.so $OBJS /tmp/var_$tag/v.o -cudart static >> $O/build.log 2>&1
