@@ -715,13 +715,6 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
             }
 #endif
 #if LJ_HS_ROUNDS == 3
-#ifdef LJ_HS_PF
-            // (experiment) the next pair of every unfinished probe starts its way into L1
-#pragma unroll
-            for (int u = 0; u < HS_U; ++u) {
-                if (need >> u & 1u) asm volatile("prefetch.global.L1 [%0];" ::"l"(slots + s0[u] + 2));
-            }
-#endif
             // One pair per LANE per round: the lane's first unfinished probe
             // is selected into (kq, pq, sq) and followed to its end, then the
             // next -- a round costs one pair scan instead of one per probe
