@@ -48,22 +48,24 @@ static inline size_t part_align_c(size_t v) { return (v + 255) & ~(size_t)255; }
 
 // tuning constants (build-time; tools/gpu_hash_variants.sh measures variants)
 #ifndef LJ_HS_NT
-#define LJ_HS_NT 384
+#define LJ_HS_NT 1024
 #endif
 #ifndef LJ_HS_CTAS
-#define LJ_HS_CTAS 2
+#define LJ_HS_CTAS 1
 #endif
 #ifndef LJ_HS_U
-#define LJ_HS_U 4
+#define LJ_HS_U 3
 #endif
 #ifndef LJ_HS_D
 #define LJ_HS_D 2
 #endif
 #ifndef LJ_HS_PIECE
-#define LJ_HS_PIECE 49152  // a multiple of HS_NT * HS_U: no partly filled last iteration (32768: 22.07, 49152: 21.84 ms)
+#define LJ_HS_PIECE 98304  // a multiple of HS_NT * HS_U (no partly filled last iteration); about 15 M records in flight
+                           // over the GPU keep the live windows of the probe table in L2 (73728: 20.16, 98304: 19.97,
+                           // 122880: 20.05 ms)
 #endif
 #ifndef LJ_HS_NC
-#define LJ_HS_NC 2048
+#define LJ_HS_NC 4096
 #endif
 #ifndef LJ_HS_SPREAD
 #define LJ_HS_SPREAD 2  // probe-table slots per position (the first slot of a position is even: one 32-B pair)
@@ -88,6 +90,11 @@ constexpr int HS_CTAS = LJ_HS_CTAS;  // CTAs per SM
 constexpr int HS_U = LJ_HS_U;        // probes per thread per iteration
 constexpr int HS_D = LJ_HS_D;        // iterations of records in flight (cp.async)
 constexpr int HS_TT = HS_NT * HS_U;  // records per iteration
+// Tuning builds whose record ring (HS_D stages x HS_TT records) holds a power-of-two record count (256 / 512 /
+// 1024 threads x 2 or 4 probes x 2 stages, 1024 x 2 x 4, ...) stop with "illegal instruction" on sm_100a (CUDA
+// 12.9), unexplained: the same source with 3 probes per thread or 3 stages passes every test, padding the
+// shared-memory layout changes nothing.  Such shapes are refused at build time.
+static_assert(((HS_D * HS_TT) & (HS_D * HS_TT - 1)) != 0, "see the note above: pick another HS_NT x HS_U x HS_D");
 constexpr int HS_CAP = 1024;         // staged spline points per window
 constexpr int HS_NC = LJ_HS_NC;      // lower-bound cells per window
 constexpr i64 HS_PIECE = LJ_HS_PIECE;  // records per work item
