@@ -77,6 +77,9 @@ static inline size_t part_align_c(size_t v) { return (v + 255) & ~(size_t)255; }
                         // of the thread per round (22.84 ms), 2 = unfinished probes compacted across the warp (29.9 ms: a
                         // lane's dependent loads no longer overlap), 0 = slot by slot
 #endif
+#ifndef LJ_HS_PADB
+#define LJ_HS_PADB 0  // (diagnostic) unused shared memory: a larger carve-out leaves less L1 for the slot loads in flight
+#endif
 #ifndef LJ_HS_LAYOUT
 #define LJ_HS_LAYOUT 0  // probe table: 0 = entries pushed forward in key order; 1 (ablation) = home pairs + tails: no
                         // displacement, but 18.4 % of C3's probes go on to a tail (chains >= 3, rank >= 1) against 16.1 %
@@ -106,7 +109,7 @@ static_assert(((HS_NC + 8) * 2) % 8 == 0, "the piece prefix and the queues follo
 __host__ __device__ constexpr size_t hs_ip_words(int nb) { return (size_t)((nb + 3) & ~1); }
 __host__ __device__ constexpr size_t hs_smem(int nb) {
     return (size_t)HS_D * HS_U * HS_NT * 16 + (size_t)HS_CAP * (8 + 32) + (HS_NC + 8) * 2 + hs_ip_words(nb) * 4 +
-           (LJ_HS_ROUNDS == 2 ? (size_t)(HS_NT / 32) * HS_QCAP * (8 + 2) : 0);
+           (LJ_HS_ROUNDS == 2 ? (size_t)(HS_NT / 32) * HS_QCAP * (8 + 2) : 0) + LJ_HS_PADB;
 }
 
 // first slot of position p in the probe table (monotone, even)
