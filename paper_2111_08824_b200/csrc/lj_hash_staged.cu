@@ -57,7 +57,7 @@ static inline size_t part_align_c(size_t v) { return (v + 255) & ~(size_t)255; }
 #define LJ_HS_U 3
 #endif
 #ifndef LJ_HS_D
-#define LJ_HS_D 2
+#define LJ_HS_D 1
 #endif
 #ifndef LJ_HS_PIECE
 #define LJ_HS_PIECE 98304  // a multiple of HS_NT * HS_U (no partly filled last iteration); about 15 M records in flight
@@ -76,6 +76,23 @@ static inline size_t part_align_c(size_t v) { return (v + 255) & ~(size_t)255; }
                         // position u at 3-9 active lanes; 22.07 ms with 2048 cells), 1 = one pair per unfinished probe
                         // of the thread per round (22.84 ms), 2 = unfinished probes compacted across the warp (29.9 ms: a
                         // lane's dependent loads no longer overlap), 0 = slot by slot
+#endif
+#ifndef LJ_HS_LDV
+#define LJ_HS_LDV 1
+#endif
+// the 32-B slot-pair load (LJ_HS_LDV: cache-hint variants, measured)
+#if LJ_HS_LDV == 1
+#define LJ_HS_LD "ld.global.nc.L1::no_allocate.v4.u64"
+#elif LJ_HS_LDV == 2
+#define LJ_HS_LD "ld.global.nc.L1::evict_first.v4.u64"
+#elif LJ_HS_LDV == 3
+#define LJ_HS_LD "ld.global.nc.L1::evict_last.v4.u64"
+#elif LJ_HS_LDV == 4
+#define LJ_HS_LD "ld.global.v4.u64"
+#elif LJ_HS_LDV == 5
+#define LJ_HS_LD "ld.global.L1::no_allocate.v4.u64"
+#else
+#define LJ_HS_LD "ld.global.nc.v4.u64"
 #endif
 #ifndef LJ_HS_PADB
 #define LJ_HS_PADB 0  // (diagnostic) unused shared memory: a larger carve-out leaves less L1 for the slot loads in flight
@@ -591,9 +608,14 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
         }
         const int niter = (int)((hi - lo + HS_TT - 1) / HS_TT);
         // records of iteration i -> this thread's slots of stage i % HS_D
-        // (evict-first in L2: read once; the slot lines are what L2 keeps)
+        // (evict-first in L2: read once; the slot lines are what L2 keeps).
+        // HS_D == 1: ONE stage -- a thread reads its records of iteration i
+        // into registers and only then starts the copies of iteration i + 1
+        // into the same slots (its own: no other thread touches them), so
+        // the copies still have a whole iteration to land, at half the
+        // shared memory (more L1 for the slot loads in flight).
 #pragma unroll
-        for (int i = 0; i < HS_D - 1; ++i) {
+        for (int i = 0; i < (HS_D == 1 ? 1 : HS_D - 1); ++i) {
             if (i < niter) {
 #pragma unroll
                 for (int u = 0; u < HS_U; ++u) {
@@ -604,7 +626,7 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
             cp_async_commit();
         }
         for (int i = 0; i < niter; ++i) {
-            {
+            if (HS_D > 1) {
                 const int f = i + HS_D - 1;
                 if (f < niter) {
 #pragma unroll
@@ -615,7 +637,7 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
                 }
                 cp_async_commit();
             }
-            asm volatile("cp.async.wait_group %0;" ::"n"(HS_D - 1) : "memory");
+            asm volatile("cp.async.wait_group %0;" ::"n"(HS_D > 1 ? HS_D - 1 : 0) : "memory");
             u64 k[HS_U], ps[HS_U];
             i64 s0[HS_U];
 #pragma unroll
@@ -630,6 +652,22 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
                     ps[u] = 0;
                 }
             }
+            if (HS_D == 1) {
+                if (i + 1 < niter) {
+#pragma unroll
+                    for (int u = 0; u < HS_U; ++u) {
+                        const i64 j = lo + (i64)(i + 1) * HS_TT + u * HS_NT + tid;
+                        // (the record just read is an operand: the copy issues after its load has returned)
+                        if (j < hi) {
+                            asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;  // after %3 %4" ::"r"(
+                                             smem_u32(rbuf + (size_t)u * HS_NT + tid)),
+                                         "l"(rec + j), "l"(pol), "l"(k[u]), "l"(ps[u])
+                                         : "memory");
+                        }
+                    }
+                }
+                cp_async_commit();
+            }
 #pragma unroll
             for (int u = 0; u < HS_U; ++u) {
                 // (one unsigned compare covers klo <= k <= khi; the reserved
@@ -643,7 +681,7 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
 #pragma unroll
             for (int u = 0; u < HS_U; ++u) {
                 if (s0[u] >= 0) {
-                    asm volatile("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+                    asm volatile(LJ_HS_LD " {%0, %1, %2, %3}, [%4];"
                                  : "=l"(e[u][0]), "=l"(e[u][1]), "=l"(e[u][2]), "=l"(e[u][3])
                                  : "l"(slots + s0[u]));
                 } else {
@@ -714,7 +752,7 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
                     const ulonglong2 *sl = slots + qs[q];
                     u64 ee[4];
                     do {
-                        asm volatile("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+                        asm volatile(LJ_HS_LD " {%0, %1, %2, %3}, [%4];"
                                      : "=l"(ee[0]), "=l"(ee[1]), "=l"(ee[2]), "=l"(ee[3])
                                      : "l"(sl));
                         sl += 2;
@@ -745,7 +783,7 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
                     }
                     sq += 2;
                     u64 ee[4];
-                    asm volatile("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+                    asm volatile(LJ_HS_LD " {%0, %1, %2, %3}, [%4];"
                                  : "=l"(ee[0]), "=l"(ee[1]), "=l"(ee[2]), "=l"(ee[3])
                                  : "l"(slots + sq));
                     fresh = !pair_scan<UNIQUE>(ee, kq, pq, acc);
@@ -758,7 +796,7 @@ __global__ void __launch_bounds__(HS_NT, HS_CTAS) k_hash_probe_staged(SplineDev 
 #pragma unroll
                 for (int u = 0; u < HS_U; ++u) {
                     if (need >> u & 1u) {
-                        asm volatile("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+                        asm volatile(LJ_HS_LD " {%0, %1, %2, %3}, [%4];"
                                      : "=l"(e[u][0]), "=l"(e[u][1]), "=l"(e[u][2]), "=l"(e[u][3])
                                      : "l"(slots + s0[u] + 2 * r));
                     }
