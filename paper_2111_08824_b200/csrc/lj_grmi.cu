@@ -256,9 +256,6 @@ __global__ void __launch_bounds__(256) k_grmi_probe_overflow(GrmiDev g, const ul
 // one table pair plus a fixed-trip branch-free binary search, one payload
 // load per match.
 
-#ifndef LJ_K1S_REC
-#define LJ_K1S_REC 0
-#endif
 constexpr int STAGE_NT = 1024;
 #ifndef LJ_STAGE_PIECE
 #define LJ_STAGE_PIECE 65536
@@ -558,16 +555,7 @@ __global__ void __launch_bounds__(STAGE_NT, 1) k_grmi_probe_staged(GrmiDev g, co
 #pragma unroll
                 for (int u = 0; u < STAGE_U; ++u) {
                     const int t = t0 + u * STAGE_NT;
-                    ulonglong2 r = make_ulonglong2(kmin, 0);
-                    if (t < ne) {
-#if LJ_K1S_REC == 1  // (experiment) the record stream without L1 allocation
-                        asm("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];" : "=l"(r.x), "=l"(r.y) : "l"(wrec + t));
-#elif LJ_K1S_REC == 2
-                        asm("ld.global.L1::no_allocate.v2.u64 {%0, %1}, [%2];" : "=l"(r.x), "=l"(r.y) : "l"(wrec + t));
-#else
-                        r = __ldcs(wrec + t);
-#endif
-                    }
+                    const ulonglong2 r = t < ne ? __ldcs(wrec + t) : make_ulonglong2(kmin, 0);
                     k[u] = r.x;
                     ps[u] = r.y;
                     // the records of two steps ahead start their way into L2
