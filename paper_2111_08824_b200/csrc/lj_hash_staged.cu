@@ -65,7 +65,7 @@ static inline size_t part_align_c(size_t v) { return (v + 255) & ~(size_t)255; }
                            // 122880: 20.05 ms)
 #endif
 #ifndef LJ_HS_NC
-#define LJ_HS_NC 4096
+#define LJ_HS_NC 32768  // lower-bound cells per window (64 KB of shared memory; 4096 / 8192 / 16384 / 32768: 18.63 / 18.51 / 18.34 / 18.22 ms)
 #endif
 #ifndef LJ_HS_SPREAD
 #define LJ_HS_SPREAD 2  // probe-table slots per position (the first slot of a position is even: one 32-B pair)
@@ -306,7 +306,7 @@ __global__ void k_slots_fill(const i64 *M, const i64 *P, const u64 *sk, const u6
 // ------------------------------------------------------------ windows
 
 // one block per window: the spline points [a0, a0 + npts) and the cells
-__global__ void __launch_bounds__(256) k_hash_windows(SplineDev m, const u64 *lay, int nb, u64 kmin, WinMeta *meta,
+__global__ void __launch_bounds__(1024) k_hash_windows(SplineDev m, const u64 *lay, int nb, u64 kmin, WinMeta *meta,
                                                       u16 *cells) {
     const int w = blockIdx.x;
     const u64 *B = lay + 4;
@@ -348,7 +348,8 @@ __global__ void __launch_bounds__(256) k_hash_windows(SplineDev m, const u64 *la
         const u64 off = (u64)c << s.cshift;
         const bool past = (s.cshift > 0 && (u64)c > ((s.khi - s.klo) >> s.cshift)) || off > s.khi - s.klo;
         const u64 L = past ? s.khi : s.klo + off;
-        i64 i = lower_bound_u64(m.keys, m.K, L) - s.a0;
+        // (over the window's own points: the clamp below makes it equal to the search over all K)
+        i64 i = lower_bound_u64(m.keys + s.a0, s.npts, L);
         if (past) i = s.npts - 1;
         cw[c] = (u16)(i < 0 ? 0 : (i > s.npts - 1 ? s.npts - 1 : i));
     }
@@ -907,7 +908,7 @@ size_t hash_staged_meta_bytes(int nb) { return hs_meta_bytes(nb); }
 int hash_windows(const LjSpline &model, const u64 *lay, int nb, u64 kmin, void *meta_ws, cudaStream_t st) {
     WinMeta *meta = reinterpret_cast<WinMeta *>(meta_ws);
     u16 *cells = reinterpret_cast<u16 *>((char *)meta_ws + (((size_t)nb * sizeof(WinMeta) + 255) & ~(size_t)255));
-    k_hash_windows<<<nb, 256, 0, st>>>(SplineDev(model), lay, nb, kmin, meta, cells);
+    k_hash_windows<<<nb, 1024, 0, st>>>(SplineDev(model), lay, nb, kmin, meta, cells);
     LJ_CK_LAUNCH();
     return LJ_OK;
 }
